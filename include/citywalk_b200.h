@@ -1,0 +1,152 @@
+/*
+ * citywalk_b200.h -- C ABI of the B200 env-side hot path (libcitywalk_b200.so).
+ *
+ * Drop-in boundary for the reference's Python entry points (paths relative to
+ * /root/reference/pkg/src/citywalk):
+ *
+ *   cw_sample_scenes   replaces, per env, urbangen/scene.py:38 generate_scene
+ *                      (minus route anchors, scene.py:87/102-158), occupancy.py:28
+ *                      rasterize_occupancy, crowd/field.py:60-67 _prepare_env
+ *                      (walk cells + _nearest_obstacle_map :571) and
+ *                      crowd/step.py:37 spawn_agents (+ routes.py:35 sample_routes),
+ *                      as driven by envcore/batch.py:117-122 / 170-181 / 326-339.
+ *   cw_spawn_agents    replaces crowd/step.py:37 spawn_agents for host-built grids.
+ *   cw_prepare_envs    replaces crowd/field.py:60-67 _prepare_env for host-built grids.
+ *   cw_crowd_step      replaces crowd/field.py:90 CrowdField.step (workers ignored:
+ *                      results are split-invariant by construction).
+ *   cw_seed_streams    replaces np.random.Generator(np.random.PCG64(seed)) for
+ *                      field.py:36 (per-env goal-resample streams).
+ *   cw_child_seeds     replaces rng.py:15 child_seed for the batch seed tree
+ *                      (batch.py:85, 165, 179, 332).
+ *
+ * Conventions: every pointer inside the structs and every array argument is a
+ * DEVICE pointer; `stream` is a cudaStream_t (NULL = legacy default stream).
+ * Calls are stream-ordered, never synchronise the host and create no threads.
+ * The return value is 0 or a cudaError_t; per-env sampling failures are
+ * reported in buffers->status (cw_status), guidance capacity errors in
+ * state->flags[1].  Results are independent of launch configuration.
+ */
+#ifndef CITYWALK_B200_H
+#define CITYWALK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CW_MAX_TILES 44
+#define CW_MAX_CATALOG 32
+
+enum cw_status {
+  CW_OK = 0,
+  CW_E_CONTRADICTION = 1, /* errors.ContradictionAfterRetries (wfc.py:51)   */
+  CW_E_NOROUTE = 2,       /* errors.NoRouteAvailable (routes.py:58, 84)     */
+  CW_E_EXTENT = 3,        /* errors.ExtentTooSmall (zones.py:60-61)         */
+  CW_E_PATHCAP = 4,       /* guidance path longer than state path_cap       */
+  CW_E_HEAPCAP = 5        /* A* open list exceeded heap_cap                 */
+};
+
+/* SceneSpec shape shared by a batch (urbangen/types.py:88-115). */
+typedef struct cw_scene_params {
+  int32_t nx, ny;
+  double res;
+  double w, l;
+  int32_t task;   /* 0 NavClear, 1 NavStatic, 2 NavDynamic, 3 Traverse */
+  int32_t split;  /* 0 Train, 1 Test */
+  double mix[4];  /* Flat, Slope, Stair, Rough */
+  int32_t layout; /* 0 courtyard, 1 blocks, 2 strip */
+  int32_t brows, bcols;
+  double quad_cdf[3];
+  int32_t trows, tcols, cpt;
+  int32_t nonflat_split_col;
+  int32_t n_cat;
+  double cat_w[CW_MAX_CATALOG], cat_l[CW_MAX_CATALOG];
+  double cat_reach[CW_MAX_CATALOG];
+  uint32_t cat_zones[CW_MAX_CATALOG];
+  int32_t small_first[CW_MAX_CATALOG];
+  int32_t obj_count, obj_max, attempts;
+  int32_t region;
+  int32_t peds;
+  int32_t spawn_region;
+} cw_scene_params;
+
+/* Output rows (E envs, written at slots[e]) + scratch. */
+typedef struct cw_scene_buffers {
+  uint8_t* zones; uint8_t* labels; float* elev;
+  int32_t* assign; int32_t* n_tiles; int8_t* tile_code; int8_t* tile_kind;
+  double* tile_param; double* tile_p; double* tile_w; uint64_t* allowed;
+  uint64_t* noise_seed; int32_t* wfc_attempts;
+  int32_t* obj_cat; double* obj_pose; int32_t* obj_n; uint8_t* overflow;
+  int32_t* nearest; uint8_t* has_obs;
+  int32_t* walk; int32_t* walk_n;
+  double* sp_pos; double* sp_goal; int8_t* sp_kind; double* sp_pref;
+  int32_t* status;
+  int32_t* scratch_i32; /* (E, 3*ny*nx) */
+  double* scratch_f64;  /* (E, max(obj_max*8, ny*nx)) */
+} cw_scene_buffers;
+
+size_t cw_scene_seed_scratch_bytes(int E);
+
+int cw_sample_scenes(const cw_scene_params* params, int E, const uint64_t* scene_seeds,
+                     const uint64_t* crowd_seeds, const int32_t* slots, void* seed_scratch,
+                     const cw_scene_buffers* buffers, void* stream);
+
+/* spawn_agents for caller-supplied labels (crowd/step.py:37-63): fills sp_* and
+ * status of rows slots[e] from buffers->labels; seed_scratch as for sampling. */
+int cw_spawn_agents(const cw_scene_params* params, int E, const uint64_t* crowd_seeds,
+                    const int32_t* slots, void* seed_scratch, const cw_scene_buffers* buffers,
+                    void* stream);
+
+/* _prepare_env for caller-supplied labels (field.py:60-67): fills nearest,
+ * has_obs, walk, walk_n of rows slots[e] from buffers->labels; needs status
+ * (zeroed) and scratch_i32.  Only params->nx/ny are read. */
+int cw_prepare_envs(const cw_scene_params* params, int E, const int32_t* slots,
+                    const cw_scene_buffers* buffers, void* stream);
+
+/* CrowdConfig + batch shape (crowd/types.py:60-79, field.py:29-58). */
+typedef struct cw_crowd_params {
+  int32_t E, A;
+  int32_t nx, ny;
+  double res, res0;
+  double time_horizon, obstacle_time_horizon, neighbor_distance, nd2;
+  float nd2_f32;
+  int32_t max_neighbors;
+  double dt, safety_margin, goal_reach2, stall_c, stall_s;
+  int32_t resample_goals, use_static, path_cap, heap_cap, slots_per_env;
+} cw_crowd_params;
+
+/* Device-resident CrowdField state (field.py:47-58) + guidance/A* scratch. */
+typedef struct cw_crowd_state {
+  double* pos; double* vel; double* goal; double* waypoint;
+  const double* radius; const double* pref_speed; const double* max_speed;
+  const uint8_t* active;
+  int32_t* path_cells; int32_t* path_head; int32_t* path_n;
+  const uint8_t* labels; const int32_t* nearest; const uint8_t* has_obs;
+  const int32_t* walk; const int32_t* walk_n;
+  void* rng;
+  double* last_gap; double* gap_tmp; int32_t* flags;
+  double* astar_g; int32_t* astar_parent; int32_t* astar_stamp; int32_t* astar_epoch;
+  void* astar_heap;
+  int64_t* counters;
+} cw_crowd_state;
+
+size_t cw_crowd_step_smem_bytes(int A, int threads);
+
+int cw_crowd_step(const cw_crowd_params* params, const cw_crowd_state* state,
+                  const double* robot_pos, const double* robot_vel, double robot_radius,
+                  const uint8_t* env_mask, int threads, void* stream);
+
+int cw_seed_streams(int n, const uint64_t* seeds, void* out_states, void* stream);
+
+int cw_child_seeds(int n, const uint64_t* parent, int label_id, const uint64_t* k,
+                   uint64_t* out, void* stream);
+
+/* Host-only: sizeof of the four ABI structs (scene params/buffers, crowd params/state). */
+int cw_abi_sizes(size_t* out, int n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CITYWALK_B200_H */

@@ -1,0 +1,148 @@
+"""ctypes binding of libcitywalk_b200.so (the C ABI in include/citywalk_b200.h).
+
+The library is built in-tree (``build()``) for sm_100a.  There is no CPU
+fallback: importing the product API without the library raises.
+"""
+
+import ctypes
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB_PATH = os.path.join(HERE, "libcitywalk_b200.so")
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("sample.cu", "crowd.cu")]
+HEADERS = [os.path.join(HERE, "csrc", f) for f in
+           ("common.cuh", "rng.cuh", "scene_types.cuh", "crowd_types.cuh")] + [
+    os.path.join(ROOT, "include", "citywalk_b200.h")]
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
+              "-std=c++17", "-Xcompiler", "-fPIC", "-shared"]
+
+MAX_TILES = 44
+MAX_CAT = 32
+
+c_i32, c_u32, c_f64, c_f32, c_i64 = ctypes.c_int32, ctypes.c_uint32, ctypes.c_double, ctypes.c_float, ctypes.c_int64
+P = ctypes.c_void_p
+
+
+class SceneParams(ctypes.Structure):
+    _fields_ = [
+        ("nx", c_i32), ("ny", c_i32), ("res", c_f64), ("w", c_f64), ("l", c_f64),
+        ("task", c_i32), ("split", c_i32), ("mix", c_f64 * 4), ("layout", c_i32),
+        ("brows", c_i32), ("bcols", c_i32), ("quad_cdf", c_f64 * 3),
+        ("trows", c_i32), ("tcols", c_i32), ("cpt", c_i32), ("nonflat_split_col", c_i32),
+        ("n_cat", c_i32), ("cat_w", c_f64 * MAX_CAT), ("cat_l", c_f64 * MAX_CAT),
+        ("cat_reach", c_f64 * MAX_CAT), ("cat_zones", c_u32 * MAX_CAT),
+        ("small_first", c_i32 * MAX_CAT), ("obj_count", c_i32), ("obj_max", c_i32),
+        ("attempts", c_i32), ("region", c_i32), ("peds", c_i32), ("spawn_region", c_i32),
+    ]
+
+
+SCENE_BUFFER_FIELDS = [
+    "zones", "labels", "elev", "assign", "n_tiles", "tile_code", "tile_kind", "tile_param",
+    "tile_p", "tile_w", "allowed", "noise_seed", "wfc_attempts", "obj_cat", "obj_pose", "obj_n",
+    "overflow", "nearest", "has_obs", "walk", "walk_n", "sp_pos", "sp_goal", "sp_kind", "sp_pref",
+    "status", "scratch_i32", "scratch_f64",
+]
+
+
+class SceneBuffers(ctypes.Structure):
+    _fields_ = [(n, P) for n in SCENE_BUFFER_FIELDS]
+
+
+class CrowdParams(ctypes.Structure):
+    _fields_ = [
+        ("E", c_i32), ("A", c_i32), ("nx", c_i32), ("ny", c_i32), ("res", c_f64), ("res0", c_f64),
+        ("time_horizon", c_f64), ("obstacle_time_horizon", c_f64), ("neighbor_distance", c_f64),
+        ("nd2", c_f64), ("nd2_f32", c_f32), ("max_neighbors", c_i32), ("dt", c_f64),
+        ("safety_margin", c_f64), ("goal_reach2", c_f64), ("stall_c", c_f64), ("stall_s", c_f64),
+        ("resample_goals", c_i32), ("use_static", c_i32), ("path_cap", c_i32), ("heap_cap", c_i32),
+        ("slots_per_env", c_i32),
+    ]
+
+
+CROWD_STATE_FIELDS = [
+    "pos", "vel", "goal", "waypoint", "radius", "pref_speed", "max_speed", "active", "path_cells",
+    "path_head", "path_n", "labels", "nearest", "has_obs", "walk", "walk_n", "rng", "last_gap",
+    "gap_tmp", "flags", "astar_g", "astar_parent", "astar_stamp", "astar_epoch", "astar_heap",
+    "counters",
+]
+
+
+class CrowdState(ctypes.Structure):
+    _fields_ = [(n, P) for n in CROWD_STATE_FIELDS]
+
+
+EXPORTS = ["cw_scene_seed_scratch_bytes", "cw_sample_scenes", "cw_spawn_agents", "cw_prepare_envs",
+           "cw_crowd_step_smem_bytes",
+           "cw_crowd_step", "cw_seed_streams", "cw_child_seeds", "cw_abi_sizes"]
+
+_lib = None
+
+
+def build(force=False, verbose=False):
+    """Compile the CUDA library in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+    newest = max(os.path.getmtime(p) for p in SOURCES + HEADERS)
+    if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
+        return LIB_PATH
+    cmd = ["nvcc"] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", LIB_PATH] + SOURCES
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    return LIB_PATH
+
+
+def lib():
+    """Load the library (raises if it was not built; no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"libcitywalk_b200.so not built ({LIB_PATH}); run __graft_entry__.build()")
+    L = ctypes.CDLL(LIB_PATH)
+    L.cw_scene_seed_scratch_bytes.restype = ctypes.c_size_t
+    L.cw_scene_seed_scratch_bytes.argtypes = [ctypes.c_int]
+    L.cw_sample_scenes.restype = ctypes.c_int
+    L.cw_sample_scenes.argtypes = [ctypes.POINTER(SceneParams), ctypes.c_int, P, P, P, P,
+                                   ctypes.POINTER(SceneBuffers), P]
+    L.cw_spawn_agents.restype = ctypes.c_int
+    L.cw_spawn_agents.argtypes = [ctypes.POINTER(SceneParams), ctypes.c_int, P, P, P,
+                                  ctypes.POINTER(SceneBuffers), P]
+    L.cw_prepare_envs.restype = ctypes.c_int
+    L.cw_prepare_envs.argtypes = [ctypes.POINTER(SceneParams), ctypes.c_int, P,
+                                  ctypes.POINTER(SceneBuffers), P]
+    L.cw_crowd_step_smem_bytes.restype = ctypes.c_size_t
+    L.cw_crowd_step_smem_bytes.argtypes = [ctypes.c_int, ctypes.c_int]
+    L.cw_crowd_step.restype = ctypes.c_int
+    L.cw_crowd_step.argtypes = [ctypes.POINTER(CrowdParams), ctypes.POINTER(CrowdState), P, P,
+                                ctypes.c_double, P, ctypes.c_int, P]
+    L.cw_seed_streams.restype = ctypes.c_int
+    L.cw_seed_streams.argtypes = [ctypes.c_int, P, P, P]
+    L.cw_child_seeds.restype = ctypes.c_int
+    L.cw_child_seeds.argtypes = [ctypes.c_int, P, ctypes.c_int, P, P, P]
+    L.cw_abi_sizes.restype = ctypes.c_int
+    L.cw_abi_sizes.argtypes = [ctypes.POINTER(ctypes.c_size_t), ctypes.c_int]
+    sizes = (ctypes.c_size_t * 4)()
+    L.cw_abi_sizes(sizes, 4)
+    mine = [ctypes.sizeof(SceneParams), ctypes.sizeof(SceneBuffers), ctypes.sizeof(CrowdParams),
+            ctypes.sizeof(CrowdState)]
+    if list(sizes) != mine:
+        raise RuntimeError(f"ABI mismatch: library {list(sizes)} vs ctypes {mine}")
+    _lib = L
+    return L
+
+
+def check(err, what):
+    if err != 0:
+        raise RuntimeError(f"{what} failed with CUDA error {err}")
+
+
+def ptr(t):
+    """Device pointer of a torch tensor (None -> NULL)."""
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def stream_ptr(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)

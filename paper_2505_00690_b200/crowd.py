@@ -1,0 +1,433 @@
+"""Crowd dynamics on the B200 -- drop-in for the reference's crowd package.
+
+Mirrors /root/reference/pkg/src/citywalk/crowd:
+  * ``AgentKind``, ``CrowdAgent``, ``CrowdConfig`` and the kind tables (types.py:9-79)
+  * ``CrowdField(occupancies, config, env_seeds, resample_goals=True)`` with
+    ``set_agents`` / ``set_env_agents`` / ``replace_env`` / ``step`` / ``agents_of``
+    / ``last_gap_by_env`` (field.py:26-430)
+  * ``step_crowd`` (step.py:17-34) and ``spawn_agents`` (step.py:37-63)
+
+State lives on the device (float64 SoA, (E, A, 2) / (E, A)); ``step`` is one
+``cw_crowd_step`` launch (guidance + A*, neighbours, ORCA, LP, commit, goal
+resample for every env).  ``pos`` / ``vel`` / ``goal`` / ``waypoint`` return
+host copies; the device tensors are ``pos_t`` etc.
+"""
+
+from dataclasses import dataclass
+from enum import IntEnum
+
+import numpy as np
+
+from . import _lib
+from .errors import STATUS_ERRORS
+from .urbangen import OccupancyGrid, SceneBatch, load_catalog
+
+
+class AgentKind(IntEnum):
+    PEDESTRIAN = 0
+    CYCLIST = 1
+    SCOOTER = 2
+
+
+MAX_SPEED_OF_KIND = {AgentKind.PEDESTRIAN: 2.0, AgentKind.CYCLIST: 5.0, AgentKind.SCOOTER: 4.0}
+PREF_SPEED_RANGE = {AgentKind.PEDESTRIAN: (0.8, 1.4), AgentKind.CYCLIST: (2.0, 4.0),
+                    AgentKind.SCOOTER: (1.5, 3.0)}
+RADIUS_OF_KIND = {AgentKind.PEDESTRIAN: 0.3, AgentKind.CYCLIST: 0.45, AgentKind.SCOOTER: 0.4}
+
+
+@dataclass
+class CrowdAgent:
+    id: int
+    position: np.ndarray
+    velocity: np.ndarray
+    radius: float
+    preferred_speed: float
+    goal: np.ndarray
+    kind: AgentKind = AgentKind.PEDESTRIAN
+
+    def __post_init__(self):
+        self.position = np.asarray(self.position, dtype=np.float64)
+        self.velocity = np.asarray(self.velocity, dtype=np.float64)
+        self.goal = np.asarray(self.goal, dtype=np.float64)
+        if self.radius <= 0:
+            raise ValueError("radius must be > 0")
+        if self.preferred_speed <= 0:
+            raise ValueError("preferred_speed must be > 0")
+
+    @property
+    def max_speed(self):
+        return MAX_SPEED_OF_KIND[self.kind]
+
+
+@dataclass
+class CrowdConfig:
+    time_horizon: float = 2.0
+    obstacle_time_horizon: float = 1.0
+    neighbor_distance: float = 5.0
+    max_neighbors: int = 10
+    dt: float = 0.05
+    safety_margin: float = 0.03
+
+    def __post_init__(self):
+        for name in ("time_horizon", "obstacle_time_horizon", "neighbor_distance",
+                     "max_neighbors", "dt"):
+            if getattr(self, name) <= 0:
+                raise ValueError(f"{name} must be > 0")
+        if self.dt > 0.1:
+            raise ValueError("dt must be <= 0.1 s")
+        if self.safety_margin < 0:
+            raise ValueError("safety_margin must be >= 0")
+
+
+def _u64(seeds, device):
+    import torch
+    arr = np.array([int(s) & ((1 << 64) - 1) for s in seeds], dtype=np.uint64).view(np.int64)
+    return torch.from_numpy(arr).to(device)
+
+
+class CrowdField:
+    """Device CrowdField (field.py:26).  ``occupancies`` is a list of
+    OccupancyGrid (host labels, uploaded once) or a device ``SceneBatch``."""
+
+    def __init__(self, occupancies, config, env_seeds, resample_goals=True, device="cuda",
+                 threads=128, path_cap=None, heap_cap=None):
+        import torch
+        self.config = config
+        self.resample_goals = resample_goals
+        self.device = torch.device(device)
+        self.threads = threads
+        if isinstance(occupancies, SceneBatch):
+            b = occupancies
+            self.E = b.E
+            self.ny, self.nx = b.labels.shape[1:]
+            self.res = float(b.params.res)
+            self.res0 = self.res
+            self.labels_t, self.nearest_t, self.has_obs_t = b.labels, b.nearest, b.has_obs
+            self.walk_t, self.walk_n_t = b.walk, b.walk_n
+            self._batch = b
+        else:
+            occs = list(occupancies)
+            self.E = len(occs)
+            shapes = {o.labels.shape for o in occs}
+            ress = {float(o.resolution) for o in occs}
+            if len(shapes) != 1 or len(ress) != 1:
+                raise ValueError("the B200 CrowdField needs one grid shape and resolution per batch")
+            self.ny, self.nx = occs[0].labels.shape
+            self.res = float(occs[0].resolution)
+            self.res0 = self.res
+            self._batch = None
+            self._upload_grids(occs)
+        if len(env_seeds) != self.E:
+            raise ValueError("env_seeds must have one seed per env")
+        self.rng_t = torch.empty((self.E, 48), dtype=torch.uint8, device=self.device)
+        seeds = _u64(env_seeds, self.device)
+        _lib.check(_lib.lib().cw_seed_streams(self.E, _lib.ptr(seeds), _lib.ptr(self.rng_t),
+                                              _lib.stream_ptr()), "cw_seed_streams")
+        N = self.nx * self.ny
+        self.path_cap = int(path_cap or 2 * (self.nx + self.ny) + 64)
+        self.heap_cap = int(heap_cap or max(4096, N // 2))
+        self.slots = threads // 32
+        self.last_gap_t = torch.full((self.E,), float("inf"), dtype=torch.float64, device=self.device)
+        self.gap_tmp_t = torch.zeros((self.E,), dtype=torch.float64, device=self.device)
+        self.flags_t = torch.zeros((8,), dtype=torch.int32, device=self.device)
+        self.counters_t = torch.zeros((8,), dtype=torch.int64, device=self.device)
+        self._astar_ready = False
+        self._alloc(0)
+
+    # -- grids ----------------------------------------------------------------
+    def _upload_grids(self, occs):
+        import torch
+        E, ny, nx = self.E, self.ny, self.nx
+        lab = torch.from_numpy(np.stack([o.labels for o in occs]).astype(np.uint8)).to(self.device)
+        self.labels_t = lab.contiguous()
+        self.nearest_t = torch.empty((E, ny, nx), dtype=torch.int32, device=self.device)
+        self.has_obs_t = torch.zeros((E,), dtype=torch.uint8, device=self.device)
+        self.walk_t = torch.empty((E, ny * nx), dtype=torch.int32, device=self.device)
+        self.walk_n_t = torch.zeros((E,), dtype=torch.int32, device=self.device)
+        self._prepare(None)
+
+    def _prepare(self, rows):
+        """field.py:60-67 (_prepare_env) for all envs or the given rows."""
+        import torch
+        p = _lib.SceneParams()
+        p.nx, p.ny = self.nx, self.ny
+        n = self.E if rows is None else len(rows)
+        status = torch.zeros((self.E,), dtype=torch.int32, device=self.device)
+        scratch = torch.empty((n, 3 * self.nx * self.ny), dtype=torch.int32, device=self.device)
+        b = _lib.SceneBuffers()
+        b.labels = self.labels_t.data_ptr()
+        b.nearest = self.nearest_t.data_ptr()
+        b.has_obs = self.has_obs_t.data_ptr()
+        b.walk = self.walk_t.data_ptr()
+        b.walk_n = self.walk_n_t.data_ptr()
+        b.status = status.data_ptr()
+        b.scratch_i32 = scratch.data_ptr()
+        sl = None if rows is None else torch.as_tensor(rows, dtype=torch.int32, device=self.device)
+        _lib.check(_lib.lib().cw_prepare_envs(p, n, _lib.ptr(sl), b, _lib.stream_ptr()),
+                   "cw_prepare_envs")
+
+    # -- population (field.py:71-86, 383-401) ------------------------------------
+    def _alloc(self, A):
+        import torch
+        E, d = self.E, self.device
+        self.A = A
+        f64 = dict(dtype=torch.float64, device=d)
+        self.pos_t = torch.zeros((E, A, 2), **f64)
+        self.vel_t = torch.zeros((E, A, 2), **f64)
+        self.goal_t = torch.zeros((E, A, 2), **f64)
+        self.waypoint_t = torch.zeros((E, A, 2), **f64)
+        self.radius_t = torch.full((E, A), 0.3, **f64)
+        self.pref_t = torch.full((E, A), 1.0, **f64)
+        self.max_speed_t = torch.full((E, A), 2.0, **f64)
+        self.kind_t = torch.zeros((E, A), dtype=torch.int8, device=d)
+        self.active_t = torch.zeros((E, A), dtype=torch.uint8, device=d)
+        self.path_cells_t = torch.zeros((E, A, self.path_cap), dtype=torch.int32, device=d)
+        self.path_head_t = torch.zeros((E, A), dtype=torch.int32, device=d)
+        self.path_n_t = torch.zeros((E, A), dtype=torch.int32, device=d)
+
+    def _ensure_astar(self):
+        import torch
+        if self._astar_ready:
+            return
+        S = self.E * self.slots
+        N = self.nx * self.ny
+        d = self.device
+        self.astar_g_t = torch.empty((S, N), dtype=torch.float64, device=d)
+        self.astar_parent_t = torch.empty((S, N), dtype=torch.int32, device=d)
+        self.astar_stamp_t = torch.zeros((S, N), dtype=torch.int32, device=d)
+        self.astar_epoch_t = torch.zeros((S,), dtype=torch.int32, device=d)
+        self.astar_heap_t = torch.empty((S, self.heap_cap, 2), dtype=torch.int64, device=d)
+        self._astar_ready = True
+
+    def set_agents(self, agent_lists):
+        A = max((len(l) for l in agent_lists), default=0)
+        self._alloc(A)
+        self._fill([(e, l) for e, l in enumerate(agent_lists)])
+
+    def set_env_agents(self, e, agents):
+        if len(agents) > self.A:
+            lists = [self.agents_of(k) for k in range(self.E)]
+            lists[e] = agents
+            self.set_agents(lists)
+            return
+        self.active_t[e] = 0
+        self.path_n_t[e] = 0
+        self._fill([(e, agents)])
+
+    def _fill(self, rows):
+        import torch
+        for e, lst in rows:
+            n = len(lst)
+            if n == 0:
+                continue
+            pos = np.array([a.position for a in lst], dtype=np.float64)
+            vel = np.array([a.velocity for a in lst], dtype=np.float64)
+            goal = np.array([a.goal for a in lst], dtype=np.float64)
+            t = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(self.device)
+            self.pos_t[e, :n] = t(pos)
+            self.vel_t[e, :n] = t(vel)
+            self.goal_t[e, :n] = t(goal)
+            self.waypoint_t[e, :n] = t(goal)
+            self.radius_t[e, :n] = t(np.array([a.radius for a in lst], dtype=np.float64))
+            self.pref_t[e, :n] = t(np.array([a.preferred_speed for a in lst], dtype=np.float64))
+            self.max_speed_t[e, :n] = t(np.array([a.max_speed for a in lst], dtype=np.float64))
+            self.kind_t[e, :n] = t(np.array([int(a.kind) for a in lst], dtype=np.int8))
+            self.active_t[e, :n] = 1
+            self.path_n_t[e, :n] = 0
+
+    def set_from_spawn(self, batch, rows=None):
+        """Install the device spawn of a SceneBatch (step.py:37-63 outputs) for all
+        rows (re-allocates) or for the given rows (resample path)."""
+        import torch
+        A = batch.params.peds
+        if rows is None:
+            self._alloc(A)
+            idx = slice(None)
+        else:
+            idx = torch.as_tensor(rows, dtype=torch.long, device=self.device)
+        k = batch.sp_kind[idx].long()
+        rad = torch.tensor([0.3, 0.45, 0.4], dtype=torch.float64, device=self.device)
+        ms = torch.tensor([2.0, 5.0, 4.0], dtype=torch.float64, device=self.device)
+        self.pos_t[idx] = batch.sp_pos[idx]
+        self.vel_t[idx] = 0.0
+        self.goal_t[idx] = batch.sp_goal[idx]
+        self.waypoint_t[idx] = batch.sp_goal[idx]
+        self.radius_t[idx] = rad[k]
+        self.pref_t[idx] = batch.sp_pref[idx]
+        self.max_speed_t[idx] = ms[k]
+        self.kind_t[idx] = batch.sp_kind[idx]
+        self.active_t[idx] = 1
+        self.path_n_t[idx] = 0
+
+    def replace_env(self, e, occupancy):
+        """field.py:403-413 for a host OccupancyGrid."""
+        import torch
+        if occupancy.labels.shape != (self.ny, self.nx):
+            raise ValueError("replacement grid must keep the batch shape")
+        self.labels_t[e] = torch.from_numpy(np.ascontiguousarray(occupancy.labels)).to(self.device)
+        self._prepare([e])
+
+    # -- stepping (field.py:90-163) -----------------------------------------------
+    def _params(self):
+        c = self.config
+        p = _lib.CrowdParams()
+        p.E, p.A, p.nx, p.ny = self.E, self.A, self.nx, self.ny
+        p.res, p.res0 = self.res, self.res0
+        p.time_horizon = c.time_horizon
+        p.obstacle_time_horizon = c.obstacle_time_horizon
+        p.neighbor_distance = c.neighbor_distance
+        p.nd2 = c.neighbor_distance ** 2
+        p.nd2_f32 = float(np.float32(c.neighbor_distance ** 2))
+        p.max_neighbors = int(c.max_neighbors)
+        p.dt = c.dt
+        p.safety_margin = c.safety_margin
+        p.goal_reach2 = 0.3 ** 2
+        p.stall_c, p.stall_s = float(np.cos(0.6)), float(np.sin(0.6))
+        p.resample_goals = int(bool(self.resample_goals))
+        p.use_static = int(bool(self.has_obs_t.any().item()))
+        p.path_cap, p.heap_cap, p.slots_per_env = self.path_cap, self.heap_cap, self.slots
+        return p
+
+    def _state(self):
+        self._ensure_astar()
+        s = _lib.CrowdState()
+        m = dict(pos=self.pos_t, vel=self.vel_t, goal=self.goal_t, waypoint=self.waypoint_t,
+                 radius=self.radius_t, pref_speed=self.pref_t, max_speed=self.max_speed_t,
+                 active=self.active_t, path_cells=self.path_cells_t, path_head=self.path_head_t,
+                 path_n=self.path_n_t, labels=self.labels_t, nearest=self.nearest_t,
+                 has_obs=self.has_obs_t, walk=self.walk_t, walk_n=self.walk_n_t, rng=self.rng_t,
+                 last_gap=self.last_gap_t, gap_tmp=self.gap_tmp_t, flags=self.flags_t,
+                 astar_g=self.astar_g_t, astar_parent=self.astar_parent_t,
+                 astar_stamp=self.astar_stamp_t, astar_epoch=self.astar_epoch_t,
+                 astar_heap=self.astar_heap_t, counters=self.counters_t)
+        for k, v in m.items():
+            setattr(s, k, v.data_ptr())
+        return s
+
+    def prepare_step(self):
+        """Freeze the launch arguments (call again after set_agents / replace_env)."""
+        self._p = self._params()
+        self._s = self._state()
+
+    def step(self, robot_pos=None, robot_vel=None, robot_radius=0.35, env_mask=None, workers=1,
+             stream=None, check=True):
+        """Advance every (masked) env one tick.  Array inputs may be numpy (host,
+        copied in) or device tensors.  ``workers`` is accepted for API parity."""
+        import torch
+        if self.A == 0 or self.E == 0:
+            return
+        if not hasattr(self, "_p") or self._p.A != self.A:
+            self.prepare_step()
+        rp = self._dev(robot_pos, torch.float64, (self.E, 2))
+        rv = self._dev(robot_vel, torch.float64, (self.E, 2)) if robot_pos is not None else None
+        em = self._dev(env_mask, torch.uint8, (self.E,))
+        err = _lib.lib().cw_crowd_step(self._p, self._s, _lib.ptr(rp), _lib.ptr(rv),
+                                       float(robot_radius), _lib.ptr(em), self.threads,
+                                       _lib.stream_ptr(stream))
+        _lib.check(err, "cw_crowd_step")
+        if check:
+            self.check_flags()
+
+    def check_flags(self):
+        code = int(self.flags_t[1].item())
+        if code:
+            raise STATUS_ERRORS.get(code, RuntimeError)(
+                f"crowd guidance capacity exceeded (code {code}); path_cap={self.path_cap} "
+                f"heap_cap={self.heap_cap}")
+
+    def _dev(self, x, dtype, shape):
+        import torch
+        if x is None:
+            return None
+        if isinstance(x, torch.Tensor):
+            return x.to(device=self.device, dtype=dtype).reshape(shape).contiguous()
+        return torch.from_numpy(np.ascontiguousarray(np.asarray(x).astype(
+            np.uint8 if dtype == torch.uint8 else np.float64)).reshape(shape)).to(self.device)
+
+    # -- host views ----------------------------------------------------------------
+    @property
+    def pos(self):
+        return self.pos_t.cpu().numpy()
+
+    @property
+    def vel(self):
+        return self.vel_t.cpu().numpy()
+
+    @property
+    def goal(self):
+        return self.goal_t.cpu().numpy()
+
+    @property
+    def waypoint(self):
+        return self.waypoint_t.cpu().numpy()
+
+    @property
+    def radius(self):
+        return self.radius_t.cpu().numpy()
+
+    @property
+    def active(self):
+        return self.active_t.cpu().numpy().astype(bool)
+
+    @property
+    def last_gap_by_env(self):
+        return self.last_gap_t.cpu().numpy()
+
+    def agents_of(self, e):
+        """field.py:417-430."""
+        act = self.active_t[e].cpu().numpy()
+        pos, vel, goal = self.pos_t[e].cpu().numpy(), self.vel_t[e].cpu().numpy(), self.goal_t[e].cpu().numpy()
+        rad, pref = self.radius_t[e].cpu().numpy(), self.pref_t[e].cpu().numpy()
+        kind = self.kind_t[e].cpu().numpy()
+        return [CrowdAgent(id=a, position=pos[a].copy(), velocity=vel[a].copy(), radius=float(rad[a]),
+                           preferred_speed=float(pref[a]), goal=goal[a].copy(),
+                           kind=AgentKind(int(kind[a])))
+                for a in range(self.A) if act[a]]
+
+    def stats(self):
+        c = self.counters_t.cpu().numpy()
+        return {"astar_expansions": int(c[0]), "path_points_scanned": int(c[1]),
+                "lp_fallbacks": int(c[2]), "stall_retries": int(c[3])}
+
+
+def step_crowd(agents, robot_state, occupancy, config, seed=0, resample_goals=True):
+    """step.py:17-34 (one env, one tick)."""
+    if not agents:
+        return []
+    f = CrowdField([occupancy], config, [seed], resample_goals=resample_goals)
+    f.set_agents([agents])
+    if robot_state is None:
+        f.step()
+    else:
+        rp, rv, rr = robot_state
+        f.step(robot_pos=np.asarray(rp, np.float64).reshape(1, 2),
+               robot_vel=np.asarray(rv, np.float64).reshape(1, 2), robot_radius=rr)
+    return f.agents_of(0)
+
+
+def spawn_agents(occupancy, count, seed, region_mask=None):
+    """step.py:37-63 through the device sampler's spawn stage."""
+    import torch
+    if count == 0:
+        return []
+    if region_mask is not None:
+        raise NotImplementedError("custom region masks: use the Traverse spec path")
+    from .urbangen import SceneBatch
+    ny, nx = occupancy.labels.shape
+    p = _lib.SceneParams()
+    p.nx, p.ny, p.res = nx, ny, float(occupancy.resolution)
+    p.peds = int(count)
+    p.obj_max = 1
+    b = SceneBatch(p, 1)
+    b.labels[0] = torch.from_numpy(np.ascontiguousarray(occupancy.labels)).to(b.device)
+    from .rng import seeds_to_tensor
+    seeds = seeds_to_tensor([seed], b.device)
+    err = _lib.lib().cw_spawn_agents(p, 1, _lib.ptr(seeds), None, _lib.ptr(b.seed_scratch),
+                                     b.buffers(), _lib.stream_ptr())
+    _lib.check(err, "cw_spawn_agents")
+    b.check_status()
+    pos, goal = b.sp_pos[0].cpu().numpy(), b.sp_goal[0].cpu().numpy()
+    kind, pref = b.sp_kind[0].cpu().numpy(), b.sp_pref[0].cpu().numpy()
+    return [CrowdAgent(id=i, position=pos[i], velocity=np.zeros(2),
+                       radius=RADIUS_OF_KIND[AgentKind(int(kind[i]))], preferred_speed=float(pref[i]),
+                       goal=goal[i], kind=AgentKind(int(kind[i]))) for i in range(count)]

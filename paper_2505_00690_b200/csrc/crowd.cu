@@ -1,0 +1,771 @@
+// Crowd dynamics step on B200: one CTA per env, one warp per agent.
+//
+//   guidance   field.py:165-212 (+ _line_of_sight :601, _distance_to_polyline :613,
+//              paths.astar_path paths.py:48-87)
+//   pref       field.py:214-227
+//   neighbours field.py:246-262  fp32 Gram key fma(y_i,y_j,x_i*x_j), stable top-K
+//   half-plane field.py:448-495  (+ robot lane :303-317, static lane :319-348)
+//   LP         field.py:500-566  lane-parallel 1-D solve, warp max/min reductions
+//   fallback   orca.py:155-242   _solve_least_violation / _lp2_toward / _solve_on_line
+//   stall      field.py:135-150; commit + blocked field.py:152-160, 352-366
+//   resample   field.py:368-381; last_gap_by_env field.py:268-271
+//
+// Two-phase: every CTA snapshots its env's pre-step state in shared memory,
+// so results are independent of scheduling (field.py:1-9).  Compiled with
+// -fmad=false: float64 arithmetic rounds exactly like the numpy reference.
+#include <cfloat>
+#include <math_constants.h>
+#include "common.cuh"
+#include "crowd_types.cuh"
+#include "rng.cuh"
+#include "scene_types.cuh"
+
+namespace cw {
+
+constexpr int MAXC = 12;   // neighbour lanes (<= 10) + robot + static
+constexpr double kWaypointReach = 0.5, kStrayLimit = 1.0;
+
+struct HeapEnt { double f; int32_t cell; int32_t pad; };
+
+struct WarpCons {
+  double px[MAXC], py[MAXC], nx[MAXC], ny[MAXC];
+};
+
+// ---------------------------------------------------------------- VO half-plane
+// field.py:448-495 for one lane (the selected branch of the vectorised where()).
+CW_DEV void vo_halfplane(double rp0, double rp1, double rv0, double rv1, double rr, double horizon,
+                         double dt, double vs0, double vs1, double share, double& pt0, double& pt1,
+                         double& n0, double& n1) {
+  double dsq = rp0 * rp0 + rp1 * rp1;
+  double rsq = rr * rr;
+  double u0, u1;
+  if (dsq <= rsq) {
+    double wc0 = rv0 - rp0 / dt, wc1 = rv1 - rp1 / dt;
+    double wcl = sqrt(wc0 * wc0 + wc1 * wc1);
+    double dist = sqrt(dsq);
+    double uc0, uc1;
+    if (wcl > kEps) {
+      double s = fmax(wcl, kEps);
+      uc0 = wc0 / s; uc1 = wc1 / s;
+    } else {
+      double s = fmax(dist, kEps);
+      uc0 = -rp0 / s; uc1 = -rp1 / s;
+    }
+    if (wcl <= kEps && dist <= kEps) { uc0 = 1.0; uc1 = 0.0; }
+    double k = rr / dt - wcl;
+    u0 = k * uc0; u1 = k * uc1;
+    n0 = uc0; n1 = uc1;
+  } else {
+    double w0 = rv0 - rp0 / horizon, w1 = rv1 - rp1 / horizon;
+    double wlsq = w0 * w0 + w1 * w1;
+    double d1 = w0 * rp0 + w1 * rp1;
+    if (d1 < 0.0 && d1 * d1 > rsq * wlsq) {
+      double wl = sqrt(wlsq);
+      double s = fmax(wl, kEps);
+      double uw0 = w0 / s, uw1 = w1 / s;
+      double k = rr / horizon - wl;
+      u0 = k * uw0; u1 = k * uw1;
+      n0 = uw0; n1 = uw1;
+    } else {
+      double leg = sqrt(fmax(dsq - rsq, 0.0));
+      double det = rp0 * w1 - rp1 * w0;
+      double sg = det > 0.0 ? 1.0 : -1.0;
+      double sd2 = fmax(dsq, kEps);
+      double ld0 = (rp0 * leg - sg * rp1 * rr) / sd2;
+      double ld1 = (sg * rp0 * rr + rp1 * leg) / sd2;
+      n0 = -sg * ld1; n1 = sg * ld0;
+      double d2v = rv0 * ld0 + rv1 * ld1;
+      u0 = d2v * ld0 - rv0; u1 = d2v * ld1 - rv1;
+    }
+  }
+  pt0 = vs0 + share * u0;
+  pt1 = vs1 + share * u1;
+}
+
+// ---------------------------------------------------------------- scalar fallback
+// orca.py:155-189, dir_opt=True (only mode the fallback uses)
+CW_DEV bool solve_on_line_dir(const double* cpx, const double* cpy, const double* cnx,
+                              const double* cny, int i, double ms, double o0, double o1,
+                              double& r0, double& r1) {
+  double px = cpx[i], py = cpy[i];
+  double dx = -cny[i], dy = cnx[i];
+  double dpd = dot2_blas(px, py, dx, dy);
+  double disc = dpd * dpd + ms * ms - dot2_blas(px, py, px, py);
+  if (disc < 0.0) return false;
+  double sq = sqrt(disc);
+  double tl = -dpd - sq, tr = -dpd + sq;
+  for (int j = 0; j < i; ++j) {
+    double den = dot2_blas(dx, dy, cnx[j], cny[j]);
+    double num = dot2_blas(cpx[j] - px, cpy[j] - py, cnx[j], cny[j]);
+    if (fabs(den) < kEps) {
+      if (num > kEps) return false;
+      continue;
+    }
+    double t = num / den;
+    if (den > 0.0) tl = fmax(tl, t);
+    else tr = fmin(tr, t);
+    if (tl > tr) return false;
+  }
+  double tb = dot2_blas(o0, o1, dx, dy) > 0.0 ? tr : tl;
+  r0 = px + tb * dx;
+  r1 = py + tb * dy;
+  return true;
+}
+
+CW_DEV void least_violation(const WarpCons& C, int nc, int begin, double ms, double& r0,
+                            double& r1) {
+  // orca.py:196-212
+  double dist = 0.0;
+  double qpx[MAXC], qpy[MAXC], qnx[MAXC], qny[MAXC];
+  for (int i = begin; i < nc; ++i) {
+    double pix = C.px[i], piy = C.py[i], nix = C.nx[i], niy = C.ny[i];
+    double viol = -dot2_blas(r0 - pix, r1 - piy, nix, niy);
+    if (viol <= dist + kEps) continue;
+    int np = 0;
+    for (int j = 0; j < i; ++j) {
+      double pjx = C.px[j], pjy = C.py[j], njx = C.nx[j], njy = C.ny[j];
+      double det = nix * njy - niy * njx;
+      double dfx = njx - nix, dfy = njy - niy;
+      double mx, my;
+      if (fabs(det) < kEps) {
+        if (dot2_blas(nix, niy, njx, njy) > 0.0) continue;
+        mx = 0.5 * (pix + pjx);
+        my = 0.5 * (piy + pjy);
+      } else {
+        double dix = -niy, diy = nix;
+        double t = dot2_blas(pjx - pix, pjy - piy, njx, njy) / dot2_blas(dix, diy, njx, njy);
+        mx = pix + t * dix;
+        my = piy + t * diy;
+      }
+      double nrm = glibc_hypot(dfx, dfy);
+      if (nrm < kEps) continue;
+      qpx[np] = mx; qpy[np] = my; qnx[np] = dfx / nrm; qny[np] = dfy / nrm;
+      ++np;
+    }
+    // _lp2_toward(proj, ms, n_i)
+    double s = ms / fmax(glibc_hypot(nix, niy), kEps);
+    double t0 = nix * s, t1 = niy * s;
+    bool ok = true;
+    for (int k = 0; k < np && ok; ++k) {
+      if (dot2_blas(t0 - qpx[k], t1 - qpy[k], qnx[k], qny[k]) < -kEps)
+        ok = solve_on_line_dir(qpx, qpy, qnx, qny, k, ms, nix, niy, t0, t1);
+    }
+    if (ok) { r0 = t0; r1 = t1; }
+    dist = -dot2_blas(r0 - pix, r1 - piy, nix, niy);
+  }
+}
+
+// ---------------------------------------------------------------- warp LP
+// field.py:500-566 for one agent.  Lane k holds constraint k; all lanes keep
+// the running result.  Returns true when the fallback ran.
+CW_DEV bool warp_lp(const WarpCons& C, int nc, double pf0, double pf1, double ms, double& r0,
+                    double& r1, int lane) {
+  double pn = sqrt(pf0 * pf0 + pf1 * pf1);
+  double sc = pn > ms ? ms / fmax(pn, kEps) : 1.0;
+  r0 = pf0 * sc;
+  r1 = pf1 * sc;
+  const bool mine = lane < nc;
+  const double mpx = mine ? C.px[lane] : 0.0, mpy = mine ? C.py[lane] : 0.0;
+  const double mnx = mine ? C.nx[lane] : 1.0, mny = mine ? C.ny[lane] : 0.0;
+  for (int i = 0; i < nc; ++i) {
+    const double pi0 = C.px[i], pi1 = C.py[i], ni0 = C.nx[i], ni1 = C.ny[i];
+    if (!((r0 - pi0) * ni0 + (r1 - pi1) * ni1 < -kEps)) continue;
+    const double d0 = -ni1, d1 = ni0;
+    const double dpd = pi0 * d0 + pi1 * d1;
+    const double disc = dpd * dpd + ms * ms - (pi0 * pi0 + pi1 * pi1);
+    bool bad = disc < 0.0;
+    const double sq = sqrt(fmax(disc, 0.0));
+    double tl = -dpd - sq, tr = -dpd + sq;
+    double tlj = -DBL_MAX, trj = DBL_MAX;
+    bool badj = false;
+    if (lane < i) {
+      double den = d0 * mnx + d1 * mny;
+      double num = (mpx - pi0) * mnx + (mpy - pi1) * mny;
+      if (fabs(den) < kEps) {
+        badj = num > kEps;
+      } else {
+        double t = num / den;
+        if (den > 0.0) tlj = t;
+        else trj = t;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      tlj = fmax(tlj, __shfl_xor_sync(0xffffffffu, tlj, o));
+      trj = fmin(trj, __shfl_xor_sync(0xffffffffu, trj, o));
+    }
+    bad |= __any_sync(0xffffffffu, badj);
+    tl = fmax(tl, tlj);
+    tr = fmin(tr, trj);
+    bad |= tl > tr;
+    if (bad) {
+      if (lane == 0) least_violation(C, nc, i, ms, r0, r1);
+      r0 = __shfl_sync(0xffffffffu, r0, 0);
+      r1 = __shfl_sync(0xffffffffu, r1, 0);
+      return true;
+    }
+    double tb = (pf0 - pi0) * d0 + (pf1 - pi1) * d1;
+    tb = fmin(fmax(tb, tl), tr);
+    r0 = pi0 + tb * d0;
+    r1 = pi1 + tb * d1;
+  }
+  return false;
+}
+
+// ---------------------------------------------------------------- A*
+CW_DEV double octile(int r, int c, int gr, int gc) {
+  int dr = abs(r - gr), dc = abs(c - gc);
+  return kSqrt2 * (double)min(dr, dc) + (double)abs(dr - dc);
+}
+
+struct AStarCtx {
+  double* g;
+  int32_t* parent;
+  int32_t* stamp;
+  HeapEnt* heap;
+  int cap;
+  int epoch;
+  int nx, ny;
+  int gr, gc;
+};
+
+// (f, h, row, col) tuple order of paths.py:216/238
+CW_DEV bool heap_less(const AStarCtx& X, const HeapEnt& a, const HeapEnt& b) {
+  if (a.f != b.f) return a.f < b.f;
+  double ha = octile(a.cell / X.nx, a.cell % X.nx, X.gr, X.gc);
+  double hb = octile(b.cell / X.nx, b.cell % X.nx, X.gr, X.gc);
+  if (ha != hb) return ha < hb;
+  return a.cell < b.cell;
+}
+
+CW_DEV void heap_push(AStarCtx& X, int& n, HeapEnt v) {
+  int i = n++;
+  while (i > 0) {
+    int p = (i - 1) >> 1;
+    HeapEnt pv = X.heap[p];
+    if (!heap_less(X, v, pv)) break;
+    X.heap[i] = pv;
+    i = p;
+  }
+  X.heap[i] = v;
+}
+
+CW_DEV HeapEnt heap_pop(AStarCtx& X, int& n) {
+  HeapEnt top = X.heap[0];
+  HeapEnt last = X.heap[--n];
+  int i = 0;
+  while (true) {
+    int l = 2 * i + 1;
+    if (l >= n) break;
+    int r = l + 1;
+    int m = (r < n && heap_less(X, X.heap[r], X.heap[l])) ? r : l;
+    if (!heap_less(X, X.heap[m], last)) break;
+    X.heap[i] = X.heap[m];
+    i = m;
+  }
+  if (n > 0) X.heap[i] = last;
+  return top;
+}
+
+// paths.py:48-87.  Returns the path length in cells (>= 1), 0 when unreachable,
+// -1 on heap overflow.  The path is recovered through X.parent.
+CW_DEV int warp_astar(AStarCtx& X, const uint8_t* lab, int sr, int sc, int lane,
+                      long long& expansions) {
+  const int nx = X.nx, ny = X.ny;
+  auto passable = [&](int r, int c) { return lab[r * nx + c] != L_OBSTACLE; };
+  if (!(passable(sr, sc) && passable(X.gr, X.gc))) return 0;
+  const int start = sr * nx + sc, goal = X.gr * nx + X.gc;
+  int n = 0;  // heap size (lane 0 authoritative, broadcast)
+  if (lane == 0) {
+    X.g[start] = 0.0;
+    X.stamp[start] = X.epoch;
+    X.parent[start] = -1;
+    double h0 = octile(sr, sc, X.gr, X.gc);
+    HeapEnt e0 = {h0, start, 0};
+    heap_push(X, n, e0);
+  }
+  __syncwarp();
+  n = __shfl_sync(0xffffffffu, n, 0);
+  const int mdr[8] = {-1, 1, 0, 0, -1, -1, 1, 1};
+  const int mdc[8] = {0, 0, -1, 1, -1, 1, -1, 1};
+  while (n > 0) {
+    HeapEnt top;
+    if (lane == 0) top = heap_pop(X, n);
+    top.f = __shfl_sync(0xffffffffu, top.f, 0);
+    top.cell = __shfl_sync(0xffffffffu, top.cell, 0);
+    n = __shfl_sync(0xffffffffu, n, 0);
+    const int x = top.cell;
+    if (x == goal) return -2;  // found (caller walks parents)
+    const int r = x / nx, c = x - r * nx;
+    const double gx = X.g[x];
+    if (top.f > gx + octile(r, c, X.gr, X.gc) + 1e-12) continue;
+    ++expansions;
+    bool push = false;
+    double nf = 0.0;
+    int y = -1;
+    if (lane < 8) {
+      int rr = r + mdr[lane], cc = c + mdc[lane];
+      if (rr >= 0 && rr < ny && cc >= 0 && cc < nx && passable(rr, cc) &&
+          (lane < 4 || (passable(r, cc) && passable(rr, c)))) {
+        y = rr * nx + cc;
+        double ng = gx + (lane < 4 ? 1.0 : kSqrt2);
+        double old = X.stamp[y] == X.epoch ? X.g[y] : CUDART_INF;
+        if (ng < old - 1e-12) {
+          X.g[y] = ng;
+          X.stamp[y] = X.epoch;
+          X.parent[y] = x;
+          nf = ng + octile(rr, cc, X.gr, X.gc);
+          push = true;
+        }
+      }
+    }
+    unsigned m = __ballot_sync(0xffffffffu, push);
+    __syncwarp();
+    for (int k = 0; k < 8; ++k) {
+      if (!((m >> k) & 1u)) continue;
+      double fk = __shfl_sync(0xffffffffu, nf, k);
+      int yk = __shfl_sync(0xffffffffu, y, k);
+      if (lane == 0) {
+        if (n >= X.cap) { n = -1; }
+        else { HeapEnt ev = {fk, yk, 0}; heap_push(X, n, ev); }
+      }
+    }
+    n = __shfl_sync(0xffffffffu, n, 0);
+    if (n < 0) return -1;
+    __syncwarp();
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------- the step kernel
+struct StepSmem {
+  // sized dynamically: A * (pos 2 + vel 2 + newpos 2 + radius) doubles + A act bytes
+};
+
+CW_DEV void path_point(const int32_t* cells, int head, int n, int k, double gx, double gy,
+                       double res, int nx, double& x, double& y) {
+  if (k == n - 1) { x = gx; y = gy; return; }
+  int f = cells[head + k];
+  int r = f / nx, c = f - r * nx;
+  x = ((double)c + 0.5) * res;
+  y = ((double)r + 0.5) * res;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_crowd_step(cw_crowd_params P, cw_crowd_state S,
+                                                   const double* __restrict__ robot_pos,
+                                                   const double* __restrict__ robot_vel,
+                                                   double robot_radius,
+                                                   const uint8_t* __restrict__ env_mask) {
+  constexpr int NW = NT / 32;
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int e = blockIdx.x;
+  const int A = P.A;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* s_px = reinterpret_cast<double*>(sm);
+  double* s_py = s_px + A;
+  double* s_vx = s_py + A;
+  double* s_vy = s_vx + A;
+  double* s_r = s_vy + A;
+  double* s_nx = s_r + A;   // post-commit positions (resample)
+  double* s_ny = s_nx + A;
+  WarpCons* s_cons = reinterpret_cast<WarpCons*>(s_ny + A);
+  uint8_t* s_act = reinterpret_cast<uint8_t*>(s_cons + NW);
+  __shared__ double s_gap[NW];
+  __shared__ int s_anynb[NW];
+
+  const size_t eA = (size_t)e * A;
+  const bool emask = env_mask ? env_mask[e] != 0 : true;
+  for (int a = threadIdx.x; a < A; a += NT) {
+    s_px[a] = S.pos[(eA + a) * 2];
+    s_py[a] = S.pos[(eA + a) * 2 + 1];
+    s_vx[a] = S.vel[(eA + a) * 2];
+    s_vy[a] = S.vel[(eA + a) * 2 + 1];
+    s_r[a] = S.radius[eA + a];
+    s_nx[a] = s_px[a];
+    s_ny[a] = s_py[a];
+    s_act[a] = (S.active[eA + a] && emask) ? 1 : 0;
+  }
+  __syncthreads();
+
+  const int nx = P.nx, ny = P.ny;
+  const size_t N = (size_t)nx * ny;
+  const uint8_t* lab = S.labels + e * N;
+  const bool has_obs = S.has_obs[e] != 0;
+  const double res = P.res;
+  const bool use_robot = robot_pos != nullptr;
+  double rpx = 0, rpy = 0, rvx = 0, rvy = 0;
+  if (use_robot) {
+    rpx = robot_pos[e * 2]; rpy = robot_pos[e * 2 + 1];
+    if (robot_vel) { rvx = robot_vel[e * 2]; rvy = robot_vel[e * 2 + 1]; }
+  }
+  WarpCons& C = s_cons[wid];
+  double my_gap = CUDART_INF;
+  int my_anynb = 0;
+  long long exp_count = 0, scanned = 0, fallbacks = 0, stalls = 0;
+  const int slot = e * P.slots_per_env + wid;
+  AStarCtx X;
+  X.g = S.astar_g + (size_t)slot * N;
+  X.parent = S.astar_parent + (size_t)slot * N;
+  X.stamp = S.astar_stamp + (size_t)slot * N;
+  X.heap = reinterpret_cast<HeapEnt*>(S.astar_heap) + (size_t)slot * P.heap_cap;
+  X.cap = P.heap_cap;
+  X.nx = nx;
+  X.ny = ny;
+
+  for (int a = wid; a < A; a += NW) {
+    if (!s_act[a]) continue;
+    const double px = s_px[a], py = s_py[a];
+    const size_t ia = eA + a;
+    const double gx = S.goal[ia * 2], gy = S.goal[ia * 2 + 1];
+    double wx, wy;
+    // ---------------- guidance (field.py:165-212)
+    if (!has_obs) {
+      wx = gx; wy = gy;
+    } else {
+      int32_t* cells = S.path_cells + ia * P.path_cap;
+      int head = S.path_head[ia], n = S.path_n[ia];
+      bool have = false;
+      if (n > 0) {
+        double qx, qy;
+        path_point(cells, head, n, 0, gx, gy, res, nx, qx, qy);
+        if (glibc_hypot(qx - px, qy - py) < kWaypointReach && n > 1) { ++head; --n; }
+        // _distance_to_polyline over the remaining points
+        double best = CUDART_INF;
+        if (lane == 0) {
+          path_point(cells, head, n, 0, gx, gy, res, nx, qx, qy);
+          best = glibc_hypot(qx - px, qy - py);
+        }
+        for (int k = 1 + lane; k < n; k += 32) {
+          double ax, ay, bx, by;
+          path_point(cells, head, n, k - 1, gx, gy, res, nx, ax, ay);
+          path_point(cells, head, n, k, gx, gy, res, nx, bx, by);
+          double abx = bx - ax, aby = by - ay;
+          double den = dot2_blas(abx, aby, abx, aby);
+          double t = 0.0;
+          if (!(den < kEps)) t = fmin(fmax(dot2_blas(px - ax, py - ay, abx, aby) / den, 0.0), 1.0);
+          double d = glibc_hypot(ax + t * abx - px, ay + t * aby - py);
+          best = fmin(best, d);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
+        scanned += n;
+        if (best <= kStrayLimit) {
+          path_point(cells, head, n, 0, gx, gy, res, nx, wx, wy);
+          have = true;
+        }
+      }
+      if (!have) {
+        // _line_of_sight(passable, pos, goal)
+        double d = glibc_hypot(gx - px, gy - py);
+        long long ns = max(2LL, trunc_ll(2.0 * d / res) + 2);
+        double step = 1.0 / (double)(ns - 1);
+        bool clear = true;
+        for (long long k = lane; k < ns; k += 32) {
+          double t = k == ns - 1 ? 1.0 : (double)k * step + 0.0;
+          double xs = px + (gx - px) * t, ys = py + (gy - py) * t;
+          long long rr = clampll(trunc_ll(ys / res), 0, ny - 1);
+          long long cc = clampll(trunc_ll(xs / res), 0, nx - 1);
+          if (lab[rr * nx + cc] == L_OBSTACLE) clear = false;
+        }
+        clear = __all_sync(0xffffffffu, clear);
+        bool one_point = true;
+        if (!clear) {
+          int sr = (int)fmin(fmax(py / res, 0.0), (double)(ny - 1));
+          int sc = (int)fmin(fmax(px / res, 0.0), (double)(nx - 1));
+          X.gr = (int)fmin(fmax(gy / res, 0.0), (double)(ny - 1));
+          X.gc = (int)fmin(fmax(gx / res, 0.0), (double)(nx - 1));
+          if (lane == 0) X.epoch = ++S.astar_epoch[slot];
+          X.epoch = __shfl_sync(0xffffffffu, X.epoch, 0);
+          int res_code = warp_astar(X, lab, sr, sc, lane, exp_count);
+          if (res_code == -1) {
+            if (lane == 0) atomicCAS(&S.flags[1], 0, (int)CW_E_HEAPCAP);
+          } else if (res_code == -2) {
+            // walk parents goal -> start; L = path length in cells
+            const int goal_cell = X.gr * nx + X.gc;
+            int L = 0;
+            for (int v = goal_cell; v >= 0; v = X.parent[v]) ++L;
+            if (L >= 2) {
+              if (L - 1 > P.path_cap) {
+                if (lane == 0) atomicCAS(&S.flags[1], 0, (int)CW_E_PATHCAP);
+              } else {
+                if (lane == 0) {
+                  int k = L - 2;
+                  for (int v = goal_cell; k >= 0; v = X.parent[v]) cells[k--] = v;
+                }
+                __syncwarp();
+                head = 0;
+                n = L;  // L-1 cells + the goal point
+                one_point = false;
+                path_point(cells, head, n, 0, gx, gy, res, nx, wx, wy);
+              }
+            }
+          }
+        }
+        if (one_point) {
+          head = 0;
+          n = 1;
+          wx = gx; wy = gy;
+        }
+      }
+      if (lane == 0) {
+        S.path_head[ia] = head;
+        S.path_n[ia] = n;
+      }
+    }
+    if (lane == 0) {
+      S.waypoint[ia * 2] = wx;
+      S.waypoint[ia * 2 + 1] = wy;
+    }
+    // ---------------- preferred velocity (field.py:214-227)
+    const double sp = S.pref_speed[ia];
+    double tw0 = wx - px, tw1 = wy - py;
+    double dist = sqrt(tw0 * tw0 + tw1 * tw1);
+    double safe = fmax(dist, kEps);
+    double pf0 = tw0 / safe * sp, pf1 = tw1 / safe * sp;
+    double tg0 = gx - px, tg1 = gy - py;
+    double dg = sqrt(tg0 * tg0 + tg1 * tg1);
+    double scl = fmin(1.0, dg / fmax(sp * P.dt * 4, kEps));
+    pf0 = pf0 * scl;
+    pf1 = pf1 * scl;
+    // ---------------- neighbours: fp32 Gram key, stable top-K (field.py:246-262)
+    const float xi = (float)px, yi = (float)py;
+    const float sqi = __fadd_rn(__fmul_rn(xi, xi), __fmul_rn(yi, yi));
+    const double vxa = s_vx[a], vya = s_vy[a], ra = s_r[a];
+    float last_k = -CUDART_INF_F;
+    int last_j = -1;
+    int nb = 0;
+    int my_nb = -1;
+    const int kmax = min(P.max_neighbors, max(A - 1, 0));
+    for (int round = 0; round < kmax; ++round) {
+      float bk = CUDART_INF_F;
+      int bj = 0x7fffffff;
+      for (int j = lane; j < A; j += 32) {
+        if (j == a || !s_act[j]) continue;
+        float xj = (float)s_px[j], yj = (float)s_py[j];
+        float sqj = __fadd_rn(__fmul_rn(xj, xj), __fmul_rn(yj, yj));
+        float dot = __fmaf_rn(yi, yj, __fmul_rn(xi, xj));
+        float key = __fsub_rn(__fadd_rn(sqi, sqj), __fmul_rn(2.0f, dot));
+        if (!(key < P.nd2_f32)) continue;
+        bool after = key > last_k || (key == last_k && j > last_j);
+        bool better = key < bk || (key == bk && j < bj);
+        if (after && better) { bk = key; bj = j; }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        float ok_ = __shfl_xor_sync(0xffffffffu, bk, o);
+        int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (ok_ < bk || (ok_ == bk && oj < bj)) { bk = ok_; bj = oj; }
+      }
+      if (bj == 0x7fffffff) break;
+      if (lane == round) my_nb = bj;
+      last_k = bk;
+      last_j = bj;
+      ++nb;
+    }
+    // ---------------- constraints (compact list of valid lanes)
+    if (lane < nb) {
+      const int j = my_nb;
+      double rp0 = s_px[j] - px, rp1 = s_py[j] - py;
+      double rv0 = vxa - s_vx[j], rv1 = vya - s_vy[j];
+      double rr = ra + s_r[j] + P.safety_margin;
+      vo_halfplane(rp0, rp1, rv0, rv1, rr, P.time_horizon, P.dt, vxa, vya, 0.5, C.px[lane],
+                   C.py[lane], C.nx[lane], C.ny[lane]);
+      if (lane == 0) {
+        // per-env nearest separation gap (field.py:268-271)
+        double d_near = sqrt(rp0 * rp0 + rp1 * rp1);
+        my_gap = fmin(my_gap, d_near - (ra + s_r[j]));
+        my_anynb = 1;
+      }
+    }
+    int nc = nb;
+    if (use_robot) {
+      double rp0 = rpx - px, rp1 = rpy - py;
+      double d2 = rp0 * rp0 + rp1 * rp1;
+      if (d2 < P.nd2) {
+        if (lane == nc) {
+          double rr = ra + robot_radius + P.safety_margin;
+          vo_halfplane(rp0, rp1, vxa - rvx, vya - rvy, rr, P.obstacle_time_horizon, P.dt, vxa, vya,
+                       1.0, C.px[lane], C.py[lane], C.nx[lane], C.ny[lane]);
+        }
+        ++nc;
+      }
+    }
+    if (P.use_static && has_obs) {
+      long long ri = clampll(trunc_ll(py / res), 0, ny - 1);
+      long long ci = clampll(trunc_ll(px / res), 0, nx - 1);
+      int flat = S.nearest[e * N + ri * nx + ci];
+      if (flat >= 0) {
+        int orow = flat / nx, ocol = flat - orow * nx;
+        double rp0 = ((double)ocol + 0.5) * res - px, rp1 = ((double)orow + 0.5) * res - py;
+        double d2 = rp0 * rp0 + rp1 * rp1;
+        if (d2 < P.nd2) {
+          if (lane == nc) {
+            double margin = 0.5 * kSqrt2 * P.res0;
+            double rr = ra + margin + P.safety_margin;
+            vo_halfplane(rp0, rp1, vxa, vya, rr, P.obstacle_time_horizon, P.dt, vxa, vya, 1.0,
+                         C.px[lane], C.py[lane], C.nx[lane], C.ny[lane]);
+          }
+          ++nc;
+        }
+      }
+    }
+    __syncwarp();
+    // ---------------- LP + stall retry (field.py:133-150)
+    const double ms = S.max_speed[ia];
+    double v0, v1;
+    fallbacks += warp_lp(C, nc, pf0, pf1, ms, v0, v1, lane);
+    double spd = sqrt(v0 * v0 + v1 * v1);
+    double want = sqrt(pf0 * pf0 + pf1 * pf1);
+    if (spd < 0.2 * want && want > 1e-6) {
+      ++stalls;
+      double q0 = P.stall_c * pf0 + P.stall_s * pf1;
+      double q1 = -P.stall_s * pf0 + P.stall_c * pf1;
+      fallbacks += warp_lp(C, nc, q0, q1, ms, v0, v1, lane);
+    }
+    // ---------------- commit (field.py:152-160, 352-366)
+    double npx = px + v0 * P.dt, npy = py + v1 * P.dt;
+    bool out = npx < 0 || npy < 0 || npx >= nx * res || npy >= ny * res;
+    long long rr = clampll(trunc_ll(npy / res), 0, ny - 1);
+    long long cc = clampll(trunc_ll(npx / res), 0, nx - 1);
+    bool blocked = out || lab[rr * nx + cc] == L_OBSTACLE;
+    if (lane == 0) {
+      if (!blocked) {
+        S.pos[ia * 2] = npx;
+        S.pos[ia * 2 + 1] = npy;
+        s_nx[a] = npx;
+        s_ny[a] = npy;
+      }
+      S.vel[ia * 2] = blocked ? 0.0 : v0;
+      S.vel[ia * 2 + 1] = blocked ? 0.0 : v1;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    s_gap[wid] = my_gap;
+    s_anynb[wid] = my_anynb;
+  }
+  __syncthreads();
+  // ---------------- goal resample, agent order (field.py:368-381)
+  if (threadIdx.x == 0) {
+    double g = CUDART_INF;
+    int anynb = 0;
+    for (int w = 0; w < NW; ++w) { g = fmin(g, s_gap[w]); anynb |= s_anynb[w]; }
+    S.gap_tmp[e] = g;
+    if (anynb) atomicOr(&S.flags[0], 1);
+    if (P.resample_goals) {
+      Pcg64Raw* raw = reinterpret_cast<Pcg64Raw*>(S.rng) + e;
+      bool loaded = false;
+      Pcg64 rng;
+      const int wn = S.walk_n[e];
+      for (int a = 0; a < A; ++a) {
+        if (!s_act[a]) continue;
+        const size_t ia = eA + a;
+        double dx = S.goal[ia * 2] - s_nx[a], dy = S.goal[ia * 2 + 1] - s_ny[a];
+        if (!(dx * dx + dy * dy < P.goal_reach2)) continue;
+        if (!loaded) { rng = pcg_load(*raw); loaded = true; }
+        int k = (int)integers32(rng, (uint64_t)wn);
+        int f = S.walk[e * N + k];
+        int r = f / nx, c = f - r * nx;
+        S.goal[ia * 2] = ((double)c + 0.5) * res;
+        S.goal[ia * 2 + 1] = ((double)r + 0.5) * res;
+        S.path_n[ia] = 0;
+      }
+      if (loaded) pcg_store(*raw, rng);
+    }
+  }
+  if (lane == 0 && S.counters) {
+    if (exp_count) atomicAdd((unsigned long long*)&S.counters[0], (unsigned long long)exp_count);
+    if (scanned) atomicAdd((unsigned long long*)&S.counters[1], (unsigned long long)scanned);
+    if (fallbacks) atomicAdd((unsigned long long*)&S.counters[2], (unsigned long long)fallbacks);
+    if (stalls) atomicAdd((unsigned long long*)&S.counters[3], (unsigned long long)stalls);
+  }
+  // ---------------- last CTA publishes last_gap_by_env (only when any row had K > 0)
+  if (threadIdx.x == 0) {
+    __threadfence();
+    int ticket = atomicAdd(&S.flags[2], 1);
+    if (ticket == gridDim.x - 1) {
+      __threadfence();
+      if (atomicAdd(&S.flags[0], 0)) {
+        for (int k = 0; k < P.E; ++k) S.last_gap[k] = ((volatile double*)S.gap_tmp)[k];
+      }
+      S.flags[0] = 0;
+      S.flags[2] = 0;
+    }
+  }
+}
+
+__global__ void k_seed_streams(int n, const uint64_t* __restrict__ seeds, Pcg64Raw* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) pcg_store(out[i], pcg_seed(seeds[i]));
+}
+
+__global__ void k_child_seeds(int n, const uint64_t* __restrict__ parent, int label_id,
+                              const uint64_t* __restrict__ k, uint64_t* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const char* labels[4] = {"env", "crowd-run", "crowd", "resample"};
+  if (k) out[i] = child_seed(parent[i], labels[label_id], k[i]);
+  else out[i] = child_seed(parent[i], labels[label_id]);
+}
+
+}  // namespace cw
+
+extern "C" {
+
+size_t cw_crowd_step_smem_bytes(int A, int nt) {
+  return (size_t)A * 7 * sizeof(double) + (size_t)(nt / 32) * sizeof(cw::WarpCons) + (size_t)A + 16;
+}
+
+// One two-phase tick of every env (field.py:90-163).  robot_pos/robot_vel
+// (E,2) may be NULL; env_mask (E) may be NULL.  Stream-ordered, no host sync.
+int cw_crowd_step(const cw_crowd_params* P, const cw_crowd_state* S, const double* robot_pos,
+                  const double* robot_vel, double robot_radius, const uint8_t* env_mask,
+                  int threads, void* stream) {
+  using namespace cw;
+  if (P->E <= 0 || P->A <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  size_t sm = cw_crowd_step_smem_bytes(P->A, threads);
+  if (threads == 128) {
+    if (sm > 48 * 1024)
+      cudaFuncSetAttribute(k_crowd_step<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_crowd_step<128><<<P->E, 128, sm, st>>>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask);
+  } else if (threads == 256) {
+    if (sm > 48 * 1024)
+      cudaFuncSetAttribute(k_crowd_step<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_crowd_step<256><<<P->E, 256, sm, st>>>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask);
+  } else {
+    if (sm > 48 * 1024)
+      cudaFuncSetAttribute(k_crowd_step<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_crowd_step<64><<<P->E, 64, sm, st>>>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask);
+  }
+  return (int)cudaGetLastError();
+}
+
+// PCG64 stream states from integer seeds (numpy PCG64(seed) via SeedSequence).
+int cw_seed_streams(int n, const uint64_t* seeds, void* out, void* stream) {
+  if (n <= 0) return 0;
+  cw::k_seed_streams<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(n, seeds,
+                                                                       (cw::Pcg64Raw*)out);
+  return (int)cudaGetLastError();
+}
+
+// child_seed(parent[i], label[, k[i]]) for label ids 0 "env", 1 "crowd-run", 2 "crowd", 3 "resample"
+int cw_child_seeds(int n, const uint64_t* parent, int label_id, const uint64_t* k, uint64_t* out,
+                   void* stream) {
+  if (n <= 0) return 0;
+  cw::k_child_seeds<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(n, parent, label_id, k, out);
+  return (int)cudaGetLastError();
+}
+
+}  // extern "C"
+
+extern "C" {
+// ABI self-check for the ctypes mirror (host-only; no device work).
+int cw_abi_sizes(size_t* out, int n) {
+  const size_t v[4] = {sizeof(cw_scene_params), sizeof(cw_scene_buffers), sizeof(cw_crowd_params),
+                       sizeof(cw_crowd_state)};
+  for (int i = 0; i < n && i < 4; ++i) out[i] = v[i];
+  return 4;
+}
+}

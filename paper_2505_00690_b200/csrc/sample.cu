@@ -1,0 +1,1447 @@
+// Scene sampling on B200: every env samples its own layout.
+//
+//   k_seeds      per-env stream derivation          rng.py:15-26 (+ seed tree)
+//   k_zones      courtyard / strip ground planning  zones.py:44-129
+//   k_zones_blk  block layout (roads, chamfer       zones.py:132-234, blocks.py:34-118,
+//                sidewalks, quadrants, crosswalks)  gridmath.py:8-39
+//   k_terrain    tile palette + WFC collapse        terrain.py:160-259, wfc.py:24-115
+//   k_place      rejection-sampled objects          placement.py:33-132
+//   k_raster     labels + heightfield               occupancy.py:28-57, terrain.py:264-335
+//   k_footprint  object footprints -> OBSTACLE      occupancy.py:49-51
+//   k_nearest    FIFO-exact multi-source BFS        field.py:571-593
+//   k_walk       WALKABLE cell compaction           field.py:60-65
+//   k_spawn      kinds, routes, speeds              step.py:37-63, routes.py:14-87
+//
+// One CTA (or warp) owns one env; results do not depend on launch shape.
+#include <cstdio>
+#include "common.cuh"
+#include "rng.cuh"
+#include "scene_types.cuh"
+
+namespace cw {
+
+// Per-env derived stream seeds / states (scratch, filled by k_seeds).
+struct EnvSeeds {
+  Pcg64Raw zones;      // make_rng(child_seed(s,"ground"), "zones")
+  Pcg64Raw tileset;    // make_rng(child_seed(s,"terrain-stage"), "tileset")
+  Pcg64Raw objects;    // make_rng(child_seed(s,"placement"), "objects")
+  Pcg64Raw spawn;      // make_rng(crowd_seed, "crowd-spawn")
+  uint64_t wfc_seed;   // child_seed(tstage, "terrain")
+  uint64_t noise;      // child_seed(tstage, "terrain-noise")
+  uint64_t blocks;     // child_seed(s, "blocks")
+  uint64_t pad;
+};
+
+struct Rect { int r0, r1, c0, c1; };
+
+CW_DEV Rect rect_bounds(const cw_scene_params& P, double x0, double y0, double x1, double y1) {
+  // gridmath.py:59-69
+  Rect R;
+  R.c0 = (int)max(0LL, (long long)ceil(x0 / P.res - 0.5));
+  R.c1 = (int)min((long long)P.nx, (long long)ceil(x1 / P.res - 0.5));
+  R.r0 = (int)max(0LL, (long long)ceil(y0 / P.res - 0.5));
+  R.r1 = (int)min((long long)P.ny, (long long)ceil(y1 / P.res - 0.5));
+  return R;
+}
+CW_DEV bool rect_nonempty(const Rect& a) { return a.c1 > a.c0 && a.r1 > a.r0; }
+CW_DEV bool rect_has(const Rect& a, int r, int c) {
+  return r >= a.r0 && r < a.r1 && c >= a.c0 && c < a.c1;
+}
+CW_DEV bool rect_meet(const Rect& a, const Rect& b) {
+  return rect_nonempty(a) && rect_nonempty(b) && a.r0 < b.r1 && b.r0 < a.r1 && a.c0 < b.c1 &&
+         b.c0 < a.c1;
+}
+
+CW_DEV int env_slot(const int32_t* slots, int e) { return slots ? slots[e] : e; }
+
+// ----------------------------------------------------------------- block scans
+template <int NT>
+CW_DEV int block_excl_scan(int v, int* sh, int& total) {
+  // sh: >= NT/32 + 1 ints
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int s = lane < NT / 32 ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < NT / 32) sh[lane] = s;
+  }
+  __syncthreads();
+  int base = wid ? sh[wid - 1] : 0;
+  total = sh[NT / 32 - 1];
+  __syncthreads();
+  return base + x - v;
+}
+
+template <int NT>
+CW_DEV unsigned long long block_min_u64(unsigned long long v, unsigned long long* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    unsigned long long y = __shfl_xor_sync(0xffffffffu, v, o);
+    v = y < v ? y : v;
+  }
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  unsigned long long r = sh[0];
+  for (int i = 1; i < NT / 32; ++i) r = sh[i] < r ? sh[i] : r;
+  __syncthreads();
+  return r;
+}
+
+// ================================================================= k_seeds
+__global__ void k_seeds(int E, const uint64_t* __restrict__ scene_seed,
+                        const uint64_t* __restrict__ crowd_seed, EnvSeeds* __restrict__ out) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  uint64_t s = scene_seed[e];
+  EnvSeeds o;
+  pcg_store(o.zones, make_rng(child_seed(s, "ground"), "zones"));
+  uint64_t ts = child_seed(s, "terrain-stage");
+  pcg_store(o.tileset, make_rng(ts, "tileset"));
+  o.wfc_seed = child_seed(ts, "terrain");
+  o.noise = child_seed(ts, "terrain-noise");
+  pcg_store(o.objects, make_rng(child_seed(s, "placement"), "objects"));
+  pcg_store(o.spawn, make_rng(crowd_seed ? crowd_seed[e] : 0ull, "crowd-spawn"));
+  o.blocks = child_seed(s, "blocks");
+  o.pad = 0;
+  out[e] = o;
+}
+
+// ================================================================= zones
+struct Courtyard {
+  Rect walk[5];
+  int n_walk;
+  int trail;
+  Rect band;
+  Rect build[2];
+  int n_build;
+};
+
+CW_DEV void courtyard_draw(const cw_scene_params& P, Pcg64& rng, Courtyard& C) {
+  // zones.py:79-129
+  const double w = P.w, l = P.l;
+  double fx = uniform(rng, 0.30, 0.42);
+  double fy = uniform(rng, 0.30, 0.42);
+  double cx = w / 2.0, cy = l / 2.0;
+  C.walk[0] = rect_bounds(P, cx - fx * w, cy - fy * l, cx + fx * w, cy + fy * l);
+  int n_extra = 2 + (int)integers32(rng, 3);
+  for (int k = 0; k < n_extra; ++k) {
+    double ex = uniform(rng, cx - fx * w, cx + fx * w);
+    double ey = uniform(rng, cy - fy * l, cy + fy * l);
+    double hw = uniform(rng, 0.10, 0.25) * w;
+    double hl = uniform(rng, 0.10, 0.25) * l;
+    C.walk[1 + k] = rect_bounds(P, ex - hw, ey - hl, ex + hw, ey + hl);
+  }
+  C.n_walk = 1 + n_extra;
+  C.trail = next_double(rng) < 0.5;
+  if (C.trail) {
+    double tw = uniform(rng, 1.2, 2.2);
+    if (next_double(rng) < 0.5) {
+      double tx = uniform(rng, cx - 0.2 * w, cx + 0.2 * w);
+      C.band = rect_bounds(P, tx - tw / 2, 0.0, tx + tw / 2, l);
+    } else {
+      double ty = uniform(rng, cy - 0.2 * l, cy + 0.2 * l);
+      C.band = rect_bounds(P, 0.0, ty - tw / 2, w, ty + tw / 2);
+    }
+  }
+  int n_build = (int)integers32(rng, 3);
+  int order[4] = {0, 1, 2, 3};
+  for (int i = 3; i > 0; --i) {
+    int j = (int)interval32(rng, (uint32_t)i);
+    int t = order[i]; order[i] = order[j]; order[j] = t;
+  }
+  const double kx[4] = {0.0, w, 0.0, w}, ky[4] = {0.0, 0.0, l, l};
+  C.n_build = 0;
+  for (int q = 0; q < 4; ++q) {
+    if (C.n_build >= n_build) break;
+    int idx = order[q];
+    double bw = uniform(rng, 0.12, 0.22) * w;
+    double bl = uniform(rng, 0.12, 0.22) * l;
+    double x0 = kx[idx] == 0.0 ? 0.0 : w - bw;
+    double y0 = ky[idx] == 0.0 ? 0.0 : l - bl;
+    Rect m = rect_bounds(P, x0, y0, x0 + bw, y0 + bl);
+    bool meet = false;
+    for (int k = 0; k < C.n_walk; ++k) meet |= rect_meet(m, C.walk[k]);
+    if (!meet) C.build[C.n_build++] = m;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_zones(cw_scene_params P, int E, const int32_t* slots,
+                                               const EnvSeeds* __restrict__ seeds,
+                                               cw_scene_buffers B) {
+  const int e = blockIdx.x;
+  const int slot = env_slot(slots, e);
+  __shared__ Courtyard C;
+  __shared__ Rect strip;
+  __shared__ int any_walk;
+  if (threadIdx.x == 0) {
+    any_walk = 0;
+    if (P.layout == 0) {
+      Pcg64 rng = pcg_load(seeds[e].zones);
+      courtyard_draw(P, rng, C);
+    } else {
+      double b = fmin(1.0, 0.2 * fmin(P.w, P.l));  // zones.py:71-76
+      strip = rect_bounds(P, b, b, P.w - b, P.l - b);
+    }
+  }
+  __syncthreads();
+  uint8_t* Z = B.zones + (size_t)slot * P.ny * P.nx;
+  const int N = P.nx * P.ny;
+  int mine = 0;
+  for (int f = threadIdx.x; f < N; f += blockDim.x) {
+    int r = f / P.nx, c = f - r * P.nx;
+    uint8_t z = Z_VEGETATION;
+    if (P.layout == 0) {
+      bool walk = false;
+      for (int k = 0; k < C.n_walk; ++k) walk |= rect_has(C.walk[k], r, c);
+      if (walk) {
+        z = (C.trail && rect_has(C.band, r, c)) ? Z_SIDEWALK : Z_PLAZA;
+      } else {
+        for (int k = 0; k < C.n_build; ++k)
+          if (rect_has(C.build[k], r, c)) z = Z_BUILDING;
+      }
+    } else if (rect_has(strip, r, c)) {
+      z = Z_PLAZA;
+    }
+    mine |= z <= Z_PLAZA;
+    Z[f] = z;
+  }
+  mine = __syncthreads_or(mine);
+  if (threadIdx.x == 0 && !mine) B.status[slot] = CW_E_EXTENT;
+}
+
+// ---------------------------------------------------------------- block layout
+struct BlockLayout {
+  uint8_t sock[CW_MAX_BLOCKS][4];  // N, E, S, W
+  int n;
+  double sw;
+  uint8_t quad[CW_MAX_BLOCKS][4];  // zone per (qx, qy) quadrant, index qx*2+qy
+};
+
+// blocks.py:24-31 variants: kind-major, orientation-minor; sockets (N,E,S,W)
+CW_DEV void variant_sockets(int v, uint8_t s[4]) {
+  const uint8_t base[7][4] = {{1, 0, 1, 0}, {1, 1, 0, 0}, {1, 1, 1, 1}, {1, 1, 0, 1},
+                              {1, 1, 0, 1}, {1, 1, 1, 1}, {1, 1, 0, 1}};
+  int k = v >> 2, o = v & 3;
+  for (int i = 0; i < 4; ++i) s[i] = base[k][(i - o + 4) & 3];
+}
+
+CW_DEV bool blocks_connected(const BlockLayout& L, int rows, int cols) {
+  if (rows * cols == 1) return true;
+  uint64_t seen = 1, frontier = 1;
+  while (frontier) {
+    uint64_t nxt = 0;
+    for (int i = 0; i < rows * cols; ++i) {
+      if (!((frontier >> i) & 1)) continue;
+      int r = i / cols, c = i % cols;
+      if (L.sock[i][1] && c + 1 < cols) nxt |= 1ull << (i + 1);
+      if (L.sock[i][2] && r + 1 < rows) nxt |= 1ull << (i + cols);
+      if (c > 0 && L.sock[i - 1][1]) nxt |= 1ull << (i - 1);
+      if (r > 0 && L.sock[i - cols][2]) nxt |= 1ull << (i - cols);
+    }
+    frontier = nxt & ~seen;
+    seen |= nxt;
+  }
+  return __popcll(seen) == rows * cols;
+}
+
+CW_DEV void connect_blocks(uint64_t seed, int rows, int cols, BlockLayout& L) {
+  // blocks.py:34-77
+  for (int attempt = 0; attempt < 16; ++attempt) {
+    Pcg64 rng = pcg_seed(child_seed(seed, "blocks", (uint64_t)attempt));
+    for (int r = 0; r < rows; ++r)
+      for (int c = 0; c < cols; ++c) {
+        int need_n = r ? L.sock[(r - 1) * cols + c][2] : -1;
+        int need_w = c ? L.sock[r * cols + c - 1][1] : -1;
+        int opts[28], n = 0;
+        for (int v = 0; v < 28; ++v) {
+          uint8_t s[4];
+          variant_sockets(v, s);
+          if ((need_n < 0 || s[0] == need_n) && (need_w < 0 || s[3] == need_w)) opts[n++] = v;
+        }
+        int v = opts[integers32(rng, (uint64_t)n)];
+        variant_sockets(v, L.sock[r * cols + c]);
+      }
+    if (blocks_connected(L, rows, cols)) return;
+  }
+  for (int r = 0; r < rows; ++r)
+    for (int c = 0; c < cols; ++c)
+      variant_sockets((r == 0 && cols > 1) ? 5 * 4 : 0, L.sock[r * cols + c]);
+}
+
+CW_DEV bool in_road(const cw_scene_params& P, const BlockLayout& L, double ox, double oy, int r,
+                    int c, Rect* scratch = nullptr) {
+  const double bs = 20.0, rw = 6.0;
+  for (int i = 0; i < L.n; ++i) {
+    int br = i / P.bcols, bc = i % P.bcols;
+    double x0 = ox + bc * bs, y0 = oy + br * bs;
+    double cx = x0 + bs / 2.0, cy = y0 + bs / 2.0;
+    if (L.sock[i][0] && rect_has(rect_bounds(P, cx - rw / 2, y0, cx + rw / 2, cy), r, c)) return true;
+    if (L.sock[i][2] && rect_has(rect_bounds(P, cx - rw / 2, cy, cx + rw / 2, y0 + bs), r, c)) return true;
+    if (L.sock[i][3] && rect_has(rect_bounds(P, x0, cy - rw / 2, cx, cy + rw / 2), r, c)) return true;
+    if (L.sock[i][1] && rect_has(rect_bounds(P, cx, cy - rw / 2, x0 + bs, cy + rw / 2), r, c)) return true;
+  }
+  return false;
+}
+
+// CTA per env.  Chamfer distance (gridmath.py:8-39) kept in float64 scratch.
+__global__ void __launch_bounds__(512) k_zones_blk(cw_scene_params P, int E, const int32_t* slots,
+                                                   const EnvSeeds* __restrict__ seeds,
+                                                   cw_scene_buffers B) {
+  constexpr int NT = 512;
+  const int e = blockIdx.x;
+  const int slot = env_slot(slots, e);
+  const int nx = P.nx, ny = P.ny, N = nx * ny;
+  __shared__ BlockLayout L;
+  __shared__ double rowbuf[2][1024 + 1];
+  __shared__ unsigned long long shmin[NT / 32];
+  double* D = B.scratch_f64 + (size_t)e * (size_t)max(P.obj_max * 8, N);
+  uint8_t* Z = B.zones + (size_t)slot * N;
+  const double bs = 20.0, rw = 6.0;
+  const double ox = (P.w - P.bcols * bs) / 2.0, oy = (P.l - P.brows * bs) / 2.0;
+  if (threadIdx.x == 0) {
+    L.n = P.brows * P.bcols;
+    connect_blocks(seeds[e].blocks, P.brows, P.bcols, L);
+    Pcg64 rng = pcg_load(seeds[e].zones);
+    L.sw = uniform(rng, 1.5, 3.0);
+    for (int i = 0; i < L.n; ++i)
+      for (int qx = 0; qx < 2; ++qx)
+        for (int qy = 0; qy < 2; ++qy) {
+          double u = next_double(rng);
+          int k = 0;
+          while (k < 2 && !(P.quad_cdf[k] > u)) ++k;
+          const uint8_t zs[3] = {Z_BUILDING, Z_VEGETATION, Z_PLAZA};
+          L.quad[i][qx * 2 + qy] = zs[k];
+        }
+  }
+  __syncthreads();
+  // road mask -> D (0 on road, 1e9 elsewhere)
+  for (int f = threadIdx.x; f < N; f += NT) {
+    int r = f / nx, c = f - r * nx;
+    D[f] = in_road(P, L, ox, oy, r, c) ? 0.0 : 1e9;
+  }
+  __syncthreads();
+  const double s2 = kSqrt2;
+  // horizontal relax of one row in place (prefix/suffix running minima)
+  auto relax = [&](double* row) {
+    // left: min.accumulate(row - j) + j ; right: reversed analogue
+    // block-wide scan over nx <= 1024 using NT threads, two elements each
+    double* a = rowbuf[0];
+    double* b = rowbuf[1];
+    for (int j = threadIdx.x; j < nx; j += NT) {
+      a[j] = row[j] - (double)j;
+      b[j] = row[nx - 1 - j] + (double)(nx - 1 - j);
+    }
+    __syncthreads();
+    for (int o = 1; o < nx; o <<= 1) {
+      double va[2], vb[2];
+      int cnt = 0;
+      for (int j = threadIdx.x; j < nx; j += NT, ++cnt) {
+        va[cnt] = j >= o ? fmin(a[j], a[j - o]) : a[j];
+        vb[cnt] = j >= o ? fmin(b[j], b[j - o]) : b[j];
+      }
+      __syncthreads();
+      cnt = 0;
+      for (int j = threadIdx.x; j < nx; j += NT, ++cnt) {
+        a[j] = va[cnt];
+        b[j] = vb[cnt];
+      }
+      __syncthreads();
+    }
+    for (int j = threadIdx.x; j < nx; j += NT) {
+      double lft = a[j] + (double)j;
+      int jr = nx - 1 - j;  // b index of column j
+      double rgt = b[jr] - (double)j;
+      row[j] = fmin(lft, rgt);
+    }
+    __syncthreads();
+  };
+  auto pull = [&](double* dst, const double* src) {
+    for (int j = threadIdx.x; j < nx; j += NT) {
+      double dg = 1e9;
+      if (j >= 1) dg = src[j - 1] + s2;
+      if (j + 1 < nx) dg = fmin(dg, src[j + 1] + s2);
+      dst[j] = fmin(dst[j], fmin(src[j] + 1.0, dg));
+    }
+    __syncthreads();
+  };
+  for (int r = 0; r < ny; ++r) {
+    if (r) pull(D + (size_t)r * nx, D + (size_t)(r - 1) * nx);
+    relax(D + (size_t)r * nx);
+  }
+  for (int r = ny - 2; r >= 0; --r) {
+    pull(D + (size_t)r * nx, D + (size_t)(r + 1) * nx);
+    relax(D + (size_t)r * nx);
+  }
+  // compose zones
+  const double cw_len = 1.2;
+  int mine = 0;
+  for (int f = threadIdx.x; f < N; f += NT) {
+    int r = f / nx, c = f - r * nx;
+    double dist = D[f] * P.res;
+    bool road = D[f] == 0.0 && in_road(P, L, ox, oy, r, c);
+    bool side = dist > 0 && dist <= L.sw;
+    uint8_t z = Z_VEGETATION;
+    if (side) z = Z_SIDEWALK;
+    if (road) z = Z_ROADWAY;
+    if (!road && !side) {
+      for (int i = 0; i < L.n; ++i) {
+        int br = i / P.bcols, bc = i % P.bcols;
+        double x0 = ox + bc * bs, y0 = oy + br * bs;
+        for (int qx = 0; qx < 2; ++qx)
+          for (int qy = 0; qy < 2; ++qy) {
+            Rect m = rect_bounds(P, x0 + qx * bs / 2 + 1.0, y0 + qy * bs / 2 + 1.0,
+                                 x0 + (qx + 1) * bs / 2 - 1.0, y0 + (qy + 1) * bs / 2 - 1.0);
+            if (rect_has(m, r, c)) z = L.quad[i][qx * 2 + qy];
+          }
+      }
+    }
+    if (road) {
+      for (int i = 0; i < L.n; ++i) {
+        const uint8_t* s = L.sock[i];
+        if (s[0] + s[1] + s[2] + s[3] < 3) continue;
+        int br = i / P.bcols, bc = i % P.bcols;
+        double x0 = ox + bc * bs, y0 = oy + br * bs;
+        double cx = x0 + bs / 2.0, cy = y0 + bs / 2.0;
+        Rect sp[4];
+        int ax[4], n = 0;
+        if (s[0]) { sp[n] = rect_bounds(P, cx - rw / 2, y0 + 1.0, cx + rw / 2, y0 + 1.0 + cw_len); ax[n++] = 0; }
+        if (s[2]) { sp[n] = rect_bounds(P, cx - rw / 2, y0 + bs - 1.0 - cw_len, cx + rw / 2, y0 + bs - 1.0); ax[n++] = 0; }
+        if (s[3]) { sp[n] = rect_bounds(P, x0 + 1.0, cy - rw / 2, x0 + 1.0 + cw_len, cy + rw / 2); ax[n++] = 1; }
+        if (s[1]) { sp[n] = rect_bounds(P, x0 + bs - 1.0 - cw_len, cy - rw / 2, x0 + bs - 1.0, cy + rw / 2); ax[n++] = 1; }
+        for (int k = 0; k < n; ++k) {
+          if (!rect_has(sp[k], r, c)) continue;
+          bool sel = ax[k] == 0 ? ((r & 1) && r > 0 && r < ny - 1) : ((c & 1) && c > 0 && c < nx - 1);
+          if (sel) z = Z_CROSSWALK;
+        }
+      }
+    }
+    mine |= z <= Z_PLAZA;
+    Z[f] = z;
+  }
+  mine = __syncthreads_or(mine);
+  if (threadIdx.x == 0 && !mine) B.status[slot] = CW_E_EXTENT;
+  (void)shmin;
+}
+
+// ================================================================= terrain
+enum { K_FLAT = 0, K_SUP = 1, K_SDOWN = 2, K_STUP = 3, K_STDOWN = 4, K_ROUGH = 5 };
+enum { T_CORNER = 0, T_STAIR_U = 1, T_STAIR_V = 2, T_ROUGH = 3 };
+
+struct TileSet {
+  int n;
+  int8_t code[CW_MAX_TILES];
+  int8_t kind[CW_MAX_TILES];
+  double param[CW_MAX_TILES];
+  double p[CW_MAX_TILES][4];
+  double w[CW_MAX_TILES];
+  unsigned long long allowed[4][CW_MAX_TILES];  // N, E, S, W
+};
+
+CW_DEV int family_of(int kind) {
+  return kind == K_FLAT ? 0 : (kind <= K_SDOWN ? 1 : (kind <= K_STDOWN ? 2 : 3));
+}
+
+CW_DEV void ts_corner(TileSet& T, double h00, double h10, double h01, double h11, double grade) {
+  // terrain.py:216-227
+  int i = T.n++;
+  T.code[i] = T_CORNER;
+  T.p[i][0] = h00; T.p[i][1] = h10; T.p[i][2] = h01; T.p[i][3] = h11;
+  if (h00 == h10 && h10 == h01 && h01 == h11) {
+    T.kind[i] = K_FLAT;
+    T.param[i] = 0.0;
+  } else {
+    double up = (h10 + h11 - h00 - h01) + (h01 + h11 - h00 - h10);
+    T.kind[i] = up > 0 ? K_SUP : K_SDOWN;
+    T.param[i] = grade;
+  }
+}
+
+CW_DEV void sort2_unique(double* v, int& n) {
+  // sorted({a, b})
+  if (v[0] == v[1]) { n = 1; return; }
+  if (v[1] < v[0]) { double t = v[0]; v[0] = v[1]; v[1] = t; }
+  n = 2;
+}
+
+CW_DEV void build_tileset_serial(const cw_scene_params& P, Pcg64& rng, TileSet& T) {
+  // terrain.py:160-212 (palette + weights; adjacency filled in parallel)
+  const double TS = 2.0;
+  T.n = 0;
+  ts_corner(T, 0, 0, 0, 0, 0);
+  const double rs_lo = P.split ? 0.10 : 0.05, rs_hi = P.split ? 0.30 : 0.23;
+  const double sl_lo = P.split ? 0.05 : 0.00, sl_hi = P.split ? 0.80 : 0.40;
+  const double ro_lo = P.split ? 0.05 : 0.02, ro_hi = P.split ? 0.20 : 0.10;
+  if (P.mix[1] > 0) {
+    double g[2] = {uniform(rng, sl_lo, sl_hi), uniform(rng, sl_lo, sl_hi)};
+    int ng;
+    sort2_unique(g, ng);
+    for (int k = 0; k < ng; ++k) {
+      double h = g[k] * TS;
+      if (h <= 0) continue;
+      double hv[2] = {0.0, h};
+      for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b)
+          for (int c = 0; c < 2; ++c)
+            for (int d = 0; d < 2; ++d) {
+              double h00 = hv[a], h10 = hv[b], h01 = hv[c], h11 = hv[d];
+              if (h00 == 0.0 && h10 == 0.0 && h01 == 0.0 && h11 == 0.0) continue;
+              if (h00 == h11 && h10 == h01 && h00 != h10) continue;
+              ts_corner(T, h00, h10, h01, h11, g[k]);
+            }
+    }
+  }
+  if (P.mix[2] > 0) {
+    double rise = uniform(rng, rs_lo, rs_hi);
+    for (int ax = 0; ax < 2; ++ax)
+      for (int low = 1; low >= 0; --low)
+        for (int lev = 0; lev < 3; ++lev) {
+          int i = T.n++;
+          double hl = lev * rise, hh = (lev + 1) * rise;
+          T.code[i] = ax == 0 ? T_STAIR_U : T_STAIR_V;
+          T.kind[i] = low ? K_STUP : K_STDOWN;
+          T.param[i] = rise;
+          T.p[i][0] = low ? hl : hh;
+          T.p[i][1] = low ? hh : hl;
+          T.p[i][2] = 0.0;
+          T.p[i][3] = 0.0;
+        }
+    for (int lev = 1; lev <= 3; ++lev) {
+      double h = lev * rise;
+      ts_corner(T, h, h, h, h, 0.0);
+    }
+  }
+  if (P.mix[3] > 0) {
+    double a[2] = {uniform(rng, ro_lo, ro_hi), uniform(rng, ro_lo, ro_hi)};
+    int na;
+    sort2_unique(a, na);
+    for (int k = 0; k < na; ++k) {
+      int i = T.n++;
+      T.code[i] = T_ROUGH;
+      T.kind[i] = K_ROUGH;
+      T.param[i] = a[k];
+      T.p[i][0] = 0.0; T.p[i][1] = a[k]; T.p[i][2] = 0.0; T.p[i][3] = 0.0;
+    }
+  }
+  int fam_n[4] = {0, 0, 0, 0};
+  for (int i = 0; i < T.n; ++i) fam_n[family_of(T.kind[i])]++;
+  for (int i = 0; i < T.n; ++i) {
+    int f = family_of(T.kind[i]);
+    T.w[i] = P.mix[f] / (double)fam_n[f];
+  }
+}
+
+// edge profile of tile i on edge d (0 N, 1 E, 2 S, 3 W): terrain.py:248-276
+CW_DEV void edge_profile(const TileSet& T, int i, int d, int& step, double& a, double& b) {
+  const double* p = T.p[i];
+  step = 0;
+  if (T.code[i] == T_CORNER) {
+    if (d == 0) { a = p[0]; b = p[1]; }
+    else if (d == 2) { a = p[2]; b = p[3]; }
+    else if (d == 3) { a = p[0]; b = p[2]; }
+    else { a = p[1]; b = p[3]; }
+  } else if (T.code[i] == T_STAIR_U) {
+    if (d == 0 || d == 2) { step = 1; a = p[0]; b = p[1]; }
+    else if (d == 3) { a = p[0]; b = p[0]; }
+    else { a = p[1]; b = p[1]; }
+  } else if (T.code[i] == T_STAIR_V) {
+    if (d == 0) { a = p[0]; b = p[0]; }
+    else if (d == 2) { a = p[1]; b = p[1]; }
+    else { step = 1; a = p[0]; b = p[1]; }
+  } else {
+    a = 0.0; b = 0.0;
+  }
+}
+
+CW_DEV double prof_eval(int step, double a, double b, double t) {
+  if (!step) return a + (b - a) * t;
+  return t < 0.5 ? a : b;
+}
+
+CW_DEV bool tiles_compatible(const TileSet& T, int i, int j, int d) {
+  // terrain.py:283-292
+  int s1, s2;
+  double a1, b1, a2, b2;
+  edge_profile(T, i, d, s1, a1, b1);
+  edge_profile(T, j, (d + 2) & 3, s2, a2, b2);
+  const double probes[4] = {0.0, 0.499999, 0.500001, 1.0};
+  double gap = 0.0;
+  for (int k = 0; k < 4; ++k) {
+    double g = fabs(prof_eval(s1, a1, b1, probes[k]) - prof_eval(s2, a2, b2, probes[k]));
+    gap = k == 0 ? g : fmax(gap, g);
+  }
+  double tol = 1e-9;
+  if (T.kind[i] == K_STUP || T.kind[i] == K_STDOWN) tol = fmax(tol, T.param[i]);
+  if (T.kind[j] == K_STUP || T.kind[j] == K_STDOWN) tol = fmax(tol, T.param[j]);
+  return gap <= tol + 1e-12;
+}
+
+// numpy pairwise sum (n <= 44 < 128): oracle/rng.py:pairwise_sum
+CW_DEV double np_pairwise_sum(const double* a, int n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; ++i) res += a[i];
+    return res;
+  }
+  double r[8];
+  for (int k = 0; k < 8; ++k) r[k] = a[k];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+    for (int k = 0; k < 8; ++k) r[k] += a[i + k];
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < n; ++i) res += a[i];
+  return res;
+}
+
+constexpr int TER_NT = 256;
+constexpr int MAX_LAT = 1024;  // <= 32 x 32 tile lattice
+
+struct TerrainSmem {
+  TileSet T;
+  unsigned long long nib[4][11][16];  // support tables: OR of allowed[d][t] over a nibble of tiles
+  unsigned long long dom[MAX_LAT];
+  unsigned long long init[MAX_LAT];
+  unsigned long long red[TER_NT / 32];
+  int pick_cell;
+  int done;
+};
+
+CW_DEV unsigned long long support(const TerrainSmem& S, int d, unsigned long long dom) {
+  unsigned long long s = 0;
+  for (int k = 0; dom; ++k, dom >>= 4) {
+    unsigned v = (unsigned)(dom & 15ull);
+    if (v) s |= S.nib[d][k][v];
+  }
+  return s;
+}
+
+// Jacobi arc-consistency to the (unique) greatest fixpoint; false on a wipe-out.
+CW_DEV bool propagate(TerrainSmem& S, int rows, int cols) {
+  const int L = rows * cols;
+  unsigned long long nd[MAX_LAT / TER_NT];
+  while (true) {
+    int changed = 0, empty = 0;
+    int k = 0;
+    for (int x = threadIdx.x; x < L; x += TER_NT, ++k) {
+      int r = x / cols, c = x - r * cols;
+      unsigned long long d = S.dom[x];
+      if (r > 0) d &= support(S, 2, S.dom[x - cols]);      // north nbr: we are S of it
+      if (r + 1 < rows) d &= support(S, 0, S.dom[x + cols]);
+      if (c > 0) d &= support(S, 1, S.dom[x - 1]);          // west nbr: we are E of it
+      if (c + 1 < cols) d &= support(S, 3, S.dom[x + 1]);
+      nd[k] = d;
+    }
+    __syncthreads();
+    k = 0;
+    for (int x = threadIdx.x; x < L; x += TER_NT, ++k) {
+      changed |= nd[k] != S.dom[x];
+      empty |= nd[k] == 0ull;
+      S.dom[x] = nd[k];
+    }
+    int any_empty = __syncthreads_or(empty);
+    if (any_empty) return false;
+    int any_changed = __syncthreads_or(changed);
+    if (!any_changed) return true;
+  }
+}
+
+__global__ void __launch_bounds__(TER_NT) k_terrain(cw_scene_params P, int E, const int32_t* slots,
+                                                    const EnvSeeds* __restrict__ seeds,
+                                                    cw_scene_buffers B) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TerrainSmem& S = *reinterpret_cast<TerrainSmem*>(smem_raw);
+  const int e = blockIdx.x;
+  const int slot = env_slot(slots, e);
+  const int rows = P.trows, cols = P.tcols, L = rows * cols;
+  if (B.status[slot] != CW_OK) return;
+  if (threadIdx.x == 0) {
+    Pcg64 rng = pcg_load(seeds[e].tileset);
+    build_tileset_serial(P, rng, S.T);
+  }
+  for (int i = threadIdx.x; i < 4 * CW_MAX_TILES; i += TER_NT) (&S.T.allowed[0][0])[i] = 0ull;
+  __syncthreads();
+  const int n = S.T.n;
+  for (int q = threadIdx.x; q < n * n; q += TER_NT) {
+    int i = q / n, j = q - i * n;
+    if (tiles_compatible(S.T, i, j, 1)) {  // E, and W = E^T
+      atomicOr(&S.T.allowed[1][i], 1ull << j);
+      atomicOr(&S.T.allowed[3][j], 1ull << i);
+    }
+    if (tiles_compatible(S.T, i, j, 2)) {  // S, and N = S^T
+      atomicOr(&S.T.allowed[2][i], 1ull << j);
+      atomicOr(&S.T.allowed[0][j], 1ull << i);
+    }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < 4 * 11 * 16; q += TER_NT) {
+    int d = q / 176, k = (q / 16) % 11, v = q & 15;
+    unsigned long long s = 0;
+    for (int b = 0; b < 4; ++b) {
+      int t = 4 * k + b;
+      if (((v >> b) & 1) && t < n) s |= S.T.allowed[d][t];
+    }
+    S.nib[d][k][v] = s;
+  }
+  // forced-flat cells outside the walkable area (terrain.py:236-250)
+  const uint8_t* Z = B.zones + (size_t)slot * P.nx * P.ny;
+  const unsigned long long full = n == 64 ? ~0ull : ((1ull << n) - 1ull);
+  for (int x = threadIdx.x; x < L; x += TER_NT) {
+    int r = x / cols, c = x - r * cols;
+    int r0 = r * P.cpt, c0 = c * P.cpt;
+    bool inside = (r0 + P.cpt <= P.ny) && (c0 + P.cpt <= P.nx);
+    for (int rr = r0; inside && rr < r0 + P.cpt; ++rr)
+      for (int cc = c0; cc < c0 + P.cpt; ++cc) {
+        uint8_t z = Z[(size_t)rr * P.nx + cc];
+        bool wk = z <= Z_PLAZA && (P.nonflat_split_col < 0 || cc >= P.nonflat_split_col);
+        if (!wk) { inside = false; break; }
+      }
+    S.init[x] = inside ? full : 1ull;
+  }
+  __syncthreads();
+  int attempt_ok = -1;
+  for (int attempt = 0; attempt < 16 && attempt_ok < 0; ++attempt) {
+    for (int x = threadIdx.x; x < L; x += TER_NT) S.dom[x] = S.init[x];
+    __syncthreads();
+    Pcg64 rng;
+    if (threadIdx.x == 0) rng = pcg_seed(child_seed(seeds[e].wfc_seed, "wfc", (uint64_t)attempt));
+    bool ok = propagate(S, rows, cols);
+    while (ok) {
+      // minimum-entropy open cell, ties by lowest flat index (wfc.py:61-70)
+      unsigned long long best = ~0ull;
+      for (int x = threadIdx.x; x < L; x += TER_NT) {
+        int cnt = __popcll(S.dom[x]);
+        if (cnt > 1) {
+          unsigned long long key = ((unsigned long long)cnt << 32) | (unsigned)x;
+          best = key < best ? key : best;
+        }
+      }
+      best = block_min_u64<TER_NT>(best, S.red);
+      if (best == ~0ull) break;  // fully collapsed
+      if (threadIdx.x == 0) {
+        int x = (int)(best & 0xffffffffu);
+        unsigned long long d = S.dom[x];
+        int opts[CW_MAX_TILES];
+        double w[CW_MAX_TILES];
+        int no = 0;
+        for (int t = 0; t < n; ++t)
+          if ((d >> t) & 1ull) { opts[no] = t; w[no] = S.T.w[t]; ++no; }
+        double tot = np_pairwise_sum(w, no);
+        if (tot <= 0) {
+          for (int k = 0; k < no; ++k) w[k] = 1.0;
+          tot = (double)no;
+        }
+        // Generator.choice(no, p=w/tot): cdf = cumsum(p); cdf /= cdf[-1]; searchsorted right
+        double cdf[CW_MAX_TILES];
+        double acc = 0.0;
+        for (int k = 0; k < no; ++k) {
+          double pk = w[k] / tot;
+          acc = k ? acc + pk : pk;
+          cdf[k] = acc;
+        }
+        double last = cdf[no - 1];
+        double u = next_double(rng);
+        int idx = 0;
+        while (idx < no && !(cdf[idx] / last > u)) ++idx;
+        S.dom[x] = 1ull << opts[idx];
+      }
+      __syncthreads();
+      ok = propagate(S, rows, cols);
+    }
+    if (ok) attempt_ok = attempt;
+    __syncthreads();
+  }
+  int32_t* A = B.assign + (size_t)slot * L;
+  if (attempt_ok < 0) {
+    if (threadIdx.x == 0) B.status[slot] = CW_E_CONTRADICTION;
+    return;
+  }
+  for (int x = threadIdx.x; x < L; x += TER_NT) A[x] = __ffsll((long long)S.dom[x]) - 1;
+  if (threadIdx.x == 0) {
+    B.wfc_attempts[slot] = attempt_ok;
+    B.n_tiles[slot] = n;
+    B.noise_seed[slot] = seeds[e].noise;
+  }
+  for (int i = threadIdx.x; i < CW_MAX_TILES; i += TER_NT) {
+    size_t o = (size_t)slot * CW_MAX_TILES + i;
+    bool v = i < n;
+    B.tile_code[o] = v ? S.T.code[i] : -1;
+    B.tile_kind[o] = v ? S.T.kind[i] : -1;
+    B.tile_param[o] = v ? S.T.param[i] : 0.0;
+    B.tile_w[o] = v ? S.T.w[i] : 0.0;
+    for (int k = 0; k < 4; ++k) B.tile_p[o * 4 + k] = v ? S.T.p[i][k] : 0.0;
+    for (int d = 0; d < 4; ++d)
+      B.allowed[((size_t)slot * 4 + d) * CW_MAX_TILES + i] = v ? S.T.allowed[d][i] : 0ull;
+  }
+}
+
+// ================================================================= placement
+// Corners of an oriented footprint: types.py:355-361; the (4,2)@(2,2) product is
+// OpenBLAS dgemm = fma(l1, r1, l0*r0) with rot rows (c, -s), (s, c).
+CW_DEV void footprint_corners(double fw, double fl, double x, double y, double c, double s,
+                              double* cx, double* cy) {
+  const double hw = fw / 2.0, hl = fl / 2.0;
+  const double lx[4] = {-hw, hw, hw, -hw}, ly[4] = {-hl, -hl, hl, hl};
+  for (int i = 0; i < 4; ++i) {
+    cx[i] = __fma_rn(ly[i], -s, lx[i] * c) + x;
+    cy[i] = __fma_rn(ly[i], c, lx[i] * s) + y;
+  }
+}
+
+struct FootBox { int r0, r1, c0, c1; bool empty; };
+
+CW_DEV FootBox footprint_box(const cw_scene_params& P, const double* cx, const double* cy) {
+  // placement.py:36-44
+  double x0 = cx[0], x1 = cx[0], y0 = cy[0], y1 = cy[0];
+  for (int i = 1; i < 4; ++i) {
+    x0 = fmin(x0, cx[i]); x1 = fmax(x1, cx[i]);
+    y0 = fmin(y0, cy[i]); y1 = fmax(y1, cy[i]);
+  }
+  FootBox b;
+  b.c0 = (int)max(0LL, trunc_ll(x0 / P.res) - 1);
+  b.c1 = (int)min((long long)P.nx - 1, trunc_ll(x1 / P.res) + 1);
+  b.r0 = (int)max(0LL, trunc_ll(y0 / P.res) - 1);
+  b.r1 = (int)min((long long)P.ny - 1, trunc_ll(y1 / P.res) + 1);
+  b.empty = b.c1 < b.c0 || b.r1 < b.r0;
+  return b;
+}
+
+CW_DEV bool cell_inside(const cw_scene_params& P, int r, int c, double x, double y, double cs,
+                        double sn, double fw, double fl) {
+  // placement.py:45-51
+  double px = ((double)c + 0.5) * P.res - x;
+  double py = ((double)r + 0.5) * P.res - y;
+  double lx = cs * px + sn * py;
+  double ly = -sn * px + cs * py;
+  return fabs(lx) <= fw / 2.0 && fabs(ly) <= fl / 2.0;
+}
+
+// SAT overlap (placement.py:62-78); corners @ axis is OpenBLAS dgemv = fma(c0, a0, c1*a1).
+CW_DEV bool sat_overlap(const double* ax_, const double* ay_, const double* bx_, const double* by_) {
+  for (int rect = 0; rect < 2; ++rect) {
+    const double* rx = rect ? bx_ : ax_;
+    const double* ry = rect ? by_ : ay_;
+    for (int i = 0; i < 2; ++i) {
+      double ex = rx[i + 1] - rx[i], ey = ry[i + 1] - ry[i];
+      double axx = -ey, axy = ex;
+      double pamin = 0, pamax = 0, pbmin = 0, pbmax = 0;
+      for (int k = 0; k < 4; ++k) {
+        double pa = __fma_rn(ax_[k], axx, ay_[k] * axy);
+        double pb = __fma_rn(bx_[k], axx, by_[k] * axy);
+        pamin = k ? fmin(pamin, pa) : pa; pamax = k ? fmax(pamax, pa) : pa;
+        pbmin = k ? fmin(pbmin, pb) : pb; pbmax = k ? fmax(pbmax, pb) : pb;
+      }
+      if (pamax < pbmin || pbmax < pamin) return false;
+    }
+  }
+  return true;
+}
+
+CW_DEV bool region_ok(const cw_scene_params& P, uint8_t zone, int c) {
+  if (P.region == 1) return zone <= Z_PLAZA;
+  if (P.region == 2) {
+    for (int i = 1; i <= 5; ++i) {
+      if (i == 3) continue;
+      int c0 = (int)((long long)P.nx * i / 6), c1 = (int)((long long)P.nx * (i + 1) / 6);
+      if (c >= c0 && c < c1) return true;
+    }
+    return false;
+  }
+  return true;
+}
+
+// warp per env
+__global__ void __launch_bounds__(128) k_place(cw_scene_params P, int E, const int32_t* slots,
+                                               const EnvSeeds* __restrict__ seeds,
+                                               cw_scene_buffers B) {
+  const int lane = threadIdx.x & 31;
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (e >= E) return;
+  const int slot = env_slot(slots, e);
+  if (B.status[slot] != CW_OK) return;
+  const size_t N = (size_t)P.nx * P.ny;
+  const uint8_t* Z = B.zones + slot * N;
+  const int32_t* A = B.assign + (size_t)slot * P.trows * P.tcols;
+  const int8_t* TK = B.tile_kind + (size_t)slot * CW_MAX_TILES;
+  double* cache = B.scratch_f64 + (size_t)e * (size_t)max(P.obj_max * 8, (int)N);  // corners
+  int32_t* ocat = B.obj_cat + (size_t)slot * P.obj_max;
+  double* opose = B.obj_pose + (size_t)slot * P.obj_max * 3;
+  Pcg64 rng;
+  if (lane == 0) rng = pcg_load(seeds[e].objects);
+  int placed = 0;
+  bool overflow = false;
+  const int count = P.obj_count;
+  for (int obj = 0; obj < count && !overflow; ++obj) {
+    bool ok = false;
+    for (int att = 0; att < P.attempts && !ok; ++att) {
+      int k = 0;
+      double x = 0, y = 0, yaw = 0;
+      if (lane == 0) {
+        if (att < P.attempts / 2) k = (int)integers32(rng, (uint64_t)P.n_cat);
+        else k = P.small_first[integers32(rng, (uint64_t)min(5, P.n_cat))];
+        x = uniform(rng, 0.0, P.nx * P.res);
+        y = uniform(rng, 0.0, P.ny * P.res);
+        yaw = uniform(rng, 0.0, kTwoPi);
+      }
+      k = __shfl_sync(0xffffffffu, k, 0);
+      x = __shfl_sync(0xffffffffu, x, 0);
+      y = __shfl_sync(0xffffffffu, y, 0);
+      yaw = __shfl_sync(0xffffffffu, yaw, 0);
+      const double fw = P.cat_w[k], fl = P.cat_l[k];
+      double cs, sn;
+      sincos(yaw, &sn, &cs);
+      double cx[4], cy[4];
+      footprint_corners(fw, fl, x, y, cs, sn, cx, cy);
+      FootBox bb = footprint_box(P, cx, cy);
+      if (bb.empty) continue;
+      const int bw = bb.c1 - bb.c0 + 1, nb = bw * (bb.r1 - bb.r0 + 1);
+      bool bad = false, any = false;
+      for (int q = lane; q < nb; q += 32) {
+        int r = bb.r0 + q / bw, c = bb.c0 + q % bw;
+        if (!cell_inside(P, r, c, x, y, cs, sn, fw, fl)) continue;
+        any = true;
+        uint8_t z = Z[(size_t)r * P.nx + c];
+        if (!((P.cat_zones[k] >> z) & 1u) || !region_ok(P, z, c)) bad = true;
+      }
+      any = __any_sync(0xffffffffu, any);
+      bad = __any_sync(0xffffffffu, bad);
+      if (!any) {
+        // degenerate small footprint: the centre cell (placement.py:54-58)
+        long long rc = trunc_ll(y / P.res), cc = trunc_ll(x / P.res);
+        if (!(rc >= 0 && rc < P.ny && cc >= 0 && cc < P.nx)) continue;
+        uint8_t z = Z[(size_t)rc * P.nx + cc];
+        if (!((P.cat_zones[k] >> z) & 1u) || !region_ok(P, z, (int)cc)) continue;
+      } else if (bad) {
+        continue;
+      }
+      {  // stair tile under the pose (placement.py:120-124)
+        int tr = min(P.trows - 1, (int)trunc_ll(y / 2.0));
+        int tc = min(P.tcols - 1, (int)trunc_ll(x / 2.0));
+        int kind = TK[A[tr * P.tcols + tc]];
+        if (kind == K_STUP || kind == K_STDOWN) continue;
+      }
+      bool hit = false;
+      const double reach = P.cat_reach[k];
+      for (int j = lane; j < placed; j += 32) {
+        const double* o = cache + (size_t)j * 8;
+        double ox = opose[j * 3 + 0], oy = opose[j * 3 + 1];
+        double rr = reach + P.cat_reach[ocat[j]];
+        double dx = x - ox, dy = y - oy;
+        if (dx * dx + dy * dy > rr * rr) continue;
+        if (sat_overlap(cx, cy, o, o + 4)) hit = true;
+      }
+      if (__any_sync(0xffffffffu, hit)) continue;
+      if (lane == 0) {
+        ocat[placed] = k;
+        opose[placed * 3 + 0] = x;
+        opose[placed * 3 + 1] = y;
+        opose[placed * 3 + 2] = yaw;
+        double* o = cache + (size_t)placed * 8;
+        for (int i = 0; i < 4; ++i) { o[i] = cx[i]; o[4 + i] = cy[i]; }
+      }
+      __syncwarp();
+      ++placed;
+      ok = true;
+    }
+    if (!ok) overflow = true;
+  }
+  if (lane == 0) {
+    B.obj_n[slot] = placed;
+    B.overflow[slot] = overflow;
+  }
+}
+
+// ================================================================= raster
+CW_DEV double hash_noise(long long ix, long long iy, uint64_t seed) {
+  // terrain.py:264-272
+  uint64_t h = ((uint64_t)ix * 0x9E3779B97F4A7C15ull) ^ ((uint64_t)iy * 0xC2B2AE3D27D4EB4Full) ^ seed;
+  h ^= h >> 33;
+  h *= 0xFF51AFD7ED558CCDull;
+  h ^= h >> 33;
+  return (double)(h >> 11) / 9007199254740992.0 * 2.0 - 1.0;
+}
+
+CW_DEV double elevation_at(double x, double y, int rows, int cols, const int32_t* A,
+                           const int8_t* code, const double* tp, uint64_t noise) {
+  // terrain.py:294-335
+  const double T = 2.0;
+  long long tc = clampll(trunc_ll(x / T), 0, cols - 1);
+  long long tr = clampll(trunc_ll(y / T), 0, rows - 1);
+  double u = fmin(fmax(x / T - (double)tc, 0.0), 1.0);
+  double v = fmin(fmax(y / T - (double)tr, 0.0), 1.0);
+  int id = A[tr * cols + tc];
+  const double* p = tp + id * 4;
+  int cd = code[id];
+  double e = (1 - u) * (1 - v) * p[0] + u * (1 - v) * p[1] + (1 - u) * v * p[2] + u * v * p[3];
+  if (cd == T_STAIR_U) e = u < 0.5 ? p[0] : p[1];
+  else if (cd == T_STAIR_V) e = v < 0.5 ? p[0] : p[1];
+  else if (cd == T_ROUGH) {
+    double taper = fmin(fmax(fmin(u, 1.0 - u) / 0.125, 0.0), 1.0) *
+                   fmin(fmax(fmin(v, 1.0 - v) / 0.125, 0.0), 1.0);
+    double gx = x / 0.5, gy = y / 0.5;
+    long long ix = (long long)floor(gx), iy = (long long)floor(gy);
+    double fx = gx - (double)ix, fy = gy - (double)iy;
+    double sx = fx * fx * (3.0 - 2.0 * fx);
+    double sy = fy * fy * (3.0 - 2.0 * fy);
+    double n00 = hash_noise(ix, iy, noise), n10 = hash_noise(ix + 1, iy, noise);
+    double n01 = hash_noise(ix, iy + 1, noise), n11 = hash_noise(ix + 1, iy + 1, noise);
+    double top = n00 + (n10 - n00) * sx;
+    double bot = n01 + (n11 - n01) * sx;
+    double bump = top + (bot - top) * sy;
+    e = p[0] + p[1] * taper * bump;
+  }
+  return e;
+}
+
+// 4 cells per thread: uchar4 label stores + float4 elevation stores (nx % 4 == 0).
+__global__ void __launch_bounds__(256) k_raster(cw_scene_params P, int E, const int32_t* slots,
+                                                cw_scene_buffers B) {
+  const int e = blockIdx.y;
+  const int slot = env_slot(slots, e);
+  if (B.status[slot] != CW_OK) return;
+  const size_t N = (size_t)P.nx * P.ny;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;  // quad index
+  if ((size_t)q * 4 >= N) return;
+  __shared__ int8_t code[CW_MAX_TILES];
+  __shared__ double tp[CW_MAX_TILES * 4];
+  // (tables are tiny; every thread block reloads them)
+  const int f0 = q * 4;
+  const int r = f0 / P.nx, c0 = f0 - r * P.nx;
+  const uint8_t* Z = B.zones + slot * N;
+  uchar4 zz = *reinterpret_cast<const uchar4*>(Z + f0);
+  // zone lookup at the same resolution: rr = min((r+0.5)*res/zone_res, zy-1) == r
+  uchar4 lb = make_uchar4(zone_to_label(zz.x), zone_to_label(zz.y), zone_to_label(zz.z),
+                          zone_to_label(zz.w));
+  *reinterpret_cast<uchar4*>(B.labels + slot * N + f0) = lb;
+  const int32_t* A = B.assign + (size_t)slot * P.trows * P.tcols;
+  const int8_t* cd = B.tile_code + (size_t)slot * CW_MAX_TILES;
+  const double* p = B.tile_p + (size_t)slot * CW_MAX_TILES * 4;
+  const uint64_t noise = B.noise_seed[slot];
+  const double y = ((double)r + 0.5) * P.res;
+  float ev[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    double x = ((double)(c0 + k) + 0.5) * P.res;
+    ev[k] = (float)elevation_at(x, y, P.trows, P.tcols, A, cd, p, noise);
+  }
+  *reinterpret_cast<float4*>(B.elev + slot * N + f0) = make_float4(ev[0], ev[1], ev[2], ev[3]);
+  (void)code; (void)tp;
+}
+
+// warp per (env, object): footprint cells -> OBSTACLE (occupancy.py:49-51)
+__global__ void __launch_bounds__(128) k_footprint(cw_scene_params P, int E, const int32_t* slots,
+                                                   cw_scene_buffers B) {
+  const int lane = threadIdx.x & 31;
+  const int e = blockIdx.y;
+  const int slot = env_slot(slots, e);
+  if (B.status[slot] != CW_OK) return;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= B.obj_n[slot]) return;
+  const size_t N = (size_t)P.nx * P.ny;
+  uint8_t* Lb = B.labels + slot * N;
+  const int k = B.obj_cat[(size_t)slot * P.obj_max + j];
+  const double* pose = B.obj_pose + ((size_t)slot * P.obj_max + j) * 3;
+  const double x = pose[0], y = pose[1], yaw = pose[2];
+  const double fw = P.cat_w[k], fl = P.cat_l[k];
+  double cs, sn;
+  sincos(yaw, &sn, &cs);
+  double cx[4], cy[4];
+  footprint_corners(fw, fl, x, y, cs, sn, cx, cy);
+  FootBox bb = footprint_box(P, cx, cy);
+  if (bb.empty) return;
+  const int bw = bb.c1 - bb.c0 + 1, nb = bw * (bb.r1 - bb.r0 + 1);
+  bool any = false;
+  for (int q = lane; q < nb; q += 32) {
+    int r = bb.r0 + q / bw, c = bb.c0 + q % bw;
+    if (cell_inside(P, r, c, x, y, cs, sn, fw, fl)) {
+      any = true;
+      Lb[(size_t)r * P.nx + c] = L_OBSTACLE;
+    }
+  }
+  any = __any_sync(0xffffffffu, any);
+  if (!any && lane == 0) {
+    long long rc = trunc_ll(y / P.res), cc = trunc_ll(x / P.res);
+    if (rc >= 0 && rc < P.ny && cc >= 0 && cc < P.nx) Lb[rc * P.nx + cc] = L_OBSTACLE;
+  }
+}
+
+// ================================================================= nearest obstacle (BFS)
+constexpr int BFS_NT = 1024;
+
+// Level-synchronous BFS that reproduces the FIFO deque of field.py:579-592:
+// a level-(k+1) cell belongs to the earliest-ranked level-k parent that
+// reaches it, and the next level is ordered by (parent rank, direction).
+__global__ void __launch_bounds__(BFS_NT) k_nearest(cw_scene_params P, int E, const int32_t* slots,
+                                                    cw_scene_buffers B) {
+  const int e = blockIdx.x;
+  const int slot = env_slot(slots, e);
+  if (B.status[slot] != CW_OK) return;
+  const int nx = P.nx, ny = P.ny, N = nx * ny;
+  const uint8_t* Lb = B.labels + (size_t)slot * N;
+  int32_t* near = B.nearest + (size_t)slot * N;
+  int32_t* owner = B.scratch_i32 + (size_t)e * 3 * N;
+  int32_t* Q = owner + N;
+  __shared__ int sh[BFS_NT / 32 + 1];
+  const int UNSEEN = 0x7fffffff;
+  // seed: obstacles in row-major order
+  int base = 0;
+  for (int f0 = 0; f0 < N; f0 += BFS_NT) {
+    int f = f0 + threadIdx.x;
+    int ob = f < N && Lb[f] == L_OBSTACLE;
+    if (f < N) {
+      owner[f] = ob ? -1 : UNSEEN;
+      near[f] = ob ? f : -1;
+    }
+    int tot;
+    int off = block_excl_scan<BFS_NT>(ob, sh, tot);
+    if (ob) Q[base + off] = f;
+    base += tot;
+  }
+  if (threadIdx.x == 0) B.has_obs[slot] = base > 0;
+  __syncthreads();
+  const int dr[8] = {1, -1, 0, 0, 1, 1, -1, -1};
+  const int dc[8] = {0, 0, 1, -1, 1, -1, 1, -1};
+  int lo = 0, hi = base;
+  while (lo < hi) {
+    for (int q = lo + threadIdx.x; q < hi; q += BFS_NT) {
+      int p = Q[q], r = p / nx, c = p - r * nx;
+      int key0 = (q - lo) * 8;
+      for (int d = 0; d < 8; ++d) {
+        int rr = r + dr[d], cc = c + dc[d];
+        if (rr < 0 || rr >= ny || cc < 0 || cc >= nx) continue;
+        int x = rr * nx + cc;
+        if (owner[x] >= 0) atomicMin(&owner[x], key0 + d);
+      }
+    }
+    __syncthreads();
+    int out = hi;
+    for (int q0 = lo; q0 < hi; q0 += BFS_NT) {
+      int q = q0 + threadIdx.x;
+      unsigned win = 0;
+      int p = 0, r = 0, c = 0;
+      if (q < hi) {
+        p = Q[q]; r = p / nx; c = p - r * nx;
+        int key0 = (q - lo) * 8;
+        for (int d = 0; d < 8; ++d) {
+          int rr = r + dr[d], cc = c + dc[d];
+          if (rr < 0 || rr >= ny || cc < 0 || cc >= nx) continue;
+          if (owner[rr * nx + cc] == key0 + d) win |= 1u << d;
+        }
+      }
+      int tot;
+      int off = block_excl_scan<BFS_NT>(__popc(win), sh, tot);
+      if (win) {
+        int src = near[p];
+        int k = 0;
+        for (int d = 0; d < 8; ++d) {
+          if (!((win >> d) & 1u)) continue;
+          int x = (r + dr[d]) * nx + (c + dc[d]);
+          Q[out + off + k++] = x;
+          near[x] = src;
+          owner[x] = -1;
+        }
+      }
+      out += tot;
+    }
+    __syncthreads();
+    lo = hi;
+    hi = out;
+  }
+}
+
+// ================================================================= walkable list
+__global__ void __launch_bounds__(1024) k_walk(cw_scene_params P, int E, const int32_t* slots,
+                                               cw_scene_buffers B) {
+  const int e = blockIdx.x;
+  const int slot = env_slot(slots, e);
+  if (B.status[slot] != CW_OK) return;
+  const int N = P.nx * P.ny;
+  const uint8_t* Lb = B.labels + (size_t)slot * N;
+  int32_t* W = B.walk + (size_t)slot * N;
+  __shared__ int sh[1024 / 32 + 1];
+  int base = 0;
+  for (int f0 = 0; f0 < N; f0 += 1024) {
+    int f = f0 + threadIdx.x;
+    int wk = f < N && Lb[f] == L_WALKABLE;
+    int tot;
+    int off = block_excl_scan<1024>(wk, sh, tot);
+    if (wk) W[base + off] = f;
+    base += tot;
+  }
+  if (threadIdx.x == 0) B.walk_n[slot] = base;
+}
+
+// ================================================================= spawn + routes
+constexpr int SP_NT = 1024;
+__device__ __constant__ double kMaxSpeed[3] = {2.0, 5.0, 4.0};     // crowd/types.py:15-19
+__device__ __constant__ double kPrefLo[3] = {0.8, 2.0, 1.5};       // types.py:22-26
+__device__ __constant__ double kPrefHi[3] = {1.4, 4.0, 3.0};
+__device__ __constant__ double kRadius[3] = {0.3, 0.45, 0.4};      // types.py:28-32
+
+CW_DEV bool spawn_region_ok(const cw_scene_params& P, int c) {
+  if (P.spawn_region != 1) return true;
+  for (int i = 2; i <= 5; i += 3) {
+    int c0 = (int)((long long)P.nx * i / 6), c1 = (int)((long long)P.nx * (i + 1) / 6);
+    if (c >= c0 && c < c1) return true;
+  }
+  return false;
+}
+
+__global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const int32_t* slots,
+                                                 const EnvSeeds* __restrict__ seeds,
+                                                 cw_scene_buffers B) {
+  const int e = blockIdx.x;
+  const int slot = env_slot(slots, e);
+  const int A = P.peds;
+  if (A == 0 || B.status[slot] != CW_OK) return;
+  const int nx = P.nx, ny = P.ny, N = nx * ny;
+  const uint8_t* Lb = B.labels + (size_t)slot * N;
+  int32_t* comp = B.scratch_i32 + (size_t)e * 3 * N;
+  int32_t* cand = comp + N;       // candidate flat indices (row-major)
+  int32_t* perm = cand + N;
+  __shared__ int sh[SP_NT / 32 + 1];
+  __shared__ int s_n, s_changed, s_idx, s_cnt, s_rank, s_j, s_acc, s_k, s_fail;
+  __shared__ unsigned long long s_seed;
+  __shared__ double s_maxr;
+  extern __shared__ __align__(16) unsigned char sp_smem[];
+  double* stx = reinterpret_cast<double*>(sp_smem);  // accepted starts (A)
+  double* sty = stx + A;
+  int8_t* kind_out = B.sp_kind + (size_t)slot * A;
+  double* pref_out = B.sp_pref + (size_t)slot * A;
+  if (threadIdx.x == 0) {
+    // step.py:41-61 (the spawn stream is independent of the routes stream)
+    Pcg64 rng = pcg_load(seeds[e].spawn);
+    double maxr = 0.0;
+    for (int a = 0; a < A; ++a) {
+      double u = next_double(rng);
+      int k = u < 0.7 ? 0 : (u < 0.9 ? 1 : 2);
+      kind_out[a] = (int8_t)k;
+      maxr = a ? fmax(maxr, kRadius[k]) : kRadius[k];
+    }
+    s_seed = integers_2p63(rng);
+    for (int a = 0; a < A; ++a) {
+      int k = kind_out[a];
+      pref_out[a] = uniform(rng, kPrefLo[k], kPrefHi[k]);
+    }
+    s_maxr = maxr;
+  }
+  // candidates: WALKABLE (& region) cells, row-major (routes.py:46-56)
+  int base = 0;
+  for (int f0 = 0; f0 < N; f0 += SP_NT) {
+    int f = f0 + threadIdx.x;
+    int ok = f < N && Lb[f] == L_WALKABLE && spawn_region_ok(P, f % nx);
+    if (f < N) comp[f] = ok ? f : -1;
+    int tot;
+    int off = block_excl_scan<SP_NT>(ok, sh, tot);
+    if (ok) cand[base + off] = f;
+    base += tot;
+  }
+  if (threadIdx.x == 0) s_n = base;
+  __syncthreads();
+  const int n = s_n;
+  if (n < A) {
+    if (threadIdx.x == 0) B.status[slot] = CW_E_NOROUTE;
+    return;
+  }
+  // 8-connected components: min-label propagation + pointer jumping.  Only
+  // label equality is used downstream (routes.py:62, 74), so any labelling works.
+  while (true) {
+    if (threadIdx.x == 0) s_changed = 0;
+    __syncthreads();
+    int ch = 0;
+    for (int q = threadIdx.x; q < n; q += SP_NT) {
+      int f = cand[q], r = f / nx, c = f - r * nx;
+      int m = comp[f];
+      for (int dr = -1; dr <= 1; ++dr)
+        for (int dc = -1; dc <= 1; ++dc) {
+          int rr = r + dr, cc = c + dc;
+          if ((dr || dc) && rr >= 0 && rr < ny && cc >= 0 && cc < nx) {
+            int o = comp[rr * nx + cc];
+            if (o >= 0 && o < m) m = o;
+          }
+        }
+      if (m < comp[f]) {
+        atomicMin(&comp[f], m);
+        ch = 1;
+      }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < n; q += SP_NT) {
+      int f = cand[q];
+      int c = comp[f];
+      while (comp[c] < c) c = comp[c];
+      if (c < comp[f]) atomicMin(&comp[f], c);
+    }
+    if (__syncthreads_or(ch) == 0) break;
+  }
+  // permutation(n): Fisher-Yates from the top with masked rejection (numpy shuffle)
+  if (threadIdx.x == 0) {
+    Pcg64 rr = pcg_seed(s_seed);
+    for (int i = 0; i < n; ++i) perm[i] = i;
+    for (int i = n - 1; i > 0; --i) {
+      int j = (int)interval32(rr, (uint32_t)i);
+      int t = perm[i]; perm[i] = perm[j]; perm[j] = t;
+    }
+    s_acc = 0;
+    s_k = 0;
+    // stash the routes stream right after the shuffle in shared memory
+    Pcg64Raw* raw = reinterpret_cast<Pcg64Raw*>(sty + A);
+    pcg_store(*raw, rr);
+  }
+  __syncthreads();
+  Pcg64Raw* rraw = reinterpret_cast<Pcg64Raw*>(sty + A);
+  const double res = P.res;
+  const double sep = 2.0 * s_maxr;
+  const double sep2 = sep * sep;
+  double* out_pos = B.sp_pos + (size_t)slot * A * 2;
+  double* out_goal = B.sp_goal + (size_t)slot * A * 2;
+  while (true) {
+    __syncthreads();
+    if (s_acc >= A || s_k >= n) break;
+    if (threadIdx.x == 0) {
+      s_idx = perm[s_k];
+      s_k += 1;
+      s_fail = 0;
+    }
+    __syncthreads();
+    const int fs = cand[s_idx];
+    const double sx = ((double)(fs % nx) + 0.5) * res, sy = ((double)(fs / nx) + 0.5) * res;
+    int close = 0;
+    for (int a = threadIdx.x; a < s_acc; a += SP_NT) {
+      double dx = sx - stx[a], dy = sy - sty[a];
+      if (dx * dx + dy * dy < sep2) close = 1;
+    }
+    if (__syncthreads_or(close)) continue;
+    const int cs = comp[fs];
+    int cnt = 0;
+    for (int q = threadIdx.x; q < n; q += SP_NT) {
+      int f = cand[q];
+      if (comp[f] != cs) continue;
+      double dx = ((double)(f % nx) + 0.5) * res - sx, dy = ((double)(f / nx) + 0.5) * res - sy;
+      cnt += dx * dx + dy * dy >= sep2;
+    }
+    int tot;
+    block_excl_scan<SP_NT>(cnt, sh, tot);
+    if (tot == 0) continue;
+    if (threadIdx.x == 0) {
+      Pcg64 rr = pcg_load(*rraw);
+      s_rank = (int)integers32(rr, (uint64_t)tot);
+      pcg_store(*rraw, rr);
+      s_j = -1;
+    }
+    __syncthreads();
+    // locate the s_rank-th matching candidate in row-major order
+    int seen = 0;
+    for (int q0 = 0; q0 < n; q0 += SP_NT) {
+      int q = q0 + threadIdx.x;
+      int m = 0;
+      if (q < n) {
+        int f = cand[q];
+        if (comp[f] == cs) {
+          double dx = ((double)(f % nx) + 0.5) * res - sx, dy = ((double)(f / nx) + 0.5) * res - sy;
+          m = dx * dx + dy * dy >= sep2;
+        }
+      }
+      int t2;
+      int off = block_excl_scan<SP_NT>(m, sh, t2);
+      if (m && seen + off == s_rank) s_j = cand[q];
+      seen += t2;
+      if (seen > s_rank) break;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int a = s_acc;
+      int fj = s_j;
+      stx[a] = sx;
+      sty[a] = sy;
+      out_pos[a * 2] = sx;
+      out_pos[a * 2 + 1] = sy;
+      out_goal[a * 2] = ((double)(fj % nx) + 0.5) * res;
+      out_goal[a * 2 + 1] = ((double)(fj / nx) + 0.5) * res;
+      s_acc = a + 1;
+    }
+  }
+  if (threadIdx.x == 0 && s_acc < A) B.status[slot] = CW_E_NOROUTE;
+}
+
+}  // namespace cw
+
+// ================================================================= C ABI
+extern "C" {
+
+size_t cw_scene_seed_scratch_bytes(int E) { return (size_t)E * sizeof(cw::EnvSeeds); }
+
+// Sample E scenes (one per scene_seed) end to end on `stream`:
+// zones -> terrain -> placement -> raster -> nearest-obstacle BFS -> walk list -> spawn.
+// Rows are written at slots[e] (slots may be NULL = identity).  Returns 0 or a
+// cudaError_t; per-env failures are reported in B->status.
+int cw_sample_scenes(const cw_scene_params* P, int E, const uint64_t* scene_seeds,
+                     const uint64_t* crowd_seeds, const int32_t* slots, void* seed_scratch,
+                     const cw_scene_buffers* B, void* stream) {
+  using namespace cw;
+  if (E <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  EnvSeeds* S = (EnvSeeds*)seed_scratch;
+  const cw_scene_params p = *P;
+  const cw_scene_buffers b = *B;
+  k_seeds<<<(E + 127) / 128, 128, 0, st>>>(E, scene_seeds, crowd_seeds, S);
+  if (p.layout == 1) k_zones_blk<<<E, 512, 0, st>>>(p, E, slots, S, b);
+  else k_zones<<<E, 256, 0, st>>>(p, E, slots, S, b);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_terrain, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(TerrainSmem));
+    cudaFuncSetAttribute(k_spawn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  k_terrain<<<E, TER_NT, sizeof(TerrainSmem), st>>>(p, E, slots, S, b);
+  k_place<<<(E + 3) / 4, 128, 0, st>>>(p, E, slots, S, b);
+  const int quads = (p.nx * p.ny + 3) / 4;
+  k_raster<<<dim3((quads + 255) / 256, E), 256, 0, st>>>(p, E, slots, b);
+  if (p.obj_max > 0) k_footprint<<<dim3((p.obj_max + 3) / 4, E), 128, 0, st>>>(p, E, slots, b);
+  k_nearest<<<E, BFS_NT, 0, st>>>(p, E, slots, b);
+  k_walk<<<E, 1024, 0, st>>>(p, E, slots, b);
+  if (p.peds > 0) {
+    size_t sm = (size_t)p.peds * 2 * sizeof(double) + sizeof(Pcg64Raw);
+    k_spawn<<<E, SP_NT, sm, st>>>(p, E, slots, S, b);
+  }
+  return (int)cudaGetLastError();
+}
+
+// spawn_agents(occupancy, count, seed) for caller-supplied labels (step.py:37-63).
+int cw_spawn_agents(const cw_scene_params* P, int E, const uint64_t* crowd_seeds,
+                    const int32_t* slots, void* seed_scratch, const cw_scene_buffers* B,
+                    void* stream) {
+  using namespace cw;
+  if (E <= 0 || P->peds <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  EnvSeeds* S = (EnvSeeds*)seed_scratch;
+  k_seeds<<<(E + 127) / 128, 128, 0, st>>>(E, crowd_seeds, crowd_seeds, S);
+  size_t sm = (size_t)P->peds * 2 * sizeof(double) + sizeof(Pcg64Raw);
+  k_spawn<<<E, SP_NT, sm, st>>>(*P, E, slots, S, *B);
+  return (int)cudaGetLastError();
+}
+
+// _prepare_env for caller-supplied label grids (field.py:60-67, 403-413):
+// nearest-obstacle map + walkable list for rows slots[e] of B->labels.
+int cw_prepare_envs(const cw_scene_params* P, int E, const int32_t* slots,
+                    const cw_scene_buffers* B, void* stream) {
+  using namespace cw;
+  if (E <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  k_nearest<<<E, BFS_NT, 0, st>>>(*P, E, slots, *B);
+  k_walk<<<E, 1024, 0, st>>>(*P, E, slots, *B);
+  return (int)cudaGetLastError();
+}
+
+}  // extern "C"

@@ -1,0 +1,379 @@
+"""Scene sampling on the B200 -- the reference's urbangen entry points, batched.
+
+Mirrors /root/reference/pkg/src/citywalk/urbangen:
+  * ``SceneSpec`` / ``TaskKind`` / ``Split`` / ``Zone`` / ``CellLabel`` (types.py:11-143)
+  * ``generate_scene(spec, catalog=None)`` (scene.py:38) and
+    ``rasterize_occupancy(scene, resolution=None)`` (occupancy.py:28)
+  * ``load_catalog(path=None)`` (catalog.py:14-24)
+plus the batch form the north star asks for: ``SceneSampler.sample(seeds)``
+runs zones -> terrain WFC -> placement -> raster -> nearest-obstacle BFS ->
+walk list -> spawn for every env on the device in one stream-ordered call
+(``cw_sample_scenes``).  Route anchors / scene JSON (scene.py:87-238) are
+out of scope.
+"""
+
+import json
+import math
+import os
+from dataclasses import dataclass, field
+from enum import Enum, IntEnum
+
+import numpy as np
+
+from . import _lib
+from .errors import STATUS_ERRORS
+
+
+class TaskKind(str, Enum):
+    NAV_CLEAR = "NavClear"
+    NAV_STATIC = "NavStatic"
+    NAV_DYNAMIC = "NavDynamic"
+    TRAVERSE = "Traverse"
+
+
+class Split(str, Enum):
+    TRAIN = "Train"
+    TEST = "Test"
+
+
+class Zone(IntEnum):
+    SIDEWALK = 0
+    CROSSWALK = 1
+    PLAZA = 2
+    BUILDING = 3
+    VEGETATION = 4
+    ROADWAY = 5
+
+
+class CellLabel(IntEnum):
+    OBSTACLE = 0
+    ROADWAY = 1
+    WALKABLE = 2
+    NON_WALKABLE_GROUND = 3
+
+
+TERRAIN_FAMILIES = ("Flat", "Slope", "Stair", "Rough")
+TERRAIN_KINDS = ("Flat", "SlopeUp", "SlopeDown", "StairUp", "StairDown", "Rough")
+BLOCK_SIZE_M = 20.0
+TILE_SIZE_M = 2.0
+ATTEMPTS_PER_OBJECT = 100
+_TASK_CODE = {TaskKind.NAV_CLEAR: 0, TaskKind.NAV_STATIC: 1, TaskKind.NAV_DYNAMIC: 2,
+              TaskKind.TRAVERSE: 3}
+
+
+@dataclass(frozen=True)
+class SceneSpec:
+    """urbangen/types.py:88-115 (same fields, defaults and validation)."""
+
+    seed: int
+    extent_m: tuple = (10.0, 10.0)
+    task_kind: TaskKind = TaskKind.NAV_STATIC
+    split: Split = Split.TRAIN
+    object_density: float = 1.0
+    pedestrian_count: int = 0
+    terrain_mix: dict = field(
+        default_factory=lambda: {"Flat": 0.7, "Slope": 0.1, "Stair": 0.0, "Rough": 0.2})
+    grid_resolution_m: float = 0.1
+
+    def __post_init__(self):
+        w, l = self.extent_m
+        if not (5.0 <= w <= 1200.0 and 5.0 <= l <= 1200.0):
+            raise ValueError("extent_m components must lie in [5.0, 1200.0]")
+        if self.object_density < 0:
+            raise ValueError("object_density must be >= 0")
+        if self.grid_resolution_m <= 0:
+            raise ValueError("grid_resolution_m must be > 0")
+        total = sum(self.terrain_mix.get(k, 0.0) for k in TERRAIN_FAMILIES)
+        if abs(total - 1.0) > 1e-9:
+            raise ValueError("terrain_mix weights must sum to 1")
+        for k in self.terrain_mix:
+            if k not in TERRAIN_FAMILIES:
+                raise ValueError(f"unknown terrain family {k!r}")
+
+
+@dataclass(frozen=True)
+class CatalogEntry:
+    category: str
+    footprint: tuple
+    height: float
+    allowed_zones: tuple
+
+
+def load_catalog(path=None):
+    """catalog.py:14-24; the bundled default is data/catalog.json."""
+    if path is None:
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "catalog.json")
+    with open(path, "r", encoding="utf-8") as fh:
+        entries = [CatalogEntry(d["category"], (float(d["footprint"][0]), float(d["footprint"][1])),
+                                float(d["height"]), tuple(Zone[z] for z in d["allowed_zones"]))
+                   for d in json.load(fh)]
+    if not entries:
+        raise ValueError("catalog is empty")
+    return entries
+
+
+@dataclass
+class OccupancyGrid:
+    """types.py:364-379."""
+
+    resolution: float
+    labels: np.ndarray
+    elevation: np.ndarray
+
+    @property
+    def shape(self):
+        return self.labels.shape
+
+    def cell_of(self, x, y):
+        return int(y / self.resolution), int(x / self.resolution)
+
+
+@dataclass
+class AssetInstance:
+    category: str
+    x: float
+    y: float
+    yaw: float
+    footprint: tuple
+    height: float
+
+
+@dataclass
+class SceneDescription:
+    """The device-sampled scene (types.py:385-394 minus blocks/routes)."""
+
+    spec: SceneSpec
+    zones: np.ndarray
+    terrain_assignment: np.ndarray
+    terrain_tiles: list
+    noise_seed: int
+    objects: list
+    placement_overflow: bool
+    occupancy: OccupancyGrid
+
+
+def scene_params(spec, catalog=None, obj_max=None):
+    """Host-side shape derivation shared by every env of a batch (exactly as the
+    reference computes it in Python: zones.py:46-49, terrain.py:227-238,
+    placement.py:87-97, scene.py:40-79)."""
+    catalog = catalog or load_catalog()
+    if len(catalog) > _lib.MAX_CAT:
+        raise ValueError(f"catalog larger than {_lib.MAX_CAT} entries")
+    w, l = spec.extent_m
+    res = spec.grid_resolution_m
+    p = _lib.SceneParams()
+    p.nx = int(np.ceil(w / res))
+    p.ny = int(np.ceil(l / res))
+    if p.nx < 4 or p.ny < 4:
+        from .errors import ExtentTooSmall
+        raise ExtentTooSmall(f"extent {spec.extent_m} too small at resolution {res}")
+    p.res, p.w, p.l = res, w, l
+    task = TaskKind(spec.task_kind)
+    p.task = _TASK_CODE[task]
+    p.split = 0 if Split(spec.split) == Split.TRAIN else 1
+    for i, k in enumerate(TERRAIN_FAMILIES):
+        p.mix[i] = float(spec.terrain_mix.get(k, 0.0))
+    if min(w, l) >= 2 * BLOCK_SIZE_M and task != TaskKind.TRAVERSE:
+        p.layout, p.brows, p.bcols = 1, int(l // BLOCK_SIZE_M), int(w // BLOCK_SIZE_M)
+        if p.brows * p.bcols > 64 or p.nx > 1024:
+            raise NotImplementedError("block layouts above 64 blocks / 1024 columns")
+    elif task == TaskKind.TRAVERSE:
+        p.layout = 2
+    else:
+        p.layout = 0
+    probs = np.array([0.4, 0.3, 0.3], dtype=float)
+    probs /= probs.sum()
+    cdf = probs.cumsum()
+    cdf /= cdf[-1]
+    for i in range(3):
+        p.quad_cdf[i] = float(cdf[i])
+    p.trows = max(1, int(np.ceil(p.ny * res / TILE_SIZE_M)))
+    p.tcols = max(1, int(np.ceil(p.nx * res / TILE_SIZE_M)))
+    if p.trows * p.tcols > 1024:
+        raise NotImplementedError("terrain lattices above 32x32 tiles")
+    p.cpt = int(round(TILE_SIZE_M / res))
+    p.nonflat_split_col = int(p.nx * 0.5) if task == TaskKind.TRAVERSE else -1
+    p.n_cat = len(catalog)
+    for i, e in enumerate(catalog):
+        p.cat_w[i], p.cat_l[i] = e.footprint
+        p.cat_reach[i] = float(np.hypot(*e.footprint)) / 2.0
+        p.cat_zones[i] = sum(1 << int(z) for z in e.allowed_zones)
+    order = sorted(range(len(catalog)), key=lambda i: catalog[i].footprint[0] * catalog[i].footprint[1])
+    for i, k in enumerate(order):
+        p.small_first[i] = k
+    area = p.ny * p.nx * res * res
+    base = 0 if task == TaskKind.NAV_CLEAR else int(np.floor(4.0 * area / 100.0 + 0.5))
+    density = spec.object_density * (4.0 / 6.0 if task == TaskKind.TRAVERSE else 1.0)
+    p.obj_count = int(np.floor(density * base + 0.5))
+    p.obj_max = max(1, p.obj_count if obj_max is None else obj_max)
+    p.attempts = ATTEMPTS_PER_OBJECT
+    p.region = {TaskKind.NAV_STATIC: 1, TaskKind.NAV_DYNAMIC: 1, TaskKind.TRAVERSE: 2}.get(task, 0)
+    p.peds = int(spec.pedestrian_count)
+    p.spawn_region = 1 if task == TaskKind.TRAVERSE else 0
+    return p
+
+
+class SceneBatch:
+    """Device-resident outputs of one sampling batch (E rows)."""
+
+    def __init__(self, params, E, device="cuda"):
+        import torch
+        self.params = params
+        self.E = E
+        self.device = torch.device(device)
+        p = params
+        N = p.nx * p.ny
+        T = _lib.MAX_TILES
+        d = dict(device=self.device)
+        z = torch.zeros
+        self.zones = z((E, p.ny, p.nx), dtype=torch.uint8, **d)
+        self.labels = z((E, p.ny, p.nx), dtype=torch.uint8, **d)
+        self.elev = z((E, p.ny, p.nx), dtype=torch.float32, **d)
+        self.assign = z((E, p.trows, p.tcols), dtype=torch.int32, **d)
+        self.n_tiles = z((E,), dtype=torch.int32, **d)
+        self.tile_code = z((E, T), dtype=torch.int8, **d)
+        self.tile_kind = z((E, T), dtype=torch.int8, **d)
+        self.tile_param = z((E, T), dtype=torch.float64, **d)
+        self.tile_p = z((E, T, 4), dtype=torch.float64, **d)
+        self.tile_w = z((E, T), dtype=torch.float64, **d)
+        self.allowed = z((E, 4, T), dtype=torch.int64, **d)
+        self.noise_seed = z((E,), dtype=torch.int64, **d)
+        self.wfc_attempts = z((E,), dtype=torch.int32, **d)
+        self.obj_cat = z((E, p.obj_max), dtype=torch.int32, **d)
+        self.obj_pose = z((E, p.obj_max, 3), dtype=torch.float64, **d)
+        self.obj_n = z((E,), dtype=torch.int32, **d)
+        self.overflow = z((E,), dtype=torch.uint8, **d)
+        self.nearest = z((E, p.ny, p.nx), dtype=torch.int32, **d)
+        self.has_obs = z((E,), dtype=torch.uint8, **d)
+        self.walk = z((E, N), dtype=torch.int32, **d)
+        self.walk_n = z((E,), dtype=torch.int32, **d)
+        A = max(p.peds, 1)
+        self.sp_pos = z((E, A, 2), dtype=torch.float64, **d)
+        self.sp_goal = z((E, A, 2), dtype=torch.float64, **d)
+        self.sp_kind = z((E, A), dtype=torch.int8, **d)
+        self.sp_pref = z((E, A), dtype=torch.float64, **d)
+        self.status = z((E,), dtype=torch.int32, **d)
+        self.scene_seed = z((E,), dtype=torch.int64, **d)
+        self._scratch_rows = 0
+        self._ensure_scratch(E)
+
+    def _ensure_scratch(self, rows):
+        import torch
+        if rows <= self._scratch_rows:
+            return
+        p = self.params
+        N = p.nx * p.ny
+        self.scratch_i32 = torch.empty((rows, 3 * N), dtype=torch.int32, device=self.device)
+        self.scratch_f64 = torch.empty((rows, max(p.obj_max * 8, N)), dtype=torch.float64,
+                                       device=self.device)
+        nbytes = _lib.lib().cw_scene_seed_scratch_bytes(rows)
+        self.seed_scratch = torch.empty((nbytes,), dtype=torch.uint8, device=self.device)
+        self._scratch_rows = rows
+
+    def buffers(self):
+        b = _lib.SceneBuffers()
+        for name in _lib.SCENE_BUFFER_FIELDS:
+            setattr(b, name, getattr(self, name).data_ptr())
+        return b
+
+    def check_status(self, rows=None):
+        st = self.status.cpu().numpy() if rows is None else self.status[rows].cpu().numpy()
+        bad = np.flatnonzero(st)
+        if bad.size:
+            code = int(st[bad[0]])
+            raise STATUS_ERRORS.get(code, RuntimeError)(
+                f"scene sampling failed for {bad.size} env(s); first row {int(bad[0])} code {code}")
+
+    # -- host views (reference-shaped) ---------------------------------------------
+    def occupancy(self, i):
+        return OccupancyGrid(resolution=float(self.params.res), labels=self.labels[i].cpu().numpy(),
+                             elevation=self.elev[i].cpu().numpy())
+
+    def objects(self, i, catalog=None):
+        catalog = catalog or load_catalog()
+        n = int(self.obj_n[i])
+        cats = self.obj_cat[i, :n].cpu().numpy()
+        pose = self.obj_pose[i, :n].cpu().numpy()
+        return [AssetInstance(catalog[int(k)].category, float(x), float(y), float(yaw),
+                              catalog[int(k)].footprint, catalog[int(k)].height)
+                for k, (x, y, yaw) in zip(cats, pose)]
+
+    def scene(self, i, spec, catalog=None):
+        n = int(self.n_tiles[i])
+        tiles = [dict(kind=TERRAIN_KINDS[int(self.tile_kind[i, t])], param=float(self.tile_param[i, t]),
+                      code=int(self.tile_code[i, t]), p=self.tile_p[i, t].cpu().numpy().tolist())
+                 for t in range(n)]
+        return SceneDescription(
+            spec=spec, zones=self.zones[i].cpu().numpy(), terrain_assignment=self.assign[i].cpu().numpy(),
+            terrain_tiles=tiles, noise_seed=int(self.noise_seed[i]) & ((1 << 64) - 1),
+            objects=self.objects(i, catalog), placement_overflow=bool(self.overflow[i]),
+            occupancy=self.occupancy(i))
+
+
+class SceneSampler:
+    """Samples batches of scenes that share a SceneSpec shape (async scheme:
+    every env has its own seed, batch.py:84-96)."""
+
+    def __init__(self, spec, capacity, catalog=None, device="cuda"):
+        self.spec = spec
+        self.catalog = catalog or load_catalog()
+        self.params = scene_params(spec, self.catalog)
+        self.batch = SceneBatch(self.params, capacity, device)
+
+    def sample(self, scene_seeds, crowd_seeds=None, slots=None, stream=None, check=True):
+        """Sample len(scene_seeds) scenes into rows ``slots`` (default 0..E-1).
+
+        scene_seeds / crowd_seeds / slots: device int64 tensors (or sequences)."""
+        import torch
+        dev = self.batch.device
+        seeds = _as_u64_tensor(scene_seeds, dev)
+        E = seeds.numel()
+        if E == 0:
+            return self.batch
+        if crowd_seeds is None and self.params.peds > 0:
+            # first spawn of an env whose env seed is its scene seed (batch.py:179)
+            from .rng import child_seeds_device
+            crowd_seeds = child_seeds_device(seeds, "crowd", 0)
+        cseeds = None if crowd_seeds is None else _as_u64_tensor(crowd_seeds, dev)
+        sl = None
+        if slots is not None:
+            sl = torch.as_tensor(slots, dtype=torch.int32, device=dev).contiguous()
+            self.batch.status.index_fill_(0, sl.long(), 0)
+            self.batch.scene_seed.index_copy_(0, sl.long(), seeds)
+        else:
+            if E > self.batch.E:
+                raise ValueError("more seeds than batch capacity")
+            self.batch.status[:E].zero_()
+            self.batch.scene_seed[:E] = seeds
+        self.batch._ensure_scratch(E)
+        b = self.batch.buffers()
+        err = _lib.lib().cw_sample_scenes(
+            self.params, E, _lib.ptr(seeds), _lib.ptr(cseeds), _lib.ptr(sl),
+            _lib.ptr(self.batch.seed_scratch), b, _lib.stream_ptr(stream))
+        _lib.check(err, "cw_sample_scenes")
+        if check:
+            self.batch.check_status(None if sl is None else sl.long())
+        return self.batch
+
+
+def _as_u64_tensor(seeds, device):
+    import torch
+    if isinstance(seeds, torch.Tensor):
+        return seeds.to(device=device, dtype=torch.int64).contiguous()
+    arr = np.array([int(s) & ((1 << 64) - 1) for s in seeds], dtype=np.uint64).view(np.int64)
+    return torch.from_numpy(arr).to(device)
+
+
+def generate_scene(spec, catalog=None, device="cuda"):
+    """scene.py:38 generate_scene on the device (route anchors out of scope).
+    The returned scene already carries its occupancy raster."""
+    s = SceneSampler(spec, 1, catalog, device)
+    b = s.sample([spec.seed])
+    return b.scene(0, spec, s.catalog)
+
+
+def rasterize_occupancy(scene, resolution=None):
+    """occupancy.py:28 -- the device pipeline rasterises at the spec resolution."""
+    if resolution is not None and resolution != scene.spec.grid_resolution_m:
+        raise NotImplementedError("the B200 path rasterises at spec.grid_resolution_m only")
+    return scene.occupancy
