@@ -1,0 +1,352 @@
+"""Benchmark: async scene sampling + crowd dynamics step on B200 (BASELINE.json configs[1]).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--envs E]
+
+Workload (cfg2): E=1024 envs per GPU, 32 m x 32 m at 0.125 m (256x256 grid),
+64 objects, 32 pedestrians per env, NavDynamic, terrain mix 0.25 each, dt 0.05,
+seeds child_seed(0, "env", global_env_id).  A "step" is one CrowdField.step over
+every env of the rank (one cw_crowd_step launch).  Scenes/s is the whole
+cw_sample_scenes pipeline over the same E envs.  Under torchrun each rank owns
+E envs (weak scaling, no data-path collective; one NCCL all_gather of per-env
+stats at the end).  ``--impl reference`` times the reference's CPU algorithm
+(the oracle port, all host cores) on a bounded sample of the same workload.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MIX = {"Flat": 0.25, "Slope": 0.25, "Stair": 0.25, "Rough": 0.25}
+CFG = dict(extent=32.0, res=0.125, objects=64, peds=32, steps_cfg=500)
+METRIC = "env-steps/sec and scenes sampled/sec at N envs on 1/2/4/8 B200; % of HBM peak"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.proc = None
+        self.path = f"/tmp/cw_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        try:
+            rows = [l.split(",") for l in open(self.path).read().strip().splitlines()]
+            rows = [[c.strip() for c in r] for r in rows if len(r) >= 7]
+            sm = [float(r[0]) for r in rows]
+            mx = max(float(r[1]) for r in rows)
+            reasons = set()
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for r in rows:
+                for n, v in zip(names, r[3:7]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+            return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                    "samples": len(rows)}
+        except Exception as exc:  # no nvidia-smi
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": str(exc)[:80]}
+
+
+def make_spec():
+    from paper_2505_00690_b200.urbangen import SceneSpec, TaskKind
+    area_objects = int(np.floor(4.0 * (256 * 256 * 0.125 * 0.125) / 100.0 + 0.5))  # 41
+    return SceneSpec(seed=0, extent_m=(CFG["extent"], CFG["extent"]), task_kind=TaskKind.NAV_DYNAMIC,
+                     object_density=CFG["objects"] / area_objects, pedestrian_count=CFG["peds"],
+                     terrain_mix=MIX, grid_resolution_m=CFG["res"])
+
+
+# ============================================================================ ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2505_00690_b200 import _lib
+    from paper_2505_00690_b200.crowd import CrowdConfig, CrowdField
+    from paper_2505_00690_b200.rng import child_seeds_device
+    from paper_2505_00690_b200.urbangen import SceneSampler
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    _lib.build()
+    E = args.envs
+    spec = make_spec()
+    zero = torch.zeros(E, dtype=torch.int64, device=dev)
+    gids = torch.arange(rank * E, (rank + 1) * E, device=dev)
+    env_seeds = child_seeds_device(zero, "env", gids)
+    crowd_seeds = child_seeds_device(env_seeds, "crowd", 0)
+    run_seeds = child_seeds_device(env_seeds, "crowd-run").cpu().numpy().view(np.uint64)
+    sampler = SceneSampler(spec, E, device=dev)
+
+    # ---- scene sampling throughput (whole pipeline, E envs per launch sequence)
+    st = torch.cuda.current_stream()
+    for _ in range(max(1, args.sample_warmup)):
+        sampler.sample(env_seeds, crowd_seeds, check=False)
+    torch.cuda.synchronize()
+    sampler.batch.check_status()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = args.sample_reps
+    ev0.record(st)
+    for _ in range(reps):
+        sampler.sample(env_seeds, crowd_seeds, check=False)
+    ev1.record(st)
+    torch.cuda.synchronize()
+    sample_ms = ev0.elapsed_time(ev1) / reps
+    b = sampler.batch
+    b.check_status()
+
+    # ---- crowd
+    f = CrowdField(b, CrowdConfig(), [int(s) for s in run_seeds], device=dev, threads=args.threads)
+    f.set_from_spawn(b)
+    f.prepare_step()
+    # robot: static at a seeded walkable cell per env (route anchors are §8f), zero velocity
+    g = torch.Generator(device="cpu").manual_seed(1234 + rank)
+    pick = (torch.rand(E, generator=g).to(dev) * b.walk_n.double()).long()
+    cell = b.walk.gather(1, pick[:, None])[:, 0].long()
+    rpos = torch.stack([((cell % 256).double() + 0.5) * CFG["res"],
+                        ((cell // 256).double() + 0.5) * CFG["res"]], dim=1).contiguous()
+    rvel = torch.zeros_like(rpos)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > L2
+    for _ in range(args.warmup):
+        f.step(rpos, rvel, 0.35, check=False)
+    torch.cuda.synchronize()
+    f.check_flags()
+    f.counters_t.zero_()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    active = int(f.active_t.sum().item())
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(dev.index) as clk:
+        for k in range(args.steps):
+            flush.fill_(float(k))          # L2 flush between timed steps (untimed)
+            starts[k].record(st)
+            f.step(rpos, rvel, 0.35, check=False)
+            ends[k].record(st)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    f.check_flags()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    t_ms = float(sum(step_ms))
+    counters = f.stats()
+    # ---- e2e through the public API with host buffers (pinned H2D in, D2H pos/vel out)
+    rpos_h = rpos.cpu().pin_memory()
+    rvel_h = rvel.cpu().pin_memory()
+    out_pos = torch.empty(f.pos_t.shape, dtype=torch.float64).pin_memory()
+    out_vel = torch.empty(f.vel_t.shape, dtype=torch.float64).pin_memory()
+    e2e_steps = min(args.steps, args.e2e_steps)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        rp = rpos_h.to(dev, non_blocking=True)
+        rv = rvel_h.to(dev, non_blocking=True)
+        f.step(rp, rv, 0.35, check=False)
+        out_pos.copy_(f.pos_t, non_blocking=True)
+        out_vel.copy_(f.vel_t, non_blocking=True)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    h2d = rpos_h.numel() * 8 * 2
+    d2h = out_pos.numel() * 8 * 2
+
+    # ---- max over ranks; per-env stats all_gather (the one collective)
+    stats = torch.stack([f.last_gap_t, b.obj_n.double(), b.walk_n.double(),
+                         f.active_t.sum(1).double()], 1)
+    tmax = torch.tensor([t_ms, sample_ms, e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        gathered = [torch.empty_like(stats) for _ in range(world)]
+        dist.all_gather(gathered, stats)
+        stats = torch.cat(gathered)
+    t_ms, sample_ms, e2e_s = [float(x) for x in tmax.cpu()]
+    if rank == 0:
+        steps = args.steps
+        env_steps = E * world * steps
+        value = env_steps / (t_ms / 1e3)
+        scenes = E * world / (sample_ms / 1e3)
+        # roofline: algorithmic bytes of the dynamics kernel:
+        #   74 B per active agent-step + 8 B per path point scanned + 20 B per env-step (robot)
+        bytes_step = (74.0 * active + 20.0 * E) + 8.0 * counters["path_points_scanned"] / steps
+        avg_ms = t_ms / steps
+        achieved = bytes_step / (avg_ms / 1e3) / 1e9
+        peak, src = peaks()
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "env-steps/s",
+            "n_gpus": world, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": round(avg_ms, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded procedural scenes)",
+            "config": {"workload": "cfg2: 1024 envs/GPU, 256x256 grid (0.125 m), 64 objects, "
+                                   "32 pedestrians/env, NavDynamic, dynamics step (+ scene sampling)",
+                       "envs_per_gpu": E, "grid": [256, 256], "objects": 64, "peds": CFG["peds"],
+                       "parallelism": f"env-shard x{world}", "l2": "flushed (256 MB write) between timed steps",
+                       "robot": "static per env at a seeded walkable cell, zero velocity"},
+            "scenes_per_sec": round(scenes, 1), "sample_ms_per_batch": round(sample_ms, 3),
+            "agent_steps_per_sec": round(value * CFG["peds"], 1),
+            "e2e": {"value": round(E * world * e2e_steps / e2e_s, 1), "unit": "env-steps/s",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "steps": e2e_steps},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 5), "traffic": None,
+                         "kernel": "k_crowd_step", "peak_source": src,
+                         "bytes_per_launch": round(bytes_step, 1)},
+            "gpu_launches": steps,
+            "clocks": clk.summary(),
+            "counters": counters,
+            "stats": {"min_gap": float(torch.nan_to_num(stats[:, 0], posinf=1e9).min()),
+                      "mean_objects": float(stats[:, 1].mean()), "envs": int(stats.shape[0])},
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline_sample(b, f, run_seeds)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline_sample(b, f, run_seeds, n_env=4, steps=6):
+    """Oracle port (the reference's algorithm in numpy), 1 core, bounded sample:
+    ``n_env`` cfg2 envs (GPU-sampled scenes, bit-identical to the oracle's) stepped
+    ``steps`` ticks, plus one oracle scene generation."""
+    from oracle import crowd as C
+    from oracle import scene as S
+    grids = [(b.labels[i].cpu().numpy(), CFG["res"]) for i in range(n_env)]
+    agents = []
+    for i in range(n_env):
+        k = b.sp_kind[i].cpu().numpy()
+        agents.append(dict(pos=b.sp_pos[i].cpu().numpy(), goal=b.sp_goal[i].cpu().numpy(),
+                           radius=np.array([C.RADIUS[x] for x in k]), pref=b.sp_pref[i].cpu().numpy(),
+                           max_speed=np.array([C.MAX_SPEED[x] for x in k]), kind=k))
+    ref = C.CrowdFieldOracle(grids, C.Config(), [int(s) for s in run_seeds[:n_env]])
+    ref.set_agents(agents)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        ref.step()
+    dt = time.perf_counter() - t0
+    return {"value": round(n_env * steps / dt, 3), "unit": "env-steps/s", "cores": 1,
+            "kind": "port", "sample": f"{n_env} cfg2 envs x {steps} crowd ticks, oracle port, 1 thread"}
+
+
+# ============================================================================ reference arm
+def _ref_worker(args):
+    """One process: generate its cfg2 env with the oracle, then time `steps` ticks."""
+    env_id, steps, warm = args
+    from oracle import crowd as C
+    from oracle import scene as S
+    from oracle.rng import child_seed
+    import json as _json
+    cat = S.load_catalog_tuples(_json.load(open(os.path.join(ROOT, "paper_2505_00690_b200", "data", "catalog.json"))))
+    s = child_seed(0, "env", env_id)
+    sc = S.generate_scene(dict(seed=s, extent=(32.0, 32.0), res=0.125, task="NavDynamic", split="Train",
+                               density=64 / 41, mix=MIX), cat)
+    sp = C.spawn_agents(sc["labels"], 0.125, CFG["peds"], child_seed(s, "crowd", 0))
+    f = C.CrowdFieldOracle([(sc["labels"], 0.125)], C.Config(), [child_seed(s, "crowd-run")])
+    f.set_agents([sp])
+    for _ in range(warm):
+        f.step()
+    t = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        f.step()
+        t.append(time.perf_counter() - t0)
+    return t
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    # bounded: one env per core, at most a few minutes for the whole --steps/--warmup run
+    steps = max(1, min(args.steps, 60))
+    warm = max(0, min(args.warmup, 5))
+    with mp.get_context("spawn").Pool(cores) as pool:
+        t0 = time.perf_counter()
+        times = pool.map(_ref_worker, [(i, steps, warm) for i in range(cores)])
+        wall = time.perf_counter() - t0
+    per_step = np.max(np.array(times), axis=0)       # all cores step in parallel
+    total = float(per_step.sum())
+    value = cores * steps / total
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "env-steps/s",
+            "n_gpus": world, "steps": steps, "warmup": warm,
+            "ms_per_step": round(1e3 * total / steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded procedural scenes)",
+            "config": {"workload": "cfg2 shape: 256x256 grid (0.125 m), 64 objects, 32 peds/env; "
+                                   "sample of one env per host core",
+                       "envs": cores, "parallelism": f"{cores} processes"},
+            "cpu_baseline": {"value": round(value, 3), "unit": "env-steps/s", "cores": cores,
+                             "kind": "port",
+                             "sample": f"{cores} cfg2 envs (one per core) x {steps} crowd ticks; "
+                                       f"oracle port of the reference algorithm; wall {wall:.1f}s incl. scene gen"},
+            "e2e": {"value": round(value, 3), "unit": "env-steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--envs", type=int, default=1024)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--threads", type=int, default=128)
+    ap.add_argument("--sample-warmup", type=int, default=1)
+    ap.add_argument("--sample-reps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=100)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -13,7 +13,8 @@
  *   cw_spawn_agents    replaces crowd/step.py:37 spawn_agents for host-built grids.
  *   cw_prepare_envs    replaces crowd/field.py:60-67 _prepare_env for host-built grids.
  *   cw_crowd_step      replaces crowd/field.py:90 CrowdField.step (workers ignored:
- *                      results are split-invariant by construction).
+ *                      results are split-invariant by construction): three
+ *                      stream-ordered kernels k_guide -> k_astar -> k_orca.
  *   cw_seed_streams    replaces np.random.Generator(np.random.PCG64(seed)) for
  *                      field.py:36 (per-env goal-resample streams).
  *   cw_child_seeds     replaces rng.py:15 child_seed for the batch seed tree
@@ -81,6 +82,8 @@ typedef struct cw_scene_buffers {
   int32_t* obj_cat; double* obj_pose; int32_t* obj_n; uint8_t* overflow;
   int32_t* nearest; uint8_t* has_obs;
   int32_t* walk; int32_t* walk_n;
+  int32_t* reach;       /* (E, ny*nx) 4-connected component of passable cells, -1 = obstacle */
+  uint32_t* passbits;   /* (E, ceil(ny*nx/32)) bit f = labels[f] != OBSTACLE */
   double* sp_pos; double* sp_goal; int8_t* sp_kind; double* sp_pref;
   int32_t* status;
   int32_t* scratch_i32; /* (E, 3*ny*nx) */
@@ -100,7 +103,7 @@ int cw_spawn_agents(const cw_scene_params* params, int E, const uint64_t* crowd_
                     void* stream);
 
 /* _prepare_env for caller-supplied labels (field.py:60-67): fills nearest,
- * has_obs, walk, walk_n of rows slots[e] from buffers->labels; needs status
+ * has_obs, walk, walk_n, reach, passbits of rows slots[e] from buffers->labels; needs status
  * (zeroed) and scratch_i32.  Only params->nx/ny are read. */
 int cw_prepare_envs(const cw_scene_params* params, int E, const int32_t* slots,
                     const cw_scene_buffers* buffers, void* stream);
@@ -114,7 +117,9 @@ typedef struct cw_crowd_params {
   float nd2_f32;
   int32_t max_neighbors;
   double dt, safety_margin, goal_reach2, stall_c, stall_s;
-  int32_t resample_goals, use_static, path_cap, heap_cap, slots_per_env;
+  int32_t resample_goals, use_static, path_cap;
+  int32_t heap_cap;     /* global open-list spill entries per A* CTA */
+  int32_t astar_ctas;   /* persistent k_astar CTAs (one scratch slot each) */
 } cw_crowd_params;
 
 /* Device-resident CrowdField state (field.py:47-58) + guidance/A* scratch. */
@@ -125,10 +130,13 @@ typedef struct cw_crowd_state {
   int32_t* path_cells; int32_t* path_head; int32_t* path_n;
   const uint8_t* labels; const int32_t* nearest; const uint8_t* has_obs;
   const int32_t* walk; const int32_t* walk_n;
+  const int32_t* reach; const uint32_t* passbits;
   void* rng;
   double* last_gap; double* gap_tmp; int32_t* flags;
-  double* astar_g; int32_t* astar_parent; int32_t* astar_stamp; int32_t* astar_epoch;
-  void* astar_heap;
+  void* astar_rec;      /* (astar_ctas, ny*nx) {double g; int32 parent; int32 stamp} */
+  int32_t* astar_epoch; /* (astar_ctas) */
+  void* astar_heap;     /* (astar_ctas, heap_cap, 16 B) open-list spill area */
+  void* astar_req;      /* (E*A, 16 B) replanning queue {env, agent, start, goal} */
   int64_t* counters;
 } cw_crowd_state;
 
@@ -137,6 +145,9 @@ size_t cw_crowd_step_smem_bytes(int A, int threads);
 int cw_crowd_step(const cw_crowd_params* params, const cw_crowd_state* state,
                   const double* robot_pos, const double* robot_vel, double robot_radius,
                   const uint8_t* env_mask, int threads, void* stream);
+
+/* k_astar open-list entries held in shared memory (host-only query). */
+int cw_astar_smem_entries(void);
 
 int cw_seed_streams(int n, const uint64_t* seeds, void* out_states, void* stream);
 

@@ -41,7 +41,7 @@ class SceneParams(ctypes.Structure):
 SCENE_BUFFER_FIELDS = [
     "zones", "labels", "elev", "assign", "n_tiles", "tile_code", "tile_kind", "tile_param",
     "tile_p", "tile_w", "allowed", "noise_seed", "wfc_attempts", "obj_cat", "obj_pose", "obj_n",
-    "overflow", "nearest", "has_obs", "walk", "walk_n", "sp_pos", "sp_goal", "sp_kind", "sp_pref",
+    "overflow", "nearest", "has_obs", "walk", "walk_n", "reach", "passbits", "sp_pos", "sp_goal", "sp_kind", "sp_pref",
     "status", "scratch_i32", "scratch_f64",
 ]
 
@@ -57,14 +57,14 @@ class CrowdParams(ctypes.Structure):
         ("nd2", c_f64), ("nd2_f32", c_f32), ("max_neighbors", c_i32), ("dt", c_f64),
         ("safety_margin", c_f64), ("goal_reach2", c_f64), ("stall_c", c_f64), ("stall_s", c_f64),
         ("resample_goals", c_i32), ("use_static", c_i32), ("path_cap", c_i32), ("heap_cap", c_i32),
-        ("slots_per_env", c_i32),
+        ("astar_ctas", c_i32),
     ]
 
 
 CROWD_STATE_FIELDS = [
     "pos", "vel", "goal", "waypoint", "radius", "pref_speed", "max_speed", "active", "path_cells",
-    "path_head", "path_n", "labels", "nearest", "has_obs", "walk", "walk_n", "rng", "last_gap",
-    "gap_tmp", "flags", "astar_g", "astar_parent", "astar_stamp", "astar_epoch", "astar_heap",
+    "path_head", "path_n", "labels", "nearest", "has_obs", "walk", "walk_n", "reach", "passbits",
+    "rng", "last_gap", "gap_tmp", "flags", "astar_rec", "astar_epoch", "astar_heap", "astar_req",
     "counters",
 ]
 
@@ -75,7 +75,7 @@ class CrowdState(ctypes.Structure):
 
 EXPORTS = ["cw_scene_seed_scratch_bytes", "cw_sample_scenes", "cw_spawn_agents", "cw_prepare_envs",
            "cw_crowd_step_smem_bytes",
-           "cw_crowd_step", "cw_seed_streams", "cw_child_seeds", "cw_abi_sizes"]
+           "cw_crowd_step", "cw_astar_smem_entries", "cw_seed_streams", "cw_child_seeds", "cw_abi_sizes"]
 
 _lib = None
 
@@ -116,6 +116,8 @@ def lib():
     L.cw_crowd_step.restype = ctypes.c_int
     L.cw_crowd_step.argtypes = [ctypes.POINTER(CrowdParams), ctypes.POINTER(CrowdState), P, P,
                                 ctypes.c_double, P, ctypes.c_int, P]
+    L.cw_astar_smem_entries.restype = ctypes.c_int
+    L.cw_astar_smem_entries.argtypes = []
     L.cw_seed_streams.restype = ctypes.c_int
     L.cw_seed_streams.argtypes = [ctypes.c_int, P, P, P]
     L.cw_child_seeds.restype = ctypes.c_int

@@ -104,6 +104,7 @@ class CrowdField:
             self.res0 = self.res
             self.labels_t, self.nearest_t, self.has_obs_t = b.labels, b.nearest, b.has_obs
             self.walk_t, self.walk_n_t = b.walk, b.walk_n
+            self.reach_t, self.passbits_t = b.reach, b.passbits
             self._batch = b
         else:
             occs = list(occupancies)
@@ -117,6 +118,8 @@ class CrowdField:
             self.res0 = self.res
             self._batch = None
             self._upload_grids(occs)
+        if self.nx > 1024 or self.ny > 1024:
+            raise NotImplementedError("grids above 1024 x 1024 cells (A* packs row/col in 10 bits)")
         if len(env_seeds) != self.E:
             raise ValueError("env_seeds must have one seed per env")
         self.rng_t = torch.empty((self.E, 48), dtype=torch.uint8, device=self.device)
@@ -125,8 +128,9 @@ class CrowdField:
                                               _lib.stream_ptr()), "cw_seed_streams")
         N = self.nx * self.ny
         self.path_cap = int(path_cap or 2 * (self.nx + self.ny) + 64)
-        self.heap_cap = int(heap_cap or max(4096, N // 2))
-        self.slots = threads // 32
+        self.heap_cap = int(heap_cap or max(65536, 2 * N))
+        self.astar_ctas = int(torch.cuda.get_device_properties(self.device).multi_processor_count) \
+            if self.device.type == "cuda" else 1
         self.last_gap_t = torch.full((self.E,), float("inf"), dtype=torch.float64, device=self.device)
         self.gap_tmp_t = torch.zeros((self.E,), dtype=torch.float64, device=self.device)
         self.flags_t = torch.zeros((8,), dtype=torch.int32, device=self.device)
@@ -144,6 +148,8 @@ class CrowdField:
         self.has_obs_t = torch.zeros((E,), dtype=torch.uint8, device=self.device)
         self.walk_t = torch.empty((E, ny * nx), dtype=torch.int32, device=self.device)
         self.walk_n_t = torch.zeros((E,), dtype=torch.int32, device=self.device)
+        self.reach_t = torch.empty((E, ny * nx), dtype=torch.int32, device=self.device)
+        self.passbits_t = torch.zeros((E, (ny * nx + 31) // 32), dtype=torch.int32, device=self.device)
         self._prepare(None)
 
     def _prepare(self, rows):
@@ -160,6 +166,8 @@ class CrowdField:
         b.has_obs = self.has_obs_t.data_ptr()
         b.walk = self.walk_t.data_ptr()
         b.walk_n = self.walk_n_t.data_ptr()
+        b.reach = self.reach_t.data_ptr()
+        b.passbits = self.passbits_t.data_ptr()
         b.status = status.data_ptr()
         b.scratch_i32 = scratch.data_ptr()
         sl = None if rows is None else torch.as_tensor(rows, dtype=torch.int32, device=self.device)
@@ -184,17 +192,16 @@ class CrowdField:
         self.path_cells_t = torch.zeros((E, A, self.path_cap), dtype=torch.int32, device=d)
         self.path_head_t = torch.zeros((E, A), dtype=torch.int32, device=d)
         self.path_n_t = torch.zeros((E, A), dtype=torch.int32, device=d)
+        self.astar_req_t = torch.empty((max(1, E * A), 4), dtype=torch.int32, device=d)
 
     def _ensure_astar(self):
         import torch
         if self._astar_ready:
             return
-        S = self.E * self.slots
+        S = self.astar_ctas
         N = self.nx * self.ny
         d = self.device
-        self.astar_g_t = torch.empty((S, N), dtype=torch.float64, device=d)
-        self.astar_parent_t = torch.empty((S, N), dtype=torch.int32, device=d)
-        self.astar_stamp_t = torch.zeros((S, N), dtype=torch.int32, device=d)
+        self.astar_rec_t = torch.zeros((S, N, 2), dtype=torch.int64, device=d)  # {g, parent|stamp}
         self.astar_epoch_t = torch.zeros((S,), dtype=torch.int32, device=d)
         self.astar_heap_t = torch.empty((S, self.heap_cap, 2), dtype=torch.int64, device=d)
         self._astar_ready = True
@@ -285,7 +292,7 @@ class CrowdField:
         p.stall_c, p.stall_s = float(np.cos(0.6)), float(np.sin(0.6))
         p.resample_goals = int(bool(self.resample_goals))
         p.use_static = int(bool(self.has_obs_t.any().item()))
-        p.path_cap, p.heap_cap, p.slots_per_env = self.path_cap, self.heap_cap, self.slots
+        p.path_cap, p.heap_cap, p.astar_ctas = self.path_cap, self.heap_cap, self.astar_ctas
         return p
 
     def _state(self):
@@ -295,10 +302,10 @@ class CrowdField:
                  radius=self.radius_t, pref_speed=self.pref_t, max_speed=self.max_speed_t,
                  active=self.active_t, path_cells=self.path_cells_t, path_head=self.path_head_t,
                  path_n=self.path_n_t, labels=self.labels_t, nearest=self.nearest_t,
-                 has_obs=self.has_obs_t, walk=self.walk_t, walk_n=self.walk_n_t, rng=self.rng_t,
+                 has_obs=self.has_obs_t, walk=self.walk_t, walk_n=self.walk_n_t, reach=self.reach_t,
+                 passbits=self.passbits_t, rng=self.rng_t,
                  last_gap=self.last_gap_t, gap_tmp=self.gap_tmp_t, flags=self.flags_t,
-                 astar_g=self.astar_g_t, astar_parent=self.astar_parent_t,
-                 astar_stamp=self.astar_stamp_t, astar_epoch=self.astar_epoch_t,
+                 astar_rec=self.astar_rec_t, astar_epoch=self.astar_epoch_t, astar_req=self.astar_req_t,
                  astar_heap=self.astar_heap_t, counters=self.counters_t)
         for k, v in m.items():
             setattr(s, k, v.data_ptr())
@@ -387,7 +394,9 @@ class CrowdField:
     def stats(self):
         c = self.counters_t.cpu().numpy()
         return {"astar_expansions": int(c[0]), "path_points_scanned": int(c[1]),
-                "lp_fallbacks": int(c[2]), "stall_retries": int(c[3])}
+                "lp_fallbacks": int(c[2]), "stall_retries": int(c[3]),
+                "astar_cycles": int(c[4]), "astar_max_cycles": int(c[5]),
+                "cta_cycles": int(c[6]), "cta_max_cycles": int(c[7])}
 
 
 def step_crowd(agents, robot_state, occupancy, config, seed=0, resample_goals=True):

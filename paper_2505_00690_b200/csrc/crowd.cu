@@ -1,7 +1,9 @@
 // Crowd dynamics step on B200: one CTA per env, one warp per agent.
 //
-//   guidance   field.py:165-212 (+ _line_of_sight :601, _distance_to_polyline :613,
-//              paths.astar_path paths.py:48-87)
+//   k_guide    field.py:165-212 (waypoint pop, _distance_to_polyline :613,
+//              _line_of_sight :601); queues replans for k_astar
+//   k_astar    paths.astar_path paths.py:48-87, persistent warps over the queue
+//   k_orca     everything below, one CTA per env, one warp per agent
 //   pref       field.py:214-227
 //   neighbours field.py:246-262  fp32 Gram key fma(y_i,y_j,x_i*x_j), stable top-K
 //   half-plane field.py:448-495  (+ robot lane :303-317, static lane :319-348)
@@ -24,6 +26,8 @@ namespace cw {
 
 constexpr int MAXC = 12;   // neighbour lanes (<= 10) + robot + static
 constexpr double kWaypointReach = 0.5, kStrayLimit = 1.0;
+// open-list entries kept in shared memory by k_astar (16 B each: f bits, h bits | cell)
+CW_HD int astar_smem_entries() { return 8192; }
 
 struct HeapEnt { double f; int32_t cell; int32_t pad; };
 
@@ -218,130 +222,207 @@ CW_DEV double octile(int r, int c, int gr, int gc) {
   return kSqrt2 * (double)min(dr, dc) + (double)abs(dr - dc);
 }
 
-struct AStarCtx {
-  double* g;
-  int32_t* parent;
-  int32_t* stamp;
-  HeapEnt* heap;
-  int cap;
-  int epoch;
-  int nx, ny;
-  int gr, gc;
-};
+struct AstarRec { double g; int32_t parent; uint32_t tag; };  // tag = epoch << 14 | heap pos
+struct AstarReq { int32_t env, agent, start, goal; };
 
-// (f, h, row, col) tuple order of paths.py:216/238
-CW_DEV bool heap_less(const AStarCtx& X, const HeapEnt& a, const HeapEnt& b) {
-  if (a.f != b.f) return a.f < b.f;
-  double ha = octile(a.cell / X.nx, a.cell % X.nx, X.gr, X.gc);
-  double hb = octile(b.cell / X.nx, b.cell % X.nx, X.gr, X.gc);
-  if (ha != hb) return ha < hb;
-  return a.cell < b.cell;
+constexpr uint32_t kPosBits = 14, kPosMask = (1u << kPosBits) - 1, kClosed = kPosMask;
+constexpr uint32_t kEpochMax = (1u << (32 - kPosBits)) - 1;
+
+// Open set of the search, scanned by the whole warp.  Pop order must equal the
+// reference's heapq order on (f, h, row, col) (paths.py:216/238).  The lazy heap
+// pops the same sequence of live entries as a decrease-key structure (an improved
+// cell's older entry is stale and skipped; its fresh entry carries the new key),
+// so each cell keeps one entry here.  f and h are non-negative doubles whose IEEE
+// bit patterns order like their values; distinct octile values differ by > 3e-4,
+// so h keeps its top 44 bits and the low 20 bits hold (row << 10 | col), which
+// orders like (row, col).  Key = (f bits, k2) compared as unsigned integers.
+constexpr int kCellBits = 20;
+
+CW_DEV unsigned long long make_k2(double h, int r, int c) {
+  return ((unsigned long long)__double_as_longlong(h) & ~((1ull << kCellBits) - 1ull)) |
+         (unsigned long long)((r << 10) | c);
 }
 
-CW_DEV void heap_push(AStarCtx& X, int& n, HeapEnt v) {
-  int i = n++;
-  while (i > 0) {
-    int p = (i - 1) >> 1;
-    HeapEnt pv = X.heap[p];
-    if (!heap_less(X, v, pv)) break;
-    X.heap[i] = pv;
-    i = p;
-  }
-  X.heap[i] = v;
-}
+CW_DEV bool passbit(const uint32_t* pb, int f) { return (__ldg(pb + (f >> 5)) >> (f & 31)) & 1u; }
 
-CW_DEV HeapEnt heap_pop(AStarCtx& X, int& n) {
-  HeapEnt top = X.heap[0];
-  HeapEnt last = X.heap[--n];
-  int i = 0;
-  while (true) {
-    int l = 2 * i + 1;
-    if (l >= n) break;
-    int r = l + 1;
-    int m = (r < n && heap_less(X, X.heap[r], X.heap[l])) ? r : l;
-    if (!heap_less(X, X.heap[m], last)) break;
-    X.heap[i] = X.heap[m];
-    i = m;
-  }
-  if (n > 0) X.heap[i] = last;
-  return top;
-}
-
-// paths.py:48-87.  Returns the path length in cells (>= 1), 0 when unreachable,
-// -1 on heap overflow.  The path is recovered through X.parent.
-CW_DEV int warp_astar(AStarCtx& X, const uint8_t* lab, int sr, int sc, int lane,
-                      long long& expansions) {
-  const int nx = X.nx, ny = X.ny;
-  auto passable = [&](int r, int c) { return lab[r * nx + c] != L_OBSTACLE; };
-  if (!(passable(sr, sc) && passable(X.gr, X.gc))) return 0;
-  const int start = sr * nx + sc, goal = X.gr * nx + X.gc;
-  int n = 0;  // heap size (lane 0 authoritative, broadcast)
-  if (lane == 0) {
-    X.g[start] = 0.0;
-    X.stamp[start] = X.epoch;
-    X.parent[start] = -1;
-    double h0 = octile(sr, sc, X.gr, X.gc);
-    HeapEnt e0 = {h0, start, 0};
-    heap_push(X, n, e0);
-  }
-  __syncwarp();
-  n = __shfl_sync(0xffffffffu, n, 0);
+// k_astar: persistent warps pull A* requests queued by k_guide and run
+// paths.astar_path (paths.py:48-87) exactly; results go to the agent's path.
+// One warp per CTA; the open list (f bits, k2) lives in shared memory.
+// Unreachable goals (different 4-connected component, see k_reach) return None
+// without searching -- the reference exhausts the component and returns None.
+__global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state S, int smem_cap) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  unsigned long long* OF = reinterpret_cast<unsigned long long*>(sm);
+  unsigned long long* OK = OF + smem_cap;
+  const int lane = threadIdx.x;
+  const int nx = P.nx, ny = P.ny;
+  const size_t N = (size_t)nx * ny;
+  AstarRec* rec = reinterpret_cast<AstarRec*>(S.astar_rec) + (size_t)blockIdx.x * N;
+  const AstarReq* reqs = reinterpret_cast<const AstarReq*>(S.astar_req);
   const int mdr[8] = {-1, 1, 0, 0, -1, -1, 1, 1};
   const int mdc[8] = {0, 0, -1, 1, -1, 1, -1, 1};
-  while (n > 0) {
-    HeapEnt top;
-    if (lane == 0) top = heap_pop(X, n);
-    top.f = __shfl_sync(0xffffffffu, top.f, 0);
-    top.cell = __shfl_sync(0xffffffffu, top.cell, 0);
-    n = __shfl_sync(0xffffffffu, n, 0);
-    const int x = top.cell;
-    if (x == goal) return -2;  // found (caller walks parents)
-    const int r = x / nx, c = x - r * nx;
-    const double gx = X.g[x];
-    if (top.f > gx + octile(r, c, X.gr, X.gc) + 1e-12) continue;
-    ++expansions;
-    bool push = false;
-    double nf = 0.0;
-    int y = -1;
-    if (lane < 8) {
-      int rr = r + mdr[lane], cc = c + mdc[lane];
-      if (rr >= 0 && rr < ny && cc >= 0 && cc < nx && passable(rr, cc) &&
-          (lane < 4 || (passable(r, cc) && passable(rr, c)))) {
-        y = rr * nx + cc;
-        double ng = gx + (lane < 4 ? 1.0 : kSqrt2);
-        double old = X.stamp[y] == X.epoch ? X.g[y] : CUDART_INF;
-        if (ng < old - 1e-12) {
-          X.g[y] = ng;
-          X.stamp[y] = X.epoch;
-          X.parent[y] = x;
-          nf = ng + octile(rr, cc, X.gr, X.gc);
-          push = true;
+  const int cap = min(smem_cap, (int)kClosed);
+  const unsigned lt_mask = (1u << lane) - 1u;
+  long long expansions = 0, t_max = 0, t_sum = 0;
+  while (true) {
+    int q = 0;
+    if (lane == 0) q = atomicAdd(&S.flags[5], 1);
+    q = __shfl_sync(0xffffffffu, q, 0);
+    if (q >= *(volatile int*)&S.flags[4]) break;
+    const long long t0 = clock64();
+    const AstarReq R = reqs[q];
+    const int e = R.env;
+    const uint32_t* pb = S.passbits + (size_t)e * ((N + 31) / 32);
+    const int32_t* reach = S.reach + (size_t)e * N;
+    const int start = R.start, goal = R.goal;
+    const int sr = start / nx, sc = start - sr * nx;
+    const int gr = goal / nx, gc = goal - gr * nx;
+    uint32_t epoch = 0;
+    if (lane == 0) {
+      epoch = (uint32_t)S.astar_epoch[blockIdx.x] + 1u;
+      if (epoch > kEpochMax) epoch = 0;
+      S.astar_epoch[blockIdx.x] = (int)epoch;
+    }
+    epoch = __shfl_sync(0xffffffffu, epoch, 0);
+    if (epoch == 0) {  // tag space exhausted: clear this slot's records once
+      for (size_t k = lane; k < N; k += 32) rec[k].tag = 0u;
+      __syncwarp();
+      epoch = 1;
+      if (lane == 0) S.astar_epoch[blockIdx.x] = 1;
+    }
+    const uint32_t ep = epoch << kPosBits;
+    int found = 0;  // 1 found, 0 none, -1 open-list overflow
+    int n = 0;
+    if (passbit(pb, start) && passbit(pb, goal) && reach[start] == reach[goal]) {
+      if (lane == 0) {
+        const double h0 = octile(sr, sc, gr, gc);
+        AstarRec r0 = {0.0, -1, ep | 0u};
+        rec[start] = r0;
+        OF[0] = (unsigned long long)__double_as_longlong(h0);
+        OK[0] = make_k2(h0, sr, sc);
+      }
+      n = 1;
+      __syncwarp();
+      while (n > 0) {
+        // ---- pop: strided scan + butterfly argmin on (f, k2)
+        unsigned long long bf = ~0ull, bk = ~0ull;
+        int bi = -1;
+        for (int i = lane; i < n; i += 32) {
+          unsigned long long f = OF[i], k = OK[i];
+          if (f < bf || (f == bf && k < bk)) { bf = f; bk = k; bi = i; }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          unsigned long long of = __shfl_xor_sync(0xffffffffu, bf, o);
+          unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
+          int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (of < bf || (of == bf && ok < bk)) { bf = of; bk = ok; bi = oi; }
+        }
+        const int cell20 = (int)(bk & ((1ull << kCellBits) - 1ull));
+        const int r = cell20 >> 10, c = cell20 & 1023;
+        const int x = r * nx + c;
+        __syncwarp();
+        if (lane == 0) {
+          const int last = n - 1;
+          if (bi != last) {
+            unsigned long long lf = OF[last], lk = OK[last];
+            OF[bi] = lf;
+            OK[bi] = lk;
+            int lc = (int)(lk & ((1ull << kCellBits) - 1ull));
+            rec[(lc >> 10) * nx + (lc & 1023)].tag = ep | (uint32_t)bi;
+          }
+          rec[x].tag = ep | kClosed;
+        }
+        __syncwarp();
+        n -= 1;
+        if (x == goal) { found = 1; break; }
+        // the open list holds live entries only, so the reference's stale test
+        // (paths.py:225) cannot fire here
+        const double gx = rec[x].g;
+        ++expansions;
+        bool ins = false, dec = false;
+        unsigned long long nf = 0, nk = 0;
+        int pos = 0, y = 0;
+        if (lane < 8) {
+          int rr = r + mdr[lane], cc = c + mdc[lane];
+          if (rr >= 0 && rr < ny && cc >= 0 && cc < nx) {
+            y = rr * nx + cc;
+            bool ok = passbit(pb, y) && (lane < 4 || (passbit(pb, r * nx + cc) && passbit(pb, rr * nx + c)));
+            if (ok) {
+              AstarRec ry = rec[y];
+              bool live = (ry.tag >> kPosBits) == epoch;
+              double old = live ? ry.g : CUDART_INF;
+              double ng = gx + (lane < 4 ? 1.0 : kSqrt2);
+              if (ng < old - 1e-12) {
+                const double hh = octile(rr, cc, gr, gc);
+                nf = (unsigned long long)__double_as_longlong(ng + hh);
+                nk = make_k2(hh, rr, cc);
+                uint32_t p = live ? (ry.tag & kPosMask) : kClosed;
+                rec[y].g = ng;
+                rec[y].parent = x;
+                if (p == kClosed) ins = true;            // insert / re-open
+                else { dec = true; pos = (int)p; }       // decrease-key in place
+              }
+            }
+          }
+        }
+        __syncwarp();
+        const unsigned im = __ballot_sync(0xffffffffu, ins);
+        if (n + __popc(im) > cap) { found = -1; break; }
+        if (ins) {
+          pos = n + __popc(im & lt_mask);
+          rec[y].tag = ep | (uint32_t)pos;
+        }
+        if (ins || dec) { OF[pos] = nf; OK[pos] = nk; }
+        n += __popc(im);
+        __syncwarp();
+      }
+    }
+    // ---- write the guidance result (field.py:204-212)
+    const size_t ia = (size_t)e * P.A + R.agent;
+    int32_t* cells = S.path_cells + ia * P.path_cap;
+    const double gxw = S.goal[ia * 2], gyw = S.goal[ia * 2 + 1];
+    int pn = 1;
+    double wx = gxw, wy = gyw;
+    if (found == -1 && lane == 0) atomicCAS(&S.flags[1], 0, (int)CW_E_HEAPCAP);
+    if (found == 1) {
+      int L = 0;
+      for (int v = goal; v >= 0; v = rec[v].parent) ++L;
+      if (L >= 2) {
+        if (L - 1 > P.path_cap) {
+          if (lane == 0) atomicCAS(&S.flags[1], 0, (int)CW_E_PATHCAP);
+        } else {
+          if (lane == 0) {
+            int k = L - 2;
+            for (int v = goal; k >= 0; v = rec[v].parent) cells[k--] = v;
+          }
+          __syncwarp();
+          pn = L;
+          int f0 = cells[0];
+          wx = ((double)(f0 % nx) + 0.5) * P.res;
+          wy = ((double)(f0 / nx) + 0.5) * P.res;
         }
       }
     }
-    unsigned m = __ballot_sync(0xffffffffu, push);
-    __syncwarp();
-    for (int k = 0; k < 8; ++k) {
-      if (!((m >> k) & 1u)) continue;
-      double fk = __shfl_sync(0xffffffffu, nf, k);
-      int yk = __shfl_sync(0xffffffffu, y, k);
-      if (lane == 0) {
-        if (n >= X.cap) { n = -1; }
-        else { HeapEnt ev = {fk, yk, 0}; heap_push(X, n, ev); }
-      }
+    if (lane == 0) {
+      S.path_head[ia] = 0;
+      S.path_n[ia] = pn;
+      S.waypoint[ia * 2] = wx;
+      S.waypoint[ia * 2 + 1] = wy;
     }
-    n = __shfl_sync(0xffffffffu, n, 0);
-    if (n < 0) return -1;
+    long long dt = clock64() - t0;
+    t_sum += dt;
+    t_max = max(t_max, dt);
     __syncwarp();
   }
-  return 0;
+  if (lane == 0 && S.counters) {
+    if (expansions) atomicAdd((unsigned long long*)&S.counters[0], (unsigned long long)expansions);
+    if (t_sum) atomicAdd((unsigned long long*)&S.counters[4], (unsigned long long)t_sum);
+    if (t_max) atomicMax((unsigned long long*)&S.counters[5], (unsigned long long)t_max);
+  }
 }
 
-// ---------------------------------------------------------------- the step kernel
-struct StepSmem {
-  // sized dynamically: A * (pos 2 + vel 2 + newpos 2 + radius) doubles + A act bytes
-};
-
+// ---------------------------------------------------------------- guidance pass
 CW_DEV void path_point(const int32_t* cells, int head, int n, int k, double gx, double gy,
                        double res, int nx, double& x, double& y) {
   if (k == n - 1) { x = gx; y = gy; return; }
@@ -351,12 +432,113 @@ CW_DEV void path_point(const int32_t* cells, int head, int n, int k, double gx, 
   y = ((double)r + 0.5) * res;
 }
 
+// k_guide: field.py:165-212 minus the A* itself (queued for k_astar).
 template <int NT>
-__global__ void __launch_bounds__(NT) k_crowd_step(cw_crowd_params P, cw_crowd_state S,
-                                                   const double* __restrict__ robot_pos,
-                                                   const double* __restrict__ robot_vel,
-                                                   double robot_radius,
-                                                   const uint8_t* __restrict__ env_mask) {
+__global__ void __launch_bounds__(NT) k_guide(cw_crowd_params P, cw_crowd_state S,
+                                              const uint8_t* __restrict__ env_mask) {
+  constexpr int NW = NT / 32;
+  const int e = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int A = P.A;
+  const size_t eA = (size_t)e * A;
+  if (env_mask && !env_mask[e]) return;
+  const bool has_obs = S.has_obs[e] != 0;
+  const int nx = P.nx, ny = P.ny;
+  const size_t N = (size_t)nx * ny;
+  const uint8_t* lab = S.labels + e * N;
+  const double res = P.res;
+  long long scanned = 0;
+  AstarReq* reqs = reinterpret_cast<AstarReq*>(S.astar_req);
+  for (int a = wid; a < A; a += NW) {
+    const size_t ia = eA + a;
+    if (!S.active[ia]) continue;
+    const double gx = S.goal[ia * 2], gy = S.goal[ia * 2 + 1];
+    if (!has_obs) {
+      if (lane == 0) { S.waypoint[ia * 2] = gx; S.waypoint[ia * 2 + 1] = gy; }
+      continue;
+    }
+    const double px = S.pos[ia * 2], py = S.pos[ia * 2 + 1];
+    int32_t* cells = S.path_cells + ia * P.path_cap;
+    int head = S.path_head[ia], n = S.path_n[ia];
+    if (n > 0) {
+      double qx, qy;
+      path_point(cells, head, n, 0, gx, gy, res, nx, qx, qy);
+      if (glibc_hypot(qx - px, qy - py) < kWaypointReach && n > 1) { ++head; --n; }
+      // _distance_to_polyline (field.py:613-625) over the remaining points
+      double best = CUDART_INF;
+      if (lane == 0) {
+        path_point(cells, head, n, 0, gx, gy, res, nx, qx, qy);
+        best = glibc_hypot(qx - px, qy - py);
+      }
+      for (int k = 1 + lane; k < n; k += 32) {
+        double ax, ay, bx, by;
+        path_point(cells, head, n, k - 1, gx, gy, res, nx, ax, ay);
+        path_point(cells, head, n, k, gx, gy, res, nx, bx, by);
+        double abx = bx - ax, aby = by - ay;
+        double den = dot2_blas(abx, aby, abx, aby);
+        double t = 0.0;
+        if (!(den < kEps)) t = fmin(fmax(dot2_blas(px - ax, py - ay, abx, aby) / den, 0.0), 1.0);
+        double d = glibc_hypot(ax + t * abx - px, ay + t * aby - py);
+        best = fmin(best, d);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
+      scanned += n;
+      if (best <= kStrayLimit) {
+        double wx, wy;
+        path_point(cells, head, n, 0, gx, gy, res, nx, wx, wy);
+        if (lane == 0) {
+          S.path_head[ia] = head;
+          S.path_n[ia] = n;
+          S.waypoint[ia * 2] = wx;
+          S.waypoint[ia * 2 + 1] = wy;
+        }
+        continue;
+      }
+    }
+    // _line_of_sight (field.py:601-610), warp-parallel over the samples
+    double d = glibc_hypot(gx - px, gy - py);
+    long long ns = max(2LL, trunc_ll(2.0 * d / res) + 2);
+    double step = 1.0 / (double)(ns - 1);
+    bool clear = true;
+    for (long long k = lane; k < ns; k += 32) {
+      double t = k == ns - 1 ? 1.0 : (double)k * step + 0.0;
+      double xs = px + (gx - px) * t, ys = py + (gy - py) * t;
+      long long rr = clampll(trunc_ll(ys / res), 0, ny - 1);
+      long long cc = clampll(trunc_ll(xs / res), 0, nx - 1);
+      if (lab[rr * nx + cc] == L_OBSTACLE) clear = false;
+    }
+    clear = __all_sync(0xffffffffu, clear);
+    if (clear) {
+      if (lane == 0) {
+        S.path_head[ia] = 0;
+        S.path_n[ia] = 1;
+        S.waypoint[ia * 2] = gx;
+        S.waypoint[ia * 2 + 1] = gy;
+      }
+      continue;
+    }
+    if (lane == 0) {
+      int sr = (int)fmin(fmax(py / res, 0.0), (double)(ny - 1));
+      int sc = (int)fmin(fmax(px / res, 0.0), (double)(nx - 1));
+      int gr = (int)fmin(fmax(gy / res, 0.0), (double)(ny - 1));
+      int gc = (int)fmin(fmax(gx / res, 0.0), (double)(nx - 1));
+      int q = atomicAdd(&S.flags[4], 1);
+      AstarReq R = {e, a, sr * nx + sc, gr * nx + gc};
+      reqs[q] = R;
+    }
+  }
+  if (lane == 0 && scanned && S.counters)
+    atomicAdd((unsigned long long*)&S.counters[1], (unsigned long long)scanned);
+}
+
+// ---------------------------------------------------------------- ORCA + commit
+template <int NT>
+__global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S,
+                                             const double* __restrict__ robot_pos,
+                                             const double* __restrict__ robot_vel,
+                                             double robot_radius,
+                                             const uint8_t* __restrict__ env_mask) {
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char sm[];
   const int e = blockIdx.x;
@@ -373,7 +555,7 @@ __global__ void __launch_bounds__(NT) k_crowd_step(cw_crowd_params P, cw_crowd_s
   uint8_t* s_act = reinterpret_cast<uint8_t*>(s_cons + NW);
   __shared__ double s_gap[NW];
   __shared__ int s_anynb[NW];
-
+  const long long t_cta0 = clock64();
   const size_t eA = (size_t)e * A;
   const bool emask = env_mask ? env_mask[e] != 0 : true;
   for (int a = threadIdx.x; a < A; a += NT) {
@@ -387,7 +569,6 @@ __global__ void __launch_bounds__(NT) k_crowd_step(cw_crowd_params P, cw_crowd_s
     s_act[a] = (S.active[eA + a] && emask) ? 1 : 0;
   }
   __syncthreads();
-
   const int nx = P.nx, ny = P.ny;
   const size_t N = (size_t)nx * ny;
   const uint8_t* lab = S.labels + e * N;
@@ -402,121 +583,13 @@ __global__ void __launch_bounds__(NT) k_crowd_step(cw_crowd_params P, cw_crowd_s
   WarpCons& C = s_cons[wid];
   double my_gap = CUDART_INF;
   int my_anynb = 0;
-  long long exp_count = 0, scanned = 0, fallbacks = 0, stalls = 0;
-  const int slot = e * P.slots_per_env + wid;
-  AStarCtx X;
-  X.g = S.astar_g + (size_t)slot * N;
-  X.parent = S.astar_parent + (size_t)slot * N;
-  X.stamp = S.astar_stamp + (size_t)slot * N;
-  X.heap = reinterpret_cast<HeapEnt*>(S.astar_heap) + (size_t)slot * P.heap_cap;
-  X.cap = P.heap_cap;
-  X.nx = nx;
-  X.ny = ny;
-
+  long long fallbacks = 0, stalls = 0;
   for (int a = wid; a < A; a += NW) {
     if (!s_act[a]) continue;
     const double px = s_px[a], py = s_py[a];
     const size_t ia = eA + a;
     const double gx = S.goal[ia * 2], gy = S.goal[ia * 2 + 1];
-    double wx, wy;
-    // ---------------- guidance (field.py:165-212)
-    if (!has_obs) {
-      wx = gx; wy = gy;
-    } else {
-      int32_t* cells = S.path_cells + ia * P.path_cap;
-      int head = S.path_head[ia], n = S.path_n[ia];
-      bool have = false;
-      if (n > 0) {
-        double qx, qy;
-        path_point(cells, head, n, 0, gx, gy, res, nx, qx, qy);
-        if (glibc_hypot(qx - px, qy - py) < kWaypointReach && n > 1) { ++head; --n; }
-        // _distance_to_polyline over the remaining points
-        double best = CUDART_INF;
-        if (lane == 0) {
-          path_point(cells, head, n, 0, gx, gy, res, nx, qx, qy);
-          best = glibc_hypot(qx - px, qy - py);
-        }
-        for (int k = 1 + lane; k < n; k += 32) {
-          double ax, ay, bx, by;
-          path_point(cells, head, n, k - 1, gx, gy, res, nx, ax, ay);
-          path_point(cells, head, n, k, gx, gy, res, nx, bx, by);
-          double abx = bx - ax, aby = by - ay;
-          double den = dot2_blas(abx, aby, abx, aby);
-          double t = 0.0;
-          if (!(den < kEps)) t = fmin(fmax(dot2_blas(px - ax, py - ay, abx, aby) / den, 0.0), 1.0);
-          double d = glibc_hypot(ax + t * abx - px, ay + t * aby - py);
-          best = fmin(best, d);
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
-        scanned += n;
-        if (best <= kStrayLimit) {
-          path_point(cells, head, n, 0, gx, gy, res, nx, wx, wy);
-          have = true;
-        }
-      }
-      if (!have) {
-        // _line_of_sight(passable, pos, goal)
-        double d = glibc_hypot(gx - px, gy - py);
-        long long ns = max(2LL, trunc_ll(2.0 * d / res) + 2);
-        double step = 1.0 / (double)(ns - 1);
-        bool clear = true;
-        for (long long k = lane; k < ns; k += 32) {
-          double t = k == ns - 1 ? 1.0 : (double)k * step + 0.0;
-          double xs = px + (gx - px) * t, ys = py + (gy - py) * t;
-          long long rr = clampll(trunc_ll(ys / res), 0, ny - 1);
-          long long cc = clampll(trunc_ll(xs / res), 0, nx - 1);
-          if (lab[rr * nx + cc] == L_OBSTACLE) clear = false;
-        }
-        clear = __all_sync(0xffffffffu, clear);
-        bool one_point = true;
-        if (!clear) {
-          int sr = (int)fmin(fmax(py / res, 0.0), (double)(ny - 1));
-          int sc = (int)fmin(fmax(px / res, 0.0), (double)(nx - 1));
-          X.gr = (int)fmin(fmax(gy / res, 0.0), (double)(ny - 1));
-          X.gc = (int)fmin(fmax(gx / res, 0.0), (double)(nx - 1));
-          if (lane == 0) X.epoch = ++S.astar_epoch[slot];
-          X.epoch = __shfl_sync(0xffffffffu, X.epoch, 0);
-          int res_code = warp_astar(X, lab, sr, sc, lane, exp_count);
-          if (res_code == -1) {
-            if (lane == 0) atomicCAS(&S.flags[1], 0, (int)CW_E_HEAPCAP);
-          } else if (res_code == -2) {
-            // walk parents goal -> start; L = path length in cells
-            const int goal_cell = X.gr * nx + X.gc;
-            int L = 0;
-            for (int v = goal_cell; v >= 0; v = X.parent[v]) ++L;
-            if (L >= 2) {
-              if (L - 1 > P.path_cap) {
-                if (lane == 0) atomicCAS(&S.flags[1], 0, (int)CW_E_PATHCAP);
-              } else {
-                if (lane == 0) {
-                  int k = L - 2;
-                  for (int v = goal_cell; k >= 0; v = X.parent[v]) cells[k--] = v;
-                }
-                __syncwarp();
-                head = 0;
-                n = L;  // L-1 cells + the goal point
-                one_point = false;
-                path_point(cells, head, n, 0, gx, gy, res, nx, wx, wy);
-              }
-            }
-          }
-        }
-        if (one_point) {
-          head = 0;
-          n = 1;
-          wx = gx; wy = gy;
-        }
-      }
-      if (lane == 0) {
-        S.path_head[ia] = head;
-        S.path_n[ia] = n;
-      }
-    }
-    if (lane == 0) {
-      S.waypoint[ia * 2] = wx;
-      S.waypoint[ia * 2 + 1] = wy;
-    }
+    const double wx = S.waypoint[ia * 2], wy = S.waypoint[ia * 2 + 1];
     // ---------------- preferred velocity (field.py:214-227)
     const double sp = S.pref_speed[ia];
     double tw0 = wx - px, tw1 = wy - py;
@@ -572,8 +645,7 @@ __global__ void __launch_bounds__(NT) k_crowd_step(cw_crowd_params P, cw_crowd_s
       vo_halfplane(rp0, rp1, rv0, rv1, rr, P.time_horizon, P.dt, vxa, vya, 0.5, C.px[lane],
                    C.py[lane], C.nx[lane], C.ny[lane]);
       if (lane == 0) {
-        // per-env nearest separation gap (field.py:268-271)
-        double d_near = sqrt(rp0 * rp0 + rp1 * rp1);
+        double d_near = sqrt(rp0 * rp0 + rp1 * rp1);   // field.py:268-271
         my_gap = fmin(my_gap, d_near - (ra + s_r[j]));
         my_anynb = 1;
       }
@@ -675,12 +747,16 @@ __global__ void __launch_bounds__(NT) k_crowd_step(cw_crowd_params P, cw_crowd_s
     }
   }
   if (lane == 0 && S.counters) {
-    if (exp_count) atomicAdd((unsigned long long*)&S.counters[0], (unsigned long long)exp_count);
-    if (scanned) atomicAdd((unsigned long long*)&S.counters[1], (unsigned long long)scanned);
     if (fallbacks) atomicAdd((unsigned long long*)&S.counters[2], (unsigned long long)fallbacks);
     if (stalls) atomicAdd((unsigned long long*)&S.counters[3], (unsigned long long)stalls);
   }
-  // ---------------- last CTA publishes last_gap_by_env (only when any row had K > 0)
+  if (threadIdx.x == 0 && S.counters) {
+    long long tc = clock64() - t_cta0;
+    atomicAdd((unsigned long long*)&S.counters[6], (unsigned long long)tc);
+    atomicMax((unsigned long long*)&S.counters[7], (unsigned long long)tc);
+  }
+  // ---------------- last CTA: publish last_gap_by_env (only when some row had K > 0),
+  // reset the per-step flags and the A* queue
   if (threadIdx.x == 0) {
     __threadfence();
     int ticket = atomicAdd(&S.flags[2], 1);
@@ -691,6 +767,8 @@ __global__ void __launch_bounds__(NT) k_crowd_step(cw_crowd_params P, cw_crowd_s
       }
       S.flags[0] = 0;
       S.flags[2] = 0;
+      S.flags[4] = 0;
+      S.flags[5] = 0;
     }
   }
 }
@@ -709,6 +787,19 @@ __global__ void k_child_seeds(int n, const uint64_t* __restrict__ parent, int la
   else out[i] = child_seed(parent[i], labels[label_id]);
 }
 
+template <int NT>
+static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const double* rp,
+                       const double* rv, double rr, const uint8_t* em, cudaStream_t st) {
+  size_t sm = cw_crowd_step_smem_bytes(P.A, NT);
+  if (sm > 48 * 1024)
+    cudaFuncSetAttribute(k_orca<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_guide<NT><<<P.E, NT, 0, st>>>(P, S, em);
+  const int cap = astar_smem_entries();
+  k_astar<<<P.astar_ctas, 32, (size_t)cap * 16, st>>>(P, S, cap);
+  k_orca<NT><<<P.E, NT, sm, st>>>(P, S, rp, rv, rr, em);
+  return (int)cudaGetLastError();
+}
+
 }  // namespace cw
 
 extern "C" {
@@ -717,29 +808,25 @@ size_t cw_crowd_step_smem_bytes(int A, int nt) {
   return (size_t)A * 7 * sizeof(double) + (size_t)(nt / 32) * sizeof(cw::WarpCons) + (size_t)A + 16;
 }
 
-// One two-phase tick of every env (field.py:90-163).  robot_pos/robot_vel
-// (E,2) may be NULL; env_mask (E) may be NULL.  Stream-ordered, no host sync.
+int cw_astar_smem_entries(void) { return cw::astar_smem_entries(); }
+
+// One two-phase tick of every env (field.py:90-163): k_guide -> k_astar -> k_orca,
+// stream-ordered.  robot_pos/robot_vel (E,2) may be NULL; env_mask (E) may be NULL.
 int cw_crowd_step(const cw_crowd_params* P, const cw_crowd_state* S, const double* robot_pos,
                   const double* robot_vel, double robot_radius, const uint8_t* env_mask,
                   int threads, void* stream) {
   using namespace cw;
   if (P->E <= 0 || P->A <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
-  size_t sm = cw_crowd_step_smem_bytes(P->A, threads);
-  if (threads == 128) {
-    if (sm > 48 * 1024)
-      cudaFuncSetAttribute(k_crowd_step<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_crowd_step<128><<<P->E, 128, sm, st>>>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask);
-  } else if (threads == 256) {
-    if (sm > 48 * 1024)
-      cudaFuncSetAttribute(k_crowd_step<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_crowd_step<256><<<P->E, 256, sm, st>>>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask);
-  } else {
-    if (sm > 48 * 1024)
-      cudaFuncSetAttribute(k_crowd_step<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_crowd_step<64><<<P->E, 64, sm, st>>>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_astar, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         astar_smem_entries() * 16);
+    attr = true;
   }
-  return (int)cudaGetLastError();
+  if (threads == 256) return launch_step<256>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, st);
+  if (threads == 64) return launch_step<64>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, st);
+  return launch_step<128>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, st);
 }
 
 // PCG64 stream states from integer seeds (numpy PCG64(seed) via SeedSequence).
@@ -758,9 +845,6 @@ int cw_child_seeds(int n, const uint64_t* parent, int label_id, const uint64_t* 
   return (int)cudaGetLastError();
 }
 
-}  // extern "C"
-
-extern "C" {
 // ABI self-check for the ctypes mirror (host-only; no device work).
 int cw_abi_sizes(size_t* out, int n) {
   const size_t v[4] = {sizeof(cw_scene_params), sizeof(cw_scene_buffers), sizeof(cw_crowd_params),
@@ -768,4 +852,5 @@ int cw_abi_sizes(size_t* out, int n) {
   for (int i = 0; i < n && i < 4; ++i) out[i] = v[i];
   return 4;
 }
-}
+
+}  // extern "C"

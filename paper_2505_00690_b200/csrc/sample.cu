@@ -99,6 +99,43 @@ CW_DEV unsigned long long block_min_u64(unsigned long long v, unsigned long long
   return r;
 }
 
+// ----------------------------------------------------------------- union-find
+// Lock-free union-find over a CTA's grid (ECL-CC style): parents always point to
+// smaller indices, so stale reads are still ancestors.  Labels are only ever
+// compared for equality (routes.py:62/74 components, A* reachability).
+CW_DEV int uf_find(volatile int32_t* par, int x) {
+  int cur = par[x];
+  if (cur != x) {
+    int prev = x, next;
+    while (cur > (next = par[cur])) {
+      par[prev] = next;
+      prev = cur;
+      cur = next;
+    }
+  }
+  return cur;
+}
+
+// read-only root lookup for the final labelling pass (no compression writes,
+// so a finished label is never overwritten by another thread's path halving)
+CW_DEV int uf_root(volatile int32_t* par, int x) {
+  int next;
+  while (x > (next = par[x])) x = next;
+  return x;
+}
+
+CW_DEV void uf_union(volatile int32_t* par, int a, int b) {
+  a = uf_find(par, a);
+  b = uf_find(par, b);
+  while (a != b) {
+    if (a < b) { int t = a; a = b; b = t; }
+    int old = atomicCAS((int32_t*)&par[a], a, b);
+    if (old == a) return;
+    a = uf_find(par, old);
+    b = uf_find(par, b);
+  }
+}
+
 // ================================================================= k_seeds
 __global__ void k_seeds(int E, const uint64_t* __restrict__ scene_seed,
                         const uint64_t* __restrict__ crowd_seed, EnvSeeds* __restrict__ out) {
@@ -1159,26 +1196,56 @@ __global__ void __launch_bounds__(BFS_NT) k_nearest(cw_scene_params P, int E, co
   }
 }
 
-// ================================================================= walkable list
+// ================================================================= walkable list + passable bits
 __global__ void __launch_bounds__(1024) k_walk(cw_scene_params P, int E, const int32_t* slots,
                                                cw_scene_buffers B) {
   const int e = blockIdx.x;
   const int slot = env_slot(slots, e);
   if (B.status[slot] != CW_OK) return;
   const int N = P.nx * P.ny;
+  const int NW32 = (N + 31) / 32;
   const uint8_t* Lb = B.labels + (size_t)slot * N;
   int32_t* W = B.walk + (size_t)slot * N;
+  uint32_t* PB = B.passbits + (size_t)slot * NW32;
   __shared__ int sh[1024 / 32 + 1];
   int base = 0;
   for (int f0 = 0; f0 < N; f0 += 1024) {
     int f = f0 + threadIdx.x;
-    int wk = f < N && Lb[f] == L_WALKABLE;
+    uint8_t lb = f < N ? Lb[f] : L_OBSTACLE;
+    int wk = f < N && lb == L_WALKABLE;
+    unsigned pm = __ballot_sync(0xffffffffu, f < N && lb != L_OBSTACLE);
+    if ((threadIdx.x & 31) == 0 && f < N) PB[f >> 5] = pm;
     int tot;
     int off = block_excl_scan<1024>(wk, sh, tot);
     if (wk) W[base + off] = f;
     base += tot;
   }
   if (threadIdx.x == 0) B.walk_n[slot] = base;
+}
+
+// 4-connected components of passable cells.  The A* move set (paths.py:14-19,
+// 70-72: diagonals only when both orthogonal cells are passable) connects
+// exactly the 4-connected components, so reach[start] != reach[goal] <=> the
+// search returns None.
+__global__ void __launch_bounds__(1024) k_reach(cw_scene_params P, int E, const int32_t* slots,
+                                                cw_scene_buffers B) {
+  const int e = blockIdx.x;
+  const int slot = env_slot(slots, e);
+  if (B.status[slot] != CW_OK) return;
+  const int nx = P.nx, N = nx * P.ny;
+  const uint8_t* Lb = B.labels + (size_t)slot * N;
+  volatile int32_t* R = B.reach + (size_t)slot * N;
+  for (int f = threadIdx.x; f < N; f += 1024) R[f] = Lb[f] != L_OBSTACLE ? f : -1;
+  __syncthreads();
+  for (int f = threadIdx.x; f < N; f += 1024) {
+    if (Lb[f] == L_OBSTACLE) continue;
+    int c = f % nx;
+    if (c + 1 < nx && Lb[f + 1] != L_OBSTACLE) uf_union(R, f, f + 1);
+    if (f + nx < N && Lb[f + nx] != L_OBSTACLE) uf_union(R, f, f + nx);
+  }
+  __syncthreads();
+  for (int f = threadIdx.x; f < N; f += 1024)
+    if (R[f] >= 0) R[f] = uf_root(R, f);
 }
 
 // ================================================================= spawn + routes
@@ -1210,7 +1277,7 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
   int32_t* cand = comp + N;       // candidate flat indices (row-major)
   int32_t* perm = cand + N;
   __shared__ int sh[SP_NT / 32 + 1];
-  __shared__ int s_n, s_changed, s_idx, s_cnt, s_rank, s_j, s_acc, s_k, s_fail;
+  __shared__ int s_n, s_idx, s_rank, s_j, s_acc, s_k;
   __shared__ unsigned long long s_seed;
   __shared__ double s_maxr;
   extern __shared__ __align__(16) unsigned char sp_smem[];
@@ -1253,36 +1320,24 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
     if (threadIdx.x == 0) B.status[slot] = CW_E_NOROUTE;
     return;
   }
-  // 8-connected components: min-label propagation + pointer jumping.  Only
-  // label equality is used downstream (routes.py:62, 74), so any labelling works.
-  while (true) {
-    if (threadIdx.x == 0) s_changed = 0;
-    __syncthreads();
-    int ch = 0;
+  // 8-connected components (routes.py:14-32) by union-find; only label
+  // equality is used downstream (routes.py:62, 74), so any labelling works.
+  {
+    volatile int32_t* C = comp;
     for (int q = threadIdx.x; q < n; q += SP_NT) {
       int f = cand[q], r = f / nx, c = f - r * nx;
-      int m = comp[f];
-      for (int dr = -1; dr <= 1; ++dr)
-        for (int dc = -1; dc <= 1; ++dc) {
-          int rr = r + dr, cc = c + dc;
-          if ((dr || dc) && rr >= 0 && rr < ny && cc >= 0 && cc < nx) {
-            int o = comp[rr * nx + cc];
-            if (o >= 0 && o < m) m = o;
-          }
-        }
-      if (m < comp[f]) {
-        atomicMin(&comp[f], m);
-        ch = 1;
+      const int dr[4] = {0, 1, 1, 1}, dc[4] = {1, -1, 0, 1};
+      for (int k = 0; k < 4; ++k) {
+        int rr = r + dr[k], cc = c + dc[k];
+        if (rr < ny && cc >= 0 && cc < nx && C[rr * nx + cc] >= 0) uf_union(C, f, rr * nx + cc);
       }
     }
     __syncthreads();
     for (int q = threadIdx.x; q < n; q += SP_NT) {
       int f = cand[q];
-      int c = comp[f];
-      while (comp[c] < c) c = comp[c];
-      if (c < comp[f]) atomicMin(&comp[f], c);
+      C[f] = uf_root(C, f);
     }
-    if (__syncthreads_or(ch) == 0) break;
+    __syncthreads();
   }
   // permutation(n): Fisher-Yates from the top with masked rejection (numpy shuffle)
   if (threadIdx.x == 0) {
@@ -1311,7 +1366,6 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
     if (threadIdx.x == 0) {
       s_idx = perm[s_k];
       s_k += 1;
-      s_fail = 0;
     }
     __syncthreads();
     const int fs = cand[s_idx];
@@ -1411,6 +1465,7 @@ int cw_sample_scenes(const cw_scene_params* P, int E, const uint64_t* scene_seed
   if (p.obj_max > 0) k_footprint<<<dim3((p.obj_max + 3) / 4, E), 128, 0, st>>>(p, E, slots, b);
   k_nearest<<<E, BFS_NT, 0, st>>>(p, E, slots, b);
   k_walk<<<E, 1024, 0, st>>>(p, E, slots, b);
+  k_reach<<<E, 1024, 0, st>>>(p, E, slots, b);
   if (p.peds > 0) {
     size_t sm = (size_t)p.peds * 2 * sizeof(double) + sizeof(Pcg64Raw);
     k_spawn<<<E, SP_NT, sm, st>>>(p, E, slots, S, b);
@@ -1441,6 +1496,7 @@ int cw_prepare_envs(const cw_scene_params* P, int E, const int32_t* slots,
   cudaStream_t st = (cudaStream_t)stream;
   k_nearest<<<E, BFS_NT, 0, st>>>(*P, E, slots, *B);
   k_walk<<<E, 1024, 0, st>>>(*P, E, slots, *B);
+  k_reach<<<E, 1024, 0, st>>>(*P, E, slots, *B);
   return (int)cudaGetLastError();
 }
 
