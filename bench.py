@@ -174,6 +174,25 @@ def run_ours(args):
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     t_ms = float(sum(step_ms))
     counters = f.stats()
+    # ---- per-kernel pass (same stream, events between the three launches)
+    n_ph = min(args.steps, args.phase_steps)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_ph)]
+    f.counters_t.zero_()
+    torch.cuda.synchronize()
+    for k in range(n_ph):
+        flush.fill_(float(k))
+        ev[k][0].record(st)
+        f.step_phase(1, rpos, rvel, 0.35)
+        ev[k][1].record(st)
+        f.step_phase(2, rpos, rvel, 0.35)
+        ev[k][2].record(st)
+        f.step_phase(4, rpos, rvel, 0.35)
+        ev[k][3].record(st)
+    torch.cuda.synchronize()
+    f.check_flags()
+    ph_ms = np.array([[ev[k][i].elapsed_time(ev[k][i + 1]) for i in range(3)] for k in range(n_ph)])
+    ph_avg = ph_ms.mean(0)
+    ph_counters = f.stats()
     # ---- e2e through the public API with host buffers (pinned H2D in, D2H pos/vel out)
     rpos_h = rpos.cpu().pin_memory()
     rvel_h = rvel.cpu().pin_memory()
@@ -208,12 +227,24 @@ def run_ours(args):
         env_steps = E * world * steps
         value = env_steps / (t_ms / 1e3)
         scenes = E * world / (sample_ms / 1e3)
-        # roofline: algorithmic bytes of the dynamics kernel:
-        #   74 B per active agent-step + 8 B per path point scanned + 20 B per env-step (robot)
+        # roofline.  Whole dynamics step, SURVEY §8d byte model: 74 B per active
+        # agent-step + 8 B per guidance path point scanned + 20 B per env-step (robot).
         bytes_step = (74.0 * active + 20.0 * E) + 8.0 * counters["path_points_scanned"] / steps
         avg_ms = t_ms / steps
         achieved = bytes_step / (avg_ms / 1e3) / 1e9
         peak, src = peaks()
+        # per kernel (dominant one reported as `roofline`): k_guide = the §8d guidance
+        # share (pos/goal/waypoint 40 B per agent + 8 B per path point); k_astar = 80 B
+        # per expansion (8 neighbour g + passable, popped g); k_orca = the rest of §8d.
+        exp_step = ph_counters["astar_expansions"] / n_ph
+        scan_step = ph_counters["path_points_scanned"] / n_ph
+        kb = {"k_guide": 40.0 * active + 8.0 * scan_step,
+              "k_astar": 80.0 * exp_step,
+              "k_orca": 34.0 * active + 20.0 * E}
+        names = ["k_guide", "k_astar", "k_orca"]
+        dom = names[int(np.argmax(ph_avg))]
+        dom_ms = float(ph_avg[names.index(dom)])
+        dom_ach = kb[dom] / (dom_ms / 1e3) / 1e9
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "env-steps/s",
             "n_gpus": world, "steps": steps, "warmup": args.warmup,
@@ -229,11 +260,17 @@ def run_ours(args):
             "e2e": {"value": round(E * world * e2e_steps / e2e_s, 1), "unit": "env-steps/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "steps": e2e_steps},
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 5), "traffic": None,
-                         "kernel": "k_crowd_step", "peak_source": src,
-                         "bytes_per_launch": round(bytes_step, 1)},
-            "gpu_launches": steps,
+            "roofline": {"bound": "hbm", "achieved": round(dom_ach, 3), "peak": peak, "unit": "GB/s",
+                         "frac": round(dom_ach / peak, 7), "traffic": args.traffic,
+                         "kernel": dom, "peak_source": src, "bytes_per_launch": round(kb[dom], 1),
+                         "avg_launch_ms": round(dom_ms, 4),
+                         "note": "latency-bound serial search; see profiles/"},
+            "roofline_step": {"bound": "hbm", "achieved": round(achieved, 3), "peak": peak, "unit": "GB/s",
+                              "frac": round(achieved / peak, 7), "bytes_per_step": round(bytes_step, 1),
+                              "model": "SURVEY 8d: 74 B/agent-step + 8 B/path point + 20 B/env-step"},
+            "kernels_ms": {n: round(float(v), 4) for n, v in zip(names, ph_avg)},
+            "kernels_share": {n: round(float(v / ph_avg.sum()), 4) for n, v in zip(names, ph_avg)},
+            "gpu_launches": 3 * steps,
             "clocks": clk.summary(),
             "counters": counters,
             "stats": {"min_gap": float(torch.nan_to_num(stats[:, 0], posinf=1e9).min()),
@@ -339,6 +376,9 @@ def main():
     ap.add_argument("--sample-reps", type=int, default=3)
     ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--phase-steps", type=int, default=100)
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="dram bytes per launch of the dominant kernel from an ncu --set full capture")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

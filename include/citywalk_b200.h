@@ -146,6 +146,13 @@ int cw_crowd_step(const cw_crowd_params* params, const cw_crowd_state* state,
                   const double* robot_pos, const double* robot_vel, double robot_radius,
                   const uint8_t* env_mask, int threads, void* stream);
 
+/* The same tick as cw_crowd_step, one phase at a time (bit 0 k_guide, bit 1
+ * k_astar, bit 2 k_orca); running 1, 2, 4 in order equals one cw_crowd_step.
+ * Lets a caller time each kernel with events on its stream. */
+int cw_crowd_step_phases(const cw_crowd_params* params, const cw_crowd_state* state,
+                         const double* robot_pos, const double* robot_vel, double robot_radius,
+                         const uint8_t* env_mask, int threads, int phases, void* stream);
+
 /* k_astar open-list entries held in shared memory (host-only query). */
 int cw_astar_smem_entries(void);
 

@@ -335,6 +335,16 @@ class CrowdField:
         if check:
             self.check_flags()
 
+    def step_phase(self, phase, robot_pos=None, robot_vel=None, robot_radius=0.35, env_mask=None,
+                   stream=None):
+        """Launch one phase of the tick (1 guide, 2 A*, 4 ORCA+commit); device inputs only."""
+        if not hasattr(self, "_p") or self._p.A != self.A:
+            self.prepare_step()
+        err = _lib.lib().cw_crowd_step_phases(self._p, self._s, _lib.ptr(robot_pos), _lib.ptr(robot_vel),
+                                              float(robot_radius), _lib.ptr(env_mask), self.threads,
+                                              int(phase), _lib.stream_ptr(stream))
+        _lib.check(err, "cw_crowd_step_phases")
+
     def check_flags(self):
         code = int(self.flags_t[1].item())
         if code:

@@ -789,14 +789,17 @@ __global__ void k_child_seeds(int n, const uint64_t* __restrict__ parent, int la
 
 template <int NT>
 static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const double* rp,
-                       const double* rv, double rr, const uint8_t* em, cudaStream_t st) {
+                       const double* rv, double rr, const uint8_t* em, int phases,
+                       cudaStream_t st) {
   size_t sm = cw_crowd_step_smem_bytes(P.A, NT);
-  if (sm > 48 * 1024)
+  if ((phases & 4) && sm > 48 * 1024)
     cudaFuncSetAttribute(k_orca<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_guide<NT><<<P.E, NT, 0, st>>>(P, S, em);
-  const int cap = astar_smem_entries();
-  k_astar<<<P.astar_ctas, 32, (size_t)cap * 16, st>>>(P, S, cap);
-  k_orca<NT><<<P.E, NT, sm, st>>>(P, S, rp, rv, rr, em);
+  if (phases & 1) k_guide<NT><<<P.E, NT, 0, st>>>(P, S, em);
+  if (phases & 2) {
+    const int cap = astar_smem_entries();
+    k_astar<<<P.astar_ctas, 32, (size_t)cap * 16, st>>>(P, S, cap);
+  }
+  if (phases & 4) k_orca<NT><<<P.E, NT, sm, st>>>(P, S, rp, rv, rr, em);
   return (int)cudaGetLastError();
 }
 
@@ -812,9 +815,9 @@ int cw_astar_smem_entries(void) { return cw::astar_smem_entries(); }
 
 // One two-phase tick of every env (field.py:90-163): k_guide -> k_astar -> k_orca,
 // stream-ordered.  robot_pos/robot_vel (E,2) may be NULL; env_mask (E) may be NULL.
-int cw_crowd_step(const cw_crowd_params* P, const cw_crowd_state* S, const double* robot_pos,
-                  const double* robot_vel, double robot_radius, const uint8_t* env_mask,
-                  int threads, void* stream) {
+int cw_crowd_step_phases(const cw_crowd_params* P, const cw_crowd_state* S,
+                         const double* robot_pos, const double* robot_vel, double robot_radius,
+                         const uint8_t* env_mask, int threads, int phases, void* stream) {
   using namespace cw;
   if (P->E <= 0 || P->A <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
@@ -824,9 +827,18 @@ int cw_crowd_step(const cw_crowd_params* P, const cw_crowd_state* S, const doubl
                          astar_smem_entries() * 16);
     attr = true;
   }
-  if (threads == 256) return launch_step<256>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, st);
-  if (threads == 64) return launch_step<64>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, st);
-  return launch_step<128>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, st);
+  if (threads == 256)
+    return launch_step<256>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, phases, st);
+  if (threads == 64)
+    return launch_step<64>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, phases, st);
+  return launch_step<128>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, phases, st);
+}
+
+int cw_crowd_step(const cw_crowd_params* P, const cw_crowd_state* S, const double* robot_pos,
+                  const double* robot_vel, double robot_radius, const uint8_t* env_mask,
+                  int threads, void* stream) {
+  return cw_crowd_step_phases(P, S, robot_pos, robot_vel, robot_radius, env_mask, threads, 7,
+                              stream);
 }
 
 // PCG64 stream states from integer seeds (numpy PCG64(seed) via SeedSequence).
