@@ -180,6 +180,29 @@ CW_DEV Pcg64 pcg_seed(uint64_t entropy) {
 // make_rng(seed, label) (src/rng.py:22-26)
 CW_DEV Pcg64 make_rng(uint64_t seed, const char* label) { return pcg_seed(child_seed(seed, label)); }
 
+// LCG jump-ahead by `delta` steps (numpy pcg64 advance: Brown's algorithm).
+CW_DEV void pcg_jump_coeffs(u128 delta, u128& mult, u128& plus, u128 inc) {
+  u128 acc_m = 1, acc_p = 0, cur_m = pcg_mult(), cur_p = inc;
+  while (delta > 0) {
+    if (delta & 1) {
+      acc_m *= cur_m;
+      acc_p = acc_p * cur_m + cur_p;
+    }
+    cur_p = (cur_m + 1) * cur_p;
+    cur_m *= cur_m;
+    delta >>= 1;
+  }
+  mult = acc_m;
+  plus = acc_p;
+}
+
+CW_DEV uint64_t xsl_rr(u128 state) {
+  uint64_t hi = (uint64_t)(state >> 64), lo = (uint64_t)state;
+  uint64_t x = hi ^ lo;
+  unsigned rot = (unsigned)(hi >> 58);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
 CW_DEV uint64_t next64(Pcg64& p) {
   p.state = p.state * pcg_mult() + p.inc;
   uint64_t hi = (uint64_t)(p.state >> 64), lo = (uint64_t)p.state;

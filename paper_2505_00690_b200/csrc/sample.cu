@@ -136,6 +136,51 @@ CW_DEV void uf_union(volatile int32_t* par, int a, int b) {
   }
 }
 
+// Connected components of the cells with ok(f) on an nx*ny grid: each row's
+// runs become stars first (no atomics), then only runs of adjacent rows are
+// united (once per overlap segment), then a read-only root pass labels cells.
+// par[f] ends as the smallest cell index of f's component (-1 where !ok).
+template <int NT, bool CONN8, typename OkF>
+CW_DEV void grid_components(volatile int32_t* par, int nx, int ny, OkF ok) {
+  const int N = nx * ny;
+  for (int r = threadIdx.x; r < ny; r += NT) {
+    int start = -1;
+    for (int c = 0; c < nx; ++c) {
+      int f = r * nx + c;
+      if (ok(f)) {
+        if (start < 0) start = f;
+        par[f] = start;
+      } else {
+        start = -1;
+        par[f] = -1;
+      }
+    }
+  }
+  __syncthreads();
+  for (int f = threadIdx.x; f < N - nx; f += NT) {
+    if (!ok(f)) continue;
+    const int c = f % nx;
+    const bool left = c > 0 && ok(f - 1);
+    if (!CONN8) {
+      const int g = f + nx;
+      if (ok(g) && !(left && ok(g - 1))) uf_union(par, f, g);
+    } else {
+      for (int d = -1; d <= 1; ++d) {
+        const int cc = c + d;
+        if (cc < 0 || cc >= nx) continue;
+        const int g = f + nx + d;
+        if (!ok(g)) continue;
+        if (left && cc - 1 >= 0 && ok(g - 1)) continue;  // united at (f-1, g-1)
+        uf_union(par, f, g);
+      }
+    }
+  }
+  __syncthreads();
+  for (int f = threadIdx.x; f < N; f += NT)
+    if (par[f] >= 0) par[f] = uf_root(par, f);
+  __syncthreads();
+}
+
 // ================================================================= k_seeds
 __global__ void k_seeds(int E, const uint64_t* __restrict__ scene_seed,
                         const uint64_t* __restrict__ crowd_seed, EnvSeeds* __restrict__ out) {
@@ -1126,7 +1171,7 @@ __global__ void __launch_bounds__(BFS_NT) k_nearest(cw_scene_params P, int E, co
   const int nx = P.nx, ny = P.ny, N = nx * ny;
   const uint8_t* Lb = B.labels + (size_t)slot * N;
   int32_t* near = B.nearest + (size_t)slot * N;
-  int32_t* owner = B.scratch_i32 + (size_t)e * 3 * N;
+  int32_t* owner = B.scratch_i32 + (size_t)e * 7 * N;
   int32_t* Q = owner + N;
   __shared__ int sh[BFS_NT / 32 + 1];
   const int UNSEEN = 0x7fffffff;
@@ -1235,17 +1280,7 @@ __global__ void __launch_bounds__(1024) k_reach(cw_scene_params P, int E, const 
   const int nx = P.nx, N = nx * P.ny;
   const uint8_t* Lb = B.labels + (size_t)slot * N;
   volatile int32_t* R = B.reach + (size_t)slot * N;
-  for (int f = threadIdx.x; f < N; f += 1024) R[f] = Lb[f] != L_OBSTACLE ? f : -1;
-  __syncthreads();
-  for (int f = threadIdx.x; f < N; f += 1024) {
-    if (Lb[f] == L_OBSTACLE) continue;
-    int c = f % nx;
-    if (c + 1 < nx && Lb[f + 1] != L_OBSTACLE) uf_union(R, f, f + 1);
-    if (f + nx < N && Lb[f + nx] != L_OBSTACLE) uf_union(R, f, f + nx);
-  }
-  __syncthreads();
-  for (int f = threadIdx.x; f < N; f += 1024)
-    if (R[f] >= 0) R[f] = uf_root(R, f);
+  grid_components<1024, false>(R, nx, P.ny, [&](int f) { return Lb[f] != L_OBSTACLE; });
 }
 
 // ================================================================= spawn + routes
@@ -1264,6 +1299,32 @@ CW_DEV bool spawn_region_ok(const cw_scene_params& P, int c) {
   return false;
 }
 
+// numpy Generator.permutation(n) = Fisher-Yates from the top over a pure next32
+// stream (random_interval, masked rejection).  Only the first few entries of the
+// final order are consumed (routes.py:69-83), so the kernel (1) generates the
+// 32-bit stream with PCG64 jump-ahead across warp 0 while lane 0 runs the serial
+// accept/reject scan, recording the swap partner j_i of every step i; (2) links
+// the steps by partner (lists of i with j_i == p); (3) resolves final[k] for a
+// batch of k in parallel by walking the swap history backwards:
+//   final[k] = V(j_k, k+1) (k >= 1), final[0] = V(0, 1), and for p < t
+//   V(p, t) = p if no step i >= t has j_i == p, else V(i*, i*+1) with i* the
+//   smallest such step (the value at i* just before step i* swaps into p).
+constexpr int ORD_BATCH = SP_NT;
+
+CW_DEV int resolve_final(int k, const int32_t* jj, const int32_t* head, const int32_t* nxt) {
+  int p, t;
+  if (k >= 1) { p = jj[k]; t = k + 1; }
+  else { p = 0; t = 1; }
+  while (true) {
+    int best = 0x7fffffff;
+    for (int i = head[p]; i >= 0; i = nxt[i])
+      if (i >= t && i < best) best = i;
+    if (best == 0x7fffffff) return p;
+    p = best;
+    t = best + 1;
+  }
+}
+
 __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const int32_t* slots,
                                                  const EnvSeeds* __restrict__ seeds,
                                                  cw_scene_buffers B) {
@@ -1272,14 +1333,24 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
   const int A = P.peds;
   if (A == 0 || B.status[slot] != CW_OK) return;
   const int nx = P.nx, ny = P.ny, N = nx * ny;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint8_t* Lb = B.labels + (size_t)slot * N;
-  int32_t* comp = B.scratch_i32 + (size_t)e * 3 * N;
+  int32_t* comp = B.scratch_i32 + (size_t)e * 7 * N;
   int32_t* cand = comp + N;       // candidate flat indices (row-major)
-  int32_t* perm = cand + N;
+  int32_t* jj = cand + N;         // swap partner of Fisher-Yates step i
+  int32_t* head = jj + N;         // per position: list of steps i with jj[i] == position
+  int32_t* nxt = head + N;
+  int32_t* csize = nxt + N;       // per component root: number of candidates
+  const int NW32 = (N + 31) / 32;
+  uint32_t* cbits = reinterpret_cast<uint32_t*>(csize + N);   // bitmap of one component
+  int32_t* cpre = reinterpret_cast<int32_t*>(cbits + NW32);    // exclusive popcount prefix
   __shared__ int sh[SP_NT / 32 + 1];
-  __shared__ int s_n, s_idx, s_rank, s_j, s_acc, s_k;
+  __shared__ int s_n, s_idx, s_rank, s_j, s_acc, s_k, s_ordn;
   __shared__ unsigned long long s_seed;
   __shared__ double s_maxr;
+  __shared__ uint32_t s_buf[64];
+  __shared__ int s_ord[ORD_BATCH];
+  __shared__ Pcg64Raw s_rng;
   extern __shared__ __align__(16) unsigned char sp_smem[];
   double* stx = reinterpret_cast<double*>(sp_smem);  // accepted starts (A)
   double* sty = stx + A;
@@ -1307,7 +1378,7 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
   for (int f0 = 0; f0 < N; f0 += SP_NT) {
     int f = f0 + threadIdx.x;
     int ok = f < N && Lb[f] == L_WALKABLE && spawn_region_ok(P, f % nx);
-    if (f < N) comp[f] = ok ? f : -1;
+    if (f < N) { comp[f] = ok ? f : -1; head[f] = -1; csize[f] = 0; }
     int tot;
     int off = block_excl_scan<SP_NT>(ok, sh, tot);
     if (ok) cand[base + off] = f;
@@ -1320,56 +1391,143 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
     if (threadIdx.x == 0) B.status[slot] = CW_E_NOROUTE;
     return;
   }
-  // 8-connected components (routes.py:14-32) by union-find; only label
-  // equality is used downstream (routes.py:62, 74), so any labelling works.
-  {
-    volatile int32_t* C = comp;
-    for (int q = threadIdx.x; q < n; q += SP_NT) {
-      int f = cand[q], r = f / nx, c = f - r * nx;
-      const int dr[4] = {0, 1, 1, 1}, dc[4] = {1, -1, 0, 1};
-      for (int k = 0; k < 4; ++k) {
-        int rr = r + dr[k], cc = c + dc[k];
-        if (rr < ny && cc >= 0 && cc < nx && C[rr * nx + cc] >= 0) uf_union(C, f, rr * nx + cc);
+  // 8-connected components (routes.py:14-32); only label equality is used
+  // downstream (routes.py:62, 74), so any labelling works.
+  grid_components<SP_NT, true>(comp, nx, ny, [&](int f) {
+    return Lb[f] == L_WALKABLE && spawn_region_ok(P, f % nx);
+  });
+  for (int q = threadIdx.x; q < n; q += SP_NT) atomicAdd(&csize[comp[cand[q]]], 1);
+  __syncthreads();
+  // ---- permutation draws (warp 0): stream generation + warp-speculative
+  // accept/reject.  Within a window where i stays above mask>>1 the mask is
+  // fixed, so value t (counting from the window start) is accepted iff
+  // (v & mask) <= i - t provided all earlier ones were; a ballot finds the
+  // first rejection, everything before it is accepted.
+  if (wid == 0) {
+    const Pcg64 base_rng = pcg_seed(s_seed);
+    u128 m1, p1, m32, p32;
+    pcg_jump_coeffs((u128)(lane + 1), m1, p1, base_rng.inc);
+    pcg_jump_coeffs((u128)32, m32, p32, base_rng.inc);
+    u128 st = m1 * base_rng.state + p1;   // S_{lane+1}: produces output #lane
+    long long consumed = 0;               // 32-bit values consumed before this round
+    int i = n - 1;
+    auto mask_of = [](int v) {
+      uint32_t m = (uint32_t)v;
+      m |= m >> 1; m |= m >> 2; m |= m >> 4; m |= m >> 8; m |= m >> 16;
+      return m;
+    };
+    uint32_t mask = i > 0 ? mask_of(i) : 0u;
+    int used_last = 0;
+    while (i > 0) {
+      uint64_t out = xsl_rr(st);
+      st = m32 * st + p32;
+      s_buf[2 * lane] = (uint32_t)out;
+      s_buf[2 * lane + 1] = (uint32_t)(out >> 32);
+      __syncwarp();
+      int used = 0;
+      for (int half = 0; half < 2 && i > 0; ++half) {
+        const uint32_t v = s_buf[32 * half + lane];
+        int pos = 0;
+        while (pos < 32 && i > 0) {
+          // classify against every possible acceptance count a_t in [0, t]:
+          // sure accept if (v&mask) <= i - t, sure reject if (v&mask) > i;
+          // the first undecided value is then resolved exactly.
+          const int t = lane - pos;
+          const bool in = lane >= pos;
+          const uint32_t vm = v & mask;
+          const bool bound = in && (i - t > (int)(mask >> 1)) && (i - t >= 1);
+          const bool sure_acc = bound && vm <= (uint32_t)(i - t);
+          const bool sure_rej = bound && vm > (uint32_t)i;
+          const unsigned qm = __ballot_sync(0xffffffffu, in && !(sure_acc || sure_rej));
+          const int f = qm ? __ffs(qm) - 1 : 32;
+          const unsigned am = __ballot_sync(0xffffffffu, sure_acc);
+          const unsigned range = (f >= 32 ? 0xffffffffu : ((1u << f) - 1u)) & ~((1u << pos) - 1u);
+          const unsigned acc_in = am & range;
+          if (in && lane < f && sure_acc) {
+            const int a_t = __popc(acc_in & ((1u << lane) - 1u));
+            jj[i - a_t] = (int32_t)vm;
+          }
+          i -= __popc(acc_in);
+          pos = f;
+          if (i > 0 && (uint32_t)i <= (mask >> 1)) mask = mask_of(i);
+          if (f < 32 && i > 0) {
+            const uint32_t vf = __shfl_sync(0xffffffffu, v, f);
+            if ((vf & mask) <= (uint32_t)i) {
+              if (lane == 0) jj[i] = (int32_t)(vf & mask);
+              --i;
+              if (i > 0 && (uint32_t)i <= (mask >> 1)) mask = mask_of(i);
+            }
+            pos = f + 1;
+          }
+        }
+        used = 32 * half + pos;
       }
+      used_last = used;
+      if (i > 0) consumed += 64;
+      __syncwarp();
     }
-    __syncthreads();
-    for (int q = threadIdx.x; q < n; q += SP_NT) {
-      int f = cand[q];
-      C[f] = uf_root(C, f);
+    if (lane == 0) {
+      // routes stream position right after the shuffle
+      const long long q = (n > 1) ? consumed + used_last : 0;
+      Pcg64 r;
+      r.inc = base_rng.inc;
+      u128 mm, pp;
+      const long long u = q >> 1;
+      if ((q & 1) == 0) {
+        pcg_jump_coeffs((u128)u, mm, pp, base_rng.inc);
+        r.state = mm * base_rng.state + pp;
+        r.has32 = 0;
+        r.buf32 = 0;
+      } else {
+        pcg_jump_coeffs((u128)(u + 1), mm, pp, base_rng.inc);
+        r.state = mm * base_rng.state + pp;
+        r.has32 = 1;
+        r.buf32 = (uint32_t)(xsl_rr(r.state) >> 32);
+      }
+      pcg_store(s_rng, r);
     }
-    __syncthreads();
-  }
-  // permutation(n): Fisher-Yates from the top with masked rejection (numpy shuffle)
-  if (threadIdx.x == 0) {
-    Pcg64 rr = pcg_seed(s_seed);
-    for (int i = 0; i < n; ++i) perm[i] = i;
-    for (int i = n - 1; i > 0; --i) {
-      int j = (int)interval32(rr, (uint32_t)i);
-      int t = perm[i]; perm[i] = perm[j]; perm[j] = t;
-    }
-    s_acc = 0;
-    s_k = 0;
-    // stash the routes stream right after the shuffle in shared memory
-    Pcg64Raw* raw = reinterpret_cast<Pcg64Raw*>(sty + A);
-    pcg_store(*raw, rr);
   }
   __syncthreads();
-  Pcg64Raw* rraw = reinterpret_cast<Pcg64Raw*>(sty + A);
+  // ---- link steps by partner position
+  for (int i = 1 + threadIdx.x; i < n; i += SP_NT) nxt[i] = atomicExch(&head[jj[i]], i);
+  if (threadIdx.x == 0) {
+    s_acc = 0;
+    s_k = 0;
+    s_ordn = 0;
+  }
+  __syncthreads();
   const double res = P.res;
   const double sep = 2.0 * s_maxr;
   const double sep2 = sep * sep;
   double* out_pos = B.sp_pos + (size_t)slot * A * 2;
   double* out_goal = B.sp_goal + (size_t)slot * A * 2;
+  // goal candidates of a start = cells of its component minus the disk of cells
+  // closer than sep (routes.py:74-76); the rank-th one in row-major order is found
+  // through a bitmap of the component with popcount prefixes and the (row-major)
+  // list of disk cells -- O(disk + log N) per route instead of a pass over N.
+  const int R = (int)ceil(sep / res) + 1;
+  const int bw = 2 * R + 1;
+  __shared__ int s_disk[SP_NT];
+  __shared__ int s_ndisk, s_bmc;
+  if (threadIdx.x == 0) s_bmc = -1;
   while (true) {
     __syncthreads();
     if (s_acc >= A || s_k >= n) break;
+    if (s_k >= s_ordn) {  // resolve the next batch of the final permutation
+      const int k = s_ordn + threadIdx.x;
+      if (k < n) s_ord[threadIdx.x] = resolve_final(k, jj, head, nxt);
+      __syncthreads();
+      if (threadIdx.x == 0) s_ordn += ORD_BATCH;
+      __syncthreads();
+    }
     if (threadIdx.x == 0) {
-      s_idx = perm[s_k];
+      s_idx = s_ord[s_k - (s_ordn - ORD_BATCH)];
       s_k += 1;
     }
     __syncthreads();
     const int fs = cand[s_idx];
-    const double sx = ((double)(fs % nx) + 0.5) * res, sy = ((double)(fs / nx) + 0.5) * res;
+    const int sr = fs / nx, sc = fs - sr * nx;
+    const double sx = ((double)sc + 0.5) * res, sy = ((double)sr + 0.5) * res;
     int close = 0;
     for (int a = threadIdx.x; a < s_acc; a += SP_NT) {
       double dx = sx - stx[a], dy = sy - sty[a];
@@ -1377,40 +1535,75 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
     }
     if (__syncthreads_or(close)) continue;
     const int cs = comp[fs];
-    int cnt = 0;
-    for (int q = threadIdx.x; q < n; q += SP_NT) {
-      int f = cand[q];
-      if (comp[f] != cs) continue;
-      double dx = ((double)(f % nx) + 0.5) * res - sx, dy = ((double)(f / nx) + 0.5) * res - sy;
-      cnt += dx * dx + dy * dy >= sep2;
-    }
-    int tot;
-    block_excl_scan<SP_NT>(cnt, sh, tot);
-    if (tot == 0) continue;
-    if (threadIdx.x == 0) {
-      Pcg64 rr = pcg_load(*rraw);
-      s_rank = (int)integers32(rr, (uint64_t)tot);
-      pcg_store(*rraw, rr);
-      s_j = -1;
-    }
-    __syncthreads();
-    // locate the s_rank-th matching candidate in row-major order
-    int seen = 0;
-    for (int q0 = 0; q0 < n; q0 += SP_NT) {
-      int q = q0 + threadIdx.x;
-      int m = 0;
-      if (q < n) {
-        int f = cand[q];
-        if (comp[f] == cs) {
-          double dx = ((double)(f % nx) + 0.5) * res - sx, dy = ((double)(f / nx) + 0.5) * res - sy;
-          m = dx * dx + dy * dy >= sep2;
+    // disk cells of the component (not "far"), row-major
+    int nd = 0;
+    for (int b0 = 0; b0 < bw * bw; b0 += SP_NT) {
+      const int b = b0 + threadIdx.x;
+      int in = 0, f = -1;
+      if (b < bw * bw) {
+        const int r = sr - R + b / bw, c = sc - R + b % bw;
+        if (r >= 0 && r < ny && c >= 0 && c < nx) {
+          f = r * nx + c;
+          if (comp[f] == cs) {
+            double dx = ((double)c + 0.5) * res - sx, dy = ((double)r + 0.5) * res - sy;
+            in = !(dx * dx + dy * dy >= sep2);
+          }
         }
       }
-      int t2;
-      int off = block_excl_scan<SP_NT>(m, sh, t2);
-      if (m && seen + off == s_rank) s_j = cand[q];
-      seen += t2;
-      if (seen > s_rank) break;
+      int tot;
+      const int off = block_excl_scan<SP_NT>(in, sh, tot);
+      if (in && nd + off < SP_NT) s_disk[nd + off] = f;
+      nd += tot;
+    }
+    const int total = csize[cs] - nd;
+    if (total == 0) continue;
+    if (threadIdx.x == 0) {
+      Pcg64 rr = pcg_load(s_rng);
+      s_rank = (int)integers32(rr, (uint64_t)total);
+      pcg_store(s_rng, rr);
+      s_ndisk = nd;
+    }
+    if (s_bmc != cs) {  // bitmap + prefix of component cs
+      for (int f0 = 0; f0 < NW32 * 32; f0 += SP_NT) {
+        const int f = f0 + threadIdx.x;
+        const unsigned bits = __ballot_sync(0xffffffffu, f < N && comp[f] == cs);
+        if (lane == 0 && (f >> 5) < NW32) cbits[f >> 5] = bits;
+      }
+      __syncthreads();
+      int base_w = 0;
+      for (int w0 = 0; w0 < NW32; w0 += SP_NT) {
+        const int w = w0 + threadIdx.x;
+        const int c = w < NW32 ? __popc(cbits[w]) : 0;
+        int tot;
+        const int off = block_excl_scan<SP_NT>(c, sh, tot);
+        if (w < NW32) cpre[w] = base_w + off;
+        base_w += tot;
+      }
+      if (threadIdx.x == 0) { cpre[NW32] = base_w; s_bmc = cs; }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int rank = s_rank;
+      const int ndisk = s_ndisk;
+      int m = 0, cell = -1;
+      for (int it = 0; it <= ndisk + 1; ++it) {
+        // cell = (rank + m)-th set bit of the component bitmap
+        const int k = rank + m;
+        int lo = 0, hi = NW32 - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (cpre[mid] <= k) lo = mid; else hi = mid - 1;
+        }
+        uint32_t w = cbits[lo];
+        int kk = k - cpre[lo];
+        while (kk-- > 0) w &= w - 1;
+        cell = lo * 32 + (__ffs(w) - 1);
+        int m2 = 0;
+        for (int d = 0; d < ndisk && d < SP_NT; ++d) m2 += s_disk[d] <= cell;
+        if (m2 == m) break;
+        m = m2;
+      }
+      s_j = cell;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1467,7 +1660,7 @@ int cw_sample_scenes(const cw_scene_params* P, int E, const uint64_t* scene_seed
   k_walk<<<E, 1024, 0, st>>>(p, E, slots, b);
   k_reach<<<E, 1024, 0, st>>>(p, E, slots, b);
   if (p.peds > 0) {
-    size_t sm = (size_t)p.peds * 2 * sizeof(double) + sizeof(Pcg64Raw);
+    size_t sm = (size_t)p.peds * 2 * sizeof(double);
     k_spawn<<<E, SP_NT, sm, st>>>(p, E, slots, S, b);
   }
   return (int)cudaGetLastError();
@@ -1482,7 +1675,7 @@ int cw_spawn_agents(const cw_scene_params* P, int E, const uint64_t* crowd_seeds
   cudaStream_t st = (cudaStream_t)stream;
   EnvSeeds* S = (EnvSeeds*)seed_scratch;
   k_seeds<<<(E + 127) / 128, 128, 0, st>>>(E, crowd_seeds, crowd_seeds, S);
-  size_t sm = (size_t)P->peds * 2 * sizeof(double) + sizeof(Pcg64Raw);
+  size_t sm = (size_t)P->peds * 2 * sizeof(double);
   k_spawn<<<E, SP_NT, sm, st>>>(*P, E, slots, S, *B);
   return (int)cudaGetLastError();
 }
