@@ -86,7 +86,7 @@ typedef struct cw_scene_buffers {
   uint32_t* passbits;   /* (E, ceil(ny*nx/32)) bit f = labels[f] != OBSTACLE */
   double* sp_pos; double* sp_goal; int8_t* sp_kind; double* sp_pref;
   int32_t* status;
-  int32_t* scratch_i32; /* (E, 7*ny*nx) */
+  int32_t* scratch_i32; /* (E, 10*ny*nx) */
   double* scratch_f64;  /* (E, max(obj_max*8, ny*nx)) */
 } cw_scene_buffers;
 

@@ -159,7 +159,7 @@ class CrowdField:
         p.nx, p.ny = self.nx, self.ny
         n = self.E if rows is None else len(rows)
         status = torch.zeros((self.E,), dtype=torch.int32, device=self.device)
-        scratch = torch.empty((n, 7 * self.nx * self.ny), dtype=torch.int32, device=self.device)
+        scratch = torch.empty((n, 10 * self.nx * self.ny), dtype=torch.int32, device=self.device)
         b = _lib.SceneBuffers()
         b.labels = self.labels_t.data_ptr()
         b.nearest = self.nearest_t.data_ptr()

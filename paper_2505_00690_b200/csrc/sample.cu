@@ -21,6 +21,8 @@
 namespace cw {
 
 // Per-env derived stream seeds / states (scratch, filled by k_seeds).
+constexpr int SCRATCH_I32_PER_CELL = 10;  // ints of scratch_i32 per grid cell and env
+
 struct EnvSeeds {
   Pcg64Raw zones;      // make_rng(child_seed(s,"ground"), "zones")
   Pcg64Raw tileset;    // make_rng(child_seed(s,"terrain-stage"), "tileset")
@@ -686,138 +688,199 @@ CW_DEV double np_pairwise_sum(const double* a, int n) {
   return res;
 }
 
-constexpr int TER_NT = 256;
-constexpr int MAX_LAT = 1024;  // <= 32 x 32 tile lattice
+// WFC runs one warp per env (terrain.py:215-259, wfc.py:24-115).  Arc
+// consistency has a unique greatest fixpoint, so the initial full propagation
+// is a Jacobi sweep over the lattice and the per-collapse propagation is a LIFO
+// worklist from the collapsed cell (the reference's order; any order reaches
+// the same fixpoint and detects the same wipe-outs).
+constexpr int TER_WARPS = 4;
 
-struct TerrainSmem {
+struct WarpWfc {
   TileSet T;
   unsigned long long nib[4][11][16];  // support tables: OR of allowed[d][t] over a nibble of tiles
-  unsigned long long dom[MAX_LAT];
-  unsigned long long init[MAX_LAT];
-  unsigned long long red[TER_NT / 32];
-  int pick_cell;
-  int done;
 };
 
-CW_DEV unsigned long long support(const TerrainSmem& S, int d, unsigned long long dom) {
+CW_DEV unsigned long long support(const WarpWfc& W, int d, unsigned long long dom) {
   unsigned long long s = 0;
   for (int k = 0; dom; ++k, dom >>= 4) {
     unsigned v = (unsigned)(dom & 15ull);
-    if (v) s |= S.nib[d][k][v];
+    if (v) s |= W.nib[d][k][v];
   }
   return s;
 }
 
-// Jacobi arc-consistency to the (unique) greatest fixpoint; false on a wipe-out.
-CW_DEV bool propagate(TerrainSmem& S, int rows, int cols) {
+// neighbour (dir d of x): 0 N, 1 E, 2 S, 3 W; tiles allowed there given dom[x]
+CW_DEV int wfc_nbr(int x, int d, int rows, int cols) {
+  const int r = x / cols, c = x - r * cols;
+  if (d == 0) return r > 0 ? x - cols : -1;
+  if (d == 1) return c + 1 < cols ? x + 1 : -1;
+  if (d == 2) return r + 1 < rows ? x + cols : -1;
+  return c > 0 ? x - 1 : -1;
+}
+
+// full Jacobi sweep to the fixpoint; false on a wipe-out
+CW_DEV bool wfc_propagate_all(const WarpWfc& W, unsigned long long* dom, int rows, int cols, int lane) {
   const int L = rows * cols;
-  unsigned long long nd[MAX_LAT / TER_NT];
   while (true) {
-    int changed = 0, empty = 0;
-    int k = 0;
-    for (int x = threadIdx.x; x < L; x += TER_NT, ++k) {
-      int r = x / cols, c = x - r * cols;
-      unsigned long long d = S.dom[x];
-      if (r > 0) d &= support(S, 2, S.dom[x - cols]);      // north nbr: we are S of it
-      if (r + 1 < rows) d &= support(S, 0, S.dom[x + cols]);
-      if (c > 0) d &= support(S, 1, S.dom[x - 1]);          // west nbr: we are E of it
-      if (c + 1 < cols) d &= support(S, 3, S.dom[x + 1]);
-      nd[k] = d;
+    bool changed = false, empty = false;
+    for (int x0 = 0; x0 < L; x0 += 32) {
+      const int x = x0 + lane;
+      unsigned long long nd = 0;
+      if (x < L) {
+        nd = dom[x];
+        const int r = x / cols, c = x - r * cols;
+        if (r > 0) nd &= support(W, 2, dom[x - cols]);
+        if (r + 1 < rows) nd &= support(W, 0, dom[x + cols]);
+        if (c > 0) nd &= support(W, 1, dom[x - 1]);
+        if (c + 1 < cols) nd &= support(W, 3, dom[x + 1]);
+      }
+      __syncwarp();
+      if (x < L) {
+        changed |= nd != dom[x];
+        empty |= nd == 0ull;
+        dom[x] = nd;
+      }
+      __syncwarp();
     }
-    __syncthreads();
-    k = 0;
-    for (int x = threadIdx.x; x < L; x += TER_NT, ++k) {
-      changed |= nd[k] != S.dom[x];
-      empty |= nd[k] == 0ull;
-      S.dom[x] = nd[k];
-    }
-    int any_empty = __syncthreads_or(empty);
-    if (any_empty) return false;
-    int any_changed = __syncthreads_or(changed);
-    if (!any_changed) return true;
+    if (__any_sync(0xffffffffu, empty)) return false;
+    if (!__any_sync(0xffffffffu, changed)) return true;
   }
 }
 
-__global__ void __launch_bounds__(TER_NT) k_terrain(cw_scene_params P, int E, const int32_t* slots,
-                                                    const EnvSeeds* __restrict__ seeds,
-                                                    cw_scene_buffers B) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  TerrainSmem& S = *reinterpret_cast<TerrainSmem*>(smem_raw);
-  const int e = blockIdx.x;
-  const int slot = env_slot(slots, e);
-  const int rows = P.trows, cols = P.tcols, L = rows * cols;
-  if (B.status[slot] != CW_OK) return;
-  if (threadIdx.x == 0) {
-    Pcg64 rng = pcg_load(seeds[e].tileset);
-    build_tileset_serial(P, rng, S.T);
-  }
-  for (int i = threadIdx.x; i < 4 * CW_MAX_TILES; i += TER_NT) (&S.T.allowed[0][0])[i] = 0ull;
-  __syncthreads();
-  const int n = S.T.n;
-  for (int q = threadIdx.x; q < n * n; q += TER_NT) {
-    int i = q / n, j = q - i * n;
-    if (tiles_compatible(S.T, i, j, 1)) {  // E, and W = E^T
-      atomicOr(&S.T.allowed[1][i], 1ull << j);
-      atomicOr(&S.T.allowed[3][j], 1ull << i);
-    }
-    if (tiles_compatible(S.T, i, j, 2)) {  // S, and N = S^T
-      atomicOr(&S.T.allowed[2][i], 1ull << j);
-      atomicOr(&S.T.allowed[0][j], 1ull << i);
-    }
-  }
-  __syncthreads();
-  for (int q = threadIdx.x; q < 4 * 11 * 16; q += TER_NT) {
-    int d = q / 176, k = (q / 16) % 11, v = q & 15;
-    unsigned long long s = 0;
-    for (int b = 0; b < 4; ++b) {
-      int t = 4 * k + b;
-      if (((v >> b) & 1) && t < n) s |= S.T.allowed[d][t];
-    }
-    S.nib[d][k][v] = s;
-  }
-  // forced-flat cells outside the walkable area (terrain.py:236-250)
-  const uint8_t* Z = B.zones + (size_t)slot * P.nx * P.ny;
-  const unsigned long long full = n == 64 ? ~0ull : ((1ull << n) - 1ull);
-  for (int x = threadIdx.x; x < L; x += TER_NT) {
-    int r = x / cols, c = x - r * cols;
-    int r0 = r * P.cpt, c0 = c * P.cpt;
-    bool inside = (r0 + P.cpt <= P.ny) && (c0 + P.cpt <= P.nx);
-    for (int rr = r0; inside && rr < r0 + P.cpt; ++rr)
-      for (int cc = c0; cc < c0 + P.cpt; ++cc) {
-        uint8_t z = Z[(size_t)rr * P.nx + cc];
-        bool wk = z <= Z_PLAZA && (P.nonflat_split_col < 0 || cc >= P.nonflat_split_col);
-        if (!wk) { inside = false; break; }
+// lane-0 LIFO worklist from cell x0 (wfc.py:89-115); false on a wipe-out
+CW_DEV bool wfc_propagate_from(const WarpWfc& W, unsigned long long* dom, int* stack,
+                               unsigned char* inq, int x0, int rows, int cols) {
+  int top = 0;
+  stack[top++] = x0;
+  inq[x0] = 1;
+  bool ok = true;
+  while (top > 0) {
+    const int x = stack[--top];
+    inq[x] = 0;
+    const unsigned long long here = dom[x];
+    if (here == 0ull) { ok = false; break; }
+    for (int d = 0; d < 4; ++d) {
+      const int y = wfc_nbr(x, d, rows, cols);
+      if (y < 0) continue;
+      const unsigned long long before = dom[y];
+      const unsigned long long after = before & support(W, d, here);
+      if (after == 0ull) { ok = false; break; }
+      if (after != before) {
+        dom[y] = after;
+        if (!inq[y]) { inq[y] = 1; stack[top++] = y; }
       }
-    S.init[x] = inside ? full : 1ull;
+    }
+    if (!ok) break;
   }
-  __syncthreads();
+  if (!ok) while (top > 0) inq[stack[--top]] = 0;
+  return ok;
+}
+
+CW_HD size_t terrain_warp_smem(int L) {
+  size_t per = sizeof(WarpWfc) + (size_t)L * 8 * 2 + (size_t)L * 4 + (size_t)L;
+  per = (per + 15) & ~(size_t)15;
+  return per;
+}
+
+__global__ void __launch_bounds__(TER_WARPS * 32) k_terrain(cw_scene_params P, int E,
+                                                            const int32_t* slots,
+                                                            const EnvSeeds* __restrict__ seeds,
+                                                            cw_scene_buffers B) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int e = blockIdx.x * TER_WARPS + wid;
+  if (e >= E) return;
+  const int slot = env_slot(slots, e);
+  if (B.status[slot] != CW_OK) return;
+  const int rows = P.trows, cols = P.tcols, L = rows * cols;
+  unsigned char* base = smem_raw + (size_t)wid * terrain_warp_smem(L);
+  WarpWfc& W = *reinterpret_cast<WarpWfc*>(base);
+  unsigned long long* dom = reinterpret_cast<unsigned long long*>(base + sizeof(WarpWfc));
+  unsigned long long* init = dom + L;
+  int* stack = reinterpret_cast<int*>(init + L);
+  unsigned char* inq = reinterpret_cast<unsigned char*>(stack + L);
+  TileSet& T = W.T;
+  if (lane == 0) {
+    Pcg64 rng = pcg_load(seeds[e].tileset);
+    build_tileset_serial(P, rng, T);
+  }
+  for (int k = lane; k < 4 * CW_MAX_TILES; k += 32) (&T.allowed[0][0])[k] = 0ull;
+  __syncwarp();
+  const int n = T.n;
+  for (int q = lane; q < n * n; q += 32) {
+    const int i = q / n, j = q - i * n;
+    if (tiles_compatible(T, i, j, 1)) {  // E, and W = E^T
+      atomicOr(&T.allowed[1][i], 1ull << j);
+      atomicOr(&T.allowed[3][j], 1ull << i);
+    }
+    if (tiles_compatible(T, i, j, 2)) {  // S, and N = S^T
+      atomicOr(&T.allowed[2][i], 1ull << j);
+      atomicOr(&T.allowed[0][j], 1ull << i);
+    }
+  }
+  __syncwarp();
+  for (int q = lane; q < 4 * 11 * 16; q += 32) {
+    const int d = q / 176, k = (q / 16) % 11, v = q & 15;
+    unsigned long long sp = 0;
+    for (int b = 0; b < 4; ++b) {
+      const int t = 4 * k + b;
+      if (((v >> b) & 1) && t < n) sp |= T.allowed[d][t];
+    }
+    W.nib[d][k][v] = sp;
+  }
+  // forced-flat tiles outside the walkable area (terrain.py:236-250)
+  const uint8_t* Z = B.zones + (size_t)slot * P.nx * P.ny;
+  const unsigned long long full = (1ull << n) - 1ull;
+  const int cpt = P.cpt;
+  for (int x = 0; x < L; ++x) {
+    const int r = x / cols, c = x - r * cols;
+    const int r0 = r * cpt, c0 = c * cpt;
+    bool inside = (r0 + cpt <= P.ny) && (c0 + cpt <= P.nx);
+    if (inside) {
+      bool bad = false;
+      for (int k = lane; k < cpt * cpt; k += 32) {
+        const int rr = r0 + k / cpt, cc = c0 + k % cpt;
+        const uint8_t z = Z[(size_t)rr * P.nx + cc];
+        bad |= !(z <= Z_PLAZA && (P.nonflat_split_col < 0 || cc >= P.nonflat_split_col));
+      }
+      inside = !__any_sync(0xffffffffu, bad);
+    }
+    if (lane == 0) init[x] = inside ? full : 1ull;
+  }
+  for (int x = lane; x < L; x += 32) inq[x] = 0;
+  __syncwarp();
   int attempt_ok = -1;
   for (int attempt = 0; attempt < 16 && attempt_ok < 0; ++attempt) {
-    for (int x = threadIdx.x; x < L; x += TER_NT) S.dom[x] = S.init[x];
-    __syncthreads();
+    for (int x = lane; x < L; x += 32) dom[x] = init[x];
+    __syncwarp();
     Pcg64 rng;
-    if (threadIdx.x == 0) rng = pcg_seed(child_seed(seeds[e].wfc_seed, "wfc", (uint64_t)attempt));
-    bool ok = propagate(S, rows, cols);
+    if (lane == 0) rng = pcg_seed(child_seed(seeds[e].wfc_seed, "wfc", (uint64_t)attempt));
+    bool ok = wfc_propagate_all(W, dom, rows, cols, lane);
     while (ok) {
       // minimum-entropy open cell, ties by lowest flat index (wfc.py:61-70)
       unsigned long long best = ~0ull;
-      for (int x = threadIdx.x; x < L; x += TER_NT) {
-        int cnt = __popcll(S.dom[x]);
+      for (int x = lane; x < L; x += 32) {
+        const int cnt = __popcll(dom[x]);
         if (cnt > 1) {
-          unsigned long long key = ((unsigned long long)cnt << 32) | (unsigned)x;
+          const unsigned long long key = ((unsigned long long)cnt << 32) | (unsigned)x;
           best = key < best ? key : best;
         }
       }
-      best = block_min_u64<TER_NT>(best, S.red);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+        best = y < best ? y : best;
+      }
       if (best == ~0ull) break;  // fully collapsed
-      if (threadIdx.x == 0) {
-        int x = (int)(best & 0xffffffffu);
-        unsigned long long d = S.dom[x];
+      int okl = 1;
+      if (lane == 0) {
+        const int x = (int)(best & 0xffffffffu);
+        const unsigned long long d = dom[x];
         int opts[CW_MAX_TILES];
         double w[CW_MAX_TILES];
         int no = 0;
         for (int t = 0; t < n; ++t)
-          if ((d >> t) & 1ull) { opts[no] = t; w[no] = S.T.w[t]; ++no; }
+          if ((d >> t) & 1ull) { opts[no] = t; w[no] = T.w[t]; ++no; }
         double tot = np_pairwise_sum(w, no);
         if (tot <= 0) {
           for (int k = 0; k < no; ++k) w[k] = 1.0;
@@ -827,43 +890,44 @@ __global__ void __launch_bounds__(TER_NT) k_terrain(cw_scene_params P, int E, co
         double cdf[CW_MAX_TILES];
         double acc = 0.0;
         for (int k = 0; k < no; ++k) {
-          double pk = w[k] / tot;
+          const double pk = w[k] / tot;
           acc = k ? acc + pk : pk;
           cdf[k] = acc;
         }
-        double last = cdf[no - 1];
-        double u = next_double(rng);
+        const double last = cdf[no - 1];
+        const double u = next_double(rng);
         int idx = 0;
         while (idx < no && !(cdf[idx] / last > u)) ++idx;
-        S.dom[x] = 1ull << opts[idx];
+        dom[x] = 1ull << opts[idx];
+        okl = wfc_propagate_from(W, dom, stack, inq, x, rows, cols);
       }
-      __syncthreads();
-      ok = propagate(S, rows, cols);
+      ok = __shfl_sync(0xffffffffu, okl, 0) != 0;
+      __syncwarp();
     }
     if (ok) attempt_ok = attempt;
-    __syncthreads();
+    __syncwarp();
   }
   int32_t* A = B.assign + (size_t)slot * L;
   if (attempt_ok < 0) {
-    if (threadIdx.x == 0) B.status[slot] = CW_E_CONTRADICTION;
+    if (lane == 0) B.status[slot] = CW_E_CONTRADICTION;
     return;
   }
-  for (int x = threadIdx.x; x < L; x += TER_NT) A[x] = __ffsll((long long)S.dom[x]) - 1;
-  if (threadIdx.x == 0) {
+  for (int x = lane; x < L; x += 32) A[x] = __ffsll((long long)dom[x]) - 1;
+  if (lane == 0) {
     B.wfc_attempts[slot] = attempt_ok;
     B.n_tiles[slot] = n;
     B.noise_seed[slot] = seeds[e].noise;
   }
-  for (int i = threadIdx.x; i < CW_MAX_TILES; i += TER_NT) {
-    size_t o = (size_t)slot * CW_MAX_TILES + i;
-    bool v = i < n;
-    B.tile_code[o] = v ? S.T.code[i] : -1;
-    B.tile_kind[o] = v ? S.T.kind[i] : -1;
-    B.tile_param[o] = v ? S.T.param[i] : 0.0;
-    B.tile_w[o] = v ? S.T.w[i] : 0.0;
-    for (int k = 0; k < 4; ++k) B.tile_p[o * 4 + k] = v ? S.T.p[i][k] : 0.0;
+  for (int i = lane; i < CW_MAX_TILES; i += 32) {
+    const size_t o = (size_t)slot * CW_MAX_TILES + i;
+    const bool v = i < n;
+    B.tile_code[o] = v ? T.code[i] : -1;
+    B.tile_kind[o] = v ? T.kind[i] : -1;
+    B.tile_param[o] = v ? T.param[i] : 0.0;
+    B.tile_w[o] = v ? T.w[i] : 0.0;
+    for (int k = 0; k < 4; ++k) B.tile_p[o * 4 + k] = v ? T.p[i][k] : 0.0;
     for (int d = 0; d < 4; ++d)
-      B.allowed[((size_t)slot * 4 + d) * CW_MAX_TILES + i] = v ? S.T.allowed[d][i] : 0ull;
+      B.allowed[((size_t)slot * 4 + d) * CW_MAX_TILES + i] = v ? T.allowed[d][i] : 0ull;
   }
 }
 
@@ -1171,7 +1235,7 @@ __global__ void __launch_bounds__(BFS_NT) k_nearest(cw_scene_params P, int E, co
   const int nx = P.nx, ny = P.ny, N = nx * ny;
   const uint8_t* Lb = B.labels + (size_t)slot * N;
   int32_t* near = B.nearest + (size_t)slot * N;
-  int32_t* owner = B.scratch_i32 + (size_t)e * 7 * N;
+  int32_t* owner = B.scratch_i32 + (size_t)e * SCRATCH_I32_PER_CELL * N + 8 * (size_t)N;
   int32_t* Q = owner + N;
   __shared__ int sh[BFS_NT / 32 + 1];
   const int UNSEEN = 0x7fffffff;
@@ -1284,7 +1348,7 @@ __global__ void __launch_bounds__(1024) k_reach(cw_scene_params P, int E, const 
 }
 
 // ================================================================= spawn + routes
-constexpr int SP_NT = 1024;
+constexpr int SP_NT = 256;
 __device__ __constant__ double kMaxSpeed[3] = {2.0, 5.0, 4.0};     // crowd/types.py:15-19
 __device__ __constant__ double kPrefLo[3] = {0.8, 2.0, 1.5};       // types.py:22-26
 __device__ __constant__ double kPrefHi[3] = {1.4, 4.0, 3.0};
@@ -1335,7 +1399,7 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
   const int nx = P.nx, ny = P.ny, N = nx * ny;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint8_t* Lb = B.labels + (size_t)slot * N;
-  int32_t* comp = B.scratch_i32 + (size_t)e * 7 * N;
+  int32_t* comp = B.scratch_i32 + (size_t)e * SCRATCH_I32_PER_CELL * N;
   int32_t* cand = comp + N;       // candidate flat indices (row-major)
   int32_t* jj = cand + N;         // swap partner of Fisher-Yates step i
   int32_t* head = jj + N;         // per position: list of steps i with jj[i] == position
@@ -1344,6 +1408,7 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
   const int NW32 = (N + 31) / 32;
   uint32_t* cbits = reinterpret_cast<uint32_t*>(csize + N);   // bitmap of one component
   int32_t* cpre = reinterpret_cast<int32_t*>(cbits + NW32);    // exclusive popcount prefix
+  int32_t* disk = csize + 2 * (size_t)N;                       // row-major disk cells (<= N)
   __shared__ int sh[SP_NT / 32 + 1];
   __shared__ int s_n, s_idx, s_rank, s_j, s_acc, s_k, s_ordn;
   __shared__ unsigned long long s_seed;
@@ -1507,7 +1572,6 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
   // list of disk cells -- O(disk + log N) per route instead of a pass over N.
   const int R = (int)ceil(sep / res) + 1;
   const int bw = 2 * R + 1;
-  __shared__ int s_disk[SP_NT];
   __shared__ int s_ndisk, s_bmc;
   if (threadIdx.x == 0) s_bmc = -1;
   while (true) {
@@ -1552,9 +1616,10 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
       }
       int tot;
       const int off = block_excl_scan<SP_NT>(in, sh, tot);
-      if (in && nd + off < SP_NT) s_disk[nd + off] = f;
+      if (in) disk[nd + off] = f;
       nd += tot;
     }
+    __syncthreads();
     const int total = csize[cs] - nd;
     if (total == 0) continue;
     if (threadIdx.x == 0) {
@@ -1599,7 +1664,7 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
         while (kk-- > 0) w &= w - 1;
         cell = lo * 32 + (__ffs(w) - 1);
         int m2 = 0;
-        for (int d = 0; d < ndisk && d < SP_NT; ++d) m2 += s_disk[d] <= cell;
+        for (int d = 0; d < ndisk; ++d) m2 += disk[d] <= cell;
         if (m2 == m) break;
         m = m2;
       }
@@ -1619,6 +1684,28 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
     }
   }
   if (threadIdx.x == 0 && s_acc < A) B.status[slot] = CW_E_NOROUTE;
+}
+
+struct SideStreams {
+  int dev = -1;
+  cudaStream_t s[2];
+  cudaEvent_t fork, join[2];
+};
+
+static SideStreams& side_streams() {
+  static SideStreams g[16];
+  int d = 0;
+  cudaGetDevice(&d);
+  SideStreams& S = g[d & 15];
+  if (S.dev != d) {
+    for (int k = 0; k < 2; ++k) {
+      cudaStreamCreateWithFlags(&S.s[k], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&S.join[k], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&S.fork, cudaEventDisableTiming);
+    S.dev = d;
+  }
+  return S;
 }
 
 }  // namespace cw
@@ -1644,25 +1731,31 @@ int cw_sample_scenes(const cw_scene_params* P, int E, const uint64_t* scene_seed
   k_seeds<<<(E + 127) / 128, 128, 0, st>>>(E, scene_seeds, crowd_seeds, S);
   if (p.layout == 1) k_zones_blk<<<E, 512, 0, st>>>(p, E, slots, S, b);
   else k_zones<<<E, 256, 0, st>>>(p, E, slots, S, b);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_terrain, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(TerrainSmem));
-    cudaFuncSetAttribute(k_spawn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
-  k_terrain<<<E, TER_NT, sizeof(TerrainSmem), st>>>(p, E, slots, S, b);
+  const size_t tsm = terrain_warp_smem(p.trows * p.tcols) * TER_WARPS;
+  cudaFuncSetAttribute(k_terrain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+  k_terrain<<<(E + TER_WARPS - 1) / TER_WARPS, TER_WARPS * 32, tsm, st>>>(p, E, slots, S, b);
   k_place<<<(E + 3) / 4, 128, 0, st>>>(p, E, slots, S, b);
   const int quads = (p.nx * p.ny + 3) / 4;
   k_raster<<<dim3((quads + 255) / 256, E), 256, 0, st>>>(p, E, slots, b);
   if (p.obj_max > 0) k_footprint<<<dim3((p.obj_max + 3) / 4, E), 128, 0, st>>>(p, E, slots, b);
-  k_nearest<<<E, BFS_NT, 0, st>>>(p, E, slots, b);
-  k_walk<<<E, 1024, 0, st>>>(p, E, slots, b);
-  k_reach<<<E, 1024, 0, st>>>(p, E, slots, b);
+  // the label consumers are independent: BFS and components/walk list run on
+  // side streams joined back before returning (fork/join keeps stream order)
+  SideStreams& ss = side_streams();
+  cudaEventRecord(ss.fork, st);
+  cudaStreamWaitEvent(ss.s[0], ss.fork, 0);
+  cudaStreamWaitEvent(ss.s[1], ss.fork, 0);
+  k_nearest<<<E, BFS_NT, 0, ss.s[0]>>>(p, E, slots, b);
+  k_walk<<<E, 1024, 0, ss.s[1]>>>(p, E, slots, b);
+  k_reach<<<E, 1024, 0, ss.s[1]>>>(p, E, slots, b);
   if (p.peds > 0) {
     size_t sm = (size_t)p.peds * 2 * sizeof(double);
+    if (sm > 48 * 1024) cudaFuncSetAttribute(k_spawn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k_spawn<<<E, SP_NT, sm, st>>>(p, E, slots, S, b);
   }
+  cudaEventRecord(ss.join[0], ss.s[0]);
+  cudaEventRecord(ss.join[1], ss.s[1]);
+  cudaStreamWaitEvent(st, ss.join[0], 0);
+  cudaStreamWaitEvent(st, ss.join[1], 0);
   return (int)cudaGetLastError();
 }
 
@@ -1676,6 +1769,7 @@ int cw_spawn_agents(const cw_scene_params* P, int E, const uint64_t* crowd_seeds
   EnvSeeds* S = (EnvSeeds*)seed_scratch;
   k_seeds<<<(E + 127) / 128, 128, 0, st>>>(E, crowd_seeds, crowd_seeds, S);
   size_t sm = (size_t)P->peds * 2 * sizeof(double);
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_spawn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k_spawn<<<E, SP_NT, sm, st>>>(*P, E, slots, S, *B);
   return (int)cudaGetLastError();
 }

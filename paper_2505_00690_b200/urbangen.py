@@ -265,7 +265,7 @@ class SceneBatch:
             return
         p = self.params
         N = p.nx * p.ny
-        self.scratch_i32 = torch.empty((rows, 7 * N), dtype=torch.int32, device=self.device)
+        self.scratch_i32 = torch.empty((rows, 10 * N), dtype=torch.int32, device=self.device)
         self.scratch_f64 = torch.empty((rows, max(p.obj_max * 8, N)), dtype=torch.float64,
                                        device=self.device)
         nbytes = _lib.lib().cw_scene_seed_scratch_bytes(rows)
