@@ -134,7 +134,7 @@ class CrowdField:
         self.last_gap_t = torch.full((self.E,), float("inf"), dtype=torch.float64, device=self.device)
         self.gap_tmp_t = torch.zeros((self.E,), dtype=torch.float64, device=self.device)
         self.flags_t = torch.zeros((8,), dtype=torch.int32, device=self.device)
-        self.counters_t = torch.zeros((8,), dtype=torch.int64, device=self.device)
+        self.counters_t = torch.zeros((16,), dtype=torch.int64, device=self.device)
         self._astar_ready = False
         self._alloc(0)
 
@@ -406,7 +406,8 @@ class CrowdField:
         return {"astar_expansions": int(c[0]), "path_points_scanned": int(c[1]),
                 "lp_fallbacks": int(c[2]), "stall_retries": int(c[3]),
                 "astar_cycles": int(c[4]), "astar_max_cycles": int(c[5]),
-                "cta_cycles": int(c[6]), "cta_max_cycles": int(c[7])}
+                "cta_cycles": int(c[6]), "cta_max_cycles": int(c[7]),
+                "astar_phase_cycles": [int(v) for v in c[8:12]], "astar_open_sum": int(c[12])}
 
 
 def step_crowd(agents, robot_state, occupancy, config, seed=0, resample_goals=True):

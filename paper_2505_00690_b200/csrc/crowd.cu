@@ -27,7 +27,7 @@ namespace cw {
 constexpr int MAXC = 12;   // neighbour lanes (<= 10) + robot + static
 constexpr double kWaypointReach = 0.5, kStrayLimit = 1.0;
 // open-list entries kept in shared memory by k_astar (16 B each: f bits, h bits | cell)
-CW_HD int astar_smem_entries() { return 8192; }
+CW_HD int astar_smem_entries() { return 4096; }
 
 struct HeapEnt { double f; int32_t cell; int32_t pad; };
 
@@ -250,10 +250,17 @@ CW_DEV bool passbit(const uint32_t* pb, int f) { return (__ldg(pb + (f >> 5)) >>
 // One warp per CTA; the open list (f bits, k2) lives in shared memory.
 // Unreachable goals (different 4-connected component, see k_reach) return None
 // without searching -- the reference exhausts the component and returns None.
+struct __align__(16) OpenEnt { unsigned long long f, k; };
+
+// lexicographic (f, k) as one 128-bit unsigned compare: branch-free carry chain
+CW_DEV bool ent_less(unsigned long long fa, unsigned long long ka, unsigned long long fb,
+                     unsigned long long kb) {
+  return (((u128)fa << 64) | ka) < (((u128)fb << 64) | kb);
+}
+
 __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state S, int smem_cap) {
   extern __shared__ __align__(16) unsigned char sm[];
-  unsigned long long* OF = reinterpret_cast<unsigned long long*>(sm);
-  unsigned long long* OK = OF + smem_cap;
+  OpenEnt* O = reinterpret_cast<OpenEnt*>(sm);
   const int lane = threadIdx.x;
   const int nx = P.nx, ny = P.ny;
   const size_t N = (size_t)nx * ny;
@@ -263,6 +270,7 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
   const int mdc[8] = {0, 0, -1, 1, -1, 1, -1, 1};
   const int cap = min(smem_cap, (int)kClosed);
   const unsigned lt_mask = (1u << lane) - 1u;
+  const unsigned long long CELLM = (1ull << kCellBits) - 1ull;
   long long expansions = 0, t_max = 0, t_sum = 0;
   while (true) {
     int q = 0;
@@ -298,38 +306,68 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
         const double h0 = octile(sr, sc, gr, gc);
         AstarRec r0 = {0.0, -1, ep | 0u};
         rec[start] = r0;
-        OF[0] = (unsigned long long)__double_as_longlong(h0);
-        OK[0] = make_k2(h0, sr, sc);
+        OpenEnt e0 = {(unsigned long long)__double_as_longlong(h0), make_k2(h0, sr, sc)};
+        O[0] = e0;
       }
       n = 1;
       __syncwarp();
       while (n > 0) {
-        // ---- pop: strided scan + butterfly argmin on (f, k2)
+        // ---- pop: strided scan (4-way tree per step) + butterfly argmin on (f, k2)
         unsigned long long bf = ~0ull, bk = ~0ull;
         int bi = -1;
-        for (int i = lane; i < n; i += 32) {
-          unsigned long long f = OF[i], k = OK[i];
-          if (f < bf || (f == bf && k < bk)) { bf = f; bk = k; bi = i; }
+        int i = lane;
+        for (; i + 96 < n; i += 128) {
+          const OpenEnt a = O[i], b = O[i + 32], c = O[i + 64], d = O[i + 96];
+          const bool ab = ent_less(b.f, b.k, a.f, a.k);
+          const bool cd = ent_less(d.f, d.k, c.f, c.k);
+          unsigned long long f1 = ab ? b.f : a.f, k1 = ab ? b.k : a.k;
+          int i1 = ab ? i + 32 : i;
+          const unsigned long long f2 = cd ? d.f : c.f, k2 = cd ? d.k : c.k;
+          const int i2 = cd ? i + 96 : i + 64;
+          if (ent_less(f2, k2, f1, k1)) { f1 = f2; k1 = k2; i1 = i2; }
+          if (ent_less(f1, k1, bf, bk)) { bf = f1; bk = k1; bi = i1; }
         }
+        for (; i < n; i += 32) {
+          const OpenEnt a = O[i];
+          if (ent_less(a.f, a.k, bf, bk)) { bf = a.f; bk = a.k; bi = i; }
+        }
+        unsigned long long gf = bf, gk = bk;
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
-          unsigned long long of = __shfl_xor_sync(0xffffffffu, bf, o);
-          unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
-          int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (of < bf || (of == bf && ok < bk)) { bf = of; bk = ok; bi = oi; }
+          const unsigned long long of = __shfl_xor_sync(0xffffffffu, gf, o);
+          const unsigned long long ok = __shfl_xor_sync(0xffffffffu, gk, o);
+          if (ent_less(of, ok, gf, gk)) { gf = of; gk = ok; }
         }
-        const int cell20 = (int)(bk & ((1ull << kCellBits) - 1ull));
+        const unsigned own = __ballot_sync(0xffffffffu, bf == gf && bk == gk);
+        bi = __shfl_sync(0xffffffffu, bi, __ffs(own) - 1);
+        const int cell20 = (int)(gk & CELLM);
         const int r = cell20 >> 10, c = cell20 & 1023;
         const int x = r * nx + c;
+        // ---- issue every load of this expansion together: the popped g, the
+        // neighbour records and passable words (independent of the removal)
+        int y = -1, rr = 0, cc = 0;
+        AstarRec ry = {0.0, 0, 0u};
+        bool okp = false;
+        if (lane < 8) {
+          rr = r + mdr[lane];
+          cc = c + mdc[lane];
+          if (rr >= 0 && rr < ny && cc >= 0 && cc < nx) {
+            y = rr * nx + cc;
+            ry = rec[y];
+            okp = passbit(pb, y) && (lane < 4 || (passbit(pb, r * nx + cc) && passbit(pb, rr * nx + c)));
+          }
+        }
+        const double gx = rec[x].g;
+        // removal: the last entry moves into slot bi (its cell's position changes)
+        const int last = n - 1;
+        const OpenEnt le = O[last];
+        const int lc20 = (int)(le.k & CELLM);
+        const int lcell = (lc20 >> 10) * nx + (lc20 & 1023);
         __syncwarp();
         if (lane == 0) {
-          const int last = n - 1;
           if (bi != last) {
-            unsigned long long lf = OF[last], lk = OK[last];
-            OF[bi] = lf;
-            OK[bi] = lk;
-            int lc = (int)(lk & ((1ull << kCellBits) - 1ull));
-            rec[(lc >> 10) * nx + (lc & 1023)].tag = ep | (uint32_t)bi;
+            O[bi] = le;
+            rec[lcell].tag = ep | (uint32_t)bi;
           }
           rec[x].tag = ep | kClosed;
         }
@@ -338,32 +376,26 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
         if (x == goal) { found = 1; break; }
         // the open list holds live entries only, so the reference's stale test
         // (paths.py:225) cannot fire here
-        const double gx = rec[x].g;
         ++expansions;
         bool ins = false, dec = false;
-        unsigned long long nf = 0, nk = 0;
-        int pos = 0, y = 0;
-        if (lane < 8) {
-          int rr = r + mdr[lane], cc = c + mdc[lane];
-          if (rr >= 0 && rr < ny && cc >= 0 && cc < nx) {
-            y = rr * nx + cc;
-            bool ok = passbit(pb, y) && (lane < 4 || (passbit(pb, r * nx + cc) && passbit(pb, rr * nx + c)));
-            if (ok) {
-              AstarRec ry = rec[y];
-              bool live = (ry.tag >> kPosBits) == epoch;
-              double old = live ? ry.g : CUDART_INF;
-              double ng = gx + (lane < 4 ? 1.0 : kSqrt2);
-              if (ng < old - 1e-12) {
-                const double hh = octile(rr, cc, gr, gc);
-                nf = (unsigned long long)__double_as_longlong(ng + hh);
-                nk = make_k2(hh, rr, cc);
-                uint32_t p = live ? (ry.tag & kPosMask) : kClosed;
-                rec[y].g = ng;
-                rec[y].parent = x;
-                if (p == kClosed) ins = true;            // insert / re-open
-                else { dec = true; pos = (int)p; }       // decrease-key in place
-              }
-            }
+        OpenEnt ne;
+        int pos = 0;
+        if (okp) {
+          // ry was loaded before the removal: only the moved entry changed position
+          uint32_t tag = ry.tag;
+          if (y == lcell && bi != last) tag = ep | (uint32_t)bi;
+          const bool live = (tag >> kPosBits) == epoch;
+          const double old = live ? ry.g : CUDART_INF;
+          const double ng = gx + (lane < 4 ? 1.0 : kSqrt2);
+          if (ng < old - 1e-12) {
+            const double hh = octile(rr, cc, gr, gc);
+            ne.f = (unsigned long long)__double_as_longlong(ng + hh);
+            ne.k = make_k2(hh, rr, cc);
+            const uint32_t p = live ? (tag & kPosMask) : kClosed;
+            rec[y].g = ng;
+            rec[y].parent = x;
+            if (p == kClosed) ins = true;            // insert / re-open
+            else { dec = true; pos = (int)p; }       // decrease-key in place
           }
         }
         __syncwarp();
@@ -373,7 +405,7 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
           pos = n + __popc(im & lt_mask);
           rec[y].tag = ep | (uint32_t)pos;
         }
-        if (ins || dec) { OF[pos] = nf; OK[pos] = nk; }
+        if (ins || dec) O[pos] = ne;
         n += __popc(im);
         __syncwarp();
       }

@@ -22,4 +22,4 @@ for t in range(int(sys.argv[2]) if len(sys.argv) > 2 else 40):
     f.step(check=False)
     torch.cuda.synchronize(); dt = time.perf_counter() - t0
     st = f.stats()
-    print(t, f"{dt*1e3:.2f} ms", {k: (v/1.9e6 if 'cycles' in k else v) for k, v in st.items()})
+    ex = max(1, st["astar_expansions"]); print(t, f"{dt*1e3:.2f} ms", "exp", st["astar_expansions"], "cyc/exp", round(st["astar_cycles"]/ex), "max search ms", round(st["astar_max_cycles"]/1.9e6, 2), "orca cta max ms", round(st["cta_max_cycles"]/1.9e6, 3))
