@@ -112,10 +112,11 @@ def run_ours(args):
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
     _lib.build()
+    from paper_2505_00690_b200 import shard
     E = args.envs
     spec = make_spec()
     zero = torch.zeros(E, dtype=torch.int64, device=dev)
-    gids = torch.arange(rank * E, (rank + 1) * E, device=dev)
+    gids = torch.from_numpy(shard.env_ids(rank, world, E)).to(dev)   # rank owns [r*E, (r+1)*E)
     env_seeds = child_seeds_device(zero, "env", gids)
     crowd_seeds = child_seeds_device(env_seeds, "crowd", 0)
     run_seeds = child_seeds_device(env_seeds, "crowd-run").cpu().numpy().view(np.uint64)
@@ -218,9 +219,7 @@ def run_ours(args):
     tmax = torch.tensor([t_ms, sample_ms, e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        gathered = [torch.empty_like(stats) for _ in range(world)]
-        dist.all_gather(gathered, stats)
-        stats = torch.cat(gathered)
+        stats = shard.gather_env_stats(stats)
     t_ms, sample_ms, e2e_s = [float(x) for x in tmax.cpu()]
     if rank == 0:
         steps = args.steps

@@ -256,3 +256,62 @@ def test_batched_env_resample_slots(torch_cuda):
     assert np.array_equal(solo.labels[0].cpu().numpy(), after[4].cpu().numpy())
     assert np.array_equal(solo.sp_pos[0].cpu().numpy(), env.crowd.pos_t[4].cpu().numpy())
     env.step_crowd()
+
+
+def test_shard_invariance_sampling_and_crowd(torch_cuda):
+    """W=1 vs W=2: global env ids [0,6) in one batch equal the two
+    shards [0,3) + [3,6) run as separate batches, over sampling and 20 ticks."""
+    from oracle.rng import child_seed
+    from paper_2505_00690_b200 import shard
+    seeds_all = shard.env_seeds(0, shard.env_ids(0, 1, 6))
+    kw = dict(extent_m=(32.0, 32.0), object_density=20 / 41, grid_resolution_m=0.25)
+    rp = np.random.default_rng(3).uniform(3.0, 29.0, (20, 6, 2))
+    b1, f1 = _device_crowd(seeds_all, kw, 8)
+    parts = []
+    for r in range(2):
+        ids = shard.env_ids(r, 2, 3)
+        parts.append(_device_crowd(shard.env_seeds(0, ids), kw, 8))
+    for t in range(20):
+        f1.step(robot_pos=rp[t], robot_vel=np.zeros((6, 2)))
+        for r, (_, f) in enumerate(parts):
+            f.step(robot_pos=rp[t, 3 * r:3 * r + 3], robot_vel=np.zeros((3, 2)))
+    for r, (b, f) in enumerate(parts):
+        sl = slice(3 * r, 3 * r + 3)
+        assert np.array_equal(b1.labels[sl].cpu().numpy(), b.labels.cpu().numpy())
+        assert np.array_equal(f1.pos[sl], f.pos)
+        assert np.array_equal(f1.vel[sl], f.vel)
+        assert np.array_equal(f1.goal[sl], f.goal)
+
+
+def test_blocks_layout_dense_crowd_matches_oracle(torch_cuda):
+    """cfg4 shape (block layout with roads/crosswalks, NavClear placement, many
+    pedestrians, neighbor_distance 3 m) against the oracle for a few ticks."""
+    from oracle import crowd as C
+    from oracle import scene as S
+    from oracle.rng import child_seed
+    from paper_2505_00690_b200.crowd import CrowdConfig, CrowdField
+    from paper_2505_00690_b200.urbangen import SceneSampler, SceneSpec, TaskKind
+    seed = child_seed(0, "env", 11)
+    spec = SceneSpec(seed=seed, extent_m=(48.0, 48.0), task_kind=TaskKind.NAV_CLEAR,
+                     object_density=0.0, pedestrian_count=96, terrain_mix=MIX,
+                     grid_resolution_m=0.25)
+    b = SceneSampler(spec, 1).sample([seed], [child_seed(seed, "crowd", 0)])
+    sc = S.generate_scene(dict(seed=seed, extent=(48.0, 48.0), res=0.25, task="NavClear",
+                               split="Train", density=0.0, mix=MIX), golden_catalog())
+    assert np.array_equal(b.zones[0].cpu().numpy(), sc["zones"])
+    assert np.array_equal(b.labels[0].cpu().numpy(), sc["labels"])
+    sp = C.spawn_agents(sc["labels"], 0.25, 96, child_seed(seed, "crowd", 0))
+    assert np.array_equal(b.sp_pos[0].cpu().numpy(), sp["pos"])
+    assert np.array_equal(b.sp_goal[0].cpu().numpy(), sp["goal"])
+    run = [child_seed(seed, "crowd-run")]
+    f = CrowdField(b, CrowdConfig(neighbor_distance=3.0), run)
+    f.set_from_spawn(b)
+    ref = C.CrowdFieldOracle([(sc["labels"], 0.25)], C.Config(neighbor_distance=3.0), run)
+    ref.set_agents([sp])
+    rng = np.random.default_rng(4)
+    for t in range(4):
+        rp = rng.uniform(5.0, 43.0, (1, 2))
+        f.step(robot_pos=rp, robot_vel=np.zeros((1, 2)))
+        ref.step(robot_pos=rp, robot_vel=np.zeros((1, 2)))
+        assert np.array_equal(f.pos, ref.pos), t
+        assert np.array_equal(f.vel, ref.vel), t
