@@ -25,7 +25,21 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 MIX = {"Flat": 0.25, "Slope": 0.25, "Stair": 0.25, "Rough": 0.25}
-CFG = dict(extent=32.0, res=0.125, objects=64, peds=32, steps_cfg=500)
+# BASELINE.json configs mapped onto the reference API.  cfg2 is the
+# bench default (the metric's single-GPU config); the others are --config runs.
+CONFIGS = {
+    "cfg1": dict(envs=16, extent=32.0, res=0.125 * 2, objects=20, peds=8, task="NavDynamic", nd=5.0,
+                 resample=0.0, steps_cfg=100),
+    "cfg2": dict(envs=1024, extent=32.0, res=0.125, objects=64, peds=32, task="NavDynamic", nd=5.0,
+                 resample=0.0, steps_cfg=500),
+    "cfg3": dict(envs=4096, extent=32.0, res=0.125, objects=100, peds=64, task="NavDynamic", nd=5.0,
+                 resample=0.0, steps_cfg=1000),
+    "cfg4": dict(envs=512, extent=64.0, res=0.125, objects=0, peds=1024, task="NavClear", nd=3.0,
+                 resample=0.0, steps_cfg=200),
+    "cfg5": dict(envs=8192, extent=32.0, res=0.125, objects=128, peds=48, task="NavDynamic", nd=5.0,
+                 resample=0.02, steps_cfg=2000),
+}
+CFG = dict(CONFIGS["cfg2"])
 METRIC = "env-steps/sec and scenes sampled/sec at N envs on 1/2/4/8 B200; % of HBM peak"
 
 
@@ -88,12 +102,15 @@ class Clocks:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": str(exc)[:80]}
 
 
-def make_spec():
+def make_spec(cfg=None):
     from paper_2505_00690_b200.urbangen import SceneSpec, TaskKind
-    area_objects = int(np.floor(4.0 * (256 * 256 * 0.125 * 0.125) / 100.0 + 0.5))  # 41
-    return SceneSpec(seed=0, extent_m=(CFG["extent"], CFG["extent"]), task_kind=TaskKind.NAV_DYNAMIC,
-                     object_density=CFG["objects"] / area_objects, pedestrian_count=CFG["peds"],
-                     terrain_mix=MIX, grid_resolution_m=CFG["res"])
+    cfg = cfg or CFG
+    n = int(np.ceil(cfg["extent"] / cfg["res"]))
+    base = int(np.floor(4.0 * (n * n * cfg["res"] * cfg["res"]) / 100.0 + 0.5))  # 41 at 32 m
+    dens = cfg["objects"] / base if cfg["objects"] else 0.0
+    return SceneSpec(seed=0, extent_m=(cfg["extent"], cfg["extent"]), task_kind=TaskKind(cfg["task"]),
+                     object_density=dens, pedestrian_count=cfg["peds"],
+                     terrain_mix=MIX, grid_resolution_m=cfg["res"])
 
 
 # ============================================================================ ours
@@ -115,6 +132,7 @@ def run_ours(args):
     from paper_2505_00690_b200 import shard
     E = args.envs
     spec = make_spec()
+    nx = int(np.ceil(CFG["extent"] / CFG["res"]))
     zero = torch.zeros(E, dtype=torch.int64, device=dev)
     gids = torch.from_numpy(shard.env_ids(rank, world, E)).to(dev)   # rank owns [r*E, (r+1)*E)
     env_seeds = child_seeds_device(zero, "env", gids)
@@ -140,15 +158,16 @@ def run_ours(args):
     b.check_status()
 
     # ---- crowd
-    f = CrowdField(b, CrowdConfig(), [int(s) for s in run_seeds], device=dev, threads=args.threads)
+    f = CrowdField(b, CrowdConfig(neighbor_distance=CFG["nd"]), [int(s) for s in run_seeds], device=dev,
+                   threads=args.threads)
     f.set_from_spawn(b)
     f.prepare_step()
     # robot: static at a seeded walkable cell per env (route anchors are §8f), zero velocity
     g = torch.Generator(device="cpu").manual_seed(1234 + rank)
     pick = (torch.rand(E, generator=g).to(dev) * b.walk_n.double()).long()
     cell = b.walk.gather(1, pick[:, None])[:, 0].long()
-    rpos = torch.stack([((cell % 256).double() + 0.5) * CFG["res"],
-                        ((cell // 256).double() + 0.5) * CFG["res"]], dim=1).contiguous()
+    rpos = torch.stack([((cell % nx).double() + 0.5) * CFG["res"],
+                        ((cell // nx).double() + 0.5) * CFG["res"]], dim=1).contiguous()
     rvel = torch.zeros_like(rpos)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > L2
     for _ in range(args.warmup):
@@ -162,10 +181,32 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    resampled = 0
+    if CFG["resample"] > 0:
+        # cfg5 driver: env i re-sampled at step t iff
+        # make_rng(0, "resample-mix", t).random(E) < p, via BatchedEnv.reset semantics
+        from paper_2505_00690_b200.rng import child_seed as _cs
+        masks = [np.flatnonzero(np.random.Generator(np.random.PCG64(_cs(0, "resample-mix", k)))
+                                .random(E * world)[rank * E:(rank + 1) * E] < CFG["resample"])
+                 for k in range(args.steps)]
+        counts = torch.zeros(E, dtype=torch.int64, device=dev)
+    def resample_mix(k):
+        nonlocal resampled
+        if CFG["resample"] > 0 and masks[k].size:
+            sl = torch.from_numpy(masks[k]).to(dev)
+            counts[sl] += 1
+            env_k = env_seeds[sl]
+            new_scene = child_seeds_device(env_k, "resample", counts[sl])
+            sampler.sample(new_scene, child_seeds_device(env_k, "crowd", counts[sl]), slots=sl,
+                           check=False)
+            f.set_from_spawn(b, rows=sl)
+            resampled += int(masks[k].size)
+
     with Clocks(dev.index) as clk:
         for k in range(args.steps):
             flush.fill_(float(k))          # L2 flush between timed steps (untimed)
             starts[k].record(st)
+            resample_mix(k)
             f.step(rpos, rvel, 0.35, check=False)
             ends[k].record(st)
         torch.cuda.synchronize()
@@ -202,9 +243,10 @@ def run_ours(args):
     e2e_steps = min(args.steps, args.e2e_steps)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
+    for k in range(e2e_steps):
         rp = rpos_h.to(dev, non_blocking=True)
         rv = rvel_h.to(dev, non_blocking=True)
+        resample_mix(k)
         f.step(rp, rv, 0.35, check=False)
         out_pos.copy_(f.pos_t, non_blocking=True)
         out_vel.copy_(f.vel_t, non_blocking=True)
@@ -249,9 +291,13 @@ def run_ours(args):
             "n_gpus": world, "steps": steps, "warmup": args.warmup,
             "ms_per_step": round(avg_ms, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded procedural scenes)",
-            "config": {"workload": "cfg2: 1024 envs/GPU, 256x256 grid (0.125 m), 64 objects, "
-                                   "32 pedestrians/env, NavDynamic, dynamics step (+ scene sampling)",
-                       "envs_per_gpu": E, "grid": [256, 256], "objects": 64, "peds": CFG["peds"],
+            "config": {"workload": f"{args.config}: {E} envs/GPU, {nx}x{nx} grid ({CFG['res']} m), "
+                                   f"{CFG['objects']} objects, {CFG['peds']} pedestrians/env, {CFG['task']}, "
+                                   f"neighbor_distance {CFG['nd']} m, dynamics step (+ scene sampling)"
+                                   + (f", Bernoulli({CFG['resample']}) re-sampling inside each step"
+                                      if CFG["resample"] else ""),
+                       "envs_per_gpu": E, "grid": [nx, nx], "objects": CFG["objects"], "peds": CFG["peds"],
+                       "resampled_envs": resampled,
                        "parallelism": f"env-shard x{world}", "l2": "flushed (256 MB write) between timed steps",
                        "robot": "static per env at a seeded walkable cell, zero velocity"},
             "scenes_per_sec": round(scenes, 1), "sample_ms_per_batch": round(sample_ms, 3),
@@ -295,30 +341,32 @@ def cpu_baseline_sample(b, f, run_seeds, n_env=4, steps=6):
         agents.append(dict(pos=b.sp_pos[i].cpu().numpy(), goal=b.sp_goal[i].cpu().numpy(),
                            radius=np.array([C.RADIUS[x] for x in k]), pref=b.sp_pref[i].cpu().numpy(),
                            max_speed=np.array([C.MAX_SPEED[x] for x in k]), kind=k))
-    ref = C.CrowdFieldOracle(grids, C.Config(), [int(s) for s in run_seeds[:n_env]])
+    ref = C.CrowdFieldOracle(grids, C.Config(neighbor_distance=CFG["nd"]), [int(s) for s in run_seeds[:n_env]])
     ref.set_agents(agents)
     t0 = time.perf_counter()
     for _ in range(steps):
         ref.step()
     dt = time.perf_counter() - t0
     return {"value": round(n_env * steps / dt, 3), "unit": "env-steps/s", "cores": 1,
-            "kind": "port", "sample": f"{n_env} cfg2 envs x {steps} crowd ticks, oracle port, 1 thread"}
+            "kind": "port", "sample": f"{n_env} envs of this config x {steps} crowd ticks, oracle port, 1 thread"}
 
 
 # ============================================================================ reference arm
 def _ref_worker(args):
-    """One process: generate its cfg2 env with the oracle, then time `steps` ticks."""
-    env_id, steps, warm = args
+    """One process: generate its env with the oracle, then time `steps` ticks."""
+    env_id, steps, warm, cfg = args
     from oracle import crowd as C
     from oracle import scene as S
     from oracle.rng import child_seed
     import json as _json
     cat = S.load_catalog_tuples(_json.load(open(os.path.join(ROOT, "paper_2505_00690_b200", "data", "catalog.json"))))
     s = child_seed(0, "env", env_id)
-    sc = S.generate_scene(dict(seed=s, extent=(32.0, 32.0), res=0.125, task="NavDynamic", split="Train",
-                               density=64 / 41, mix=MIX), cat)
-    sp = C.spawn_agents(sc["labels"], 0.125, CFG["peds"], child_seed(s, "crowd", 0))
-    f = C.CrowdFieldOracle([(sc["labels"], 0.125)], C.Config(), [child_seed(s, "crowd-run")])
+    spec = make_spec(cfg)
+    sc = S.generate_scene(dict(seed=s, extent=spec.extent_m, res=cfg["res"], task=cfg["task"], split="Train",
+                               density=spec.object_density, mix=MIX), cat)
+    sp = C.spawn_agents(sc["labels"], cfg["res"], cfg["peds"], child_seed(s, "crowd", 0))
+    f = C.CrowdFieldOracle([(sc["labels"], cfg["res"])], C.Config(neighbor_distance=cfg["nd"]),
+                           [child_seed(s, "crowd-run")])
     f.set_agents([sp])
     for _ in range(warm):
         f.step()
@@ -341,7 +389,7 @@ def run_reference(args):
     warm = max(0, min(args.warmup, 5))
     with mp.get_context("spawn").Pool(cores) as pool:
         t0 = time.perf_counter()
-        times = pool.map(_ref_worker, [(i, steps, warm) for i in range(cores)])
+        times = pool.map(_ref_worker, [(i, steps, warm, dict(CFG)) for i in range(cores)])
         wall = time.perf_counter() - t0
     per_step = np.max(np.array(times), axis=0)       # all cores step in parallel
     total = float(per_step.sum())
@@ -351,12 +399,12 @@ def run_reference(args):
             "ms_per_step": round(1e3 * total / steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded procedural scenes)",
-            "config": {"workload": "cfg2 shape: 256x256 grid (0.125 m), 64 objects, 32 peds/env; "
-                                   "sample of one env per host core",
+            "config": {"workload": f"{args.config} shape: {CFG['extent']} m at {CFG['res']} m, "
+                                   f"{CFG['objects']} objects, {CFG['peds']} peds/env; sample of one env per host core",
                        "envs": cores, "parallelism": f"{cores} processes"},
             "cpu_baseline": {"value": round(value, 3), "unit": "env-steps/s", "cores": cores,
                              "kind": "port",
-                             "sample": f"{cores} cfg2 envs (one per core) x {steps} crowd ticks; "
+                             "sample": f"{cores} {args.config} envs (one per core) x {steps} crowd ticks; "
                                        f"oracle port of the reference algorithm; wall {wall:.1f}s incl. scene gen"},
             "e2e": {"value": round(value, 3), "unit": "env-steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -368,7 +416,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--envs", type=int, default=1024)
+    ap.add_argument("--envs", type=int, default=None)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--threads", type=int, default=128)
     ap.add_argument("--sample-warmup", type=int, default=1)
@@ -379,6 +428,10 @@ def main():
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per launch of the dominant kernel from an ncu --set full capture")
     args = ap.parse_args()
+    CFG.clear()
+    CFG.update(CONFIGS[args.config])
+    if args.envs is None:
+        args.envs = CFG["envs"]
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":

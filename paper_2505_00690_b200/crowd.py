@@ -128,8 +128,9 @@ class CrowdField:
                                               _lib.stream_ptr()), "cw_seed_streams")
         N = self.nx * self.ny
         self.path_cap = int(path_cap or 2 * (self.nx + self.ny) + 64)
-        self.heap_cap = int(heap_cap or max(65536, 2 * N))
-        self.astar_ctas = int(torch.cuda.get_device_properties(self.device).multi_processor_count) \
+        self.heap_cap = int(heap_cap or min(max(65536, N), (1 << 19) - 1))
+        # persistent A* search warps: 3 per SM (64 KB open list each), one scratch slot each
+        self.astar_ctas = 3 * int(torch.cuda.get_device_properties(self.device).multi_processor_count) \
             if self.device.type == "cuda" else 1
         self.last_gap_t = torch.full((self.E,), float("inf"), dtype=torch.float64, device=self.device)
         self.gap_tmp_t = torch.zeros((self.E,), dtype=torch.float64, device=self.device)
@@ -203,7 +204,7 @@ class CrowdField:
         d = self.device
         self.astar_rec_t = torch.zeros((S, N, 2), dtype=torch.int64, device=d)  # {g, parent|stamp}
         self.astar_epoch_t = torch.zeros((S,), dtype=torch.int32, device=d)
-        self.astar_heap_t = torch.empty((S, self.heap_cap, 2), dtype=torch.int64, device=d)
+        self.astar_heap_t = torch.empty((S, self.heap_cap, 2), dtype=torch.int64, device=d)  # open-list spill
         self._astar_ready = True
 
     def set_agents(self, agent_lists):

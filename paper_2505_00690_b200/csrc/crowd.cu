@@ -28,6 +28,7 @@ constexpr int MAXC = 12;   // neighbour lanes (<= 10) + robot + static
 constexpr double kWaypointReach = 0.5, kStrayLimit = 1.0;
 // open-list entries kept in shared memory by k_astar (16 B each: f bits, h bits | cell)
 CW_HD int astar_smem_entries() { return 4096; }
+constexpr int kAstarCtasPerSm = 3;
 
 struct HeapEnt { double f; int32_t cell; int32_t pad; };
 
@@ -225,7 +226,7 @@ CW_DEV double octile(int r, int c, int gr, int gc) {
 struct AstarRec { double g; int32_t parent; uint32_t tag; };  // tag = epoch << 14 | heap pos
 struct AstarReq { int32_t env, agent, start, goal; };
 
-constexpr uint32_t kPosBits = 14, kPosMask = (1u << kPosBits) - 1, kClosed = kPosMask;
+constexpr uint32_t kPosBits = 19, kPosMask = (1u << kPosBits) - 1, kClosed = kPosMask;
 constexpr uint32_t kEpochMax = (1u << (32 - kPosBits)) - 1;
 
 // Open set of the search, scanned by the whole warp.  Pop order must equal the
@@ -260,7 +261,7 @@ CW_DEV bool ent_less(unsigned long long fa, unsigned long long ka, unsigned long
 
 __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state S, int smem_cap) {
   extern __shared__ __align__(16) unsigned char sm[];
-  OpenEnt* O = reinterpret_cast<OpenEnt*>(sm);
+  OpenEnt* const Osm = reinterpret_cast<OpenEnt*>(sm);
   const int lane = threadIdx.x;
   const int nx = P.nx, ny = P.ny;
   const size_t N = (size_t)nx * ny;
@@ -268,7 +269,8 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
   const AstarReq* reqs = reinterpret_cast<const AstarReq*>(S.astar_req);
   const int mdr[8] = {-1, 1, 0, 0, -1, -1, 1, 1};
   const int mdc[8] = {0, 0, -1, 1, -1, 1, -1, 1};
-  const int cap = min(smem_cap, (int)kClosed);
+  OpenEnt* const Ogl = reinterpret_cast<OpenEnt*>(S.astar_heap) + (size_t)blockIdx.x * P.heap_cap;
+  const int gcap = min(P.heap_cap, (int)kClosed);
   const unsigned lt_mask = (1u << lane) - 1u;
   const unsigned long long CELLM = (1ull << kCellBits) - 1ull;
   long long expansions = 0, t_max = 0, t_sum = 0;
@@ -301,6 +303,8 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
     const uint32_t ep = epoch << kPosBits;
     int found = 0;  // 1 found, 0 none, -1 open-list overflow
     int n = 0;
+    OpenEnt* O = Osm;                 // spills to the global slot when full
+    int cap = min(smem_cap, gcap);
     if (passbit(pb, start) && passbit(pb, goal) && reach[start] == reach[goal]) {
       if (lane == 0) {
         const double h0 = octile(sr, sc, gr, gc);
@@ -400,7 +404,17 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
         }
         __syncwarp();
         const unsigned im = __ballot_sync(0xffffffffu, ins);
-        if (n + __popc(im) > cap) { found = -1; break; }
+        if (n + __popc(im) > cap) {
+          if (O == Osm && n + __popc(im) <= gcap) {
+            for (int k = lane; k < n; k += 32) Ogl[k] = Osm[k];
+            __syncwarp();
+            O = Ogl;
+            cap = gcap;
+          } else {
+            found = -1;
+            break;
+          }
+        }
         if (ins) {
           pos = n + __popc(im & lt_mask);
           rec[y].tag = ep | (uint32_t)pos;

@@ -257,7 +257,7 @@ class SceneBatch:
         self.status = z((E,), dtype=torch.int32, **d)
         self.scene_seed = z((E,), dtype=torch.int64, **d)
         self._scratch_rows = 0
-        self._ensure_scratch(E)
+        self._ensure_scratch(min(E, SceneSampler.max_rows))
 
     def _ensure_scratch(self, rows):
         import torch
@@ -322,6 +322,8 @@ class SceneSampler:
         self.params = scene_params(spec, self.catalog)
         self.batch = SceneBatch(self.params, capacity, device)
 
+    max_rows = 2048   # envs per cw_sample_scenes call (bounds the scratch footprint)
+
     def sample(self, scene_seeds, crowd_seeds=None, slots=None, stream=None, check=True):
         """Sample len(scene_seeds) scenes into rows ``slots`` (default 0..E-1).
 
@@ -331,6 +333,19 @@ class SceneSampler:
         seeds = _as_u64_tensor(scene_seeds, dev)
         E = seeds.numel()
         if E == 0:
+            return self.batch
+        if E > self.max_rows:
+            if crowd_seeds is None and self.params.peds > 0:
+                from .rng import child_seeds_device
+                crowd_seeds = child_seeds_device(seeds, "crowd", 0)
+            cs = None if crowd_seeds is None else _as_u64_tensor(crowd_seeds, dev)
+            sl = (torch.arange(E, device=dev) if slots is None
+                  else torch.as_tensor(slots, dtype=torch.int64, device=dev))
+            for k in range(0, E, self.max_rows):
+                part = slice(k, min(E, k + self.max_rows))
+                self.sample(seeds[part], None if cs is None else cs[part], sl[part], stream, check=False)
+            if check:
+                self.batch.check_status(sl)
             return self.batch
         if crowd_seeds is None and self.params.peds > 0:
             # first spawn of an env whose env seed is its scene seed (batch.py:179)
