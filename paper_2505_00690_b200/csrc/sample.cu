@@ -268,9 +268,7 @@ __global__ void __launch_bounds__(256) k_zones(cw_scene_params P, int E, const i
   const int slot = env_slot(slots, e);
   __shared__ Courtyard C;
   __shared__ Rect strip;
-  __shared__ int any_walk;
   if (threadIdx.x == 0) {
-    any_walk = 0;
     if (P.layout == 0) {
       Pcg64 rng = pcg_load(seeds[e].zones);
       courtyard_draw(P, rng, C);
@@ -365,7 +363,7 @@ CW_DEV void connect_blocks(uint64_t seed, int rows, int cols, BlockLayout& L) {
 }
 
 CW_DEV bool in_road(const cw_scene_params& P, const BlockLayout& L, double ox, double oy, int r,
-                    int c, Rect* scratch = nullptr) {
+                    int c) {
   const double bs = 20.0, rw = 6.0;
   for (int i = 0; i < L.n; ++i) {
     int br = i / P.bcols, bc = i % P.bcols;
@@ -389,7 +387,6 @@ __global__ void __launch_bounds__(512) k_zones_blk(cw_scene_params P, int E, con
   const int nx = P.nx, ny = P.ny, N = nx * ny;
   __shared__ BlockLayout L;
   __shared__ double rowbuf[2][1024 + 1];
-  __shared__ unsigned long long shmin[NT / 32];
   double* D = B.scratch_f64 + (size_t)e * (size_t)max(P.obj_max * 8, N);
   uint8_t* Z = B.zones + (size_t)slot * N;
   const double bs = 20.0, rw = 6.0;
@@ -516,7 +513,6 @@ __global__ void __launch_bounds__(512) k_zones_blk(cw_scene_params P, int E, con
   }
   mine = __syncthreads_or(mine);
   if (threadIdx.x == 0 && !mine) B.status[slot] = CW_E_EXTENT;
-  (void)shmin;
 }
 
 // ================================================================= terrain
@@ -1158,30 +1154,38 @@ __global__ void __launch_bounds__(256) k_raster(cw_scene_params P, int E, const 
   const size_t N = (size_t)P.nx * P.ny;
   const int q = blockIdx.x * blockDim.x + threadIdx.x;  // quad index
   if ((size_t)q * 4 >= N) return;
-  __shared__ int8_t code[CW_MAX_TILES];
-  __shared__ double tp[CW_MAX_TILES * 4];
-  // (tables are tiny; every thread block reloads them)
   const int f0 = q * 4;
-  const int r = f0 / P.nx, c0 = f0 - r * P.nx;
   const uint8_t* Z = B.zones + slot * N;
-  uchar4 zz = *reinterpret_cast<const uchar4*>(Z + f0);
-  // zone lookup at the same resolution: rr = min((r+0.5)*res/zone_res, zy-1) == r
-  uchar4 lb = make_uchar4(zone_to_label(zz.x), zone_to_label(zz.y), zone_to_label(zz.z),
-                          zone_to_label(zz.w));
-  *reinterpret_cast<uchar4*>(B.labels + slot * N + f0) = lb;
   const int32_t* A = B.assign + (size_t)slot * P.trows * P.tcols;
   const int8_t* cd = B.tile_code + (size_t)slot * CW_MAX_TILES;
   const double* p = B.tile_p + (size_t)slot * CW_MAX_TILES * 4;
   const uint64_t noise = B.noise_seed[slot];
-  const double y = ((double)r + 0.5) * P.res;
-  float ev[4];
+  // zone lookup at the same resolution: rr = min((r+0.5)*res/zone_res, zy-1) == r
+  if ((P.nx & 3) == 0 && (N & 3) == 0) {
+    // fast path: the 4 cells share a row -> uchar4 label + float4 elevation stores
+    const int r = f0 / P.nx, c0 = f0 - r * P.nx;
+    const uchar4 zz = *reinterpret_cast<const uchar4*>(Z + f0);
+    const uchar4 lb = make_uchar4(zone_to_label(zz.x), zone_to_label(zz.y), zone_to_label(zz.z),
+                                  zone_to_label(zz.w));
+    *reinterpret_cast<uchar4*>(B.labels + slot * N + f0) = lb;
+    const double y = ((double)r + 0.5) * P.res;
+    float ev[4];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    double x = ((double)(c0 + k) + 0.5) * P.res;
-    ev[k] = (float)elevation_at(x, y, P.trows, P.tcols, A, cd, p, noise);
+    for (int k = 0; k < 4; ++k) {
+      const double x = ((double)(c0 + k) + 0.5) * P.res;
+      ev[k] = (float)elevation_at(x, y, P.trows, P.tcols, A, cd, p, noise);
+    }
+    *reinterpret_cast<float4*>(B.elev + slot * N + f0) = make_float4(ev[0], ev[1], ev[2], ev[3]);
+  } else {
+    for (int k = 0; k < 4; ++k) {
+      const int f = f0 + k;
+      if ((size_t)f >= N) break;
+      const int r = f / P.nx, c = f - r * P.nx;
+      B.labels[slot * N + f] = zone_to_label(Z[f]);
+      const double x = ((double)c + 0.5) * P.res, y = ((double)r + 0.5) * P.res;
+      B.elev[slot * N + f] = (float)elevation_at(x, y, P.trows, P.tcols, A, cd, p, noise);
+    }
   }
-  *reinterpret_cast<float4*>(B.elev + slot * N + f0) = make_float4(ev[0], ev[1], ev[2], ev[3]);
-  (void)code; (void)tp;
 }
 
 // warp per (env, object): footprint cells -> OBSTACLE (occupancy.py:49-51)
