@@ -28,7 +28,6 @@ constexpr int MAXC = 12;   // neighbour lanes (<= 10) + robot + static
 constexpr double kWaypointReach = 0.5, kStrayLimit = 1.0;
 // open-list entries kept in shared memory by k_astar (16 B each: f bits, h bits | cell)
 CW_HD int astar_smem_entries() { return 4096; }
-constexpr int kAstarCtasPerSm = 3;
 
 struct HeapEnt { double f; int32_t cell; int32_t pad; };
 

@@ -315,3 +315,37 @@ def test_blocks_layout_dense_crowd_matches_oracle(torch_cuda):
         ref.step(robot_pos=rp, robot_vel=np.zeros((1, 2)))
         assert np.array_equal(f.pos, ref.pos), t
         assert np.array_equal(f.vel, ref.vel), t
+
+
+@pytest.mark.parametrize("ext,res,task,peds", [((13.3, 17.7), 0.1, "NavStatic", 5),
+                                              ((21.0, 9.5), 0.25, "NavDynamic", 6),
+                                              ((44.0, 40.5), 0.5, "NavStatic", 12),
+                                              ((30.0, 12.0), 0.2, "Traverse", 4)])
+def test_odd_shaped_scenes_match_oracle(ext, res, task, peds, torch_cuda):
+    """Non-square grids whose width is not a multiple of 4, block and strip
+    layouts, Traverse regions: every sampling output bit-exact vs the oracle."""
+    from oracle import crowd as C
+    from oracle import scene as S
+    from oracle.rng import child_seed
+    from paper_2505_00690_b200.urbangen import SceneSampler, SceneSpec, TaskKind
+    mix = {"Flat": 0.3, "Slope": 0.3, "Stair": 0.2, "Rough": 0.2}
+    for i in range(2):
+        seed = child_seed(31, "env", i)
+        spec = SceneSpec(seed=seed, extent_m=ext, task_kind=TaskKind(task), object_density=1.0,
+                         pedestrian_count=peds, terrain_mix=mix, grid_resolution_m=res)
+        b = SceneSampler(spec, 1).sample([seed], [child_seed(seed, "crowd", 0)])
+        sc = S.generate_scene(dict(seed=seed, extent=ext, res=res, task=task, split="Train",
+                                   density=1.0, mix=mix), golden_catalog())
+        assert np.array_equal(b.zones[0].cpu().numpy(), sc["zones"])
+        assert np.array_equal(b.assign[0].cpu().numpy(), sc["assign"])
+        assert np.array_equal(b.labels[0].cpu().numpy(), sc["labels"])
+        assert np.array_equal(b.elev[0].cpu().numpy().view(np.uint32), sc["elev"].view(np.uint32))
+        m = int(b.obj_n[0])
+        assert m == len(sc["objects"])
+        near = C.nearest_obstacle_map(sc["labels"])
+        if near is not None:
+            assert np.array_equal(b.nearest[0].cpu().numpy(), near)
+        if task != "Traverse":   # traverse spawn uses the segment mask (batch.py:174-176)
+            sp = C.spawn_agents(sc["labels"], res, peds, child_seed(seed, "crowd", 0))
+            assert np.array_equal(b.sp_pos[0, :peds].cpu().numpy(), sp["pos"])
+            assert np.array_equal(b.sp_goal[0, :peds].cpu().numpy(), sp["goal"])
