@@ -83,7 +83,9 @@ typedef struct cw_scene_buffers {
   int32_t* nearest; uint8_t* has_obs;
   int32_t* walk; int32_t* walk_n;
   int32_t* reach;       /* (E, ny*nx) 4-connected component of passable cells, -1 = obstacle */
-  uint32_t* passbits;   /* (E, ceil(ny*nx/32)) bit f = labels[f] != OBSTACLE */
+  uint8_t* moves;       /* (E, ny*nx) A* move table: bit d set iff move d (N S W E NW NE SW SE)
+                           from the cell is legal (paths.py:70-72: in bounds, passable,
+                           diagonals need both orthogonal cells passable) */
   double* sp_pos; double* sp_goal; int8_t* sp_kind; double* sp_pref;
   int32_t* status;
   int32_t* scratch_i32; /* (E, 10*ny*nx) */
@@ -103,7 +105,7 @@ int cw_spawn_agents(const cw_scene_params* params, int E, const uint64_t* crowd_
                     void* stream);
 
 /* _prepare_env for caller-supplied labels (field.py:60-67): fills nearest,
- * has_obs, walk, walk_n, reach, passbits of rows slots[e] from buffers->labels; needs status
+ * has_obs, walk, walk_n, reach, moves of rows slots[e] from buffers->labels; needs status
  * (zeroed) and scratch_i32.  Only params->nx/ny are read. */
 int cw_prepare_envs(const cw_scene_params* params, int E, const int32_t* slots,
                     const cw_scene_buffers* buffers, void* stream);
@@ -118,8 +120,8 @@ typedef struct cw_crowd_params {
   int32_t max_neighbors;
   double dt, safety_margin, goal_reach2, stall_c, stall_s;
   int32_t resample_goals, use_static, path_cap;
-  int32_t heap_cap;     /* global open-list spill entries per A* CTA */
-  int32_t astar_ctas;   /* persistent k_astar CTAs (one scratch slot each) */
+  int32_t heap_cap;     /* A* far-pool entries (16 B) per k_astar CTA */
+  int32_t astar_ctas;   /* persistent k_astar CTAs, one search warp each (one per SM) */
 } cw_crowd_params;
 
 /* Device-resident CrowdField state (field.py:47-58) + guidance/A* scratch. */
@@ -130,12 +132,12 @@ typedef struct cw_crowd_state {
   int32_t* path_cells; int32_t* path_head; int32_t* path_n;
   const uint8_t* labels; const int32_t* nearest; const uint8_t* has_obs;
   const int32_t* walk; const int32_t* walk_n;
-  const int32_t* reach; const uint32_t* passbits;
+  const int32_t* reach; const uint8_t* moves;
   void* rng;
   double* last_gap; double* gap_tmp; int32_t* flags;
-  void* astar_rec;      /* (astar_ctas, ny*nx) {double g; int32 parent; int32 stamp} */
-  int32_t* astar_epoch; /* (astar_ctas) */
-  void* astar_heap;     /* (astar_ctas, heap_cap, 16 B) open-list spill area */
+  void* astar_rec;      /* astar_ctas x cw_astar_slot_bytes(nx, ny): overflow g/move tiles,
+                           parent per cell, tile-slot map (no initialisation needed) */
+  void* astar_heap;     /* (astar_ctas, heap_cap, 16 B) A* far pool */
   void* astar_req;      /* (E*A, 16 B) replanning queue {env, agent, start, goal} */
   int64_t* counters;
 } cw_crowd_state;
@@ -153,8 +155,8 @@ int cw_crowd_step_phases(const cw_crowd_params* params, const cw_crowd_state* st
                          const double* robot_pos, const double* robot_vel, double robot_radius,
                          const uint8_t* env_mask, int threads, int phases, void* stream);
 
-/* k_astar open-list entries held in shared memory (host-only query). */
-int cw_astar_smem_entries(void);
+/* Bytes of astar_rec per k_astar CTA for an nx x ny grid (host-only query). */
+size_t cw_astar_slot_bytes(int nx, int ny);
 
 int cw_seed_streams(int n, const uint64_t* seeds, void* out_states, void* stream);
 

@@ -12,9 +12,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB_PATH = os.path.join(HERE, "libcitywalk_b200.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("sample.cu", "crowd.cu")]
-HEADERS = [os.path.join(HERE, "csrc", f) for f in
-           ("common.cuh", "rng.cuh", "scene_types.cuh", "crowd_types.cuh")] + [
-    os.path.join(ROOT, "include", "citywalk_b200.h")]
+HEADERS = sorted(os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))
+                 if f.endswith(".cuh")) + [os.path.join(ROOT, "include", "citywalk_b200.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
               "-std=c++17", "-Xcompiler", "-fPIC", "-shared"]
 
@@ -41,7 +40,7 @@ class SceneParams(ctypes.Structure):
 SCENE_BUFFER_FIELDS = [
     "zones", "labels", "elev", "assign", "n_tiles", "tile_code", "tile_kind", "tile_param",
     "tile_p", "tile_w", "allowed", "noise_seed", "wfc_attempts", "obj_cat", "obj_pose", "obj_n",
-    "overflow", "nearest", "has_obs", "walk", "walk_n", "reach", "passbits", "sp_pos", "sp_goal", "sp_kind", "sp_pref",
+    "overflow", "nearest", "has_obs", "walk", "walk_n", "reach", "moves", "sp_pos", "sp_goal", "sp_kind", "sp_pref",
     "status", "scratch_i32", "scratch_f64",
 ]
 
@@ -63,8 +62,8 @@ class CrowdParams(ctypes.Structure):
 
 CROWD_STATE_FIELDS = [
     "pos", "vel", "goal", "waypoint", "radius", "pref_speed", "max_speed", "active", "path_cells",
-    "path_head", "path_n", "labels", "nearest", "has_obs", "walk", "walk_n", "reach", "passbits",
-    "rng", "last_gap", "gap_tmp", "flags", "astar_rec", "astar_epoch", "astar_heap", "astar_req",
+    "path_head", "path_n", "labels", "nearest", "has_obs", "walk", "walk_n", "reach", "moves",
+    "rng", "last_gap", "gap_tmp", "flags", "astar_rec", "astar_heap", "astar_req",
     "counters",
 ]
 
@@ -75,7 +74,7 @@ class CrowdState(ctypes.Structure):
 
 EXPORTS = ["cw_scene_seed_scratch_bytes", "cw_sample_scenes", "cw_spawn_agents", "cw_prepare_envs",
            "cw_crowd_step_smem_bytes",
-           "cw_crowd_step", "cw_crowd_step_phases", "cw_astar_smem_entries", "cw_seed_streams", "cw_child_seeds", "cw_abi_sizes"]
+           "cw_crowd_step", "cw_crowd_step_phases", "cw_astar_slot_bytes", "cw_seed_streams", "cw_child_seeds", "cw_abi_sizes"]
 
 _lib = None
 
@@ -119,8 +118,8 @@ def lib():
     L.cw_crowd_step_phases.restype = ctypes.c_int
     L.cw_crowd_step_phases.argtypes = [ctypes.POINTER(CrowdParams), ctypes.POINTER(CrowdState), P,
                                        P, ctypes.c_double, P, ctypes.c_int, ctypes.c_int, P]
-    L.cw_astar_smem_entries.restype = ctypes.c_int
-    L.cw_astar_smem_entries.argtypes = []
+    L.cw_astar_slot_bytes.restype = ctypes.c_size_t
+    L.cw_astar_slot_bytes.argtypes = [ctypes.c_int, ctypes.c_int]
     L.cw_seed_streams.restype = ctypes.c_int
     L.cw_seed_streams.argtypes = [ctypes.c_int, P, P, P]
     L.cw_child_seeds.restype = ctypes.c_int

@@ -104,7 +104,7 @@ class CrowdField:
             self.res0 = self.res
             self.labels_t, self.nearest_t, self.has_obs_t = b.labels, b.nearest, b.has_obs
             self.walk_t, self.walk_n_t = b.walk, b.walk_n
-            self.reach_t, self.passbits_t = b.reach, b.passbits
+            self.reach_t, self.moves_t = b.reach, b.moves
             self._batch = b
         else:
             occs = list(occupancies)
@@ -129,8 +129,8 @@ class CrowdField:
         N = self.nx * self.ny
         self.path_cap = int(path_cap or 2 * (self.nx + self.ny) + 64)
         self.heap_cap = int(heap_cap or min(max(65536, N), (1 << 19) - 1))
-        # persistent A* search warps: 3 per SM (64 KB open list each), one scratch slot each
-        self.astar_ctas = 3 * int(torch.cuda.get_device_properties(self.device).multi_processor_count) \
+        # persistent A* search warps: one per SM (each owns ~200 KB of shared memory)
+        self.astar_ctas = int(torch.cuda.get_device_properties(self.device).multi_processor_count) \
             if self.device.type == "cuda" else 1
         self.last_gap_t = torch.full((self.E,), float("inf"), dtype=torch.float64, device=self.device)
         self.gap_tmp_t = torch.zeros((self.E,), dtype=torch.float64, device=self.device)
@@ -150,7 +150,7 @@ class CrowdField:
         self.walk_t = torch.empty((E, ny * nx), dtype=torch.int32, device=self.device)
         self.walk_n_t = torch.zeros((E,), dtype=torch.int32, device=self.device)
         self.reach_t = torch.empty((E, ny * nx), dtype=torch.int32, device=self.device)
-        self.passbits_t = torch.zeros((E, (ny * nx + 31) // 32), dtype=torch.int32, device=self.device)
+        self.moves_t = torch.zeros((E, ny * nx), dtype=torch.uint8, device=self.device)
         self._prepare(None)
 
     def _prepare(self, rows):
@@ -168,7 +168,7 @@ class CrowdField:
         b.walk = self.walk_t.data_ptr()
         b.walk_n = self.walk_n_t.data_ptr()
         b.reach = self.reach_t.data_ptr()
-        b.passbits = self.passbits_t.data_ptr()
+        b.moves = self.moves_t.data_ptr()
         b.status = status.data_ptr()
         b.scratch_i32 = scratch.data_ptr()
         sl = None if rows is None else torch.as_tensor(rows, dtype=torch.int32, device=self.device)
@@ -202,9 +202,9 @@ class CrowdField:
         S = self.astar_ctas
         N = self.nx * self.ny
         d = self.device
-        self.astar_rec_t = torch.zeros((S, N, 2), dtype=torch.int64, device=d)  # {g, parent|stamp}
-        self.astar_epoch_t = torch.zeros((S,), dtype=torch.int32, device=d)
-        self.astar_heap_t = torch.empty((S, self.heap_cap, 2), dtype=torch.int64, device=d)  # open-list spill
+        slot = int(_lib.lib().cw_astar_slot_bytes(self.nx, self.ny))
+        self.astar_rec_t = torch.empty((S * slot // 8,), dtype=torch.int64, device=d)
+        self.astar_heap_t = torch.empty((S, self.heap_cap, 2), dtype=torch.int64, device=d)  # far pool
         self._astar_ready = True
 
     def set_agents(self, agent_lists):
@@ -304,9 +304,9 @@ class CrowdField:
                  active=self.active_t, path_cells=self.path_cells_t, path_head=self.path_head_t,
                  path_n=self.path_n_t, labels=self.labels_t, nearest=self.nearest_t,
                  has_obs=self.has_obs_t, walk=self.walk_t, walk_n=self.walk_n_t, reach=self.reach_t,
-                 passbits=self.passbits_t, rng=self.rng_t,
+                 moves=self.moves_t, rng=self.rng_t,
                  last_gap=self.last_gap_t, gap_tmp=self.gap_tmp_t, flags=self.flags_t,
-                 astar_rec=self.astar_rec_t, astar_epoch=self.astar_epoch_t, astar_req=self.astar_req_t,
+                 astar_rec=self.astar_rec_t, astar_req=self.astar_req_t,
                  astar_heap=self.astar_heap_t, counters=self.counters_t)
         for k, v in m.items():
             setattr(s, k, v.data_ptr())
@@ -408,7 +408,7 @@ class CrowdField:
                 "lp_fallbacks": int(c[2]), "stall_retries": int(c[3]),
                 "astar_cycles": int(c[4]), "astar_max_cycles": int(c[5]),
                 "cta_cycles": int(c[6]), "cta_max_cycles": int(c[7]),
-                "astar_phase_cycles": [int(v) for v in c[8:12]], "astar_open_sum": int(c[12])}
+                "astar_stale_pops": int(c[10])}
 
 
 def step_crowd(agents, robot_state, occupancy, config, seed=0, resample_goals=True):

@@ -1,0 +1,614 @@
+// A* replanning search (paths.astar_path, reference crowd/paths.py:48-87) on B200.
+//
+// One warp runs one search; persistent warps pull requests queued by k_guide.
+// The open set is the reference's lazy heapq, reproduced entry for entry:
+// every push of paths.py:80-84 becomes one entry keyed (f, h, row, col), a
+// popped entry whose f exceeds g + h + 1e-12 is skipped (paths.py:70-71), and
+// the goal test precedes the stale test (paths.py:66-69).  Only the container
+// differs -- the pop order of a min-priority queue with unique keys is the
+// sorted order of its contents, whatever the data structure:
+//
+//   head  the (up to) 32 smallest keys, sorted, one per lane in registers.
+//         pop = lane 0 + one shuffle-down; insert = ballot rank + shuffle-up.
+//   near  unsorted entries with key < F2, in shared memory (NC entries).
+//   far   unsorted entries with key >= F2, in the warp's global slot.
+//   Invariant: every head key < T <= every near/far key.
+//   refill (head empty): band extraction -- near entries with
+//         f < fmin + delta are bitonic-sorted into the head (32 at a time,
+//         merged; the rest go back), near is compacted in the same pass and,
+//         when large, its part above fmin + delta2 is demoted to far.  When
+//         near is empty, far entries below a split key move to near.
+//   A decrease-key also drops the cell's stale entry from the head when it
+//   is there (a stale pop is a no-op in the reference).
+//
+// Key = (f bits, k2) compared as one unsigned 128-bit integer.  f, h >= 0, so
+// their IEEE bit patterns order like their values; distinct octile h values
+// differ by > 3e-4, so k2 keeps h's top 44 bits and puts (row << 10 | col)
+// in the low 20 bits, which orders like (row, col).
+//
+// Search-local cell state (g, the move byte) lives in 8x8-cell tiles in
+// shared memory, handed out on first write and released when the search ends
+// (see make_key2 below); the tile slot rides in every key, so a pop reads
+// g(x) and moves(x) with one shared load each.
+#pragma once
+
+namespace cw {
+
+using u64 = unsigned long long;
+
+struct Key {
+  u64 f, k;
+};
+
+constexpr u64 kInf64 = ~0ull;
+
+CW_DEV Key key_inf() { return {kInf64, kInf64}; }
+
+CW_DEV bool klt(const Key& a, const Key& b) {
+  return (((u128)a.f << 64) | a.k) < (((u128)b.f << 64) | b.k);
+}
+
+CW_DEV Key shfl_key(const Key& v, int src) {
+  return {__shfl_sync(0xffffffffu, v.f, src), __shfl_sync(0xffffffffu, v.k, src)};
+}
+CW_DEV Key shfl_key_xor(const Key& v, int m) {
+  return {__shfl_xor_sync(0xffffffffu, v.f, m), __shfl_xor_sync(0xffffffffu, v.k, m)};
+}
+CW_DEV Key shfl_key_down(const Key& v, int d) {
+  return {__shfl_down_sync(0xffffffffu, v.f, d), __shfl_down_sync(0xffffffffu, v.k, d)};
+}
+CW_DEV Key shfl_key_up(const Key& v, int d) {
+  return {__shfl_up_sync(0xffffffffu, v.f, d), __shfl_up_sync(0xffffffffu, v.k, d)};
+}
+
+// ascending bitonic sort of one key per lane (empty lanes hold +inf)
+CW_DEV void warp_sort(Key& v, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const Key p = shfl_key_xor(v, j);
+      const bool keep_min = ((lane & j) == 0) == ((lane & k) == 0);
+      if (klt(p, v) == keep_min) v = p;
+    }
+  }
+}
+
+// finish a bitonic sequence into ascending order
+CW_DEV void warp_bitonic_clean(Key& v, int lane) {
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1) {
+    const Key p = shfl_key_xor(v, j);
+    if (klt(p, v) == ((lane & j) == 0)) v = p;
+  }
+}
+
+// Open set of one search (warp-uniform except hd).
+struct OpenSet {
+  Key hd;              // this lane's head entry (+inf beyond h)
+  Key T;               // every near/far key >= T
+  Key F2;              // near < F2 <= far
+  double delta, delta2;
+  int h, nn, nf;
+  int err;
+};
+
+struct Pools {
+  OpenEnt* near;       // shared memory, NC entries
+  OpenEnt* stg;        // shared memory, 64-entry staging area
+  OpenEnt* far;        // global, far_cap entries
+  int NC, far_cap;
+};
+
+CW_DEV u64 f_plus(u64 fb, double d) {
+  const u64 t = (u64)__double_as_longlong(__longlong_as_double((long long)fb) + d);
+  return t <= fb ? fb + 1ull : t;
+}
+
+CW_DEV u64 warp_min_u64(u64 v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+CW_DEV int warp_sum(int v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// min f over A[0, n) (loads issued four at a time)
+CW_DEV u64 fmin_of(const OpenEnt* A, int n, int lane) {
+  u64 fm = kInf64;
+  for (int i = lane; i < n; i += 128) {
+    const u64 a = A[i].f;
+    const u64 b = i + 32 < n ? A[i + 32].f : kInf64;
+    const u64 c = i + 64 < n ? A[i + 64].f : kInf64;
+    const u64 d = i + 96 < n ? A[i + 96].f : kInf64;
+    fm = min(fm, min(min(a, b), min(c, d)));
+  }
+  return warp_min_u64(fm);
+}
+
+CW_DEV int count_lt(const OpenEnt* A, int n, const Key& K, int lane) {
+  int c = 0;
+  for (int i = lane; i < n; i += 32) {
+    const OpenEnt e = A[i];
+    c += klt(Key{e.f, e.k}, K);
+  }
+  return warp_sum(c);
+}
+
+// A split key K with 1 <= |{A < K}| <= target (n > 0, fm = min f of A): first
+// by f (K = (fm + delta, 0), shrinking delta), then, for an equal-f plateau
+// larger than target, by bisection on k within f == fm.
+CW_DEV Key choose_split(const OpenEnt* A, int n, u64 fm, int target, double& delta, int lane) {
+  Key K = {f_plus(fm, delta), 0ull};
+  int c = count_lt(A, n, K, lane);
+  while (c > target && K.f > fm + 1ull) {
+    delta *= 0.25;
+    K = {f_plus(fm, delta), 0ull};
+    c = count_lt(A, n, K, lane);
+  }
+  if (c > target) {
+    u64 kmin = kInf64, kmax = 0ull;
+    for (int i = lane; i < n; i += 32) {
+      const OpenEnt e = A[i];
+      if (e.f == fm) { kmin = min(kmin, e.k); kmax = max(kmax, e.k); }
+    }
+    kmin = warp_min_u64(kmin);
+    kmax = ~warp_min_u64(~kmax);
+    u64 lo = kmin, hi = kmax + 1ull;   // |< (fm, lo)| <= target < |< (fm, hi)|
+    while (hi - lo > 1ull) {
+      const u64 mid = lo + (hi - lo) / 2ull;
+      if (count_lt(A, n, Key{fm, mid}, lane) > target) hi = mid;
+      else lo = mid;
+    }
+    K = {fm, lo > kmin ? lo : kmin + 1ull};
+  }
+  return K;
+}
+
+// Near is about to overflow: demote its entries >= a split key to far.
+__device__ __noinline__ OpenSet split_near(OpenSet st, const Pools pl, int lane) {
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const u64 fm = fmin_of(pl.near, st.nn, lane);
+  const Key K = choose_split(pl.near, st.nn, fm, pl.NC / 2, st.delta2, lane);
+  int w = 0;
+  for (int base = 0; base < st.nn; base += 32) {
+    const int i = base + lane;
+    OpenEnt v = {kInf64, kInf64};
+    if (i < st.nn) v = pl.near[i];
+    const bool dem = i < st.nn && !klt(Key{v.f, v.k}, K);
+    const bool keep = i < st.nn && !dem;
+    const unsigned dm = __ballot_sync(0xffffffffu, dem);
+    const unsigned km = __ballot_sync(0xffffffffu, keep);
+    if (dem && st.nf + __popc(dm) <= pl.far_cap) pl.far[st.nf + __popc(dm & lt_mask)] = v;
+    st.nf += __popc(dm);
+    __syncwarp();
+    if (keep) pl.near[w + __popc(km & lt_mask)] = v;
+    w += __popc(km);
+  }
+  st.nn = w;
+  st.F2 = K;
+  if (st.nf > pl.far_cap) st.err = 1;
+  __syncwarp();
+  return st;
+}
+
+// Head is empty: (far -> near if near is empty), then near -> head.
+__device__ __noinline__ OpenSet refill(OpenSet st, const Pools pl, int lane) {
+  const unsigned lt_mask = (1u << lane) - 1u;
+  if (st.nn == 0) {
+    // ---------------- far -> near: entries below a split key (<= 3/4 of near)
+    const u64 fm = fmin_of(pl.far, st.nf, lane);
+    const Key K = choose_split(pl.far, st.nf, fm, (3 * pl.NC) / 4, st.delta2, lane);
+    int w = 0;
+    OpenEnt v = {kInf64, kInf64};
+    if (lane < st.nf) v = pl.far[lane];
+    for (int base = 0; base < st.nf; base += 32) {
+      const int i = base + lane;
+      OpenEnt vn = {kInf64, kInf64};
+      if (i + 32 < st.nf) vn = pl.far[i + 32];          // prefetch the next chunk
+      const bool in = i < st.nf && klt(Key{v.f, v.k}, K);
+      const bool keep = i < st.nf && !in;
+      const unsigned bm = __ballot_sync(0xffffffffu, in);
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      if (in) pl.near[st.nn + __popc(bm & lt_mask)] = v;
+      st.nn += __popc(bm);
+      __syncwarp();
+      if (keep) pl.far[w + __popc(km & lt_mask)] = v;
+      w += __popc(km);
+      v = vn;
+    }
+    st.nf = w;
+    st.F2 = K;
+    if (st.nn < pl.NC / 16 && st.delta2 < 1024.0) st.delta2 *= 2.0;
+    __syncwarp();
+  }
+  // ---------------- near -> head: f < fmin(near) + delta, sorted; a large
+  // near also demotes its part at or above fmin + delta2 to far
+  const u64 fm = fmin_of(pl.near, st.nn, lane);
+  Key B = {f_plus(fm, st.delta), 0ull};
+  if (klt(st.F2, B)) B = st.F2;
+  if (st.nn > pl.NC / 4) {
+    Key sp = {f_plus(fm, st.delta2), 0ull};
+    if (klt(sp, B)) sp = B;
+    if (klt(sp, st.F2)) st.F2 = sp;
+  }
+  Key acc = key_inf();
+  bool rejected = false;
+  int ns = 0, w = 0, nband = 0;
+  // merge `take` staged keys into the sorted accumulator; the larger half of
+  // the pairing returns to near (compacted behind the reads)
+  auto merge = [&](int take) {
+    Key cv = key_inf();
+    if (lane < take) { const OpenEnt s = pl.stg[lane]; cv = {s.f, s.k}; }
+    __syncwarp();
+    if (lane < ns - take) pl.stg[lane] = pl.stg[lane + take];
+    __syncwarp();
+    ns -= take;
+    warp_sort(cv, lane);
+    const Key rv = shfl_key(cv, 31 - lane);
+    const bool rl = klt(rv, acc);
+    const Key hi = rl ? acc : rv;
+    if (rl) acc = rv;
+    warp_bitonic_clean(acc, lane);
+    const bool back = hi.f != kInf64;
+    const unsigned rm = __ballot_sync(0xffffffffu, back);
+    if (rm) rejected = true;
+    if (back) { OpenEnt o = {hi.f, hi.k}; pl.near[w + __popc(rm & lt_mask)] = o; }
+    w += __popc(rm);
+  };
+  OpenEnt v = {kInf64, kInf64};
+  if (lane < st.nn) v = pl.near[lane];
+  for (int base = 0; base < st.nn; base += 32) {
+    const int i = base + lane;
+    OpenEnt vn = {kInf64, kInf64};
+    if (i + 32 < st.nn) vn = pl.near[i + 32];           // prefetch the next chunk
+    const Key kv = {v.f, v.k};
+    const bool in = i < st.nn && klt(kv, B);
+    const bool dem = i < st.nn && !in && !klt(kv, st.F2);
+    const bool keep = i < st.nn && !in && !dem;
+    const unsigned bm = __ballot_sync(0xffffffffu, in);
+    const unsigned km = __ballot_sync(0xffffffffu, keep);
+    const unsigned dm = __ballot_sync(0xffffffffu, dem);
+    nband += __popc(bm);
+    if (in) pl.stg[ns + __popc(bm & lt_mask)] = v;
+    ns += __popc(bm);
+    if (dem && st.nf + __popc(dm) <= pl.far_cap) pl.far[st.nf + __popc(dm & lt_mask)] = v;
+    st.nf += __popc(dm);
+    __syncwarp();
+    if (keep) pl.near[w + __popc(km & lt_mask)] = v;    // compaction never passes the reads
+    w += __popc(km);
+    while (ns >= 32) merge(32);
+    v = vn;
+  }
+  if (ns > 0) merge(ns);
+  st.nn = w;
+  st.h = __popc(__ballot_sync(0xffffffffu, acc.f != kInf64));
+  st.hd = acc;
+  if (rejected) {
+    // T = successor of the largest head key
+    const Key mx = shfl_key(acc, 31);
+    st.T.k = mx.k + 1ull;
+    st.T.f = mx.f + (st.T.k == 0ull ? 1ull : 0ull);
+  } else {
+    st.T = B;
+  }
+  if (nband > 48) st.delta *= 0.5;
+  else if (nband < 16 && st.delta < 64.0) st.delta *= 2.0;
+  if (st.nn > pl.NC / 2) st.delta2 = fmax(st.delta2 * 0.5, st.delta);
+  if (st.nf > pl.far_cap) st.err = 1;
+  __syncwarp();
+  return st;
+}
+
+// Search-local cell state lives in 8x8-cell tiles: g (f64, +inf when unset)
+// and the move byte.  A tile gets a slot the first time the search writes one
+// of its cells; slots [0, S) are in shared memory, the rest in the warp's
+// global backing store.  The slot is part of every key, so a pop addresses
+// g(x) and moves(x) directly.  Key k2 layout (ordering = (h, row, col)):
+//   [63:41] floor(h * 4096)   distinct octile h differ by > 3.5e-4, so this is
+//                             injective and monotone on the values that occur
+//   [40:31] row  [30:21] col  [20:5] tile slot  [4:0] 0
+constexpr u64 kCellMask2 = ((1ull << 20) - 1ull) << 21;
+constexpr unsigned kNoSlot = 0xFFFFu;
+
+CW_DEV u64 make_key2(double h, int r, int c, int slot) {
+  return ((u64)(h * 4096.0) << 41) | ((u64)r << 31) | ((u64)c << 21) | ((u64)slot << 5);
+}
+
+// bytes of the per-warp global scratch for an nx x ny grid with S shared
+// slots: overflow tiles (g f64 + move byte), parent i32 per cell, slot->tile map
+CW_HD size_t astar_slot_bytes(int nx, int ny, int S) {
+  const size_t nt = (size_t)((nx + 7) / 8) * ((ny + 7) / 8);
+  const size_t b = nt * 64 * 9 + (size_t)nx * ny * 4 + (nt + (size_t)S) * 4;
+  return (b + 255) & ~(size_t)255;
+}
+
+// Launch shape of k_astar: one search warp per SM owning ~200 KB of shared
+// memory -- near pool NC x 16 B + 64-entry staging, the tile map (2 B per
+// tile) and NS tile slots of 576 B (64 x f64 g + 64 move bytes).
+struct AstarShape {
+  int NC, NS;
+  size_t smem;
+};
+
+CW_HD AstarShape astar_shape(int nx, int ny) {
+  const int nt = ((nx + 7) / 8) * ((ny + 7) / 8);
+  const int NC = 1024;
+  const size_t fixed = (size_t)(NC + 64) * 16 + (((size_t)nt * 2 + 15) & ~(size_t)15);
+  const size_t budget = 200 * 1024;
+  int NS = budget > fixed ? (int)((budget - fixed) / 576) : 0;
+  NS = NS > nt ? nt : NS;
+  return {NC, NS, fixed + (size_t)NS * 576};
+}
+
+// k_astar: persistent warps pull requests queued by k_guide and run
+// paths.astar_path exactly; results go to the agent's path (field.py:204-212).
+// Unreachable goals (different 4-connected component, see k_reach) return None
+// without searching -- the reference exhausts the component and returns None.
+__global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state S, int NC, int NS) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int lane = threadIdx.x;
+  const int nx = P.nx, ny = P.ny;
+  const int N = nx * ny;
+  const int TW = (nx + 7) >> 3, NT = TW * ((ny + 7) >> 3);
+  const AstarReq* reqs = reinterpret_cast<const AstarReq*>(S.astar_req);
+  Pools pl;
+  pl.near = reinterpret_cast<OpenEnt*>(sm);
+  pl.stg = pl.near + NC;
+  pl.far = reinterpret_cast<OpenEnt*>(S.astar_heap) + (size_t)blockIdx.x * P.heap_cap;
+  pl.NC = NC;
+  pl.far_cap = P.heap_cap;
+  uint16_t* const tmap = reinterpret_cast<uint16_t*>(pl.stg + 64);         // NT
+  double* const gts = reinterpret_cast<double*>(
+      reinterpret_cast<unsigned char*>(tmap) + (((size_t)NT * 2 + 15) & ~(size_t)15));  // NS x 64
+  uint8_t* const mts = reinterpret_cast<uint8_t*>(gts + (size_t)NS * 64);               // NS x 64
+  unsigned char* const gbase = reinterpret_cast<unsigned char*>(S.astar_rec) +
+                               (size_t)blockIdx.x * astar_slot_bytes(nx, ny, NS);
+  double* const gtg = reinterpret_cast<double*>(gbase);                         // NT x 64
+  uint8_t* const mtg = gbase + (size_t)NT * 64 * 8;                              // NT x 64
+  int32_t* const parent = reinterpret_cast<int32_t*>(mtg + (size_t)NT * 64);     // N
+  int32_t* const s2t = parent + N;                                               // NT + NS
+  auto gtile = [&](int s) -> double* { return s < NS ? gts + s * 64 : gtg + (size_t)(s - NS) * 64; };
+  auto mtile = [&](int s) -> uint8_t* { return s < NS ? mts + s * 64 : mtg + (size_t)(s - NS) * 64; };
+  for (int t = lane; t < NT; t += 32) tmap[t] = kNoSlot;
+  __syncwarp();
+  const unsigned lt_mask = (1u << lane) - 1u;
+  // paths.py:75 move order: N S W E, then the diagonals (nibble per lane, +1)
+  const int dr_ = lane < 8 ? (int)((0x22001120u >> (4 * lane)) & 0xF) - 1 : 0;
+  const int dc_ = lane < 8 ? (int)((0x20202011u >> (4 * lane)) & 0xF) - 1 : 0;
+  const unsigned lanebit = lane < 8 ? 1u << lane : 0u;
+  const double w_ = lane < 4 ? 1.0 : kSqrt2;
+  long long* const dbg = (S.counters && S.counters[14]) ? reinterpret_cast<long long*>(S.counters[14]) : nullptr;
+  long long t_max = 0, t_sum = 0;
+  unsigned long long n_exp = 0, n_stale = 0;
+  double delta = 1.0, delta2 = 4.0;   // adaptive band widths, carried across searches
+  while (true) {
+    int q = 0;
+    if (lane == 0) q = atomicAdd(&S.flags[5], 1);
+    q = __shfl_sync(0xffffffffu, q, 0);
+    if (q >= *(volatile int*)&S.flags[4]) break;
+    const long long t0 = clock64();
+    const AstarReq R = reqs[q];
+    const int e = R.env;
+    const uint8_t* mvt = S.moves + (size_t)e * N;
+    const uint8_t* lab = S.labels + (size_t)e * N;
+    const int32_t* reach = S.reach + (size_t)e * N;
+    const int start = R.start, goal = R.goal;
+    const int sr = start / nx, sc = start - sr * nx;
+    const int gr = goal / nx, gc = goal - gr * nx;
+    int found = 0;  // 1 found, 0 none, -1 open-set overflow
+    int used = 0;   // tile slots handed out
+    unsigned s_exp = 0, s_stale = 0;
+    // give tile t the next slot: g = +inf, move bytes copied from the env table
+    auto new_tile = [&](int t) {
+      const int s = used++;
+      double* gp = gtile(s);
+      uint8_t* mp = mtile(s);
+      const int r0 = (t / TW) * 8, c0 = (t % TW) * 8;
+      gp[lane] = CUDART_INF;
+      gp[lane + 32] = CUDART_INF;
+      for (int j = lane; j < 64; j += 32) {
+        const int rr = r0 + (j >> 3), cc = c0 + (j & 7);
+        mp[j] = (rr < ny && cc < nx) ? mvt[rr * nx + cc] : (uint8_t)0;
+      }
+      if (lane == 0) { tmap[t] = (uint16_t)s; s2t[s] = t; }
+      return s;
+    };
+    if (lab[start] != L_OBSTACLE && lab[goal] != L_OBSTACLE && reach[start] == reach[goal]) {
+      const double h0 = octile(sr, sc, gr, gc);
+      const int s0 = new_tile((sr >> 3) * TW + (sc >> 3));
+      __syncwarp();
+      if (lane == 0) {
+        gtile(s0)[(sr & 7) * 8 + (sc & 7)] = 0.0;
+        parent[start] = -1;
+      }
+      OpenSet st;
+      st.hd = key_inf();
+      if (lane == 0) st.hd = {(u64)__double_as_longlong(h0), make_key2(h0, sr, sc, s0)};
+      st.T = key_inf();
+      st.F2 = {f_plus((u64)__double_as_longlong(h0), delta2), 0ull};
+      st.delta = delta;
+      st.delta2 = delta2;
+      st.h = 1;
+      st.nn = 0;
+      st.nf = 0;
+      st.err = 0;
+      __syncwarp();
+      while (true) {
+        if (st.h == 0) {
+          if (st.nn == 0 && st.nf == 0) break;
+          st = refill(st, pl, lane);
+          if (st.err) { found = -1; break; }
+          continue;
+        }
+        // ---------------- pop the head minimum
+        const Key top = shfl_key(st.hd, 0);
+        {
+          const Key nxt = shfl_key_down(st.hd, 1);
+          st.hd = lane < 31 ? nxt : key_inf();
+        }
+        st.h -= 1;
+        const int r = (int)(top.k >> 31) & 1023, c = (int)(top.k >> 21) & 1023;
+        const int sx = (int)(top.k >> 5) & 0xFFFF;
+        const int x = r * nx + c;
+        const int ix = (r & 7) * 8 + (c & 7);
+        // g(x), moves(x) and the neighbours' tile slots are read together
+        const double gx = gtile(sx)[ix];
+        const unsigned mv = mtile(sx)[ix];
+        const int rr = r + dr_, cc = c + dc_;
+        const bool legal = (mv & lanebit) != 0u;
+        const int ty = legal ? (rr >> 3) * TW + (cc >> 3) : 0;
+        const int iy = (rr & 7) * 8 + (cc & 7);
+        int sy = legal ? (int)tmap[ty] : (int)kNoSlot;
+        const double hh = octile(rr, cc, gr, gc);
+        const double hx = octile(r, c, gr, gc);
+        if (x == goal) { found = 1; break; }
+        // stale entry (paths.py:70-71)
+        if (__longlong_as_double((long long)top.f) > gx + hx + 1e-12) { ++s_stale; continue; }
+        ++s_exp;
+        const double gy = sy != (int)kNoSlot ? gtile(sy)[iy] : CUDART_INF;
+        const double ng = gx + w_;
+        const bool push = legal && ng < gy - 1e-12;
+        const bool fresh = gy == CUDART_INF;
+        // first write into a tile: hand out slots (one per distinct tile)
+        const bool need = push && sy == (int)kNoSlot;
+        const unsigned nm = __ballot_sync(0xffffffffu, need);
+        if (nm) {
+          const unsigned peers = __match_any_sync(0xffffffffu, need ? ty : -1 - lane);
+          const int leader = __ffs(peers) - 1;
+          const unsigned lm = __ballot_sync(0xffffffffu, need && leader == lane);
+          unsigned L = lm;
+          int mine = 0;
+          while (L) {
+            const int ld = __ffs(L) - 1;
+            L &= L - 1;
+            const int s = new_tile(__shfl_sync(0xffffffffu, ty, ld));
+            if (lane == ld) mine = s;
+          }
+          const int got = __shfl_sync(0xffffffffu, mine, leader);
+          if (need) sy = got;
+          __syncwarp();
+        }
+        if (push) {
+          gtile(sy)[iy] = ng;
+          parent[rr * nx + cc] = x;
+        }
+        const Key ne = {(u64)__double_as_longlong(ng + hh), make_key2(hh, rr, cc, sy)};
+        // pushes below T go into the sorted head, the rest to near / far by F2
+        const bool toH = push && klt(ne, st.T);
+        unsigned mh = __ballot_sync(0xffffffffu, toH);
+        const unsigned pm = __ballot_sync(0xffffffffu, push && !toH);
+        if (st.nn + 16 > NC && (pm | mh)) {
+          st = split_near(st, pl, lane);
+          if (st.err) { found = -1; break; }
+        }
+        if (pm) {
+          const bool toN = push && !toH && klt(ne, st.F2);
+          const bool toF = push && !toH && !toN;
+          const unsigned nmk = __ballot_sync(0xffffffffu, toN);
+          const unsigned fmk = __ballot_sync(0xffffffffu, toF);
+          if (st.nf + 16 > pl.far_cap) { found = -1; break; }
+          if (toN) { OpenEnt o = {ne.f, ne.k}; pl.near[st.nn + __popc(nmk & lt_mask)] = o; }
+          if (toF) { OpenEnt o = {ne.f, ne.k}; pl.far[st.nf + __popc(fmk & lt_mask)] = o; }
+          st.nn += __popc(nmk);
+          st.nf += __popc(fmk);
+        }
+        while (mh) {
+          const int s = __ffs(mh) - 1;
+          mh &= mh - 1;
+          const Key v = shfl_key(ne, s);
+          if (!__shfl_sync(0xffffffffu, fresh, s)) {
+            // decrease-key: the cell's previous (now stale) entry leaves the head
+            // if it is there -- a stale pop is a no-op (paths.py:70-71)
+            const unsigned om = __ballot_sync(0xffffffffu, lane < st.h && ((st.hd.k ^ v.k) & kCellMask2) == 0ull);
+            if (om) {
+              const int L = __ffs(om) - 1;
+              const Key dn = shfl_key_down(st.hd, 1);
+              if (lane >= L) st.hd = lane < st.h - 1 ? dn : key_inf();
+              st.h -= 1;
+            }
+          }
+          const Key up = shfl_key_up(st.hd, 1);
+          const int p = __popc(__ballot_sync(0xffffffffu, lane < st.h && klt(st.hd, v)));
+          if (st.h == 32) {
+            // full head: its largest key (or v itself) moves to the pool and bounds it
+            const Key ev = p == 32 ? v : shfl_key(st.hd, 31);
+            const bool evn = klt(ev, st.F2);
+            if (lane == 0) {
+              OpenEnt o = {ev.f, ev.k};
+              if (evn) pl.near[st.nn] = o;
+              else pl.far[st.nf] = o;
+            }
+            st.nn += evn;
+            st.nf += !evn;
+            st.T = ev;
+            if (p == 32) continue;
+            st.h = 31;
+          }
+          if (lane > p && lane <= st.h) st.hd = up;
+          if (lane == p) st.hd = v;
+          st.h += 1;
+        }
+        __syncwarp();
+      }
+      delta = st.delta;
+      delta2 = st.delta2;
+    }
+    // ---- write the guidance result (field.py:204-212)
+    const size_t ia = (size_t)e * P.A + R.agent;
+    int32_t* cells = S.path_cells + ia * P.path_cap;
+    int pn = 1;
+    double wx = S.goal[ia * 2], wy = S.goal[ia * 2 + 1];
+    if (found == -1 && lane == 0) atomicCAS(&S.flags[1], 0, (int)CW_E_HEAPCAP);
+    if (found == 1) {
+      int L = 1;
+      for (int v = goal; v != start; v = parent[v]) ++L;
+      if (L >= 2) {
+        if (L - 1 > P.path_cap) {
+          if (lane == 0) atomicCAS(&S.flags[1], 0, (int)CW_E_PATHCAP);
+        } else {
+          if (lane == 0) {
+            int k = L - 2;
+            for (int v = goal; k >= 0; v = parent[v]) cells[k--] = v;
+          }
+          __syncwarp();
+          pn = L;
+          const int f0 = cells[0];
+          wx = ((double)(f0 % nx) + 0.5) * P.res;
+          wy = ((double)(f0 / nx) + 0.5) * P.res;
+        }
+      }
+    }
+    if (lane == 0) {
+      S.path_head[ia] = 0;
+      S.path_n[ia] = pn;
+      S.waypoint[ia * 2] = wx;
+      S.waypoint[ia * 2 + 1] = wy;
+    }
+    // release the tiles
+    __syncwarp();
+    for (int k = lane; k < used; k += 32) tmap[s2t[k]] = kNoSlot;
+    __syncwarp();
+    const long long dt = clock64() - t0;
+    if (dbg && lane == 0) {
+      long long* d = dbg + (size_t)q * 8;
+      d[0] = dt; d[1] = s_exp; d[2] = s_stale; d[3] = used;
+    }
+    n_exp += s_exp;
+    n_stale += s_stale;
+    t_sum += dt;
+    t_max = max(t_max, dt);
+  }
+  if (lane == 0 && S.counters) {
+    if (n_exp) atomicAdd((unsigned long long*)&S.counters[0], n_exp);
+    if (t_sum) atomicAdd((unsigned long long*)&S.counters[4], (unsigned long long)t_sum);
+    if (t_max) atomicMax((unsigned long long*)&S.counters[5], (unsigned long long)t_max);
+    if (n_stale) atomicAdd((unsigned long long*)&S.counters[10], n_stale);
+  }
+}
+
+}  // namespace cw

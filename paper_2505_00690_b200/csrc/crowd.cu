@@ -26,10 +26,6 @@ namespace cw {
 
 constexpr int MAXC = 12;   // neighbour lanes (<= 10) + robot + static
 constexpr double kWaypointReach = 0.5, kStrayLimit = 1.0;
-// open-list entries kept in shared memory by k_astar (16 B each: f bits, h bits | cell)
-CW_HD int astar_smem_entries() { return 4096; }
-
-struct HeapEnt { double f; int32_t cell; int32_t pad; };
 
 struct WarpCons {
   double px[MAXC], py[MAXC], nx[MAXC], ny[MAXC];
@@ -222,250 +218,12 @@ CW_DEV double octile(int r, int c, int gr, int gc) {
   return kSqrt2 * (double)min(dr, dc) + (double)abs(dr - dc);
 }
 
-struct AstarRec { double g; int32_t parent; uint32_t tag; };  // tag = epoch << 14 | heap pos
 struct AstarReq { int32_t env, agent, start, goal; };
-
-constexpr uint32_t kPosBits = 19, kPosMask = (1u << kPosBits) - 1, kClosed = kPosMask;
-constexpr uint32_t kEpochMax = (1u << (32 - kPosBits)) - 1;
-
-// Open set of the search, scanned by the whole warp.  Pop order must equal the
-// reference's heapq order on (f, h, row, col) (paths.py:216/238).  The lazy heap
-// pops the same sequence of live entries as a decrease-key structure (an improved
-// cell's older entry is stale and skipped; its fresh entry carries the new key),
-// so each cell keeps one entry here.  f and h are non-negative doubles whose IEEE
-// bit patterns order like their values; distinct octile values differ by > 3e-4,
-// so h keeps its top 44 bits and the low 20 bits hold (row << 10 | col), which
-// orders like (row, col).  Key = (f bits, k2) compared as unsigned integers.
-constexpr int kCellBits = 20;
-
-CW_DEV unsigned long long make_k2(double h, int r, int c) {
-  return ((unsigned long long)__double_as_longlong(h) & ~((1ull << kCellBits) - 1ull)) |
-         (unsigned long long)((r << 10) | c);
-}
-
-CW_DEV bool passbit(const uint32_t* pb, int f) { return (__ldg(pb + (f >> 5)) >> (f & 31)) & 1u; }
-
-// k_astar: persistent warps pull A* requests queued by k_guide and run
-// paths.astar_path (paths.py:48-87) exactly; results go to the agent's path.
-// One warp per CTA; the open list (f bits, k2) lives in shared memory.
-// Unreachable goals (different 4-connected component, see k_reach) return None
-// without searching -- the reference exhausts the component and returns None.
 struct __align__(16) OpenEnt { unsigned long long f, k; };
 
-// lexicographic (f, k) as one 128-bit unsigned compare: branch-free carry chain
-CW_DEV bool ent_less(unsigned long long fa, unsigned long long ka, unsigned long long fb,
-                     unsigned long long kb) {
-  return (((u128)fa << 64) | ka) < (((u128)fb << 64) | kb);
-}
-
-__global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state S, int smem_cap) {
-  extern __shared__ __align__(16) unsigned char sm[];
-  OpenEnt* const Osm = reinterpret_cast<OpenEnt*>(sm);
-  const int lane = threadIdx.x;
-  const int nx = P.nx, ny = P.ny;
-  const size_t N = (size_t)nx * ny;
-  AstarRec* rec = reinterpret_cast<AstarRec*>(S.astar_rec) + (size_t)blockIdx.x * N;
-  const AstarReq* reqs = reinterpret_cast<const AstarReq*>(S.astar_req);
-  const int mdr[8] = {-1, 1, 0, 0, -1, -1, 1, 1};
-  const int mdc[8] = {0, 0, -1, 1, -1, 1, -1, 1};
-  OpenEnt* const Ogl = reinterpret_cast<OpenEnt*>(S.astar_heap) + (size_t)blockIdx.x * P.heap_cap;
-  const int gcap = min(P.heap_cap, (int)kClosed);
-  const unsigned lt_mask = (1u << lane) - 1u;
-  const unsigned long long CELLM = (1ull << kCellBits) - 1ull;
-  long long expansions = 0, t_max = 0, t_sum = 0;
-  while (true) {
-    int q = 0;
-    if (lane == 0) q = atomicAdd(&S.flags[5], 1);
-    q = __shfl_sync(0xffffffffu, q, 0);
-    if (q >= *(volatile int*)&S.flags[4]) break;
-    const long long t0 = clock64();
-    const AstarReq R = reqs[q];
-    const int e = R.env;
-    const uint32_t* pb = S.passbits + (size_t)e * ((N + 31) / 32);
-    const int32_t* reach = S.reach + (size_t)e * N;
-    const int start = R.start, goal = R.goal;
-    const int sr = start / nx, sc = start - sr * nx;
-    const int gr = goal / nx, gc = goal - gr * nx;
-    uint32_t epoch = 0;
-    if (lane == 0) {
-      epoch = (uint32_t)S.astar_epoch[blockIdx.x] + 1u;
-      if (epoch > kEpochMax) epoch = 0;
-      S.astar_epoch[blockIdx.x] = (int)epoch;
-    }
-    epoch = __shfl_sync(0xffffffffu, epoch, 0);
-    if (epoch == 0) {  // tag space exhausted: clear this slot's records once
-      for (size_t k = lane; k < N; k += 32) rec[k].tag = 0u;
-      __syncwarp();
-      epoch = 1;
-      if (lane == 0) S.astar_epoch[blockIdx.x] = 1;
-    }
-    const uint32_t ep = epoch << kPosBits;
-    int found = 0;  // 1 found, 0 none, -1 open-list overflow
-    int n = 0;
-    OpenEnt* O = Osm;                 // spills to the global slot when full
-    int cap = min(smem_cap, gcap);
-    if (passbit(pb, start) && passbit(pb, goal) && reach[start] == reach[goal]) {
-      if (lane == 0) {
-        const double h0 = octile(sr, sc, gr, gc);
-        AstarRec r0 = {0.0, -1, ep | 0u};
-        rec[start] = r0;
-        OpenEnt e0 = {(unsigned long long)__double_as_longlong(h0), make_k2(h0, sr, sc)};
-        O[0] = e0;
-      }
-      n = 1;
-      __syncwarp();
-      while (n > 0) {
-        // ---- pop: strided scan (4-way tree per step) + butterfly argmin on (f, k2)
-        unsigned long long bf = ~0ull, bk = ~0ull;
-        int bi = -1;
-        int i = lane;
-        for (; i + 96 < n; i += 128) {
-          const OpenEnt a = O[i], b = O[i + 32], c = O[i + 64], d = O[i + 96];
-          const bool ab = ent_less(b.f, b.k, a.f, a.k);
-          const bool cd = ent_less(d.f, d.k, c.f, c.k);
-          unsigned long long f1 = ab ? b.f : a.f, k1 = ab ? b.k : a.k;
-          int i1 = ab ? i + 32 : i;
-          const unsigned long long f2 = cd ? d.f : c.f, k2 = cd ? d.k : c.k;
-          const int i2 = cd ? i + 96 : i + 64;
-          if (ent_less(f2, k2, f1, k1)) { f1 = f2; k1 = k2; i1 = i2; }
-          if (ent_less(f1, k1, bf, bk)) { bf = f1; bk = k1; bi = i1; }
-        }
-        for (; i < n; i += 32) {
-          const OpenEnt a = O[i];
-          if (ent_less(a.f, a.k, bf, bk)) { bf = a.f; bk = a.k; bi = i; }
-        }
-        unsigned long long gf = bf, gk = bk;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          const unsigned long long of = __shfl_xor_sync(0xffffffffu, gf, o);
-          const unsigned long long ok = __shfl_xor_sync(0xffffffffu, gk, o);
-          if (ent_less(of, ok, gf, gk)) { gf = of; gk = ok; }
-        }
-        const unsigned own = __ballot_sync(0xffffffffu, bf == gf && bk == gk);
-        bi = __shfl_sync(0xffffffffu, bi, __ffs(own) - 1);
-        const int cell20 = (int)(gk & CELLM);
-        const int r = cell20 >> 10, c = cell20 & 1023;
-        const int x = r * nx + c;
-        // ---- issue every load of this expansion together: the popped g, the
-        // neighbour records and passable words (independent of the removal)
-        int y = -1, rr = 0, cc = 0;
-        AstarRec ry = {0.0, 0, 0u};
-        bool okp = false;
-        if (lane < 8) {
-          rr = r + mdr[lane];
-          cc = c + mdc[lane];
-          if (rr >= 0 && rr < ny && cc >= 0 && cc < nx) {
-            y = rr * nx + cc;
-            ry = rec[y];
-            okp = passbit(pb, y) && (lane < 4 || (passbit(pb, r * nx + cc) && passbit(pb, rr * nx + c)));
-          }
-        }
-        const double gx = rec[x].g;
-        // removal: the last entry moves into slot bi (its cell's position changes)
-        const int last = n - 1;
-        const OpenEnt le = O[last];
-        const int lc20 = (int)(le.k & CELLM);
-        const int lcell = (lc20 >> 10) * nx + (lc20 & 1023);
-        __syncwarp();
-        if (lane == 0) {
-          if (bi != last) {
-            O[bi] = le;
-            rec[lcell].tag = ep | (uint32_t)bi;
-          }
-          rec[x].tag = ep | kClosed;
-        }
-        __syncwarp();
-        n -= 1;
-        if (x == goal) { found = 1; break; }
-        // the open list holds live entries only, so the reference's stale test
-        // (paths.py:225) cannot fire here
-        ++expansions;
-        bool ins = false, dec = false;
-        OpenEnt ne;
-        int pos = 0;
-        if (okp) {
-          // ry was loaded before the removal: only the moved entry changed position
-          uint32_t tag = ry.tag;
-          if (y == lcell && bi != last) tag = ep | (uint32_t)bi;
-          const bool live = (tag >> kPosBits) == epoch;
-          const double old = live ? ry.g : CUDART_INF;
-          const double ng = gx + (lane < 4 ? 1.0 : kSqrt2);
-          if (ng < old - 1e-12) {
-            const double hh = octile(rr, cc, gr, gc);
-            ne.f = (unsigned long long)__double_as_longlong(ng + hh);
-            ne.k = make_k2(hh, rr, cc);
-            const uint32_t p = live ? (tag & kPosMask) : kClosed;
-            rec[y].g = ng;
-            rec[y].parent = x;
-            if (p == kClosed) ins = true;            // insert / re-open
-            else { dec = true; pos = (int)p; }       // decrease-key in place
-          }
-        }
-        __syncwarp();
-        const unsigned im = __ballot_sync(0xffffffffu, ins);
-        if (n + __popc(im) > cap) {
-          if (O == Osm && n + __popc(im) <= gcap) {
-            for (int k = lane; k < n; k += 32) Ogl[k] = Osm[k];
-            __syncwarp();
-            O = Ogl;
-            cap = gcap;
-          } else {
-            found = -1;
-            break;
-          }
-        }
-        if (ins) {
-          pos = n + __popc(im & lt_mask);
-          rec[y].tag = ep | (uint32_t)pos;
-        }
-        if (ins || dec) O[pos] = ne;
-        n += __popc(im);
-        __syncwarp();
-      }
-    }
-    // ---- write the guidance result (field.py:204-212)
-    const size_t ia = (size_t)e * P.A + R.agent;
-    int32_t* cells = S.path_cells + ia * P.path_cap;
-    const double gxw = S.goal[ia * 2], gyw = S.goal[ia * 2 + 1];
-    int pn = 1;
-    double wx = gxw, wy = gyw;
-    if (found == -1 && lane == 0) atomicCAS(&S.flags[1], 0, (int)CW_E_HEAPCAP);
-    if (found == 1) {
-      int L = 0;
-      for (int v = goal; v >= 0; v = rec[v].parent) ++L;
-      if (L >= 2) {
-        if (L - 1 > P.path_cap) {
-          if (lane == 0) atomicCAS(&S.flags[1], 0, (int)CW_E_PATHCAP);
-        } else {
-          if (lane == 0) {
-            int k = L - 2;
-            for (int v = goal; k >= 0; v = rec[v].parent) cells[k--] = v;
-          }
-          __syncwarp();
-          pn = L;
-          int f0 = cells[0];
-          wx = ((double)(f0 % nx) + 0.5) * P.res;
-          wy = ((double)(f0 / nx) + 0.5) * P.res;
-        }
-      }
-    }
-    if (lane == 0) {
-      S.path_head[ia] = 0;
-      S.path_n[ia] = pn;
-      S.waypoint[ia * 2] = wx;
-      S.waypoint[ia * 2 + 1] = wy;
-    }
-    long long dt = clock64() - t0;
-    t_sum += dt;
-    t_max = max(t_max, dt);
-    __syncwarp();
-  }
-  if (lane == 0 && S.counters) {
-    if (expansions) atomicAdd((unsigned long long*)&S.counters[0], (unsigned long long)expansions);
-    if (t_sum) atomicAdd((unsigned long long*)&S.counters[4], (unsigned long long)t_sum);
-    if (t_max) atomicMax((unsigned long long*)&S.counters[5], (unsigned long long)t_max);
-  }
-}
+}  // namespace cw
+#include "astar.cuh"
+namespace cw {
 
 // ---------------------------------------------------------------- guidance pass
 CW_DEV void path_point(const int32_t* cells, int head, int n, int k, double gx, double gy,
@@ -841,8 +599,8 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
     cudaFuncSetAttribute(k_orca<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (phases & 1) k_guide<NT><<<P.E, NT, 0, st>>>(P, S, em);
   if (phases & 2) {
-    const int cap = astar_smem_entries();
-    k_astar<<<P.astar_ctas, 32, (size_t)cap * 16, st>>>(P, S, cap);
+    const AstarShape A = astar_shape(P.nx, P.ny);
+    k_astar<<<P.astar_ctas, 32, A.smem, st>>>(P, S, A.NC, A.NS);
   }
   if (phases & 4) k_orca<NT><<<P.E, NT, sm, st>>>(P, S, rp, rv, rr, em);
   return (int)cudaGetLastError();
@@ -856,7 +614,11 @@ size_t cw_crowd_step_smem_bytes(int A, int nt) {
   return (size_t)A * 7 * sizeof(double) + (size_t)(nt / 32) * sizeof(cw::WarpCons) + (size_t)A + 16;
 }
 
-int cw_astar_smem_entries(void) { return cw::astar_smem_entries(); }
+// Bytes of A* scratch (astar_rec) per k_astar CTA for an nx x ny grid.
+size_t cw_astar_slot_bytes(int nx, int ny) {
+  const cw::AstarShape A = cw::astar_shape(nx, ny);
+  return cw::astar_slot_bytes(nx, ny, A.NS);
+}
 
 // One two-phase tick of every env (field.py:90-163): k_guide -> k_astar -> k_orca,
 // stream-ordered.  robot_pos/robot_vel (E,2) may be NULL; env_mask (E) may be NULL.
@@ -866,12 +628,8 @@ int cw_crowd_step_phases(const cw_crowd_params* P, const cw_crowd_state* S,
   using namespace cw;
   if (P->E <= 0 || P->A <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_astar, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         astar_smem_entries() * 16);
-    attr = true;
-  }
+  const AstarShape A = astar_shape(P->nx, P->ny);
+  cudaFuncSetAttribute(k_astar, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)A.smem);
   if (threads == 256)
     return launch_step<256>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, phases, st);
   if (threads == 64)

@@ -1309,25 +1309,38 @@ __global__ void __launch_bounds__(BFS_NT) k_nearest(cw_scene_params P, int E, co
   }
 }
 
-// ================================================================= walkable list + passable bits
+// ================================================================= walkable list + A* move table
+// moves[f] bit d: move d of paths.py:75 (N S W E, NW NE SW SE) is legal from cell
+// f -- target in bounds and passable, diagonals also need both orthogonal cells
+// passable (paths.py:70-72).  One byte load replaces the per-neighbour tests.
 __global__ void __launch_bounds__(1024) k_walk(cw_scene_params P, int E, const int32_t* slots,
                                                cw_scene_buffers B) {
   const int e = blockIdx.x;
   const int slot = env_slot(slots, e);
   if (B.status[slot] != CW_OK) return;
-  const int N = P.nx * P.ny;
-  const int NW32 = (N + 31) / 32;
+  const int nx = P.nx, ny = P.ny, N = nx * ny;
   const uint8_t* Lb = B.labels + (size_t)slot * N;
   int32_t* W = B.walk + (size_t)slot * N;
-  uint32_t* PB = B.passbits + (size_t)slot * NW32;
+  uint8_t* MV = B.moves + (size_t)slot * N;
   __shared__ int sh[1024 / 32 + 1];
   int base = 0;
   for (int f0 = 0; f0 < N; f0 += 1024) {
     int f = f0 + threadIdx.x;
     uint8_t lb = f < N ? Lb[f] : L_OBSTACLE;
     int wk = f < N && lb == L_WALKABLE;
-    unsigned pm = __ballot_sync(0xffffffffu, f < N && lb != L_OBSTACLE);
-    if ((threadIdx.x & 31) == 0 && f < N) PB[f >> 5] = pm;
+    if (f < N) {
+      const int r = f / nx, c = f - r * nx;
+      auto ps = [&](int rr, int cc) {
+        return rr >= 0 && rr < ny && cc >= 0 && cc < nx && Lb[rr * nx + cc] != L_OBSTACLE;
+      };
+      const bool n = ps(r - 1, c), s = ps(r + 1, c), w = ps(r, c - 1), ea = ps(r, c + 1);
+      const unsigned mv = (unsigned)n | ((unsigned)s << 1) | ((unsigned)w << 2) | ((unsigned)ea << 3) |
+                          ((unsigned)(n && w && ps(r - 1, c - 1)) << 4) |
+                          ((unsigned)(n && ea && ps(r - 1, c + 1)) << 5) |
+                          ((unsigned)(s && w && ps(r + 1, c - 1)) << 6) |
+                          ((unsigned)(s && ea && ps(r + 1, c + 1)) << 7);
+      MV[f] = (uint8_t)mv;
+    }
     int tot;
     int off = block_excl_scan<1024>(wk, sh, tot);
     if (wk) W[base + off] = f;

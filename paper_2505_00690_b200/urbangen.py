@@ -248,7 +248,7 @@ class SceneBatch:
         self.walk = z((E, N), dtype=torch.int32, **d)
         self.walk_n = z((E,), dtype=torch.int32, **d)
         self.reach = z((E, N), dtype=torch.int32, **d)
-        self.passbits = z((E, (N + 31) // 32), dtype=torch.int32, **d)
+        self.moves = z((E, N), dtype=torch.uint8, **d)
         A = max(p.peds, 1)
         self.sp_pos = z((E, A, 2), dtype=torch.float64, **d)
         self.sp_goal = z((E, A, 2), dtype=torch.float64, **d)
