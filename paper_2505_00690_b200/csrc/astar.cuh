@@ -98,7 +98,23 @@ struct Pools {
   OpenEnt* stg;        // shared memory, 64-entry staging area
   OpenEnt* far;        // global, far_cap entries
   int NC, far_cap;
+  const double* gts;   // g tiles: slots [0, NS) in shared memory, the rest at gtg
+  const double* gtg;
+  int NS, gr, gc;      // tile slots in shared memory; goal row / col of the search
 };
+
+CW_DEV double octile(int r, int c, int gr, int gc);
+
+// An entry whose cell has since been improved is stale for good (g only
+// decreases); the reference pops it and skips it (paths.py:70-71), so it can
+// be dropped whenever the pools are scanned.  Key layout: see make_key2.
+CW_DEV bool stale_entry(const OpenEnt& v, const Pools& pl) {
+  const int r = (int)(v.k >> 31) & 1023, c = (int)(v.k >> 21) & 1023;
+  const int sl = (int)(v.k >> 5) & 0xFFFF;
+  const double* gp = sl < pl.NS ? pl.gts + sl * 64 : pl.gtg + (size_t)(sl - pl.NS) * 64;
+  const double g = gp[(r & 7) * 8 + (c & 7)];
+  return __longlong_as_double((long long)v.f) > g + octile(r, c, pl.gr, pl.gc) + 1e-12;
+}
 
 CW_DEV u64 f_plus(u64 fb, double d) {
   const u64 t = (u64)__double_as_longlong(__longlong_as_double((long long)fb) + d);
@@ -179,8 +195,9 @@ __device__ __noinline__ OpenSet split_near(OpenSet st, const Pools pl, int lane)
     const int i = base + lane;
     OpenEnt v = {kInf64, kInf64};
     if (i < st.nn) v = pl.near[i];
-    const bool dem = i < st.nn && !klt(Key{v.f, v.k}, K);
-    const bool keep = i < st.nn && !dem;
+    const bool live = i < st.nn && !stale_entry(v, pl);
+    const bool dem = live && !klt(Key{v.f, v.k}, K);
+    const bool keep = live && !dem;
     const unsigned dm = __ballot_sync(0xffffffffu, dem);
     const unsigned km = __ballot_sync(0xffffffffu, keep);
     if (dem && st.nf + __popc(dm) <= pl.far_cap) pl.far[st.nf + __popc(dm & lt_mask)] = v;
@@ -210,8 +227,9 @@ __device__ __noinline__ OpenSet refill(OpenSet st, const Pools pl, int lane) {
       const int i = base + lane;
       OpenEnt vn = {kInf64, kInf64};
       if (i + 32 < st.nf) vn = pl.far[i + 32];          // prefetch the next chunk
-      const bool in = i < st.nf && klt(Key{v.f, v.k}, K);
-      const bool keep = i < st.nf && !in;
+      const bool live = i < st.nf && !stale_entry(v, pl);
+      const bool in = live && klt(Key{v.f, v.k}, K);
+      const bool keep = live && !in;
       const unsigned bm = __ballot_sync(0xffffffffu, in);
       const unsigned km = __ballot_sync(0xffffffffu, keep);
       if (in) pl.near[st.nn + __popc(bm & lt_mask)] = v;
@@ -267,9 +285,10 @@ __device__ __noinline__ OpenSet refill(OpenSet st, const Pools pl, int lane) {
     OpenEnt vn = {kInf64, kInf64};
     if (i + 32 < st.nn) vn = pl.near[i + 32];           // prefetch the next chunk
     const Key kv = {v.f, v.k};
-    const bool in = i < st.nn && klt(kv, B);
-    const bool dem = i < st.nn && !in && !klt(kv, st.F2);
-    const bool keep = i < st.nn && !in && !dem;
+    const bool live = i < st.nn && !stale_entry(v, pl);
+    const bool in = live && klt(kv, B);
+    const bool dem = live && !in && !klt(kv, st.F2);
+    const bool keep = live && !in && !dem;
     const unsigned bm = __ballot_sync(0xffffffffu, in);
     const unsigned km = __ballot_sync(0xffffffffu, keep);
     const unsigned dm = __ballot_sync(0xffffffffu, dem);
@@ -373,6 +392,9 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
   int32_t* const parent = reinterpret_cast<int32_t*>(mtg + (size_t)NT * 64);     // N
   int32_t* const s2t = parent + N;                                               // NT + NS
   auto gtile = [&](int s) -> double* { return s < NS ? gts + s * 64 : gtg + (size_t)(s - NS) * 64; };
+  pl.gts = gts;
+  pl.gtg = gtg;
+  pl.NS = NS;
   auto mtile = [&](int s) -> uint8_t* { return s < NS ? mts + s * 64 : mtg + (size_t)(s - NS) * 64; };
   for (int t = lane; t < NT; t += 32) tmap[t] = kNoSlot;
   __syncwarp();
@@ -400,6 +422,8 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
     const int start = R.start, goal = R.goal;
     const int sr = start / nx, sc = start - sr * nx;
     const int gr = goal / nx, gc = goal - gr * nx;
+    pl.gr = gr;
+    pl.gc = gc;
     int found = 0;  // 1 found, 0 none, -1 open-set overflow
     int used = 0;   // tile slots handed out
     unsigned s_exp = 0, s_stale = 0;
@@ -499,24 +523,21 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
         }
         const Key ne = {(u64)__double_as_longlong(ng + hh), make_key2(hh, rr, cc, sy)};
         // pushes below T go into the sorted head, the rest to near / far by F2
-        const bool toH = push && klt(ne, st.T);
-        unsigned mh = __ballot_sync(0xffffffffu, toH);
-        const unsigned pm = __ballot_sync(0xffffffffu, push && !toH);
-        if (st.nn + 16 > NC && (pm | mh)) {
+        if (st.nn + 16 > NC) {
           st = split_near(st, pl, lane);
           if (st.err) { found = -1; break; }
         }
-        if (pm) {
-          const bool toN = push && !toH && klt(ne, st.F2);
-          const bool toF = push && !toH && !toN;
-          const unsigned nmk = __ballot_sync(0xffffffffu, toN);
-          const unsigned fmk = __ballot_sync(0xffffffffu, toF);
-          if (st.nf + 16 > pl.far_cap) { found = -1; break; }
-          if (toN) { OpenEnt o = {ne.f, ne.k}; pl.near[st.nn + __popc(nmk & lt_mask)] = o; }
-          if (toF) { OpenEnt o = {ne.f, ne.k}; pl.far[st.nf + __popc(fmk & lt_mask)] = o; }
-          st.nn += __popc(nmk);
-          st.nf += __popc(fmk);
-        }
+        const bool toH = push && klt(ne, st.T);
+        const bool toN = push && !toH && klt(ne, st.F2);
+        const bool toF = push && !toH && !toN;
+        unsigned mh = __ballot_sync(0xffffffffu, toH);
+        const unsigned nmk = __ballot_sync(0xffffffffu, toN);
+        const unsigned fmk = __ballot_sync(0xffffffffu, toF);
+        if (st.nf + 16 > pl.far_cap) { found = -1; break; }
+        if (toN) { OpenEnt o = {ne.f, ne.k}; pl.near[st.nn + __popc(nmk & lt_mask)] = o; }
+        if (toF) { OpenEnt o = {ne.f, ne.k}; pl.far[st.nf + __popc(fmk & lt_mask)] = o; }
+        st.nn += __popc(nmk);
+        st.nf += __popc(fmk);
         while (mh) {
           const int s = __ffs(mh) - 1;
           mh &= mh - 1;
@@ -524,7 +545,7 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
           if (!__shfl_sync(0xffffffffu, fresh, s)) {
             // decrease-key: the cell's previous (now stale) entry leaves the head
             // if it is there -- a stale pop is a no-op (paths.py:70-71)
-            const unsigned om = __ballot_sync(0xffffffffu, lane < st.h && ((st.hd.k ^ v.k) & kCellMask2) == 0ull);
+            const unsigned om = __ballot_sync(0xffffffffu, ((st.hd.k ^ v.k) & kCellMask2) == 0ull);
             if (om) {
               const int L = __ffs(om) - 1;
               const Key dn = shfl_key_down(st.hd, 1);
@@ -533,7 +554,7 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
             }
           }
           const Key up = shfl_key_up(st.hd, 1);
-          const int p = __popc(__ballot_sync(0xffffffffu, lane < st.h && klt(st.hd, v)));
+          const int p = __popc(__ballot_sync(0xffffffffu, klt(st.hd, v)));   // +inf beyond h
           if (st.h == 32) {
             // full head: its largest key (or v itself) moves to the pool and bounds it
             const Key ev = p == 32 ? v : shfl_key(st.hd, 31);
