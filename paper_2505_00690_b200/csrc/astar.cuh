@@ -470,14 +470,14 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
           continue;
         }
         // ---------------- pop the head minimum
-        const Key top = shfl_key(st.hd, 0);
+        const u64 topk = __shfl_sync(0xffffffffu, st.hd.k, 0);   // f is not needed
         {
           const Key nxt = shfl_key_down(st.hd, 1);
           st.hd = lane < 31 ? nxt : key_inf();
         }
         st.h -= 1;
-        const int r = (int)(top.k >> 31) & 1023, c = (int)(top.k >> 21) & 1023;
-        const int sx = (int)(top.k >> 5) & 0xFFFF;
+        const int r = (int)(topk >> 31) & 1023, c = (int)(topk >> 21) & 1023;
+        const int sx = (int)(topk >> 5) & 0xFFFF;
         const int x = r * nx + c;
         const int ix = (r & 7) * 8 + (c & 7);
         // g(x), moves(x) and the neighbours' tile slots are read together
@@ -485,22 +485,37 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
         const unsigned mv = mtile(sx)[ix];
         const int rr = r + dr_, cc = c + dc_;
         const bool legal = (mv & lanebit) != 0u;
-        const int ty = legal ? (rr >> 3) * TW + (cc >> 3) : 0;
+        // the tile-map read does not wait for the move byte (index clamped)
+        const int ty = min(max((rr >> 3) * TW + (cc >> 3), 0), NT - 1);
         const int iy = (rr & 7) * 8 + (cc & 7);
-        int sy = legal ? (int)tmap[ty] : (int)kNoSlot;
+        const int sy0 = (int)tmap[ty];
+        int sy = legal ? sy0 : (int)kNoSlot;
         const double hh = octile(rr, cc, gr, gc);
-        const double hx = octile(r, c, gr, gc);
         if (x == goal) { found = 1; break; }
-        // stale entry (paths.py:70-71)
-        if (__longlong_as_double((long long)top.f) > gx + hx + 1e-12) { ++s_stale; continue; }
+        // No stale test (paths.py:70-71) is needed here: the head never holds a
+        // stale entry (refills drop them, decrease-keys evict the old head copy),
+        // and re-expanding a cell with its current g would relax nothing anyway.
         ++s_exp;
         const double gy = sy != (int)kNoSlot ? gtile(sy)[iy] : CUDART_INF;
         const double ng = gx + w_;
         const bool push = legal && ng < gy - 1e-12;
         const bool fresh = gy == CUDART_INF;
-        // first write into a tile: hand out slots (one per distinct tile)
+        // routing never looks at the tile slot ((h, row, col) is unique per
+        // cell), so it is decided together with the first-write test
+        const Key ne0 = {(u64)__double_as_longlong(ng + hh), make_key2(hh, rr, cc, 0)};
+        if (st.nn + 16 > NC) {
+          st = split_near(st, pl, lane);
+          if (st.err) { found = -1; break; }
+        }
         const bool need = push && sy == (int)kNoSlot;
+        const bool toH = push && klt(ne0, st.T);
+        const bool toN = push && !toH && klt(ne0, st.F2);
+        const bool toF = push && !toH && !toN;
         const unsigned nm = __ballot_sync(0xffffffffu, need);
+        unsigned mh = __ballot_sync(0xffffffffu, toH);
+        const unsigned nmk = __ballot_sync(0xffffffffu, toN);
+        const unsigned fmk = __ballot_sync(0xffffffffu, toF);
+        // first write into a tile: hand out slots (one per distinct tile)
         if (nm) {
           const unsigned peers = __match_any_sync(0xffffffffu, need ? ty : -1 - lane);
           const int leader = __ffs(peers) - 1;
@@ -521,18 +536,7 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
           gtile(sy)[iy] = ng;
           parent[rr * nx + cc] = x;
         }
-        const Key ne = {(u64)__double_as_longlong(ng + hh), make_key2(hh, rr, cc, sy)};
-        // pushes below T go into the sorted head, the rest to near / far by F2
-        if (st.nn + 16 > NC) {
-          st = split_near(st, pl, lane);
-          if (st.err) { found = -1; break; }
-        }
-        const bool toH = push && klt(ne, st.T);
-        const bool toN = push && !toH && klt(ne, st.F2);
-        const bool toF = push && !toH && !toN;
-        unsigned mh = __ballot_sync(0xffffffffu, toH);
-        const unsigned nmk = __ballot_sync(0xffffffffu, toN);
-        const unsigned fmk = __ballot_sync(0xffffffffu, toF);
+        const Key ne = {ne0.f, ne0.k | ((u64)sy << 5)};
         if (st.nf + 16 > pl.far_cap) { found = -1; break; }
         if (toN) { OpenEnt o = {ne.f, ne.k}; pl.near[st.nn + __popc(nmk & lt_mask)] = o; }
         if (toF) { OpenEnt o = {ne.f, ne.k}; pl.far[st.nf + __popc(fmk & lt_mask)] = o; }

@@ -79,6 +79,10 @@ for k in range(steps):
     c = f.counters_t.cpu().numpy().copy()
     d = dbg.cpu().numpy()
     for r_ in d[np.argsort(-d[:, 0])[:2]]:
+        if os.environ.get("LAB_PHASES"):
+            ph_ = [(int(r_[4 + i // 2]) >> (32 * (i % 2))) & 0xFFFFFFFF for i in range(6)] + [int(r_[7])]
+            print("      phases/exp [pop, loads+stale, gy+push, alloc, store+key, route+pool, inserts]:",
+                  " ".join(f"{v / max(r_[1], 1):5.0f}" for v in ph_))
         print(f"   search cyc {r_[0]/1e6:6.2f}M exp {r_[1]:6d} cyc/exp {r_[0]/max(r_[1],1):6.0f} stale {r_[2]:6d} "
               f"tiles {r_[3]:6d}")
     f.check_flags()
