@@ -408,7 +408,7 @@ class CrowdField:
                 "lp_fallbacks": int(c[2]), "stall_retries": int(c[3]),
                 "astar_cycles": int(c[4]), "astar_max_cycles": int(c[5]),
                 "cta_cycles": int(c[6]), "cta_max_cycles": int(c[7]),
-                "astar_stale_pops": int(c[10])}
+                "astar_global_retries": int(c[10])}
 
 
 def step_crowd(agents, robot_state, occupancy, config, seed=0, resample_goals=True):

@@ -98,9 +98,8 @@ struct Pools {
   OpenEnt* stg;        // shared memory, 64-entry staging area
   OpenEnt* far;        // global, far_cap entries
   int NC, far_cap;
-  const double* gts;   // g tiles: slots [0, NS) in shared memory, the rest at gtg
-  const double* gtg;
-  int NS, gr, gc;      // tile slots in shared memory; goal row / col of the search
+  const double* gt;    // g tiles of the running search (shared or global)
+  int gr, gc;          // goal row / col of the running search
 };
 
 CW_DEV double octile(int r, int c, int gr, int gc);
@@ -111,8 +110,7 @@ CW_DEV double octile(int r, int c, int gr, int gc);
 CW_DEV bool stale_entry(const OpenEnt& v, const Pools& pl) {
   const int r = (int)(v.k >> 31) & 1023, c = (int)(v.k >> 21) & 1023;
   const int sl = (int)(v.k >> 5) & 0xFFFF;
-  const double* gp = sl < pl.NS ? pl.gts + sl * 64 : pl.gtg + (size_t)(sl - pl.NS) * 64;
-  const double g = gp[(r & 7) * 8 + (c & 7)];
+  const double g = pl.gt[(size_t)sl * 64 + (r & 7) * 8 + (c & 7)];
   return __longlong_as_double((long long)v.f) > g + octile(r, c, pl.gr, pl.gc) + 1e-12;
 }
 
@@ -364,6 +362,199 @@ CW_HD AstarShape astar_shape(int nx, int ny) {
   return {NC, NS, fixed + (size_t)NS * 576};
 }
 
+// Per-CTA layout shared by the two search instantiations.
+struct SearchEnv {
+  int nx, ny, N, TW, NT, NS;
+  uint16_t* tmap;        // shared: tile -> slot (kNoSlot when unused)
+  double* gts;           // shared: NS x 64 g
+  uint8_t* mts;          // shared: NS x 64 move bytes
+  double* gtg;           // global: NT x 64 g (all-global instantiation)
+  uint8_t* mtg;          // global: NT x 64 move bytes
+  int32_t* parent;       // global: N
+  int32_t* s2t;          // global: slot -> tile
+};
+
+// One search, paths.astar_path (paths.py:48-87).  kGlob = false keeps every
+// tile in shared memory and returns -2 when they run out (the caller retries
+// with kGlob = true, all tiles in the global backing store).  Returns 1 found,
+// 0 no path, -1 open-set overflow; `used` = tile slots handed out.
+template <bool kGlob>
+CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int start, int goal,
+                      double& delta, double& delta2, unsigned& s_exp, int& used, int lane) {
+  double* const gt = kGlob ? E.gtg : E.gts;
+  uint8_t* const mt = kGlob ? E.mtg : E.mts;
+  const int cap = kGlob ? E.NT : E.NS;
+  const int nx = E.nx, ny = E.ny, TW = E.TW, NT = E.NT, NC = pl.NC;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  // paths.py:75 move order: N S W E, then the diagonals (nibble per lane, +1)
+  const int dr_ = lane < 8 ? (int)((0x22001120u >> (4 * lane)) & 0xF) - 1 : 0;
+  const int dc_ = lane < 8 ? (int)((0x20202011u >> (4 * lane)) & 0xF) - 1 : 0;
+  const unsigned lanebit = lane < 8 ? 1u << lane : 0u;
+  const double w_ = lane < 4 ? 1.0 : kSqrt2;
+  const int sr = start / nx, sc = start - sr * nx;
+  const int gr = goal / nx, gc = goal - gr * nx;
+  pl.gt = gt;
+  pl.gr = gr;
+  pl.gc = gc;
+  // give tile t the next slot: g = +inf, move bytes copied from the env table
+  auto new_tile = [&](int t) {
+    const int s = used++;
+    double* gp = gt + (size_t)s * 64;
+    uint8_t* mp = mt + (size_t)s * 64;
+    const int r0 = (t / TW) * 8, c0 = (t % TW) * 8;
+    gp[lane] = CUDART_INF;
+    gp[lane + 32] = CUDART_INF;
+    for (int j = lane; j < 64; j += 32) {
+      const int rr = r0 + (j >> 3), cc = c0 + (j & 7);
+      mp[j] = (rr < ny && cc < nx) ? mvt[rr * nx + cc] : (uint8_t)0;
+    }
+    if (lane == 0) { E.tmap[t] = (uint16_t)s; E.s2t[s] = t; }
+    return s;
+  };
+  const double h0 = octile(sr, sc, gr, gc);
+  const int s0 = new_tile((sr >> 3) * TW + (sc >> 3));
+  __syncwarp();
+  if (lane == 0) {
+    gt[(size_t)s0 * 64 + (sr & 7) * 8 + (sc & 7)] = 0.0;
+    E.parent[start] = -1;
+  }
+  OpenSet st;
+  st.hd = key_inf();
+  if (lane == 0) st.hd = {(u64)__double_as_longlong(h0), make_key2(h0, sr, sc, s0)};
+  st.T = key_inf();
+  st.F2 = {f_plus((u64)__double_as_longlong(h0), delta2), 0ull};
+  st.delta = delta;
+  st.delta2 = delta2;
+  st.h = 1;
+  st.nn = 0;
+  st.nf = 0;
+  st.err = 0;
+  int found = 0;
+  __syncwarp();
+  while (true) {
+    if (st.h == 0) {
+      if (st.nn == 0 && st.nf == 0) break;
+      st = refill(st, pl, lane);
+      if (st.err) { found = -1; break; }
+      continue;
+    }
+    // ---------------- pop the head minimum
+    const u64 topk = __shfl_sync(0xffffffffu, st.hd.k, 0);   // f is not needed
+    {
+      const Key nxt = shfl_key_down(st.hd, 1);
+      st.hd = lane < 31 ? nxt : key_inf();
+    }
+    st.h -= 1;
+    const int r = (int)(topk >> 31) & 1023, c = (int)(topk >> 21) & 1023;
+    const int sx = (int)(topk >> 5) & 0xFFFF;
+    const int x = r * nx + c;
+    const int ix = sx * 64 + (r & 7) * 8 + (c & 7);
+    // g(x), moves(x) and the neighbours' tile slots are read together
+    const double gx = gt[ix];
+    const unsigned mv = mt[ix];
+    const int rr = r + dr_, cc = c + dc_;
+    const bool legal = (mv & lanebit) != 0u;
+    // the tile-map read does not wait for the move byte (index clamped)
+    const int ty = min(max((rr >> 3) * TW + (cc >> 3), 0), NT - 1);
+    const int iy = (rr & 7) * 8 + (cc & 7);
+    const int sy0 = (int)E.tmap[ty];
+    int sy = legal ? sy0 : (int)kNoSlot;
+    const double hh = octile(rr, cc, gr, gc);
+    if (x == goal) { found = 1; break; }
+    // No stale test (paths.py:70-71) is needed here: the head never holds a
+    // stale entry (refills drop them, decrease-keys evict the old head copy),
+    // and re-expanding a cell with its current g would relax nothing anyway.
+    ++s_exp;
+    const double gy = sy != (int)kNoSlot ? gt[(size_t)sy * 64 + iy] : CUDART_INF;
+    const double ng = gx + w_;
+    const bool push = legal && ng < gy - 1e-12;
+    const bool fresh = gy == CUDART_INF;
+    // routing never looks at the tile slot ((h, row, col) is unique per
+    // cell), so it is decided together with the first-write test
+    const Key ne0 = {(u64)__double_as_longlong(ng + hh), make_key2(hh, rr, cc, 0)};
+    if (st.nn + 16 > NC) {
+      st = split_near(st, pl, lane);
+      if (st.err) { found = -1; break; }
+    }
+    const bool need = push && sy == (int)kNoSlot;
+    const bool toH = push && klt(ne0, st.T);
+    const bool toN = push && !toH && klt(ne0, st.F2);
+    const bool toF = push && !toH && !toN;
+    const unsigned nm = __ballot_sync(0xffffffffu, need);
+    unsigned mh = __ballot_sync(0xffffffffu, toH);
+    const unsigned nmk = __ballot_sync(0xffffffffu, toN);
+    const unsigned fmk = __ballot_sync(0xffffffffu, toF);
+    // first write into a tile: hand out slots (one per distinct tile)
+    if (nm) {
+      const unsigned peers = __match_any_sync(0xffffffffu, need ? ty : -1 - lane);
+      const int leader = __ffs(peers) - 1;
+      const unsigned lm = __ballot_sync(0xffffffffu, need && leader == lane);
+      if (used + __popc(lm) > cap) { found = -2; break; }   // only when !kGlob
+      unsigned L = lm;
+      int mine = 0;
+      while (L) {
+        const int ld = __ffs(L) - 1;
+        L &= L - 1;
+        const int s = new_tile(__shfl_sync(0xffffffffu, ty, ld));
+        if (lane == ld) mine = s;
+      }
+      const int got = __shfl_sync(0xffffffffu, mine, leader);
+      if (need) sy = got;
+      __syncwarp();
+    }
+    if (push) {
+      gt[(size_t)sy * 64 + iy] = ng;
+      E.parent[rr * nx + cc] = x;
+    }
+    const Key ne = {ne0.f, ne0.k | ((u64)sy << 5)};
+    if (st.nf + 16 > pl.far_cap) { found = -1; break; }
+    if (toN) { OpenEnt o = {ne.f, ne.k}; pl.near[st.nn + __popc(nmk & lt_mask)] = o; }
+    if (toF) { OpenEnt o = {ne.f, ne.k}; pl.far[st.nf + __popc(fmk & lt_mask)] = o; }
+    st.nn += __popc(nmk);
+    st.nf += __popc(fmk);
+    while (mh) {
+      const int s = __ffs(mh) - 1;
+      mh &= mh - 1;
+      const Key v = shfl_key(ne, s);
+      if (!__shfl_sync(0xffffffffu, fresh, s)) {
+        // decrease-key: the cell's previous (now stale) entry leaves the head
+        // if it is there -- a stale pop is a no-op (paths.py:70-71)
+        const unsigned om = __ballot_sync(0xffffffffu, ((st.hd.k ^ v.k) & kCellMask2) == 0ull);
+        if (om) {
+          const int L = __ffs(om) - 1;
+          const Key dn = shfl_key_down(st.hd, 1);
+          if (lane >= L) st.hd = lane < st.h - 1 ? dn : key_inf();
+          st.h -= 1;
+        }
+      }
+      const Key up = shfl_key_up(st.hd, 1);
+      const int p = __popc(__ballot_sync(0xffffffffu, klt(st.hd, v)));   // +inf beyond h
+      if (st.h == 32) {
+        // full head: its largest key (or v itself) moves to the pool and bounds it
+        const Key ev = p == 32 ? v : shfl_key(st.hd, 31);
+        const bool evn = klt(ev, st.F2);
+        if (lane == 0) {
+          OpenEnt o = {ev.f, ev.k};
+          if (evn) pl.near[st.nn] = o;
+          else pl.far[st.nf] = o;
+        }
+        st.nn += evn;
+        st.nf += !evn;
+        st.T = ev;
+        if (p == 32) continue;
+        st.h = 31;
+      }
+      if (lane > p && lane <= st.h) st.hd = up;
+      if (lane == p) st.hd = v;
+      st.h += 1;
+    }
+    __syncwarp();
+  }
+  delta = st.delta;
+  delta2 = st.delta2;
+  return found;
+}
+
 // k_astar: persistent warps pull requests queued by k_guide and run
 // paths.astar_path exactly; results go to the agent's path (field.py:204-212).
 // Unreachable goals (different 4-connected component, see k_reach) return None
@@ -371,9 +562,14 @@ CW_HD AstarShape astar_shape(int nx, int ny) {
 __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state S, int NC, int NS) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int lane = threadIdx.x;
-  const int nx = P.nx, ny = P.ny;
-  const int N = nx * ny;
-  const int TW = (nx + 7) >> 3, NT = TW * ((ny + 7) >> 3);
+  SearchEnv E;
+  E.nx = P.nx;
+  E.ny = P.ny;
+  E.N = P.nx * P.ny;
+  E.TW = (P.nx + 7) >> 3;
+  E.NT = E.TW * ((P.ny + 7) >> 3);
+  E.NS = NS;
+  const int nx = E.nx, N = E.N, NT = E.NT;
   const AstarReq* reqs = reinterpret_cast<const AstarReq*>(S.astar_req);
   Pools pl;
   pl.near = reinterpret_cast<OpenEnt*>(sm);
@@ -381,32 +577,21 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
   pl.far = reinterpret_cast<OpenEnt*>(S.astar_heap) + (size_t)blockIdx.x * P.heap_cap;
   pl.NC = NC;
   pl.far_cap = P.heap_cap;
-  uint16_t* const tmap = reinterpret_cast<uint16_t*>(pl.stg + 64);         // NT
-  double* const gts = reinterpret_cast<double*>(
-      reinterpret_cast<unsigned char*>(tmap) + (((size_t)NT * 2 + 15) & ~(size_t)15));  // NS x 64
-  uint8_t* const mts = reinterpret_cast<uint8_t*>(gts + (size_t)NS * 64);               // NS x 64
+  E.tmap = reinterpret_cast<uint16_t*>(pl.stg + 64);
+  E.gts = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(E.tmap) +
+                                    (((size_t)NT * 2 + 15) & ~(size_t)15));
+  E.mts = reinterpret_cast<uint8_t*>(E.gts + (size_t)NS * 64);
   unsigned char* const gbase = reinterpret_cast<unsigned char*>(S.astar_rec) +
-                               (size_t)blockIdx.x * astar_slot_bytes(nx, ny, NS);
-  double* const gtg = reinterpret_cast<double*>(gbase);                         // NT x 64
-  uint8_t* const mtg = gbase + (size_t)NT * 64 * 8;                              // NT x 64
-  int32_t* const parent = reinterpret_cast<int32_t*>(mtg + (size_t)NT * 64);     // N
-  int32_t* const s2t = parent + N;                                               // NT + NS
-  auto gtile = [&](int s) -> double* { return s < NS ? gts + s * 64 : gtg + (size_t)(s - NS) * 64; };
-  pl.gts = gts;
-  pl.gtg = gtg;
-  pl.NS = NS;
-  auto mtile = [&](int s) -> uint8_t* { return s < NS ? mts + s * 64 : mtg + (size_t)(s - NS) * 64; };
-  for (int t = lane; t < NT; t += 32) tmap[t] = kNoSlot;
+                               (size_t)blockIdx.x * astar_slot_bytes(nx, E.ny, NS);
+  E.gtg = reinterpret_cast<double*>(gbase);
+  E.mtg = gbase + (size_t)NT * 64 * 8;
+  E.parent = reinterpret_cast<int32_t*>(E.mtg + (size_t)NT * 64);
+  E.s2t = E.parent + N;
+  for (int t = lane; t < NT; t += 32) E.tmap[t] = kNoSlot;
   __syncwarp();
-  const unsigned lt_mask = (1u << lane) - 1u;
-  // paths.py:75 move order: N S W E, then the diagonals (nibble per lane, +1)
-  const int dr_ = lane < 8 ? (int)((0x22001120u >> (4 * lane)) & 0xF) - 1 : 0;
-  const int dc_ = lane < 8 ? (int)((0x20202011u >> (4 * lane)) & 0xF) - 1 : 0;
-  const unsigned lanebit = lane < 8 ? 1u << lane : 0u;
-  const double w_ = lane < 4 ? 1.0 : kSqrt2;
   long long* const dbg = (S.counters && S.counters[14]) ? reinterpret_cast<long long*>(S.counters[14]) : nullptr;
   long long t_max = 0, t_sum = 0;
-  unsigned long long n_exp = 0, n_stale = 0;
+  unsigned long long n_exp = 0, n_glob = 0;
   double delta = 1.0, delta2 = 4.0;   // adaptive band widths, carried across searches
   while (true) {
     int q = 0;
@@ -420,168 +605,23 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
     const uint8_t* lab = S.labels + (size_t)e * N;
     const int32_t* reach = S.reach + (size_t)e * N;
     const int start = R.start, goal = R.goal;
-    const int sr = start / nx, sc = start - sr * nx;
-    const int gr = goal / nx, gc = goal - gr * nx;
-    pl.gr = gr;
-    pl.gc = gc;
     int found = 0;  // 1 found, 0 none, -1 open-set overflow
     int used = 0;   // tile slots handed out
-    unsigned s_exp = 0, s_stale = 0;
-    // give tile t the next slot: g = +inf, move bytes copied from the env table
-    auto new_tile = [&](int t) {
-      const int s = used++;
-      double* gp = gtile(s);
-      uint8_t* mp = mtile(s);
-      const int r0 = (t / TW) * 8, c0 = (t % TW) * 8;
-      gp[lane] = CUDART_INF;
-      gp[lane + 32] = CUDART_INF;
-      for (int j = lane; j < 64; j += 32) {
-        const int rr = r0 + (j >> 3), cc = c0 + (j & 7);
-        mp[j] = (rr < ny && cc < nx) ? mvt[rr * nx + cc] : (uint8_t)0;
-      }
-      if (lane == 0) { tmap[t] = (uint16_t)s; s2t[s] = t; }
-      return s;
+    unsigned s_exp = 0;
+    auto release = [&]() {
+      __syncwarp();
+      for (int k = lane; k < used; k += 32) E.tmap[E.s2t[k]] = kNoSlot;
+      __syncwarp();
+      used = 0;
     };
     if (lab[start] != L_OBSTACLE && lab[goal] != L_OBSTACLE && reach[start] == reach[goal]) {
-      const double h0 = octile(sr, sc, gr, gc);
-      const int s0 = new_tile((sr >> 3) * TW + (sc >> 3));
-      __syncwarp();
-      if (lane == 0) {
-        gtile(s0)[(sr & 7) * 8 + (sc & 7)] = 0.0;
-        parent[start] = -1;
+      found = run_search<false>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane);
+      if (found == -2) {   // more tiles than shared memory holds: redo it all-global
+        release();
+        s_exp = 0;
+        ++n_glob;
+        found = run_search<true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane);
       }
-      OpenSet st;
-      st.hd = key_inf();
-      if (lane == 0) st.hd = {(u64)__double_as_longlong(h0), make_key2(h0, sr, sc, s0)};
-      st.T = key_inf();
-      st.F2 = {f_plus((u64)__double_as_longlong(h0), delta2), 0ull};
-      st.delta = delta;
-      st.delta2 = delta2;
-      st.h = 1;
-      st.nn = 0;
-      st.nf = 0;
-      st.err = 0;
-      __syncwarp();
-      while (true) {
-        if (st.h == 0) {
-          if (st.nn == 0 && st.nf == 0) break;
-          st = refill(st, pl, lane);
-          if (st.err) { found = -1; break; }
-          continue;
-        }
-        // ---------------- pop the head minimum
-        const u64 topk = __shfl_sync(0xffffffffu, st.hd.k, 0);   // f is not needed
-        {
-          const Key nxt = shfl_key_down(st.hd, 1);
-          st.hd = lane < 31 ? nxt : key_inf();
-        }
-        st.h -= 1;
-        const int r = (int)(topk >> 31) & 1023, c = (int)(topk >> 21) & 1023;
-        const int sx = (int)(topk >> 5) & 0xFFFF;
-        const int x = r * nx + c;
-        const int ix = (r & 7) * 8 + (c & 7);
-        // g(x), moves(x) and the neighbours' tile slots are read together
-        const double gx = gtile(sx)[ix];
-        const unsigned mv = mtile(sx)[ix];
-        const int rr = r + dr_, cc = c + dc_;
-        const bool legal = (mv & lanebit) != 0u;
-        // the tile-map read does not wait for the move byte (index clamped)
-        const int ty = min(max((rr >> 3) * TW + (cc >> 3), 0), NT - 1);
-        const int iy = (rr & 7) * 8 + (cc & 7);
-        const int sy0 = (int)tmap[ty];
-        int sy = legal ? sy0 : (int)kNoSlot;
-        const double hh = octile(rr, cc, gr, gc);
-        if (x == goal) { found = 1; break; }
-        // No stale test (paths.py:70-71) is needed here: the head never holds a
-        // stale entry (refills drop them, decrease-keys evict the old head copy),
-        // and re-expanding a cell with its current g would relax nothing anyway.
-        ++s_exp;
-        const double gy = sy != (int)kNoSlot ? gtile(sy)[iy] : CUDART_INF;
-        const double ng = gx + w_;
-        const bool push = legal && ng < gy - 1e-12;
-        const bool fresh = gy == CUDART_INF;
-        // routing never looks at the tile slot ((h, row, col) is unique per
-        // cell), so it is decided together with the first-write test
-        const Key ne0 = {(u64)__double_as_longlong(ng + hh), make_key2(hh, rr, cc, 0)};
-        if (st.nn + 16 > NC) {
-          st = split_near(st, pl, lane);
-          if (st.err) { found = -1; break; }
-        }
-        const bool need = push && sy == (int)kNoSlot;
-        const bool toH = push && klt(ne0, st.T);
-        const bool toN = push && !toH && klt(ne0, st.F2);
-        const bool toF = push && !toH && !toN;
-        const unsigned nm = __ballot_sync(0xffffffffu, need);
-        unsigned mh = __ballot_sync(0xffffffffu, toH);
-        const unsigned nmk = __ballot_sync(0xffffffffu, toN);
-        const unsigned fmk = __ballot_sync(0xffffffffu, toF);
-        // first write into a tile: hand out slots (one per distinct tile)
-        if (nm) {
-          const unsigned peers = __match_any_sync(0xffffffffu, need ? ty : -1 - lane);
-          const int leader = __ffs(peers) - 1;
-          const unsigned lm = __ballot_sync(0xffffffffu, need && leader == lane);
-          unsigned L = lm;
-          int mine = 0;
-          while (L) {
-            const int ld = __ffs(L) - 1;
-            L &= L - 1;
-            const int s = new_tile(__shfl_sync(0xffffffffu, ty, ld));
-            if (lane == ld) mine = s;
-          }
-          const int got = __shfl_sync(0xffffffffu, mine, leader);
-          if (need) sy = got;
-          __syncwarp();
-        }
-        if (push) {
-          gtile(sy)[iy] = ng;
-          parent[rr * nx + cc] = x;
-        }
-        const Key ne = {ne0.f, ne0.k | ((u64)sy << 5)};
-        if (st.nf + 16 > pl.far_cap) { found = -1; break; }
-        if (toN) { OpenEnt o = {ne.f, ne.k}; pl.near[st.nn + __popc(nmk & lt_mask)] = o; }
-        if (toF) { OpenEnt o = {ne.f, ne.k}; pl.far[st.nf + __popc(fmk & lt_mask)] = o; }
-        st.nn += __popc(nmk);
-        st.nf += __popc(fmk);
-        while (mh) {
-          const int s = __ffs(mh) - 1;
-          mh &= mh - 1;
-          const Key v = shfl_key(ne, s);
-          if (!__shfl_sync(0xffffffffu, fresh, s)) {
-            // decrease-key: the cell's previous (now stale) entry leaves the head
-            // if it is there -- a stale pop is a no-op (paths.py:70-71)
-            const unsigned om = __ballot_sync(0xffffffffu, ((st.hd.k ^ v.k) & kCellMask2) == 0ull);
-            if (om) {
-              const int L = __ffs(om) - 1;
-              const Key dn = shfl_key_down(st.hd, 1);
-              if (lane >= L) st.hd = lane < st.h - 1 ? dn : key_inf();
-              st.h -= 1;
-            }
-          }
-          const Key up = shfl_key_up(st.hd, 1);
-          const int p = __popc(__ballot_sync(0xffffffffu, klt(st.hd, v)));   // +inf beyond h
-          if (st.h == 32) {
-            // full head: its largest key (or v itself) moves to the pool and bounds it
-            const Key ev = p == 32 ? v : shfl_key(st.hd, 31);
-            const bool evn = klt(ev, st.F2);
-            if (lane == 0) {
-              OpenEnt o = {ev.f, ev.k};
-              if (evn) pl.near[st.nn] = o;
-              else pl.far[st.nf] = o;
-            }
-            st.nn += evn;
-            st.nf += !evn;
-            st.T = ev;
-            if (p == 32) continue;
-            st.h = 31;
-          }
-          if (lane > p && lane <= st.h) st.hd = up;
-          if (lane == p) st.hd = v;
-          st.h += 1;
-        }
-        __syncwarp();
-      }
-      delta = st.delta;
-      delta2 = st.delta2;
     }
     // ---- write the guidance result (field.py:204-212)
     const size_t ia = (size_t)e * P.A + R.agent;
@@ -591,14 +631,14 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
     if (found == -1 && lane == 0) atomicCAS(&S.flags[1], 0, (int)CW_E_HEAPCAP);
     if (found == 1) {
       int L = 1;
-      for (int v = goal; v != start; v = parent[v]) ++L;
+      for (int v = goal; v != start; v = E.parent[v]) ++L;
       if (L >= 2) {
         if (L - 1 > P.path_cap) {
           if (lane == 0) atomicCAS(&S.flags[1], 0, (int)CW_E_PATHCAP);
         } else {
           if (lane == 0) {
             int k = L - 2;
-            for (int v = goal; k >= 0; v = parent[v]) cells[k--] = v;
+            for (int v = goal; k >= 0; v = E.parent[v]) cells[k--] = v;
           }
           __syncwarp();
           pn = L;
@@ -614,17 +654,14 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
       S.waypoint[ia * 2] = wx;
       S.waypoint[ia * 2 + 1] = wy;
     }
-    // release the tiles
-    __syncwarp();
-    for (int k = lane; k < used; k += 32) tmap[s2t[k]] = kNoSlot;
-    __syncwarp();
+    const int used_final = used;
+    release();
     const long long dt = clock64() - t0;
     if (dbg && lane == 0) {
       long long* d = dbg + (size_t)q * 8;
-      d[0] = dt; d[1] = s_exp; d[2] = s_stale; d[3] = used;
+      d[0] = dt; d[1] = s_exp; d[2] = 0; d[3] = used_final;
     }
     n_exp += s_exp;
-    n_stale += s_stale;
     t_sum += dt;
     t_max = max(t_max, dt);
   }
@@ -632,7 +669,7 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
     if (n_exp) atomicAdd((unsigned long long*)&S.counters[0], n_exp);
     if (t_sum) atomicAdd((unsigned long long*)&S.counters[4], (unsigned long long)t_sum);
     if (t_max) atomicMax((unsigned long long*)&S.counters[5], (unsigned long long)t_max);
-    if (n_stale) atomicAdd((unsigned long long*)&S.counters[10], n_stale);
+    if (n_glob) atomicAdd((unsigned long long*)&S.counters[10], n_glob);
   }
 }
 

@@ -88,5 +88,5 @@ for k in range(steps):
     f.check_flags()
     run(4)
     tot += t
-    print(f"step {k:3d} req {nreq:5d} exp {c[0]:8d} stale {c[10]:7d} max_cyc {c[5]/1e6:7.2f}M  ms {t:7.3f}", flush=True)
+    print(f"step {k:3d} req {nreq:5d} exp {c[0]:8d} glob {c[10]:3d} max_cyc {c[5]/1e6:7.2f}M  ms {t:7.3f}", flush=True)
 print(f"TOTAL {tot:.2f} ms over {steps} ticks")
