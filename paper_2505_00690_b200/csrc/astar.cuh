@@ -44,8 +44,10 @@ constexpr u64 kInf64 = ~0ull;
 
 CW_DEV Key key_inf() { return {kInf64, kInf64}; }
 
+// branch-free lexicographic compare (bitwise predicate logic: no short-circuit
+// control flow for the compiler to turn into divergent branches)
 CW_DEV bool klt(const Key& a, const Key& b) {
-  return (((u128)a.f << 64) | a.k) < (((u128)b.f << 64) | b.k);
+  return (a.f < b.f) | ((a.f == b.f) & (a.k < b.k));
 }
 
 CW_DEV Key shfl_key(const Key& v, int src) {
@@ -467,7 +469,7 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
     ++s_exp;
     const double gy = sy != (int)kNoSlot ? gt[(size_t)sy * 64 + iy] : CUDART_INF;
     const double ng = gx + w_;
-    const bool push = legal && ng < gy - 1e-12;
+    const bool push = legal & (ng < gy - 1e-12);
     const bool fresh = gy == CUDART_INF;
     // routing never looks at the tile slot ((h, row, col) is unique per
     // cell), so it is decided together with the first-write test
@@ -476,14 +478,16 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
       st = split_near(st, pl, lane);
       if (st.err) { found = -1; break; }
     }
-    const bool need = push && sy == (int)kNoSlot;
-    const bool toH = push && klt(ne0, st.T);
-    const bool toN = push && !toH && klt(ne0, st.F2);
-    const bool toF = push && !toH && !toN;
+    const bool ltT = klt(ne0, st.T), ltF2 = klt(ne0, st.F2);
+    const bool need = push & (sy == (int)kNoSlot);
+    const bool toH = push & ltT;
+    const bool toN = push & !ltT & ltF2;
+    const bool toF = push & !ltT & !ltF2;
     const unsigned nm = __ballot_sync(0xffffffffu, need);
     unsigned mh = __ballot_sync(0xffffffffu, toH);
     const unsigned nmk = __ballot_sync(0xffffffffu, toN);
     const unsigned fmk = __ballot_sync(0xffffffffu, toF);
+    const unsigned decm = __ballot_sync(0xffffffffu, push & !fresh);
     // first write into a tile: hand out slots (one per distinct tile)
     if (nm) {
       const unsigned peers = __match_any_sync(0xffffffffu, need ? ty : -1 - lane);
@@ -516,7 +520,7 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
       const int s = __ffs(mh) - 1;
       mh &= mh - 1;
       const Key v = shfl_key(ne, s);
-      if (!__shfl_sync(0xffffffffu, fresh, s)) {
+      if ((decm >> s) & 1u) {
         // decrease-key: the cell's previous (now stale) entry leaves the head
         // if it is there -- a stale pop is a no-op (paths.py:70-71)
         const unsigned om = __ballot_sync(0xffffffffu, ((st.hd.k ^ v.k) & kCellMask2) == 0ull);
