@@ -336,12 +336,32 @@ __global__ void __launch_bounds__(NT) k_guide(cw_crowd_params P, cw_crowd_state 
 }
 
 // ---------------------------------------------------------------- ORCA + commit
+// Agent binning for the neighbour search (used when A is large).
+struct Bins {
+  int ncx, ncy;     // 0 = no binning
+  double inv_cs;
+};
+
+CW_HD Bins make_bins(const cw_crowd_params& P) {
+  Bins b = {0, 0, 0.0};
+  if (P.A < 128) return b;
+  const double cs = P.neighbor_distance + 0.5;
+  b.ncx = (int)ceil(P.nx * P.res / cs);
+  b.ncy = (int)ceil(P.ny * P.res / cs);
+  b.inv_cs = 1.0 / cs;
+  return b;
+}
+
+CW_HD size_t bins_smem_bytes(const Bins& b, int A) {
+  return b.ncx > 0 ? (size_t)(b.ncx * b.ncy + 1 + 2 * A) * 4 : 0;
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S,
                                              const double* __restrict__ robot_pos,
                                              const double* __restrict__ robot_vel,
                                              double robot_radius,
-                                             const uint8_t* __restrict__ env_mask) {
+                                             const uint8_t* __restrict__ env_mask, Bins bins) {
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char sm[];
   const int e = blockIdx.x;
@@ -356,6 +376,10 @@ __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S
   double* s_ny = s_nx + A;
   WarpCons* s_cons = reinterpret_cast<WarpCons*>(s_ny + A);
   uint8_t* s_act = reinterpret_cast<uint8_t*>(s_cons + NW);
+  // agent binning (large A): cell ends after the scatter, sorted agent ids, agent cell
+  int* s_cend = reinterpret_cast<int*>(s_act + ((A + 15) & ~15));
+  int* s_sorted = s_cend + bins.ncx * bins.ncy + 1;
+  int* s_cell = s_sorted + A;
   __shared__ double s_gap[NW];
   __shared__ int s_anynb[NW];
   const long long t_cta0 = clock64();
@@ -372,6 +396,43 @@ __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S
     s_act[a] = (S.active[eA + a] && emask) ? 1 : 0;
   }
   __syncthreads();
+  if (bins.ncx > 0) {
+    // counting sort of the active agents into square cells of side >= nd + 0.5 m:
+    // every j with fp32 key(i, j) < nd^2 (key error < 0.03 m^2 on <= 128 m grids)
+    // lies in the 3 x 3 cells around i; selection below still uses (key, index)
+    const int nc = bins.ncx * bins.ncy;
+    for (int c = threadIdx.x; c <= nc; c += NT) s_cend[c] = 0;
+    __syncthreads();
+    for (int a = threadIdx.x; a < A; a += NT) {
+      int cell = -1;
+      if (s_act[a]) {
+        const int cx = min(max((int)(s_px[a] * bins.inv_cs), 0), bins.ncx - 1);
+        const int cy = min(max((int)(s_py[a] * bins.inv_cs), 0), bins.ncy - 1);
+        cell = cy * bins.ncx + cx;
+        atomicAdd(&s_cend[cell + 1], 1);
+      }
+      s_cell[a] = cell;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {   // exclusive scan of the counts (one warp)
+      int carry = 0;
+      for (int c0 = 0; c0 <= nc; c0 += 32) {
+        const int c = c0 + lane;
+        int v = c <= nc ? s_cend[c] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= o) v += t;
+        }
+        if (c <= nc) s_cend[c] = v + carry;
+        carry += __shfl_sync(0xffffffffu, v, 31);
+      }
+    }
+    __syncthreads();
+    for (int a = threadIdx.x; a < A; a += NT)   // afterwards s_cend[c] = end of cell c
+      if (s_cell[a] >= 0) s_sorted[atomicAdd(&s_cend[s_cell[a]], 1)] = a;
+    __syncthreads();
+  }
   const int nx = P.nx, ny = P.ny;
   const size_t N = (size_t)nx * ny;
   const uint8_t* lab = S.labels + e * N;
@@ -413,19 +474,37 @@ __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S
     int nb = 0;
     int my_nb = -1;
     const int kmax = min(P.max_neighbors, max(A - 1, 0));
+    // candidate ranges: all agents, or the three cell-row runs around a's cell
+    int rs[3] = {0, 0, 0}, re[3] = {A, 0, 0};
+    if (bins.ncx > 0) {
+      const int cx = s_cell[a] % bins.ncx, cy = s_cell[a] / bins.ncx;
+      const int x0 = max(cx - 1, 0), x1 = min(cx + 1, bins.ncx - 1);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int row = cy - 1 + d;
+        const bool ok = row >= 0 && row < bins.ncy;
+        const int c0 = row * bins.ncx + x0, c1 = row * bins.ncx + x1;
+        rs[d] = ok ? (c0 > 0 ? s_cend[c0 - 1] : 0) : 0;
+        re[d] = ok ? s_cend[c1] : 0;
+      }
+    }
     for (int round = 0; round < kmax; ++round) {
       float bk = CUDART_INF_F;
       int bj = 0x7fffffff;
-      for (int j = lane; j < A; j += 32) {
-        if (j == a || !s_act[j]) continue;
-        float xj = (float)s_px[j], yj = (float)s_py[j];
-        float sqj = __fadd_rn(__fmul_rn(xj, xj), __fmul_rn(yj, yj));
-        float dot = __fmaf_rn(yi, yj, __fmul_rn(xi, xj));
-        float key = __fsub_rn(__fadd_rn(sqi, sqj), __fmul_rn(2.0f, dot));
-        if (!(key < P.nd2_f32)) continue;
-        bool after = key > last_k || (key == last_k && j > last_j);
-        bool better = key < bk || (key == bk && j < bj);
-        if (after && better) { bk = key; bj = j; }
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        for (int t = rs[d] + lane; t < re[d]; t += 32) {
+          const int j = bins.ncx > 0 ? s_sorted[t] : t;
+          if (j == a || !s_act[j]) continue;
+          float xj = (float)s_px[j], yj = (float)s_py[j];
+          float sqj = __fadd_rn(__fmul_rn(xj, xj), __fmul_rn(yj, yj));
+          float dot = __fmaf_rn(yi, yj, __fmul_rn(xi, xj));
+          float key = __fsub_rn(__fadd_rn(sqi, sqj), __fmul_rn(2.0f, dot));
+          if (!(key < P.nd2_f32)) continue;
+          bool after = key > last_k || (key == last_k && j > last_j);
+          bool better = key < bk || (key == bk && j < bj);
+          if (after && better) { bk = key; bj = j; }
+        }
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
@@ -594,7 +673,8 @@ template <int NT>
 static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const double* rp,
                        const double* rv, double rr, const uint8_t* em, int phases,
                        cudaStream_t st) {
-  size_t sm = cw_crowd_step_smem_bytes(P.A, NT);
+  const Bins bins = make_bins(P);
+  size_t sm = cw_crowd_step_smem_bytes(P.A, NT) + bins_smem_bytes(bins, P.A);
   if ((phases & 4) && sm > 48 * 1024)
     cudaFuncSetAttribute(k_orca<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (phases & 1) k_guide<NT><<<P.E, NT, 0, st>>>(P, S, em);
@@ -602,7 +682,7 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
     const AstarShape A = astar_shape(P.nx, P.ny);
     k_astar<<<P.astar_ctas, 32, A.smem, st>>>(P, S, A.NC, A.NS);
   }
-  if (phases & 4) k_orca<NT><<<P.E, NT, sm, st>>>(P, S, rp, rv, rr, em);
+  if (phases & 4) k_orca<NT><<<P.E, NT, sm, st>>>(P, S, rp, rv, rr, em, bins);
   return (int)cudaGetLastError();
 }
 
@@ -611,7 +691,8 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
 extern "C" {
 
 size_t cw_crowd_step_smem_bytes(int A, int nt) {
-  return (size_t)A * 7 * sizeof(double) + (size_t)(nt / 32) * sizeof(cw::WarpCons) + (size_t)A + 16;
+  return (size_t)A * 7 * sizeof(double) + (size_t)(nt / 32) * sizeof(cw::WarpCons) +
+         (size_t)((A + 15) & ~15) + 16;
 }
 
 // Bytes of A* scratch (astar_rec) per k_astar CTA for an nx x ny grid.

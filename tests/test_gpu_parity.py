@@ -170,13 +170,15 @@ def test_crowd_matches_oracle(shape, torch_cuda):
         assert np.array_equal(f.goal, ref.goal), t
 
 
-def test_dense_open_grid_fallback_matches_oracle(torch_cuda):
+@pytest.mark.parametrize("arena,E,A,T", [(12.0, 4, 40, 150), (24.0, 2, 200, 60)])
+def test_dense_open_grid_fallback_matches_oracle(arena, E, A, T, torch_cuda):
     """Obstacle-free dense crowds exercise the least-violation fallback and the
-    stall retry heavily (acceptance sweep shape, tests/test_acceptance.py:209-249)."""
+    stall retry heavily (acceptance sweep shape, tests/test_acceptance.py:209-249).
+    A = 200 runs the cell-binned neighbour search (A >= 128)."""
     from oracle import crowd as C
     from paper_2505_00690_b200.crowd import CrowdAgent, CrowdConfig, CrowdField
     from paper_2505_00690_b200.urbangen import OccupancyGrid
-    arena, res, E, A = 12.0, 0.1, 4, 40
+    res = 0.1
     n = int(arena / res)
     labels = np.full((n, n), 2, np.uint8)
     occ = OccupancyGrid(res, labels, np.zeros((n, n), np.float32))
@@ -200,7 +202,7 @@ def test_dense_open_grid_fallback_matches_oracle(torch_cuda):
     ref.set_agents([dict(pos=np.array([a.position for a in l]), goal=np.array([a.goal for a in l]),
                          radius=np.full(A, 0.3), pref=np.array([a.preferred_speed for a in l]),
                          max_speed=np.full(A, 2.0), kind=np.zeros(A, np.int8)) for l in lists])
-    for t in range(150):
+    for t in range(T):
         f.step()
         ref.step()
         assert np.array_equal(f.pos, ref.pos), t
@@ -283,9 +285,11 @@ def test_shard_invariance_sampling_and_crowd(torch_cuda):
         assert np.array_equal(f1.goal[sl], f.goal)
 
 
-def test_blocks_layout_dense_crowd_matches_oracle(torch_cuda):
+@pytest.mark.parametrize("peds", [96, 160])
+def test_blocks_layout_dense_crowd_matches_oracle(peds, torch_cuda):
     """cfg4 shape (block layout with roads/crosswalks, NavClear placement, many
-    pedestrians, neighbor_distance 3 m) against the oracle for a few ticks."""
+    pedestrians, neighbor_distance 3 m) against the oracle for a few ticks;
+    160 pedestrians run the cell-binned neighbour search."""
     from oracle import crowd as C
     from oracle import scene as S
     from oracle.rng import child_seed
@@ -293,14 +297,14 @@ def test_blocks_layout_dense_crowd_matches_oracle(torch_cuda):
     from paper_2505_00690_b200.urbangen import SceneSampler, SceneSpec, TaskKind
     seed = child_seed(0, "env", 11)
     spec = SceneSpec(seed=seed, extent_m=(48.0, 48.0), task_kind=TaskKind.NAV_CLEAR,
-                     object_density=0.0, pedestrian_count=96, terrain_mix=MIX,
+                     object_density=0.0, pedestrian_count=peds, terrain_mix=MIX,
                      grid_resolution_m=0.25)
     b = SceneSampler(spec, 1).sample([seed], [child_seed(seed, "crowd", 0)])
     sc = S.generate_scene(dict(seed=seed, extent=(48.0, 48.0), res=0.25, task="NavClear",
                                split="Train", density=0.0, mix=MIX), golden_catalog())
     assert np.array_equal(b.zones[0].cpu().numpy(), sc["zones"])
     assert np.array_equal(b.labels[0].cpu().numpy(), sc["labels"])
-    sp = C.spawn_agents(sc["labels"], 0.25, 96, child_seed(seed, "crowd", 0))
+    sp = C.spawn_agents(sc["labels"], 0.25, peds, child_seed(seed, "crowd", 0))
     assert np.array_equal(b.sp_pos[0].cpu().numpy(), sp["pos"])
     assert np.array_equal(b.sp_goal[0].cpu().numpy(), sp["goal"])
     run = [child_seed(seed, "crowd-run")]
