@@ -120,8 +120,8 @@ typedef struct cw_crowd_params {
   int32_t max_neighbors;
   double dt, safety_margin, goal_reach2, stall_c, stall_s;
   int32_t resample_goals, use_static, path_cap;
-  int32_t heap_cap;     /* A* far-pool entries (16 B) per k_astar CTA */
-  int32_t astar_ctas;   /* persistent k_astar CTAs, one search warp each (one per SM) */
+  int32_t heap_cap;     /* A* far-pool entries (16 B) per search warp */
+  int32_t astar_ctas;   /* persistent k_astar CTAs (one per SM, cw_astar_warps() warps each) */
 } cw_crowd_params;
 
 /* Device-resident CrowdField state (field.py:47-58) + guidance/A* scratch. */
@@ -135,9 +135,9 @@ typedef struct cw_crowd_state {
   const int32_t* reach; const uint8_t* moves;
   void* rng;
   double* last_gap; double* gap_tmp; int32_t* flags;
-  void* astar_rec;      /* astar_ctas x cw_astar_slot_bytes(nx, ny): overflow g/move tiles,
-                           parent per cell, tile-slot map (no initialisation needed) */
-  void* astar_heap;     /* (astar_ctas, heap_cap, 16 B) A* far pool */
+  void* astar_rec;      /* astar_ctas * cw_astar_warps() x cw_astar_slot_bytes(nx, ny): all-global
+                           g/move tiles, parent per cell, tile log (no initialisation needed) */
+  void* astar_heap;     /* (astar_ctas * cw_astar_warps(), heap_cap, 16 B) A* far pools */
   void* astar_req;      /* (E*A, 16 B) replanning queue {env, agent, start, goal} */
   int64_t* counters;
 } cw_crowd_state;
@@ -155,7 +155,9 @@ int cw_crowd_step_phases(const cw_crowd_params* params, const cw_crowd_state* st
                          const double* robot_pos, const double* robot_vel, double robot_radius,
                          const uint8_t* env_mask, int threads, int phases, void* stream);
 
-/* Bytes of astar_rec per k_astar CTA for an nx x ny grid (host-only query). */
+/* Search warps per k_astar CTA (host-only query). */
+int cw_astar_warps(void);
+/* Bytes of astar_rec per k_astar search warp for an nx x ny grid (host-only query). */
 size_t cw_astar_slot_bytes(int nx, int ny);
 
 int cw_seed_streams(int n, const uint64_t* seeds, void* out_states, void* stream);

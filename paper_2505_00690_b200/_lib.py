@@ -74,7 +74,7 @@ class CrowdState(ctypes.Structure):
 
 EXPORTS = ["cw_scene_seed_scratch_bytes", "cw_sample_scenes", "cw_spawn_agents", "cw_prepare_envs",
            "cw_crowd_step_smem_bytes",
-           "cw_crowd_step", "cw_crowd_step_phases", "cw_astar_slot_bytes", "cw_seed_streams", "cw_child_seeds", "cw_abi_sizes"]
+           "cw_crowd_step", "cw_crowd_step_phases", "cw_astar_slot_bytes", "cw_astar_warps", "cw_seed_streams", "cw_child_seeds", "cw_abi_sizes"]
 
 _lib = None
 
@@ -118,6 +118,8 @@ def lib():
     L.cw_crowd_step_phases.restype = ctypes.c_int
     L.cw_crowd_step_phases.argtypes = [ctypes.POINTER(CrowdParams), ctypes.POINTER(CrowdState), P,
                                        P, ctypes.c_double, P, ctypes.c_int, ctypes.c_int, P]
+    L.cw_astar_warps.restype = ctypes.c_int
+    L.cw_astar_warps.argtypes = []
     L.cw_astar_slot_bytes.restype = ctypes.c_size_t
     L.cw_astar_slot_bytes.argtypes = [ctypes.c_int, ctypes.c_int]
     L.cw_seed_streams.restype = ctypes.c_int

@@ -129,7 +129,7 @@ class CrowdField:
         N = self.nx * self.ny
         self.path_cap = int(path_cap or 2 * (self.nx + self.ny) + 64)
         self.heap_cap = int(heap_cap or min(max(65536, N), (1 << 19) - 1))
-        # persistent A* search warps: one per SM (each owns ~200 KB of shared memory)
+        # persistent A* CTAs: one per SM, cw_astar_warps() search warps sharing its tile pool
         self.astar_ctas = int(torch.cuda.get_device_properties(self.device).multi_processor_count) \
             if self.device.type == "cuda" else 1
         self.last_gap_t = torch.full((self.E,), float("inf"), dtype=torch.float64, device=self.device)
@@ -199,7 +199,7 @@ class CrowdField:
         import torch
         if self._astar_ready:
             return
-        S = self.astar_ctas
+        S = self.astar_ctas * int(_lib.lib().cw_astar_warps())   # search warps
         N = self.nx * self.ny
         d = self.device
         slot = int(_lib.lib().cw_astar_slot_bytes(self.nx, self.ny))

@@ -346,46 +346,74 @@ CW_HD size_t astar_slot_bytes(int nx, int ny, int S) {
   return (b + 255) & ~(size_t)255;
 }
 
-// Launch shape of k_astar: one search warp per SM owning ~200 KB of shared
-// memory -- near pool NC x 16 B + 64-entry staging, the tile map (2 B per
-// tile) and NS tile slots of 576 B (64 x f64 g + 64 move bytes).
+// Launch shape of k_astar: one CTA per SM with W search warps (one per SM
+// sub-partition).  Each warp owns a near pool (NC x 16 B), a 64-entry staging
+// area and a tile map (2 B per tile); the NS tile slots of 576 B (64 x f64 g +
+// 64 move bytes) form one pool shared by the CTA's warps (a locked stack of
+// free slot ids), so a lone long search can use nearly all of it.
+constexpr int kAstarWarps = 4;
+
 struct AstarShape {
-  int NC, NS;
+  int NC, NS, W;
+  size_t per_warp;   // bytes of one warp's private block
   size_t smem;
 };
 
 CW_HD AstarShape astar_shape(int nx, int ny) {
   const int nt = ((nx + 7) / 8) * ((ny + 7) / 8);
-  const int NC = 1024;
-  const size_t fixed = (size_t)(NC + 64) * 16 + (((size_t)nt * 2 + 15) & ~(size_t)15);
-  const size_t budget = 200 * 1024;
-  int NS = budget > fixed ? (int)((budget - fixed) / 576) : 0;
-  NS = NS > nt ? nt : NS;
-  return {NC, NS, fixed + (size_t)NS * 576};
+  const int W = kAstarWarps, NC = 512;
+  const size_t per_warp = (size_t)(NC + 64) * 16 + (((size_t)nt * 2 + 15) & ~(size_t)15);
+  const size_t budget = 220 * 1024, head = 16;   // lock + stack top
+  const size_t fixed = W * per_warp + head;
+  int NS = budget > fixed ? (int)((budget - fixed) / (576 + 2)) : 0;
+  NS = NS > W * nt ? W * nt : NS;
+  NS = NS > 65535 ? 65535 : NS;
+  const size_t stack = ((size_t)NS * 2 + 15) & ~(size_t)15;
+  return {NC, NS, W, per_warp, fixed + stack + (size_t)NS * 576};
 }
 
 // Per-CTA layout shared by the two search instantiations.
 struct SearchEnv {
   int nx, ny, N, TW, NT, NS;
-  uint16_t* tmap;        // shared: tile -> slot (kNoSlot when unused)
-  double* gts;           // shared: NS x 64 g
-  uint8_t* mts;          // shared: NS x 64 move bytes
-  double* gtg;           // global: NT x 64 g (all-global instantiation)
-  uint8_t* mtg;          // global: NT x 64 move bytes
-  int32_t* parent;       // global: N
-  int32_t* s2t;          // global: slot -> tile
+  uint16_t* tmap;        // shared, this warp: tile -> slot (kNoSlot when unused)
+  double* gts;           // shared, CTA pool: NS x 64 g
+  uint8_t* mts;          // shared, CTA pool: NS x 64 move bytes
+  uint16_t* free_ids;    // shared, CTA pool: stack of free slot ids
+  int* pool_lock;        // shared: [0] lock, [1] stack top
+  uint16_t* wbuf;        // shared, this warp: 8 freshly taken slot ids
+  double* gtg;           // global, this warp: NT x 64 g (all-global instantiation)
+  uint8_t* mtg;          // global, this warp: NT x 64 move bytes
+  int32_t* parent;       // global, this warp: N
+  int32_t* s2t;          // global, this warp: allocation k -> slot << 16 | tile
 };
 
+// Take n slots from the CTA pool (lane 0; false if it holds fewer).
+CW_DEV bool pool_take(const SearchEnv& E, int n, uint16_t* out) {
+  while (atomicCAS(&E.pool_lock[0], 0, 1) != 0) {}
+  __threadfence_block();
+  volatile int* top_p = &E.pool_lock[1];
+  volatile uint16_t* ids = E.free_ids;
+  const int top = *top_p;
+  const bool ok = top >= n;
+  if (ok) {
+    for (int i = 0; i < n; ++i) out[i] = ids[top - 1 - i];
+    *top_p = top - n;
+  }
+  __threadfence_block();
+  atomicExch(&E.pool_lock[0], 0);
+  return ok;
+}
+
 // One search, paths.astar_path (paths.py:48-87).  kGlob = false keeps every
-// tile in shared memory and returns -2 when they run out (the caller retries
-// with kGlob = true, all tiles in the global backing store).  Returns 1 found,
-// 0 no path, -1 open-set overflow; `used` = tile slots handed out.
+// tile in the CTA's shared pool and returns -2 when the pool runs dry (the
+// caller releases and retries with kGlob = true, all tiles in the warp's global
+// backing store).  Returns 1 found, 0 no path, -1 open-set overflow; `used` =
+// tiles handed out (recorded in s2t).
 template <bool kGlob>
 CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int start, int goal,
                       double& delta, double& delta2, unsigned& s_exp, int& used, int lane) {
   double* const gt = kGlob ? E.gtg : E.gts;
   uint8_t* const mt = kGlob ? E.mtg : E.mts;
-  const int cap = kGlob ? E.NT : E.NS;
   const int nx = E.nx, ny = E.ny, TW = E.TW, NT = E.NT, NC = pl.NC;
   const unsigned lt_mask = (1u << lane) - 1u;
   // paths.py:75 move order: N S W E, then the diagonals (nibble per lane, +1)
@@ -398,9 +426,10 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
   pl.gt = gt;
   pl.gr = gr;
   pl.gc = gc;
-  // give tile t the next slot: g = +inf, move bytes copied from the env table
-  auto new_tile = [&](int t) {
-    const int s = used++;
+  // tile t gets slot s: g = +inf, move bytes copied from the env table
+  auto new_tile = [&](int t, int s) {
+    if (lane == 0) E.s2t[used] = (s << 16) | t;
+    ++used;
     double* gp = gt + (size_t)s * 64;
     uint8_t* mp = mt + (size_t)s * 64;
     const int r0 = (t / TW) * 8, c0 = (t % TW) * 8;
@@ -410,11 +439,21 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
       const int rr = r0 + (j >> 3), cc = c0 + (j & 7);
       mp[j] = (rr < ny && cc < nx) ? mvt[rr * nx + cc] : (uint8_t)0;
     }
-    if (lane == 0) { E.tmap[t] = (uint16_t)s; E.s2t[s] = t; }
+    if (lane == 0) E.tmap[t] = (uint16_t)s;
     return s;
   };
+  // n slot ids for this warp: sequential (all-global) or from the CTA pool
+  auto take = [&](int n) -> bool {
+    if (kGlob) return true;
+    bool ok = false;
+    if (lane == 0) ok = pool_take(E, n, E.wbuf);
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    __syncwarp();
+    return ok;
+  };
   const double h0 = octile(sr, sc, gr, gc);
-  const int s0 = new_tile((sr >> 3) * TW + (sc >> 3));
+  if (!take(1)) return -2;
+  const int s0 = new_tile((sr >> 3) * TW + (sc >> 3), kGlob ? 0 : (int)E.wbuf[0]);
   __syncwarp();
   if (lane == 0) {
     gt[(size_t)s0 * 64 + (sr & 7) * 8 + (sc & 7)] = 0.0;
@@ -493,13 +532,14 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
       const unsigned peers = __match_any_sync(0xffffffffu, need ? ty : -1 - lane);
       const int leader = __ffs(peers) - 1;
       const unsigned lm = __ballot_sync(0xffffffffu, need && leader == lane);
-      if (used + __popc(lm) > cap) { found = -2; break; }   // only when !kGlob
+      if (!take(__popc(lm))) { found = -2; break; }   // only when !kGlob
       unsigned L = lm;
-      int mine = 0;
+      int mine = 0, k = 0;
       while (L) {
         const int ld = __ffs(L) - 1;
         L &= L - 1;
-        const int s = new_tile(__shfl_sync(0xffffffffu, ty, ld));
+        const int s = new_tile(__shfl_sync(0xffffffffu, ty, ld), kGlob ? used : (int)E.wbuf[k]);
+        ++k;
         if (lane == ld) mine = s;
       }
       const int got = __shfl_sync(0xffffffffu, mine, leader);
@@ -563,9 +603,11 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
 // paths.astar_path exactly; results go to the agent's path (field.py:204-212).
 // Unreachable goals (different 4-connected component, see k_reach) return None
 // without searching -- the reference exhausts the component and returns None.
-__global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state S, int NC, int NS) {
+__global__ void __launch_bounds__(32 * kAstarWarps, 1) k_astar(cw_crowd_params P, cw_crowd_state S, int NC,
+                                                            int NS) {
   extern __shared__ __align__(16) unsigned char sm[];
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kAstarWarps + w;       // global search-warp id (scratch slot)
   SearchEnv E;
   E.nx = P.nx;
   E.ny = P.ny;
@@ -575,24 +617,31 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
   E.NS = NS;
   const int nx = E.nx, N = E.N, NT = E.NT;
   const AstarReq* reqs = reinterpret_cast<const AstarReq*>(S.astar_req);
+  const AstarShape shp = astar_shape(P.nx, P.ny);
+  unsigned char* const wblk = sm + (size_t)w * shp.per_warp;
   Pools pl;
-  pl.near = reinterpret_cast<OpenEnt*>(sm);
+  pl.near = reinterpret_cast<OpenEnt*>(wblk);
   pl.stg = pl.near + NC;
-  pl.far = reinterpret_cast<OpenEnt*>(S.astar_heap) + (size_t)blockIdx.x * P.heap_cap;
+  pl.far = reinterpret_cast<OpenEnt*>(S.astar_heap) + (size_t)gw * P.heap_cap;
   pl.NC = NC;
   pl.far_cap = P.heap_cap;
   E.tmap = reinterpret_cast<uint16_t*>(pl.stg + 64);
-  E.gts = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(E.tmap) +
-                                    (((size_t)NT * 2 + 15) & ~(size_t)15));
+  unsigned char* const pool = sm + (size_t)kAstarWarps * shp.per_warp;
+  E.pool_lock = reinterpret_cast<int*>(pool);
+  E.free_ids = reinterpret_cast<uint16_t*>(pool + 16);
+  E.gts = reinterpret_cast<double*>(pool + 16 + (((size_t)NS * 2 + 15) & ~(size_t)15));
   E.mts = reinterpret_cast<uint8_t*>(E.gts + (size_t)NS * 64);
+  E.wbuf = reinterpret_cast<uint16_t*>(pl.stg) + 0;   // staging area doubles as the slot buffer
   unsigned char* const gbase = reinterpret_cast<unsigned char*>(S.astar_rec) +
-                               (size_t)blockIdx.x * astar_slot_bytes(nx, E.ny, NS);
+                               (size_t)gw * astar_slot_bytes(nx, E.ny, NS);
   E.gtg = reinterpret_cast<double*>(gbase);
   E.mtg = gbase + (size_t)NT * 64 * 8;
   E.parent = reinterpret_cast<int32_t*>(E.mtg + (size_t)NT * 64);
   E.s2t = E.parent + N;
   for (int t = lane; t < NT; t += 32) E.tmap[t] = kNoSlot;
-  __syncwarp();
+  for (int i = threadIdx.x; i < NS; i += blockDim.x) E.free_ids[i] = (uint16_t)i;
+  if (threadIdx.x == 0) { E.pool_lock[0] = 0; E.pool_lock[1] = NS; }
+  __syncthreads();
   long long* const dbg = (S.counters && S.counters[14]) ? reinterpret_cast<long long*>(S.counters[14]) : nullptr;
   long long t_max = 0, t_sum = 0;
   unsigned long long n_exp = 0, n_glob = 0;
@@ -612,16 +661,34 @@ __global__ void __launch_bounds__(32) k_astar(cw_crowd_params P, cw_crowd_state 
     int found = 0;  // 1 found, 0 none, -1 open-set overflow
     int used = 0;   // tile slots handed out
     unsigned s_exp = 0;
+    bool pooled = true;   // tiles came from the CTA pool (false after an all-global retry)
     auto release = [&]() {
       __syncwarp();
-      for (int k = lane; k < used; k += 32) E.tmap[E.s2t[k]] = kNoSlot;
+      if (lane == 0 && pooled && used) {
+        while (atomicCAS(&E.pool_lock[0], 0, 1) != 0) {}
+        __threadfence_block();
+      }
+      __syncwarp();
+      const int top = pooled ? *(volatile int*)&E.pool_lock[1] : 0;
+      for (int k = lane; k < used; k += 32) {
+        const int v = E.s2t[k];
+        E.tmap[v & 0xFFFF] = kNoSlot;
+        if (pooled) ((volatile uint16_t*)E.free_ids)[top + k] = (uint16_t)(v >> 16);
+      }
+      __syncwarp();
+      if (lane == 0 && pooled && used) {
+        *(volatile int*)&E.pool_lock[1] = top + used;
+        __threadfence_block();
+        atomicExch(&E.pool_lock[0], 0);
+      }
       __syncwarp();
       used = 0;
     };
     if (lab[start] != L_OBSTACLE && lab[goal] != L_OBSTACLE && reach[start] == reach[goal]) {
       found = run_search<false>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane);
-      if (found == -2) {   // more tiles than shared memory holds: redo it all-global
+      if (found == -2) {   // the shared tile pool ran dry: redo it all-global
         release();
+        pooled = false;
         s_exp = 0;
         ++n_glob;
         found = run_search<true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane);

@@ -680,7 +680,7 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
   if (phases & 1) k_guide<NT><<<P.E, NT, 0, st>>>(P, S, em);
   if (phases & 2) {
     const AstarShape A = astar_shape(P.nx, P.ny);
-    k_astar<<<P.astar_ctas, 32, A.smem, st>>>(P, S, A.NC, A.NS);
+    k_astar<<<P.astar_ctas, 32 * kAstarWarps, A.smem, st>>>(P, S, A.NC, A.NS);
   }
   if (phases & 4) k_orca<NT><<<P.E, NT, sm, st>>>(P, S, rp, rv, rr, em, bins);
   return (int)cudaGetLastError();
@@ -695,7 +695,10 @@ size_t cw_crowd_step_smem_bytes(int A, int nt) {
          (size_t)((A + 15) & ~15) + 16;
 }
 
-// Bytes of A* scratch (astar_rec) per k_astar CTA for an nx x ny grid.
+// Search warps per k_astar CTA (astar_rec / astar_heap hold one slot per warp).
+int cw_astar_warps(void) { return cw::kAstarWarps; }
+
+// Bytes of A* scratch (astar_rec) per k_astar search warp for an nx x ny grid.
 size_t cw_astar_slot_bytes(int nx, int ny) {
   const cw::AstarShape A = cw::astar_shape(nx, ny);
   return cw::astar_slot_bytes(nx, ny, A.NS);
