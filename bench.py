@@ -52,6 +52,17 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def traffic_of(kernel):
+    """dram read+write bytes per launch of `kernel` from the committed ncu --set full
+    capture (profiles/r1_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as fh:
+            k = json.load(fh)["kernels"][kernel]
+        return float(k["dram_read_bytes"] + k["dram_write_bytes"])
+    except Exception:
+        return None
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -177,6 +188,7 @@ def run_ours(args):
     f.counters_t.zero_()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     active = int(f.active_t.sum().item())
     if world > 1:
         dist.barrier()
@@ -207,6 +219,7 @@ def run_ours(args):
             flush.fill_(float(k))          # L2 flush between timed steps (untimed)
             starts[k].record(st)
             resample_mix(k)
+            mids[k].record(st)
             f.step(rpos, rvel, 0.35, check=False)
             ends[k].record(st)
         torch.cuda.synchronize()
@@ -214,6 +227,7 @@ def run_ours(args):
         dist.barrier()
     f.check_flags()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    resample_ms = float(np.mean([s.elapsed_time(m) for s, m in zip(starts, mids)]))
     t_ms = float(sum(step_ms))
     counters = f.stats()
     # ---- per-kernel pass (same stream, events between the three launches)
@@ -301,12 +315,15 @@ def run_ours(args):
                        "parallelism": f"env-shard x{world}", "l2": "flushed (256 MB write) between timed steps",
                        "robot": "static per env at a seeded walkable cell, zero velocity"},
             "scenes_per_sec": round(scenes, 1), "sample_ms_per_batch": round(sample_ms, 3),
+            "resample_ms_per_step": round(resample_ms, 3),
             "agent_steps_per_sec": round(value * CFG["peds"], 1),
             "e2e": {"value": round(E * world * e2e_steps / e2e_s, 1), "unit": "env-steps/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "steps": e2e_steps},
             "roofline": {"bound": "hbm", "achieved": round(dom_ach, 3), "peak": peak, "unit": "GB/s",
-                         "frac": round(dom_ach / peak, 7), "traffic": args.traffic,
+                         "frac": round(dom_ach / peak, 7),
+                         "traffic": args.traffic if args.traffic is not None else traffic_of(dom),
+                         "traffic_source": "ncu --set full, profiles/r1_traffic.json (cfg2 tick 21)",
                          "kernel": dom, "peak_source": src, "bytes_per_launch": round(kb[dom], 1),
                          "avg_launch_ms": round(dom_ms, 4),
                          "note": "latency-bound serial search; see profiles/"},
@@ -328,12 +345,12 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def cpu_baseline_sample(b, f, run_seeds, n_env=4, steps=6):
+def cpu_baseline_sample(b, f, run_seeds, n_env=12, warm=2, steps=10):
     """Oracle port (the reference's algorithm in numpy), 1 core, bounded sample:
-    ``n_env`` cfg2 envs (GPU-sampled scenes, bit-identical to the oracle's) stepped
-    ``steps`` ticks, plus one oracle scene generation."""
+    ``n_env`` envs of this config (GPU-sampled scenes, bit-identical to the
+    oracle's), ``warm`` untimed ticks from spawn (every agent plans at tick 0),
+    then ``steps`` timed ticks -- about 10-20 s of CPU work at cfg2."""
     from oracle import crowd as C
-    from oracle import scene as S
     grids = [(b.labels[i].cpu().numpy(), CFG["res"]) for i in range(n_env)]
     agents = []
     for i in range(n_env):
@@ -343,12 +360,16 @@ def cpu_baseline_sample(b, f, run_seeds, n_env=4, steps=6):
                            max_speed=np.array([C.MAX_SPEED[x] for x in k]), kind=k))
     ref = C.CrowdFieldOracle(grids, C.Config(neighbor_distance=CFG["nd"]), [int(s) for s in run_seeds[:n_env]])
     ref.set_agents(agents)
+    for _ in range(warm):
+        ref.step()
     t0 = time.perf_counter()
     for _ in range(steps):
         ref.step()
     dt = time.perf_counter() - t0
     return {"value": round(n_env * steps / dt, 3), "unit": "env-steps/s", "cores": 1,
-            "kind": "port", "sample": f"{n_env} envs of this config x {steps} crowd ticks, oracle port, 1 thread"}
+            "kind": "port", "seconds": round(dt, 2),
+            "sample": f"{n_env} envs of this config, {warm} untimed + {steps} timed crowd ticks from spawn, "
+                      f"oracle port (numpy restatement of the reference), 1 thread"}
 
 
 # ============================================================================ reference arm
