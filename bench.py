@@ -345,7 +345,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def cpu_baseline_sample(b, f, run_seeds, n_env=12, warm=2, steps=10):
+def cpu_baseline_sample(b, f, run_seeds, n_env=12, warm=2, steps=40):
     """Oracle port (the reference's algorithm in numpy), 1 core, bounded sample:
     ``n_env`` envs of this config (GPU-sampled scenes, bit-identical to the
     oracle's), ``warm`` untimed ticks from spawn (every agent plans at tick 0),

@@ -121,7 +121,8 @@ typedef struct cw_crowd_params {
   double dt, safety_margin, goal_reach2, stall_c, stall_s;
   int32_t resample_goals, use_static, path_cap;
   int32_t heap_cap;     /* A* far-pool entries (16 B) per search warp */
-  int32_t astar_ctas;   /* persistent k_astar CTAs (one per SM, cw_astar_warps() warps each) */
+  int32_t astar_ctas;   /* persistent k_astar CTAs (one per SM) */
+  int32_t astar_warps;  /* search warps per CTA: 1 = latency shape, else cw_astar_warps() */
 } cw_crowd_params;
 
 /* Device-resident CrowdField state (field.py:47-58) + guidance/A* scratch. */

@@ -90,12 +90,13 @@ class CrowdField:
     OccupancyGrid (host labels, uploaded once) or a device ``SceneBatch``."""
 
     def __init__(self, occupancies, config, env_seeds, resample_goals=True, device="cuda",
-                 threads=128, path_cap=None, heap_cap=None):
+                 threads=128, path_cap=None, heap_cap=None, astar_warps=None):
         import torch
         self.config = config
         self.resample_goals = resample_goals
         self.device = torch.device(device)
         self.threads = threads
+        self.astar_warps = astar_warps
         if isinstance(occupancies, SceneBatch):
             b = occupancies
             self.E = b.E
@@ -294,6 +295,9 @@ class CrowdField:
         p.resample_goals = int(bool(self.resample_goals))
         p.use_static = int(bool(self.has_obs_t.any().item()))
         p.path_cap, p.heap_cap, p.astar_ctas = self.path_cap, self.heap_cap, self.astar_ctas
+        # few replans per tick (small batches): one search warp per SM, whose tick
+        # latency is the longest search; large batches: four per SM for throughput
+        p.astar_warps = self.astar_warps or (1 if self.E * self.A < 131072 else 4)
         return p
 
     def _state(self):

@@ -350,8 +350,10 @@ CW_HD size_t astar_slot_bytes(int nx, int ny, int S) {
 // sub-partition).  Each warp owns a near pool (NC x 16 B), a 64-entry staging
 // area and a tile map (2 B per tile); the NS tile slots of 576 B (64 x f64 g +
 // 64 move bytes) form one pool shared by the CTA's warps (a locked stack of
-// free slot ids), so a lone long search can use nearly all of it.
-constexpr int kAstarWarps = 4;
+// free slot ids), so a lone long search can use nearly all of it.  W = 1 is
+// the latency shape (few searches per tick: the tick waits on the longest
+// one), W = 4 the throughput shape (many searches per tick).
+constexpr int kAstarWarps = 4;   // scratch is sized for the larger shape
 
 struct AstarShape {
   int NC, NS, W;
@@ -359,9 +361,9 @@ struct AstarShape {
   size_t smem;
 };
 
-CW_HD AstarShape astar_shape(int nx, int ny) {
+CW_HD AstarShape astar_shape(int nx, int ny, int W) {
   const int nt = ((nx + 7) / 8) * ((ny + 7) / 8);
-  const int W = kAstarWarps, NC = 512;
+  const int NC = W == 1 ? 1024 : 512;
   const size_t per_warp = (size_t)(NC + 64) * 16 + (((size_t)nt * 2 + 15) & ~(size_t)15);
   const size_t budget = 220 * 1024, head = 16;   // lock + stack top
   const size_t fixed = W * per_warp + head;
@@ -370,6 +372,12 @@ CW_HD AstarShape astar_shape(int nx, int ny) {
   NS = NS > 65535 ? 65535 : NS;
   const size_t stack = ((size_t)NS * 2 + 15) & ~(size_t)15;
   return {NC, NS, W, per_warp, fixed + stack + (size_t)NS * 576};
+}
+
+// Per-warp global scratch stride: sized for the larger pool of the two shapes.
+CW_HD size_t astar_slot_stride(int nx, int ny) {
+  const int a = astar_shape(nx, ny, 1).NS, b = astar_shape(nx, ny, kAstarWarps).NS;
+  return astar_slot_bytes(nx, ny, a > b ? a : b);
 }
 
 // Per-CTA layout shared by the two search instantiations.
@@ -603,8 +611,8 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
 // paths.astar_path exactly; results go to the agent's path (field.py:204-212).
 // Unreachable goals (different 4-connected component, see k_reach) return None
 // without searching -- the reference exhausts the component and returns None.
-__global__ void __launch_bounds__(32 * kAstarWarps, 1) k_astar(cw_crowd_params P, cw_crowd_state S, int NC,
-                                                            int NS) {
+template <int W>
+__global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd_state S, int NC, int NS) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gw = blockIdx.x * kAstarWarps + w;       // global search-warp id (scratch slot)
@@ -617,7 +625,7 @@ __global__ void __launch_bounds__(32 * kAstarWarps, 1) k_astar(cw_crowd_params P
   E.NS = NS;
   const int nx = E.nx, N = E.N, NT = E.NT;
   const AstarReq* reqs = reinterpret_cast<const AstarReq*>(S.astar_req);
-  const AstarShape shp = astar_shape(P.nx, P.ny);
+  const AstarShape shp = astar_shape(P.nx, P.ny, W);
   unsigned char* const wblk = sm + (size_t)w * shp.per_warp;
   Pools pl;
   pl.near = reinterpret_cast<OpenEnt*>(wblk);
@@ -626,14 +634,14 @@ __global__ void __launch_bounds__(32 * kAstarWarps, 1) k_astar(cw_crowd_params P
   pl.NC = NC;
   pl.far_cap = P.heap_cap;
   E.tmap = reinterpret_cast<uint16_t*>(pl.stg + 64);
-  unsigned char* const pool = sm + (size_t)kAstarWarps * shp.per_warp;
+  unsigned char* const pool = sm + (size_t)W * shp.per_warp;
   E.pool_lock = reinterpret_cast<int*>(pool);
   E.free_ids = reinterpret_cast<uint16_t*>(pool + 16);
   E.gts = reinterpret_cast<double*>(pool + 16 + (((size_t)NS * 2 + 15) & ~(size_t)15));
   E.mts = reinterpret_cast<uint8_t*>(E.gts + (size_t)NS * 64);
   E.wbuf = reinterpret_cast<uint16_t*>(pl.stg) + 0;   // staging area doubles as the slot buffer
   unsigned char* const gbase = reinterpret_cast<unsigned char*>(S.astar_rec) +
-                               (size_t)gw * astar_slot_bytes(nx, E.ny, NS);
+                               (size_t)gw * astar_slot_stride(nx, E.ny);
   E.gtg = reinterpret_cast<double*>(gbase);
   E.mtg = gbase + (size_t)NT * 64 * 8;
   E.parent = reinterpret_cast<int32_t*>(E.mtg + (size_t)NT * 64);

@@ -679,8 +679,10 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
     cudaFuncSetAttribute(k_orca<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (phases & 1) k_guide<NT><<<P.E, NT, 0, st>>>(P, S, em);
   if (phases & 2) {
-    const AstarShape A = astar_shape(P.nx, P.ny);
-    k_astar<<<P.astar_ctas, 32 * kAstarWarps, A.smem, st>>>(P, S, A.NC, A.NS);
+    const int W = P.astar_warps == 1 ? 1 : kAstarWarps;
+    const AstarShape A = astar_shape(P.nx, P.ny, W);
+    if (W == 1) k_astar<1><<<P.astar_ctas, 32, A.smem, st>>>(P, S, A.NC, A.NS);
+    else k_astar<kAstarWarps><<<P.astar_ctas, 32 * kAstarWarps, A.smem, st>>>(P, S, A.NC, A.NS);
   }
   if (phases & 4) k_orca<NT><<<P.E, NT, sm, st>>>(P, S, rp, rv, rr, em, bins);
   return (int)cudaGetLastError();
@@ -700,8 +702,7 @@ int cw_astar_warps(void) { return cw::kAstarWarps; }
 
 // Bytes of A* scratch (astar_rec) per k_astar search warp for an nx x ny grid.
 size_t cw_astar_slot_bytes(int nx, int ny) {
-  const cw::AstarShape A = cw::astar_shape(nx, ny);
-  return cw::astar_slot_bytes(nx, ny, A.NS);
+  return cw::astar_slot_stride(nx, ny);
 }
 
 // One two-phase tick of every env (field.py:90-163): k_guide -> k_astar -> k_orca,
@@ -712,8 +713,12 @@ int cw_crowd_step_phases(const cw_crowd_params* P, const cw_crowd_state* S,
   using namespace cw;
   if (P->E <= 0 || P->A <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
-  const AstarShape A = astar_shape(P->nx, P->ny);
-  cudaFuncSetAttribute(k_astar, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)A.smem);
+  static int attr_set = 0;   // opt-in shared memory (<= 227 KB) for both k_astar shapes
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_astar<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_astar<kAstarWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set = 1;
+  }
   if (threads == 256)
     return launch_step<256>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, phases, st);
   if (threads == 64)
