@@ -332,7 +332,7 @@ def run_ours(args):
                               "model": "SURVEY 8d: 74 B/agent-step + 8 B/path point + 20 B/env-step"},
             "kernels_ms": {n: round(float(v), 4) for n, v in zip(names, ph_avg)},
             "kernels_share": {n: round(float(v / ph_avg.sum()), 4) for n, v in zip(names, ph_avg)},
-            "gpu_launches": 3 * steps,
+            "gpu_launches": 4 * steps,   # k_guide, k_astar, k_orca (two passes) per tick
             "clocks": clk.summary(),
             "counters": counters,
             "stats": {"min_gap": float(torch.nan_to_num(stats[:, 0], posinf=1e9).min()),

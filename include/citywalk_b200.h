@@ -141,6 +141,7 @@ typedef struct cw_crowd_state {
   void* astar_heap;     /* (astar_ctas * cw_astar_warps(), heap_cap, 16 B) A* far pools */
   void* astar_req;      /* (E*A, 16 B) replanning queue {env, agent, start, goal} */
   int64_t* counters;
+  uint8_t* env_req;     /* (E) scratch: env queued a replan this tick (k_guide -> k_orca) */
 } cw_crowd_state;
 
 size_t cw_crowd_step_smem_bytes(int A, int threads);
@@ -151,7 +152,9 @@ int cw_crowd_step(const cw_crowd_params* params, const cw_crowd_state* state,
 
 /* The same tick as cw_crowd_step, one phase at a time (bit 0 k_guide, bit 1
  * k_astar, bit 2 k_orca); running 1, 2, 4 in order equals one cw_crowd_step.
- * Lets a caller time each kernel with events on its stream. */
+ * Lets a caller time each kernel with events on its stream.  phases == 7 (what
+ * cw_crowd_step runs) overlaps the k_orca of envs without replans with k_astar on
+ * two internal streams that are joined back into `stream` before returning. */
 int cw_crowd_step_phases(const cw_crowd_params* params, const cw_crowd_state* state,
                          const double* robot_pos, const double* robot_vel, double robot_radius,
                          const uint8_t* env_mask, int threads, int phases, void* stream);

@@ -64,7 +64,7 @@ CROWD_STATE_FIELDS = [
     "pos", "vel", "goal", "waypoint", "radius", "pref_speed", "max_speed", "active", "path_cells",
     "path_head", "path_n", "labels", "nearest", "has_obs", "walk", "walk_n", "reach", "moves",
     "rng", "last_gap", "gap_tmp", "flags", "astar_rec", "astar_heap", "astar_req",
-    "counters",
+    "counters", "env_req",
 ]
 
 

@@ -137,6 +137,7 @@ class CrowdField:
         self.gap_tmp_t = torch.zeros((self.E,), dtype=torch.float64, device=self.device)
         self.flags_t = torch.zeros((8,), dtype=torch.int32, device=self.device)
         self.counters_t = torch.zeros((16,), dtype=torch.int64, device=self.device)
+        self.env_req_t = torch.zeros((self.E,), dtype=torch.uint8, device=self.device)
         self._astar_ready = False
         self._alloc(0)
 
@@ -311,7 +312,7 @@ class CrowdField:
                  moves=self.moves_t, rng=self.rng_t,
                  last_gap=self.last_gap_t, gap_tmp=self.gap_tmp_t, flags=self.flags_t,
                  astar_rec=self.astar_rec_t, astar_req=self.astar_req_t,
-                 astar_heap=self.astar_heap_t, counters=self.counters_t)
+                 astar_heap=self.astar_heap_t, counters=self.counters_t, env_req=self.env_req_t)
         for k, v in m.items():
             setattr(s, k, v.data_ptr())
         return s

@@ -365,7 +365,8 @@ CW_HD AstarShape astar_shape(int nx, int ny, int W) {
   const int nt = ((nx + 7) / 8) * ((ny + 7) / 8);
   const int NC = W == 1 ? 1024 : 512;
   const size_t per_warp = (size_t)(NC + 64) * 16 + (((size_t)nt * 2 + 15) & ~(size_t)15);
-  const size_t budget = 220 * 1024, head = 16;   // lock + stack top
+  // W = 1 leaves ~30 KB of the SM's 228 KB for k_orca CTAs running beside it
+  const size_t budget = (W == 1 ? 196 : 220) * 1024, head = 16;   // lock + stack top
   const size_t fixed = W * per_warp + head;
   int NS = budget > fixed ? (int)((budget - fixed) / (576 + 2)) : 0;
   NS = NS > W * nt ? W * nt : NS;

@@ -244,7 +244,13 @@ __global__ void __launch_bounds__(NT) k_guide(cw_crowd_params P, cw_crowd_state 
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int A = P.A;
   const size_t eA = (size_t)e * A;
-  if (env_mask && !env_mask[e]) return;
+  __shared__ int s_req;   // some agent of this env queued a replan
+  if (env_mask && !env_mask[e]) {
+    if (threadIdx.x == 0) S.env_req[e] = 0;
+    return;
+  }
+  if (threadIdx.x == 0) s_req = 0;
+  __syncthreads();
   const bool has_obs = S.has_obs[e] != 0;
   const int nx = P.nx, ny = P.ny;
   const size_t N = (size_t)nx * ny;
@@ -329,10 +335,13 @@ __global__ void __launch_bounds__(NT) k_guide(cw_crowd_params P, cw_crowd_state 
       int q = atomicAdd(&S.flags[4], 1);
       AstarReq R = {e, a, sr * nx + sc, gr * nx + gc};
       reqs[q] = R;
+      s_req = 1;
     }
   }
   if (lane == 0 && scanned && S.counters)
     atomicAdd((unsigned long long*)&S.counters[1], (unsigned long long)scanned);
+  __syncthreads();
+  if (threadIdx.x == 0) S.env_req[e] = (uint8_t)s_req;
 }
 
 // ---------------------------------------------------------------- ORCA + commit
@@ -361,7 +370,8 @@ __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S
                                              const double* __restrict__ robot_pos,
                                              const double* __restrict__ robot_vel,
                                              double robot_radius,
-                                             const uint8_t* __restrict__ env_mask, Bins bins) {
+                                             const uint8_t* __restrict__ env_mask, Bins bins,
+                                             int pass) {
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char sm[];
   const int e = blockIdx.x;
@@ -382,267 +392,272 @@ __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S
   int* s_cell = s_sorted + A;
   __shared__ double s_gap[NW];
   __shared__ int s_anynb[NW];
+  // pass 0: every env; pass 1: envs without A* requests (runs beside k_astar);
+  // pass 2: envs with requests (after k_astar).  The body is per env.
+  const bool skip = (pass == 1 && S.env_req[e]) || (pass == 2 && !S.env_req[e]);
+  if (!skip) {
   const long long t_cta0 = clock64();
-  const size_t eA = (size_t)e * A;
-  const bool emask = env_mask ? env_mask[e] != 0 : true;
-  for (int a = threadIdx.x; a < A; a += NT) {
-    s_px[a] = S.pos[(eA + a) * 2];
-    s_py[a] = S.pos[(eA + a) * 2 + 1];
-    s_vx[a] = S.vel[(eA + a) * 2];
-    s_vy[a] = S.vel[(eA + a) * 2 + 1];
-    s_r[a] = S.radius[eA + a];
-    s_nx[a] = s_px[a];
-    s_ny[a] = s_py[a];
-    s_act[a] = (S.active[eA + a] && emask) ? 1 : 0;
-  }
-  __syncthreads();
-  if (bins.ncx > 0) {
-    // counting sort of the active agents into square cells of side >= nd + 0.5 m:
-    // every j with fp32 key(i, j) < nd^2 (key error < 0.03 m^2 on <= 128 m grids)
-    // lies in the 3 x 3 cells around i; selection below still uses (key, index)
-    const int nc = bins.ncx * bins.ncy;
-    for (int c = threadIdx.x; c <= nc; c += NT) s_cend[c] = 0;
-    __syncthreads();
+    const size_t eA = (size_t)e * A;
+    const bool emask = env_mask ? env_mask[e] != 0 : true;
     for (int a = threadIdx.x; a < A; a += NT) {
-      int cell = -1;
-      if (s_act[a]) {
-        const int cx = min(max((int)(s_px[a] * bins.inv_cs), 0), bins.ncx - 1);
-        const int cy = min(max((int)(s_py[a] * bins.inv_cs), 0), bins.ncy - 1);
-        cell = cy * bins.ncx + cx;
-        atomicAdd(&s_cend[cell + 1], 1);
-      }
-      s_cell[a] = cell;
+      s_px[a] = S.pos[(eA + a) * 2];
+      s_py[a] = S.pos[(eA + a) * 2 + 1];
+      s_vx[a] = S.vel[(eA + a) * 2];
+      s_vy[a] = S.vel[(eA + a) * 2 + 1];
+      s_r[a] = S.radius[eA + a];
+      s_nx[a] = s_px[a];
+      s_ny[a] = s_py[a];
+      s_act[a] = (S.active[eA + a] && emask) ? 1 : 0;
     }
     __syncthreads();
-    if (threadIdx.x < 32) {   // exclusive scan of the counts (one warp)
-      int carry = 0;
-      for (int c0 = 0; c0 <= nc; c0 += 32) {
-        const int c = c0 + lane;
-        int v = c <= nc ? s_cend[c] : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int t = __shfl_up_sync(0xffffffffu, v, o);
-          if (lane >= o) v += t;
-        }
-        if (c <= nc) s_cend[c] = v + carry;
-        carry += __shfl_sync(0xffffffffu, v, 31);
-      }
-    }
-    __syncthreads();
-    for (int a = threadIdx.x; a < A; a += NT)   // afterwards s_cend[c] = end of cell c
-      if (s_cell[a] >= 0) s_sorted[atomicAdd(&s_cend[s_cell[a]], 1)] = a;
-    __syncthreads();
-  }
-  const int nx = P.nx, ny = P.ny;
-  const size_t N = (size_t)nx * ny;
-  const uint8_t* lab = S.labels + e * N;
-  const bool has_obs = S.has_obs[e] != 0;
-  const double res = P.res;
-  const bool use_robot = robot_pos != nullptr;
-  double rpx = 0, rpy = 0, rvx = 0, rvy = 0;
-  if (use_robot) {
-    rpx = robot_pos[e * 2]; rpy = robot_pos[e * 2 + 1];
-    if (robot_vel) { rvx = robot_vel[e * 2]; rvy = robot_vel[e * 2 + 1]; }
-  }
-  WarpCons& C = s_cons[wid];
-  double my_gap = CUDART_INF;
-  int my_anynb = 0;
-  long long fallbacks = 0, stalls = 0;
-  for (int a = wid; a < A; a += NW) {
-    if (!s_act[a]) continue;
-    const double px = s_px[a], py = s_py[a];
-    const size_t ia = eA + a;
-    const double gx = S.goal[ia * 2], gy = S.goal[ia * 2 + 1];
-    const double wx = S.waypoint[ia * 2], wy = S.waypoint[ia * 2 + 1];
-    // ---------------- preferred velocity (field.py:214-227)
-    const double sp = S.pref_speed[ia];
-    double tw0 = wx - px, tw1 = wy - py;
-    double dist = sqrt(tw0 * tw0 + tw1 * tw1);
-    double safe = fmax(dist, kEps);
-    double pf0 = tw0 / safe * sp, pf1 = tw1 / safe * sp;
-    double tg0 = gx - px, tg1 = gy - py;
-    double dg = sqrt(tg0 * tg0 + tg1 * tg1);
-    double scl = fmin(1.0, dg / fmax(sp * P.dt * 4, kEps));
-    pf0 = pf0 * scl;
-    pf1 = pf1 * scl;
-    // ---------------- neighbours: fp32 Gram key, stable top-K (field.py:246-262)
-    const float xi = (float)px, yi = (float)py;
-    const float sqi = __fadd_rn(__fmul_rn(xi, xi), __fmul_rn(yi, yi));
-    const double vxa = s_vx[a], vya = s_vy[a], ra = s_r[a];
-    float last_k = -CUDART_INF_F;
-    int last_j = -1;
-    int nb = 0;
-    int my_nb = -1;
-    const int kmax = min(P.max_neighbors, max(A - 1, 0));
-    // candidate ranges: all agents, or the three cell-row runs around a's cell
-    int rs[3] = {0, 0, 0}, re[3] = {A, 0, 0};
     if (bins.ncx > 0) {
-      const int cx = s_cell[a] % bins.ncx, cy = s_cell[a] / bins.ncx;
-      const int x0 = max(cx - 1, 0), x1 = min(cx + 1, bins.ncx - 1);
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const int row = cy - 1 + d;
-        const bool ok = row >= 0 && row < bins.ncy;
-        const int c0 = row * bins.ncx + x0, c1 = row * bins.ncx + x1;
-        rs[d] = ok ? (c0 > 0 ? s_cend[c0 - 1] : 0) : 0;
-        re[d] = ok ? s_cend[c1] : 0;
+      // counting sort of the active agents into square cells of side >= nd + 0.5 m:
+      // every j with fp32 key(i, j) < nd^2 (key error < 0.03 m^2 on <= 128 m grids)
+      // lies in the 3 x 3 cells around i; selection below still uses (key, index)
+      const int nc = bins.ncx * bins.ncy;
+      for (int c = threadIdx.x; c <= nc; c += NT) s_cend[c] = 0;
+      __syncthreads();
+      for (int a = threadIdx.x; a < A; a += NT) {
+        int cell = -1;
+        if (s_act[a]) {
+          const int cx = min(max((int)(s_px[a] * bins.inv_cs), 0), bins.ncx - 1);
+          const int cy = min(max((int)(s_py[a] * bins.inv_cs), 0), bins.ncy - 1);
+          cell = cy * bins.ncx + cx;
+          atomicAdd(&s_cend[cell + 1], 1);
+        }
+        s_cell[a] = cell;
       }
-    }
-    for (int round = 0; round < kmax; ++round) {
-      float bk = CUDART_INF_F;
-      int bj = 0x7fffffff;
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        for (int t = rs[d] + lane; t < re[d]; t += 32) {
-          const int j = bins.ncx > 0 ? s_sorted[t] : t;
-          if (j == a || !s_act[j]) continue;
-          float xj = (float)s_px[j], yj = (float)s_py[j];
-          float sqj = __fadd_rn(__fmul_rn(xj, xj), __fmul_rn(yj, yj));
-          float dot = __fmaf_rn(yi, yj, __fmul_rn(xi, xj));
-          float key = __fsub_rn(__fadd_rn(sqi, sqj), __fmul_rn(2.0f, dot));
-          if (!(key < P.nd2_f32)) continue;
-          bool after = key > last_k || (key == last_k && j > last_j);
-          bool better = key < bk || (key == bk && j < bj);
-          if (after && better) { bk = key; bj = j; }
+      __syncthreads();
+      if (threadIdx.x < 32) {   // exclusive scan of the counts (one warp)
+        int carry = 0;
+        for (int c0 = 0; c0 <= nc; c0 += 32) {
+          const int c = c0 + lane;
+          int v = c <= nc ? s_cend[c] : 0;
+  #pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += t;
+          }
+          if (c <= nc) s_cend[c] = v + carry;
+          carry += __shfl_sync(0xffffffffu, v, 31);
         }
       }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        float ok_ = __shfl_xor_sync(0xffffffffu, bk, o);
-        int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-        if (ok_ < bk || (ok_ == bk && oj < bj)) { bk = ok_; bj = oj; }
-      }
-      if (bj == 0x7fffffff) break;
-      if (lane == round) my_nb = bj;
-      last_k = bk;
-      last_j = bj;
-      ++nb;
+      __syncthreads();
+      for (int a = threadIdx.x; a < A; a += NT)   // afterwards s_cend[c] = end of cell c
+        if (s_cell[a] >= 0) s_sorted[atomicAdd(&s_cend[s_cell[a]], 1)] = a;
+      __syncthreads();
     }
-    // ---------------- constraints (compact list of valid lanes)
-    if (lane < nb) {
-      const int j = my_nb;
-      double rp0 = s_px[j] - px, rp1 = s_py[j] - py;
-      double rv0 = vxa - s_vx[j], rv1 = vya - s_vy[j];
-      double rr = ra + s_r[j] + P.safety_margin;
-      vo_halfplane(rp0, rp1, rv0, rv1, rr, P.time_horizon, P.dt, vxa, vya, 0.5, C.px[lane],
-                   C.py[lane], C.nx[lane], C.ny[lane]);
-      if (lane == 0) {
-        double d_near = sqrt(rp0 * rp0 + rp1 * rp1);   // field.py:268-271
-        my_gap = fmin(my_gap, d_near - (ra + s_r[j]));
-        my_anynb = 1;
-      }
-    }
-    int nc = nb;
+    const int nx = P.nx, ny = P.ny;
+    const size_t N = (size_t)nx * ny;
+    const uint8_t* lab = S.labels + e * N;
+    const bool has_obs = S.has_obs[e] != 0;
+    const double res = P.res;
+    const bool use_robot = robot_pos != nullptr;
+    double rpx = 0, rpy = 0, rvx = 0, rvy = 0;
     if (use_robot) {
-      double rp0 = rpx - px, rp1 = rpy - py;
-      double d2 = rp0 * rp0 + rp1 * rp1;
-      if (d2 < P.nd2) {
-        if (lane == nc) {
-          double rr = ra + robot_radius + P.safety_margin;
-          vo_halfplane(rp0, rp1, vxa - rvx, vya - rvy, rr, P.obstacle_time_horizon, P.dt, vxa, vya,
-                       1.0, C.px[lane], C.py[lane], C.nx[lane], C.ny[lane]);
-        }
-        ++nc;
-      }
+      rpx = robot_pos[e * 2]; rpy = robot_pos[e * 2 + 1];
+      if (robot_vel) { rvx = robot_vel[e * 2]; rvy = robot_vel[e * 2 + 1]; }
     }
-    if (P.use_static && has_obs) {
-      long long ri = clampll(trunc_ll(py / res), 0, ny - 1);
-      long long ci = clampll(trunc_ll(px / res), 0, nx - 1);
-      int flat = S.nearest[e * N + ri * nx + ci];
-      if (flat >= 0) {
-        int orow = flat / nx, ocol = flat - orow * nx;
-        double rp0 = ((double)ocol + 0.5) * res - px, rp1 = ((double)orow + 0.5) * res - py;
+    WarpCons& C = s_cons[wid];
+    double my_gap = CUDART_INF;
+    int my_anynb = 0;
+    long long fallbacks = 0, stalls = 0;
+    for (int a = wid; a < A; a += NW) {
+      if (!s_act[a]) continue;
+      const double px = s_px[a], py = s_py[a];
+      const size_t ia = eA + a;
+      const double gx = S.goal[ia * 2], gy = S.goal[ia * 2 + 1];
+      const double wx = S.waypoint[ia * 2], wy = S.waypoint[ia * 2 + 1];
+      // ---------------- preferred velocity (field.py:214-227)
+      const double sp = S.pref_speed[ia];
+      double tw0 = wx - px, tw1 = wy - py;
+      double dist = sqrt(tw0 * tw0 + tw1 * tw1);
+      double safe = fmax(dist, kEps);
+      double pf0 = tw0 / safe * sp, pf1 = tw1 / safe * sp;
+      double tg0 = gx - px, tg1 = gy - py;
+      double dg = sqrt(tg0 * tg0 + tg1 * tg1);
+      double scl = fmin(1.0, dg / fmax(sp * P.dt * 4, kEps));
+      pf0 = pf0 * scl;
+      pf1 = pf1 * scl;
+      // ---------------- neighbours: fp32 Gram key, stable top-K (field.py:246-262)
+      const float xi = (float)px, yi = (float)py;
+      const float sqi = __fadd_rn(__fmul_rn(xi, xi), __fmul_rn(yi, yi));
+      const double vxa = s_vx[a], vya = s_vy[a], ra = s_r[a];
+      float last_k = -CUDART_INF_F;
+      int last_j = -1;
+      int nb = 0;
+      int my_nb = -1;
+      const int kmax = min(P.max_neighbors, max(A - 1, 0));
+      // candidate ranges: all agents, or the three cell-row runs around a's cell
+      int rs[3] = {0, 0, 0}, re[3] = {A, 0, 0};
+      if (bins.ncx > 0) {
+        const int cx = s_cell[a] % bins.ncx, cy = s_cell[a] / bins.ncx;
+        const int x0 = max(cx - 1, 0), x1 = min(cx + 1, bins.ncx - 1);
+  #pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const int row = cy - 1 + d;
+          const bool ok = row >= 0 && row < bins.ncy;
+          const int c0 = row * bins.ncx + x0, c1 = row * bins.ncx + x1;
+          rs[d] = ok ? (c0 > 0 ? s_cend[c0 - 1] : 0) : 0;
+          re[d] = ok ? s_cend[c1] : 0;
+        }
+      }
+      for (int round = 0; round < kmax; ++round) {
+        float bk = CUDART_INF_F;
+        int bj = 0x7fffffff;
+  #pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          for (int t = rs[d] + lane; t < re[d]; t += 32) {
+            const int j = bins.ncx > 0 ? s_sorted[t] : t;
+            if (j == a || !s_act[j]) continue;
+            float xj = (float)s_px[j], yj = (float)s_py[j];
+            float sqj = __fadd_rn(__fmul_rn(xj, xj), __fmul_rn(yj, yj));
+            float dot = __fmaf_rn(yi, yj, __fmul_rn(xi, xj));
+            float key = __fsub_rn(__fadd_rn(sqi, sqj), __fmul_rn(2.0f, dot));
+            if (!(key < P.nd2_f32)) continue;
+            bool after = key > last_k || (key == last_k && j > last_j);
+            bool better = key < bk || (key == bk && j < bj);
+            if (after && better) { bk = key; bj = j; }
+          }
+        }
+  #pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          float ok_ = __shfl_xor_sync(0xffffffffu, bk, o);
+          int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+          if (ok_ < bk || (ok_ == bk && oj < bj)) { bk = ok_; bj = oj; }
+        }
+        if (bj == 0x7fffffff) break;
+        if (lane == round) my_nb = bj;
+        last_k = bk;
+        last_j = bj;
+        ++nb;
+      }
+      // ---------------- constraints (compact list of valid lanes)
+      if (lane < nb) {
+        const int j = my_nb;
+        double rp0 = s_px[j] - px, rp1 = s_py[j] - py;
+        double rv0 = vxa - s_vx[j], rv1 = vya - s_vy[j];
+        double rr = ra + s_r[j] + P.safety_margin;
+        vo_halfplane(rp0, rp1, rv0, rv1, rr, P.time_horizon, P.dt, vxa, vya, 0.5, C.px[lane],
+                     C.py[lane], C.nx[lane], C.ny[lane]);
+        if (lane == 0) {
+          double d_near = sqrt(rp0 * rp0 + rp1 * rp1);   // field.py:268-271
+          my_gap = fmin(my_gap, d_near - (ra + s_r[j]));
+          my_anynb = 1;
+        }
+      }
+      int nc = nb;
+      if (use_robot) {
+        double rp0 = rpx - px, rp1 = rpy - py;
         double d2 = rp0 * rp0 + rp1 * rp1;
         if (d2 < P.nd2) {
           if (lane == nc) {
-            double margin = 0.5 * kSqrt2 * P.res0;
-            double rr = ra + margin + P.safety_margin;
-            vo_halfplane(rp0, rp1, vxa, vya, rr, P.obstacle_time_horizon, P.dt, vxa, vya, 1.0,
-                         C.px[lane], C.py[lane], C.nx[lane], C.ny[lane]);
+            double rr = ra + robot_radius + P.safety_margin;
+            vo_halfplane(rp0, rp1, vxa - rvx, vya - rvy, rr, P.obstacle_time_horizon, P.dt, vxa, vya,
+                         1.0, C.px[lane], C.py[lane], C.nx[lane], C.ny[lane]);
           }
           ++nc;
         }
       }
+      if (P.use_static && has_obs) {
+        long long ri = clampll(trunc_ll(py / res), 0, ny - 1);
+        long long ci = clampll(trunc_ll(px / res), 0, nx - 1);
+        int flat = S.nearest[e * N + ri * nx + ci];
+        if (flat >= 0) {
+          int orow = flat / nx, ocol = flat - orow * nx;
+          double rp0 = ((double)ocol + 0.5) * res - px, rp1 = ((double)orow + 0.5) * res - py;
+          double d2 = rp0 * rp0 + rp1 * rp1;
+          if (d2 < P.nd2) {
+            if (lane == nc) {
+              double margin = 0.5 * kSqrt2 * P.res0;
+              double rr = ra + margin + P.safety_margin;
+              vo_halfplane(rp0, rp1, vxa, vya, rr, P.obstacle_time_horizon, P.dt, vxa, vya, 1.0,
+                           C.px[lane], C.py[lane], C.nx[lane], C.ny[lane]);
+            }
+            ++nc;
+          }
+        }
+      }
+      __syncwarp();
+      // ---------------- LP + stall retry (field.py:133-150)
+      const double ms = S.max_speed[ia];
+      double v0, v1;
+      fallbacks += warp_lp(C, nc, pf0, pf1, ms, v0, v1, lane);
+      double spd = sqrt(v0 * v0 + v1 * v1);
+      double want = sqrt(pf0 * pf0 + pf1 * pf1);
+      if (spd < 0.2 * want && want > 1e-6) {
+        ++stalls;
+        double q0 = P.stall_c * pf0 + P.stall_s * pf1;
+        double q1 = -P.stall_s * pf0 + P.stall_c * pf1;
+        fallbacks += warp_lp(C, nc, q0, q1, ms, v0, v1, lane);
+      }
+      // ---------------- commit (field.py:152-160, 352-366)
+      double npx = px + v0 * P.dt, npy = py + v1 * P.dt;
+      bool out = npx < 0 || npy < 0 || npx >= nx * res || npy >= ny * res;
+      long long rr = clampll(trunc_ll(npy / res), 0, ny - 1);
+      long long cc = clampll(trunc_ll(npx / res), 0, nx - 1);
+      bool blocked = out || lab[rr * nx + cc] == L_OBSTACLE;
+      if (lane == 0) {
+        if (!blocked) {
+          S.pos[ia * 2] = npx;
+          S.pos[ia * 2 + 1] = npy;
+          s_nx[a] = npx;
+          s_ny[a] = npy;
+        }
+        S.vel[ia * 2] = blocked ? 0.0 : v0;
+        S.vel[ia * 2 + 1] = blocked ? 0.0 : v1;
+      }
+      __syncwarp();
     }
-    __syncwarp();
-    // ---------------- LP + stall retry (field.py:133-150)
-    const double ms = S.max_speed[ia];
-    double v0, v1;
-    fallbacks += warp_lp(C, nc, pf0, pf1, ms, v0, v1, lane);
-    double spd = sqrt(v0 * v0 + v1 * v1);
-    double want = sqrt(pf0 * pf0 + pf1 * pf1);
-    if (spd < 0.2 * want && want > 1e-6) {
-      ++stalls;
-      double q0 = P.stall_c * pf0 + P.stall_s * pf1;
-      double q1 = -P.stall_s * pf0 + P.stall_c * pf1;
-      fallbacks += warp_lp(C, nc, q0, q1, ms, v0, v1, lane);
-    }
-    // ---------------- commit (field.py:152-160, 352-366)
-    double npx = px + v0 * P.dt, npy = py + v1 * P.dt;
-    bool out = npx < 0 || npy < 0 || npx >= nx * res || npy >= ny * res;
-    long long rr = clampll(trunc_ll(npy / res), 0, ny - 1);
-    long long cc = clampll(trunc_ll(npx / res), 0, nx - 1);
-    bool blocked = out || lab[rr * nx + cc] == L_OBSTACLE;
     if (lane == 0) {
-      if (!blocked) {
-        S.pos[ia * 2] = npx;
-        S.pos[ia * 2 + 1] = npy;
-        s_nx[a] = npx;
-        s_ny[a] = npy;
-      }
-      S.vel[ia * 2] = blocked ? 0.0 : v0;
-      S.vel[ia * 2 + 1] = blocked ? 0.0 : v1;
+      s_gap[wid] = my_gap;
+      s_anynb[wid] = my_anynb;
     }
-    __syncwarp();
-  }
-  if (lane == 0) {
-    s_gap[wid] = my_gap;
-    s_anynb[wid] = my_anynb;
-  }
-  __syncthreads();
-  // ---------------- goal resample, agent order (field.py:368-381)
-  if (threadIdx.x == 0) {
-    double g = CUDART_INF;
-    int anynb = 0;
-    for (int w = 0; w < NW; ++w) { g = fmin(g, s_gap[w]); anynb |= s_anynb[w]; }
-    S.gap_tmp[e] = g;
-    if (anynb) atomicOr(&S.flags[0], 1);
-    if (P.resample_goals) {
-      Pcg64Raw* raw = reinterpret_cast<Pcg64Raw*>(S.rng) + e;
-      bool loaded = false;
-      Pcg64 rng;
-      const int wn = S.walk_n[e];
-      for (int a = 0; a < A; ++a) {
-        if (!s_act[a]) continue;
-        const size_t ia = eA + a;
-        double dx = S.goal[ia * 2] - s_nx[a], dy = S.goal[ia * 2 + 1] - s_ny[a];
-        if (!(dx * dx + dy * dy < P.goal_reach2)) continue;
-        if (!loaded) { rng = pcg_load(*raw); loaded = true; }
-        int k = (int)integers32(rng, (uint64_t)wn);
-        int f = S.walk[e * N + k];
-        int r = f / nx, c = f - r * nx;
-        S.goal[ia * 2] = ((double)c + 0.5) * res;
-        S.goal[ia * 2 + 1] = ((double)r + 0.5) * res;
-        S.path_n[ia] = 0;
+    __syncthreads();
+    // ---------------- goal resample, agent order (field.py:368-381)
+    if (threadIdx.x == 0) {
+      double g = CUDART_INF;
+      int anynb = 0;
+      for (int w = 0; w < NW; ++w) { g = fmin(g, s_gap[w]); anynb |= s_anynb[w]; }
+      S.gap_tmp[e] = g;
+      if (anynb) atomicOr(&S.flags[0], 1);
+      if (P.resample_goals) {
+        Pcg64Raw* raw = reinterpret_cast<Pcg64Raw*>(S.rng) + e;
+        bool loaded = false;
+        Pcg64 rng;
+        const int wn = S.walk_n[e];
+        for (int a = 0; a < A; ++a) {
+          if (!s_act[a]) continue;
+          const size_t ia = eA + a;
+          double dx = S.goal[ia * 2] - s_nx[a], dy = S.goal[ia * 2 + 1] - s_ny[a];
+          if (!(dx * dx + dy * dy < P.goal_reach2)) continue;
+          if (!loaded) { rng = pcg_load(*raw); loaded = true; }
+          int k = (int)integers32(rng, (uint64_t)wn);
+          int f = S.walk[e * N + k];
+          int r = f / nx, c = f - r * nx;
+          S.goal[ia * 2] = ((double)c + 0.5) * res;
+          S.goal[ia * 2 + 1] = ((double)r + 0.5) * res;
+          S.path_n[ia] = 0;
+        }
+        if (loaded) pcg_store(*raw, rng);
       }
-      if (loaded) pcg_store(*raw, rng);
     }
-  }
-  if (lane == 0 && S.counters) {
-    if (fallbacks) atomicAdd((unsigned long long*)&S.counters[2], (unsigned long long)fallbacks);
-    if (stalls) atomicAdd((unsigned long long*)&S.counters[3], (unsigned long long)stalls);
-  }
-  if (threadIdx.x == 0 && S.counters) {
-    long long tc = clock64() - t_cta0;
-    atomicAdd((unsigned long long*)&S.counters[6], (unsigned long long)tc);
-    atomicMax((unsigned long long*)&S.counters[7], (unsigned long long)tc);
+    if (lane == 0 && S.counters) {
+      if (fallbacks) atomicAdd((unsigned long long*)&S.counters[2], (unsigned long long)fallbacks);
+      if (stalls) atomicAdd((unsigned long long*)&S.counters[3], (unsigned long long)stalls);
+    }
+    if (threadIdx.x == 0 && S.counters) {
+      long long tc = clock64() - t_cta0;
+      atomicAdd((unsigned long long*)&S.counters[6], (unsigned long long)tc);
+      atomicMax((unsigned long long*)&S.counters[7], (unsigned long long)tc);
+    }
   }
   // ---------------- last CTA: publish last_gap_by_env (only when some row had K > 0),
   // reset the per-step flags and the A* queue
   if (threadIdx.x == 0) {
     __threadfence();
     int ticket = atomicAdd(&S.flags[2], 1);
-    if (ticket == gridDim.x - 1) {
+    if (ticket == (pass == 0 ? 1 : 2) * (int)gridDim.x - 1) {   // last CTA over all passes
       __threadfence();
       if (atomicAdd(&S.flags[0], 0)) {
         for (int k = 0; k < P.E; ++k) S.last_gap[k] = ((volatile double*)S.gap_tmp)[k];
@@ -669,6 +684,35 @@ __global__ void k_child_seeds(int n, const uint64_t* __restrict__ parent, int la
   else out[i] = child_seed(parent[i], labels[label_id]);
 }
 
+// Internal streams for the overlapped tick: k_astar (+ the requesting envs' k_orca)
+// on a high-priority stream, the other envs' k_orca on a low-priority one, both
+// joined back into the caller's stream.  Created once per process.
+struct TickStreams {
+  cudaStream_t hi = nullptr, lo = nullptr;
+  cudaEvent_t guided, hi_done, lo_done;
+};
+
+static TickStreams& tick_streams() {
+  static TickStreams t;
+  if (!t.hi) {
+    int least, greatest;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    cudaStreamCreateWithPriority(&t.hi, cudaStreamNonBlocking, greatest);
+    cudaStreamCreateWithPriority(&t.lo, cudaStreamNonBlocking, least);
+    cudaEventCreateWithFlags(&t.guided, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&t.hi_done, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&t.lo_done, cudaEventDisableTiming);
+  }
+  return t;
+}
+
+static void launch_astar(const cw_crowd_params& P, const cw_crowd_state& S, cudaStream_t st) {
+  const int W = P.astar_warps == 1 ? 1 : kAstarWarps;
+  const AstarShape A = astar_shape(P.nx, P.ny, W);
+  if (W == 1) k_astar<1><<<P.astar_ctas, 32, A.smem, st>>>(P, S, A.NC, A.NS);
+  else k_astar<kAstarWarps><<<P.astar_ctas, 32 * kAstarWarps, A.smem, st>>>(P, S, A.NC, A.NS);
+}
+
 template <int NT>
 static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const double* rp,
                        const double* rv, double rr, const uint8_t* em, int phases,
@@ -677,14 +721,33 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
   size_t sm = cw_crowd_step_smem_bytes(P.A, NT) + bins_smem_bytes(bins, P.A);
   if ((phases & 4) && sm > 48 * 1024)
     cudaFuncSetAttribute(k_orca<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (phases & 1) k_guide<NT><<<P.E, NT, 0, st>>>(P, S, em);
-  if (phases & 2) {
-    const int W = P.astar_warps == 1 ? 1 : kAstarWarps;
-    const AstarShape A = astar_shape(P.nx, P.ny, W);
-    if (W == 1) k_astar<1><<<P.astar_ctas, 32, A.smem, st>>>(P, S, A.NC, A.NS);
-    else k_astar<kAstarWarps><<<P.astar_ctas, 32 * kAstarWarps, A.smem, st>>>(P, S, A.NC, A.NS);
+  if (phases == 7) {
+    // overlapped tick: envs without replans commit beside the A* searches.  An SM
+    // runs one L1 / shared-memory split at a time, so k_orca asks for the same
+    // max-shared carveout as k_astar to be co-resident with it.
+    static bool carve = false;
+    if (!carve) {
+      cudaFuncSetAttribute(k_orca<NT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           (int)cudaSharedmemCarveoutMaxShared);
+      carve = true;
+    }
+    TickStreams& T = tick_streams();
+    k_guide<NT><<<P.E, NT, 0, st>>>(P, S, em);
+    cudaEventRecord(T.guided, st);
+    cudaStreamWaitEvent(T.hi, T.guided, 0);
+    cudaStreamWaitEvent(T.lo, T.guided, 0);
+    launch_astar(P, S, T.hi);
+    k_orca<NT><<<P.E, NT, sm, T.lo>>>(P, S, rp, rv, rr, em, bins, 1);
+    k_orca<NT><<<P.E, NT, sm, T.hi>>>(P, S, rp, rv, rr, em, bins, 2);
+    cudaEventRecord(T.hi_done, T.hi);
+    cudaEventRecord(T.lo_done, T.lo);
+    cudaStreamWaitEvent(st, T.hi_done, 0);
+    cudaStreamWaitEvent(st, T.lo_done, 0);
+    return (int)cudaGetLastError();
   }
-  if (phases & 4) k_orca<NT><<<P.E, NT, sm, st>>>(P, S, rp, rv, rr, em, bins);
+  if (phases & 1) k_guide<NT><<<P.E, NT, 0, st>>>(P, S, em);
+  if (phases & 2) launch_astar(P, S, st);
+  if (phases & 4) k_orca<NT><<<P.E, NT, sm, st>>>(P, S, rp, rv, rr, em, bins, 0);
   return (int)cudaGetLastError();
 }
 
