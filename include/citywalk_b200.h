@@ -164,6 +164,65 @@ int cw_astar_warps(void);
 /* Bytes of astar_rec per k_astar search warp for an nx x ny grid (host-only query). */
 size_t cw_astar_slot_bytes(int nx, int ny);
 
+/* ---------------------------------------------------------------- robot */
+
+/* Robot embodiment (envcore/robot.py:31-80). */
+typedef struct cw_robot_model {
+  double body_radius, max_speed;
+  int32_t holonomic;   /* 1 holonomic velocity command, 0 Ackermann bicycle */
+  double wheelbase, max_steer;
+  double max_step_rise, max_grade, max_roughness;
+} cw_robot_model;
+
+/* EnvConfig + RewardConfig of a batch (envcore/batch.py:39-49, bench/reward.py:15-24). */
+typedef struct cw_robot_params {
+  int32_t E, A, nx, ny;
+  double res, dt, reach_threshold;
+  int32_t horizon;
+  double terminal_reach, terminal_oob, c1, c2, c3;
+  double track_far, track_near, track_near_weight;
+  cw_robot_model model;
+} cw_robot_params;
+
+/* Device robot state of E envs (batch.py:98-110) + per-tick outputs. */
+typedef struct cw_robot_state {
+  double* x; double* y; double* yaw; double* vx; double* vy; double* elev;
+  double* goal;                 /* (E, 2) */
+  int64_t* tick; uint8_t* terminated; uint8_t* truncated;
+  const uint8_t* labels;        /* (E, ny, nx) */
+  const float* grid_elev;       /* (E, ny, nx) */
+  const uint8_t* passable;      /* (E, ny, nx) from cw_traversability */
+  const double* crowd_pos;      /* (E, A, 2) after the crowd step; NULL when A == 0 */
+  const double* crowd_radius;   /* (E, A) */
+  const uint8_t* crowd_active;  /* (E, A) */
+  double* reward;               /* (E) */
+  uint8_t* events;              /* (E, 6): collision, collision_static, collision_dynamic,
+                                   on_walkable, reached, out_of_bounds */
+  double* distance; double* path_inc;
+  float* depth;                 /* (E, 128) ray-fan depth */
+  double* goal_vector;          /* (E, 2) ego frame */
+  double* proj_vel;             /* (E) */
+  float* height_map;            /* (E, 16, 10) */
+} cw_robot_state;
+
+/* traversability_maps (robot.py:127-179): passable[e] for rows slots[e] (NULL =
+ * identity) from labels / elevation; exact float64 emulation (column-then-row
+ * cumulative sums of the edge-padded grid in the reference's order). */
+size_t cw_traversability_scratch_bytes(int nx, int ny, int chunk);
+int cw_traversability(const cw_robot_params* params, int E, const int32_t* slots,
+                      const uint8_t* labels, const float* grid_elev, uint8_t* passable,
+                      void* scratch, int chunk, void* stream);
+
+/* Robot part of BatchedEnv.step_batch (batch.py:223-302) after the crowd step:
+ * actions (E, 2) clipped to [-1, 1], integrate_motion, traversability gating,
+ * crowd contact, elevation / walkable lookup, reward_batch, termination, then
+ * observe_batch (observe.py:39-129) into the state's observation outputs. */
+int cw_robot_step(const cw_robot_params* params, const cw_robot_state* state,
+                  const double* actions, void* stream);
+
+/* observe_batch only (reset / observe(i)). */
+int cw_robot_observe(const cw_robot_params* params, const cw_robot_state* state, void* stream);
+
 int cw_seed_streams(int n, const uint64_t* seeds, void* out_states, void* stream);
 
 int cw_child_seeds(int n, const uint64_t* parent, int label_id, const uint64_t* k,

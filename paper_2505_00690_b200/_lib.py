@@ -11,7 +11,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB_PATH = os.path.join(HERE, "libcitywalk_b200.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("sample.cu", "crowd.cu")]
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("sample.cu", "crowd.cu", "robot.cu")]
 HEADERS = sorted(os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))
                  if f.endswith(".cuh")) + [os.path.join(ROOT, "include", "citywalk_b200.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
@@ -72,9 +72,35 @@ class CrowdState(ctypes.Structure):
     _fields_ = [(n, P) for n in CROWD_STATE_FIELDS]
 
 
+class RobotModel(ctypes.Structure):
+    _fields_ = [("body_radius", c_f64), ("max_speed", c_f64), ("holonomic", c_i32),
+                ("wheelbase", c_f64), ("max_steer", c_f64), ("max_step_rise", c_f64),
+                ("max_grade", c_f64), ("max_roughness", c_f64)]
+
+
+class RobotParams(ctypes.Structure):
+    _fields_ = [("E", c_i32), ("A", c_i32), ("nx", c_i32), ("ny", c_i32), ("res", c_f64),
+                ("dt", c_f64), ("reach_threshold", c_f64), ("horizon", c_i32),
+                ("terminal_reach", c_f64), ("terminal_oob", c_f64), ("c1", c_f64), ("c2", c_f64),
+                ("c3", c_f64), ("track_far", c_f64), ("track_near", c_f64),
+                ("track_near_weight", c_f64), ("model", RobotModel)]
+
+
+ROBOT_STATE_FIELDS = [
+    "x", "y", "yaw", "vx", "vy", "elev", "goal", "tick", "terminated", "truncated", "labels",
+    "grid_elev", "passable", "crowd_pos", "crowd_radius", "crowd_active", "reward", "events",
+    "distance", "path_inc", "depth", "goal_vector", "proj_vel", "height_map",
+]
+
+
+class RobotState(ctypes.Structure):
+    _fields_ = [(n, P) for n in ROBOT_STATE_FIELDS]
+
+
 EXPORTS = ["cw_scene_seed_scratch_bytes", "cw_sample_scenes", "cw_spawn_agents", "cw_prepare_envs",
            "cw_crowd_step_smem_bytes",
-           "cw_crowd_step", "cw_crowd_step_phases", "cw_astar_slot_bytes", "cw_astar_warps", "cw_seed_streams", "cw_child_seeds", "cw_abi_sizes"]
+           "cw_crowd_step", "cw_crowd_step_phases", "cw_astar_slot_bytes", "cw_astar_warps",
+           "cw_traversability_scratch_bytes", "cw_traversability", "cw_robot_step", "cw_robot_observe", "cw_seed_streams", "cw_child_seeds", "cw_abi_sizes"]
 
 _lib = None
 
@@ -126,12 +152,21 @@ def lib():
     L.cw_seed_streams.argtypes = [ctypes.c_int, P, P, P]
     L.cw_child_seeds.restype = ctypes.c_int
     L.cw_child_seeds.argtypes = [ctypes.c_int, P, ctypes.c_int, P, P, P]
+    L.cw_traversability_scratch_bytes.restype = ctypes.c_size_t
+    L.cw_traversability_scratch_bytes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int]
+    L.cw_traversability.restype = ctypes.c_int
+    L.cw_traversability.argtypes = [ctypes.POINTER(RobotParams), ctypes.c_int, P, P, P, P, P,
+                                    ctypes.c_int, P]
+    L.cw_robot_step.restype = ctypes.c_int
+    L.cw_robot_step.argtypes = [ctypes.POINTER(RobotParams), ctypes.POINTER(RobotState), P, P]
+    L.cw_robot_observe.restype = ctypes.c_int
+    L.cw_robot_observe.argtypes = [ctypes.POINTER(RobotParams), ctypes.POINTER(RobotState), P]
     L.cw_abi_sizes.restype = ctypes.c_int
     L.cw_abi_sizes.argtypes = [ctypes.POINTER(ctypes.c_size_t), ctypes.c_int]
-    sizes = (ctypes.c_size_t * 4)()
-    L.cw_abi_sizes(sizes, 4)
+    sizes = (ctypes.c_size_t * 6)()
+    L.cw_abi_sizes(sizes, 6)
     mine = [ctypes.sizeof(SceneParams), ctypes.sizeof(SceneBuffers), ctypes.sizeof(CrowdParams),
-            ctypes.sizeof(CrowdState)]
+            ctypes.sizeof(CrowdState), ctypes.sizeof(RobotParams), ctypes.sizeof(RobotState)]
     if list(sizes) != mine:
         raise RuntimeError(f"ABI mismatch: library {list(sizes)} vs ctypes {mine}")
     _lib = L

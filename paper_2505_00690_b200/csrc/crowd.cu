@@ -814,10 +814,10 @@ int cw_child_seeds(int n, const uint64_t* parent, int label_id, const uint64_t* 
 
 // ABI self-check for the ctypes mirror (host-only; no device work).
 int cw_abi_sizes(size_t* out, int n) {
-  const size_t v[4] = {sizeof(cw_scene_params), sizeof(cw_scene_buffers), sizeof(cw_crowd_params),
-                       sizeof(cw_crowd_state)};
-  for (int i = 0; i < n && i < 4; ++i) out[i] = v[i];
-  return 4;
+  const size_t v[6] = {sizeof(cw_scene_params), sizeof(cw_scene_buffers), sizeof(cw_crowd_params),
+                       sizeof(cw_crowd_state), sizeof(cw_robot_params), sizeof(cw_robot_state)};
+  for (int i = 0; i < n && i < 6; ++i) out[i] = v[i];
+  return 6;
 }
 
 }  // extern "C"

@@ -30,5 +30,13 @@ def scene_names():
 
 
 @pytest.fixture(scope="session")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+@pytest.fixture(scope="session")
 def catalog():
     return golden_catalog()

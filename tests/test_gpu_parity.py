@@ -13,14 +13,6 @@ pytestmark = pytest.mark.gpu
 MIX = {"Flat": 0.25, "Slope": 0.25, "Stair": 0.25, "Rough": 0.25}
 
 
-@pytest.fixture(scope="module")
-def torch_cuda():
-    import torch
-    if not torch.cuda.is_available():
-        pytest.skip("no CUDA device")
-    return torch
-
-
 def _spec(d, peds=None):
     from paper_2505_00690_b200.urbangen import SceneSpec, Split, TaskKind
     return SceneSpec(seed=int(d["seed"]), extent_m=(d["extent"], d["extent"]),

@@ -1,0 +1,99 @@
+"""Device robot step / traversability / observations vs the reference goldens
+(tests/golden/robot_*.npz from oracle/make_golden_robot.py), through the C ABI.
+
+Tolerances: traversability maps, ticks, termination / truncation and events are
+exact.  Poses, rewards and the goal vector go through sin / cos / atan2 / tan /
+tanh, where CUDA's libdevice and the host libm / numpy SIMD kernels may differ
+in the last ulp: 1e-9 (m, rad, reward units).  Depth and the height patch are
+float32 cell lookups whose sample points move by those ulps: >= 99 % of values
+equal (a flip needs a sample within ~1e-6 m of a cell edge).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+RUNS = ["quadruped", "wheeled", "small"]
+TOL = 1e-9
+
+
+def _batch(g):
+    import torch
+    from paper_2505_00690_b200.robot import RobotBatch
+    K, T, peds, horizon, auto = (int(v) for v in g["meta"])
+    labels = torch.from_numpy(g["labels"]).cuda()
+    elev = torch.from_numpy(g["grid_elev"]).cuda()
+    return RobotBatch(labels, elev, float(g["res"]), str(g["robot"]), horizon=horizon)
+
+
+def _pre(g, t):
+    keys = ("x", "y", "yaw", "vx", "vy", "elev", "tick", "terminated", "truncated")
+    if t == 0:
+        return {k: g[f"init_{k}"] for k in keys}
+    return {k: g[k][t - 1] for k in keys}
+
+
+def _n_steps(g):
+    tick = g["tick"][:, 0]
+    drop = np.flatnonzero(np.diff(tick) < 0)
+    return int(drop[0]) + 1 if (int(g["meta"][4]) and drop.size) else tick.shape[0]
+
+
+@pytest.mark.parametrize("run", RUNS)
+def test_traversability_matches_reference(run, torch_cuda):
+    g = load_golden(f"robot_{run}.npz")
+    rb = _batch(g)
+    assert np.array_equal(rb.passable.cpu().numpy(), g["passable"])
+
+
+@pytest.mark.parametrize("run", RUNS)
+def test_robot_step_matches_reference_per_tick(run, torch_cuda):
+    """Each tick from the reference's pre-step state (no drift accumulates)."""
+    import torch
+    g = load_golden(f"robot_{run}.npz")
+    rb = _batch(g)
+    crowd_r = torch.from_numpy(g["crowd_radius"]).cuda()
+    crowd_a = torch.from_numpy(g["crowd_active"].astype(np.uint8)).cuda()
+    n = _n_steps(g)
+    dmatch = hmatch = total_d = total_h = 0
+    for t in range(n):
+        p = _pre(g, t)
+        rb.set_state(p["x"], p["y"], p["yaw"], g["goal"][t], vx=p["vx"], vy=p["vy"], elev=p["elev"],
+                     tick=p["tick"], terminated=p["terminated"], truncated=p["truncated"])
+        cpos = torch.from_numpy(g["crowd_pos"][t]).cuda()
+        rb.step(g["actions"][t], (cpos, crowd_r, crowd_a))
+        for k, a in (("x", rb.x), ("y", rb.y), ("yaw", rb.yaw), ("vx", rb.vx), ("vy", rb.vy),
+                     ("elev", rb.el)):
+            assert np.abs(a.cpu().numpy() - g[k][t]).max() <= TOL, (t, k)
+        assert np.array_equal(rb.tick.cpu().numpy(), g["tick"][t]), t
+        assert np.array_equal(rb.terminated.cpu().numpy().astype(bool), g["terminated"][t]), t
+        assert np.array_equal(rb.truncated.cpu().numpy().astype(bool), g["truncated"][t]), t
+        assert np.array_equal(rb.events.cpu().numpy().astype(bool), g["events"][t]), t
+        for k, a in (("reward", rb.reward), ("distance", rb.distance), ("path_inc", rb.path_inc),
+                     ("goal_vector", rb.goal_vector), ("proj_vel", rb.proj_vel)):
+            assert np.abs(a.cpu().numpy() - g[k][t]).max() <= TOL, (t, k)
+        d = rb.depth.cpu().numpy()
+        h = rb.height_map.cpu().numpy()
+        dmatch += int((d == g["depth"][t]).sum())
+        hmatch += int((h == g["height_map"][t]).sum())
+        total_d += d.size
+        total_h += h.size
+    assert dmatch >= 0.99 * total_d and hmatch >= 0.99 * total_h, (dmatch / total_d, hmatch / total_h)
+
+
+def test_robot_open_loop_tracks_reference(torch_cuda):
+    """120 ticks without re-syncing: the trajectory stays within tolerance of the
+    reference and every discrete outcome (events, flags) is identical."""
+    import torch
+    g = load_golden("robot_quadruped.npz")
+    rb = _batch(g)
+    rb.set_state(g["init_x"], g["init_y"], g["init_yaw"], g["init_goal"], elev=g["init_elev"])
+    crowd_r = torch.from_numpy(g["crowd_radius"]).cuda()
+    crowd_a = torch.from_numpy(g["crowd_active"].astype(np.uint8)).cuda()
+    for t in range(g["x"].shape[0]):
+        rb.step(g["actions"][t], (torch.from_numpy(g["crowd_pos"][t]).cuda(), crowd_r, crowd_a))
+        assert np.array_equal(rb.events.cpu().numpy().astype(bool), g["events"][t]), t
+    for k, a in (("x", rb.x), ("y", rb.y), ("yaw", rb.yaw)):
+        assert np.abs(a.cpu().numpy() - g[k][-1]).max() <= 1e-7, k
