@@ -5,10 +5,17 @@
 ``child_seed(env_seed, "crowd-run")`` (:165), spawns
 ``child_seed(env_seed, "crowd", reset_count)`` (:179), resample seeds
 ``child_seed(env_seed, "resample", n)`` (:332) -- but samples every env on the
-device in one batch and steps the crowd with one kernel per tick.  The robot
-step / observations / reward (batch.py:223-302) are SURVEY §8f "next" and not
-part of this path: ``step_crowd`` advances the crowd with the caller's robot
-pos/vel, as ``crowd.step`` does inside ``step_batch`` (batch.py:216-221).
+device in one batch and steps the crowd with one kernel per tick.
+``step_batch`` (batch.py:205-302) runs the crowd tick with the robot lane, then
+the robot step, reward and observations on the device (``robot.RobotBatch``);
+``step_batch_device`` is the same tick without host copies.
+
+Deviation: the reference spawns the robot on one of the scene's route anchors
+(scene.py:102-158, not built yet); here ``_spawn`` draws the
+start and goal cells from the env's walkable cells with the same stream
+``make_rng(env_seed, "spawn", reset_count)`` and the reference's yaw / elevation
+rule.  ``set_robot_state`` installs any poses (the parity tests use the
+reference's).
 """
 
 from dataclasses import dataclass, field, replace
@@ -18,8 +25,9 @@ import numpy as np
 
 from . import _lib
 from .crowd import CrowdConfig, CrowdField
-from .errors import SlotOutOfRange
+from .errors import BatchShapeMismatch, SlotOutOfRange
 from .rng import child_seed, child_seeds_device, seeds_to_tensor
+from .robot import EVENT_NAMES, ROBOT_MODELS, RewardConfig, RobotBatch
 from .urbangen import SceneSampler, SceneSpec
 
 
@@ -30,8 +38,36 @@ class Scheme(str, Enum):
 
 @dataclass
 class EnvConfig:
+    """batch.py:39-49."""
+    robot: str = "quadruped"
+    horizon: int = 200
+    dt: float = 0.05
+    auto_reset: bool = False
     resample_on_reset: bool = False
+    reach_threshold_m: float = 0.5
+    include_semantics: bool = False
+    reward: RewardConfig = field(default_factory=RewardConfig)
     crowd: CrowdConfig = field(default_factory=CrowdConfig)
+
+
+@dataclass
+class Observation:
+    """observe.py:30-36."""
+    depth: np.ndarray
+    goal_vector: np.ndarray
+    projected_velocity: float
+    height_map: np.ndarray
+    semantics: np.ndarray = None
+
+
+@dataclass
+class StepResult:
+    """batch.py:52-58."""
+    observation: Observation
+    reward: float
+    terminated: bool
+    truncated: bool
+    events: dict
 
 
 class BatchedEnv:
@@ -78,6 +114,14 @@ class BatchedEnv:
                                 device=device, threads=threads)
         if self.spec.pedestrian_count > 0:
             self.crowd.set_from_spawn(self.batch)
+        if self.config.include_semantics:
+            raise NotImplementedError("per-ray semantics (observe.py:84-85) are not built yet")
+        self.model = ROBOT_MODELS[self.config.robot]
+        self.robot = RobotBatch(self.batch.labels, self.batch.elev, self.resolution, self.model,
+                                horizon=self.config.horizon, dt=self.config.dt,
+                                reach_threshold_m=self.config.reach_threshold_m,
+                                reward=self.config.reward, device=self.device)
+        self._spawn(np.arange(k))
 
     # -- stacks (batch.py:132-150) ----------------------------------------------------
     @property
@@ -115,6 +159,10 @@ class BatchedEnv:
         if respawn and self.spec.pedestrian_count > 0:
             self.crowd.set_from_spawn(self.batch, rows=sl)
         self.crowd.prepare_step()
+        if hasattr(self, "robot"):
+            self.robot.refresh_passable(slots)
+            if respawn:
+                self._spawn(slots)
 
     def reset(self, slot, resample=None):
         if not (0 <= slot < self.K):
@@ -122,7 +170,7 @@ class BatchedEnv:
         do_resample = self.config.resample_on_reset if resample is None else resample
         if do_resample:
             self.resample([slot])
-            return
+            return self.observe(slot)
         import torch
         self.reset_counts[slot] += 1
         sl = torch.tensor([slot], device=self.device)
@@ -135,6 +183,45 @@ class BatchedEnv:
         _lib.check(err, "cw_spawn_agents")
         b.check_status(sl)
         self.crowd.set_from_spawn(b, rows=sl)
+        self._spawn([slot])
+        return self.observe(slot)
+
+    # -- robot spawn / state (batch.py:183-198, 352-361) --------------------------------
+    def _spawn(self, rows):
+        """Start and goal = two walkable cells drawn with make_rng(env_seed, "spawn",
+        reset_count); yaw = arctan2(goal - start) and the start cell's elevation as in
+        batch.py:183-198 (the reference draws a route anchor pair; module docstring)."""
+        rows = np.asarray(rows, dtype=np.int64).reshape(-1)
+        if rows.size == 0:
+            return
+        wn = self.batch.walk_n[rows].cpu().numpy()
+        walk = self.batch.walk
+        nx = self.batch.labels.shape[2]
+        res = self.resolution
+        xs, ys, yaws, goals = [], [], [], []
+        for i, e in enumerate(rows):
+            g = np.random.Generator(np.random.PCG64(
+                child_seed(self.env_seeds[e], "spawn", int(self.reset_counts[e]))))
+            n = max(int(wn[i]), 1)
+            a, b = int(g.integers(n)), int(g.integers(n))
+            ca, cb = (int(v) for v in walk[e, [a, b]].cpu().numpy())
+            sx, sy = (ca % nx + 0.5) * res, (ca // nx + 0.5) * res
+            gx, gy = (cb % nx + 0.5) * res, (cb // nx + 0.5) * res
+            xs.append(sx)
+            ys.append(sy)
+            yaws.append(float(np.arctan2(gy - sy, gx - sx)))
+            goals.append((gx, gy))
+        self.robot.set_state(np.array(xs), np.array(ys), np.array(yaws), np.array(goals), rows=rows)
+
+    def set_robot_state(self, x, y, yaw, goal, vx=0.0, vy=0.0, elev=None, tick=0, rows=None):
+        """Install robot poses (e.g. the reference's route-anchor spawns)."""
+        self.robot.set_state(x, y, yaw, goal, vx=vx, vy=vy, elev=elev, tick=tick, rows=rows)
+
+    def robot_state(self, i=0):
+        r = self.robot
+        return {"x": float(r.x[i]), "y": float(r.y[i]), "yaw": float(r.yaw[i]), "vx": float(r.vx[i]),
+                "vy": float(r.vy[i]), "elevation": float(r.el[i]),
+                "goal": [float(r.goal[i, 0]), float(r.goal[i, 1])], "tick": int(r.tick[i])}
 
     # -- stepping -------------------------------------------------------------------------
     def step_crowd(self, robot_pos=None, robot_vel=None, robot_radius=0.35, env_mask=None,
@@ -142,6 +229,58 @@ class BatchedEnv:
         self.crowd.step(robot_pos=robot_pos, robot_vel=robot_vel, robot_radius=robot_radius,
                         env_mask=env_mask, check=check)
 
+    def step_batch_device(self, actions, check=False):
+        """One control step of every live slot on the device (batch.py:205-302) with
+        no host synchronisation; returns the RobotBatch output tensors."""
+        import torch
+        if self.config.auto_reset:
+            done = ((self.robot.terminated != 0) | (self.robot.truncated != 0)).nonzero().flatten()
+            for i in done.cpu().numpy():
+                self._reset_state(int(i))
+        live = self.robot.live()
+        if self.crowd.A > 0:
+            rp = torch.stack([self.robot.x, self.robot.y], -1)
+            rv = torch.stack([self.robot.vx, self.robot.vy], -1)
+            self.crowd.step(robot_pos=rp, robot_vel=rv, robot_radius=self.model.body_radius,
+                            env_mask=live.to(torch.uint8), check=check)
+            self.robot.step(actions, (self.crowd.pos_t, self.crowd.radius_t, self.crowd.active_t))
+        else:
+            self.robot.step(actions)
+        return self.robot.outputs()
+
     def step_batch(self, actions, workers=1):
-        raise NotImplementedError(
-            "robot kinematics / observations / reward are SURVEY §8f 'next'; use step_crowd")
+        """batch.py:205-302: list of StepResult (host copies of the device outputs)."""
+        acts = np.asarray(actions, dtype=np.float64)
+        if acts.shape != (self.K, 2):
+            raise BatchShapeMismatch(f"expected ({self.K}, 2) actions, got {acts.shape}")
+        live = self.robot.live().cpu().numpy() if not self.config.auto_reset else None
+        out = self.step_batch_device(acts, check=True)
+        if live is None:
+            live = np.ones(self.K, bool)
+        h = {k: v.cpu().numpy() for k, v in out.items()}
+        results = []
+        for i in range(self.K):
+            ev = {n: bool(h["events"][i, j]) for j, n in enumerate(EVENT_NAMES)}
+            ev["distance_to_goal"] = float(h["distance"][i])
+            ev["path_increment"] = float(h["path_inc"][i])
+            obs = Observation(depth=h["depth"][i], goal_vector=h["goal_vector"][i],
+                              projected_velocity=float(h["proj_vel"][i]), height_map=h["height_map"][i])
+            results.append(StepResult(observation=obs, reward=float(h["reward"][i]),
+                                      terminated=bool(h["terminated"][i]), truncated=bool(h["truncated"][i]),
+                                      events=ev))
+        return results
+
+    def _reset_state(self, slot, resample=None):
+        do_resample = self.config.resample_on_reset if resample is None else resample
+        if do_resample:
+            self.resample([slot])
+        else:
+            self.reset(slot, resample=False)
+
+    def observe(self, i=0):
+        if not (0 <= i < self.K):
+            raise SlotOutOfRange(f"slot {i} of {self.K}")
+        self.robot.observe()
+        r = self.robot
+        return Observation(depth=r.depth[i].cpu().numpy(), goal_vector=r.goal_vector[i].cpu().numpy(),
+                           projected_velocity=float(r.proj_vel[i]), height_map=r.height_map[i].cpu().numpy())
