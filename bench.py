@@ -269,6 +269,10 @@ def run_ours(args):
     h2d = rpos_h.numel() * 8 * 2
     d2h = out_pos.numel() * 8 * 2
 
+    # ---- full env step (crowd tick with the robot lane + robot step + reward + 128-ray
+    # observations), the path the reference's perf harness times (harness.py:87-124)
+    sb = measure_step_batch(b, f, dev, st, flush, min(args.steps, 200)) if not args.no_step_batch else None
+
     # ---- max over ranks; per-env stats all_gather (the one collective)
     stats = torch.stack([f.last_gap_t, b.obj_n.double(), b.walk_n.double(),
                          f.active_t.sum(1).double()], 1)
@@ -330,6 +334,7 @@ def run_ours(args):
             "roofline_step": {"bound": "hbm", "achieved": round(achieved, 3), "peak": peak, "unit": "GB/s",
                               "frac": round(achieved / peak, 7), "bytes_per_step": round(bytes_step, 1),
                               "model": "SURVEY 8d: 74 B/agent-step + 8 B/path point + 20 B/env-step"},
+            "step_batch": sb,
             "kernels_ms": {n: round(float(v), 4) for n, v in zip(names, ph_avg)},
             "kernels_share": {n: round(float(v / ph_avg.sum()), 4) for n, v in zip(names, ph_avg)},
             "gpu_launches": 4 * steps,   # k_guide, k_astar, k_orca (two passes) per tick
@@ -343,6 +348,49 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def measure_step_batch(b, f, dev, st, flush, steps):
+    """BatchedEnv.step_batch_device semantics on the bench batch: crowd tick with the
+    robot lane (env_mask = live), then cw_robot_step (integrate, gating, contact,
+    reward, observations); random actions resident on the device; L2 flushed."""
+    import torch
+    from paper_2505_00690_b200.robot import RobotBatch
+    E = b.E
+    rb = RobotBatch(b.labels, b.elev, float(b.params.res), "quadruped", horizon=10 ** 9)
+    g = torch.Generator(device="cpu").manual_seed(7)
+    wn = b.walk_n.long()
+    pick = (torch.rand((E, 2), generator=g).to(dev) * wn[:, None].double()).long()
+    cells = b.walk.gather(1, pick)
+    nx = b.labels.shape[2]
+    res = float(b.params.res)
+    xy = lambda c: (((c % nx).double() + 0.5) * res, ((c // nx).double() + 0.5) * res)
+    sx, sy = xy(cells[:, 0])
+    gx, gy = xy(cells[:, 1])
+    rb.set_state(sx, sy, torch.atan2(gy - sy, gx - sx), torch.stack([gx, gy], 1))
+    acts = torch.rand((steps + 5, E, 2), generator=g).to(dev) * 2.0 - 1.0
+
+    def tick(k):
+        rp = torch.stack([rb.x, rb.y], -1)
+        rv = torch.stack([rb.vx, rb.vy], -1)
+        f.step(rp, rv, rb.model.body_radius, env_mask=rb.live().to(torch.uint8), check=False)
+        rb.step(acts[k], (f.pos_t, f.radius_t, f.active_t))
+
+    for k in range(5):
+        tick(k)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for k in range(steps):
+        flush.fill_(float(k))
+        ev[k][0].record(st)
+        tick(5 + k)
+        ev[k][1].record(st)
+    torch.cuda.synchronize()
+    ms = float(np.mean([a.elapsed_time(c) for a, c in ev]))
+    return {"value": round(E / (ms / 1e3), 1), "unit": "env-steps/s", "ms_per_step": round(ms, 4),
+            "steps": steps, "robot": "quadruped",
+            "what": "BatchedEnv.step_batch semantics: crowd tick with robot lane + robot step + reward + "
+                    "128-ray depth fan + 16x10 height patch, device-resident actions, L2 flushed"}
 
 
 def cpu_baseline_sample(b, f, run_seeds, n_env=12, warm=2, steps=40):
@@ -445,6 +493,7 @@ def main():
     ap.add_argument("--sample-reps", type=int, default=3)
     ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-step-batch", action="store_true")
     ap.add_argument("--phase-steps", type=int, default=100)
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per launch of the dominant kernel from an ncu --set full capture")
