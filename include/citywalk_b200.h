@@ -98,6 +98,15 @@ int cw_sample_scenes(const cw_scene_params* params, int E, const uint64_t* scene
                      const uint64_t* crowd_seeds, const int32_t* slots, void* seed_scratch,
                      const cw_scene_buffers* buffers, void* stream);
 
+/* Route anchors (urbangen/scene.py:102-178) for rows slots[e] of buffers->labels
+ * (scene seeds as for cw_sample_scenes): routes (E, 8, 2, 2) float64
+ * [[start x, y], [goal x, y]], n_routes (E); NoRouteAvailable in buffers->status.
+ * scratch: cw_route_scratch_bytes(nx, ny, chunk) (chunk envs per launch). */
+size_t cw_route_scratch_bytes(int nx, int ny, int chunk);
+int cw_route_anchors(const cw_scene_params* params, int E, const uint64_t* scene_seeds,
+                     const int32_t* slots, const cw_scene_buffers* buffers, double* routes,
+                     int32_t* n_routes, void* scratch, int chunk, void* stream);
+
 /* spawn_agents for caller-supplied labels (crowd/step.py:37-63): fills sp_* and
  * status of rows slots[e] from buffers->labels; seed_scratch as for sampling. */
 int cw_spawn_agents(const cw_scene_params* params, int E, const uint64_t* crowd_seeds,

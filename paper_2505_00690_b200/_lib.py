@@ -11,7 +11,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB_PATH = os.path.join(HERE, "libcitywalk_b200.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("sample.cu", "crowd.cu", "robot.cu")]
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("sample.cu", "crowd.cu", "robot.cu", "routes.cu")]
 HEADERS = sorted(os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))
                  if f.endswith(".cuh")) + [os.path.join(ROOT, "include", "citywalk_b200.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
@@ -100,7 +100,8 @@ class RobotState(ctypes.Structure):
 EXPORTS = ["cw_scene_seed_scratch_bytes", "cw_sample_scenes", "cw_spawn_agents", "cw_prepare_envs",
            "cw_crowd_step_smem_bytes",
            "cw_crowd_step", "cw_crowd_step_phases", "cw_astar_slot_bytes", "cw_astar_warps",
-           "cw_traversability_scratch_bytes", "cw_traversability", "cw_robot_step", "cw_robot_observe", "cw_seed_streams", "cw_child_seeds", "cw_abi_sizes"]
+           "cw_traversability_scratch_bytes", "cw_traversability", "cw_robot_step", "cw_robot_observe",
+           "cw_route_scratch_bytes", "cw_route_anchors", "cw_seed_streams", "cw_child_seeds", "cw_abi_sizes"]
 
 _lib = None
 
@@ -161,6 +162,11 @@ def lib():
     L.cw_robot_step.argtypes = [ctypes.POINTER(RobotParams), ctypes.POINTER(RobotState), P, P]
     L.cw_robot_observe.restype = ctypes.c_int
     L.cw_robot_observe.argtypes = [ctypes.POINTER(RobotParams), ctypes.POINTER(RobotState), P]
+    L.cw_route_scratch_bytes.restype = ctypes.c_size_t
+    L.cw_route_scratch_bytes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int]
+    L.cw_route_anchors.restype = ctypes.c_int
+    L.cw_route_anchors.argtypes = [ctypes.POINTER(SceneParams), ctypes.c_int, P, P,
+                                   ctypes.POINTER(SceneBuffers), P, P, P, ctypes.c_int, P]
     L.cw_abi_sizes.restype = ctypes.c_int
     L.cw_abi_sizes.argtypes = [ctypes.POINTER(ctypes.c_size_t), ctypes.c_int]
     sizes = (ctypes.c_size_t * 6)()

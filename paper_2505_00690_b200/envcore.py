@@ -10,12 +10,9 @@ device in one batch and steps the crowd with one kernel per tick.
 the robot step, reward and observations on the device (``robot.RobotBatch``);
 ``step_batch_device`` is the same tick without host copies.
 
-Deviation: the reference spawns the robot on one of the scene's route anchors
-(scene.py:102-158, not built yet); here ``_spawn`` draws the
-start and goal cells from the env's walkable cells with the same stream
-``make_rng(env_seed, "spawn", reset_count)`` and the reference's yaw / elevation
-rule.  ``set_robot_state`` installs any poses (the parity tests use the
-reference's).
+The robot spawns on one of the scene's route anchors (scene.py:102-178, sampled
+on the device by ``cw_route_anchors``) exactly as ``batch.py:183-198`` picks it;
+``set_robot_state`` installs any other poses.
 """
 
 from dataclasses import dataclass, field, replace
@@ -188,29 +185,23 @@ class BatchedEnv:
 
     # -- robot spawn / state (batch.py:183-198, 352-361) --------------------------------
     def _spawn(self, rows):
-        """Start and goal = two walkable cells drawn with make_rng(env_seed, "spawn",
-        reset_count); yaw = arctan2(goal - start) and the start cell's elevation as in
-        batch.py:183-198 (the reference draws a route anchor pair; module docstring)."""
+        """batch.py:183-198: route = make_rng(env_seed, "spawn", reset_count).integers(
+        len(routes)) of the scene's route anchors (cw_route_anchors); yaw toward the
+        goal, elevation of the start cell."""
         rows = np.asarray(rows, dtype=np.int64).reshape(-1)
         if rows.size == 0:
             return
-        wn = self.batch.walk_n[rows].cpu().numpy()
-        walk = self.batch.walk
-        nx = self.batch.labels.shape[2]
-        res = self.resolution
+        routes = self.batch.routes[rows].cpu().numpy()
+        nr = self.batch.n_routes[rows].cpu().numpy()
         xs, ys, yaws, goals = [], [], [], []
         for i, e in enumerate(rows):
             g = np.random.Generator(np.random.PCG64(
                 child_seed(self.env_seeds[e], "spawn", int(self.reset_counts[e]))))
-            n = max(int(wn[i]), 1)
-            a, b = int(g.integers(n)), int(g.integers(n))
-            ca, cb = (int(v) for v in walk[e, [a, b]].cpu().numpy())
-            sx, sy = (ca % nx + 0.5) * res, (ca // nx + 0.5) * res
-            gx, gy = (cb % nx + 0.5) * res, (cb // nx + 0.5) * res
-            xs.append(sx)
-            ys.append(sy)
+            (sx, sy), (gx, gy) = routes[i, int(g.integers(int(nr[i])))]
+            xs.append(float(sx))
+            ys.append(float(sy))
             yaws.append(float(np.arctan2(gy - sy, gx - sx)))
-            goals.append((gx, gy))
+            goals.append((float(gx), float(gy)))
         self.robot.set_state(np.array(xs), np.array(ys), np.array(yaws), np.array(goals), rows=rows)
 
     def set_robot_state(self, x, y, yaw, goal, vx=0.0, vy=0.0, elev=None, tick=0, rows=None):

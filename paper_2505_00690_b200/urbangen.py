@@ -255,6 +255,8 @@ class SceneBatch:
         self.sp_kind = z((E, A), dtype=torch.int8, **d)
         self.sp_pref = z((E, A), dtype=torch.float64, **d)
         self.status = z((E,), dtype=torch.int32, **d)
+        self.routes = z((E, 8, 2, 2), dtype=torch.float64, **d)   # scene.routes (scene.py:87)
+        self.n_routes = z((E,), dtype=torch.int32, **d)
         self.scene_seed = z((E,), dtype=torch.int64, **d)
         self._scratch_rows = 0
         self._ensure_scratch(min(E, SceneSampler.max_rows))
@@ -316,8 +318,9 @@ class SceneSampler:
     """Samples batches of scenes that share a SceneSpec shape (async scheme:
     every env has its own seed, batch.py:84-96)."""
 
-    def __init__(self, spec, capacity, catalog=None, device="cuda"):
+    def __init__(self, spec, capacity, catalog=None, device="cuda", routes=True):
         self.spec = spec
+        self.routes = routes   # also sample scene.routes (scene.py:87, cw_route_anchors)
         self.catalog = catalog or load_catalog()
         self.params = scene_params(spec, self.catalog)
         self.batch = SceneBatch(self.params, capacity, device)
@@ -368,6 +371,13 @@ class SceneSampler:
             self.params, E, _lib.ptr(seeds), _lib.ptr(cseeds), _lib.ptr(sl),
             _lib.ptr(self.batch.seed_scratch), b, _lib.stream_ptr(stream))
         _lib.check(err, "cw_sample_scenes")
+        if self.routes:
+            # route anchors (scene.py:87, 102-178) reuse the sampler scratch (40 B/cell/env)
+            p = self.params
+            err = _lib.lib().cw_route_anchors(
+                p, E, _lib.ptr(seeds), _lib.ptr(sl), b, _lib.ptr(self.batch.routes),
+                _lib.ptr(self.batch.n_routes), _lib.ptr(self.batch.scratch_i32), E, _lib.stream_ptr(stream))
+            _lib.check(err, "cw_route_anchors")
         if check:
             self.batch.check_status(None if sl is None else sl.long())
         return self.batch

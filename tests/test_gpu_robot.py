@@ -100,8 +100,8 @@ def test_robot_open_loop_tracks_reference(torch_cuda):
 
 
 def test_batched_env_step_batch_matches_reference(torch_cuda):
-    """BatchedEnv.step_batch end to end (crowd tick with the robot lane, robot step,
-    reward, observations) from the reference's spawn poses.  The crowd sees the
+    """BatchedEnv.step_batch end to end (route-anchor spawn, crowd tick with the robot
+    lane, robot step, reward, observations).  The crowd sees the
     robot through its VO lane, so it inherits the robot's last-ulp trig
     differences: measured drift stays ~1e-14 over 120 ticks (asserted 1e-9);
     every event and flag is identical."""
@@ -115,7 +115,12 @@ def test_batched_env_step_batch_matches_reference(torch_cuda):
                      grid_resolution_m=0.25)
     env = BatchedEnv(spec, Scheme.ASYNC, master_seed=0, k=K, config=EnvConfig(robot="quadruped"))
     assert np.array_equal(env.labels_stack.cpu().numpy(), g["labels"])
-    env.set_robot_state(g["init_x"], g["init_y"], g["init_yaw"], g["init_goal"], elev=g["init_elev"])
+    # the device spawn (route anchors + batch.py:183-198) lands on the reference's poses
+    for i in range(K):
+        st = env.robot_state(i)
+        assert (st["x"], st["y"], st["yaw"], st["elevation"]) == (
+            g["init_x"][i], g["init_y"][i], g["init_yaw"][i], g["init_elev"][i]), i
+        assert st["goal"] == list(g["init_goal"][i]), i
     names = ("collision", "collision_static", "collision_dynamic", "on_walkable", "reached",
              "out_of_bounds")
     for t in range(T):
