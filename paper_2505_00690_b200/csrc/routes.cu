@@ -2,11 +2,17 @@
 // the candidate (start, goal) pairs the robot spawns on (envcore/batch.py:183-198).
 //
 // One CTA (1024 threads) per env:
-//   1. clearance = chamfer_distance(~walkable) (gridmath.py:8-39) by warp 0: each
-//      row pass is an elementwise pull from the previous row plus the two running
-//      minima min.accumulate(row - j) + j / its mirror, done as lane-blocked warp
-//      scans.  min is exact and the +-j are the same elementwise float64 ops, so
-//      the field is bit-identical to numpy's.
+//   1. clearance test chamfer_distance(~walkable) * res >= 0.4 (gridmath.py:8-39).
+//      The two-pass (1, sqrt2) chamfer with full-row relaxation is the octile
+//      distance to the nearest non-walkable cell (shortest octile paths can be
+//      taken row-monotone), so the test is evaluated by a stencil over the
+//      cells within ceil(0.4 / res) of each cell, reading the walkable bitmap in
+//      shared memory; a borderline distance is an integer (exact in any order),
+//      irrational ones sit >= 3.5e-4 from the threshold.  Above a 6-cell radius
+//      the exact two-pass transform runs instead (warp 0: each row pass is the
+//      elementwise pull plus the two running minima min.accumulate(row - j) + j
+//      as lane-blocked warp scans -- min is exact and the +-j are numpy's
+//      elementwise float64 ops).
 //   2. candidates = walkable cells with clearance >= 0.4 m (else all walkable),
 //      row-major (np.nonzero order), block-scan compaction.
 //   3. geodesic fields (paths.py:21-45 dijkstra_field on the walkable grid, 8-
@@ -14,12 +20,17 @@
 //      minimum over paths of a left-fold sum of 1's and sqrt(2)'s; its optimum
 //      lies within a few ulps of a + b*sqrt(2) for the shortest-path move counts
 //      (a, b), and distinct lengths a + b*sqrt(2) differ by > 3.5e-4.  The kernel
-//      finds (a, b) exactly with integer comparisons (da^2 vs 2 db^2): four
-//      256-thread groups run the four source fields at once with directional
-//      sweeps (H, V and both diagonals, each way; one thread per line) until no
-//      cell improves -- ties are exact, so any shortest path is fine and a few
-//      rounds converge.  geo = (a + b*sqrt(2)) * res then decides the window
-//      tests exactly as the reference except on exact-equality coincidences
+//      finds (a, b) exactly: a cell's distance is the 64-bit key
+//      (round((a + b sqrt2) 2^24) << 28) | b, whose integer order is the order of
+//      the exact lengths (the rounding error < b / 2 units is far below the
+//      3.5e-4 * 2^24 gap), so relaxations are atomicMin's.  Four 256-thread
+//      groups run the four source fields at once as Dial's algorithm with unit
+//      buckets on the exact length: bucket = floor(a + b sqrt2) = key >> 52
+//      (exact for b < 3400).  Every move costs >= 1, so a bucket's cells are final when
+//      it is expanded and pushes land in the next two buckets (three rotating
+//      lists, pushes deduplicated by per-cell bucket stamps, stale entries
+//      skipped) -- every cell is expanded once and the fields are exact.  geo = (a + b*sqrt(2)) * res then decides
+//      the window tests as the reference except on exact-equality coincidences
 //      (none in the golden set, tests/test_gpu_routes.py).
 //   4. the windowed pair draws of scene.py:121-144 with the scene's
 //      make_rng(seed, "routes") stream (thread 0), ok-lists compacted in order.
@@ -37,16 +48,22 @@ constexpr unsigned long long kNoDist = ~0ull;
 
 CW_DEV int route_row(const int32_t* slots, int e) { return slots ? slots[e] : e; }
 
-// exact (a1 + b1 sqrt2) < (a2 + b2 sqrt2)
-CW_DEV bool ab_less(long long a1, long long b1, long long a2, long long b2) {
-  const long long da = a1 - a2, db = b1 - b2;
-  if (da <= 0 && db <= 0) return da < 0 || db < 0;
-  if (da >= 0 && db >= 0) return false;
-  if (da < 0) return da * da > 2 * db * db;     // db > 0
-  return da * da < 2 * db * db;                 // da > 0, db < 0
+// distance key: (round((a + b sqrt2) 2^24) << 28) | b  (a, b < 2^28)
+constexpr unsigned long long kKeyS = 1ull << 24;
+constexpr unsigned long long kKeyR = 23726566ull;          // round(sqrt(2) * 2^24)
+CW_DEV unsigned long long ab_key(unsigned long long a, unsigned long long b) {
+  return ((a * kKeyS + b * kKeyR) << 28) | b;
 }
-
-CW_DEV unsigned long long ab_pack(unsigned a, unsigned b) { return ((unsigned long long)a << 32) | b; }
+CW_DEV void ab_decode(unsigned long long key, unsigned long long& a, unsigned long long& b) {
+  b = key & ((1ull << 28) - 1);
+  a = ((key >> 28) - b * kKeyR) / kKeyS;
+}
+// floor(a + b sqrt2) = top bits of the key: b sqrt2 (b > 0) is >= 1 / (2.83 b)
+// from every integer, far above the key's rounding b / 2 * 2^-24 for b < 3400
+CW_DEV long long ab_bucket(unsigned long long key) { return (long long)(key >> 52); }
+// the key one move further: a + 1 (orthogonal) or b + 1 (diagonal), no decode
+constexpr unsigned long long kStepOrth = kKeyS << 28;
+constexpr unsigned long long kStepDiag = (kKeyR << 28) + 1ull;
 
 // block-wide exclusive scan of one int per thread
 CW_DEV int rt_excl_scan(int v, int* sh, int& total) {
@@ -141,8 +158,9 @@ CW_DEV void chamfer_row(double* row, const double* prev, int nx, int lane) {
   __syncwarp();
 }
 
-// scratch per env: fields 4 x N u64, cand N i32, ok N i32 (D aliases field 0)
-CW_HD size_t route_scratch_per_env(int nx, int ny) { return (size_t)nx * ny * (4 * 8 + 4 + 4); }
+// scratch per env: 4 fields x (key u64 + two bucket-list halves i32 + stamp i32),
+// cand N i32, ok N i32 (the chamfer's D aliases field 0's keys)
+CW_HD size_t route_scratch_per_env(int nx, int ny) { return (size_t)nx * ny * (4 * 20 + 4 + 4); }
 
 __global__ void __launch_bounds__(RT_NT, 1) k_routes(cw_scene_params P, int e0, int n,
                                                      const uint64_t* __restrict__ scene_seeds,
@@ -164,7 +182,9 @@ __global__ void __launch_bounds__(RT_NT, 1) k_routes(cw_scene_params P, int e0, 
   const uint8_t* lab = B.labels + (size_t)row_e * N;
   unsigned char* base = scratch + (size_t)k * route_scratch_per_env(nx, ny);
   unsigned long long* F = reinterpret_cast<unsigned long long*>(base);           // 4 x N
-  int32_t* cand = reinterpret_cast<int32_t*>(base + (size_t)N * 32);
+  int32_t* FL = reinterpret_cast<int32_t*>(base + (size_t)N * 32);               // 4 x 2 x N lists
+  int32_t* ST = FL + (size_t)N * 8;                                              // 4 x N stamps
+  int32_t* cand = ST + (size_t)N * 4;
   int32_t* okl = cand + N;
   double* D = reinterpret_cast<double*>(F);                                      // chamfer (field 0)
   const int NW = (N + 31) / 32;
@@ -178,14 +198,46 @@ __global__ void __launch_bounds__(RT_NT, 1) k_routes(cw_scene_params P, int e0, 
   }
   __syncthreads();
   auto walk = [&](int r, int c) { return (s_walk[(r * nx + c) >> 5] >> ((r * nx + c) & 31)) & 1u; };
-  // ---- 1. clearance (warp 0)
-  for (int f = tid; f < N; f += RT_NT) D[f] = walk(f / nx, f % nx) ? 1e9 : 0.0;
-  __syncthreads();
-  if (wid == 0) {
-    for (int r = 0; r < ny; ++r) chamfer_row(D + (size_t)r * nx, r ? D + (size_t)(r - 1) * nx : nullptr, nx, lane);
-    for (int r = ny - 2; r >= 0; --r) chamfer_row(D + (size_t)r * nx, D + (size_t)(r + 1) * nx, nx, lane);
+  // ---- 1. clearance
+  const int rad = (int)ceil(kMinClear / res);
+  const bool stencil = rad <= 6;
+  auto win_bits = [&](int rr, int c0, int w) -> unsigned long long {   // w <= 13 bits from column c0
+    const int f = rr * nx + c0, wd = f >> 5, sh = f & 31;
+    unsigned long long x = s_walk[wd];
+    if (sh + w > 32) x |= (unsigned long long)s_walk[wd + 1] << 32;
+    return (x >> sh) & ((1ull << w) - 1ull);
+  };
+  auto clear_at = [&](int f) -> bool {   // chamfer(~walkable) * res >= 0.4 for a walkable cell
+    if (!stencil) return D[f] * res >= kMinClear;
+    const int r = f / nx, c = f - r * nx;
+    if (r - rad >= 0 && r + rad < ny && c - rad >= 0 && c + rad < nx) {
+      bool all = true;   // fast path: the whole window walkable
+      for (int dr = -rad; dr <= rad && all; ++dr)
+        all = win_bits(r + dr, c - rad, 2 * rad + 1) == ((1ull << (2 * rad + 1)) - 1ull);
+      if (all) return true;
+    }
+    for (int dr = -rad; dr <= rad; ++dr) {
+      const int rr = r + dr;
+      if (rr < 0 || rr >= ny) continue;
+      for (int dc = -rad; dc <= rad; ++dc) {
+        const int cc = c + dc;
+        if (cc < 0 || cc >= nx || walk(rr, cc)) continue;
+        const int ar = abs(dr), ac = abs(dc);
+        const double o = kSqrt2 * (double)min(ar, ac) + (double)abs(ar - ac);
+        if (o * res < kMinClear) return false;
+      }
+    }
+    return true;
+  };
+  if (!stencil) {
+    for (int f = tid; f < N; f += RT_NT) D[f] = walk(f / nx, f % nx) ? 1e9 : 0.0;
+    __syncthreads();
+    if (wid == 0) {
+      for (int r = 0; r < ny; ++r) chamfer_row(D + (size_t)r * nx, r ? D + (size_t)(r - 1) * nx : nullptr, nx, lane);
+      for (int r = ny - 2; r >= 0; --r) chamfer_row(D + (size_t)r * nx, D + (size_t)(r + 1) * nx, nx, lane);
+    }
+    __syncthreads();
   }
-  __syncthreads();
   // ---- 2. candidates
   int nc = 0;
   for (int pass = 0; pass < 2 && nc == 0; ++pass) {
@@ -193,7 +245,7 @@ __global__ void __launch_bounds__(RT_NT, 1) k_routes(cw_scene_params P, int e0, 
     for (int f0 = 0; f0 < N; f0 += RT_NT) {
       const int f = f0 + tid;
       const bool w = f < N && walk(f / nx, f % nx);
-      const bool c = w && (pass == 1 || D[f] * res >= kMinClear);
+      const bool c = w && (pass == 1 || clear_at(f));
       int tot;
       const int off = rt_excl_scan(c ? 1 : 0, sh, tot);
       if (c) cand[basec + off] = f;
@@ -227,80 +279,104 @@ __global__ void __launch_bounds__(RT_NT, 1) k_routes(cw_scene_params P, int e0, 
   }
   __syncthreads();
   const int nf = traverse ? 1 : 4;
-  // fields: group g (256 threads) owns source g
+  // fields: group g (256 threads) owns source g; Dial's buckets with atomicMin
+  // keys, one named barrier (id 1 + g) per group.  Lists: 3 rotating buckets of
+  // capacity 2N/3 each carved from the group's 2N list space.
   const int g = tid >> 8, gt = tid & 255;
-  unsigned long long* Fg = F + (size_t)g * N;
-  for (int f = gt; f < N && g < nf; f += 256) Fg[f] = kNoDist;
-  __syncthreads();
-  if (g < nf && gt == 0) Fg[cand[s_src[g]]] = ab_pack(0, 0);
-  __syncthreads();
-  // relax v from u (move u -> v; diagonal needs the two corner cells walkable)
-  auto relax = [&](unsigned long long& carry, int ru, int cu, int rv, int cv, bool diag, bool& ch) {
-    const size_t fv = (size_t)rv * nx + cv;
-    unsigned long long cur = Fg[fv];
-    if (carry != kNoDist && walk(rv, cv) && (!diag || (walk(ru, cv) && walk(rv, cu)))) {
-      const unsigned a = (unsigned)(carry >> 32) + (diag ? 0u : 1u);
-      const unsigned b = (unsigned)(carry & 0xffffffffu) + (diag ? 1u : 0u);
-      if (cur == kNoDist || ab_less(a, b, (long long)(cur >> 32), (long long)(cur & 0xffffffffu))) {
-        cur = ab_pack(a, b);
-        Fg[fv] = cur;
-        ch = true;
-      }
+  __shared__ int s_fn[4][3];   // bucket list sizes
+  if (g < nf) {
+    unsigned long long* Fg = F + (size_t)g * N;
+    const int cap = (2 * N) / 3;
+    int32_t* Lb = FL + (size_t)g * 2 * N;
+    int32_t* St = ST + (size_t)g * N;
+    for (int f = gt; f < N; f += 256) { Fg[f] = kNoDist; St[f] = -1; }
+    auto gsync = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory"); };
+    gsync();
+    if (gt == 0) {
+      const int f0 = cand[s_src[g]];
+      Fg[f0] = ab_key(0, 0);
+      Lb[0] = ((f0 / nx) << 16) | (f0 % nx);
+      s_fn[g][0] = 1;
+      s_fn[g][1] = 0;
+      s_fn[g][2] = 0;
     }
-    carry = cur;
-  };
-  for (int round = 0; round < 4096; ++round) {
-    bool ch = false;
-    if (g < nf) {
-      // rows east / west
-      for (int r = gt; r < ny; r += 256) {
-        unsigned long long c0 = Fg[(size_t)r * nx];
-        for (int c = 1; c < nx; ++c) relax(c0, r, c - 1, r, c, false, ch);
-        c0 = Fg[(size_t)r * nx + nx - 1];
-        for (int c = nx - 2; c >= 0; --c) relax(c0, r, c + 1, r, c, false, ch);
+    gsync();
+    for (long long k = 0;; ++k) {
+      const int cur = (int)(k % 3);
+      const int n_cur = s_fn[g][cur];
+      if (n_cur == 0 && s_fn[g][(cur + 1) % 3] == 0 && s_fn[g][(cur + 2) % 3] == 0) break;
+      const int32_t* Lc = Lb + (size_t)cur * cap;
+      // items (cell, move) in batches of 4 per thread: loads and atomics of a
+      // batch are issued back to back; list entries are packed (row << 16 | col)
+      constexpr int BT = 4;
+      for (int q0 = gt; q0 < n_cur * 8; q0 += 256 * BT) {
+        int pu[BT], v[BT], rv[BT], cv[BT];
+        unsigned long long kk[BT];
+        bool ok[BT];
+#pragma unroll
+        for (int i = 0; i < BT; ++i) {
+          const int q = q0 + i * 256;
+          pu[i] = q < n_cur * 8 ? Lc[q >> 3] : -1;
+        }
+#pragma unroll
+        for (int i = 0; i < BT; ++i)
+          kk[i] = pu[i] >= 0 ? (unsigned long long)((volatile unsigned long long*)Fg)[(pu[i] >> 16) * nx + (pu[i] & 0xFFFF)] : ~0ull;
+#pragma unroll
+        for (int i = 0; i < BT; ++i) {
+          const int d = (q0 + i * 256) & 7;
+          ok[i] = false;
+          v[i] = 0;
+          rv[i] = cv[i] = 0;
+          if (pu[i] < 0 || ab_bucket(kk[i]) != k) continue;   // stale: improved into an earlier bucket
+          const int ru = pu[i] >> 16, cu = pu[i] & 0xFFFF;
+          const int dr = (int)((0x22001120u >> (4 * d)) & 0xF) - 1;
+          const int dc = (int)((0x20202011u >> (4 * d)) & 0xF) - 1;
+          rv[i] = ru + dr;
+          cv[i] = cu + dc;
+          if (rv[i] < 0 || rv[i] >= ny || cv[i] < 0 || cv[i] >= nx || !walk(rv[i], cv[i])) continue;
+          const bool diag = d >= 4;
+          if (diag && !(walk(ru, cv[i]) && walk(rv[i], cu))) continue;
+          kk[i] += diag ? kStepDiag : kStepOrth;
+          v[i] = rv[i] * nx + cv[i];
+          ok[i] = true;
+        }
+        // most relaxations improve nothing: a cached read filters them before the atomic
+        unsigned long long old[BT];
+#pragma unroll
+        for (int i = 0; i < BT; ++i) old[i] = ok[i] ? (unsigned long long)((volatile unsigned long long*)Fg)[v[i]] : 0ull;
+#pragma unroll
+        for (int i = 0; i < BT; ++i) {
+          ok[i] = ok[i] && kk[i] < old[i];
+          if (ok[i]) old[i] = atomicMin(&Fg[v[i]], kk[i]);
+        }
+        int jj[BT], st_old[BT];
+#pragma unroll
+        for (int i = 0; i < BT; ++i) {
+          ok[i] = ok[i] && kk[i] < old[i];
+          jj[i] = ok[i] ? (int)ab_bucket(kk[i]) : -1;   // k + 1 or k + 2
+        }
+#pragma unroll
+        for (int i = 0; i < BT; ++i) st_old[i] = ok[i] ? atomicExch(&St[v[i]], jj[i]) : jj[i];
+#pragma unroll
+        for (int i = 0; i < BT; ++i) {
+          if (ok[i] && st_old[i] != jj[i]) {
+            const int slot = jj[i] % 3;
+            Lb[(size_t)slot * cap + atomicAdd(&s_fn[g][slot], 1)] = (rv[i] << 16) | cv[i];
+          }
+        }
       }
+      gsync();
+      if (gt == 0) s_fn[g][cur] = 0;
+      gsync();
     }
-    __syncthreads();
-    if (g < nf) {
-      // columns south / north
-      for (int c = gt; c < nx; c += 256) {
-        unsigned long long c0 = Fg[c];
-        for (int r = 1; r < ny; ++r) relax(c0, r - 1, c, r, c, false, ch);
-        c0 = Fg[(size_t)(ny - 1) * nx + c];
-        for (int r = ny - 2; r >= 0; --r) relax(c0, r + 1, c, r, c, false, ch);
-      }
-    }
-    __syncthreads();
-    if (g < nf) {
-      // diagonals r - c = const (down-right / up-left)
-      for (int L = gt; L < nx + ny - 1; L += 256) {
-        const int d = L - (ny - 1);                   // c = r + d
-        const int r0 = max(0, -d), r1 = min(ny - 1, nx - 1 - d);
-        if (r0 >= r1) continue;
-        unsigned long long c0 = Fg[(size_t)r0 * nx + r0 + d];
-        for (int r = r0 + 1; r <= r1; ++r) relax(c0, r - 1, r - 1 + d, r, r + d, true, ch);
-        c0 = Fg[(size_t)r1 * nx + r1 + d];
-        for (int r = r1 - 1; r >= r0; --r) relax(c0, r + 1, r + 1 + d, r, r + d, true, ch);
-      }
-    }
-    __syncthreads();
-    if (g < nf) {
-      // diagonals r + c = const (down-left / up-right)
-      for (int L = gt; L < nx + ny - 1; L += 256) {
-        const int r0 = max(0, L - (nx - 1)), r1 = min(ny - 1, L);
-        if (r0 >= r1) continue;
-        unsigned long long c0 = Fg[(size_t)r0 * nx + (L - r0)];
-        for (int r = r0 + 1; r <= r1; ++r) relax(c0, r - 1, L - r + 1, r, L - r, true, ch);
-        c0 = Fg[(size_t)r1 * nx + (L - r1)];
-        for (int r = r1 - 1; r >= r0; --r) relax(c0, r + 1, L - r - 1, r, L - r, true, ch);
-      }
-    }
-    if (__syncthreads_or(ch) == 0) break;
   }
+  __syncthreads();
   auto geo_of = [&](int fi, int f) -> double {
     const unsigned long long v = F[(size_t)fi * N + f];
     if (v == kNoDist) return CUDART_INF;
-    return ((double)(v >> 32) + (double)(v & 0xffffffffu) * kSqrt2) * res;
+    unsigned long long a, b;
+    ab_decode(v, a, b);
+    return ((double)a + (double)b * kSqrt2) * res;
   };
   auto xs_of = [&](int f) { return ((double)(f % nx) + 0.5) * res; };
   auto ys_of = [&](int f) { return ((double)(f / nx) + 0.5) * res; };

@@ -326,6 +326,7 @@ class SceneSampler:
         self.batch = SceneBatch(self.params, capacity, device)
 
     max_rows = 2048   # envs per cw_sample_scenes call (bounds the scratch footprint)
+    route_chunk = 296  # envs per route-anchor launch (2 CTAs per SM; 88 B/cell/env scratch)
 
     def sample(self, scene_seeds, crowd_seeds=None, slots=None, stream=None, check=True):
         """Sample len(scene_seeds) scenes into rows ``slots`` (default 0..E-1).
@@ -372,11 +373,16 @@ class SceneSampler:
             _lib.ptr(self.batch.seed_scratch), b, _lib.stream_ptr(stream))
         _lib.check(err, "cw_sample_scenes")
         if self.routes:
-            # route anchors (scene.py:87, 102-178) reuse the sampler scratch (40 B/cell/env)
+            # route anchors (scene.py:87, 102-178), chunked through their own scratch
             p = self.params
+            chunk = min(E, self.route_chunk)
+            nbytes = int(_lib.lib().cw_route_scratch_bytes(p.nx, p.ny, chunk))
+            if getattr(self.batch, "route_scratch", None) is None or self.batch.route_scratch.numel() * 8 < nbytes:
+                self.batch.route_scratch = torch.empty(nbytes // 8 + 1, dtype=torch.int64, device=dev)
             err = _lib.lib().cw_route_anchors(
                 p, E, _lib.ptr(seeds), _lib.ptr(sl), b, _lib.ptr(self.batch.routes),
-                _lib.ptr(self.batch.n_routes), _lib.ptr(self.batch.scratch_i32), E, _lib.stream_ptr(stream))
+                _lib.ptr(self.batch.n_routes), _lib.ptr(self.batch.route_scratch), chunk,
+                _lib.stream_ptr(stream))
             _lib.check(err, "cw_route_anchors")
         if check:
             self.batch.check_status(None if sl is None else sl.long())
