@@ -319,6 +319,8 @@ def run_ours(args):
                        "parallelism": f"env-shard x{world}", "l2": "flushed (256 MB write) between timed steps",
                        "robot": "static per env at a seeded walkable cell, zero velocity"},
             "scenes_per_sec": round(scenes, 1), "sample_ms_per_batch": round(sample_ms, 3),
+            "sample_includes": "zones, WFC terrain, placement, raster + heightfield, nearest-obstacle map, "
+                               "walk list, reach labels, A* move table, pedestrian spawn, route anchors",
             "resample_ms_per_step": round(resample_ms, 3),
             "agent_steps_per_sec": round(value * CFG["peds"], 1),
             "e2e": {"value": round(E * world * e2e_steps / e2e_s, 1), "unit": "env-steps/s",
