@@ -39,6 +39,8 @@ extern "C" {
 
 #define CW_MAX_TILES 44
 #define CW_MAX_CATALOG 32
+#define CW_MAX_BLOCKS 64
+#define CW_ZONE_PARAMS 8
 
 enum cw_status {
   CW_OK = 0,
@@ -90,6 +92,11 @@ typedef struct cw_scene_buffers {
   int32_t* status;
   int32_t* scratch_i32; /* (E, 10*ny*nx) */
   double* scratch_f64;  /* (E, max(obj_max*8, ny*nx)) */
+  double* zone_params;  /* (E, CW_ZONE_PARAMS) ZoneMap.params (zones.py:69-122):
+                           courtyard [blob_half x, y, extra_rects, trail, buildings],
+                           blocks [sidewalk_width, road_width], strip [border_m] */
+  uint8_t* block_var;   /* (E, CW_MAX_BLOCKS) block variant kind*4 + orientation of
+                           connect_blocks (blocks.py:34-77), row-major; layout 1 only */
 } cw_scene_buffers;
 
 size_t cw_scene_seed_scratch_bytes(int E);
@@ -97,6 +104,16 @@ size_t cw_scene_seed_scratch_bytes(int E);
 int cw_sample_scenes(const cw_scene_params* params, int E, const uint64_t* scene_seeds,
                      const uint64_t* crowd_seeds, const int32_t* slots, void* seed_scratch,
                      const cw_scene_buffers* buffers, void* stream);
+
+/* Run-length coding of the sampled grids for scene_to_dict (urbangen/scene.py:163-178,
+ * jsonio.rle_encode jsonio.py:42-54): rows rows[e] (NULL = e) of buffers->zones (ny*nx u8)
+ * and buffers->assign (trows*tcols int32).  Count pass (offsets = pairs = NULL):
+ * runs[2e] = zone runs, runs[2e+1] = assignment runs.  Fill pass: int32
+ * [value, run, ...] lists at pairs + offsets[2e] (zones) and pairs + offsets[2e+1]
+ * (assignment), offsets in int32 elements (2 per run). */
+int cw_scene_rle(const cw_scene_params* params, int E, const int32_t* rows,
+                 const cw_scene_buffers* buffers, int32_t* runs, const int64_t* offsets,
+                 int32_t* pairs, void* stream);
 
 /* Route anchors (urbangen/scene.py:102-178) for rows slots[e] of buffers->labels
  * (scene seeds as for cw_sample_scenes): routes (E, 8, 2, 2) float64

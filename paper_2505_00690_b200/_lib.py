@@ -11,7 +11,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB_PATH = os.path.join(HERE, "libcitywalk_b200.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("sample.cu", "crowd.cu", "robot.cu", "routes.cu")]
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("sample.cu", "crowd.cu", "robot.cu", "routes.cu", "sceneio.cu")]
 HEADERS = sorted(os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))
                  if f.endswith(".cuh")) + [os.path.join(ROOT, "include", "citywalk_b200.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
@@ -19,6 +19,8 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 MAX_TILES = 44
 MAX_CAT = 32
+MAX_BLOCKS = 64
+ZONE_PARAMS = 8
 
 c_i32, c_u32, c_f64, c_f32, c_i64 = ctypes.c_int32, ctypes.c_uint32, ctypes.c_double, ctypes.c_float, ctypes.c_int64
 P = ctypes.c_void_p
@@ -41,7 +43,7 @@ SCENE_BUFFER_FIELDS = [
     "zones", "labels", "elev", "assign", "n_tiles", "tile_code", "tile_kind", "tile_param",
     "tile_p", "tile_w", "allowed", "noise_seed", "wfc_attempts", "obj_cat", "obj_pose", "obj_n",
     "overflow", "nearest", "has_obs", "walk", "walk_n", "reach", "moves", "sp_pos", "sp_goal", "sp_kind", "sp_pref",
-    "status", "scratch_i32", "scratch_f64",
+    "status", "scratch_i32", "scratch_f64", "zone_params", "block_var",
 ]
 
 
@@ -101,7 +103,8 @@ EXPORTS = ["cw_scene_seed_scratch_bytes", "cw_sample_scenes", "cw_spawn_agents",
            "cw_crowd_step_smem_bytes",
            "cw_crowd_step", "cw_crowd_step_phases", "cw_astar_slot_bytes", "cw_astar_warps",
            "cw_traversability_scratch_bytes", "cw_traversability", "cw_robot_step", "cw_robot_observe",
-           "cw_route_scratch_bytes", "cw_route_anchors", "cw_seed_streams", "cw_child_seeds", "cw_abi_sizes"]
+           "cw_route_scratch_bytes", "cw_route_anchors", "cw_seed_streams", "cw_child_seeds", "cw_abi_sizes",
+           "cw_scene_rle"]
 
 _lib = None
 
@@ -128,6 +131,9 @@ def lib():
     L = ctypes.CDLL(LIB_PATH)
     L.cw_scene_seed_scratch_bytes.restype = ctypes.c_size_t
     L.cw_scene_seed_scratch_bytes.argtypes = [ctypes.c_int]
+    L.cw_scene_rle.restype = ctypes.c_int
+    L.cw_scene_rle.argtypes = [ctypes.POINTER(SceneParams), ctypes.c_int, P,
+                               ctypes.POINTER(SceneBuffers), P, P, P, P]
     L.cw_sample_scenes.restype = ctypes.c_int
     L.cw_sample_scenes.argtypes = [ctypes.POINTER(SceneParams), ctypes.c_int, P, P, P, P,
                                    ctypes.POINTER(SceneBuffers), P]

@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(RT_NT, 1) k_routes(cw_scene_params P, int e0, 
                                                      unsigned char* scratch) {
   extern __shared__ uint32_t s_walk[];   // walkable bits
   __shared__ int sh[RT_NT / 32 + 1];
-  __shared__ int s_nc, s_src[4], s_np, s_changed[4];
+  __shared__ int s_src[4], s_np, s_changed[4];
   __shared__ double s_pairs[RT_MAX * 4];
   const int k = blockIdx.x;
   if (k >= n) return;

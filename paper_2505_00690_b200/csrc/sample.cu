@@ -204,6 +204,8 @@ __global__ void k_seeds(int E, const uint64_t* __restrict__ scene_seed,
 
 // ================================================================= zones
 struct Courtyard {
+  double fx, fy;
+  int n_extra;
   Rect walk[5];
   int n_walk;
   int trail;
@@ -220,6 +222,9 @@ CW_DEV void courtyard_draw(const cw_scene_params& P, Pcg64& rng, Courtyard& C) {
   double cx = w / 2.0, cy = l / 2.0;
   C.walk[0] = rect_bounds(P, cx - fx * w, cy - fy * l, cx + fx * w, cy + fy * l);
   int n_extra = 2 + (int)integers32(rng, 3);
+  C.fx = fx;
+  C.fy = fy;
+  C.n_extra = n_extra;
   for (int k = 0; k < n_extra; ++k) {
     double ex = uniform(rng, cx - fx * w, cx + fx * w);
     double ey = uniform(rng, cy - fy * l, cy + fy * l);
@@ -269,12 +274,20 @@ __global__ void __launch_bounds__(256) k_zones(cw_scene_params P, int E, const i
   __shared__ Courtyard C;
   __shared__ Rect strip;
   if (threadIdx.x == 0) {
+    double* zp = B.zone_params + (size_t)slot * CW_ZONE_PARAMS;
+    for (int k = 0; k < CW_ZONE_PARAMS; ++k) zp[k] = 0.0;
     if (P.layout == 0) {
       Pcg64 rng = pcg_load(seeds[e].zones);
       courtyard_draw(P, rng, C);
+      zp[0] = C.fx;
+      zp[1] = C.fy;
+      zp[2] = C.n_extra;
+      zp[3] = C.trail;
+      zp[4] = C.n_build;
     } else {
       double b = fmin(1.0, 0.2 * fmin(P.w, P.l));  // zones.py:71-76
       strip = rect_bounds(P, b, b, P.w - b, P.l - b);
+      zp[0] = b;
     }
   }
   __syncthreads();
@@ -306,6 +319,7 @@ __global__ void __launch_bounds__(256) k_zones(cw_scene_params P, int E, const i
 // ---------------------------------------------------------------- block layout
 struct BlockLayout {
   uint8_t sock[CW_MAX_BLOCKS][4];  // N, E, S, W
+  uint8_t var[CW_MAX_BLOCKS];      // kind * 4 + orientation
   int n;
   double sw;
   uint8_t quad[CW_MAX_BLOCKS][4];  // zone per (qx, qy) quadrant, index qx*2+qy
@@ -353,13 +367,16 @@ CW_DEV void connect_blocks(uint64_t seed, int rows, int cols, BlockLayout& L) {
           if ((need_n < 0 || s[0] == need_n) && (need_w < 0 || s[3] == need_w)) opts[n++] = v;
         }
         int v = opts[integers32(rng, (uint64_t)n)];
+        L.var[r * cols + c] = (uint8_t)v;
         variant_sockets(v, L.sock[r * cols + c]);
       }
     if (blocks_connected(L, rows, cols)) return;
   }
   for (int r = 0; r < rows; ++r)
-    for (int c = 0; c < cols; ++c)
-      variant_sockets((r == 0 && cols > 1) ? 5 * 4 : 0, L.sock[r * cols + c]);
+    for (int c = 0; c < cols; ++c) {
+      L.var[r * cols + c] = (r == 0 && cols > 1) ? 5 * 4 : 0;
+      variant_sockets(L.var[r * cols + c], L.sock[r * cols + c]);
+    }
 }
 
 CW_DEV bool in_road(const cw_scene_params& P, const BlockLayout& L, double ox, double oy, int r,
@@ -396,6 +413,11 @@ __global__ void __launch_bounds__(512) k_zones_blk(cw_scene_params P, int E, con
     connect_blocks(seeds[e].blocks, P.brows, P.bcols, L);
     Pcg64 rng = pcg_load(seeds[e].zones);
     L.sw = uniform(rng, 1.5, 3.0);
+    double* zp = B.zone_params + (size_t)slot * CW_ZONE_PARAMS;
+    for (int k = 0; k < CW_ZONE_PARAMS; ++k) zp[k] = 0.0;
+    zp[0] = L.sw;
+    zp[1] = rw;
+    for (int i = 0; i < CW_MAX_BLOCKS; ++i) B.block_var[(size_t)slot * CW_MAX_BLOCKS + i] = i < L.n ? L.var[i] : 0;
     for (int i = 0; i < L.n; ++i)
       for (int qx = 0; qx < 2; ++qx)
         for (int qy = 0; qy < 2; ++qy) {

@@ -1,4 +1,3 @@
 // Host<->device structs come from the public C ABI header (single source of truth).
 #pragma once
 #include "citywalk_b200.h"
-#define CW_MAX_BLOCKS 64

@@ -104,6 +104,7 @@ class BatchedEnv:
         self.spec = replace(base, seed=self.env_seeds[0])
         self.reset_counts = np.zeros(k, dtype=np.int64)
         self.sampler = SceneSampler(self.spec, k, catalog, device)
+        self._scene_hashes = [None] * k
         crowd_seeds = child_seeds_device(self.env_seeds_t, "crowd", 0)
         self.batch = self.sampler.sample(self.scene_seeds_t, crowd_seeds)
         run = child_seeds_device(self.env_seeds_t, "crowd-run").cpu().numpy().view(np.uint64)
@@ -133,6 +134,16 @@ class BatchedEnv:
     def resolution(self):
         return float(self.batch.params.res)
 
+    @property
+    def scene_hashes(self):
+        """scene_hash of every slot's current scene (batch.py:100, 130): computed
+        on first use from the device batch and refreshed for resampled slots."""
+        stale = [i for i, h in enumerate(self._scene_hashes) if h is None]
+        if stale:
+            for i, h in zip(stale, self.sampler.scene_hashes(stale)):
+                self._scene_hashes[i] = h
+        return list(self._scene_hashes)
+
     # -- resample / reset (batch.py:326-346) --------------------------------------------
     def resample(self, slots, respawn=True):
         """Re-sample the scenes of ``slots`` (Async) and respawn their crowds; the
@@ -153,6 +164,8 @@ class BatchedEnv:
         crowd_seed = child_seeds_device(env, "crowd", cnt)
         self.scene_seeds_t[sl] = new_scene
         self.sampler.sample(new_scene, crowd_seed, slots=sl)
+        for i in slots:
+            self._scene_hashes[int(i)] = None
         if respawn and self.spec.pedestrian_count > 0:
             self.crowd.set_from_spawn(self.batch, rows=sl)
         self.crowd.prepare_step()

@@ -8,8 +8,9 @@ Mirrors /root/reference/pkg/src/citywalk/urbangen:
 plus the batch form the north star asks for: ``SceneSampler.sample(seeds)``
 runs zones -> terrain WFC -> placement -> raster -> nearest-obstacle BFS ->
 walk list -> spawn for every env on the device in one stream-ordered call
-(``cw_sample_scenes``).  Route anchors / scene JSON (scene.py:87-238) are
-out of scope.
+(``cw_sample_scenes``), then the route anchors (``cw_route_anchors``,
+scene.py:87, 102-178).  Scene JSON / hashes (scene.py:163-238) are in
+``sceneio`` (``SceneSampler.scene_dicts`` / ``scene_hashes``).
 """
 
 import json
@@ -90,6 +91,23 @@ class SceneSpec:
             if k not in TERRAIN_FAMILIES:
                 raise ValueError(f"unknown terrain family {k!r}")
 
+    def to_dict(self):
+        """types.py:117-127."""
+        return {"seed": int(self.seed), "extent_m": [float(self.extent_m[0]), float(self.extent_m[1])],
+                "task_kind": TaskKind(self.task_kind).value, "split": Split(self.split).value,
+                "object_density": float(self.object_density), "pedestrian_count": int(self.pedestrian_count),
+                "terrain_mix": {k: float(self.terrain_mix.get(k, 0.0)) for k in TERRAIN_FAMILIES},
+                "grid_resolution_m": float(self.grid_resolution_m)}
+
+    @staticmethod
+    def from_dict(d):
+        """types.py:129-140."""
+        return SceneSpec(seed=int(d["seed"]), extent_m=(float(d["extent_m"][0]), float(d["extent_m"][1])),
+                         task_kind=TaskKind(d["task_kind"]), split=Split(d["split"]),
+                         object_density=float(d["object_density"]),
+                         pedestrian_count=int(d["pedestrian_count"]), terrain_mix=dict(d["terrain_mix"]),
+                         grid_resolution_m=float(d["grid_resolution_m"]))
+
 
 @dataclass(frozen=True)
 class CatalogEntry:
@@ -128,8 +146,126 @@ class OccupancyGrid:
         return int(y / self.resolution), int(x / self.resolution)
 
 
+BLOCK_KINDS = ("Straight", "Curve", "Roundabout", "Diverging", "Merging", "Intersection",
+               "TIntersection")
+BLOCK_SOCKETS = ((1, 0, 1, 0), (1, 1, 0, 0), (1, 1, 1, 1), (1, 1, 0, 1), (1, 1, 0, 1),
+                 (1, 1, 1, 1), (1, 1, 0, 1))   # types.py:148-156 (N, E, S, W)
+DIR_N, DIR_E, DIR_S, DIR_W = 0, 1, 2, 3
+SCHEMA_VERSION = 1
+
+
+def rotated_sockets(kind, orientation):
+    """types.py:159-163."""
+    base = BLOCK_SOCKETS[BLOCK_KINDS.index(kind)]
+    o = orientation % 4
+    return tuple(base[(i - o) % 4] for i in range(4))
+
+
+@dataclass
+class BlockNode:
+    """types.py:166-179."""
+    kind: str
+    cell: tuple
+    orientation: int
+    sockets: tuple
+
+    def to_dict(self):
+        return {"kind": self.kind, "cell": [int(self.cell[0]), int(self.cell[1])],
+                "orientation": int(self.orientation), "sockets": [int(v) for v in self.sockets]}
+
+
+@dataclass
+class BlockGraph:
+    """types.py:182-215; ``from_variants`` rebuilds edges / capped exactly as
+    blocks.py:80-100 (_assemble) from the device's per-block variants."""
+    rows: int
+    cols: int
+    nodes: list
+    edges: list
+    capped: list
+
+    def node_at(self, row, col):
+        return self.nodes[row * self.cols + col]
+
+    @staticmethod
+    def from_variants(rows, cols, variants):
+        nodes = []
+        for i in range(rows * cols):
+            k, o = int(variants[i]) >> 2, int(variants[i]) & 3
+            nodes.append(BlockNode(BLOCK_KINDS[k], (i // cols, i % cols), o,
+                                   rotated_sockets(BLOCK_KINDS[k], o)))
+        edges, capped = [], []
+        for r in range(rows):
+            for c in range(cols):
+                so = nodes[r * cols + c].sockets
+                if so[DIR_E]:
+                    (edges.append(((r, c), (r, c + 1))) if c + 1 < cols else capped.append(((r, c), DIR_E)))
+                if so[DIR_S]:
+                    (edges.append(((r, c), (r + 1, c))) if r + 1 < rows else capped.append(((r, c), DIR_S)))
+                if so[DIR_N] and r == 0:
+                    capped.append(((r, c), DIR_N))
+                if so[DIR_W] and c == 0:
+                    capped.append(((r, c), DIR_W))
+        return BlockGraph(rows, cols, nodes, edges, capped)
+
+    def to_dict(self):
+        return {"rows": int(self.rows), "cols": int(self.cols), "nodes": [n.to_dict() for n in self.nodes],
+                "edges": [[[int(a[0]), int(a[1])], [int(b[0]), int(b[1])]] for a, b in self.edges],
+                "capped": [[[int(c[0]), int(c[1])], int(d)] for c, d in self.capped]}
+
+    @staticmethod
+    def from_dict(d):
+        nodes = [BlockNode(n["kind"], (n["cell"][0], n["cell"][1]), n["orientation"], tuple(n["sockets"]))
+                 for n in d["nodes"]]
+        return BlockGraph(d["rows"], d["cols"], nodes, [((a[0], a[1]), (b[0], b[1])) for a, b in d["edges"]],
+                          [((c[0], c[1]), dd) for c, dd in d["capped"]])
+
+
+@dataclass
+class ZoneMap:
+    """types.py:218-229.  ``rle`` carries the device run-length code of ``grid``
+    (cw_scene_rle) when the map came from a device batch."""
+    resolution: float
+    grid: np.ndarray
+    params: dict
+    rle: list = None
+
+    @property
+    def shape(self):
+        return self.grid.shape
+
+
+@dataclass
+class TerrainTile:
+    """types.py:237-259."""
+    kind: str
+    param: float
+    base: float
+    shape: dict
+
+    def to_dict(self):
+        return {"kind": self.kind, "param": float(self.param), "base": float(self.base), "shape": self.shape}
+
+    @staticmethod
+    def from_dict(d):
+        return TerrainTile(d["kind"], float(d["param"]), float(d["base"]), d["shape"])
+
+
+@dataclass
+class TerrainGrid:
+    """types.py:262-300 (``assignment_rle`` as for ZoneMap.rle)."""
+    tile_size: float
+    rows: int
+    cols: int
+    tiles: list
+    assignment: np.ndarray
+    noise_seed: int
+    assignment_rle: list = None
+
+
 @dataclass
 class AssetInstance:
+    """types.py:328-361."""
     category: str
     x: float
     y: float
@@ -137,19 +273,30 @@ class AssetInstance:
     footprint: tuple
     height: float
 
+    def to_dict(self):
+        return {"category": self.category, "x": float(self.x), "y": float(self.y), "yaw": float(self.yaw),
+                "footprint": [float(self.footprint[0]), float(self.footprint[1])],
+                "height": float(self.height)}
+
+    @staticmethod
+    def from_dict(d):
+        return AssetInstance(d["category"], float(d["x"]), float(d["y"]), float(d["yaw"]),
+                             (float(d["footprint"][0]), float(d["footprint"][1])), float(d["height"]))
+
 
 @dataclass
 class SceneDescription:
-    """The device-sampled scene (types.py:385-394 minus blocks/routes)."""
-
-    spec: SceneSpec
-    zones: np.ndarray
-    terrain_assignment: np.ndarray
-    terrain_tiles: list
-    noise_seed: int
+    """types.py:385-394; ``occupancy`` is the device raster of the same scene
+    (None for scenes loaded from JSON)."""
+    spec: "SceneSpec"
+    blocks: BlockGraph
+    zones: ZoneMap
+    terrain: TerrainGrid
     objects: list
-    placement_overflow: bool
-    occupancy: OccupancyGrid
+    routes: list
+    schema_version: int = SCHEMA_VERSION
+    placement_overflow: bool = False
+    occupancy: "OccupancyGrid" = None
 
 
 def scene_params(spec, catalog=None, obj_max=None):
@@ -258,6 +405,8 @@ class SceneBatch:
         self.routes = z((E, 8, 2, 2), dtype=torch.float64, **d)   # scene.routes (scene.py:87)
         self.n_routes = z((E,), dtype=torch.int32, **d)
         self.scene_seed = z((E,), dtype=torch.int64, **d)
+        self.zone_params = z((E, _lib.ZONE_PARAMS), dtype=torch.float64, **d)   # ZoneMap.params
+        self.block_var = z((E, _lib.MAX_BLOCKS), dtype=torch.uint8, **d)        # connect_blocks
         self._scratch_rows = 0
         self._ensure_scratch(min(E, SceneSampler.max_rows))
 
@@ -303,15 +452,12 @@ class SceneBatch:
                 for k, (x, y, yaw) in zip(cats, pose)]
 
     def scene(self, i, spec, catalog=None):
-        n = int(self.n_tiles[i])
-        tiles = [dict(kind=TERRAIN_KINDS[int(self.tile_kind[i, t])], param=float(self.tile_param[i, t]),
-                      code=int(self.tile_code[i, t]), p=self.tile_p[i, t].cpu().numpy().tolist())
-                 for t in range(n)]
-        return SceneDescription(
-            spec=spec, zones=self.zones[i].cpu().numpy(), terrain_assignment=self.assign[i].cpu().numpy(),
-            terrain_tiles=tiles, noise_seed=int(self.noise_seed[i]) & ((1 << 64) - 1),
-            objects=self.objects(i, catalog), placement_overflow=bool(self.overflow[i]),
-            occupancy=self.occupancy(i))
+        """SceneDescription of row i (types.py:385-394) with its device raster;
+        ``spec`` is the batch spec (the row's seed is its scene seed)."""
+        from .sceneio import batch_scene_dicts, scene_from_dict
+        sc = scene_from_dict(batch_scene_dicts(self, spec, [i], catalog)[0])
+        sc.occupancy = self.occupancy(i)
+        return sc
 
 
 class SceneSampler:
@@ -389,6 +535,17 @@ class SceneSampler:
         return self.batch
 
 
+    def scene_dicts(self, rows=None):
+        """scene_to_dict (scene.py:163-178) of sampled rows (device run-length code)."""
+        from .sceneio import batch_scene_dicts
+        return batch_scene_dicts(self.batch, self.spec, rows, self.catalog)
+
+    def scene_hashes(self, rows=None):
+        """scene_hash (scene.py:229-230) of sampled rows."""
+        from .sceneio import batch_scene_hashes
+        return batch_scene_hashes(self.batch, self.spec, rows, self.catalog)
+
+
 def _as_u64_tensor(seeds, device):
     import torch
     if isinstance(seeds, torch.Tensor):
@@ -398,7 +555,7 @@ def _as_u64_tensor(seeds, device):
 
 
 def generate_scene(spec, catalog=None, device="cuda"):
-    """scene.py:38 generate_scene on the device (route anchors out of scope).
+    """scene.py:38 generate_scene on the device (including the route anchors).
     The returned scene already carries its occupancy raster."""
     s = SceneSampler(spec, 1, catalog, device)
     b = s.sample([spec.seed])
