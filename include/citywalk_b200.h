@@ -185,6 +185,19 @@ int cw_crowd_step_phases(const cw_crowd_params* params, const cw_crowd_state* st
                          const double* robot_pos, const double* robot_vel, double robot_radius,
                          const uint8_t* env_mask, int threads, int phases, void* stream);
 
+/* `ticks` consecutive cw_crowd_step calls with the same robot inputs and env mask,
+ * run without a per-tick barrier: every env advances on its own (envs share no
+ * state), its searches served by a persistent A* kernel through a device queue.
+ * The final state is bit-identical to the synchronous ticks (last_gap included).
+ * Blocks the calling host thread until the run is done (it polls the device to
+ * stop launching rounds); device work is ordered after prior work on `stream`.
+ * scratch: cw_crowd_run_scratch_bytes(E, A, ticks) bytes of device memory.
+ * Returns 0, a CUDA error, 9001 (device queue error) or 9002 (host time limit). */
+size_t cw_crowd_run_scratch_bytes(int E, int A, int ticks);
+int cw_crowd_run(const cw_crowd_params* params, const cw_crowd_state* state,
+                 const double* robot_pos, const double* robot_vel, double robot_radius,
+                 const uint8_t* env_mask, int threads, int ticks, void* scratch, void* stream);
+
 /* Search warps per k_astar CTA (host-only query). */
 int cw_astar_warps(void);
 /* Bytes of astar_rec per k_astar search warp for an nx x ny grid (host-only query). */

@@ -341,6 +341,30 @@ class CrowdField:
         if check:
             self.check_flags()
 
+    def run(self, ticks, robot_pos=None, robot_vel=None, robot_radius=0.35, env_mask=None,
+            stream=None, check=True):
+        """``ticks`` calls of ``step`` with the same inputs, without a per-tick
+        barrier across envs (``cw_crowd_run``): each env advances on its own and
+        the final state is bit-identical.  Blocks until the run is done."""
+        import torch
+        ticks = int(ticks)
+        if self.A == 0 or self.E == 0 or ticks <= 0:
+            return
+        if not hasattr(self, "_p") or self._p.A != self.A:
+            self.prepare_step()
+        rp = self._dev(robot_pos, torch.float64, (self.E, 2))
+        rv = self._dev(robot_vel, torch.float64, (self.E, 2)) if robot_pos is not None else None
+        em = self._dev(env_mask, torch.uint8, (self.E,))
+        nbytes = int(_lib.lib().cw_crowd_run_scratch_bytes(self.E, self.A, ticks))
+        if getattr(self, "_run_scratch", None) is None or self._run_scratch.numel() < nbytes:
+            self._run_scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        err = _lib.lib().cw_crowd_run(self._p, self._s, _lib.ptr(rp), _lib.ptr(rv), float(robot_radius),
+                                      _lib.ptr(em), self.threads, ticks, _lib.ptr(self._run_scratch),
+                                      _lib.stream_ptr(stream))
+        _lib.check(err, "cw_crowd_run")
+        if check:
+            self.check_flags()
+
     def step_phase(self, phase, robot_pos=None, robot_vel=None, robot_radius=0.35, env_mask=None,
                    stream=None):
         """Launch one phase of the tick (1 guide, 2 A*, 4 ORCA+commit); device inputs only."""

@@ -612,8 +612,12 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
 // paths.astar_path exactly; results go to the agent's path (field.py:204-212).
 // Unreachable goals (different 4-connected component, see k_reach) return None
 // without searching -- the reference exhausts the component and returns None.
-template <int W>
-__global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd_state S, int NC, int NS) {
+// kRing: persistent search server of cw_crowd_run -- requests come from the
+// run ring (runq.cuh) until q->shutdown, and each finished search decrements
+// its env's pending count.
+template <int W, bool kRing>
+__global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd_state S, int NC, int NS,
+                                                     RunArgs ra) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gw = blockIdx.x * kAstarWarps + w;       // global search-warp id (scratch slot)
@@ -651,17 +655,29 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
   for (int i = threadIdx.x; i < NS; i += blockDim.x) E.free_ids[i] = (uint16_t)i;
   if (threadIdx.x == 0) { E.pool_lock[0] = 0; E.pool_lock[1] = NS; }
   __syncthreads();
-  long long* const dbg = (S.counters && S.counters[14]) ? reinterpret_cast<long long*>(S.counters[14]) : nullptr;
+  long long* const dbg = (!kRing && S.counters && S.counters[14])
+                             ? reinterpret_cast<long long*>(S.counters[14]) : nullptr;
   long long t_max = 0, t_sum = 0;
   unsigned long long n_exp = 0, n_glob = 0;
   double delta = 1.0, delta2 = 4.0;   // adaptive band widths, carried across searches
   while (true) {
     int q = 0;
-    if (lane == 0) q = atomicAdd(&S.flags[5], 1);
-    q = __shfl_sync(0xffffffffu, q, 0);
-    if (q >= *(volatile int*)&S.flags[4]) break;
+    AstarReq R;
+    if (kRing) {
+      int ok = 0;
+      if (lane == 0) ok = ring_pop(ra, R);
+      if (!__shfl_sync(0xffffffffu, ok, 0)) break;
+      R.env = __shfl_sync(0xffffffffu, R.env, 0);
+      R.agent = __shfl_sync(0xffffffffu, R.agent, 0);
+      R.start = __shfl_sync(0xffffffffu, R.start, 0);
+      R.goal = __shfl_sync(0xffffffffu, R.goal, 0);
+    } else {
+      if (lane == 0) q = atomicAdd(&S.flags[5], 1);
+      q = __shfl_sync(0xffffffffu, q, 0);
+      if (q >= *(volatile int*)&S.flags[4]) break;
+      R = reqs[q];
+    }
     const long long t0 = clock64();
-    const AstarReq R = reqs[q];
     const int e = R.env;
     const uint8_t* mvt = S.moves + (size_t)e * N;
     const uint8_t* lab = S.labels + (size_t)e * N;
@@ -736,10 +752,17 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
     }
     const int used_final = used;
     release();
+    if (kRing) {   // publish the result, then count the env's search as done
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        atomicSub(&ra.pending[e], 1);
+      }
+    }
     const long long dt = clock64() - t0;
     if (dbg && lane == 0) {
       long long* d = dbg + (size_t)q * 8;
-      d[0] = dt; d[1] = s_exp; d[2] = 0; d[3] = used_final;
+      d[0] = dt; d[1] = s_exp; d[2] = e; d[3] = used_final;
     }
     n_exp += s_exp;
     t_sum += dt;

@@ -15,7 +15,11 @@
 // Two-phase: every CTA snapshots its env's pre-step state in shared memory,
 // so results are independent of scheduling (field.py:1-9).  Compiled with
 // -fmad=false: float64 arithmetic rounds exactly like the numpy reference.
+#include <algorithm>
 #include <cfloat>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <math_constants.h>
 #include "common.cuh"
 #include "crowd_types.cuh"
@@ -222,6 +226,7 @@ struct AstarReq { int32_t env, agent, start, goal; };
 struct __align__(16) OpenEnt { unsigned long long f, k; };
 
 }  // namespace cw
+#include "runq.cuh"
 #include "astar.cuh"
 namespace cw {
 
@@ -236,21 +241,23 @@ CW_DEV void path_point(const int32_t* cells, int head, int n, int k, double gx, 
 }
 
 // k_guide: field.py:165-212 minus the A* itself (queued for k_astar).
-template <int NT>
-__global__ void __launch_bounds__(NT) k_guide(cw_crowd_params P, cw_crowd_state S,
-                                              const uint8_t* __restrict__ env_mask) {
+// Body shared by k_guide (requests appended to astar_req) and k_round (requests
+// pushed to the run ring).  Returns the env's request count (CTA-uniform).
+template <int NT, bool kRing>
+__device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int e,
+                         const uint8_t* __restrict__ env_mask, const RunArgs* ra) {
   constexpr int NW = NT / 32;
-  const int e = blockIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int A = P.A;
   const size_t eA = (size_t)e * A;
-  __shared__ int s_req;   // some agent of this env queued a replan
+  __shared__ int s_req;   // replans this env queued
   if (env_mask && !env_mask[e]) {
     if (threadIdx.x == 0) S.env_req[e] = 0;
-    return;
+    return 0;
   }
   if (threadIdx.x == 0) s_req = 0;
   __syncthreads();
+  int my_req = 0;
   const bool has_obs = S.has_obs[e] != 0;
   const int nx = P.nx, ny = P.ny;
   const size_t N = (size_t)nx * ny;
@@ -332,16 +339,29 @@ __global__ void __launch_bounds__(NT) k_guide(cw_crowd_params P, cw_crowd_state 
       int sc = (int)fmin(fmax(px / res, 0.0), (double)(nx - 1));
       int gr = (int)fmin(fmax(gy / res, 0.0), (double)(ny - 1));
       int gc = (int)fmin(fmax(gx / res, 0.0), (double)(nx - 1));
-      int q = atomicAdd(&S.flags[4], 1);
       AstarReq R = {e, a, sr * nx + sc, gr * nx + gc};
-      reqs[q] = R;
-      s_req = 1;
+      if (kRing) {
+        ring_push(*ra, R);
+      } else {
+        int q = atomicAdd(&S.flags[4], 1);
+        reqs[q] = R;
+      }
+      ++my_req;
     }
   }
   if (lane == 0 && scanned && S.counters)
     atomicAdd((unsigned long long*)&S.counters[1], (unsigned long long)scanned);
+  if (lane == 0 && my_req) atomicAdd(&s_req, my_req);
   __syncthreads();
-  if (threadIdx.x == 0) S.env_req[e] = (uint8_t)s_req;
+  const int n_req = s_req;
+  if (threadIdx.x == 0) S.env_req[e] = (uint8_t)(n_req > 0);
+  return n_req;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_guide(cw_crowd_params P, cw_crowd_state S,
+                                              const uint8_t* __restrict__ env_mask) {
+  guide_env<NT, false>(P, S, blockIdx.x, env_mask, nullptr);
 }
 
 // ---------------------------------------------------------------- ORCA + commit
@@ -365,16 +385,15 @@ CW_HD size_t bins_smem_bytes(const Bins& b, int A) {
   return b.ncx > 0 ? (size_t)(b.ncx * b.ncy + 1 + 2 * A) * 4 : 0;
 }
 
+// ORCA + commit + goal resample of env e (body of k_orca and k_round).  With
+// ra != nullptr the env's gap goes to the run history at ``tick`` instead of
+// gap_tmp / flags[0].
 template <int NT>
-__global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S,
-                                             const double* __restrict__ robot_pos,
-                                             const double* __restrict__ robot_vel,
-                                             double robot_radius,
-                                             const uint8_t* __restrict__ env_mask, Bins bins,
-                                             int pass) {
+__device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int e,
+                         const double* __restrict__ robot_pos, const double* __restrict__ robot_vel,
+                         double robot_radius, const uint8_t* __restrict__ env_mask, const Bins& bins,
+                         unsigned char* sm, const RunArgs* ra, int tick) {
   constexpr int NW = NT / 32;
-  extern __shared__ __align__(16) unsigned char sm[];
-  const int e = blockIdx.x;
   const int A = P.A;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* s_px = reinterpret_cast<double*>(sm);
@@ -392,10 +411,7 @@ __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S
   int* s_cell = s_sorted + A;
   __shared__ double s_gap[NW];
   __shared__ int s_anynb[NW];
-  // pass 0: every env; pass 1: envs without A* requests (runs beside k_astar);
-  // pass 2: envs with requests (after k_astar).  The body is per env.
-  const bool skip = (pass == 1 && S.env_req[e]) || (pass == 2 && !S.env_req[e]);
-  if (!skip) {
+  {
   const long long t_cta0 = clock64();
     const size_t eA = (size_t)e * A;
     const bool emask = env_mask ? env_mask[e] != 0 : true;
@@ -619,8 +635,13 @@ __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S
       double g = CUDART_INF;
       int anynb = 0;
       for (int w = 0; w < NW; ++w) { g = fmin(g, s_gap[w]); anynb |= s_anynb[w]; }
-      S.gap_tmp[e] = g;
-      if (anynb) atomicOr(&S.flags[0], 1);
+      if (ra) {
+        ra->gap_hist[(size_t)e * ra->T + tick] = g;
+        if (anynb) ra->anynb[tick] = 1;
+      } else {
+        S.gap_tmp[e] = g;
+        if (anynb) atomicOr(&S.flags[0], 1);
+      }
       if (P.resample_goals) {
         Pcg64Raw* raw = reinterpret_cast<Pcg64Raw*>(S.rng) + e;
         bool loaded = false;
@@ -652,6 +673,21 @@ __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S
       atomicMax((unsigned long long*)&S.counters[7], (unsigned long long)tc);
     }
   }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S,
+                                             const double* __restrict__ robot_pos,
+                                             const double* __restrict__ robot_vel,
+                                             double robot_radius,
+                                             const uint8_t* __restrict__ env_mask, Bins bins,
+                                             int pass) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int e = blockIdx.x;
+  // pass 0: every env; pass 1: envs without A* requests (runs beside k_astar);
+  // pass 2: envs with requests (after k_astar).  The body is per env.
+  const bool skip = (pass == 1 && S.env_req[e]) || (pass == 2 && !S.env_req[e]);
+  if (!skip) orca_env<NT>(P, S, e, robot_pos, robot_vel, robot_radius, env_mask, bins, sm, nullptr, 0);
   // ---------------- last CTA: publish last_gap_by_env (only when some row had K > 0),
   // reset the per-step flags and the A* queue
   if (threadIdx.x == 0) {
@@ -668,6 +704,86 @@ __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S
       S.flags[5] = 0;
     }
   }
+}
+
+// ---------------------------------------------------------------- multi-tick run
+// One CTA per env: advance the env tick after tick until it has to wait for its
+// own searches (then park in WAIT) or reaches T; a WAIT env resumes once the
+// server has finished all of that tick's searches (pending == 0).
+template <int NT>
+__global__ void __launch_bounds__(NT) k_round(cw_crowd_params P, cw_crowd_state S,
+                                              const double* __restrict__ robot_pos,
+                                              const double* __restrict__ robot_vel, double robot_radius,
+                                              const uint8_t* __restrict__ env_mask, Bins bins,
+                                              RunArgs ra) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int e = blockIdx.x;
+  __shared__ int s_st, s_go;
+  if (threadIdx.x == 0) {
+    const int st = ra.env_state[e];
+    int go = (st & 3) != kRunDone;
+    if ((st & 3) == kRunWait) {
+      go = ld_acquire_i32(&ra.pending[e]) == 0;
+      if (go) __threadfence();
+    }
+    s_st = st;
+    s_go = go;
+  }
+  __syncthreads();
+  if (!s_go) return;
+  int t = s_st >> 2;
+  bool guide = (s_st & 3) == kRunGuide;
+  while (true) {
+    if (guide) {
+      if (threadIdx.x == 0) {
+        ra.pending[e] = kPendingGuard;   // searches may finish before the count is known
+        __threadfence();
+      }
+      const int n = guide_env<NT, true>(P, S, e, env_mask, &ra);
+      if (threadIdx.x == 0) {
+        const int left = atomicSub(&ra.pending[e], kPendingGuard - n) - (kPendingGuard - n);
+        if (left) ra.env_state[e] = (t << 2) | kRunWait;
+        else __threadfence();
+        s_go = left == 0;
+      }
+      __syncthreads();
+      if (!s_go) return;
+    }
+    orca_env<NT>(P, S, e, robot_pos, robot_vel, robot_radius, env_mask, bins, sm, &ra, t);
+    __syncthreads();
+    if (++t == ra.T) {
+      if (threadIdx.x == 0) {
+        ra.env_state[e] = (t << 2) | kRunDone;
+        __threadfence();
+        if (atomicAdd(&ra.q->n_done, 1) + 1 == ra.E) atomicExch(&ra.q->shutdown, 1);
+      }
+      return;
+    }
+    guide = true;
+  }
+}
+
+__global__ void k_run_init(RunArgs ra) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) *ra.q = RunQueue{0ull, 0ull, 0, 0, 0, 0};
+  if (i < (size_t)ra.E) { ra.env_state[i] = 0; ra.pending[i] = 0; }
+  if (i < (size_t)ra.T) ra.anynb[i] = 0;
+  if (i <= ra.mask) ra.seq[i] = i;
+}
+
+// last_gap_by_env as T synchronous ticks leave it: the gaps of the last tick on
+// which some env had a neighbour (k_orca's last-CTA publication).
+__global__ void k_run_finish(cw_crowd_state S, RunArgs ra) {
+  __shared__ int s_t;
+  if (threadIdx.x == 0) {
+    int t = ra.T - 1;
+    while (t >= 0 && !ra.anynb[t]) --t;
+    s_t = t;
+  }
+  __syncthreads();
+  if (s_t < 0) return;
+  for (int e = threadIdx.x; e < ra.E; e += blockDim.x)
+    S.last_gap[e] = ra.gap_hist[(size_t)e * ra.T + s_t];
 }
 
 __global__ void k_seed_streams(int n, const uint64_t* __restrict__ seeds, Pcg64Raw* out) {
@@ -709,8 +825,130 @@ static TickStreams& tick_streams() {
 static void launch_astar(const cw_crowd_params& P, const cw_crowd_state& S, cudaStream_t st) {
   const int W = P.astar_warps == 1 ? 1 : kAstarWarps;
   const AstarShape A = astar_shape(P.nx, P.ny, W);
-  if (W == 1) k_astar<1><<<P.astar_ctas, 32, A.smem, st>>>(P, S, A.NC, A.NS);
-  else k_astar<kAstarWarps><<<P.astar_ctas, 32 * kAstarWarps, A.smem, st>>>(P, S, A.NC, A.NS);
+  const RunArgs none = {};
+  if (W == 1) k_astar<1, false><<<P.astar_ctas, 32, A.smem, st>>>(P, S, A.NC, A.NS, none);
+  else k_astar<kAstarWarps, false><<<P.astar_ctas, 32 * kAstarWarps, A.smem, st>>>(P, S, A.NC, A.NS, none);
+}
+
+// ---- cw_crowd_run scratch layout
+struct RunLayout {
+  unsigned long long cap;
+  size_t q, env_state, pending, seq, items, gap_hist, anynb, total;
+};
+
+static RunLayout run_layout(int E, int A, int T) {
+  RunLayout L;
+  unsigned long long need = 2ull * (unsigned long long)E * (unsigned long long)A, cap = 1024;
+  while (cap < need) cap <<= 1;
+  L.cap = cap;
+  auto up = [](size_t v) { return (v + 255) & ~(size_t)255; };
+  L.q = 0;
+  L.env_state = up(sizeof(RunQueue));
+  L.pending = L.env_state + up((size_t)E * 4);
+  L.seq = L.pending + up((size_t)E * 4);
+  L.items = L.seq + up((size_t)cap * 8);
+  L.gap_hist = L.items + up((size_t)cap * sizeof(AstarReq));
+  L.anynb = L.gap_hist + up((size_t)E * T * 8);
+  L.total = L.anynb + up((size_t)T * 4);
+  return L;
+}
+
+template <int NT>
+static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const double* rp,
+                      const double* rv, double rr, const uint8_t* em, int ticks, void* scratch,
+                      cudaStream_t st) {
+  const Bins bins = make_bins(P);
+  const size_t sm = cw_crowd_step_smem_bytes(P.A, NT) + bins_smem_bytes(bins, P.A);
+  static bool attrs = false;
+  if (!attrs) {
+    cudaFuncSetAttribute(k_astar<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    // the server and the rounds share SMs only under one L1 / shared split
+    cudaFuncSetAttribute(k_astar<1, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(k_round<NT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    attrs = true;
+  }
+  if (sm > 48 * 1024)
+    cudaFuncSetAttribute(k_round<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const RunLayout L = run_layout(P.E, P.A, ticks);
+  unsigned char* base = static_cast<unsigned char*>(scratch);
+  RunArgs ra;
+  ra.q = reinterpret_cast<RunQueue*>(base + L.q);
+  ra.env_state = reinterpret_cast<int*>(base + L.env_state);
+  ra.pending = reinterpret_cast<int*>(base + L.pending);
+  ra.seq = reinterpret_cast<unsigned long long*>(base + L.seq);
+  ra.items = reinterpret_cast<AstarReq*>(base + L.items);
+  ra.gap_hist = reinterpret_cast<double*>(base + L.gap_hist);
+  ra.anynb = reinterpret_cast<int*>(base + L.anynb);
+  ra.T = ticks;
+  ra.E = P.E;
+  ra.mask = L.cap - 1;
+  const size_t n_init = std::max<size_t>(std::max<size_t>(P.E, ticks), L.cap);
+  k_run_init<<<(unsigned)((n_init + 255) / 256), 256, 0, st>>>(ra);
+
+  struct Host {
+    int* poll = nullptr;       // pinned: 8 x {n_done, shutdown, error, pad}
+    int* one = nullptr;
+    cudaEvent_t ev[8], start, srv_done, rounds_done;
+    cudaStream_t copy;
+  };
+  static Host H;
+  if (!H.poll) {
+    cudaHostAlloc(&H.poll, 8 * 32, cudaHostAllocDefault);
+    cudaHostAlloc(&H.one, 16, cudaHostAllocDefault);
+    H.one[0] = 1;
+    for (auto& ev : H.ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&H.start, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&H.srv_done, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&H.rounds_done, cudaEventDisableTiming);
+    cudaStreamCreateWithFlags(&H.copy, cudaStreamNonBlocking);
+  }
+  TickStreams& TS = tick_streams();
+  cudaEventRecord(H.start, st);
+  cudaStreamWaitEvent(TS.hi, H.start, 0);
+  cudaStreamWaitEvent(TS.lo, H.start, 0);
+  const AstarShape shp = astar_shape(P.nx, P.ny, 1);
+  int srv_ctas = P.astar_ctas;
+  if (const char* v = getenv("CW_RUN_SERVER_CTAS")) srv_ctas = std::min(srv_ctas, atoi(v));
+  k_astar<1, true><<<srv_ctas, 32, shp.smem, TS.hi>>>(P, S, shp.NC, shp.NS, ra);
+  cudaEventRecord(H.srv_done, TS.hi);
+  int err = (int)cudaGetLastError();
+  const auto t_begin = std::chrono::steady_clock::now();
+  constexpr int kInFlight = 6;
+  static const bool debug = getenv("CW_RUN_DEBUG") != nullptr;
+  int status = 0;
+  for (long long i = 0;; ++i) {
+    k_round<NT><<<P.E, NT, sm, TS.lo>>>(P, S, rp, rv, rr, em, bins, ra);
+    cudaMemcpyAsync(H.poll + (i & 7) * 8, ra.q, 32, cudaMemcpyDeviceToHost, TS.lo);
+    cudaEventRecord(H.ev[i & 7], TS.lo);
+    if (i >= kInFlight) {
+      const long long j = i - kInFlight;
+      cudaEventSynchronize(H.ev[j & 7]);
+      const int* pv = H.poll + (j & 7) * 8 + 4;   // n_done, shutdown, error
+      if (debug && (j % 2000 == 0 || pv[2])) {
+        if (j == 0) fprintf(stderr, "server smem %d NC %d NS %d ctas %d round smem %zu\n", shp.smem, shp.NC,
+                            shp.NS, srv_ctas, sm);
+        const unsigned long long* hq = reinterpret_cast<const unsigned long long*>(pv - 4);
+        fprintf(stderr, "cw_crowd_run round %lld: head %llu tail %llu done %d/%d shutdown %d error %d\n",
+                j, hq[0], hq[1], pv[0], P.E, pv[1], pv[2]);
+      }
+      if (pv[0] >= P.E) break;
+      if (pv[2]) { status = 9001; break; }
+      const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_begin).count();
+      if (secs > 300.0 || (err = (int)cudaGetLastError()) != 0) { status = err ? err : 9002; break; }
+    }
+  }
+  if (status) {   // end the server through the copy engine (no SM needed)
+    cudaMemcpyAsync(&ra.q->shutdown, H.one, 4, cudaMemcpyHostToDevice, H.copy);
+    cudaStreamSynchronize(H.copy);
+  }
+  cudaStreamWaitEvent(TS.lo, H.srv_done, 0);
+  k_run_finish<<<1, 256, 0, TS.lo>>>(S, ra);
+  cudaEventRecord(H.rounds_done, TS.lo);
+  cudaStreamWaitEvent(st, H.rounds_done, 0);
+  if (status) return status;
+  return (int)cudaGetLastError();
 }
 
 template <int NT>
@@ -763,6 +1001,27 @@ size_t cw_crowd_step_smem_bytes(int A, int nt) {
 // Search warps per k_astar CTA (astar_rec / astar_heap hold one slot per warp).
 int cw_astar_warps(void) { return cw::kAstarWarps; }
 
+// Scratch bytes of cw_crowd_run for E envs x A agents over `ticks` ticks.
+size_t cw_crowd_run_scratch_bytes(int E, int A, int ticks) {
+  return cw::run_layout(E, A, ticks).total;
+}
+
+// `ticks` synchronous cw_crowd_step calls with the same inputs, run without a
+// per-tick barrier (runq.cuh); same final state bit for bit.
+int cw_crowd_run(const cw_crowd_params* P, const cw_crowd_state* S, const double* robot_pos,
+                 const double* robot_vel, double robot_radius, const uint8_t* env_mask, int threads,
+                 int ticks, void* scratch, void* stream) {
+  using namespace cw;
+  if (P->E <= 0 || P->A <= 0 || ticks <= 0) return 0;
+  if (!scratch) return (int)cudaErrorInvalidValue;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (threads == 256)
+    return launch_run<256>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, ticks, scratch, st);
+  if (threads == 64)
+    return launch_run<64>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, ticks, scratch, st);
+  return launch_run<128>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, ticks, scratch, st);
+}
+
 // Bytes of A* scratch (astar_rec) per k_astar search warp for an nx x ny grid.
 size_t cw_astar_slot_bytes(int nx, int ny) {
   return cw::astar_slot_stride(nx, ny);
@@ -778,8 +1037,13 @@ int cw_crowd_step_phases(const cw_crowd_params* P, const cw_crowd_state* S,
   cudaStream_t st = (cudaStream_t)stream;
   static int attr_set = 0;   // opt-in shared memory (<= 227 KB) for both k_astar shapes
   if (!attr_set) {
-    cudaFuncSetAttribute(k_astar<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_astar<kAstarWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_astar<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_astar<kAstarWarps, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    cudaFuncSetAttribute(k_astar<1, false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(k_astar<kAstarWarps, false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
     attr_set = 1;
   }
   if (threads == 256)

@@ -1,0 +1,83 @@
+// Multi-tick asynchronous run (cw_crowd_run): device queues and per-env state.
+//
+// Envs never read each other's state (SPEC: no cross-env sharing), so a run of
+// T ticks needs no global barrier per tick.  Each env advances through
+//   guide -> [its A* searches] -> ORCA + commit -> guide of the next tick ...
+// on its own: short "round" kernels (one CTA per env) advance every env as far
+// as it can go without waiting, and a persistent k_astar server drains a
+// bounded MPMC ring of search requests concurrently on another stream.  An env
+// whose tick needs searches parks in WAIT with a pending count; the server
+// decrements it and the next round that sees zero resumes the env.  Per env the
+// operations, their order and their inputs are exactly those of T synchronous
+// cw_crowd_step calls, so the final state is bit-identical; the only
+// cross-env quantity, last_gap_by_env (field.py:268-271: published on ticks
+// where any env had a neighbour), is rebuilt from a per-(env, tick) history.
+#pragma once
+
+namespace cw {
+
+enum { kRunGuide = 0, kRunWait = 1, kRunDone = 3 };
+constexpr int kPendingGuard = 1 << 24;   // > any per-env request count
+constexpr long long kSpinCycles = 8ll << 30;    // ~4.5 s: a full ring slot is an error, not a hang
+constexpr long long kIdleCycles = 64ll << 30;   // ~35 s backstop for an idle server warp (the
+                                                // host normally ends the run via q->shutdown)
+
+struct RunQueue {                 // device-resident control words
+  unsigned long long head, tail;  // ring positions claimed by consumers / producers
+  int n_done, shutdown, error, pad;
+};
+
+struct RunArgs {                  // kernel parameter (pointers into cw_crowd_run scratch)
+  RunQueue* q;
+  int* env_state;                 // tick << 2 | phase
+  int* pending;                   // outstanding searches of the env's current tick
+  unsigned long long* seq;        // ring slot sequence numbers (Vyukov bounded MPMC)
+  AstarReq* items;
+  double* gap_hist;               // (E, T) per-tick gap of every env
+  int* anynb;                     // (T) some env had K > 0 at tick t
+  int T, E;
+  unsigned long long mask;        // ring capacity - 1 (power of two)
+};
+
+CW_DEV unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+CW_DEV void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+CW_DEV int ld_acquire_i32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// producer (one thread): blocks only while the slot's previous item is unread
+CW_DEV void ring_push(const RunArgs& ra, const AstarReq& R) {
+  const unsigned long long pos = atomicAdd(&ra.q->tail, 1ull);
+  unsigned long long* sq = ra.seq + (pos & ra.mask);
+  const long long t0 = clock64();
+  while (ld_acquire_u64(sq) != pos) {
+    if (clock64() - t0 > kSpinCycles) { atomicCAS(&ra.q->error, 0, 1); return; }
+  }
+  ra.items[pos & ra.mask] = R;
+  st_release_u64(sq, pos + 1);
+}
+
+// consumer (lane 0 of a server warp): false on shutdown / error
+CW_DEV bool ring_pop(const RunArgs& ra, AstarReq& R) {
+  const unsigned long long pos = atomicAdd(&ra.q->head, 1ull);
+  unsigned long long* sq = ra.seq + (pos & ra.mask);
+  const long long t0 = clock64();
+  while (ld_acquire_u64(sq) != pos + 1) {
+    if (*(volatile int*)&ra.q->shutdown) return false;
+    if (clock64() - t0 > kIdleCycles) { atomicCAS(&ra.q->error, 0, 2); return false; }
+    __nanosleep(64);
+  }
+  R = ra.items[pos & ra.mask];
+  st_release_u64(sq, pos + ra.mask + 1);
+  return true;
+}
+
+}  // namespace cw

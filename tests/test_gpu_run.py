@@ -1,0 +1,91 @@
+"""cw_crowd_run (CrowdField.run): T ticks without a per-tick barrier across
+envs must leave exactly the state of T synchronous CrowdField.step calls --
+positions, velocities, goals, waypoints, guidance paths, RNG streams and
+last_gap_by_env, bit for bit -- with robots, env masks, split runs, and the
+cfg2 shape (256^2 grids, 32 pedestrians, A* replans every tick)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+MIX = {"Flat": 0.25, "Slope": 0.25, "Stair": 0.25, "Rough": 0.25}
+FIELDS = ("pos_t", "vel_t", "goal_t", "waypoint_t", "path_cells_t", "path_head_t", "path_n_t", "rng_t",
+          "last_gap_t", "active_t")
+
+
+def _pair(E, ext, res, peds, objs, nd=5.0):
+    from oracle.rng import child_seed
+    from paper_2505_00690_b200.crowd import CrowdConfig, CrowdField
+    from paper_2505_00690_b200.urbangen import SceneSampler, SceneSpec, TaskKind
+    seeds = [child_seed(0, "env", i) for i in range(E)]
+    area = int(np.floor(4.0 * ext * ext / 100.0 + 0.5))
+    spec = SceneSpec(seed=0, extent_m=(ext, ext), task_kind=TaskKind.NAV_DYNAMIC, pedestrian_count=peds,
+                     object_density=objs / area, terrain_mix=MIX, grid_resolution_m=res)
+    b = SceneSampler(spec, E).sample(seeds, [child_seed(s, "crowd", 0) for s in seeds])
+    run = [child_seed(s, "crowd-run") for s in seeds]
+    fs = []
+    for _ in range(2):
+        f = CrowdField(b, CrowdConfig(neighbor_distance=nd), run)
+        f.set_from_spawn(b)
+        fs.append(f)
+    return b, fs
+
+
+def _robot(b, E, res, seed=3):
+    import torch
+    g = np.random.default_rng(seed)
+    nx = b.params.nx
+    walk_n = b.walk_n.cpu().numpy()
+    cells = np.array([int(b.walk[e, int(g.integers(walk_n[e]))]) for e in range(E)])
+    rp = np.stack([((cells % nx) + 0.5) * res, ((cells // nx) + 0.5) * res], 1)
+    rv = g.uniform(-0.5, 0.5, (E, 2))
+    return torch.from_numpy(rp).cuda(), torch.from_numpy(rv).cuda()
+
+
+def _same(a, b, what):
+    for k in FIELDS:
+        x, y = getattr(a, k).cpu().numpy(), getattr(b, k).cpu().numpy()
+        if k == "rng_t":   # Pcg64Raw: state, inc, buffered half, has-half (bytes 40-47 are padding)
+            x, y = x[:, :40], y[:, :40]
+        assert np.array_equal(x, y), (what, k, np.argwhere(x != y)[:4])
+
+
+@pytest.mark.parametrize("E,ext,res,peds,objs,T", [(16, 32.0, 0.25, 8, 20, 40),
+                                                   (24, 32.0, 0.125, 32, 64, 25),
+                                                   (6, 24.0, 0.25, 48, 40, 30)])
+def test_run_equals_synchronous_ticks(E, ext, res, peds, objs, T, torch_cuda):
+    b, (f, g) = _pair(E, ext, res, peds, objs)
+    rp, rv = _robot(b, E, res)
+    for _ in range(T):
+        f.step(rp, rv, 0.35)
+    g.run(T, rp, rv, 0.35)
+    torch_cuda.cuda.synchronize()
+    _same(f, g, "run")
+    assert np.isfinite(g.last_gap_t.cpu().numpy()).any()
+
+
+def test_run_with_env_mask_and_split_runs(torch_cuda):
+    import torch
+    E, T = 12, 30
+    b, (f, g) = _pair(E, 32.0, 0.25, 8, 20)
+    rp, rv = _robot(b, E, 0.25, seed=9)
+    mask = torch.from_numpy((np.arange(E) % 3 != 1).astype(np.uint8)).cuda()
+    for _ in range(T):
+        f.step(rp, rv, 0.35, env_mask=mask)
+    g.run(11, rp, rv, 0.35, env_mask=mask)
+    g.run(1, rp, rv, 0.35, env_mask=mask)
+    g.run(T - 12, rp, rv, 0.35, env_mask=mask)
+    _same(f, g, "masked split run")
+
+
+def test_run_without_robot_then_steps(torch_cuda):
+    E = 8
+    b, (f, g) = _pair(E, 32.0, 0.25, 8, 20)
+    for _ in range(15):
+        f.step()
+    g.run(15)
+    _same(f, g, "no robot")
+    for _ in range(3):   # synchronous ticks continue from the run's state
+        f.step()
+        g.step()
+    _same(f, g, "after run")

@@ -62,6 +62,8 @@ def run(phases):
 
 
 tot = 0.0
+tick_max = []
+mats = []
 for k in range(steps):
     run(1)
     torch.cuda.synchronize()
@@ -78,15 +80,31 @@ for k in range(steps):
     t = e0.elapsed_time(e1)
     c = f.counters_t.cpu().numpy().copy()
     d = dbg.cpu().numpy()
+    if os.environ.get("LAB_ENVSUM"):
+        per_env = np.zeros(E)
+        np.maximum.at(per_env, d[:nreq, 2].astype(np.int64), d[:nreq, 0].astype(np.float64))
+        env_sum = per_env if k == 0 else env_sum + per_env
+        tick_max.append(per_env.max())
+        mats.append(per_env.copy())
     for r_ in d[np.argsort(-d[:, 0])[:2]]:
         if os.environ.get("LAB_PHASES"):
             ph_ = [(int(r_[4 + i // 2]) >> (32 * (i % 2))) & 0xFFFFFFFF for i in range(6)] + [int(r_[7])]
             print("      phases/exp [pop, loads+stale, gy+push, alloc, store+key, route+pool, inserts]:",
                   " ".join(f"{v / max(r_[1], 1):5.0f}" for v in ph_))
-        print(f"   search cyc {r_[0]/1e6:6.2f}M exp {r_[1]:6d} cyc/exp {r_[0]/max(r_[1],1):6.0f} stale {r_[2]:6d} "
+        print(f"   search cyc {r_[0]/1e6:6.2f}M exp {r_[1]:6d} cyc/exp {r_[0]/max(r_[1],1):6.0f} env {r_[2]:6d} "
               f"tiles {r_[3]:6d}")
     f.check_flags()
     run(4)
     tot += t
     print(f"step {k:3d} req {nreq:5d} exp {c[0]:8d} glob {c[10]:3d} max_cyc {c[5]/1e6:7.2f}M  ms {t:7.3f}", flush=True)
 print(f"TOTAL {tot:.2f} ms over {steps} ticks")
+if os.environ.get("LAB_ENVSUM"):
+    srt = np.sort(env_sum)[::-1]
+    M = np.stack(mats)   # (ticks, E)
+    np.save(os.path.join(ROOT, "gpurun_out", "lab_env_tick.npy"), M)
+    for G in (1, 2, 4, 8, 16, 32, 64, 128):
+        grp = M.reshape(M.shape[0], G, -1).max(axis=2).sum(axis=0)
+        print(f"  G={G:4d}: max over groups of summed tick-max {grp.max()/1e6:7.1f}M cycles")
+    print(f"sum over ticks of max-search cycles {sum(tick_max)/1e6:.1f}M; max over envs of summed "
+          f"cycles {srt[0]/1e6:.1f}M; next envs {[round(v/1e6, 1) for v in srt[1:8]]}")
+
