@@ -96,6 +96,7 @@ class CrowdField:
         self.resample_goals = resample_goals
         self.device = torch.device(device)
         self.threads = threads
+        self.run_threads = None   # cw_crowd_run CTA size; None: one lane per agent
         self.astar_warps = astar_warps
         if isinstance(occupancies, SceneBatch):
             b = occupancies
@@ -342,7 +343,7 @@ class CrowdField:
             self.check_flags()
 
     def run(self, ticks, robot_pos=None, robot_vel=None, robot_radius=0.35, env_mask=None,
-            stream=None, check=True):
+            stream=None, check=True, threads=None):
         """``ticks`` calls of ``step`` with the same inputs, without a per-tick
         barrier across envs (``cw_crowd_run``): each env advances on its own and
         the final state is bit-identical.  Blocks until the run is done."""
@@ -359,11 +360,17 @@ class CrowdField:
         if getattr(self, "_run_scratch", None) is None or self._run_scratch.numel() < nbytes:
             self._run_scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         err = _lib.lib().cw_crowd_run(self._p, self._s, _lib.ptr(rp), _lib.ptr(rv), float(robot_radius),
-                                      _lib.ptr(em), self.threads, ticks, _lib.ptr(self._run_scratch),
+                                      _lib.ptr(em), int(threads or self.run_threads or self._run_nt()), ticks,
+                                      _lib.ptr(self._run_scratch),
                                       _lib.stream_ptr(stream))
         _lib.check(err, "cw_crowd_run")
         if check:
             self.check_flags()
+
+    def _run_nt(self):
+        """Round CTA size: one lane per agent below 128 agents (lane ORCA / guide),
+        else the warp-per-agent shape with cell binning."""
+        return 32 if self.A <= 32 else 64 if self.A <= 64 else 128 if self.A < 128 else 256
 
     def step_phase(self, phase, robot_pos=None, robot_vel=None, robot_radius=0.35, env_mask=None,
                    stream=None):

@@ -361,12 +361,13 @@ struct AstarShape {
   size_t smem;
 };
 
-CW_HD AstarShape astar_shape(int nx, int ny, int W) {
+CW_HD AstarShape astar_shape(int nx, int ny, int W, int budget_kb = 0) {
   const int nt = ((nx + 7) / 8) * ((ny + 7) / 8);
   const int NC = W == 1 ? 1024 : 512;
   const size_t per_warp = (size_t)(NC + 64) * 16 + (((size_t)nt * 2 + 15) & ~(size_t)15);
   // W = 1 leaves ~30 KB of the SM's 228 KB for k_orca CTAs running beside it
-  const size_t budget = (W == 1 ? 196 : 220) * 1024, head = 16;   // lock + stack top
+  if (budget_kb <= 0) budget_kb = W == 1 ? 196 : 220;
+  const size_t budget = (size_t)budget_kb * 1024, head = 16;   // lock + stack top
   const size_t fixed = W * per_warp + head;
   int NS = budget > fixed ? (int)((budget - fixed) / (576 + 2)) : 0;
   NS = NS > W * nt ? W * nt : NS;
@@ -756,7 +757,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
       __syncwarp();
       if (lane == 0) {
         __threadfence();
-        atomicSub(&ra.pending[e], 1);
+        if (atomicSub(&ra.pending[e], 1) == 1) ready_push(ra, e);   // the env's last search
       }
     }
     const long long dt = clock64() - t0;

@@ -20,6 +20,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 #include <math_constants.h>
 #include "common.cuh"
 #include "crowd_types.cuh"
@@ -216,6 +217,69 @@ CW_DEV bool warp_lp(const WarpCons& C, int nc, double pf0, double pf1, double ms
   return false;
 }
 
+// ---------------------------------------------------------------- lane LP
+// warp_lp for one agent held by one lane (constraints in registers, lane
+// order).  Identical arithmetic: the lane-parallel max / min over j < i of
+// warp_lp is an exact reduction, taken here in j order.
+constexpr int MAXK = MAXC - 2;   // neighbour lanes
+
+CW_DEV bool lane_lp(const double (&cpx)[MAXC], const double (&cpy)[MAXC], const double (&cnx)[MAXC],
+                    const double (&cny)[MAXC], int nc, double pf0, double pf1, double ms, double& r0,
+                    double& r1) {
+  double pn = sqrt(pf0 * pf0 + pf1 * pf1);
+  double sc = pn > ms ? ms / fmax(pn, kEps) : 1.0;
+  r0 = pf0 * sc;
+  r1 = pf1 * sc;
+#pragma unroll
+  for (int i = 0; i < MAXC; ++i) {
+    if (i >= nc) break;
+    const double pi0 = cpx[i], pi1 = cpy[i], ni0 = cnx[i], ni1 = cny[i];
+    if (!((r0 - pi0) * ni0 + (r1 - pi1) * ni1 < -kEps)) continue;
+    const double d0 = -ni1, d1 = ni0;
+    const double dpd = pi0 * d0 + pi1 * d1;
+    const double disc = dpd * dpd + ms * ms - (pi0 * pi0 + pi1 * pi1);
+    bool bad = disc < 0.0;
+    const double sq = sqrt(fmax(disc, 0.0));
+    double tl = -dpd - sq, tr = -dpd + sq;
+    double tlj = -DBL_MAX, trj = DBL_MAX;
+#pragma unroll
+    for (int j = 0; j < MAXC; ++j) {
+      if (j >= i) break;
+      const double den = d0 * cnx[j] + d1 * cny[j];
+      const double num = (cpx[j] - pi0) * cnx[j] + (cpy[j] - pi1) * cny[j];
+      if (fabs(den) < kEps) {
+        bad |= num > kEps;
+      } else {
+        const double t = num / den;
+        if (den > 0.0) tlj = fmax(tlj, t);
+        else trj = fmin(trj, t);
+      }
+    }
+    tl = fmax(tl, tlj);
+    tr = fmin(tr, trj);
+    bad |= tl > tr;
+    if (bad) {
+      WarpCons C;
+#pragma unroll
+      for (int k = 0; k < MAXC; ++k) { C.px[k] = cpx[k]; C.py[k] = cpy[k]; C.nx[k] = cnx[k]; C.ny[k] = cny[k]; }
+      least_violation(C, nc, i, ms, r0, r1);
+      return true;
+    }
+    double tb = (pf0 - pi0) * d0 + (pf1 - pi1) * d1;
+    tb = fmin(fmax(tb, tl), tr);
+    r0 = pi0 + tb * d0;
+    r1 = pi1 + tb * d1;
+  }
+  return false;
+}
+
+// register-array slot write with a run-time index (keeps the array in registers)
+CW_DEV void put_slot(double (&a)[MAXC], int k, double v) {
+#pragma unroll
+  for (int r = 0; r < MAXC; ++r)
+    if (r == k) a[r] = v;
+}
+
 // ---------------------------------------------------------------- A*
 CW_DEV double octile(int r, int c, int gr, int gc) {
   int dr = abs(r - gr), dc = abs(c - gc);
@@ -246,8 +310,7 @@ CW_DEV void path_point(const int32_t* cells, int head, int n, int k, double gx, 
 template <int NT, bool kRing>
 __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int e,
                          const uint8_t* __restrict__ env_mask, const RunArgs* ra) {
-  constexpr int NW = NT / 32;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int A = P.A;
   const size_t eA = (size_t)e * A;
   __shared__ int s_req;   // replans this env queued
@@ -265,12 +328,15 @@ __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
   const double res = P.res;
   long long scanned = 0;
   AstarReq* reqs = reinterpret_cast<AstarReq*>(S.astar_req);
-  for (int a = wid; a < A; a += NW) {
+  // one agent per thread: every decision below is a boolean (near the path,
+  // line of sight clear), so each lane stops its scans at the first hit
+  for (int a = threadIdx.x; a < A; a += NT) {
     const size_t ia = eA + a;
     if (!S.active[ia]) continue;
     const double gx = S.goal[ia * 2], gy = S.goal[ia * 2 + 1];
     if (!has_obs) {
-      if (lane == 0) { S.waypoint[ia * 2] = gx; S.waypoint[ia * 2 + 1] = gy; }
+      S.waypoint[ia * 2] = gx;
+      S.waypoint[ia * 2 + 1] = gy;
       continue;
     }
     const double px = S.pos[ia * 2], py = S.pos[ia * 2 + 1];
@@ -280,74 +346,64 @@ __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
       double qx, qy;
       path_point(cells, head, n, 0, gx, gy, res, nx, qx, qy);
       if (glibc_hypot(qx - px, qy - py) < kWaypointReach && n > 1) { ++head; --n; }
-      // _distance_to_polyline (field.py:613-625) over the remaining points
-      double best = CUDART_INF;
-      if (lane == 0) {
-        path_point(cells, head, n, 0, gx, gy, res, nx, qx, qy);
-        best = glibc_hypot(qx - px, qy - py);
-      }
-      for (int k = 1 + lane; k < n; k += 32) {
-        double ax, ay, bx, by;
-        path_point(cells, head, n, k - 1, gx, gy, res, nx, ax, ay);
+      // _distance_to_polyline (field.py:613-625) <= kStrayLimit (field.py:190)
+      path_point(cells, head, n, 0, gx, gy, res, nx, qx, qy);
+      bool near = glibc_hypot(qx - px, qy - py) <= kStrayLimit;
+      double bx = qx, by = qy;
+      for (int k = 1; k < n && !near; ++k) {
+        const double ax = bx, ay = by;
         path_point(cells, head, n, k, gx, gy, res, nx, bx, by);
         double abx = bx - ax, aby = by - ay;
         double den = dot2_blas(abx, aby, abx, aby);
         double t = 0.0;
         if (!(den < kEps)) t = fmin(fmax(dot2_blas(px - ax, py - ay, abx, aby) / den, 0.0), 1.0);
-        double d = glibc_hypot(ax + t * abx - px, ay + t * aby - py);
-        best = fmin(best, d);
+        near = glibc_hypot(ax + t * abx - px, ay + t * aby - py) <= kStrayLimit;
       }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
-      scanned += n;
-      if (best <= kStrayLimit) {
-        double wx, wy;
-        path_point(cells, head, n, 0, gx, gy, res, nx, wx, wy);
-        if (lane == 0) {
-          S.path_head[ia] = head;
-          S.path_n[ia] = n;
-          S.waypoint[ia * 2] = wx;
-          S.waypoint[ia * 2 + 1] = wy;
-        }
+      scanned += n;   // the reference scans every remaining point (traffic model)
+      if (near) {
+        S.path_head[ia] = head;
+        S.path_n[ia] = n;
+        S.waypoint[ia * 2] = qx;
+        S.waypoint[ia * 2 + 1] = qy;
         continue;
       }
     }
-    // _line_of_sight (field.py:601-610), warp-parallel over the samples
+    // _line_of_sight (field.py:601-610)
     double d = glibc_hypot(gx - px, gy - py);
     long long ns = max(2LL, trunc_ll(2.0 * d / res) + 2);
     double step = 1.0 / (double)(ns - 1);
     bool clear = true;
-    for (long long k = lane; k < ns; k += 32) {
+    for (long long k = 0; k < ns && clear; ++k) {
       double t = k == ns - 1 ? 1.0 : (double)k * step + 0.0;
       double xs = px + (gx - px) * t, ys = py + (gy - py) * t;
       long long rr = clampll(trunc_ll(ys / res), 0, ny - 1);
       long long cc = clampll(trunc_ll(xs / res), 0, nx - 1);
-      if (lab[rr * nx + cc] == L_OBSTACLE) clear = false;
+      clear = lab[rr * nx + cc] != L_OBSTACLE;
     }
-    clear = __all_sync(0xffffffffu, clear);
     if (clear) {
-      if (lane == 0) {
-        S.path_head[ia] = 0;
-        S.path_n[ia] = 1;
-        S.waypoint[ia * 2] = gx;
-        S.waypoint[ia * 2 + 1] = gy;
-      }
+      S.path_head[ia] = 0;
+      S.path_n[ia] = 1;
+      S.waypoint[ia * 2] = gx;
+      S.waypoint[ia * 2 + 1] = gy;
       continue;
     }
-    if (lane == 0) {
-      int sr = (int)fmin(fmax(py / res, 0.0), (double)(ny - 1));
-      int sc = (int)fmin(fmax(px / res, 0.0), (double)(nx - 1));
-      int gr = (int)fmin(fmax(gy / res, 0.0), (double)(ny - 1));
-      int gc = (int)fmin(fmax(gx / res, 0.0), (double)(nx - 1));
-      AstarReq R = {e, a, sr * nx + sc, gr * nx + gc};
-      if (kRing) {
-        ring_push(*ra, R);
-      } else {
-        int q = atomicAdd(&S.flags[4], 1);
-        reqs[q] = R;
-      }
-      ++my_req;
+    int sr = (int)fmin(fmax(py / res, 0.0), (double)(ny - 1));
+    int sc = (int)fmin(fmax(px / res, 0.0), (double)(nx - 1));
+    int gr = (int)fmin(fmax(gy / res, 0.0), (double)(ny - 1));
+    int gc = (int)fmin(fmax(gx / res, 0.0), (double)(nx - 1));
+    AstarReq R = {e, a, sr * nx + sc, gr * nx + gc};
+    if (kRing) {
+      ring_push(*ra, R);
+    } else {
+      int q = atomicAdd(&S.flags[4], 1);
+      reqs[q] = R;
     }
+    ++my_req;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    scanned += __shfl_xor_sync(0xffffffffu, scanned, o);
+    my_req += __shfl_xor_sync(0xffffffffu, my_req, o);
   }
   if (lane == 0 && scanned && S.counters)
     atomicAdd((unsigned long long*)&S.counters[1], (unsigned long long)scanned);
@@ -478,7 +534,139 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
     double my_gap = CUDART_INF;
     int my_anynb = 0;
     long long fallbacks = 0, stalls = 0;
-    for (int a = wid; a < A; a += NW) {
+    const bool lanes = bins.ncx == 0 && P.max_neighbors <= MAXK;
+    if (lanes) {
+      // ---------------- lane per agent (A < 128): same operations as the warp path
+      const int kmax = min(P.max_neighbors, max(A - 1, 0));
+      for (int a = threadIdx.x; a < A; a += NT) {
+        if (!s_act[a]) continue;
+        const double px = s_px[a], py = s_py[a];
+        const size_t ia = eA + a;
+        const double gx = S.goal[ia * 2], gy = S.goal[ia * 2 + 1];
+        const double wx = S.waypoint[ia * 2], wy = S.waypoint[ia * 2 + 1];
+        const double sp = S.pref_speed[ia];
+        double tw0 = wx - px, tw1 = wy - py;
+        double dist = sqrt(tw0 * tw0 + tw1 * tw1);
+        double safe = fmax(dist, kEps);
+        double pf0 = tw0 / safe * sp, pf1 = tw1 / safe * sp;
+        double tg0 = gx - px, tg1 = gy - py;
+        double dg = sqrt(tg0 * tg0 + tg1 * tg1);
+        double scl = fmin(1.0, dg / fmax(sp * P.dt * 4, kEps));
+        pf0 = pf0 * scl;
+        pf1 = pf1 * scl;
+        // stable top-K by (fp32 key, index): the scan visits j in increasing order,
+        // so a new entry goes after every kept entry with key <= its key
+        const float xi = (float)px, yi = (float)py;
+        const float sqi = __fadd_rn(__fmul_rn(xi, xi), __fmul_rn(yi, yi));
+        const double vxa = s_vx[a], vya = s_vy[a], ra = s_r[a];
+        float tk[MAXK];
+        int tj[MAXK];
+#pragma unroll
+        for (int k = 0; k < MAXK; ++k) { tk[k] = CUDART_INF_F; tj[k] = 0; }
+        int nb = 0;
+        for (int j = 0; j < A; ++j) {
+          if (j == a || !s_act[j]) continue;
+          float xj = (float)s_px[j], yj = (float)s_py[j];
+          float sqj = __fadd_rn(__fmul_rn(xj, xj), __fmul_rn(yj, yj));
+          float dot = __fmaf_rn(yi, yj, __fmul_rn(xi, xj));
+          float key = __fsub_rn(__fadd_rn(sqi, sqj), __fmul_rn(2.0f, dot));
+          if (!(key < P.nd2_f32)) continue;
+          int pos = 0;
+#pragma unroll
+          for (int k = 0; k < MAXK; ++k) pos += (k < nb && tk[k] <= key);
+          if (pos >= kmax) continue;
+#pragma unroll
+          for (int k = MAXK - 1; k > 0; --k)
+            if (k > pos) { tk[k] = tk[k - 1]; tj[k] = tj[k - 1]; }
+#pragma unroll
+          for (int k = 0; k < MAXK; ++k)
+            if (k == pos) { tk[k] = key; tj[k] = j; }
+          nb = min(nb + 1, kmax);
+        }
+        double cpx[MAXC], cpy[MAXC], cnx[MAXC], cny[MAXC];
+#pragma unroll
+        for (int k = 0; k < MAXC; ++k) { cpx[k] = 0.0; cpy[k] = 0.0; cnx[k] = 1.0; cny[k] = 0.0; }
+#pragma unroll
+        for (int k = 0; k < MAXK; ++k) {
+          if (k >= nb) break;
+          const int j = tj[k];
+          double rp0 = s_px[j] - px, rp1 = s_py[j] - py;
+          double rv0 = vxa - s_vx[j], rv1 = vya - s_vy[j];
+          double rr = ra + s_r[j] + P.safety_margin;
+          vo_halfplane(rp0, rp1, rv0, rv1, rr, P.time_horizon, P.dt, vxa, vya, 0.5, cpx[k], cpy[k],
+                       cnx[k], cny[k]);
+          if (k == 0) {
+            double d_near = sqrt(rp0 * rp0 + rp1 * rp1);   // field.py:268-271
+            my_gap = fmin(my_gap, d_near - (ra + s_r[j]));
+            my_anynb = 1;
+          }
+        }
+        int nc = nb;
+        if (use_robot) {
+          double rp0 = rpx - px, rp1 = rpy - py;
+          double d2 = rp0 * rp0 + rp1 * rp1;
+          if (d2 < P.nd2) {
+            double rr = ra + robot_radius + P.safety_margin;
+            double q0, q1, m0, m1;
+            vo_halfplane(rp0, rp1, vxa - rvx, vya - rvy, rr, P.obstacle_time_horizon, P.dt, vxa, vya,
+                         1.0, q0, q1, m0, m1);
+            put_slot(cpx, nc, q0); put_slot(cpy, nc, q1); put_slot(cnx, nc, m0); put_slot(cny, nc, m1);
+            ++nc;
+          }
+        }
+        if (P.use_static && has_obs) {
+          long long ri = clampll(trunc_ll(py / res), 0, ny - 1);
+          long long ci = clampll(trunc_ll(px / res), 0, nx - 1);
+          int flat = S.nearest[e * N + ri * nx + ci];
+          if (flat >= 0) {
+            int orow = flat / nx, ocol = flat - orow * nx;
+            double rp0 = ((double)ocol + 0.5) * res - px, rp1 = ((double)orow + 0.5) * res - py;
+            double d2 = rp0 * rp0 + rp1 * rp1;
+            if (d2 < P.nd2) {
+              double margin = 0.5 * kSqrt2 * P.res0;
+              double rr = ra + margin + P.safety_margin;
+              double q0, q1, m0, m1;
+              vo_halfplane(rp0, rp1, vxa, vya, rr, P.obstacle_time_horizon, P.dt, vxa, vya, 1.0, q0, q1,
+                           m0, m1);
+              put_slot(cpx, nc, q0); put_slot(cpy, nc, q1); put_slot(cnx, nc, m0); put_slot(cny, nc, m1);
+              ++nc;
+            }
+          }
+        }
+        const double ms = S.max_speed[ia];
+        double v0, v1;
+        fallbacks += lane_lp(cpx, cpy, cnx, cny, nc, pf0, pf1, ms, v0, v1);
+        double spd = sqrt(v0 * v0 + v1 * v1);
+        double want = sqrt(pf0 * pf0 + pf1 * pf1);
+        if (spd < 0.2 * want && want > 1e-6) {
+          ++stalls;
+          double q0 = P.stall_c * pf0 + P.stall_s * pf1;
+          double q1 = -P.stall_s * pf0 + P.stall_c * pf1;
+          fallbacks += lane_lp(cpx, cpy, cnx, cny, nc, q0, q1, ms, v0, v1);
+        }
+        double npx = px + v0 * P.dt, npy = py + v1 * P.dt;
+        bool out = npx < 0 || npy < 0 || npx >= nx * res || npy >= ny * res;
+        long long rr = clampll(trunc_ll(npy / res), 0, ny - 1);
+        long long cc = clampll(trunc_ll(npx / res), 0, nx - 1);
+        bool blocked = out || lab[rr * nx + cc] == L_OBSTACLE;
+        if (!blocked) {
+          S.pos[ia * 2] = npx;
+          S.pos[ia * 2 + 1] = npy;
+          s_nx[a] = npx;
+          s_ny[a] = npy;
+        }
+        S.vel[ia * 2] = blocked ? 0.0 : v0;
+        S.vel[ia * 2 + 1] = blocked ? 0.0 : v1;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        my_gap = fmin(my_gap, __shfl_xor_sync(0xffffffffu, my_gap, o));
+        my_anynb |= __shfl_xor_sync(0xffffffffu, my_anynb, o);
+        fallbacks += __shfl_xor_sync(0xffffffffu, fallbacks, o);
+        stalls += __shfl_xor_sync(0xffffffffu, stalls, o);
+      }
+    }
+    for (int a = wid; a < A && !lanes; a += NW) {
       if (!s_act[a]) continue;
       const double px = s_px[a], py = s_py[a];
       const size_t ia = eA + a;
@@ -707,9 +895,12 @@ __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S
 }
 
 // ---------------------------------------------------------------- multi-tick run
-// One CTA per env: advance the env tick after tick until it has to wait for its
-// own searches (then park in WAIT) or reaches T; a WAIT env resumes once the
-// server has finished all of that tick's searches (pending == 0).
+// Round CTAs pop ready envs (ring of env ids) and advance each one tick after
+// tick until it has to wait for its own searches (the server re-queues it when
+// the last one finishes), has run `burst` ticks (re-queued at the back), or
+// reaches T; a CTA exits when no env is ready, and the host keeps launching
+// rounds until every env is done.  An env is in the ring at most once, so no
+// two CTAs ever work on the same env.
 template <int NT>
 __global__ void __launch_bounds__(NT) k_round(cw_crowd_params P, cw_crowd_state S,
                                               const double* __restrict__ robot_pos,
@@ -717,56 +908,67 @@ __global__ void __launch_bounds__(NT) k_round(cw_crowd_params P, cw_crowd_state 
                                               const uint8_t* __restrict__ env_mask, Bins bins,
                                               RunArgs ra) {
   extern __shared__ __align__(16) unsigned char sm[];
-  const int e = blockIdx.x;
-  __shared__ int s_st, s_go;
-  if (threadIdx.x == 0) {
-    const int st = ra.env_state[e];
-    int go = (st & 3) != kRunDone;
-    if ((st & 3) == kRunWait) {
-      go = ld_acquire_i32(&ra.pending[e]) == 0;
-      if (go) __threadfence();
-    }
-    s_st = st;
-    s_go = go;
-  }
-  __syncthreads();
-  if (!s_go) return;
-  int t = s_st >> 2;
-  bool guide = (s_st & 3) == kRunGuide;
+  __shared__ int s_e, s_st, s_go;
   while (true) {
-    if (guide) {
-      if (threadIdx.x == 0) {
-        ra.pending[e] = kPendingGuard;   // searches may finish before the count is known
-        __threadfence();
+    if (threadIdx.x == 0) {
+      const int e = ready_pop(ra);
+      s_e = e;
+      if (e >= 0) {
+        __threadfence();   // the server's results (acquire through the ring) before reading state
+        s_st = ra.env_state[e];
       }
-      const int n = guide_env<NT, true>(P, S, e, env_mask, &ra);
-      if (threadIdx.x == 0) {
-        const int left = atomicSub(&ra.pending[e], kPendingGuard - n) - (kPendingGuard - n);
-        if (left) ra.env_state[e] = (t << 2) | kRunWait;
-        else __threadfence();
-        s_go = left == 0;
-      }
-      __syncthreads();
-      if (!s_go) return;
     }
-    orca_env<NT>(P, S, e, robot_pos, robot_vel, robot_radius, env_mask, bins, sm, &ra, t);
     __syncthreads();
-    if (++t == ra.T) {
-      if (threadIdx.x == 0) {
-        ra.env_state[e] = (t << 2) | kRunDone;
-        __threadfence();
-        if (atomicAdd(&ra.q->n_done, 1) + 1 == ra.E) atomicExch(&ra.q->shutdown, 1);
+    const int e = s_e;
+    if (e < 0) return;
+    int t = s_st >> 2;
+    bool guide = (s_st & 3) == kRunGuide;
+    for (int burst = 0;; ++burst) {
+      if (burst == ra.burst) {   // yield to the envs queued behind this one
+        if (threadIdx.x == 0) {
+          ra.env_state[e] = (t << 2) | kRunGuide;
+          __threadfence();
+          ready_push(ra, e);
+        }
+        break;
       }
-      return;
+      if (guide) {
+        if (threadIdx.x == 0) {
+          ra.pending[e] = kPendingGuard;   // searches may finish before the count is known
+          ra.env_state[e] = (t << 2) | kRunWait;
+          __threadfence();
+        }
+        const int n = guide_env<NT, true>(P, S, e, env_mask, &ra);
+        if (threadIdx.x == 0) {
+          const int left = atomicSub(&ra.pending[e], kPendingGuard - n) - (kPendingGuard - n);
+          __threadfence();
+          s_go = left == 0;   // else the server queues the env after its last search
+        }
+        __syncthreads();
+        if (!s_go) break;
+      }
+      orca_env<NT>(P, S, e, robot_pos, robot_vel, robot_radius, env_mask, bins, sm, &ra, t);
+      __syncthreads();
+      if (++t == ra.T) {
+        if (threadIdx.x == 0) {
+          ra.env_state[e] = (t << 2) | kRunDone;
+          __threadfence();
+          if (atomicAdd(&ra.q->n_done, 1) + 1 == ra.E) atomicExch(&ra.q->shutdown, 1);
+        }
+        break;
+      }
+      guide = true;
     }
-    guide = true;
+    __syncthreads();
   }
 }
 
 __global__ void k_run_init(RunArgs ra) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i == 0) *ra.q = RunQueue{0ull, 0ull, 0, 0, 0, 0};
-  if (i < (size_t)ra.E) { ra.env_state[i] = 0; ra.pending[i] = 0; }
+  // every env starts in the ready ring (positions 0..E-1)
+  if (i == 0) *ra.q = RunQueue{0ull, 0ull, 0, 0, 0, 0, 0ull, (unsigned long long)ra.E};
+  if (i < (size_t)ra.E) { ra.env_state[i] = 0; ra.pending[i] = 0; ra.ritems[i] = (int)i; }
+  if (i <= ra.rmask) ra.rseq[i] = i < (size_t)ra.E ? i + 1 : i;
   if (i < (size_t)ra.T) ra.anynb[i] = 0;
   if (i <= ra.mask) ra.seq[i] = i;
 }
@@ -832,8 +1034,8 @@ static void launch_astar(const cw_crowd_params& P, const cw_crowd_state& S, cuda
 
 // ---- cw_crowd_run scratch layout
 struct RunLayout {
-  unsigned long long cap;
-  size_t q, env_state, pending, seq, items, gap_hist, anynb, total;
+  unsigned long long cap, rcap;
+  size_t q, env_state, pending, seq, items, rseq, ritems, gap_hist, anynb, total;
 };
 
 static RunLayout run_layout(int E, int A, int T) {
@@ -847,11 +1049,18 @@ static RunLayout run_layout(int E, int A, int T) {
   L.pending = L.env_state + up((size_t)E * 4);
   L.seq = L.pending + up((size_t)E * 4);
   L.items = L.seq + up((size_t)cap * 8);
-  L.gap_hist = L.items + up((size_t)cap * sizeof(AstarReq));
+  unsigned long long rcap = 1024;
+  while (rcap < (unsigned long long)E) rcap <<= 1;
+  L.rcap = rcap;
+  L.rseq = L.items + up((size_t)cap * sizeof(AstarReq));
+  L.ritems = L.rseq + up((size_t)rcap * 8);
+  L.gap_hist = L.ritems + up((size_t)rcap * 4);
   L.anynb = L.gap_hist + up((size_t)E * T * 8);
   L.total = L.anynb + up((size_t)T * 4);
   return L;
 }
+
+constexpr int kRoundStreams = 8;   // max; CW_RUN_STREAMS picks how many are used
 
 template <int NT>
 static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const double* rp,
@@ -864,6 +1073,13 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
     cudaFuncSetAttribute(k_astar<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     // the server and the rounds share SMs only under one L1 / shared split
     cudaFuncSetAttribute(k_astar<1, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(k_astar<kAstarWarps, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    cudaFuncSetAttribute(k_astar<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_astar<2, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(k_astar<kAstarWarps, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          (int)cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(k_round<NT>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          (int)cudaSharedmemCarveoutMaxShared);
@@ -879,19 +1095,24 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
   ra.pending = reinterpret_cast<int*>(base + L.pending);
   ra.seq = reinterpret_cast<unsigned long long*>(base + L.seq);
   ra.items = reinterpret_cast<AstarReq*>(base + L.items);
+  ra.rseq = reinterpret_cast<unsigned long long*>(base + L.rseq);
+  ra.ritems = reinterpret_cast<int*>(base + L.ritems);
+  ra.rmask = L.rcap - 1;
   ra.gap_hist = reinterpret_cast<double*>(base + L.gap_hist);
   ra.anynb = reinterpret_cast<int*>(base + L.anynb);
   ra.T = ticks;
   ra.E = P.E;
   ra.mask = L.cap - 1;
-  const size_t n_init = std::max<size_t>(std::max<size_t>(P.E, ticks), L.cap);
+  static const int burst = getenv("CW_RUN_BURST") ? atoi(getenv("CW_RUN_BURST")) : 2;
+  ra.burst = std::max(1, burst);
+  const size_t n_init = std::max<size_t>(std::max<size_t>(std::max<size_t>(P.E, ticks), L.cap), L.rcap);
   k_run_init<<<(unsigned)((n_init + 255) / 256), 256, 0, st>>>(ra);
 
   struct Host {
     int* poll = nullptr;       // pinned: 8 x {n_done, shutdown, error, pad}
     int* one = nullptr;
-    cudaEvent_t ev[8], start, srv_done, rounds_done;
-    cudaStream_t copy;
+    cudaEvent_t ev[8], start, srv_done, rounds_done[kRoundStreams];
+    cudaStream_t copy, rs[kRoundStreams];
   };
   static Host H;
   if (!H.poll) {
@@ -901,34 +1122,59 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
     for (auto& ev : H.ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&H.start, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&H.srv_done, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&H.rounds_done, cudaEventDisableTiming);
+    int least, greatest;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    for (int k = 0; k < kRoundStreams; ++k) {
+      cudaEventCreateWithFlags(&H.rounds_done[k], cudaEventDisableTiming);
+      cudaStreamCreateWithPriority(&H.rs[k], cudaStreamNonBlocking, least);
+    }
     cudaStreamCreateWithFlags(&H.copy, cudaStreamNonBlocking);
   }
   TickStreams& TS = tick_streams();
   cudaEventRecord(H.start, st);
   cudaStreamWaitEvent(TS.hi, H.start, 0);
-  cudaStreamWaitEvent(TS.lo, H.start, 0);
-  const AstarShape shp = astar_shape(P.nx, P.ny, 1);
-  int srv_ctas = P.astar_ctas;
+  for (int k = 0; k < kRoundStreams; ++k) cudaStreamWaitEvent(H.rs[k], H.start, 0);
+  // The server leaves some SMs without a search CTA, so round CTAs always have
+  // somewhere to run whatever their register / shared-memory footprint (the
+  // server's warps wait on the rounds' requests: they must never starve them).
+  // two search warps per CTA: twice the concurrent searches of the latency shape
+  // at nearly its per-expansion cost (the run is bound by each env's own chain)
+  static const int srv_w = getenv("CW_RUN_SERVER_W") ? atoi(getenv("CW_RUN_SERVER_W")) : 2;
+  static const int srv_kb = getenv("CW_RUN_SERVER_KB") ? atoi(getenv("CW_RUN_SERVER_KB")) : 0;
+  const AstarShape shp = astar_shape(P.nx, P.ny, srv_w == 4 ? kAstarWarps : srv_w == 2 ? 2 : 1, srv_kb);
+  static const int margin = getenv("CW_RUN_MARGIN") ? atoi(getenv("CW_RUN_MARGIN")) : 0;
+  int srv_ctas = P.astar_ctas - std::max(4, margin > 0 ? margin : P.astar_ctas / 8);
   if (const char* v = getenv("CW_RUN_SERVER_CTAS")) srv_ctas = std::min(srv_ctas, atoi(v));
-  k_astar<1, true><<<srv_ctas, 32, shp.smem, TS.hi>>>(P, S, shp.NC, shp.NS, ra);
+  srv_ctas = std::max(srv_ctas, 1);
+  if (srv_w == 4)
+    k_astar<kAstarWarps, true><<<srv_ctas, 32 * kAstarWarps, shp.smem, TS.hi>>>(P, S, shp.NC, shp.NS, ra);
+  else if (srv_w == 2)
+    k_astar<2, true><<<srv_ctas, 64, shp.smem, TS.hi>>>(P, S, shp.NC, shp.NS, ra);
+  else
+    k_astar<1, true><<<srv_ctas, 32, shp.smem, TS.hi>>>(P, S, shp.NC, shp.NS, ra);
   cudaEventRecord(H.srv_done, TS.hi);
   int err = (int)cudaGetLastError();
   const auto t_begin = std::chrono::steady_clock::now();
-  constexpr int kInFlight = 6;
+  static const int n_rs = std::min(kRoundStreams, std::max(1, getenv("CW_RUN_STREAMS") ? atoi(getenv("CW_RUN_STREAMS")) : 4));
+  static const int kInFlight = std::min(7, std::max(1, getenv("CW_RUN_INFLIGHT") ? atoi(getenv("CW_RUN_INFLIGHT")) : 6));
   static const bool debug = getenv("CW_RUN_DEBUG") != nullptr;
   int status = 0;
+  long long n_rounds = 0;
+  static const int rpm = getenv("CW_RUN_ROUND_CTAS_PER_SM") ? atoi(getenv("CW_RUN_ROUND_CTAS_PER_SM")) : 4;
+  const int round_ctas = std::max(1, std::min(P.E, P.astar_ctas * rpm));
   for (long long i = 0;; ++i) {
-    k_round<NT><<<P.E, NT, sm, TS.lo>>>(P, S, rp, rv, rr, em, bins, ra);
-    cudaMemcpyAsync(H.poll + (i & 7) * 8, ra.q, 32, cudaMemcpyDeviceToHost, TS.lo);
-    cudaEventRecord(H.ev[i & 7], TS.lo);
+    n_rounds = i + 1;
+    cudaStream_t rs = H.rs[i % n_rs];
+    k_round<NT><<<round_ctas, NT, sm, rs>>>(P, S, rp, rv, rr, em, bins, ra);
+    cudaMemcpyAsync(H.poll + (i & 7) * 8, ra.q, 32, cudaMemcpyDeviceToHost, rs);
+    cudaEventRecord(H.ev[i & 7], rs);
     if (i >= kInFlight) {
       const long long j = i - kInFlight;
       cudaEventSynchronize(H.ev[j & 7]);
       const int* pv = H.poll + (j & 7) * 8 + 4;   // n_done, shutdown, error
       if (debug && (j % 2000 == 0 || pv[2])) {
-        if (j == 0) fprintf(stderr, "server smem %d NC %d NS %d ctas %d round smem %zu\n", shp.smem, shp.NC,
-                            shp.NS, srv_ctas, sm);
+        if (j == 0) fprintf(stderr, "server smem %zu NC %d NS %d ctas %d round smem %zu\n", shp.smem,
+                            shp.NC, shp.NS, srv_ctas, sm);
         const unsigned long long* hq = reinterpret_cast<const unsigned long long*>(pv - 4);
         fprintf(stderr, "cw_crowd_run round %lld: head %llu tail %llu done %d/%d shutdown %d error %d\n",
                 j, hq[0], hq[1], pv[0], P.E, pv[1], pv[2]);
@@ -943,10 +1189,14 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
     cudaMemcpyAsync(&ra.q->shutdown, H.one, 4, cudaMemcpyHostToDevice, H.copy);
     cudaStreamSynchronize(H.copy);
   }
-  cudaStreamWaitEvent(TS.lo, H.srv_done, 0);
-  k_run_finish<<<1, 256, 0, TS.lo>>>(S, ra);
-  cudaEventRecord(H.rounds_done, TS.lo);
-  cudaStreamWaitEvent(st, H.rounds_done, 0);
+  for (int k = 1; k < kRoundStreams; ++k) {
+    cudaEventRecord(H.rounds_done[k], H.rs[k]);
+    cudaStreamWaitEvent(H.rs[0], H.rounds_done[k], 0);
+  }
+  cudaStreamWaitEvent(H.rs[0], H.srv_done, 0);
+  k_run_finish<<<1, 256, 0, H.rs[0]>>>(S, ra);
+  cudaEventRecord(H.rounds_done[0], H.rs[0]);
+  cudaStreamWaitEvent(st, H.rounds_done[0], 0);
   if (status) return status;
   return (int)cudaGetLastError();
 }
@@ -1015,6 +1265,8 @@ int cw_crowd_run(const cw_crowd_params* P, const cw_crowd_state* S, const double
   if (P->E <= 0 || P->A <= 0 || ticks <= 0) return 0;
   if (!scratch) return (int)cudaErrorInvalidValue;
   cudaStream_t st = (cudaStream_t)stream;
+  if (threads == 32)
+    return launch_run<32>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, ticks, scratch, st);
   if (threads == 256)
     return launch_run<256>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, ticks, scratch, st);
   if (threads == 64)

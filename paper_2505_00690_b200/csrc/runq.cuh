@@ -16,15 +16,16 @@
 
 namespace cw {
 
-enum { kRunGuide = 0, kRunWait = 1, kRunDone = 3 };
+enum { kRunGuide = 0, kRunWait = 1, kRunDone = 3, kRunBusy = 1 << 30 };
 constexpr int kPendingGuard = 1 << 24;   // > any per-env request count
 constexpr long long kSpinCycles = 8ll << 30;    // ~4.5 s: a full ring slot is an error, not a hang
 constexpr long long kIdleCycles = 64ll << 30;   // ~35 s backstop for an idle server warp (the
                                                 // host normally ends the run via q->shutdown)
 
 struct RunQueue {                 // device-resident control words
-  unsigned long long head, tail;  // ring positions claimed by consumers / producers
+  unsigned long long head, tail;  // search ring positions claimed by consumers / producers
   int n_done, shutdown, error, pad;
+  unsigned long long rhead, rtail;  // ready-env ring
 };
 
 struct RunArgs {                  // kernel parameter (pointers into cw_crowd_run scratch)
@@ -33,11 +34,21 @@ struct RunArgs {                  // kernel parameter (pointers into cw_crowd_ru
   int* pending;                   // outstanding searches of the env's current tick
   unsigned long long* seq;        // ring slot sequence numbers (Vyukov bounded MPMC)
   AstarReq* items;
+  unsigned long long* rseq;       // ready-env ring (each env is in it at most once)
+  int* ritems;
+  unsigned long long rmask;
   double* gap_hist;               // (E, T) per-tick gap of every env
   int* anynb;                     // (T) some env had K > 0 at tick t
   int T, E;
+  int burst;                      // ticks one round CTA may run back to back (bounds round length)
   unsigned long long mask;        // ring capacity - 1 (power of two)
 };
+
+CW_DEV long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 CW_DEV unsigned long long ld_acquire_u64(const unsigned long long* p) {
   unsigned long long v;
@@ -46,6 +57,9 @@ CW_DEV unsigned long long ld_acquire_u64(const unsigned long long* p) {
 }
 CW_DEV void st_release_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+CW_DEV void st_release_i32(int* p, int v) {
+  asm volatile("st.release.gpu.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 CW_DEV int ld_acquire_i32(const int* p) {
   int v;
@@ -63,6 +77,39 @@ CW_DEV void ring_push(const RunArgs& ra, const AstarReq& R) {
   }
   ra.items[pos & ra.mask] = R;
   st_release_u64(sq, pos + 1);
+}
+
+// ready ring: push (blocking, never full: capacity >= E) / non-blocking pop
+CW_DEV void ready_push(const RunArgs& ra, int e) {
+  const unsigned long long pos = atomicAdd(&ra.q->rtail, 1ull);
+  unsigned long long* sq = ra.rseq + (pos & ra.rmask);
+  const long long t0 = clock64();
+  while (ld_acquire_u64(sq) != pos) {
+    if (clock64() - t0 > kSpinCycles) { atomicCAS(&ra.q->error, 0, 3); return; }
+  }
+  ra.ritems[pos & ra.rmask] = e;
+  st_release_u64(sq, pos + 1);
+}
+
+CW_DEV int ready_pop(const RunArgs& ra) {   // -1: empty right now
+  unsigned long long pos = *(volatile unsigned long long*)&ra.q->rhead;
+  while (true) {
+    unsigned long long* sq = ra.rseq + (pos & ra.rmask);
+    const long long dif = (long long)(ld_acquire_u64(sq) - (pos + 1));
+    if (dif == 0) {
+      const unsigned long long old = atomicCAS(&ra.q->rhead, pos, pos + 1);
+      if (old == pos) {
+        const int e = *(volatile int*)&ra.ritems[pos & ra.rmask];
+        st_release_u64(sq, pos + ra.rmask + 1);
+        return e;
+      }
+      pos = old;
+    } else if (dif < 0) {
+      return -1;
+    } else {
+      pos = *(volatile unsigned long long*)&ra.q->rhead;
+    }
+  }
 }
 
 // consumer (lane 0 of a server warp): false on shutdown / error

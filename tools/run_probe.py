@@ -42,7 +42,9 @@ rpos = torch.stack([((cell % nx).double() + 0.5) * CFG["res"],
 rvel = torch.zeros_like(rpos)
 fields = []
 for _ in range(2):
-    f = CrowdField(b, CrowdConfig(neighbor_distance=CFG["nd"]), run_seeds, device=dev)
+    f = CrowdField(b, CrowdConfig(neighbor_distance=CFG["nd"]), run_seeds, device=dev,
+                   threads=int(os.environ.get("PROBE_THREADS", 128)))
+    f.run_threads = int(os.environ["PROBE_RUN_THREADS"]) if "PROBE_RUN_THREADS" in os.environ else None
     f.set_from_spawn(b)
     f.prepare_step()
     for _ in range(20):
@@ -61,6 +63,7 @@ sync_ms = e0.elapsed_time(e1) / T
 h.run(1, rpos, rvel, 0.35)   # warm the run path (first-call attributes)
 torch.cuda.synchronize()
 f.step(rpos, rvel, 0.35, check=False)
+h.counters_t.zero_()
 e0.record(st)
 h.run(T, rpos, rvel, 0.35)
 e1.record(st)
@@ -68,5 +71,9 @@ torch.cuda.synchronize()
 run_ms = e0.elapsed_time(e1) / T
 same = all(np.array_equal(getattr(f, k).cpu().numpy(), getattr(h, k).cpu().numpy())
            for k in ("pos_t", "vel_t", "goal_t", "waypoint_t", "path_n_t", "last_gap_t"))
+c = h.counters_t.cpu().numpy()
+clk = 1.92e6   # cycles per ms (approx. boost clock)
+print(f"  run: expansions {c[0]:,} search warp-cycles {c[4]/1e6:.0f}M (= {c[4]/clk/T:.2f} warp-ms/tick), "
+      f"max search {c[5]/1e6:.1f}M cyc, orca CTA-cycles {c[6]/1e6:.0f}M (= {c[6]/clk/T:.2f} CTA-ms/tick)")
 print(f"{cfgname} E={E} T={T}: sync {sync_ms:.3f} ms/tick ({E / sync_ms * 1e3:,.0f} env-steps/s); "
       f"run {run_ms:.3f} ms/tick ({E / run_ms * 1e3:,.0f} env-steps/s); identical={same}")
