@@ -395,6 +395,7 @@ struct SearchEnv {
   uint8_t* mtg;          // global, this warp: NT x 64 move bytes
   int32_t* parent;       // global, this warp: N
   int32_t* s2t;          // global, this warp: allocation k -> slot << 16 | tile
+  long long* trace;      // debug (counters[15]): expanded cell + f bits of one search
 };
 
 // Take n slots from the CTA pool (lane 0; false if it holds fewer).
@@ -511,6 +512,10 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
     const int sy0 = (int)E.tmap[ty];
     int sy = legal ? sy0 : (int)kNoSlot;
     const double hh = octile(rr, cc, gr, gc);
+    if (E.trace && lane == 0 && s_exp < (1u << 20)) {
+      E.trace[2 * s_exp] = x;
+      E.trace[2 * s_exp + 1] = __double_as_longlong(gx);
+    }
     if (x == goal) { found = 1; break; }
     // No stale test (paths.py:70-71) is needed here: the head never holds a
     // stale entry (refills drop them, decrease-keys evict the old head copy),
@@ -581,6 +586,19 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
           st.h -= 1;
         }
       }
+      if (!klt(v, st.T)) {
+        // an eviction earlier in this loop lowered T to or below v: v now
+        // belongs to the pools (the head must stay below every pool key)
+        const bool vn = klt(v, st.F2);
+        if (lane == 0) {
+          OpenEnt o = {v.f, v.k};
+          if (vn) pl.near[st.nn] = o;
+          else pl.far[st.nf] = o;
+        }
+        st.nn += vn;
+        st.nf += !vn;
+        continue;
+      }
       const Key up = shfl_key_up(st.hd, 1);
       const int p = __popc(__ballot_sync(0xffffffffu, klt(st.hd, v)));   // +inf beyond h
       if (st.h == 32) {
@@ -639,6 +657,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
   pl.far = reinterpret_cast<OpenEnt*>(S.astar_heap) + (size_t)gw * P.heap_cap;
   pl.NC = NC;
   pl.far_cap = P.heap_cap;
+
   E.tmap = reinterpret_cast<uint16_t*>(pl.stg + 64);
   unsigned char* const pool = sm + (size_t)W * shp.per_warp;
   E.pool_lock = reinterpret_cast<int*>(pool);
@@ -658,6 +677,8 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
   __syncthreads();
   long long* const dbg = (!kRing && S.counters && S.counters[14])
                              ? reinterpret_cast<long long*>(S.counters[14]) : nullptr;
+  long long* const trace = (!kRing && S.counters && S.counters[15])
+                               ? reinterpret_cast<long long*>(S.counters[15]) : nullptr;
   long long t_max = 0, t_sum = 0;
   unsigned long long n_exp = 0, n_glob = 0;
   double delta = 1.0, delta2 = 4.0;   // adaptive band widths, carried across searches
@@ -679,6 +700,8 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
       R = reqs[q];
     }
     const long long t0 = clock64();
+    E.trace = (trace && q == 0) ? trace : nullptr;
+
     const int e = R.env;
     const uint8_t* mvt = S.moves + (size_t)e * N;
     const uint8_t* lab = S.labels + (size_t)e * N;

@@ -69,8 +69,15 @@ h.run(T, rpos, rvel, 0.35)
 e1.record(st)
 torch.cuda.synchronize()
 run_ms = e0.elapsed_time(e1) / T
-same = all(np.array_equal(getattr(f, k).cpu().numpy(), getattr(h, k).cpu().numpy())
-           for k in ("pos_t", "vel_t", "goal_t", "waypoint_t", "path_n_t", "last_gap_t"))
+same = True
+for k in ("pos_t", "vel_t", "goal_t", "waypoint_t", "path_n_t", "last_gap_t"):
+    x, y = getattr(f, k).cpu().numpy(), getattr(h, k).cpu().numpy()
+    if not np.array_equal(x, y):
+        same = False
+        bad = np.argwhere(x != y)
+        envs = np.unique(bad[:, 0]) if bad.ndim > 1 and bad.shape[1] > 0 else bad
+        print(f"  MISMATCH {k}: {len(bad)} entries, envs {envs[:10]} (of {len(envs)})")
+print("  flags sync", f.flags_t.cpu().numpy()[:2], "run", h.flags_t.cpu().numpy()[:2])
 c = h.counters_t.cpu().numpy()
 clk = 1.92e6   # cycles per ms (approx. boost clock)
 print(f"  run: expansions {c[0]:,} search warp-cycles {c[4]/1e6:.0f}M (= {c[4]/clk/T:.2f} warp-ms/tick), "
