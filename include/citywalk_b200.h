@@ -194,6 +194,9 @@ int cw_crowd_step_phases(const cw_crowd_params* params, const cw_crowd_state* st
  * scratch: cw_crowd_run_scratch_bytes(E, A, ticks) bytes of device memory.
  * Returns 0, a CUDA error, 9001 (device queue error) or 9002 (host time limit). */
 size_t cw_crowd_run_scratch_bytes(int E, int A, int ticks);
+/* Round kernels the last cw_crowd_run launched (host-only query; the run also
+ * launches one init, one search-server and one finish kernel). */
+long long cw_crowd_run_rounds(void);
 int cw_crowd_run(const cw_crowd_params* params, const cw_crowd_state* state,
                  const double* robot_pos, const double* robot_vel, double robot_radius,
                  const uint8_t* env_mask, int threads, int ticks, void* scratch, void* stream);

@@ -328,77 +328,141 @@ __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
   const double res = P.res;
   long long scanned = 0;
   AstarReq* reqs = reinterpret_cast<AstarReq*>(S.astar_req);
-  // one agent per thread: every decision below is a boolean (near the path,
-  // line of sight clear), so each lane stops its scans at the first hit
-  for (int a = threadIdx.x; a < A; a += NT) {
+  // Every decision below is a boolean (near the path: min distance <= 1 m,
+  // field.py:190; line of sight clear), so scans stop at the first hit.
+  // Phase A, one lane per agent: waypoint pop + the first kLaneSegs segments.
+  // Phase B, the whole warp per deferred agent: the rest of the polyline and
+  // the line-of-sight samples, 32 at a time (the original warp-parallel scans).
+  constexpr int kLaneSegs = 8;
+  const int A_pad = (A + 31) & ~31;   // whole warps iterate together (ballots below)
+  for (int a0 = threadIdx.x - lane; a0 < A_pad; a0 += NT) {
+    const int a = a0 + lane;
     const size_t ia = eA + a;
-    if (!S.active[ia]) continue;
-    const double gx = S.goal[ia * 2], gy = S.goal[ia * 2 + 1];
-    if (!has_obs) {
-      S.waypoint[ia * 2] = gx;
-      S.waypoint[ia * 2 + 1] = gy;
-      continue;
-    }
-    const double px = S.pos[ia * 2], py = S.pos[ia * 2 + 1];
-    int32_t* cells = S.path_cells + ia * P.path_cap;
-    int head = S.path_head[ia], n = S.path_n[ia];
-    if (n > 0) {
-      double qx, qy;
-      path_point(cells, head, n, 0, gx, gy, res, nx, qx, qy);
-      if (glibc_hypot(qx - px, qy - py) < kWaypointReach && n > 1) { ++head; --n; }
-      // _distance_to_polyline (field.py:613-625) <= kStrayLimit (field.py:190)
-      path_point(cells, head, n, 0, gx, gy, res, nx, qx, qy);
-      bool near = glibc_hypot(qx - px, qy - py) <= kStrayLimit;
-      double bx = qx, by = qy;
-      for (int k = 1; k < n && !near; ++k) {
-        const double ax = bx, ay = by;
-        path_point(cells, head, n, k, gx, gy, res, nx, bx, by);
-        double abx = bx - ax, aby = by - ay;
-        double den = dot2_blas(abx, aby, abx, aby);
-        double t = 0.0;
-        if (!(den < kEps)) t = fmin(fmax(dot2_blas(px - ax, py - ay, abx, aby) / den, 0.0), 1.0);
-        near = glibc_hypot(ax + t * abx - px, ay + t * aby - py) <= kStrayLimit;
+    int need = 0;            // 1: continue the polyline scan at segment kLaneSegs + 1; 2: line of sight
+    int head = 0, n = 0;
+    double px = 0.0, py = 0.0, gx = 0.0, gy = 0.0;
+    if (a < A && S.active[ia]) {
+      gx = S.goal[ia * 2];
+      gy = S.goal[ia * 2 + 1];
+      if (!has_obs) {
+        S.waypoint[ia * 2] = gx;
+        S.waypoint[ia * 2 + 1] = gy;
+      } else {
+        px = S.pos[ia * 2];
+        py = S.pos[ia * 2 + 1];
+        const int32_t* cells = S.path_cells + ia * P.path_cap;
+        head = S.path_head[ia];
+        n = S.path_n[ia];
+        need = 2;
+        if (n > 0) {
+          double qx, qy;
+          path_point(cells, head, n, 0, gx, gy, res, nx, qx, qy);
+          if (glibc_hypot(qx - px, qy - py) < kWaypointReach && n > 1) { ++head; --n; }
+          path_point(cells, head, n, 0, gx, gy, res, nx, qx, qy);
+          bool near = glibc_hypot(qx - px, qy - py) <= kStrayLimit;
+          double bx = qx, by = qy;
+          const int kend = min(n, kLaneSegs + 1);
+          for (int k = 1; k < kend && !near; ++k) {
+            const double ax = bx, ay = by;
+            path_point(cells, head, n, k, gx, gy, res, nx, bx, by);
+            double abx = bx - ax, aby = by - ay;
+            double den = dot2_blas(abx, aby, abx, aby);
+            double t = 0.0;
+            if (!(den < kEps)) t = fmin(fmax(dot2_blas(px - ax, py - ay, abx, aby) / den, 0.0), 1.0);
+            near = glibc_hypot(ax + t * abx - px, ay + t * aby - py) <= kStrayLimit;
+          }
+          scanned += n;   // the reference scans every remaining point (traffic model)
+          if (near) {
+            S.path_head[ia] = head;
+            S.path_n[ia] = n;
+            S.waypoint[ia * 2] = qx;
+            S.waypoint[ia * 2 + 1] = qy;
+            need = 0;
+          } else if (n > kLaneSegs + 1) {
+            need = 1;
+          }
+        }
       }
-      scanned += n;   // the reference scans every remaining point (traffic model)
-      if (near) {
-        S.path_head[ia] = head;
-        S.path_n[ia] = n;
-        S.waypoint[ia * 2] = qx;
-        S.waypoint[ia * 2 + 1] = qy;
-        continue;
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, need != 0);
+    while (todo) {
+      const int s = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int sa = a0 + s;
+      const size_t sia = eA + sa;
+      const int sneed = __shfl_sync(0xffffffffu, need, s);
+      const int shead = __shfl_sync(0xffffffffu, head, s), sn = __shfl_sync(0xffffffffu, n, s);
+      const double spx = __shfl_sync(0xffffffffu, px, s), spy = __shfl_sync(0xffffffffu, py, s);
+      const double sgx = __shfl_sync(0xffffffffu, gx, s), sgy = __shfl_sync(0xffffffffu, gy, s);
+      if (sneed == 1) {   // segments kLaneSegs + 1 .. n - 1, 32 per step
+        const int32_t* cells = S.path_cells + sia * P.path_cap;
+        bool near = false;
+        for (int k0 = kLaneSegs + 1; k0 < sn && !near; k0 += 32) {
+          const int k = k0 + lane;
+          bool mine = false;
+          if (k < sn) {
+            double ax, ay, bx, by;
+            path_point(cells, shead, sn, k - 1, sgx, sgy, res, nx, ax, ay);
+            path_point(cells, shead, sn, k, sgx, sgy, res, nx, bx, by);
+            double abx = bx - ax, aby = by - ay;
+            double den = dot2_blas(abx, aby, abx, aby);
+            double t = 0.0;
+            if (!(den < kEps)) t = fmin(fmax(dot2_blas(spx - ax, spy - ay, abx, aby) / den, 0.0), 1.0);
+            mine = glibc_hypot(ax + t * abx - spx, ay + t * aby - spy) <= kStrayLimit;
+          }
+          near = __any_sync(0xffffffffu, mine);
+        }
+        if (near) {
+          if (lane == 0) {
+            double wx, wy;
+            path_point(cells, shead, sn, 0, sgx, sgy, res, nx, wx, wy);
+            S.path_head[sia] = shead;
+            S.path_n[sia] = sn;
+            S.waypoint[sia * 2] = wx;
+            S.waypoint[sia * 2 + 1] = wy;
+          }
+          continue;
+        }
+      }
+      // _line_of_sight (field.py:601-610), 32 samples per step
+      double d = glibc_hypot(sgx - spx, sgy - spy);
+      long long ns = max(2LL, trunc_ll(2.0 * d / res) + 2);
+      double step = 1.0 / (double)(ns - 1);
+      bool clear = true;
+      for (long long k0 = 0; k0 < ns && clear; k0 += 32) {
+        const long long k = k0 + lane;
+        bool blocked = false;
+        if (k < ns) {
+          double t = k == ns - 1 ? 1.0 : (double)k * step + 0.0;
+          double xs = spx + (sgx - spx) * t, ys = spy + (sgy - spy) * t;
+          long long rr = clampll(trunc_ll(ys / res), 0, ny - 1);
+          long long cc = clampll(trunc_ll(xs / res), 0, nx - 1);
+          blocked = lab[rr * nx + cc] == L_OBSTACLE;
+        }
+        clear = !__any_sync(0xffffffffu, blocked);
+      }
+      if (lane == 0) {
+        if (clear) {
+          S.path_head[sia] = 0;
+          S.path_n[sia] = 1;
+          S.waypoint[sia * 2] = sgx;
+          S.waypoint[sia * 2 + 1] = sgy;
+        } else {
+          int sr = (int)fmin(fmax(spy / res, 0.0), (double)(ny - 1));
+          int sc = (int)fmin(fmax(spx / res, 0.0), (double)(nx - 1));
+          int gr = (int)fmin(fmax(sgy / res, 0.0), (double)(ny - 1));
+          int gc = (int)fmin(fmax(sgx / res, 0.0), (double)(nx - 1));
+          AstarReq R = {e, sa, sr * nx + sc, gr * nx + gc};
+          if (kRing) {
+            ring_push(*ra, R);
+          } else {
+            int q = atomicAdd(&S.flags[4], 1);
+            reqs[q] = R;
+          }
+          ++my_req;
+        }
       }
     }
-    // _line_of_sight (field.py:601-610)
-    double d = glibc_hypot(gx - px, gy - py);
-    long long ns = max(2LL, trunc_ll(2.0 * d / res) + 2);
-    double step = 1.0 / (double)(ns - 1);
-    bool clear = true;
-    for (long long k = 0; k < ns && clear; ++k) {
-      double t = k == ns - 1 ? 1.0 : (double)k * step + 0.0;
-      double xs = px + (gx - px) * t, ys = py + (gy - py) * t;
-      long long rr = clampll(trunc_ll(ys / res), 0, ny - 1);
-      long long cc = clampll(trunc_ll(xs / res), 0, nx - 1);
-      clear = lab[rr * nx + cc] != L_OBSTACLE;
-    }
-    if (clear) {
-      S.path_head[ia] = 0;
-      S.path_n[ia] = 1;
-      S.waypoint[ia * 2] = gx;
-      S.waypoint[ia * 2 + 1] = gy;
-      continue;
-    }
-    int sr = (int)fmin(fmax(py / res, 0.0), (double)(ny - 1));
-    int sc = (int)fmin(fmax(px / res, 0.0), (double)(nx - 1));
-    int gr = (int)fmin(fmax(gy / res, 0.0), (double)(ny - 1));
-    int gc = (int)fmin(fmax(gx / res, 0.0), (double)(nx - 1));
-    AstarReq R = {e, a, sr * nx + sc, gr * nx + gc};
-    if (kRing) {
-      ring_push(*ra, R);
-    } else {
-      int q = atomicAdd(&S.flags[4], 1);
-      reqs[q] = R;
-    }
-    ++my_req;
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -444,7 +508,7 @@ CW_HD size_t bins_smem_bytes(const Bins& b, int A) {
 // ORCA + commit + goal resample of env e (body of k_orca and k_round).  With
 // ra != nullptr the env's gap goes to the run history at ``tick`` instead of
 // gap_tmp / flags[0].
-template <int NT>
+template <int NT, bool kLanes>
 __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int e,
                          const double* __restrict__ robot_pos, const double* __restrict__ robot_vel,
                          double robot_radius, const uint8_t* __restrict__ env_mask, const Bins& bins,
@@ -534,7 +598,7 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
     double my_gap = CUDART_INF;
     int my_anynb = 0;
     long long fallbacks = 0, stalls = 0;
-    const bool lanes = bins.ncx == 0 && P.max_neighbors <= MAXK;
+    const bool lanes = kLanes && bins.ncx == 0 && P.max_neighbors <= MAXK;
     if (lanes) {
       // ---------------- lane per agent (A < 128): same operations as the warp path
       const int kmax = min(P.max_neighbors, max(A - 1, 0));
@@ -875,7 +939,7 @@ __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S
   // pass 0: every env; pass 1: envs without A* requests (runs beside k_astar);
   // pass 2: envs with requests (after k_astar).  The body is per env.
   const bool skip = (pass == 1 && S.env_req[e]) || (pass == 2 && !S.env_req[e]);
-  if (!skip) orca_env<NT>(P, S, e, robot_pos, robot_vel, robot_radius, env_mask, bins, sm, nullptr, 0);
+  if (!skip) orca_env<NT, false>(P, S, e, robot_pos, robot_vel, robot_radius, env_mask, bins, sm, nullptr, 0);
   // ---------------- last CTA: publish last_gap_by_env (only when some row had K > 0),
   // reset the per-step flags and the A* queue
   if (threadIdx.x == 0) {
@@ -947,7 +1011,7 @@ __global__ void __launch_bounds__(NT) k_round(cw_crowd_params P, cw_crowd_state 
         __syncthreads();
         if (!s_go) break;
       }
-      orca_env<NT>(P, S, e, robot_pos, robot_vel, robot_radius, env_mask, bins, sm, &ra, t);
+      orca_env<NT, true>(P, S, e, robot_pos, robot_vel, robot_radius, env_mask, bins, sm, &ra, t);
       __syncthreads();
       if (++t == ra.T) {
         if (threadIdx.x == 0) {
@@ -1060,7 +1124,8 @@ static RunLayout run_layout(int E, int A, int T) {
   return L;
 }
 
-constexpr int kRoundStreams = 8;   // max; CW_RUN_STREAMS picks how many are used
+constexpr int kRoundStreams = 8;
+static long long g_last_rounds = 0;   // rounds launched by the last cw_crowd_run   // max; CW_RUN_STREAMS picks how many are used
 
 template <int NT>
 static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const double* rp,
@@ -1185,6 +1250,7 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
       if (secs > 300.0 || (err = (int)cudaGetLastError()) != 0) { status = err ? err : 9002; break; }
     }
   }
+  g_last_rounds = n_rounds;
   if (status) {   // end the server through the copy engine (no SM needed)
     cudaMemcpyAsync(&ra.q->shutdown, H.one, 4, cudaMemcpyHostToDevice, H.copy);
     cudaStreamSynchronize(H.copy);
@@ -1255,6 +1321,9 @@ int cw_astar_warps(void) { return cw::kAstarWarps; }
 size_t cw_crowd_run_scratch_bytes(int E, int A, int ticks) {
   return cw::run_layout(E, A, ticks).total;
 }
+
+// Round kernels launched by the last cw_crowd_run (host-only query).
+long long cw_crowd_run_rounds(void) { return cw::g_last_rounds; }
 
 // `ticks` synchronous cw_crowd_step calls with the same inputs, run without a
 // per-tick barrier (runq.cuh); same final state bit for bit.
