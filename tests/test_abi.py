@@ -11,7 +11,7 @@ from conftest import ROOT
 def _declared():
     with open(os.path.join(ROOT, "include", "citywalk_b200.h")) as fh:
         text = fh.read()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t)\s+(cw_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|long long)\s+(cw_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_the_exports():
