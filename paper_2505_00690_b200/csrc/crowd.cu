@@ -965,7 +965,7 @@ __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S
 // reaches T; a CTA exits when no env is ready, and the host keeps launching
 // rounds until every env is done.  An env is in the ring at most once, so no
 // two CTAs ever work on the same env.
-template <int NT>
+template <int NT, bool kLanes>
 __global__ void __launch_bounds__(NT) k_round(cw_crowd_params P, cw_crowd_state S,
                                               const double* __restrict__ robot_pos,
                                               const double* __restrict__ robot_vel, double robot_radius,
@@ -1011,7 +1011,7 @@ __global__ void __launch_bounds__(NT) k_round(cw_crowd_params P, cw_crowd_state 
         __syncthreads();
         if (!s_go) break;
       }
-      orca_env<NT, true>(P, S, e, robot_pos, robot_vel, robot_radius, env_mask, bins, sm, &ra, t);
+      orca_env<NT, kLanes>(P, S, e, robot_pos, robot_vel, robot_radius, env_mask, bins, sm, &ra, t);
       __syncthreads();
       if (++t == ra.T) {
         if (threadIdx.x == 0) {
@@ -1146,12 +1146,19 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
                          (int)cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(k_astar<kAstarWarps, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          (int)cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(k_round<NT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncSetAttribute(k_round<NT, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(k_round<NT, false>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          (int)cudaSharedmemCarveoutMaxShared);
     attrs = true;
   }
-  if (sm > 48 * 1024)
-    cudaFuncSetAttribute(k_round<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  // lane-per-agent ORCA below 128 agents; the binned warp path (96 registers,
+  // so its CTAs share SMs with the search server) above
+  const bool lanes = bins.ncx == 0 && P.max_neighbors <= MAXK;
+  if (sm > 48 * 1024) {
+    cudaFuncSetAttribute(k_round<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_round<NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  }
   const RunLayout L = run_layout(P.E, P.A, ticks);
   unsigned char* base = static_cast<unsigned char*>(scratch);
   RunArgs ra;
@@ -1230,7 +1237,8 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
   for (long long i = 0;; ++i) {
     n_rounds = i + 1;
     cudaStream_t rs = H.rs[i % n_rs];
-    k_round<NT><<<round_ctas, NT, sm, rs>>>(P, S, rp, rv, rr, em, bins, ra);
+    if (lanes) k_round<NT, true><<<round_ctas, NT, sm, rs>>>(P, S, rp, rv, rr, em, bins, ra);
+    else k_round<NT, false><<<round_ctas, NT, sm, rs>>>(P, S, rp, rv, rr, em, bins, ra);
     cudaMemcpyAsync(H.poll + (i & 7) * 8, ra.q, 32, cudaMemcpyDeviceToHost, rs);
     cudaEventRecord(H.ev[i & 7], rs);
     if (i >= kInFlight) {
