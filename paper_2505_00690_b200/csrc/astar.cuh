@@ -780,7 +780,15 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
       __syncwarp();
       if (lane == 0) {
         __threadfence();
-        if (atomicSub(&ra.pending[e], 1) == 1) ready_push(ra, e);   // the env's last search
+        if (atomicSub(&ra.pending[e], 1) == 1) {   // the env's last search
+          if (ra.trace) {
+            long long* tr = ra.trace + (size_t)e * 8;
+            const long long now = global_ns();
+            tr[kTrSearchWait] += now - tr[kTrMark];
+            tr[kTrMark] = now;
+          }
+          urgent_push(ra, e);
+        }
       }
     }
     const long long dt = clock64() - t0;

@@ -602,6 +602,17 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
     if (lanes) {
       // ---------------- lane per agent (A < 128): same operations as the warp path
       const int kmax = min(P.max_neighbors, max(A - 1, 0));
+      // the fp32 Gram operands of every agent, once (field.py:246-253: p32, |p32|^2)
+      float* s_fx = reinterpret_cast<float*>(s_cend);
+      float* s_fy = s_fx + A;
+      float* s_fsq = s_fy + A;
+      for (int a = threadIdx.x; a < A; a += NT) {
+        const float xj = (float)s_px[a], yj = (float)s_py[a];
+        s_fx[a] = xj;
+        s_fy[a] = yj;
+        s_fsq[a] = __fadd_rn(__fmul_rn(xj, xj), __fmul_rn(yj, yj));
+      }
+      __syncthreads();
       for (int a = threadIdx.x; a < A; a += NT) {
         if (!s_act[a]) continue;
         const double px = s_px[a], py = s_py[a];
@@ -630,8 +641,7 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
         int nb = 0;
         for (int j = 0; j < A; ++j) {
           if (j == a || !s_act[j]) continue;
-          float xj = (float)s_px[j], yj = (float)s_py[j];
-          float sqj = __fadd_rn(__fmul_rn(xj, xj), __fmul_rn(yj, yj));
+          const float xj = s_fx[j], yj = s_fy[j], sqj = s_fsq[j];
           float dot = __fmaf_rn(yi, yj, __fmul_rn(xi, xj));
           float key = __fsub_rn(__fadd_rn(sqi, sqj), __fmul_rn(2.0f, dot));
           if (!(key < P.nd2_f32)) continue;
@@ -927,7 +937,7 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
   }
 }
 
-template <int NT>
+template <int NT, bool kLanes = false>
 __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S,
                                              const double* __restrict__ robot_pos,
                                              const double* __restrict__ robot_vel,
@@ -939,7 +949,7 @@ __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S
   // pass 0: every env; pass 1: envs without A* requests (runs beside k_astar);
   // pass 2: envs with requests (after k_astar).  The body is per env.
   const bool skip = (pass == 1 && S.env_req[e]) || (pass == 2 && !S.env_req[e]);
-  if (!skip) orca_env<NT, false>(P, S, e, robot_pos, robot_vel, robot_radius, env_mask, bins, sm, nullptr, 0);
+  if (!skip) orca_env<NT, kLanes>(P, S, e, robot_pos, robot_vel, robot_radius, env_mask, bins, sm, nullptr, 0);
   // ---------------- last CTA: publish last_gap_by_env (only when some row had K > 0),
   // reset the per-step flags and the A* queue
   if (threadIdx.x == 0) {
@@ -980,6 +990,12 @@ __global__ void __launch_bounds__(NT) k_round(cw_crowd_params P, cw_crowd_state 
       if (e >= 0) {
         __threadfence();   // the server's results (acquire through the ring) before reading state
         s_st = ra.env_state[e];
+        if (ra.trace) {
+          long long* tr = ra.trace + (size_t)e * 8;
+          const long long now = global_ns();
+          tr[kTrQueueWait] += now - tr[kTrMark];
+          tr[kTrMark] = now;
+        }
       }
     }
     __syncthreads();
@@ -990,6 +1006,12 @@ __global__ void __launch_bounds__(NT) k_round(cw_crowd_params P, cw_crowd_state 
     for (int burst = 0;; ++burst) {
       if (burst == ra.burst) {   // yield to the envs queued behind this one
         if (threadIdx.x == 0) {
+          if (ra.trace) {
+            long long* tr = ra.trace + (size_t)e * 8;
+            const long long now = global_ns();
+            tr[kTrBusy] += now - tr[kTrMark];
+            tr[kTrMark] = now;
+          }
           ra.env_state[e] = (t << 2) | kRunGuide;
           __threadfence();
           ready_push(ra, e);
@@ -1004,6 +1026,13 @@ __global__ void __launch_bounds__(NT) k_round(cw_crowd_params P, cw_crowd_state 
         }
         const int n = guide_env<NT, true>(P, S, e, env_mask, &ra);
         if (threadIdx.x == 0) {
+          if (ra.trace && n) {   // busy until here; a search wait starts (the server may be done)
+            long long* tr = ra.trace + (size_t)e * 8;
+            const long long now = global_ns();
+            tr[kTrBusy] += now - tr[kTrMark];
+            tr[kTrMark] = now;
+            tr[kTrWaits] += 1;
+          }
           const int left = atomicSub(&ra.pending[e], kPendingGuard - n) - (kPendingGuard - n);
           __threadfence();
           s_go = left == 0;   // else the server queues the env after its last search
@@ -1015,6 +1044,12 @@ __global__ void __launch_bounds__(NT) k_round(cw_crowd_params P, cw_crowd_state 
       __syncthreads();
       if (++t == ra.T) {
         if (threadIdx.x == 0) {
+          if (ra.trace) {
+            long long* tr = ra.trace + (size_t)e * 8;
+            const long long now = global_ns();
+            tr[kTrBusy] += now - tr[kTrMark];
+            tr[kTrDone] = now;
+          }
           ra.env_state[e] = (t << 2) | kRunDone;
           __threadfence();
           if (atomicAdd(&ra.q->n_done, 1) + 1 == ra.E) atomicExch(&ra.q->shutdown, 1);
@@ -1029,10 +1064,14 @@ __global__ void __launch_bounds__(NT) k_round(cw_crowd_params P, cw_crowd_state 
 
 __global__ void k_run_init(RunArgs ra) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ra.trace && i < (size_t)ra.E) ra.trace[i * 8 + kTrMark] = global_ns();
   // every env starts in the ready ring (positions 0..E-1)
-  if (i == 0) *ra.q = RunQueue{0ull, 0ull, 0, 0, 0, 0, 0ull, (unsigned long long)ra.E};
+  if (i == 0) *ra.q = RunQueue{0ull, 0ull, 0, 0, 0, 0, 0ull, (unsigned long long)ra.E, 0ull, 0ull};
   if (i < (size_t)ra.E) { ra.env_state[i] = 0; ra.pending[i] = 0; ra.ritems[i] = (int)i; }
-  if (i <= ra.rmask) ra.rseq[i] = i < (size_t)ra.E ? i + 1 : i;
+  if (i <= ra.rmask) {
+    ra.rseq[i] = i < (size_t)ra.E ? i + 1 : i;
+    ra.useq[i] = i;
+  }
   if (i < (size_t)ra.T) ra.anynb[i] = 0;
   if (i <= ra.mask) ra.seq[i] = i;
 }
@@ -1099,7 +1138,7 @@ static void launch_astar(const cw_crowd_params& P, const cw_crowd_state& S, cuda
 // ---- cw_crowd_run scratch layout
 struct RunLayout {
   unsigned long long cap, rcap;
-  size_t q, env_state, pending, seq, items, rseq, ritems, gap_hist, anynb, total;
+  size_t q, env_state, pending, seq, items, rseq, ritems, useq, uitems, gap_hist, anynb, total;
 };
 
 static RunLayout run_layout(int E, int A, int T) {
@@ -1118,7 +1157,9 @@ static RunLayout run_layout(int E, int A, int T) {
   L.rcap = rcap;
   L.rseq = L.items + up((size_t)cap * sizeof(AstarReq));
   L.ritems = L.rseq + up((size_t)rcap * 8);
-  L.gap_hist = L.ritems + up((size_t)rcap * 4);
+  L.useq = L.ritems + up((size_t)rcap * 4);
+  L.uitems = L.useq + up((size_t)rcap * 8);
+  L.gap_hist = L.uitems + up((size_t)rcap * 4);
   L.anynb = L.gap_hist + up((size_t)E * T * 8);
   L.total = L.anynb + up((size_t)T * 4);
   return L;
@@ -1169,14 +1210,25 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
   ra.items = reinterpret_cast<AstarReq*>(base + L.items);
   ra.rseq = reinterpret_cast<unsigned long long*>(base + L.rseq);
   ra.ritems = reinterpret_cast<int*>(base + L.ritems);
+  ra.useq = reinterpret_cast<unsigned long long*>(base + L.useq);
+  ra.uitems = reinterpret_cast<int*>(base + L.uitems);
   ra.rmask = L.rcap - 1;
   ra.gap_hist = reinterpret_cast<double*>(base + L.gap_hist);
   ra.anynb = reinterpret_cast<int*>(base + L.anynb);
   ra.T = ticks;
   ra.E = P.E;
   ra.mask = L.cap - 1;
-  static const int burst = getenv("CW_RUN_BURST") ? atoi(getenv("CW_RUN_BURST")) : 2;
+  static const int burst = getenv("CW_RUN_BURST") ? atoi(getenv("CW_RUN_BURST")) : 8;
   ra.burst = std::max(1, burst);
+  static long long* trace = nullptr;
+  static int trace_e = 0;
+  static const bool want_trace = getenv("CW_RUN_TRACE") != nullptr;
+  ra.trace = nullptr;
+  if (want_trace) {
+    if (trace_e < P.E) { if (trace) cudaFree(trace); cudaMalloc(&trace, (size_t)P.E * 64); trace_e = P.E; }
+    cudaMemsetAsync(trace, 0, (size_t)P.E * 64, st);
+    ra.trace = trace;
+  }
   const size_t n_init = std::max<size_t>(std::max<size_t>(std::max<size_t>(P.E, ticks), L.cap), L.rcap);
   k_run_init<<<(unsigned)((n_init + 255) / 256), 256, 0, st>>>(ra);
 
@@ -1259,6 +1311,33 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
     }
   }
   g_last_rounds = n_rounds;
+  if (ra.trace) {
+    cudaDeviceSynchronize();
+    std::vector<long long> tr((size_t)P.E * 8);
+    cudaMemcpy(tr.data(), ra.trace, tr.size() * 8, cudaMemcpyDeviceToHost);
+    std::vector<int> order(P.E);
+    for (int e = 0; e < P.E; ++e) order[e] = e;
+    long long t_first = tr[kTrDone], t_last = tr[kTrDone];
+    for (int e = 0; e < P.E; ++e) {
+      t_first = std::min(t_first, tr[(size_t)e * 8 + kTrDone]);
+      t_last = std::max(t_last, tr[(size_t)e * 8 + kTrDone]);
+    }
+    std::sort(order.begin(), order.end(),
+              [&](int a, int b) { return tr[(size_t)a * 8 + kTrDone] > tr[(size_t)b * 8 + kTrDone]; });
+    double sb = 0, ss = 0, sq = 0;
+    for (int e = 0; e < P.E; ++e) {
+      sb += tr[(size_t)e * 8 + kTrBusy];
+      ss += tr[(size_t)e * 8 + kTrSearchWait];
+      sq += tr[(size_t)e * 8 + kTrQueueWait];
+    }
+    fprintf(stderr, "cw_crowd_run trace: done spread %.2f ms; mean per env: busy %.2f ms, search wait %.2f ms, "
+            "queue wait %.2f ms\n", (t_last - t_first) * 1e-6, sb / P.E * 1e-6, ss / P.E * 1e-6, sq / P.E * 1e-6);
+    for (int k = 0; k < 6; ++k) {
+      const long long* r = &tr[(size_t)order[k] * 8];
+      fprintf(stderr, "  env %5d: busy %.2f ms, search wait %.2f ms (%lld waits), queue wait %.2f ms\n", order[k],
+              r[kTrBusy] * 1e-6, r[kTrSearchWait] * 1e-6, r[kTrWaits], r[kTrQueueWait] * 1e-6);
+    }
+  }
   if (status) {   // end the server through the copy engine (no SM needed)
     cudaMemcpyAsync(&ra.q->shutdown, H.one, 4, cudaMemcpyHostToDevice, H.copy);
     cudaStreamSynchronize(H.copy);
@@ -1309,7 +1388,13 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
   }
   if (phases & 1) k_guide<NT><<<P.E, NT, 0, st>>>(P, S, em);
   if (phases & 2) launch_astar(P, S, st);
-  if (phases & 4) k_orca<NT><<<P.E, NT, sm, st>>>(P, S, rp, rv, rr, em, bins, 0);
+  static const bool lanes_dbg = getenv("CW_ORCA_LANES") != nullptr;   // profiling the lane path
+  if ((phases & 4) && lanes_dbg) {
+    if (sm > 48 * 1024) cudaFuncSetAttribute(k_orca<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_orca<NT, true><<<P.E, NT, sm, st>>>(P, S, rp, rv, rr, em, bins, 0);
+  } else if (phases & 4) {
+    k_orca<NT><<<P.E, NT, sm, st>>>(P, S, rp, rv, rr, em, bins, 0);
+  }
   return (int)cudaGetLastError();
 }
 
@@ -1318,8 +1403,9 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
 extern "C" {
 
 size_t cw_crowd_step_smem_bytes(int A, int nt) {
+  // + fp32 (x, y, x^2 + y^2) per agent for the lane path (aliases the unused bins region)
   return (size_t)A * 7 * sizeof(double) + (size_t)(nt / 32) * sizeof(cw::WarpCons) +
-         (size_t)((A + 15) & ~15) + 16;
+         (size_t)((A + 15) & ~15) + 16 + (size_t)A * 3 * sizeof(float);
 }
 
 // Search warps per k_astar CTA (astar_rec / astar_heap hold one slot per warp).

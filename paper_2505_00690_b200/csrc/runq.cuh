@@ -25,7 +25,8 @@ constexpr long long kIdleCycles = 64ll << 30;   // ~35 s backstop for an idle se
 struct RunQueue {                 // device-resident control words
   unsigned long long head, tail;  // search ring positions claimed by consumers / producers
   int n_done, shutdown, error, pad;
-  unsigned long long rhead, rtail;  // ready-env ring
+  unsigned long long rhead, rtail;  // ready-env ring (start, yields)
+  unsigned long long uhead, utail;  // urgent ring: envs the server released (their chain waits)
 };
 
 struct RunArgs {                  // kernel parameter (pointers into cw_crowd_run scratch)
@@ -36,19 +37,26 @@ struct RunArgs {                  // kernel parameter (pointers into cw_crowd_ru
   AstarReq* items;
   unsigned long long* rseq;       // ready-env ring (each env is in it at most once)
   int* ritems;
+  unsigned long long* useq;       // urgent ring, same capacity
+  int* uitems;
   unsigned long long rmask;
   double* gap_hist;               // (E, T) per-tick gap of every env
   int* anynb;                     // (T) some env had K > 0 at tick t
   int T, E;
   int burst;                      // ticks one round CTA may run back to back (bounds round length)
   unsigned long long mask;        // ring capacity - 1 (power of two)
+  long long* trace;               // debug (CW_RUN_TRACE): per env 8 x i64, see kTr*
 };
 
+// debug trace slots per env (ns from %globaltimer)
+enum { kTrMark = 0, kTrBusy, kTrSearchWait, kTrQueueWait, kTrWaits, kTrDone, kTrTicksBusy, kTrPad };
 CW_DEV long long global_ns() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+
+
 
 CW_DEV unsigned long long ld_acquire_u64(const unsigned long long* p) {
   unsigned long long v;
@@ -80,26 +88,27 @@ CW_DEV void ring_push(const RunArgs& ra, const AstarReq& R) {
 }
 
 // ready ring: push (blocking, never full: capacity >= E) / non-blocking pop
-CW_DEV void ready_push(const RunArgs& ra, int e) {
-  const unsigned long long pos = atomicAdd(&ra.q->rtail, 1ull);
-  unsigned long long* sq = ra.rseq + (pos & ra.rmask);
+CW_DEV void env_push(const RunArgs& ra, unsigned long long* tail, unsigned long long* seq, int* items,
+                     int e) {
+  const unsigned long long pos = atomicAdd(tail, 1ull);
+  unsigned long long* sq = seq + (pos & ra.rmask);
   const long long t0 = clock64();
   while (ld_acquire_u64(sq) != pos) {
     if (clock64() - t0 > kSpinCycles) { atomicCAS(&ra.q->error, 0, 3); return; }
   }
-  ra.ritems[pos & ra.rmask] = e;
+  items[pos & ra.rmask] = e;
   st_release_u64(sq, pos + 1);
 }
 
-CW_DEV int ready_pop(const RunArgs& ra) {   // -1: empty right now
-  unsigned long long pos = *(volatile unsigned long long*)&ra.q->rhead;
+CW_DEV int env_pop(const RunArgs& ra, unsigned long long* head, unsigned long long* seq, int* items) {
+  unsigned long long pos = *(volatile unsigned long long*)head;   // -1: empty right now
   while (true) {
-    unsigned long long* sq = ra.rseq + (pos & ra.rmask);
+    unsigned long long* sq = seq + (pos & ra.rmask);
     const long long dif = (long long)(ld_acquire_u64(sq) - (pos + 1));
     if (dif == 0) {
-      const unsigned long long old = atomicCAS(&ra.q->rhead, pos, pos + 1);
+      const unsigned long long old = atomicCAS(head, pos, pos + 1);
       if (old == pos) {
-        const int e = *(volatile int*)&ra.ritems[pos & ra.rmask];
+        const int e = *(volatile int*)&items[pos & ra.rmask];
         st_release_u64(sq, pos + ra.rmask + 1);
         return e;
       }
@@ -107,9 +116,17 @@ CW_DEV int ready_pop(const RunArgs& ra) {   // -1: empty right now
     } else if (dif < 0) {
       return -1;
     } else {
-      pos = *(volatile unsigned long long*)&ra.q->rhead;
+      pos = *(volatile unsigned long long*)head;
     }
   }
+}
+
+CW_DEV void ready_push(const RunArgs& ra, int e) { env_push(ra, &ra.q->rtail, ra.rseq, ra.ritems, e); }
+CW_DEV void urgent_push(const RunArgs& ra, int e) { env_push(ra, &ra.q->utail, ra.useq, ra.uitems, e); }
+// urgent envs first: their searches are done and their chain is the run's critical path
+CW_DEV int ready_pop(const RunArgs& ra) {
+  const int e = env_pop(ra, &ra.q->uhead, ra.useq, ra.uitems);
+  return e >= 0 ? e : env_pop(ra, &ra.q->rhead, ra.rseq, ra.ritems);
 }
 
 // consumer (lane 0 of a server warp): false on shutdown / error

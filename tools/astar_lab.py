@@ -86,6 +86,11 @@ for k in range(steps):
         env_sum = per_env if k == 0 else env_sum + per_env
         tick_max.append(per_env.max())
         mats.append(per_env.copy())
+        if k == 0:
+            env_cnt = np.zeros(E); env_exp = np.zeros(E); env_ticks = np.zeros(E)
+        np.add.at(env_cnt, d[:nreq, 2].astype(np.int64), 1)
+        np.add.at(env_exp, d[:nreq, 2].astype(np.int64), d[:nreq, 1].astype(np.float64))
+        env_ticks[np.unique(d[:nreq, 2].astype(np.int64))] += 1
     for r_ in d[np.argsort(-d[:, 0])[:2]]:
         if os.environ.get("LAB_PHASES"):
             ph_ = [(int(r_[4 + i // 2]) >> (32 * (i % 2))) & 0xFFFFFFFF for i in range(6)] + [int(r_[7])]
@@ -105,6 +110,10 @@ if os.environ.get("LAB_ENVSUM"):
     for G in (1, 2, 4, 8, 16, 32, 64, 128):
         grp = M.reshape(M.shape[0], G, -1).max(axis=2).sum(axis=0)
         print(f"  G={G:4d}: max over groups of summed tick-max {grp.max()/1e6:7.1f}M cycles")
+    top = np.argsort(-env_sum)[:6]
+    for e_ in top:
+        print(f"  env {e_}: summed cycles {env_sum[e_]/1e6:.1f}M, searches {env_cnt[e_]:.0f} in {env_ticks[e_]:.0f} "
+              f"ticks, expansions {env_exp[e_]:.0f} ({env_exp[e_]/max(env_cnt[e_],1):.0f}/search)")
     print(f"sum over ticks of max-search cycles {sum(tick_max)/1e6:.1f}M; max over envs of summed "
           f"cycles {srt[0]/1e6:.1f}M; next envs {[round(v/1e6, 1) for v in srt[1:8]]}")
 
