@@ -87,6 +87,16 @@ CW_DEV void vo_halfplane(double rp0, double rp1, double rv0, double rv1, double 
   pt1 = vs1 + share * u1;
 }
 
+// one out-of-line copy for the lane path (three call sites per agent)
+struct HalfPlane { double p0, p1, n0, n1; };
+__device__ __noinline__ HalfPlane vo_halfplane_ool(double rp0, double rp1, double rv0, double rv1, double rr,
+                                                   double horizon, double dt, double vs0, double vs1,
+                                                   double share) {
+  HalfPlane h;
+  vo_halfplane(rp0, rp1, rv0, rv1, rr, horizon, dt, vs0, vs1, share, h.p0, h.p1, h.n0, h.n1);
+  return h;
+}
+
 // ---------------------------------------------------------------- scalar fallback
 // orca.py:155-189, dir_opt=True (only mode the fallback uses)
 CW_DEV bool solve_on_line_dir(const double* cpx, const double* cpy, const double* cnx,
@@ -117,8 +127,8 @@ CW_DEV bool solve_on_line_dir(const double* cpx, const double* cpy, const double
   return true;
 }
 
-CW_DEV void least_violation(const WarpCons& C, int nc, int begin, double ms, double& r0,
-                            double& r1) {
+__device__ __noinline__ void least_violation(const WarpCons& C, int nc, int begin, double ms, double& r0,
+                                             double& r1) {
   // orca.py:196-212
   double dist = 0.0;
   double qpx[MAXC], qpy[MAXC], qnx[MAXC], qny[MAXC];
@@ -223,6 +233,14 @@ CW_DEV bool warp_lp(const WarpCons& C, int nc, double pf0, double pf1, double ms
 // warp_lp is an exact reduction, taken here in j order.
 constexpr int MAXK = MAXC - 2;   // neighbour lanes
 
+// register-array slot read with a run-time index (keeps the array in registers)
+CW_DEV double get_slot(const double (&a)[MAXC], int k) {
+  double v = a[0];
+#pragma unroll
+  for (int r = 1; r < MAXC; ++r) v = r == k ? a[r] : v;
+  return v;
+}
+
 CW_DEV bool lane_lp(const double (&cpx)[MAXC], const double (&cpy)[MAXC], const double (&cnx)[MAXC],
                     const double (&cny)[MAXC], int nc, double pf0, double pf1, double ms, double& r0,
                     double& r1) {
@@ -230,10 +248,12 @@ CW_DEV bool lane_lp(const double (&cpx)[MAXC], const double (&cpy)[MAXC], const 
   double sc = pn > ms ? ms / fmax(pn, kEps) : 1.0;
   r0 = pf0 * sc;
   r1 = pf1 * sc;
-#pragma unroll
-  for (int i = 0; i < MAXC; ++i) {
-    if (i >= nc) break;
-    const double pi0 = cpx[i], pi1 = cpy[i], ni0 = cnx[i], ni1 = cny[i];
+  // the constraint loop stays rolled (one copy of the body: instruction-cache
+  // footprint); the inner j loop is unrolled over the register arrays
+#pragma unroll 1
+  for (int i = 0; i < nc; ++i) {
+    const double pi0 = get_slot(cpx, i), pi1 = get_slot(cpy, i);
+    const double ni0 = get_slot(cnx, i), ni1 = get_slot(cny, i);
     if (!((r0 - pi0) * ni0 + (r1 - pi1) * ni1 < -kEps)) continue;
     const double d0 = -ni1, d1 = ni0;
     const double dpd = pi0 * d0 + pi1 * d1;
@@ -598,7 +618,9 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
     double my_gap = CUDART_INF;
     int my_anynb = 0;
     long long fallbacks = 0, stalls = 0;
-    const bool lanes = kLanes && bins.ncx == 0 && P.max_neighbors <= MAXK;
+    // kLanes: the caller guarantees no binning (A < 128) and max_neighbors <= MAXK,
+    // so each instantiation holds one of the two paths (code size, registers)
+    constexpr bool lanes = kLanes;
     if (lanes) {
       // ---------------- lane per agent (A < 128): same operations as the warp path
       const int kmax = min(P.max_neighbors, max(A - 1, 0));
@@ -660,20 +682,24 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
         double cpx[MAXC], cpy[MAXC], cnx[MAXC], cny[MAXC];
 #pragma unroll
         for (int k = 0; k < MAXC; ++k) { cpx[k] = 0.0; cpy[k] = 0.0; cnx[k] = 1.0; cny[k] = 0.0; }
+        if (nb > 0) {   // field.py:268-271: gap to the nearest neighbour
+          const int j = tj[0];
+          double rp0 = s_px[j] - px, rp1 = s_py[j] - py;
+          double d_near = sqrt(rp0 * rp0 + rp1 * rp1);
+          my_gap = fmin(my_gap, d_near - (ra + s_r[j]));
+          my_anynb = 1;
+        }
+        int tjk = tj[0];
+#pragma unroll 1
+        for (int k = 0; k < nb; ++k) {   // rolled: one copy of vo_halfplane
 #pragma unroll
-        for (int k = 0; k < MAXK; ++k) {
-          if (k >= nb) break;
-          const int j = tj[k];
+          for (int r = 0; r < MAXK; ++r) tjk = r == k ? tj[r] : tjk;
+          const int j = tjk;
           double rp0 = s_px[j] - px, rp1 = s_py[j] - py;
           double rv0 = vxa - s_vx[j], rv1 = vya - s_vy[j];
           double rr = ra + s_r[j] + P.safety_margin;
-          vo_halfplane(rp0, rp1, rv0, rv1, rr, P.time_horizon, P.dt, vxa, vya, 0.5, cpx[k], cpy[k],
-                       cnx[k], cny[k]);
-          if (k == 0) {
-            double d_near = sqrt(rp0 * rp0 + rp1 * rp1);   // field.py:268-271
-            my_gap = fmin(my_gap, d_near - (ra + s_r[j]));
-            my_anynb = 1;
-          }
+          const HalfPlane h = vo_halfplane_ool(rp0, rp1, rv0, rv1, rr, P.time_horizon, P.dt, vxa, vya, 0.5);
+          put_slot(cpx, k, h.p0); put_slot(cpy, k, h.p1); put_slot(cnx, k, h.n0); put_slot(cny, k, h.n1);
         }
         int nc = nb;
         if (use_robot) {
@@ -681,10 +707,9 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
           double d2 = rp0 * rp0 + rp1 * rp1;
           if (d2 < P.nd2) {
             double rr = ra + robot_radius + P.safety_margin;
-            double q0, q1, m0, m1;
-            vo_halfplane(rp0, rp1, vxa - rvx, vya - rvy, rr, P.obstacle_time_horizon, P.dt, vxa, vya,
-                         1.0, q0, q1, m0, m1);
-            put_slot(cpx, nc, q0); put_slot(cpy, nc, q1); put_slot(cnx, nc, m0); put_slot(cny, nc, m1);
+            const HalfPlane h = vo_halfplane_ool(rp0, rp1, vxa - rvx, vya - rvy, rr, P.obstacle_time_horizon,
+                                                 P.dt, vxa, vya, 1.0);
+            put_slot(cpx, nc, h.p0); put_slot(cpy, nc, h.p1); put_slot(cnx, nc, h.n0); put_slot(cny, nc, h.n1);
             ++nc;
           }
         }
@@ -699,24 +724,26 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
             if (d2 < P.nd2) {
               double margin = 0.5 * kSqrt2 * P.res0;
               double rr = ra + margin + P.safety_margin;
-              double q0, q1, m0, m1;
-              vo_halfplane(rp0, rp1, vxa, vya, rr, P.obstacle_time_horizon, P.dt, vxa, vya, 1.0, q0, q1,
-                           m0, m1);
-              put_slot(cpx, nc, q0); put_slot(cpy, nc, q1); put_slot(cnx, nc, m0); put_slot(cny, nc, m1);
+              const HalfPlane h = vo_halfplane_ool(rp0, rp1, vxa, vya, rr, P.obstacle_time_horizon, P.dt, vxa,
+                                                   vya, 1.0);
+              put_slot(cpx, nc, h.p0); put_slot(cpy, nc, h.p1); put_slot(cnx, nc, h.n0); put_slot(cny, nc, h.n1);
               ++nc;
             }
           }
         }
         const double ms = S.max_speed[ia];
         double v0, v1;
-        fallbacks += lane_lp(cpx, cpy, cnx, cny, nc, pf0, pf1, ms, v0, v1);
-        double spd = sqrt(v0 * v0 + v1 * v1);
-        double want = sqrt(pf0 * pf0 + pf1 * pf1);
-        if (spd < 0.2 * want && want > 1e-6) {
-          ++stalls;
-          double q0 = P.stall_c * pf0 + P.stall_s * pf1;
-          double q1 = -P.stall_s * pf0 + P.stall_c * pf1;
+        const double want = sqrt(pf0 * pf0 + pf1 * pf1);
+        double q0 = pf0, q1 = pf1;
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {   // second pass = stall retry (one LP copy)
           fallbacks += lane_lp(cpx, cpy, cnx, cny, nc, q0, q1, ms, v0, v1);
+          if (pass == 1) break;
+          const double spd = sqrt(v0 * v0 + v1 * v1);
+          if (!(spd < 0.2 * want && want > 1e-6)) break;
+          ++stalls;
+          q0 = P.stall_c * pf0 + P.stall_s * pf1;
+          q1 = -P.stall_s * pf0 + P.stall_c * pf1;
         }
         double npx = px + v0 * P.dt, npy = py + v1 * P.dt;
         bool out = npx < 0 || npy < 0 || npx >= nx * res || npy >= ny * res;
