@@ -127,8 +127,8 @@ CW_DEV bool solve_on_line_dir(const double* cpx, const double* cpy, const double
   return true;
 }
 
-__device__ __noinline__ void least_violation(const WarpCons& C, int nc, int begin, double ms, double& r0,
-                                             double& r1) {
+CW_DEV void least_violation(const WarpCons& C, int nc, int begin, double ms, double& r0,
+                            double& r1) {
   // orca.py:196-212
   double dist = 0.0;
   double qpx[MAXC], qpy[MAXC], qnx[MAXC], qny[MAXC];
@@ -168,6 +168,12 @@ __device__ __noinline__ void least_violation(const WarpCons& C, int nc, int begi
     if (ok) { r0 = t0; r1 = t1; }
     dist = -dot2_blas(r0 - pix, r1 - piy, nix, niy);
   }
+}
+
+// out-of-line copy for the lane path (rare; keeps the round kernel's hot code small)
+__device__ __noinline__ void least_violation_ool(const WarpCons& C, int nc, int begin, double ms, double& r0,
+                                                 double& r1) {
+  least_violation(C, nc, begin, ms, r0, r1);
 }
 
 // ---------------------------------------------------------------- warp LP
@@ -282,7 +288,7 @@ CW_DEV bool lane_lp(const double (&cpx)[MAXC], const double (&cpy)[MAXC], const 
       WarpCons C;
 #pragma unroll
       for (int k = 0; k < MAXC; ++k) { C.px[k] = cpx[k]; C.py[k] = cpy[k]; C.nx[k] = cnx[k]; C.ny[k] = cny[k]; }
-      least_violation(C, nc, i, ms, r0, r1);
+      least_violation_ool(C, nc, i, ms, r0, r1);
       return true;
     }
     double tb = (pf0 - pi0) * d0 + (pf1 - pi1) * d1;
