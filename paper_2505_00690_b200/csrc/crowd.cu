@@ -667,12 +667,24 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
 #pragma unroll
         for (int k = 0; k < MAXK; ++k) { tk[k] = CUDART_INF_F; tj[k] = 0; }
         int nb = 0;
-        for (int j = 0; j < A; ++j) {
-          if (j == a || !s_act[j]) continue;
+        // per 32-candidate chunk: the range test for every j without divergence
+        // (a bitmask), then each lane inserts only its own in-range j, in j order
+        for (int j0 = 0; j0 < A; j0 += 32) {
+         unsigned inr = 0u;
+         const int jn = min(32, A - j0);
+         for (int u = 0; u < jn; ++u) {
+          const int j = j0 + u;
           const float xj = s_fx[j], yj = s_fy[j], sqj = s_fsq[j];
           float dot = __fmaf_rn(yi, yj, __fmul_rn(xi, xj));
           float key = __fsub_rn(__fadd_rn(sqi, sqj), __fmul_rn(2.0f, dot));
-          if (!(key < P.nd2_f32)) continue;
+          inr |= (unsigned)((key < P.nd2_f32) & (j != a) & (s_act[j] != 0)) << u;
+         }
+         while (inr) {
+          const int j = j0 + __ffs(inr) - 1;
+          inr &= inr - 1u;
+          const float xj = s_fx[j], yj = s_fy[j], sqj = s_fsq[j];
+          float dot = __fmaf_rn(yi, yj, __fmul_rn(xi, xj));
+          float key = __fsub_rn(__fadd_rn(sqi, sqj), __fmul_rn(2.0f, dot));
           int pos = 0;
 #pragma unroll
           for (int k = 0; k < MAXK; ++k) pos += (k < nb && tk[k] <= key);
@@ -684,6 +696,7 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
           for (int k = 0; k < MAXK; ++k)
             if (k == pos) { tk[k] = key; tj[k] = j; }
           nb = min(nb + 1, kmax);
+         }
         }
         double cpx[MAXC], cpy[MAXC], cnx[MAXC], cny[MAXC];
 #pragma unroll
@@ -1057,7 +1070,10 @@ __global__ void __launch_bounds__(NT) k_round(cw_crowd_params P, cw_crowd_state 
           ra.env_state[e] = (t << 2) | kRunWait;
           __threadfence();
         }
+        const long long tg0 = clock64();
         const int n = guide_env<NT, true>(P, S, e, env_mask, &ra);
+        if (threadIdx.x == 0 && S.counters)
+          atomicAdd((unsigned long long*)&S.counters[8], (unsigned long long)(clock64() - tg0));
         if (threadIdx.x == 0) {
           if (ra.trace && n) {   // busy until here; a search wait starts (the server may be done)
             long long* tr = ra.trace + (size_t)e * 8;

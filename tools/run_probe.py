@@ -81,6 +81,7 @@ print("  flags sync", f.flags_t.cpu().numpy()[:2], "run", h.flags_t.cpu().numpy(
 c = h.counters_t.cpu().numpy()
 clk = 1.92e6   # cycles per ms (approx. boost clock)
 print(f"  run: expansions {c[0]:,} search warp-cycles {c[4]/1e6:.0f}M (= {c[4]/clk/T:.2f} warp-ms/tick), "
-      f"max search {c[5]/1e6:.1f}M cyc, orca CTA-cycles {c[6]/1e6:.0f}M (= {c[6]/clk/T:.2f} CTA-ms/tick)")
+      f"max search {c[5]/1e6:.1f}M cyc, orca CTA-cycles {c[6]/1e6:.0f}M (= {c[6]/clk/T:.2f} CTA-ms/tick), "
+      f"guide CTA-cycles {c[8]/1e6:.0f}M (= {c[8]/clk/T:.2f} CTA-ms/tick)")
 print(f"{cfgname} E={E} T={T}: sync {sync_ms:.3f} ms/tick ({E / sync_ms * 1e3:,.0f} env-steps/s); "
       f"run {run_ms:.3f} ms/tick ({E / run_ms * 1e3:,.0f} env-steps/s); identical={same}")
