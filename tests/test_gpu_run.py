@@ -89,3 +89,48 @@ def test_run_without_robot_then_steps(torch_cuda):
         f.step()
         g.step()
     _same(f, g, "after run")
+
+
+def test_run_edge_cases(torch_cuda):
+    """One env, one tick, one agent; every env masked; an open arena (no obstacles,
+    so no searches at all); run(0) is a no-op."""
+    import torch
+    from paper_2505_00690_b200.crowd import CrowdAgent, CrowdConfig, CrowdField
+    from paper_2505_00690_b200.urbangen import OccupancyGrid
+    b, (f, g) = _pair(1, 16.0, 0.25, 1, 4)
+    for _ in range(1):
+        f.step()
+    g.run(1)
+    _same(f, g, "E=1 T=1")
+    g.run(0)
+    _same(f, g, "run(0)")
+    b, (f, g) = _pair(6, 32.0, 0.25, 8, 20)
+    mask = torch.zeros(6, dtype=torch.uint8, device="cuda")
+    for _ in range(5):
+        f.step(env_mask=mask)
+    g.run(5, env_mask=mask)
+    _same(f, g, "all masked")
+    ny = nx = 64
+    occ = OccupancyGrid(0.25, np.full((ny, nx), 2, np.uint8), np.zeros((ny, nx), np.float32))
+    rng = np.random.default_rng(5)
+    agents = [[CrowdAgent(i, rng.uniform(1, 15, 2), np.zeros(2), 0.3, 1.2, rng.uniform(1, 15, 2))
+               for i in range(12)] for _ in range(3)]
+    fs = []
+    for _ in range(2):
+        h = CrowdField([occ] * 3, CrowdConfig(), [11, 12, 13])
+        h.set_agents(agents)
+        fs.append(h)
+    for _ in range(40):
+        fs[0].step()
+    fs[1].run(40)
+    _same(fs[0], fs[1], "open arena")
+
+
+def test_run_full_cfg2_batch_matches_steps(torch_cuda):
+    """1024 cfg2 envs x 30 ticks: every env's state equals 30 synchronous steps."""
+    b, (f, g) = _pair(1024, 32.0, 0.125, 32, 64)
+    rp, rv = _robot(b, 1024, 0.125, seed=21)
+    for _ in range(30):
+        f.step(rp, rv, 0.35)
+    g.run(30, rp, rv, 0.35)
+    _same(f, g, "cfg2 x 1024")
