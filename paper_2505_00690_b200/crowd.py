@@ -97,6 +97,7 @@ class CrowdField:
         self.device = torch.device(device)
         self.threads = threads
         self.run_threads = None   # cw_crowd_run CTA size; None: one lane per agent
+        self.run_history_bytes = 256 << 20   # per-call cap of the run's (env, tick) gap history
         self.astar_warps = astar_warps
         if isinstance(occupancies, SceneBatch):
             b = occupancies
@@ -356,14 +357,18 @@ class CrowdField:
         rp = self._dev(robot_pos, torch.float64, (self.E, 2))
         rv = self._dev(robot_vel, torch.float64, (self.E, 2)) if robot_pos is not None else None
         em = self._dev(env_mask, torch.uint8, (self.E,))
-        nbytes = int(_lib.lib().cw_crowd_run_scratch_bytes(self.E, self.A, ticks))
+        # the per-(env, tick) gap history bounds one call's length: long runs go in
+        # chunks (a chunk boundary is a barrier across envs; results are unchanged)
+        chunk = max(1, min(ticks, self.run_history_bytes // (8 * self.E)))
+        nbytes = int(_lib.lib().cw_crowd_run_scratch_bytes(self.E, self.A, chunk))
         if getattr(self, "_run_scratch", None) is None or self._run_scratch.numel() < nbytes:
             self._run_scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
-        err = _lib.lib().cw_crowd_run(self._p, self._s, _lib.ptr(rp), _lib.ptr(rv), float(robot_radius),
-                                      _lib.ptr(em), int(threads or self.run_threads or self._run_nt()), ticks,
-                                      _lib.ptr(self._run_scratch),
-                                      _lib.stream_ptr(stream))
-        _lib.check(err, "cw_crowd_run")
+        nt = int(threads or self.run_threads or self._run_nt())
+        for t0 in range(0, ticks, chunk):
+            err = _lib.lib().cw_crowd_run(self._p, self._s, _lib.ptr(rp), _lib.ptr(rv), float(robot_radius),
+                                          _lib.ptr(em), nt, min(chunk, ticks - t0), _lib.ptr(self._run_scratch),
+                                          _lib.stream_ptr(stream))
+            _lib.check(err, "cw_crowd_run")
         if check:
             self.check_flags()
 

@@ -78,6 +78,17 @@ def test_run_with_env_mask_and_split_runs(torch_cuda):
     _same(f, g, "masked split run")
 
 
+def test_run_in_chunks_matches(torch_cuda):
+    """A run longer than one call's history budget goes in chunks; same state."""
+    E = 8
+    b, (f, g) = _pair(E, 32.0, 0.25, 8, 20)
+    g.run_history_bytes = 8 * E * 7      # 7 ticks per call
+    for _ in range(23):
+        f.step()
+    g.run(23)
+    _same(f, g, "chunked")
+
+
 def test_run_without_robot_then_steps(torch_cuda):
     E = 8
     b, (f, g) = _pair(E, 32.0, 0.25, 8, 20)
