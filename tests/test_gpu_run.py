@@ -145,3 +145,25 @@ def test_run_full_cfg2_batch_matches_steps(torch_cuda):
         f.step(rp, rv, 0.35)
     g.run(30, rp, rv, 0.35)
     _same(f, g, "cfg2 x 1024")
+
+
+def test_run_binned_warp_path(torch_cuda):
+    """A >= 128 (cell-binned neighbour search, warp-per-agent rounds) on a block layout."""
+    from oracle.rng import child_seed
+    from paper_2505_00690_b200.crowd import CrowdConfig, CrowdField
+    from paper_2505_00690_b200.urbangen import SceneSampler, SceneSpec, TaskKind
+    seeds = [child_seed(0, "env", 40 + i) for i in range(3)]
+    spec = SceneSpec(seed=0, extent_m=(48.0, 48.0), task_kind=TaskKind.NAV_CLEAR, object_density=0.0,
+                     pedestrian_count=140, terrain_mix=MIX, grid_resolution_m=0.25)
+    b = SceneSampler(spec, 3).sample(seeds, [child_seed(s, "crowd", 0) for s in seeds])
+    run = [child_seed(s, "crowd-run") for s in seeds]
+    fs = []
+    for _ in range(2):
+        f = CrowdField(b, CrowdConfig(neighbor_distance=3.0), run)
+        f.set_from_spawn(b)
+        fs.append(f)
+    rp, rv = _robot(b, 3, 0.25, seed=4)
+    for _ in range(12):
+        fs[0].step(rp, rv, 0.35)
+    fs[1].run(12, rp, rv, 0.35)
+    _same(fs[0], fs[1], "A=140 binned")
