@@ -342,7 +342,9 @@ CW_DEV u64 make_key2(double h, int r, int c, int slot) {
 // slots: overflow tiles (g f64 + move byte), parent i32 per cell, slot->tile map
 CW_HD size_t astar_slot_bytes(int nx, int ny, int S) {
   const size_t nt = (size_t)((nx + 7) / 8) * ((ny + 7) / 8);
-  const size_t b = nt * 64 * 9 + (size_t)nx * ny * 4 + (nt + (size_t)S) * 4;
+  // global tiles: every tile at slot >= S plus the shared pool's S slot ids (a
+  // search whose pool runs dry continues here under the same ids)
+  const size_t b = (nt + (size_t)S) * 64 * 9 + (size_t)nx * ny * 4 + (nt + (size_t)S) * 4;
   return (b + 255) & ~(size_t)255;
 }
 
@@ -376,11 +378,16 @@ CW_HD AstarShape astar_shape(int nx, int ny, int W, int budget_kb = 0) {
   return {NC, NS, W, per_warp, fixed + stack + (size_t)NS * 576};
 }
 
-// Per-warp global scratch stride: sized for the larger pool of the two shapes.
-CW_HD size_t astar_slot_stride(int nx, int ny) {
-  const int a = astar_shape(nx, ny, 1).NS, b = astar_shape(nx, ny, kAstarWarps).NS;
-  return astar_slot_bytes(nx, ny, a > b ? a : b);
+// Largest shared pool (slot ids) of the search shapes in use (1, 2 or 4 warps per CTA);
+// launches clamp NS to it.
+CW_HD int astar_ns_cap(int nx, int ny) {
+  const int a = astar_shape(nx, ny, 1).NS, b = astar_shape(nx, ny, 2).NS;
+  const int c = astar_shape(nx, ny, kAstarWarps).NS;
+  return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
+
+// Per-warp global scratch stride: sized for the largest pool of the shapes.
+CW_HD size_t astar_slot_stride(int nx, int ny) { return astar_slot_bytes(nx, ny, astar_ns_cap(nx, ny)); }
 
 // Per-CTA layout shared by the two search instantiations.
 struct SearchEnv {
@@ -420,9 +427,21 @@ CW_DEV bool pool_take(const SearchEnv& E, int n, uint16_t* out) {
 // caller releases and retries with kGlob = true, all tiles in the warp's global
 // backing store).  Returns 1 found, 0 no path, -1 open-set overflow; `used` =
 // tiles handed out (recorded in s2t).
+// Resumable search state: a shared-memory search whose tile pool runs dry hands
+// its open set over (the popped, not yet expanded cell back in the head) and
+// continues all-global on the same open set and the same slot ids -- the used
+// tiles are copied to the global store at their slot index first -- instead of
+// starting over.  New global tiles then take slots slot_base + k.
+struct Resume {
+  OpenSet st;
+  int active;      // st holds a search in progress
+  int slot_base;   // first slot id of new global tiles
+  int gcount;      // global tiles handed out so far
+};
+
 template <bool kGlob>
 CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int start, int goal,
-                      double& delta, double& delta2, unsigned& s_exp, int& used, int lane) {
+                      double& delta, double& delta2, unsigned& s_exp, int& used, int lane, Resume& rs) {
   double* const gt = kGlob ? E.gtg : E.gts;
   uint8_t* const mt = kGlob ? E.mtg : E.mts;
   const int nx = E.nx, ny = E.ny, TW = E.TW, NT = E.NT, NC = pl.NC;
@@ -455,32 +474,37 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
   };
   // n slot ids for this warp: sequential (all-global) or from the CTA pool
   auto take = [&](int n) -> bool {
-    if (kGlob) return true;
+    if (kGlob) return true;   // slots rs.slot_base + rs.gcount ... (see new_tile calls)
     bool ok = false;
     if (lane == 0) ok = pool_take(E, n, E.wbuf);
     ok = __shfl_sync(0xffffffffu, ok, 0);
     __syncwarp();
     return ok;
   };
-  const double h0 = octile(sr, sc, gr, gc);
-  if (!take(1)) return -2;
-  const int s0 = new_tile((sr >> 3) * TW + (sc >> 3), kGlob ? 0 : (int)E.wbuf[0]);
-  __syncwarp();
-  if (lane == 0) {
-    gt[(size_t)s0 * 64 + (sr & 7) * 8 + (sc & 7)] = 0.0;
-    E.parent[start] = -1;
-  }
   OpenSet st;
-  st.hd = key_inf();
-  if (lane == 0) st.hd = {(u64)__double_as_longlong(h0), make_key2(h0, sr, sc, s0)};
-  st.T = key_inf();
-  st.F2 = {f_plus((u64)__double_as_longlong(h0), delta2), 0ull};
-  st.delta = delta;
-  st.delta2 = delta2;
-  st.h = 1;
-  st.nn = 0;
-  st.nf = 0;
-  st.err = 0;
+  if (kGlob && rs.active) {
+    st = rs.st;                 // continue the handed-over search
+    rs.active = 0;
+  } else {
+    const double h0 = octile(sr, sc, gr, gc);
+    if (!take(1)) return -2;
+    const int s0 = new_tile((sr >> 3) * TW + (sc >> 3), kGlob ? rs.slot_base + rs.gcount++ : (int)E.wbuf[0]);
+    __syncwarp();
+    if (lane == 0) {
+      gt[(size_t)s0 * 64 + (sr & 7) * 8 + (sc & 7)] = 0.0;
+      E.parent[start] = -1;
+    }
+    st.hd = key_inf();
+    if (lane == 0) st.hd = {(u64)__double_as_longlong(h0), make_key2(h0, sr, sc, s0)};
+    st.T = key_inf();
+    st.F2 = {f_plus((u64)__double_as_longlong(h0), delta2), 0ull};
+    st.delta = delta;
+    st.delta2 = delta2;
+    st.h = 1;
+    st.nn = 0;
+    st.nf = 0;
+    st.err = 0;
+  }
   int found = 0;
   __syncwarp();
   while (true) {
@@ -491,7 +515,8 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
       continue;
     }
     // ---------------- pop the head minimum
-    const u64 topk = __shfl_sync(0xffffffffu, st.hd.k, 0);   // f is not needed
+    const Key popped = shfl_key(st.hd, 0);
+    const u64 topk = popped.k;
     {
       const Key nxt = shfl_key_down(st.hd, 1);
       st.hd = lane < 31 ? nxt : key_inf();
@@ -547,13 +572,22 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
       const unsigned peers = __match_any_sync(0xffffffffu, need ? ty : -1 - lane);
       const int leader = __ffs(peers) - 1;
       const unsigned lm = __ballot_sync(0xffffffffu, need && leader == lane);
-      if (!take(__popc(lm))) { found = -2; break; }   // only when !kGlob
+      if (!take(__popc(lm))) {   // only when !kGlob: hand the search over (see Resume)
+        const Key up = shfl_key_up(st.hd, 1);
+        st.hd = lane == 0 ? popped : up;
+        st.h += 1;
+        --s_exp;
+        rs.st = st;
+        rs.active = 1;
+        found = -2;
+        break;
+      }
       unsigned L = lm;
       int mine = 0, k = 0;
       while (L) {
         const int ld = __ffs(L) - 1;
         L &= L - 1;
-        const int s = new_tile(__shfl_sync(0xffffffffu, ty, ld), kGlob ? used : (int)E.wbuf[k]);
+        const int s = new_tile(__shfl_sync(0xffffffffu, ty, ld), kGlob ? rs.slot_base + rs.gcount++ : (int)E.wbuf[k]);
         ++k;
         if (lane == ld) mine = s;
       }
@@ -667,9 +701,10 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
   E.wbuf = reinterpret_cast<uint16_t*>(pl.stg) + 0;   // staging area doubles as the slot buffer
   unsigned char* const gbase = reinterpret_cast<unsigned char*>(S.astar_rec) +
                                (size_t)gw * astar_slot_stride(nx, E.ny);
+  const int NTG = NT + astar_ns_cap(nx, E.ny);   // global store: every tile + the pool's slot ids
   E.gtg = reinterpret_cast<double*>(gbase);
-  E.mtg = gbase + (size_t)NT * 64 * 8;
-  E.parent = reinterpret_cast<int32_t*>(E.mtg + (size_t)NT * 64);
+  E.mtg = gbase + (size_t)NTG * 64 * 8;
+  E.parent = reinterpret_cast<int32_t*>(E.mtg + (size_t)NTG * 64);
   E.s2t = E.parent + N;
   for (int t = lane; t < NT; t += 32) E.tmap[t] = kNoSlot;
   for (int i = threadIdx.x; i < NS; i += blockDim.x) E.free_ids[i] = (uint16_t)i;
@@ -734,13 +769,52 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
       used = 0;
     };
     if (lab[start] != L_OBSTACLE && lab[goal] != L_OBSTACLE && reach[start] == reach[goal]) {
-      found = run_search<false>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane);
-      if (found == -2) {   // the shared tile pool ran dry: redo it all-global
+      Resume rs;
+      rs.active = 0;
+      rs.slot_base = 0;
+      rs.gcount = 0;
+      found = run_search<false>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs);
+      if (found == -2 && rs.active) {
+        // the shared tile pool ran dry mid-search: move the used tiles to the
+        // global store at their slot ids, give the slots back to the CTA pool
+        // and continue all-global on the same open set
+        for (int k = 0; k < used; ++k) {
+          const int sl = E.s2t[k] >> 16;
+          E.gtg[(size_t)sl * 64 + lane] = E.gts[(size_t)sl * 64 + lane];
+          E.gtg[(size_t)sl * 64 + lane + 32] = E.gts[(size_t)sl * 64 + lane + 32];
+          E.mtg[(size_t)sl * 64 + lane] = E.mts[(size_t)sl * 64 + lane];
+          E.mtg[(size_t)sl * 64 + lane + 32] = E.mts[(size_t)sl * 64 + lane + 32];
+        }
+        __syncwarp();
+        if (lane == 0) {
+          while (atomicCAS(&E.pool_lock[0], 0, 1) != 0) {}
+          __threadfence_block();
+        }
+        __syncwarp();
+        const int top = *(volatile int*)&E.pool_lock[1];
+        for (int k = lane; k < used; k += 32)
+          ((volatile uint16_t*)E.free_ids)[top + k] = (uint16_t)(E.s2t[k] >> 16);
+        __syncwarp();
+        if (lane == 0) {
+          *(volatile int*)&E.pool_lock[1] = top + used;
+          __threadfence_block();
+          atomicExch(&E.pool_lock[0], 0);
+        }
+        __syncwarp();
+        pooled = false;   // the final release only clears the tile map
+        rs.slot_base = NS;
+        rs.gcount = 0;
+        ++n_glob;
+        found = run_search<true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs);
+      } else if (found == -2) {   // no tile even for the start cell: all-global from scratch
         release();
         pooled = false;
         s_exp = 0;
         ++n_glob;
-        found = run_search<true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane);
+        rs.active = 0;
+        rs.slot_base = 0;
+        rs.gcount = 0;
+        found = run_search<true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs);
       }
     }
     // ---- write the guidance result (field.py:204-212)

@@ -1314,7 +1314,8 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
   // at nearly its per-expansion cost (the run is bound by each env's own chain)
   static const int srv_w = getenv("CW_RUN_SERVER_W") ? atoi(getenv("CW_RUN_SERVER_W")) : 2;
   static const int srv_kb = getenv("CW_RUN_SERVER_KB") ? atoi(getenv("CW_RUN_SERVER_KB")) : 0;
-  const AstarShape shp = astar_shape(P.nx, P.ny, srv_w == 4 ? kAstarWarps : srv_w == 2 ? 2 : 1, srv_kb);
+  AstarShape shp = astar_shape(P.nx, P.ny, srv_w == 4 ? kAstarWarps : srv_w == 2 ? 2 : 1, srv_kb);
+  shp.NS = std::min(shp.NS, astar_ns_cap(P.nx, P.ny));   // the global store holds NS slot ids
   static const int margin = getenv("CW_RUN_MARGIN") ? atoi(getenv("CW_RUN_MARGIN")) : 0;
   int srv_ctas = P.astar_ctas - std::max(4, margin > 0 ? margin : P.astar_ctas / 8);
   if (const char* v = getenv("CW_RUN_SERVER_CTAS")) srv_ctas = std::min(srv_ctas, atoi(v));

@@ -84,3 +84,32 @@ def test_every_search_matches_oracle_dense_scenes(warps, torch_cuda):
             checked += 1
         f.step_phase(4)
     assert checked > 100
+
+
+@pytest.mark.parametrize("warps", [1, 4])
+def test_astar_pool_handover_matches_oracle(warps, torch_cuda):
+    """A search that floods a 200 x 200 cup (~40k cells, more tiles than the shared
+    pool holds) hands its open set over to the global store mid-search and must
+    still pop in the reference order: same path as the oracle."""
+    from paper_2505_00690_b200.crowd import CrowdAgent, CrowdConfig, CrowdField
+    from paper_2505_00690_b200.urbangen import OccupancyGrid
+    ny = nx = 256
+    res = 0.125
+    passable = np.ones((ny, nx), bool)
+    passable[30:231, 30] = False
+    passable[30:231, 230] = False
+    passable[230, 30:231] = False
+    st, gl = 220 * nx + 130, 245 * nx + 131
+    want = _oracle_cells(passable, st, gl)
+    occ = OccupancyGrid(res, np.where(passable, 2, 0).astype(np.uint8), np.zeros((ny, nx), np.float32))
+    f = CrowdField([occ], CrowdConfig(), [0], astar_warps=warps)
+    at = lambda c: np.array([(c % nx + 0.5) * res, (c // nx + 0.5) * res])
+    f.set_agents([[CrowdAgent(0, at(st), np.zeros(2), 0.3, 1.0, at(gl))]])
+    f.prepare_step()
+    f.counters_t.zero_()
+    f.step_phase(1)
+    f.step_phase(2)
+    assert int(f.counters_t[10]) == 1, "the search should have outgrown the shared tile pool"
+    n = int(f.path_n_t[0, 0])
+    assert n == len(want) + 1
+    assert f.path_cells_t[0, 0, :n - 1].cpu().numpy().tolist() == want
