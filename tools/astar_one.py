@@ -1,4 +1,5 @@
-"""Run single A* searches (start, goal on a label grid) through the product
+"""Run single A* searches (start, goal on a label grid; e.g. the cases of
+tests/golden/astar_regress.npz exported with np.savez) through the product
 k_astar via CrowdField and compare with the oracle (GPU).
 Usage: python tools/astar_one.py case.npz [...]"""
 import os

@@ -43,6 +43,7 @@ rvel = torch.zeros_like(rpos)
 fields = []
 for _ in range(2):
     f = CrowdField(b, CrowdConfig(neighbor_distance=CFG["nd"]), run_seeds, device=dev,
+                   astar_warps=int(os.environ["PROBE_ASTAR_WARPS"]) if "PROBE_ASTAR_WARPS" in os.environ else None,
                    threads=int(os.environ.get("PROBE_THREADS", 128)))
     f.run_threads = int(os.environ["PROBE_RUN_THREADS"]) if "PROBE_RUN_THREADS" in os.environ else None
     f.set_from_spawn(b)
