@@ -207,25 +207,27 @@ __global__ void __launch_bounds__(RT_NT, 1) k_routes(cw_scene_params P, int e0, 
     if (sh + w > 32) x |= (unsigned long long)s_walk[wd + 1] << 32;
     return (x >> sh) & ((1ull << w) - 1ull);
   };
+  // The clearance ball: offsets (dr, dc) with octile(|dr|, |dc|) * res < 0.4.  For a
+  // fixed |dr| the octile distance grows with |dc|, so the ball's row |dr| is the
+  // column range |dc| <= s_half[|dr|] (-1: empty) -- one bit-window test per row.
+  __shared__ int s_half[8];
+  if (stencil && tid <= rad) {
+    int m = -1;
+    for (int ac = 0; ac <= rad; ++ac) {
+      const double o = kSqrt2 * (double)min(tid, ac) + (double)abs(tid - ac);
+      if (o * res < kMinClear) m = ac;
+    }
+    s_half[tid] = m;
+  }
+  __syncthreads();
   auto clear_at = [&](int f) -> bool {   // chamfer(~walkable) * res >= 0.4 for a walkable cell
     if (!stencil) return D[f] * res >= kMinClear;
     const int r = f / nx, c = f - r * nx;
-    if (r - rad >= 0 && r + rad < ny && c - rad >= 0 && c + rad < nx) {
-      bool all = true;   // fast path: the whole window walkable
-      for (int dr = -rad; dr <= rad && all; ++dr)
-        all = win_bits(r + dr, c - rad, 2 * rad + 1) == ((1ull << (2 * rad + 1)) - 1ull);
-      if (all) return true;
-    }
     for (int dr = -rad; dr <= rad; ++dr) {
-      const int rr = r + dr;
-      if (rr < 0 || rr >= ny) continue;
-      for (int dc = -rad; dc <= rad; ++dc) {
-        const int cc = c + dc;
-        if (cc < 0 || cc >= nx || walk(rr, cc)) continue;
-        const int ar = abs(dr), ac = abs(dc);
-        const double o = kSqrt2 * (double)min(ar, ac) + (double)abs(ar - ac);
-        if (o * res < kMinClear) return false;
-      }
+      const int rr = r + dr, m = s_half[abs(dr)];
+      if (rr < 0 || rr >= ny || m < 0) continue;
+      const int lo = max(c - m, 0), hi = min(c + m, nx - 1), w = hi - lo + 1;
+      if (win_bits(rr, lo, w) != ((1ull << w) - 1ull)) return false;   // a non-walkable cell in the ball
     }
     return true;
   };
