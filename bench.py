@@ -373,7 +373,9 @@ def run_ours(args):
                          "traffic_source": "ncu --set full, profiles/r1_traffic.json (cfg2 tick 21)",
                          "kernel": dom, "peak_source": src, "bytes_per_launch": round(kb[dom], 1),
                          "avg_launch_ms": round(dom_ms, 4),
-                         "note": "latency-bound serial search; see profiles/"},
+                         "note": "latency-bound serial search; measured per kernel in the synchronous tick "
+                                 "(events around each launch); the multi-tick run overlaps the same device "
+                                 "bodies, see roofline_step and profiles/r1_run_trace_cfg2.txt"},
             "roofline_step": {"bound": "hbm", "achieved": round(achieved, 3), "peak": peak, "unit": "GB/s",
                               "frac": round(achieved / peak, 7), "bytes_per_step": round(bytes_step, 1),
                               "model": "SURVEY 8d: 74 B/agent-step + 8 B/path point + 20 B/env-step"},

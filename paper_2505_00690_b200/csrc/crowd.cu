@@ -550,7 +550,7 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
   double* s_nx = s_r + A;   // post-commit positions (resample)
   double* s_ny = s_nx + A;
   WarpCons* s_cons = reinterpret_cast<WarpCons*>(s_ny + A);
-  uint8_t* s_act = reinterpret_cast<uint8_t*>(s_cons + NW);
+  uint8_t* s_act = reinterpret_cast<uint8_t*>(s_cons + (kLanes ? 0 : NW));   // lanes: no WarpCons
   // agent binning (large A): cell ends after the scatter, sorted agent ids, agent cell
   int* s_cend = reinterpret_cast<int*>(s_act + ((A + 15) & ~15));
   int* s_sorted = s_cend + bins.ncx * bins.ncy + 1;
@@ -1215,14 +1215,19 @@ static RunLayout run_layout(int E, int A, int T) {
 }
 
 constexpr int kRoundStreams = 8;
-static long long g_last_rounds = 0;   // rounds launched by the last cw_crowd_run   // max; CW_RUN_STREAMS picks how many are used
+static long long g_last_rounds = 0;   // rounds launched by the last cw_crowd_run
 
 template <int NT>
 static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const double* rp,
                       const double* rv, double rr, const uint8_t* em, int ticks, void* scratch,
                       cudaStream_t st) {
   const Bins bins = make_bins(P);
-  const size_t sm = cw_crowd_step_smem_bytes(P.A, NT) + bins_smem_bytes(bins, P.A);
+  const bool lanes_ok = bins.ncx == 0 && P.max_neighbors <= MAXK;
+  // the lane path needs no per-warp constraint block: a smaller footprint lets two
+  // round CTAs share an SM with a search-server CTA
+  const size_t sm = lanes_ok ? (size_t)P.A * 7 * sizeof(double) + (size_t)((P.A + 15) & ~15) + 16 +
+                                   (size_t)P.A * 3 * sizeof(float)
+                             : cw_crowd_step_smem_bytes(P.A, NT) + bins_smem_bytes(bins, P.A);
   static bool attrs = false;
   if (!attrs) {
     cudaFuncSetAttribute(k_astar<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -1244,7 +1249,7 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
   }
   // lane-per-agent ORCA below 128 agents; the binned warp path (96 registers,
   // so its CTAs share SMs with the search server) above
-  const bool lanes = bins.ncx == 0 && P.max_neighbors <= MAXK;
+  const bool lanes = lanes_ok;
   if (sm > 48 * 1024) {
     cudaFuncSetAttribute(k_round<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cudaFuncSetAttribute(k_round<NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
