@@ -510,13 +510,20 @@ def _ref_worker(args):
     from oracle.rng import child_seed
     import json as _json
     cat = S.load_catalog_tuples(_json.load(open(os.path.join(ROOT, "paper_2505_00690_b200", "data", "catalog.json"))))
+    from oracle import routes as R
     s = child_seed(0, "env", env_id)
     spec = make_spec(cfg)
+    # one env sample as BatchedEnv builds it: generate_scene (incl. raster and the
+    # route anchors, scene.py:38-90), crowd spawn (step.py:37) and _prepare_env
+    # (nearest-obstacle BFS, field.py:60-67)
+    ts = time.perf_counter()
     sc = S.generate_scene(dict(seed=s, extent=spec.extent_m, res=cfg["res"], task=cfg["task"], split="Train",
                                density=spec.object_density, mix=MIX), cat)
+    R.sample_route_anchors(sc["labels"], cfg["res"], s, spec.extent_m, cfg["task"])
     sp = C.spawn_agents(sc["labels"], cfg["res"], cfg["peds"], child_seed(s, "crowd", 0))
     f = C.CrowdFieldOracle([(sc["labels"], cfg["res"])], C.Config(neighbor_distance=cfg["nd"]),
                            [child_seed(s, "crowd-run")])
+    t_scene = time.perf_counter() - ts
     f.set_agents([sp])
     for _ in range(warm):
         f.step()
@@ -525,7 +532,7 @@ def _ref_worker(args):
         t0 = time.perf_counter()
         f.step()
         t.append(time.perf_counter() - t0)
-    return t
+    return t, t_scene
 
 
 def run_reference(args):
@@ -539,8 +546,10 @@ def run_reference(args):
     warm = max(0, min(args.warmup, 5))
     with mp.get_context("spawn").Pool(cores) as pool:
         t0 = time.perf_counter()
-        times = pool.map(_ref_worker, [(i, steps, warm, dict(CFG)) for i in range(cores)])
+        res = pool.map(_ref_worker, [(i, steps, warm, dict(CFG)) for i in range(cores)])
         wall = time.perf_counter() - t0
+    times = [r[0] for r in res]
+    t_scene = max(r[1] for r in res)                 # all cores sample one scene each, in parallel
     per_step = np.max(np.array(times), axis=0)       # all cores step in parallel
     total = float(per_step.sum())
     value = cores * steps / total
@@ -557,7 +566,10 @@ def run_reference(args):
                              "sample": f"{cores} {args.config} envs (one per core) x {steps} crowd ticks; "
                                        f"oracle port of the reference algorithm; wall {wall:.1f}s incl. scene gen"},
             "e2e": {"value": round(value, 3), "unit": "env-steps/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "scenes_per_sec": round(cores / t_scene, 4),
+            "sample_includes": "generate_scene (zones, WFC terrain, placement, raster + heightfield), route "
+                               "anchors, crowd spawn, nearest-obstacle map; one scene per core"}
     print(json.dumps(line), flush=True)
 
 
