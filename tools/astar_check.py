@@ -59,9 +59,12 @@ for t in range(T):
     reqs = f.astar_req_t[:nreq].cpu().numpy()
     phase(2)
     torch.cuda.synchronize()
+    per_tick = 0
+    cap = int(os.environ.get("ASTAR_CHECK_MAX", 1 << 30))
     for e, a, st, gl in reqs:
-        if e not in labs:
+        if e not in labs or per_tick >= cap:
             continue
+        per_tick += 1
         ref = C.astar(labs[e], (st // nx, st % nx), (gl // nx, gl % nx))
         n = int(f.path_n_t[e, a])
         cells = f.path_cells_t[e, a, :max(n - 1, 0)].cpu().numpy()
