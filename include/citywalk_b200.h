@@ -194,6 +194,17 @@ int cw_crowd_step_phases(const cw_crowd_params* params, const cw_crowd_state* st
  * scratch: cw_crowd_run_scratch_bytes(E, A, ticks) bytes of device memory.
  * Returns 0, a CUDA error, 9001 (device queue error) or 9002 (host time limit). */
 size_t cw_crowd_run_scratch_bytes(int E, int A, int ticks);
+/* One segment of a tick window [0, ticks): env e runs its ticks start_tick[e] ..
+ * stop_tick[e] - 1 (NULL: 0 / ticks).  flags bit 0: first segment of the window
+ * (resets the per-(env, tick) gap history kept in scratch), bit 1: last segment
+ * (publishes last_gap_by_env from it).  Between segments the caller may replace
+ * env state (e.g. re-sample the scenes of the envs stopped at a re-sampling
+ * tick); per env the result equals the same ticks run synchronously.
+ * cw_crowd_run == one segment with NULL, NULL, flags 3. */
+int cw_crowd_run_window(const cw_crowd_params* params, const cw_crowd_state* state,
+                        const double* robot_pos, const double* robot_vel, double robot_radius,
+                        const uint8_t* env_mask, int threads, int ticks, const int32_t* start_tick,
+                        const int32_t* stop_tick, int flags, void* scratch, void* stream);
 /* Round kernels the last cw_crowd_run launched (host-only query; the run also
  * launches one init, one search-server and one finish kernel). */
 long long cw_crowd_run_rounds(void);

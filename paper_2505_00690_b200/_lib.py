@@ -105,7 +105,7 @@ EXPORTS = ["cw_scene_seed_scratch_bytes", "cw_sample_scenes", "cw_spawn_agents",
            "cw_traversability_scratch_bytes", "cw_traversability", "cw_robot_step", "cw_robot_observe",
            "cw_route_scratch_bytes", "cw_route_anchors", "cw_seed_streams", "cw_child_seeds", "cw_abi_sizes",
            "cw_scene_rle", "cw_crowd_run_scratch_bytes", "cw_crowd_run",
-           "cw_crowd_run_rounds"]
+           "cw_crowd_run_rounds", "cw_crowd_run_window"]
 
 _lib = None
 
@@ -154,6 +154,9 @@ def lib():
                                        P, ctypes.c_double, P, ctypes.c_int, ctypes.c_int, P]
     L.cw_crowd_run_scratch_bytes.restype = ctypes.c_size_t
     L.cw_crowd_run_scratch_bytes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int]
+    L.cw_crowd_run_window.restype = ctypes.c_int
+    L.cw_crowd_run_window.argtypes = [ctypes.POINTER(CrowdParams), ctypes.POINTER(CrowdState), P, P,
+                                      ctypes.c_double, P, ctypes.c_int, ctypes.c_int, P, P, ctypes.c_int, P, P]
     L.cw_crowd_run_rounds.restype = ctypes.c_longlong
     L.cw_crowd_run_rounds.argtypes = []
     L.cw_crowd_run.restype = ctypes.c_int

@@ -372,6 +372,39 @@ class CrowdField:
         if check:
             self.check_flags()
 
+    def run_window(self, ticks, start, stop, first, last, robot_pos=None, robot_vel=None, robot_radius=0.35,
+                   env_mask=None, stream=None, check=True, threads=None):
+        """One segment of a ``ticks``-long window (``cw_crowd_run_window``): env e runs
+        its ticks ``start[e]`` .. ``stop[e] - 1`` without a barrier across envs.
+        ``first`` resets the window's per-(env, tick) gap history, ``last`` publishes
+        ``last_gap_by_env`` from it.  Between segments the caller may replace env
+        state (re-sampled scenes, respawned crowds); per env the result equals the
+        same ticks stepped synchronously."""
+        import torch
+        ticks = int(ticks)
+        if self.A == 0 or self.E == 0 or ticks <= 0:
+            return
+        if not hasattr(self, "_p") or self._p.A != self.A:
+            self.prepare_step()
+        rp = self._dev(robot_pos, torch.float64, (self.E, 2))
+        rv = self._dev(robot_vel, torch.float64, (self.E, 2)) if robot_pos is not None else None
+        em = self._dev(env_mask, torch.uint8, (self.E,))
+        st = torch.as_tensor(start, dtype=torch.int32).to(self.device).contiguous()
+        sp = torch.as_tensor(stop, dtype=torch.int32).to(self.device).contiguous()
+        nbytes = int(_lib.lib().cw_crowd_run_scratch_bytes(self.E, self.A, ticks))
+        if getattr(self, "_win_scratch", None) is None or self._win_scratch.numel() < nbytes:
+            if not first:
+                raise ValueError("run_window: the window's scratch is gone; start it with first=True")
+            self._win_scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        flags = (1 if first else 0) | (2 if last else 0)
+        err = _lib.lib().cw_crowd_run_window(self._p, self._s, _lib.ptr(rp), _lib.ptr(rv), float(robot_radius),
+                                             _lib.ptr(em), int(threads or self.run_threads or self._run_nt()),
+                                             ticks, _lib.ptr(st), _lib.ptr(sp), flags,
+                                             _lib.ptr(self._win_scratch), _lib.stream_ptr(stream))
+        _lib.check(err, "cw_crowd_run_window")
+        if check:
+            self.check_flags()
+
     def _run_nt(self):
         """Round CTA size: one lane per agent below 128 agents (lane ORCA / guide),
         else the warp-per-agent shape with cell binning."""

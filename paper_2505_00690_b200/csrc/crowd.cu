@@ -1048,6 +1048,16 @@ __global__ void __launch_bounds__(NT) k_round(cw_crowd_params P, cw_crowd_state 
     const int e = s_e;
     if (e < 0) return;
     int t = s_st >> 2;
+    const int stop = ra.stop ? ra.stop[e] : ra.T;
+    if (t >= stop) {   // nothing to run in this call (cw_crowd_run_window)
+      if (threadIdx.x == 0) {
+        ra.env_state[e] = (t << 2) | kRunDone;
+        __threadfence();
+        if (atomicAdd(&ra.q->n_done, 1) + 1 == ra.E) atomicExch(&ra.q->shutdown, 1);
+      }
+      __syncthreads();
+      continue;
+    }
     bool guide = (s_st & 3) == kRunGuide;
     for (int burst = 0;; ++burst) {
       if (burst == ra.burst) {   // yield to the envs queued behind this one
@@ -1091,7 +1101,7 @@ __global__ void __launch_bounds__(NT) k_round(cw_crowd_params P, cw_crowd_state 
       }
       orca_env<NT, kLanes>(P, S, e, robot_pos, robot_vel, robot_radius, env_mask, bins, sm, &ra, t);
       __syncthreads();
-      if (++t == ra.T) {
+      if (++t == stop) {
         if (threadIdx.x == 0) {
           if (ra.trace) {
             long long* tr = ra.trace + (size_t)e * 8;
@@ -1116,12 +1126,16 @@ __global__ void k_run_init(RunArgs ra) {
   if (ra.trace && i < (size_t)ra.E) ra.trace[i * 8 + kTrMark] = global_ns();
   // every env starts in the ready ring (positions 0..E-1)
   if (i == 0) *ra.q = RunQueue{0ull, 0ull, 0, 0, 0, 0, 0ull, (unsigned long long)ra.E, 0ull, 0ull};
-  if (i < (size_t)ra.E) { ra.env_state[i] = 0; ra.pending[i] = 0; ra.ritems[i] = (int)i; }
+  if (i < (size_t)ra.E) {
+    ra.env_state[i] = (ra.start ? ra.start[i] : 0) << 2;   // kRunGuide at the env's first tick
+    ra.pending[i] = 0;
+    ra.ritems[i] = (int)i;
+  }
   if (i <= ra.rmask) {
     ra.rseq[i] = i < (size_t)ra.E ? i + 1 : i;
     ra.useq[i] = i;
   }
-  if (i < (size_t)ra.T) ra.anynb[i] = 0;
+  if (ra.init_hist && i < (size_t)ra.T) ra.anynb[i] = 0;
   if (i <= ra.mask) ra.seq[i] = i;
 }
 
@@ -1219,8 +1233,8 @@ static long long g_last_rounds = 0;   // rounds launched by the last cw_crowd_ru
 
 template <int NT>
 static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const double* rp,
-                      const double* rv, double rr, const uint8_t* em, int ticks, void* scratch,
-                      cudaStream_t st) {
+                      const double* rv, double rr, const uint8_t* em, int ticks, const int32_t* start,
+                      const int32_t* stop, int flags, void* scratch, cudaStream_t st) {
   const Bins bins = make_bins(P);
   const bool lanes_ok = bins.ncx == 0 && P.max_neighbors <= MAXK;
   // the lane path needs no per-warp constraint block: a smaller footprint lets two
@@ -1271,6 +1285,9 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
   ra.anynb = reinterpret_cast<int*>(base + L.anynb);
   ra.T = ticks;
   ra.E = P.E;
+  ra.start = start;
+  ra.stop = stop;
+  ra.init_hist = flags & 1;
   ra.mask = L.cap - 1;
   static const int burst = getenv("CW_RUN_BURST") ? atoi(getenv("CW_RUN_BURST")) : 8;
   ra.burst = std::max(1, burst);
@@ -1402,7 +1419,7 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
     cudaStreamWaitEvent(H.rs[0], H.rounds_done[k], 0);
   }
   cudaStreamWaitEvent(H.rs[0], H.srv_done, 0);
-  k_run_finish<<<1, 256, 0, H.rs[0]>>>(S, ra);
+  if (flags & 2) k_run_finish<<<1, 256, 0, H.rs[0]>>>(S, ra);
   cudaEventRecord(H.rounds_done[0], H.rs[0]);
   cudaStreamWaitEvent(st, H.rounds_done[0], 0);
   if (status) return status;
@@ -1476,20 +1493,30 @@ long long cw_crowd_run_rounds(void) { return cw::g_last_rounds; }
 
 // `ticks` synchronous cw_crowd_step calls with the same inputs, run without a
 // per-tick barrier (runq.cuh); same final state bit for bit.
-int cw_crowd_run(const cw_crowd_params* P, const cw_crowd_state* S, const double* robot_pos,
-                 const double* robot_vel, double robot_radius, const uint8_t* env_mask, int threads,
-                 int ticks, void* scratch, void* stream) {
+int cw_crowd_run_window(const cw_crowd_params* P, const cw_crowd_state* S, const double* robot_pos,
+                        const double* robot_vel, double robot_radius, const uint8_t* env_mask, int threads,
+                        int ticks, const int32_t* start_tick, const int32_t* stop_tick, int flags,
+                        void* scratch, void* stream) {
   using namespace cw;
   if (P->E <= 0 || P->A <= 0 || ticks <= 0) return 0;
   if (!scratch) return (int)cudaErrorInvalidValue;
   cudaStream_t st = (cudaStream_t)stream;
+  const double* rp = robot_pos;
+  const double* rv = robot_vel;
   if (threads == 32)
-    return launch_run<32>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, ticks, scratch, st);
+    return launch_run<32>(*P, *S, rp, rv, robot_radius, env_mask, ticks, start_tick, stop_tick, flags, scratch, st);
   if (threads == 256)
-    return launch_run<256>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, ticks, scratch, st);
+    return launch_run<256>(*P, *S, rp, rv, robot_radius, env_mask, ticks, start_tick, stop_tick, flags, scratch, st);
   if (threads == 64)
-    return launch_run<64>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, ticks, scratch, st);
-  return launch_run<128>(*P, *S, robot_pos, robot_vel, robot_radius, env_mask, ticks, scratch, st);
+    return launch_run<64>(*P, *S, rp, rv, robot_radius, env_mask, ticks, start_tick, stop_tick, flags, scratch, st);
+  return launch_run<128>(*P, *S, rp, rv, robot_radius, env_mask, ticks, start_tick, stop_tick, flags, scratch, st);
+}
+
+int cw_crowd_run(const cw_crowd_params* P, const cw_crowd_state* S, const double* robot_pos,
+                 const double* robot_vel, double robot_radius, const uint8_t* env_mask, int threads,
+                 int ticks, void* scratch, void* stream) {
+  return cw_crowd_run_window(P, S, robot_pos, robot_vel, robot_radius, env_mask, threads, ticks, nullptr,
+                             nullptr, 3, scratch, stream);
 }
 
 // Bytes of A* scratch (astar_rec) per k_astar search warp for an nx x ny grid.

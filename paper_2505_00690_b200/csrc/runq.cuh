@@ -42,7 +42,10 @@ struct RunArgs {                  // kernel parameter (pointers into cw_crowd_ru
   unsigned long long rmask;
   double* gap_hist;               // (E, T) per-tick gap of every env
   int* anynb;                     // (T) some env had K > 0 at tick t
-  int T, E;
+  int T, E;                       // T: length of the tick window (history), E: envs
+  const int* start;               // per env first tick of this call (nullptr: 0)
+  const int* stop;                // per env tick to stop at, exclusive (nullptr: T)
+  int init_hist;                  // reset the (env, tick) gap history (first call of a window)
   int burst;                      // ticks one round CTA may run back to back (bounds round length)
   unsigned long long mask;        // ring capacity - 1 (power of two)
   long long* trace;               // debug (CW_RUN_TRACE): per env 8 x i64, see kTr*

@@ -288,3 +288,54 @@ class BatchedEnv:
         r = self.robot
         return Observation(depth=r.depth[i].cpu().numpy(), goal_vector=r.goal_vector[i].cpu().numpy(),
                            projected_velocity=float(r.proj_vel[i]), height_map=r.height_map[i].cpu().numpy())
+
+
+def run_with_resampling(sampler, field, env_seeds, counts, events, ticks, robot_pos=None, robot_vel=None,
+                        robot_radius=0.35):
+    """``ticks`` crowd ticks of every env where env e's scene is re-sampled before
+    tick t for every e in ``events[t]`` (the bench's cfg5 driver):
+    re-sample seed ``child_seed(env_seed, "resample", n)``, crowd respawn seed
+    ``child_seed(env_seed, "crowd", n)`` with n the env's running count (``counts``,
+    int64 device tensor, updated in place) -- the same state as re-sampling and
+    stepping tick by tick (``batch.py:326-339`` + ``CrowdField.step``).
+
+    Runs as segments of ``cw_crowd_run_window``: each env advances without a
+    barrier up to its next re-sampling tick; the envs stopped there are re-sampled
+    together (one batched ``SceneSampler.sample``) and respawned, and the next
+    segment continues.  Returns the number of re-sampled scenes."""
+    import torch
+    dev = field.device
+    E = field.E
+    ev_ticks = [[] for _ in range(E)]
+    for t in range(ticks):
+        for e in np.asarray(events[t], dtype=np.int64).reshape(-1):
+            ev_ticks[int(e)].append(t)
+    nxt = np.zeros(E, dtype=np.int64)            # index of each env's next event
+    cur = np.zeros(E, dtype=np.int64)            # each env's next tick
+    env_t = env_seeds if isinstance(env_seeds, torch.Tensor) else seeds_to_tensor(env_seeds, dev)
+    first, resampled = True, 0
+    while True:
+        due = [e for e in range(E) if nxt[e] < len(ev_ticks[e]) and ev_ticks[e][nxt[e]] == cur[e]]
+        if due:
+            sl = torch.as_tensor(due, dtype=torch.int64, device=dev)
+            counts[sl] += 1
+            env_k = env_t[sl]
+            sampler.sample(child_seeds_device(env_k, "resample", counts[sl]),
+                           child_seeds_device(env_k, "crowd", counts[sl]), slots=sl, check=False)
+            field.set_from_spawn(sampler.batch, rows=sl)
+            for e in due:
+                nxt[e] += 1
+            resampled += len(due)
+        if (cur >= ticks).all():
+            break
+        stop = np.array([ev_ticks[e][nxt[e]] if nxt[e] < len(ev_ticks[e]) else ticks for e in range(E)],
+                        dtype=np.int64)
+        last = bool((stop >= ticks).all())
+        field.run_window(ticks, cur.astype(np.int32), stop.astype(np.int32), first, last, robot_pos, robot_vel,
+                         robot_radius, check=False)
+        first = False
+        cur = stop
+        if last:
+            break
+    field.check_flags()
+    return resampled

@@ -167,3 +167,46 @@ def test_run_binned_warp_path(torch_cuda):
         fs[0].step(rp, rv, 0.35)
     fs[1].run(12, rp, rv, 0.35)
     _same(fs[0], fs[1], "A=140 binned")
+
+
+def test_run_with_resampling_matches_synchronous_driver(torch_cuda):
+    """cfg5-style driver: ~10 % of envs re-sampled before each tick.  The segmented
+    run (envcore.run_with_resampling: cw_crowd_run_window between batched
+    re-samples) leaves the state of re-sampling + stepping tick by tick."""
+    import torch
+    from oracle.rng import child_seed
+    from paper_2505_00690_b200.crowd import CrowdConfig, CrowdField
+    from paper_2505_00690_b200.envcore import run_with_resampling
+    from paper_2505_00690_b200.rng import child_seeds_device, seeds_to_tensor
+    from paper_2505_00690_b200.urbangen import SceneSampler, SceneSpec, TaskKind
+    E, T = 16, 40
+    seeds = [child_seed(0, "env", i) for i in range(E)]
+    spec = SceneSpec(seed=0, extent_m=(32.0, 32.0), task_kind=TaskKind.NAV_DYNAMIC, pedestrian_count=8,
+                     object_density=20 / 41, terrain_mix=MIX, grid_resolution_m=0.25)
+    rng = np.random.default_rng(8)
+    events = [np.flatnonzero(rng.random(E) < 0.1) for _ in range(T)]
+    out = []
+    for mode in ("sync", "run"):
+        sampler = SceneSampler(spec, E)
+        b = sampler.sample(seeds, [child_seed(s, "crowd", 0) for s in seeds])
+        f = CrowdField(b, CrowdConfig(), [child_seed(s, "crowd-run") for s in seeds])
+        f.set_from_spawn(b)
+        env_t = seeds_to_tensor(seeds, "cuda")
+        counts = torch.zeros(E, dtype=torch.int64, device="cuda")
+        rp, rv = _robot(b, E, 0.25, seed=2)
+        if mode == "sync":
+            for t in range(T):
+                if len(events[t]):
+                    sl = torch.as_tensor(events[t], dtype=torch.int64, device="cuda")
+                    counts[sl] += 1
+                    sampler.sample(child_seeds_device(env_t[sl], "resample", counts[sl]),
+                                   child_seeds_device(env_t[sl], "crowd", counts[sl]), slots=sl)
+                    f.set_from_spawn(b, rows=sl)
+                f.step(rp, rv, 0.35)
+        else:
+            n = run_with_resampling(sampler, f, env_t, counts, events, T, rp, rv, 0.35)
+            assert n == sum(len(x) for x in events)
+        torch_cuda.cuda.synchronize()
+        out.append((f, b.labels.cpu().numpy()))
+    assert np.array_equal(out[0][1], out[1][1])
+    _same(out[0][0], out[1][0], "resampling driver")
