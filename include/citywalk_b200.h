@@ -149,6 +149,7 @@ typedef struct cw_crowd_params {
   int32_t heap_cap;     /* A* far-pool entries (16 B) per search warp */
   int32_t astar_ctas;   /* persistent k_astar CTAs (one per SM) */
   int32_t astar_warps;  /* search warps per CTA: 1 = latency shape, else cw_astar_warps() */
+  int32_t run_server_warps; /* cw_crowd_run search-server warps per CTA: 0 = 2, or 1 / 2 / 4 */
 } cw_crowd_params;
 
 /* Device-resident CrowdField state (field.py:47-58) + guidance/A* scratch. */

@@ -58,7 +58,7 @@ class CrowdParams(ctypes.Structure):
         ("nd2", c_f64), ("nd2_f32", c_f32), ("max_neighbors", c_i32), ("dt", c_f64),
         ("safety_margin", c_f64), ("goal_reach2", c_f64), ("stall_c", c_f64), ("stall_s", c_f64),
         ("resample_goals", c_i32), ("use_static", c_i32), ("path_cap", c_i32), ("heap_cap", c_i32),
-        ("astar_ctas", c_i32), ("astar_warps", c_i32),
+        ("astar_ctas", c_i32), ("astar_warps", c_i32), ("run_server_warps", c_i32),
     ]
 
 

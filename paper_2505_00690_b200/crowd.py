@@ -98,6 +98,7 @@ class CrowdField:
         self.threads = threads
         self.run_threads = None   # cw_crowd_run CTA size; None: one lane per agent
         self.run_history_bytes = 256 << 20   # per-call cap of the run's (env, tick) gap history
+        self.run_server_warps = None   # search warps per server CTA in cw_crowd_run (None: 2)
         self.astar_warps = astar_warps
         if isinstance(occupancies, SceneBatch):
             b = occupancies
@@ -301,6 +302,7 @@ class CrowdField:
         # few replans per tick (small batches): one search warp per SM, whose tick
         # latency is the longest search; large batches: four per SM for throughput
         p.astar_warps = self.astar_warps or (1 if self.E * self.A < 131072 else 4)
+        p.run_server_warps = int(self.run_server_warps or 0)
         return p
 
     def _state(self):

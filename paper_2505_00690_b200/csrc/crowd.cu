@@ -1334,7 +1334,8 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
   // server's warps wait on the rounds' requests: they must never starve them).
   // two search warps per CTA: twice the concurrent searches of the latency shape
   // at nearly its per-expansion cost (the run is bound by each env's own chain)
-  static const int srv_w = getenv("CW_RUN_SERVER_W") ? atoi(getenv("CW_RUN_SERVER_W")) : 2;
+  static const int srv_w_env = getenv("CW_RUN_SERVER_W") ? atoi(getenv("CW_RUN_SERVER_W")) : 0;
+  const int srv_w = srv_w_env ? srv_w_env : (P.run_server_warps ? P.run_server_warps : 2);
   static const int srv_kb = getenv("CW_RUN_SERVER_KB") ? atoi(getenv("CW_RUN_SERVER_KB")) : 0;
   AstarShape shp = astar_shape(P.nx, P.ny, srv_w == 4 ? kAstarWarps : srv_w == 2 ? 2 : 1, srv_kb);
   shp.NS = std::min(shp.NS, astar_ns_cap(P.nx, P.ny));   // the global store holds NS slot ids

@@ -291,7 +291,7 @@ class BatchedEnv:
 
 
 def run_with_resampling(sampler, field, env_seeds, counts, events, ticks, robot_pos=None, robot_vel=None,
-                        robot_radius=0.35):
+                        robot_radius=0.35, window=5):
     """``ticks`` crowd ticks of every env where env e's scene is re-sampled before
     tick t for every e in ``events[t]`` (the bench's cfg5 driver):
     re-sample seed ``child_seed(env_seed, "resample", n)``, crowd respawn seed
@@ -299,10 +299,11 @@ def run_with_resampling(sampler, field, env_seeds, counts, events, ticks, robot_
     int64 device tensor, updated in place) -- the same state as re-sampling and
     stepping tick by tick (``batch.py:326-339`` + ``CrowdField.step``).
 
-    Runs as segments of ``cw_crowd_run_window``: each env advances without a
-    barrier up to its next re-sampling tick; the envs stopped there are re-sampled
-    together (one batched ``SceneSampler.sample``) and respawned, and the next
-    segment continues.  Returns the number of re-sampled scenes."""
+    Runs in windows of ``window`` ticks (``cw_crowd_run_window`` segments): inside a
+    window every env advances without a barrier to the window's end or to its next
+    re-sampling tick; at the window boundary the envs stopped at a re-sampling tick
+    are re-sampled together (one batched ``SceneSampler.sample``) and respawned, and
+    they catch up in the next window.  Returns the number of re-sampled scenes."""
     import torch
     dev = field.device
     E = field.E
@@ -314,6 +315,13 @@ def run_with_resampling(sampler, field, env_seeds, counts, events, ticks, robot_
     cur = np.zeros(E, dtype=np.int64)            # each env's next tick
     env_t = env_seeds if isinstance(env_seeds, torch.Tensor) else seeds_to_tensor(env_seeds, dev)
     first, resampled = True, 0
+    windows = rounds = samples = 0
+    w_end = 0
+    # every re-sampled env plans all its agents on its first tick: bursts of
+    # searches, served best by the wide (4 warps per CTA) search server
+    saved = field.run_server_warps
+    field.run_server_warps = saved or 4
+    field.prepare_step()
     while True:
         due = [e for e in range(E) if nxt[e] < len(ev_ticks[e]) and ev_ticks[e][nxt[e]] == cur[e]]
         if due:
@@ -326,16 +334,26 @@ def run_with_resampling(sampler, field, env_seeds, counts, events, ticks, robot_
             for e in due:
                 nxt[e] += 1
             resampled += len(due)
+            samples += 1
         if (cur >= ticks).all():
             break
-        stop = np.array([ev_ticks[e][nxt[e]] if nxt[e] < len(ev_ticks[e]) else ticks for e in range(E)],
-                        dtype=np.int64)
+        w_end = min(ticks, max(w_end + window, int(cur.min()) + 1))
+        nev = np.array([ev_ticks[e][nxt[e]] if nxt[e] < len(ev_ticks[e]) else ticks for e in range(E)],
+                       dtype=np.int64)
+        stop = np.maximum(cur, np.minimum(nev, np.maximum(w_end, cur)))
+        # an env due for a re-sample at its current tick waits for the next boundary
+        stop = np.where(nev == cur, cur, stop)
         last = bool((stop >= ticks).all())
         field.run_window(ticks, cur.astype(np.int32), stop.astype(np.int32), first, last, robot_pos, robot_vel,
                          robot_radius, check=False)
+        windows += 1
+        rounds += int(_lib.lib().cw_crowd_run_rounds())
         first = False
         cur = stop
         if last:
             break
+    field.run_server_warps = saved
+    field.prepare_step()
     field.check_flags()
+    field.last_run_stats = {"windows": windows, "rounds": rounds, "sample_calls": samples}
     return resampled
