@@ -443,7 +443,8 @@ def run_ours(args):
             line["run"] = {"rounds": run["rounds"], "astar_expansions": run["expansions"],
                            "resampled_envs": run["resampled"],
                            "what": "cw_crowd_run: persistent A* server + ready-env ring + round kernels"
-                                   + ("; cfg5 re-sampling as barrier-free segments between batched re-samples"
+                                   + ("; cfg5 re-sampling: barrier-free 5-tick windows (cw_crowd_run_window) "
+                                      "between batched re-samples of the envs that reached their re-sample tick"
                                       if CFG["resample"] else "")}
             if CFG["resample"]:
                 line["config"]["resampled_envs"] = run["resampled"]
