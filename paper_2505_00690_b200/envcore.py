@@ -290,8 +290,20 @@ class BatchedEnv:
                            projected_velocity=float(r.proj_vel[i]), height_map=r.height_map[i].cpu().numpy())
 
 
+_SCENE_OUT = None
+
+
+def _scene_out_fields():
+    """SceneBatch outputs a re-sampled row consists of (everything but scratch)."""
+    global _SCENE_OUT
+    if _SCENE_OUT is None:
+        _SCENE_OUT = [n for n in _lib.SCENE_BUFFER_FIELDS if not n.startswith("scratch")] + [
+            "routes", "n_routes", "scene_seed"]
+    return _SCENE_OUT
+
+
 def run_with_resampling(sampler, field, env_seeds, counts, events, ticks, robot_pos=None, robot_vel=None,
-                        robot_radius=0.35, window=5):
+                        robot_radius=0.35, window=5, overlap=False):
     """``ticks`` crowd ticks of every env where env e's scene is re-sampled before
     tick t for every e in ``events[t]`` (the bench's cfg5 driver):
     re-sample seed ``child_seed(env_seed, "resample", n)``, crowd respawn seed
@@ -302,11 +314,17 @@ def run_with_resampling(sampler, field, env_seeds, counts, events, ticks, robot_
     Runs in windows of ``window`` ticks (``cw_crowd_run_window`` segments): inside a
     window every env advances without a barrier to the window's end or to its next
     re-sampling tick; at the window boundary the envs stopped at a re-sampling tick
-    are re-sampled together (one batched ``SceneSampler.sample``) and respawned, and
-    they catch up in the next window.  Returns the number of re-sampled scenes."""
+    get their new scene and respawn, and catch up in the next window.  The envs due
+    at a boundary are known when its window starts (next re-sampling tick <= window
+    end), so with ``overlap`` their scenes are sampled into a pool batch on a side
+    stream while the window runs and copied into their rows at the boundary (off by
+    default: the sampling kernels compete with the run for the SMs, measured slower).
+    Returns the number of re-sampled scenes."""
     import torch
+    from .urbangen import SceneSampler
     dev = field.device
     E = field.E
+    batch = sampler.batch
     ev_ticks = [[] for _ in range(E)]
     for t in range(ticks):
         for e in np.asarray(events[t], dtype=np.int64).reshape(-1):
@@ -317,32 +335,69 @@ def run_with_resampling(sampler, field, env_seeds, counts, events, ticks, robot_
     first, resampled = True, 0
     windows = rounds = samples = 0
     w_end = 0
-    # every re-sampled env plans all its agents on its first tick: bursts of
-    # searches, served best by the wide (4 warps per CTA) search server
     saved = field.run_server_warps
-    field.run_server_warps = saved or 4
+    field.run_server_warps = saved or 4   # respawned envs plan every agent: search bursts
     field.prepare_step()
+
+    def next_ev():
+        return np.array([ev_ticks[e][nxt[e]] if nxt[e] < len(ev_ticks[e]) else ticks for e in range(E)],
+                        dtype=np.int64)
+
+    def resample_now(rows):
+        nonlocal resampled, samples
+        sl = torch.as_tensor(rows, dtype=torch.int64, device=dev)
+        counts[sl] += 1
+        env_k = env_t[sl]
+        sampler.sample(child_seeds_device(env_k, "resample", counts[sl]),
+                       child_seeds_device(env_k, "crowd", counts[sl]), slots=sl, check=False)
+        field.set_from_spawn(batch, rows=sl)
+        nxt[rows] += 1
+        resampled += len(rows)
+        samples += 1
+
+    side = torch.cuda.Stream(device=dev) if overlap else None
+    pool = None
+    pending = None                               # (env rows, pool stream event) sampled ahead
     while True:
-        due = [e for e in range(E) if nxt[e] < len(ev_ticks[e]) and ev_ticks[e][nxt[e]] == cur[e]]
-        if due:
-            sl = torch.as_tensor(due, dtype=torch.int64, device=dev)
+        if pending is not None:                  # boundary: install the scenes sampled ahead
+            rows, done = pending
+            torch.cuda.current_stream().wait_event(done)
+            sl = torch.as_tensor(rows, dtype=torch.int64, device=dev)
+            k = len(rows)
+            for name in _scene_out_fields():
+                getattr(batch, name).index_copy_(0, sl, getattr(pool.batch, name)[:k])
             counts[sl] += 1
-            env_k = env_t[sl]
-            sampler.sample(child_seeds_device(env_k, "resample", counts[sl]),
-                           child_seeds_device(env_k, "crowd", counts[sl]), slots=sl, check=False)
-            field.set_from_spawn(sampler.batch, rows=sl)
-            for e in due:
-                nxt[e] += 1
-            resampled += len(due)
-            samples += 1
+            field.set_from_spawn(batch, rows=sl)
+            nxt[rows] += 1
+            resampled += k
+            pending = None
+        nev = next_ev()
+        due = np.flatnonzero((nev == cur) & (nev < ticks))   # re-sampling tick reached (or tick 0)
+        if due.size:
+            resample_now(due)
+            nev = next_ev()
         if (cur >= ticks).all():
             break
         w_end = min(ticks, max(w_end + window, int(cur.min()) + 1))
-        nev = np.array([ev_ticks[e][nxt[e]] if nxt[e] < len(ev_ticks[e]) else ticks for e in range(E)],
-                       dtype=np.int64)
         stop = np.maximum(cur, np.minimum(nev, np.maximum(w_end, cur)))
-        # an env due for a re-sample at its current tick waits for the next boundary
-        stop = np.where(nev == cur, cur, stop)
+        if overlap:
+            ahead = np.flatnonzero((nev > cur) & (nev <= w_end) & (nev < ticks))
+            if ahead.size:
+                if pool is None or pool.batch.E < ahead.size:
+                    cap = max(int(ahead.size * 1.5), 64)
+                    pool = SceneSampler(sampler.spec, cap, catalog=sampler.catalog, device=dev,
+                                        routes=sampler.routes)
+                sl = torch.as_tensor(ahead, dtype=torch.int64, device=dev)
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side):
+                    env_k = env_t[sl]
+                    cnt = counts[sl] + 1
+                    pool.sample(child_seeds_device(env_k, "resample", cnt), child_seeds_device(env_k, "crowd", cnt),
+                                stream=side, check=False)
+                    done = torch.cuda.Event()
+                    done.record(side)
+                pending = (ahead, done)
+                samples += 1
         last = bool((stop >= ticks).all())
         field.run_window(ticks, cur.astype(np.int32), stop.astype(np.int32), first, last, robot_pos, robot_vel,
                          robot_radius, check=False)
@@ -350,7 +405,7 @@ def run_with_resampling(sampler, field, env_seeds, counts, events, ticks, robot_
         rounds += int(_lib.lib().cw_crowd_run_rounds())
         first = False
         cur = stop
-        if last:
+        if last and pending is None:
             break
     field.run_server_warps = saved
     field.prepare_step()

@@ -169,7 +169,8 @@ def test_run_binned_warp_path(torch_cuda):
     _same(fs[0], fs[1], "A=140 binned")
 
 
-def test_run_with_resampling_matches_synchronous_driver(torch_cuda):
+@pytest.mark.parametrize("overlap", [False, True])
+def test_run_with_resampling_matches_synchronous_driver(overlap, torch_cuda):
     """cfg5-style driver: ~10 % of envs re-sampled before each tick.  The segmented
     run (envcore.run_with_resampling: cw_crowd_run_window between batched
     re-samples) leaves the state of re-sampling + stepping tick by tick."""
@@ -204,7 +205,7 @@ def test_run_with_resampling_matches_synchronous_driver(torch_cuda):
                     f.set_from_spawn(b, rows=sl)
                 f.step(rp, rv, 0.35)
         else:
-            n = run_with_resampling(sampler, f, env_t, counts, events, T, rp, rv, 0.35)
+            n = run_with_resampling(sampler, f, env_t, counts, events, T, rp, rv, 0.35, overlap=overlap)
             assert n == sum(len(x) for x in events)
         torch_cuda.cuda.synchronize()
         out.append((f, b.labels.cpu().numpy()))
