@@ -193,7 +193,8 @@ int cw_crowd_step_phases(const cw_crowd_params* params, const cw_crowd_state* st
  * Blocks the calling host thread until the run is done (it polls the device to
  * stop launching rounds); device work is ordered after prior work on `stream`.
  * scratch: cw_crowd_run_scratch_bytes(E, A, ticks) bytes of device memory.
- * Returns 0, a CUDA error, 9001 (device queue error) or 9002 (host time limit). */
+ * Returns 0, a CUDA error, 9001 (device queue error) or 9002 (no env-tick completed for
+ * 120 s: the host watchdog ended the run). */
 size_t cw_crowd_run_scratch_bytes(int E, int A, int ticks);
 /* One segment of a tick window [0, ticks): env e runs its ticks start_tick[e] ..
  * stop_tick[e] - 1 (NULL: 0 / ticks).  flags bit 0: first segment of the window

@@ -1101,6 +1101,7 @@ __global__ void __launch_bounds__(NT) k_round(cw_crowd_params P, cw_crowd_state 
       }
       orca_env<NT, kLanes>(P, S, e, robot_pos, robot_vel, robot_radius, env_mask, bins, sm, &ra, t);
       __syncthreads();
+      if (threadIdx.x == 0) atomicAdd(&ra.q->progress, 1);
       if (++t == stop) {
         if (threadIdx.x == 0) {
           if (ra.trace) {
@@ -1351,7 +1352,8 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
     k_astar<1, true><<<srv_ctas, 32, shp.smem, TS.hi>>>(P, S, shp.NC, shp.NS, ra);
   cudaEventRecord(H.srv_done, TS.hi);
   int err = (int)cudaGetLastError();
-  const auto t_begin = std::chrono::steady_clock::now();
+  auto t_progress = std::chrono::steady_clock::now();
+  int last_progress = -1;
   static const int n_rs = std::min(kRoundStreams, std::max(1, getenv("CW_RUN_STREAMS") ? atoi(getenv("CW_RUN_STREAMS")) : 4));
   static const int kInFlight = std::min(7, std::max(1, getenv("CW_RUN_INFLIGHT") ? atoi(getenv("CW_RUN_INFLIGHT")) : 6));
   static const bool debug = getenv("CW_RUN_DEBUG") != nullptr;
@@ -1379,8 +1381,14 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
       }
       if (pv[0] >= P.E) break;
       if (pv[2]) { status = 9001; break; }
-      const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_begin).count();
-      if (secs > 300.0 || (err = (int)cudaGetLastError()) != 0) { status = err ? err : 9002; break; }
+      // watchdog: a run may take long, but it must keep completing env-ticks
+      const auto now = std::chrono::steady_clock::now();
+      if (pv[3] != last_progress) {
+        last_progress = pv[3];
+        t_progress = now;
+      }
+      const double stalled = std::chrono::duration<double>(now - t_progress).count();
+      if (stalled > 120.0 || (err = (int)cudaGetLastError()) != 0) { status = err ? err : 9002; break; }
     }
   }
   g_last_rounds = n_rounds;

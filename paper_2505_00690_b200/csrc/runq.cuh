@@ -24,7 +24,7 @@ constexpr long long kIdleCycles = 64ll << 30;   // ~35 s backstop for an idle se
 
 struct RunQueue {                 // device-resident control words
   unsigned long long head, tail;  // search ring positions claimed by consumers / producers
-  int n_done, shutdown, error, pad;
+  int n_done, shutdown, error, progress;   // progress: env-ticks completed (wraps; host watchdog)
   unsigned long long rhead, rtail;  // ready-env ring (start, yields)
   unsigned long long uhead, utail;  // urgent ring: envs the server released (their chain waits)
 };
