@@ -820,30 +820,35 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
     // ---- write the guidance result (field.py:204-212)
     const size_t ia = (size_t)e * P.A + R.agent;
     int32_t* cells = S.path_cells + ia * P.path_cap;
-    int pn = 1;
+    int pn = 1, head = 0;
     double wx = S.goal[ia * 2], wy = S.goal[ia * 2 + 1];
     if (found == -1 && lane == 0) atomicCAS(&S.flags[1], 0, (int)CW_E_HEAPCAP);
     if (found == 1) {
-      int L = 1;
-      for (int v = goal; v != start; v = E.parent[v]) ++L;
-      if (L >= 2) {
-        if (L - 1 > P.path_cap) {
-          if (lane == 0) atomicCAS(&S.flags[1], 0, (int)CW_E_PATHCAP);
-        } else {
-          if (lane == 0) {
-            int k = L - 2;
-            for (int v = goal; k >= 0; v = E.parent[v]) cells[k--] = v;
-          }
-          __syncwarp();
-          pn = L;
-          const int f0 = cells[0];
-          wx = ((double)(f0 % nx) + 0.5) * P.res;
-          wy = ((double)(f0 / nx) + 0.5) * P.res;
+      // one walk of the parent chain (goal -> start, L2 pointer chasing), writing the
+      // cells back to front: the path is cells[head .. path_cap - 1] in forward order
+      int count = 0, over = 0;
+      if (lane == 0) {
+        for (int v = goal; v != start; v = E.parent[v]) {
+          if (count == P.path_cap) { over = 1; break; }
+          cells[P.path_cap - 1 - count] = v;
+          ++count;
         }
+      }
+      count = __shfl_sync(0xffffffffu, count, 0);
+      over = __shfl_sync(0xffffffffu, over, 0);
+      __syncwarp();
+      if (over) {
+        if (lane == 0) atomicCAS(&S.flags[1], 0, (int)CW_E_PATHCAP);
+      } else if (count >= 1) {
+        pn = count + 1;
+        head = P.path_cap - count;
+        const int f0 = cells[head];
+        wx = ((double)(f0 % nx) + 0.5) * P.res;
+        wy = ((double)(f0 / nx) + 0.5) * P.res;
       }
     }
     if (lane == 0) {
-      S.path_head[ia] = 0;
+      S.path_head[ia] = head;
       S.path_n[ia] = pn;
       S.waypoint[ia * 2] = wx;
       S.waypoint[ia * 2 + 1] = wy;

@@ -17,6 +17,12 @@ pytestmark = pytest.mark.gpu
 MIX = {"Flat": 0.25, "Slope": 0.25, "Stair": 0.25, "Rough": 0.25}
 
 
+def _path(f, e, a):
+    """The agent's guidance cells (path_cells[head : head + path_n - 1])."""
+    hd, n = int(f.path_head_t[e, a]), int(f.path_n_t[e, a])
+    return f.path_cells_t[e, a, hd:hd + n - 1].cpu().numpy().tolist()
+
+
 def _oracle_cells(passable, st, gl):
     from oracle import crowd as C
     ny, nx = passable.shape
@@ -44,7 +50,7 @@ def test_astar_regressions(warps, torch_cuda):
         f.step_phase(2)
         n = int(f.path_n_t[0, 0])
         assert n == len(want) + 1, (k, n, len(want) + 1)
-        assert f.path_cells_t[0, 0, :n - 1].cpu().numpy().tolist() == want, k
+        assert _path(f, 0, 0) == want, k
 
 
 @pytest.mark.parametrize("warps", [1, 4])
@@ -80,7 +86,7 @@ def test_every_search_matches_oracle_dense_scenes(warps, torch_cuda):
                 assert n == 1, (t, e, a)
                 continue
             assert n == len(want) + 1, (t, e, a, n, len(want) + 1)
-            assert f.path_cells_t[e, a, :n - 1].cpu().numpy().tolist() == want, (t, e, a)
+            assert _path(f, e, a) == want, (t, e, a)
             checked += 1
         f.step_phase(4)
     assert checked > 100
@@ -112,4 +118,4 @@ def test_astar_pool_handover_matches_oracle(warps, torch_cuda):
     assert int(f.counters_t[10]) == 1, "the search should have outgrown the shared tile pool"
     n = int(f.path_n_t[0, 0])
     assert n == len(want) + 1
-    assert f.path_cells_t[0, 0, :n - 1].cpu().numpy().tolist() == want
+    assert _path(f, 0, 0) == want

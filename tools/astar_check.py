@@ -67,7 +67,8 @@ for t in range(T):
         per_tick += 1
         ref = C.astar(labs[e], (st // nx, st % nx), (gl // nx, gl % nx))
         n = int(f.path_n_t[e, a])
-        cells = f.path_cells_t[e, a, :max(n - 1, 0)].cpu().numpy()
+        hd = int(f.path_head_t[e, a])
+        cells = f.path_cells_t[e, a, hd:hd + max(n - 1, 0)].cpu().numpy()
         want = [] if ref is None else [r * nx + c for r, c in ref[1:]]
         ok = (ref is None and n == 1) or (ref is not None and n == len(ref) and list(cells) == want)
         checked += 1

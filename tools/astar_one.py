@@ -40,7 +40,8 @@ for path in sys.argv[1:]:
             res_ok = []
             for e in range(E):
                 n = int(f.path_n_t[e, 0])
-                cells = f.path_cells_t[e, 0, :n - 1].cpu().numpy().tolist()
+                hd = int(f.path_head_t[e, 0])
+                cells = f.path_cells_t[e, 0, hd:hd + n - 1].cpu().numpy().tolist()
                 res_ok.append(n == len(ref) and cells == want)
             print(f"{os.path.basename(path)} W={w} rep {rep}: oracle n {len(ref)}; device ok per env {res_ok}",
                   flush=True)
