@@ -221,6 +221,27 @@ class BatchedEnv:
         """Install robot poses (e.g. the reference's route-anchor spawns)."""
         self.robot.set_state(x, y, yaw, goal, vx=vx, vy=vy, elev=elev, tick=tick, rows=rows)
 
+    # robot pose arrays as the reference exposes them (batch.py:98-110), host copies
+    @property
+    def x(self):
+        return self.robot.x.cpu().numpy()
+
+    @property
+    def y(self):
+        return self.robot.y.cpu().numpy()
+
+    @property
+    def yaw(self):
+        return self.robot.yaw.cpu().numpy()
+
+    @property
+    def vx(self):
+        return self.robot.vx.cpu().numpy()
+
+    @property
+    def vy(self):
+        return self.robot.vy.cpu().numpy()
+
     def robot_state(self, i=0):
         r = self.robot
         return {"x": float(r.x[i]), "y": float(r.y[i]), "yaw": float(r.yaw[i]), "vx": float(r.vx[i]),
