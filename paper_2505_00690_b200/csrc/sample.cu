@@ -1481,7 +1481,7 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
   int base = 0;
   for (int f0 = 0; f0 < N; f0 += SP_NT) {
     int f = f0 + threadIdx.x;
-    int ok = f < N && Lb[f] == L_WALKABLE && spawn_region_ok(P, f % nx);
+    int ok = f < N && Lb[f] == L_WALKABLE && (P.spawn_region != 1 || spawn_region_ok(P, f % nx));
     if (f < N) { comp[f] = ok ? f : -1; head[f] = -1; csize[f] = 0; }
     int tot;
     int off = block_excl_scan<SP_NT>(ok, sh, tot);
@@ -1498,7 +1498,7 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
   // 8-connected components (routes.py:14-32); only label equality is used
   // downstream (routes.py:62, 74), so any labelling works.
   grid_components<SP_NT, true>(comp, nx, ny, [&](int f) {
-    return Lb[f] == L_WALKABLE && spawn_region_ok(P, f % nx);
+    return Lb[f] == L_WALKABLE && (P.spawn_region != 1 || spawn_region_ok(P, f % nx));
   });
   for (int q = threadIdx.x; q < n; q += SP_NT) atomicAdd(&csize[comp[cand[q]]], 1);
   __syncthreads();
