@@ -211,3 +211,40 @@ def test_run_with_resampling_matches_synchronous_driver(overlap, torch_cuda):
         out.append((f, b.labels.cpu().numpy()))
     assert np.array_equal(out[0][1], out[1][1])
     _same(out[0][0], out[1][0], "resampling driver")
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_run_random_configs(case, torch_cuda):
+    """Seeded random shapes (agent counts 1..130 across the lane / binned paths, grid sizes,
+    resolutions, densities, neighbour radii, robots on / off, random env masks): a run
+    equals the same number of synchronous steps."""
+    import torch
+    from oracle.rng import child_seed
+    from paper_2505_00690_b200.crowd import CrowdConfig, CrowdField
+    from paper_2505_00690_b200.urbangen import SceneSampler, SceneSpec, TaskKind
+    r = np.random.default_rng(100 + case)
+    A = int([1, 5, 17, 40, 70, 130][case])
+    E = int(r.integers(2, 12))
+    res = float(r.choice([0.1, 0.2, 0.25]))
+    ext = float(r.choice([12.0, 20.0, 32.0])) if A < 100 else 48.0
+    task = TaskKind.NAV_DYNAMIC if A < 100 else TaskKind.NAV_CLEAR
+    nd = float(r.choice([3.0, 5.0]))
+    T = int(r.integers(10, 40))
+    seeds = [child_seed(0, "env", 1000 * case + i) for i in range(E)]
+    spec = SceneSpec(seed=0, extent_m=(ext, ext), task_kind=task, pedestrian_count=A,
+                     object_density=float(r.uniform(0.2, 1.5)) if task == TaskKind.NAV_DYNAMIC else 0.0,
+                     terrain_mix=MIX, grid_resolution_m=res)
+    b = SceneSampler(spec, E).sample(seeds, [child_seed(s, "crowd", 0) for s in seeds])
+    run = [child_seed(s, "crowd-run") for s in seeds]
+    fs = []
+    for _ in range(2):
+        f = CrowdField(b, CrowdConfig(neighbor_distance=nd), run)
+        f.set_from_spawn(b)
+        fs.append(f)
+    robot = case % 2 == 0
+    rp, rv = _robot(b, E, res, seed=case) if robot else (None, None)
+    mask = torch.from_numpy((r.random(E) < 0.8).astype(np.uint8)).cuda() if case % 3 == 1 else None
+    for _ in range(T):
+        fs[0].step(rp, rv, 0.35, env_mask=mask)
+    fs[1].run(T, rp, rv, 0.35, env_mask=mask)
+    _same(fs[0], fs[1], f"random case {case}: E={E} A={A} ext={ext} res={res} nd={nd} T={T}")
