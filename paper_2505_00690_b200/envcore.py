@@ -68,7 +68,12 @@ class StepResult:
 
 
 class BatchedEnv:
-    """K env slots: device scenes + device crowd (batch.py:62)."""
+    """K env slots: device scenes + device crowd (batch.py:62).
+
+    ``cache`` (an ``AssetCache``, cache.py:15-39) is accepted for API parity: every
+    slot is sampled on the device in one batch, and equal specs give bit-identical
+    rows (the Sync scheme's shared scene), so nothing is looked up; the scenes'
+    identities are ``scene_hashes`` either way."""
 
     def __init__(self, specs, scheme, master_seed, k=None, cache=None, config=None,
                  env_seeds=None, device="cuda", threads=128, catalog=None):
