@@ -176,10 +176,111 @@ __device__ __noinline__ void least_violation_ool(const WarpCons& C, int nc, int 
   least_violation(C, nc, begin, ms, r0, r1);
 }
 
+// ---------------------------------------------------------------- warp fallback
+// orca.py:155-242 (_solve_least_violation / _lp2_toward / _solve_on_line, dir_opt)
+// with the whole warp for the warp path (C and Q in shared memory, warp-uniform
+// control flow); the lane path keeps the scalar copy above (measured: deferring its
+// rare fallbacks to the whole warp costs more in the common case than it saves).  The projected constraints of row i (orca.py:196-207) are built
+// one per lane j < i and compacted in j order by a ballot; each line solve
+// (orca.py:155-189) reduces over j < k in parallel: it fails iff some j is
+// degenerate with num > eps or the running bounds cross -- the bounds only
+// tighten, so they cross at some prefix iff the full max(tl) > min(tr) -- and
+// otherwise ends at the full max / min.  Same float operations, exact reductions.
+CW_DEV bool warp_solve_on_line_dir(const WarpCons& Q, int k, double ms, double o0, double o1, double& r0,
+                                   double& r1, int lane) {
+  const double px = Q.px[k], py = Q.py[k];
+  const double dx = -Q.ny[k], dy = Q.nx[k];
+  const double dpd = dot2_blas(px, py, dx, dy);
+  const double disc = dpd * dpd + ms * ms - dot2_blas(px, py, px, py);
+  if (disc < 0.0) return false;
+  const double sq = sqrt(disc);
+  double tl = -dpd - sq, tr = -dpd + sq;
+  double tlj = -DBL_MAX, trj = DBL_MAX;
+  bool bad = false;
+  if (lane < k) {
+    const double den = dot2_blas(dx, dy, Q.nx[lane], Q.ny[lane]);
+    const double num = dot2_blas(Q.px[lane] - px, Q.py[lane] - py, Q.nx[lane], Q.ny[lane]);
+    if (fabs(den) < kEps) {
+      bad = num > kEps;
+    } else {
+      const double t = num / den;
+      if (den > 0.0) tlj = t;
+      else trj = t;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    tlj = fmax(tlj, __shfl_xor_sync(0xffffffffu, tlj, o));
+    trj = fmin(trj, __shfl_xor_sync(0xffffffffu, trj, o));
+  }
+  tl = fmax(tl, tlj);
+  tr = fmin(tr, trj);
+  if (__any_sync(0xffffffffu, bad) || tl > tr) return false;
+  const double tb = dot2_blas(o0, o1, dx, dy) > 0.0 ? tr : tl;
+  r0 = px + tb * dx;
+  r1 = py + tb * dy;
+  return true;
+}
+
+CW_DEV void warp_least_violation(const WarpCons& C, WarpCons& Q, int nc, int begin, double ms, double& r0,
+                                 double& r1, int lane) {
+  double dist = 0.0;
+  for (int i = begin; i < nc; ++i) {
+    const double pix = C.px[i], piy = C.py[i], nix = C.nx[i], niy = C.ny[i];
+    const double viol = -dot2_blas(r0 - pix, r1 - piy, nix, niy);
+    if (viol <= dist + kEps) continue;
+    bool valid = false;
+    double mx = 0.0, my = 0.0, qx = 0.0, qy = 0.0;
+    if (lane < i) {
+      const double pjx = C.px[lane], pjy = C.py[lane], njx = C.nx[lane], njy = C.ny[lane];
+      const double det = nix * njy - niy * njx;
+      const double dfx = njx - nix, dfy = njy - niy;
+      bool keep = true;
+      if (fabs(det) < kEps) {
+        if (dot2_blas(nix, niy, njx, njy) > 0.0) keep = false;
+        mx = 0.5 * (pix + pjx);
+        my = 0.5 * (piy + pjy);
+      } else {
+        const double dix = -niy, diy = nix;
+        const double t = dot2_blas(pjx - pix, pjy - piy, njx, njy) / dot2_blas(dix, diy, njx, njy);
+        mx = pix + t * dix;
+        my = piy + t * diy;
+      }
+      if (keep) {
+        const double nrm = glibc_hypot(dfx, dfy);
+        if (!(nrm < kEps)) {
+          valid = true;
+          qx = dfx / nrm;
+          qy = dfy / nrm;
+        }
+      }
+    }
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    const int np = __popc(vm);
+    __syncwarp();
+    if (valid) {
+      const int k = __popc(vm & ((1u << lane) - 1u));
+      Q.px[k] = mx; Q.py[k] = my; Q.nx[k] = qx; Q.ny[k] = qy;
+    }
+    __syncwarp();
+    // _lp2_toward(proj, ms, n_i)
+    const double sc = ms / fmax(glibc_hypot(nix, niy), kEps);
+    double t0 = nix * sc, t1 = niy * sc;
+    bool ok = true;
+    for (int k = 0; k < np && ok; ++k) {
+      if (dot2_blas(t0 - Q.px[k], t1 - Q.py[k], Q.nx[k], Q.ny[k]) < -kEps)
+        ok = warp_solve_on_line_dir(Q, k, ms, nix, niy, t0, t1, lane);
+    }
+    if (ok) { r0 = t0; r1 = t1; }
+    dist = -dot2_blas(r0 - pix, r1 - piy, nix, niy);
+  }
+  __syncwarp();
+}
+
 // ---------------------------------------------------------------- warp LP
 // field.py:500-566 for one agent.  Lane k holds constraint k; all lanes keep
 // the running result.  Returns true when the fallback ran.
-CW_DEV bool warp_lp(const WarpCons& C, int nc, double pf0, double pf1, double ms, double& r0,
+CW_DEV bool warp_lp(const WarpCons& C, WarpCons& Q, int nc, double pf0, double pf1, double ms, double& r0,
                     double& r1, int lane) {
   double pn = sqrt(pf0 * pf0 + pf1 * pf1);
   double sc = pn > ms ? ms / fmax(pn, kEps) : 1.0;
@@ -220,9 +321,7 @@ CW_DEV bool warp_lp(const WarpCons& C, int nc, double pf0, double pf1, double ms
     tr = fmin(tr, trj);
     bad |= tl > tr;
     if (bad) {
-      if (lane == 0) least_violation(C, nc, i, ms, r0, r1);
-      r0 = __shfl_sync(0xffffffffu, r0, 0);
-      r1 = __shfl_sync(0xffffffffu, r1, 0);
+      warp_least_violation(C, Q, nc, i, ms, r0, r1, lane);
       return true;
     }
     double tb = (pf0 - pi0) * d0 + (pf1 - pi1) * d1;
@@ -550,7 +649,7 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
   double* s_nx = s_r + A;   // post-commit positions (resample)
   double* s_ny = s_nx + A;
   WarpCons* s_cons = reinterpret_cast<WarpCons*>(s_ny + A);
-  uint8_t* s_act = reinterpret_cast<uint8_t*>(s_cons + (kLanes ? 0 : NW));   // lanes: no WarpCons
+  uint8_t* s_act = reinterpret_cast<uint8_t*>(s_cons + (kLanes ? 0 : 2 * NW));   // warp path: C, then Q (fallback); lanes: none
   // agent binning (large A): cell ends after the scatter, sorted agent ids, agent cell
   int* s_cend = reinterpret_cast<int*>(s_act + ((A + 15) & ~15));
   int* s_sorted = s_cend + bins.ncx * bins.ncy + 1;
@@ -621,6 +720,7 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
       if (robot_vel) { rvx = robot_vel[e * 2]; rvy = robot_vel[e * 2 + 1]; }
     }
     WarpCons& C = s_cons[wid];
+    WarpCons& Q = s_cons[NW + wid];   // warp path only (lane path: no WarpCons)
     double my_gap = CUDART_INF;
     int my_anynb = 0;
     long long fallbacks = 0, stalls = 0;
@@ -906,14 +1006,14 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
       // ---------------- LP + stall retry (field.py:133-150)
       const double ms = S.max_speed[ia];
       double v0, v1;
-      fallbacks += warp_lp(C, nc, pf0, pf1, ms, v0, v1, lane);
+      fallbacks += warp_lp(C, Q, nc, pf0, pf1, ms, v0, v1, lane);
       double spd = sqrt(v0 * v0 + v1 * v1);
       double want = sqrt(pf0 * pf0 + pf1 * pf1);
       if (spd < 0.2 * want && want > 1e-6) {
         ++stalls;
         double q0 = P.stall_c * pf0 + P.stall_s * pf1;
         double q1 = -P.stall_s * pf0 + P.stall_c * pf1;
-        fallbacks += warp_lp(C, nc, q0, q1, ms, v0, v1, lane);
+        fallbacks += warp_lp(C, Q, nc, q0, q1, ms, v0, v1, lane);
       }
       // ---------------- commit (field.py:152-160, 352-366)
       double npx = px + v0 * P.dt, npy = py + v1 * P.dt;
@@ -1485,7 +1585,7 @@ extern "C" {
 
 size_t cw_crowd_step_smem_bytes(int A, int nt) {
   // + fp32 (x, y, x^2 + y^2) per agent for the lane path (aliases the unused bins region)
-  return (size_t)A * 7 * sizeof(double) + (size_t)(nt / 32) * sizeof(cw::WarpCons) +
+  return (size_t)A * 7 * sizeof(double) + (size_t)(nt / 32) * 2 * sizeof(cw::WarpCons) +
          (size_t)((A + 15) & ~15) + 16 + (size_t)A * 3 * sizeof(float);
 }
 
