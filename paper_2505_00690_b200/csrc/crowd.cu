@@ -741,8 +741,12 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
         s_fsq[a] = __fadd_rn(__fmul_rn(xj, xj), __fmul_rn(yj, yj));
       }
       __syncthreads();
-      for (int a = threadIdx.x; a < A; a += NT) {
-        if (!s_act[a]) continue;
+      // A <= NT: thread (wid, lane) takes agent lane * NW + wid, so the CTA's warps
+      // share the env's agents instead of warp 0 taking all of them
+      const bool spread = A <= NT;
+      for (int t = threadIdx.x; t < (spread ? NT : A); t += NT) {
+        const int a = spread ? lane * NW + wid : t;
+        if (a >= A || !s_act[a]) continue;
         const double px = s_px[a], py = s_py[a];
         const size_t ia = eA + a;
         const double gx = S.goal[ia * 2], gy = S.goal[ia * 2 + 1];
@@ -1039,36 +1043,50 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
     }
     __syncthreads();
     // ---------------- goal resample, agent order (field.py:368-381)
-    if (threadIdx.x == 0) {
-      double g = CUDART_INF;
-      int anynb = 0;
-      for (int w = 0; w < NW; ++w) { g = fmin(g, s_gap[w]); anynb |= s_anynb[w]; }
-      if (ra) {
-        ra->gap_hist[(size_t)e * ra->T + tick] = g;
-        if (anynb) ra->anynb[tick] = 1;
-      } else {
-        S.gap_tmp[e] = g;
-        if (anynb) atomicOr(&S.flags[0], 1);
+    // warp 0: lanes test 32 agents' goal reach at once (independent loads), lane 0
+    // then draws for the reached ones in agent order (rare: the rng stream order is
+    // the reference's)
+    if (wid == 0) {
+      if (lane == 0) {
+        double g = CUDART_INF;
+        int anynb = 0;
+        for (int w = 0; w < NW; ++w) { g = fmin(g, s_gap[w]); anynb |= s_anynb[w]; }
+        if (ra) {
+          ra->gap_hist[(size_t)e * ra->T + tick] = g;
+          if (anynb) ra->anynb[tick] = 1;
+        } else {
+          S.gap_tmp[e] = g;
+          if (anynb) atomicOr(&S.flags[0], 1);
+        }
       }
       if (P.resample_goals) {
         Pcg64Raw* raw = reinterpret_cast<Pcg64Raw*>(S.rng) + e;
         bool loaded = false;
         Pcg64 rng;
         const int wn = S.walk_n[e];
-        for (int a = 0; a < A; ++a) {
-          if (!s_act[a]) continue;
-          const size_t ia = eA + a;
-          double dx = S.goal[ia * 2] - s_nx[a], dy = S.goal[ia * 2 + 1] - s_ny[a];
-          if (!(dx * dx + dy * dy < P.goal_reach2)) continue;
-          if (!loaded) { rng = pcg_load(*raw); loaded = true; }
-          int k = (int)integers32(rng, (uint64_t)wn);
-          int f = S.walk[e * N + k];
-          int r = f / nx, c = f - r * nx;
-          S.goal[ia * 2] = ((double)c + 0.5) * res;
-          S.goal[ia * 2 + 1] = ((double)r + 0.5) * res;
-          S.path_n[ia] = 0;
+        for (int a0 = 0; a0 < A; a0 += 32) {
+          bool hit = false;
+          if (a0 + lane < A && s_act[a0 + lane]) {
+            const size_t ia = eA + a0 + lane;
+            double dx = S.goal[ia * 2] - s_nx[a0 + lane], dy = S.goal[ia * 2 + 1] - s_ny[a0 + lane];
+            hit = dx * dx + dy * dy < P.goal_reach2;
+          }
+          unsigned m = __ballot_sync(0xffffffffu, hit);
+          if (lane != 0) continue;
+          while (m) {
+            const int a = a0 + __ffs(m) - 1;
+            m &= m - 1u;
+            const size_t ia = eA + a;
+            if (!loaded) { rng = pcg_load(*raw); loaded = true; }
+            int k = (int)integers32(rng, (uint64_t)wn);
+            int f = S.walk[e * N + k];
+            int r = f / nx, c = f - r * nx;
+            S.goal[ia * 2] = ((double)c + 0.5) * res;
+            S.goal[ia * 2 + 1] = ((double)r + 0.5) * res;
+            S.path_n[ia] = 0;
+          }
         }
-        if (loaded) pcg_store(*raw, rng);
+        if (lane == 0 && loaded) pcg_store(*raw, rng);
       }
     }
     if (lane == 0 && S.counters) {
