@@ -334,9 +334,11 @@ def run_ours(args):
                          f.active_t.sum(1).double()], 1)
     tmax = torch.tensor([t_ms, sample_ms, e2e_s, run["ms"] if run else 0.0, run["e2e_s"] if run else 0.0],
                         dtype=torch.float64, device=dev)
+    csum = shard.state_checksum(f.pos_t, f.vel_t, f.goal_t, f.last_gap_t)   # per env, exact
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         stats = shard.gather_env_stats(stats)
+        csum = shard.gather_env_stats(csum[:, None])[:, 0]
     t_ms, sample_ms, e2e_s, run_ms_max, run_e2e_max = [float(x) for x in tmax.cpu()]
     if rank == 0:
         steps = args.steps
@@ -402,7 +404,12 @@ def run_ours(args):
             "clocks": clk.summary(),
             "counters": counters,
             "stats": {"min_gap": float(torch.nan_to_num(stats[:, 0], posinf=1e9).min()),
-                      "mean_objects": float(stats[:, 1].mean()), "envs": int(stats.shape[0])},
+                      "mean_objects": float(stats[:, 1].mean()), "envs": int(stats.shape[0]),
+                      # checksum of the per-env state checksums (pos, vel, goal, last gap after
+                      # the whole bench) over all envs, and over the first E global envs --
+                      # the latter is the same for every N (weak scaling, env-sharded)
+                      "state_checksum": hex(shard.checksum_of(csum)),
+                      "state_checksum_first_envs": hex(shard.checksum_of(csum[:E]))},
         }
         if run is not None and env_steps / (run_ms_max / 1e3) < line["value"]:
             run["slower"] = True   # e.g. cfg4: the synchronous tick stays the headline

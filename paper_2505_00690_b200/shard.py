@@ -47,3 +47,37 @@ def max_over_ranks(value, device=None, group=None):
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+_P = 2147483647   # 2^31 - 1: every product below stays < 2^62, every row sum < 2^63
+
+
+def _weighted_mod(words):
+    """Two position-weighted sums mod P over the columns of (R, n) int64 words < P."""
+    import torch
+    k = torch.arange(words.shape[1], dtype=torch.int64, device=words.device)
+    w1 = (k * 40503 + 1) % _P
+    w2 = (k * 69069 + 12345) % _P
+    s1 = ((words * w1) % _P).sum(1) % _P
+    s2 = ((words * w2) % _P).sum(1) % _P
+    return s1 * _P + s2
+
+
+def state_checksum(*arrays):
+    """Per-env checksum of float64 state arrays shaped (E, ...): the exact bit
+    patterns, position-weighted, reduced mod 2^31 - 1 (two independent sums,
+    an int64 < 2^62 per env).  Integer arithmetic only, so the value is the same
+    on any device and for any sharding of the envs."""
+    import torch
+    parts = [torch.as_tensor(a).reshape(a.shape[0], -1).to(torch.float64) for a in arrays]
+    x = torch.cat(parts, 1).contiguous().view(torch.int64)
+    words = torch.stack([x & 0xFFFFFFFF, (x >> 32) & 0xFFFFFFFF], 2).reshape(x.shape[0], -1) % _P
+    return _weighted_mod(words)
+
+
+def checksum_of(checksums):
+    """Checksum of per-env checksums (in global env order) -> python int."""
+    import torch
+    c = torch.as_tensor(checksums).reshape(1, -1).to(torch.int64)
+    words = torch.stack([c % _P, c // _P], 2).reshape(1, -1)
+    return int(_weighted_mod(words)[0])

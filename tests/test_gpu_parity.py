@@ -255,7 +255,7 @@ def test_batched_env_resample_slots(torch_cuda):
 def test_shard_invariance_sampling_and_crowd(torch_cuda):
     """W=1 vs W=2: global env ids [0,6) in one batch equal the two
     shards [0,3) + [3,6) run as separate batches, over sampling and 20 ticks."""
-    from oracle.rng import child_seed
+    import torch
     from paper_2505_00690_b200 import shard
     seeds_all = shard.env_seeds(0, shard.env_ids(0, 1, 6))
     kw = dict(extent_m=(32.0, 32.0), object_density=20 / 41, grid_resolution_m=0.25)
@@ -275,6 +275,10 @@ def test_shard_invariance_sampling_and_crowd(torch_cuda):
         assert np.array_equal(f1.pos[sl], f.pos)
         assert np.array_equal(f1.vel[sl], f.vel)
         assert np.array_equal(f1.goal[sl], f.goal)
+        # the bench's per-env state checksum: on device == on host, and shard-invariant
+        c_dev = shard.state_checksum(f.pos_t, f.vel_t, f.goal_t).cpu()
+        assert torch.equal(c_dev, shard.state_checksum(f.pos, f.vel, f.goal))
+        assert torch.equal(c_dev, shard.state_checksum(f1.pos_t, f1.vel_t, f1.goal_t).cpu()[sl])
 
 
 @pytest.mark.parametrize("peds", [96, 160])

@@ -30,7 +30,7 @@ def _per_env_stats(global_ids, catalog_path):
     from oracle.rng import child_seed
     cat = S.load_catalog_tuples(json.load(open(catalog_path)))
     mix = {"Flat": 0.25, "Slope": 0.25, "Stair": 0.25, "Rough": 0.25}
-    rows = []
+    rows, sums = [], []
     for gid in global_ids:
         s = child_seed(0, "env", int(gid))
         sc = S.generate_scene(dict(seed=s, extent=(12.0, 12.0), res=0.25, task="NavDynamic",
@@ -42,7 +42,8 @@ def _per_env_stats(global_ids, catalog_path):
             f.step()
         rows.append([float(f.pos.sum()), float(f.vel.sum()), len(sc["objects"]),
                      float((sc["labels"] == 2).sum()), float(f.last_gap_by_env[0]), 3.0])
-    return torch.tensor(rows, dtype=torch.float64)
+        sums.append(shard.state_checksum(f.pos, f.vel, f.goal)[0])
+    return torch.tensor(rows, dtype=torch.float64), torch.stack(sums)
 
 
 def _worker(rank, world, port, per_rank, catalog_path, out_path):
@@ -50,11 +51,12 @@ def _worker(rank, world, port, per_rank, catalog_path, out_path):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     ids = shard.env_ids(rank, world, per_rank)
-    local = _per_env_stats(ids, catalog_path)
+    local, csum = _per_env_stats(ids, catalog_path)
     full = shard.gather_env_stats(local)
+    csum_full = shard.gather_env_stats(csum[:, None])[:, 0]
     t = shard.max_over_ranks(float(rank) + 0.5)
     if rank == 0:
-        torch.save({"full": full, "max": t}, out_path)
+        torch.save({"full": full, "csum": csum_full, "max": t}, out_path)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -74,6 +76,27 @@ def test_two_rank_gloo_gather_matches_single_process(tmp_path):
     per_rank = 2
     mp.spawn(_worker, args=(2, _free_port(), per_rank, cat, out), nprocs=2, join=True)
     got = torch.load(out)
-    ref = _per_env_stats(np.arange(2 * per_rank), cat)
+    ref, ref_sum = _per_env_stats(np.arange(2 * per_rank), cat)
     assert torch.equal(got["full"], ref)          # sharding-invariant, rank-ordered
+    assert torch.equal(got["csum"], ref_sum)      # per-env state checksums, exact
+    assert shard.checksum_of(got["csum"]) == shard.checksum_of(ref_sum)
     assert got["max"] == 1.5                      # max over ranks
+
+
+def test_state_checksum_exact_and_shard_invariant():
+    g = torch.Generator().manual_seed(5)
+    pos = torch.randn(8, 7, 2, dtype=torch.float64, generator=g)
+    vel = torch.randn(8, 7, 2, dtype=torch.float64, generator=g)
+    c = shard.state_checksum(pos, vel)
+    assert c.dtype == torch.int64 and c.shape == (8,)
+    assert torch.equal(torch.cat([shard.state_checksum(pos[:3], vel[:3]),
+                                  shard.state_checksum(pos[3:], vel[3:])]), c)
+    assert torch.equal(shard.state_checksum(pos.numpy(), vel.numpy()), c)
+    v2 = vel.clone()
+    v2[5, 6, 1] = np.nextafter(v2[5, 6, 1].item(), np.inf)     # one ulp in one env
+    c2 = shard.state_checksum(pos, v2)
+    assert (c2 != c).tolist() == [False] * 5 + [True] + [False] * 2
+    assert shard.checksum_of(c) != shard.checksum_of(c2)
+    assert shard.checksum_of(c) != shard.checksum_of(c.flip(0))     # order matters
+    z = torch.zeros(3, 4, dtype=torch.float64)
+    assert not torch.equal(shard.state_checksum(z), shard.state_checksum(-z))   # bits, not values
