@@ -1373,6 +1373,22 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
                          (int)cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(k_round<NT, false>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          (int)cudaSharedmemCarveoutMaxShared);
+    // Reserve the per-thread local memory (stack) of every kernel of the run now, while
+    // nothing is running: a launch that outgrows the reservation makes the driver grow
+    // it, which waits for the device to drain -- and the persistent server only drains
+    // after the rounds that launch is holding back.
+    size_t need = 0;
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, k_round<NT, true>) == cudaSuccess) need = std::max(need, fa.localSizeBytes);
+    if (cudaFuncGetAttributes(&fa, k_round<NT, false>) == cudaSuccess) need = std::max(need, fa.localSizeBytes);
+    if (cudaFuncGetAttributes(&fa, k_astar<1, true>) == cudaSuccess) need = std::max(need, fa.localSizeBytes);
+    if (cudaFuncGetAttributes(&fa, k_astar<2, true>) == cudaSuccess) need = std::max(need, fa.localSizeBytes);
+    if (cudaFuncGetAttributes(&fa, k_astar<kAstarWarps, true>) == cudaSuccess)
+      need = std::max(need, fa.localSizeBytes);
+    size_t cur = 0;
+    cudaDeviceGetLimit(&cur, cudaLimitStackSize);
+    if (need > cur) cudaDeviceSetLimit(cudaLimitStackSize, (need + 255) & ~(size_t)255);
+    cudaGetLastError();
     attrs = true;
   }
   // lane-per-agent ORCA below 128 agents; the binned warp path (96 registers,

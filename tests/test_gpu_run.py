@@ -248,3 +248,24 @@ def test_run_random_configs(case, torch_cuda):
         fs[0].step(rp, rv, 0.35, env_mask=mask)
     fs[1].run(T, rp, rv, 0.35, env_mask=mask)
     _same(fs[0], fs[1], f"random case {case}: E={E} A={A} ext={ext} res={res} nd={nd} T={T}")
+
+
+def test_run_as_first_crowd_launch_of_a_process(tmp_path):
+    """A run whose kernels are the process's first crowd launches (no prior step):
+    the run reserves its kernels' local memory before starting the persistent
+    server, so no launch can wait on a driver resize while the server runs."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import numpy as np, torch\n"
+        "from test_gpu_run import _pair\n"
+        "b, (f, g) = _pair(8, 32.0, 0.125, 32, 64)\n"
+        "f.run(6)\n"
+        "for _ in range(6): g.step()\n"
+        "assert np.array_equal(f.pos_t.cpu().numpy(), g.pos_t.cpu().numpy())\n"
+        "print('ok')\n" % (root, os.path.join(root, "tests")))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
