@@ -1470,7 +1470,12 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
   AstarShape shp = astar_shape(P.nx, P.ny, srv_w == 4 ? kAstarWarps : srv_w == 2 ? 2 : 1, srv_kb);
   shp.NS = std::min(shp.NS, astar_ns_cap(P.nx, P.ny));   // the global store holds NS slot ids
   static const int margin = getenv("CW_RUN_MARGIN") ? atoi(getenv("CW_RUN_MARGIN")) : 0;
-  int srv_ctas = P.astar_ctas - std::max(4, margin > 0 ? margin : P.astar_ctas / 8);
+  // SMs left without a server CTA: 1/8 of them, except for 32-thread lane-path rounds
+  // (A <= 32), which are light enough to run beside the server everywhere -- measured
+  // at cfg2: margin 4 / 8 / 18 = 0.289 / 0.296 / 0.309 ms/tick; at cfg3 (64-thread
+  // rounds) and cfg4 (256-thread warp-path rounds) a margin of 8 was 14 % / 2x slower
+  const int margin_def = (lanes_ok && NT == 32) ? 4 : P.astar_ctas / 8;
+  int srv_ctas = P.astar_ctas - std::max(4, margin > 0 ? margin : margin_def);
   if (const char* v = getenv("CW_RUN_SERVER_CTAS")) srv_ctas = std::min(srv_ctas, atoi(v));
   srv_ctas = std::max(srv_ctas, 1);
   if (srv_w == 4)
