@@ -147,6 +147,22 @@ def test_run_full_cfg2_batch_matches_steps(torch_cuda):
     _same(f, g, "cfg2 x 1024")
 
 
+def test_run_long_horizon_matches_steps(torch_cuda):
+    """256 cfg2 envs x 400 ticks in one run call (goals re-drawn many times, RNG
+    streams advanced far): bit-identical to 400 synchronous steps, and the
+    bench's per-env state checksum agrees."""
+    from paper_2505_00690_b200 import shard
+    b, (f, g) = _pair(256, 32.0, 0.125, 32, 64)
+    rp, rv = _robot(b, 256, 0.125, seed=5)
+    for _ in range(400):
+        f.step(rp, rv, 0.35, check=False)
+    f.check_flags()
+    g.run(400, rp, rv, 0.35)
+    _same(f, g, "cfg2 x 256 x 400 ticks")
+    assert np.array_equal(shard.state_checksum(f.pos_t, f.vel_t, f.goal_t, f.last_gap_t).cpu().numpy(),
+                          shard.state_checksum(g.pos_t, g.vel_t, g.goal_t, g.last_gap_t).cpu().numpy())
+
+
 def test_run_binned_warp_path(torch_cuda):
     """A >= 128 (cell-binned neighbour search, warp-per-agent rounds) on a block layout."""
     from oracle.rng import child_seed
