@@ -537,10 +537,12 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
     const int sy0 = (int)E.tmap[ty];
     int sy = legal ? sy0 : (int)kNoSlot;
     const double hh = octile(rr, cc, gr, gc);
+#ifdef CW_ASTAR_TRACE   // expansion-order trace for tools/astar_trace.py (debug builds only)
     if (E.trace && lane == 0 && s_exp < (1u << 20)) {
       E.trace[2 * s_exp] = x;
       E.trace[2 * s_exp + 1] = __double_as_longlong(gx);
     }
+#endif
     if (x == goal) { found = 1; break; }
     // No stale test (paths.py:70-71) is needed here: the head never holds a
     // stale entry (refills drop them, decrease-keys evict the old head copy),

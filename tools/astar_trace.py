@@ -1,5 +1,8 @@
 """Compare the device A* expansion order (counters[15] trace) of one search with
-the oracle's heapq pop order (GPU).  Usage: python tools/astar_trace.py case.npz [W]"""
+the oracle's heapq pop order (GPU).  Usage: python tools/astar_trace.py case.npz [W]
+
+The trace is compiled only into debug builds: rebuild the library with the
+_lib.NVCC_FLAGS command plus -DCW_ASTAR_TRACE before using this tool."""
 import heapq
 import math
 import os
