@@ -72,7 +72,9 @@ typedef struct cw_scene_params {
   int32_t obj_count, obj_max, attempts;
   int32_t region;
   int32_t peds;
-  int32_t spawn_region;
+  int32_t spawn_region;   /* 1: Traverse strip columns (batch.py:174-177) */
+  int32_t route_roadway;  /* cw_sample_routes: 1 = Walkable | Roadway (vehicle kinds, routes.py:52-55) */
+  double route_max_radius; /* cw_sample_routes: separation radius (routes.py:62-63) */
 } cw_scene_params;
 
 /* Output rows (E envs, written at slots[e]) + scratch. */
@@ -97,6 +99,7 @@ typedef struct cw_scene_buffers {
                            blocks [sidewalk_width, road_width], strip [border_m] */
   uint8_t* block_var;   /* (E, CW_MAX_BLOCKS) block variant kind*4 + orientation of
                            connect_blocks (blocks.py:34-77), row-major; layout 1 only */
+  const uint8_t* region; /* (E, ny*nx) optional route region mask (step.py:37 region_mask); NULL = none */
 } cw_scene_buffers;
 
 size_t cw_scene_seed_scratch_bytes(int E);
@@ -129,6 +132,31 @@ int cw_route_anchors(const cw_scene_params* params, int E, const uint64_t* scene
 int cw_spawn_agents(const cw_scene_params* params, int E, const uint64_t* crowd_seeds,
                     const int32_t* slots, void* seed_scratch, const cw_scene_buffers* buffers,
                     void* stream);
+
+/* sample_routes(occupancy, count, seed, kind, region_mask, max_radius) (crowd/routes.py:35-87)
+ * for rows slots[e] of buffers->labels: params->peds routes seeded PCG64(route_seeds[e]),
+ * params->route_roadway / route_max_radius, optional buffers->region; starts in sp_pos,
+ * goals in sp_goal, NoRouteAvailable in status.  spawn_agents(region_mask=) is
+ * cw_spawn_agents with buffers->region set. */
+int cw_sample_routes(const cw_scene_params* params, int E, const uint64_t* route_seeds,
+                     const int32_t* slots, void* seed_scratch, const cw_scene_buffers* buffers,
+                     void* stream);
+
+/* connected_components (crowd/routes.py:14-32): 8-connected component ids numbered in
+ * row-major order of first cell, -1 elsewhere; ok / comp / rank_scratch (E, ny*nx). */
+int cw_connected_components(int nx, int ny, int E, const uint8_t* ok, int32_t* comp,
+                            int32_t* rank_scratch, void* stream);
+
+/* rasterize_occupancy(scene, resolution) (urbangen/occupancy.py:28-57) at params->res,
+ * nx, ny: buffers->zones rows are (zone_ny, zone_nx) grids at zone_res; assign,
+ * tile_code, tile_p, noise_seed, obj_cat, obj_pose, obj_n, status (zero) are inputs;
+ * labels and elev ((ny, nx) rows) are written. */
+int cw_rasterize(const cw_scene_params* params, int E, const int32_t* slots, int zone_nx,
+                 int zone_ny, double zone_res, const cw_scene_buffers* buffers, void* stream);
+
+/* Parity tooling: sin / cos of n doubles as the device computes them (mode 0: CUDA
+ * sincos, 1: the correctly rounded cr_sincos of common.cuh). */
+int cw_trig_probe(int n, const double* x, double* s, double* c, int mode, void* stream);
 
 /* _prepare_env for caller-supplied labels (field.py:60-67): fills nearest,
  * has_obs, walk, walk_n, reach, moves of rows slots[e] from buffers->labels; needs status
@@ -218,6 +246,33 @@ int cw_crowd_run(const cw_crowd_params* params, const cw_crowd_state* state,
 int cw_astar_warps(void);
 /* Bytes of astar_rec per k_astar search warp for an nx x ny grid (host-only query). */
 size_t cw_astar_slot_bytes(int nx, int ny);
+
+
+/* ---------------------------------------------------------------- ORCA building blocks
+ * The tick's pieces as standalone batched calls (device pointers, stream-ordered):
+ *
+ *   cw_orca_lp            replaces crowd/field.py:500 _batched_lp (and orca.py:130
+ *                         solve_velocity as one row): points/normals (N, L, 2) f64,
+ *                         valid (N, L) u8, pref (N, 2), max_speed (N), lane_active (N) u8
+ *                         (NULL = all) -> out (N, 2); fell_back (N) i32 or NULL.  L <= 64.
+ *   cw_orca_halfplanes    replaces field.py:448 _vo_halfplane / orca.py:23 orca_halfplane,
+ *                         elementwise over n rows (horizon, share per row).
+ *   cw_crowd_constraints  replaces field.py:214 _preferred_velocities + :229
+ *                         _build_constraints for envs [e0, e1) of a crowd state: act
+ *                         ((e1-e0), A) u8; outputs pref (rows, 2), points / normals
+ *                         (rows, lmax, 2), valid (rows, lmax) u8 with lmax = kmax +
+ *                         (robot_pos != NULL) + use_static (kmax = min(max_neighbors,
+ *                         A-1)), inr (rows) in-range neighbour counts, gap (rows). */
+int cw_orca_lp(int N, int L, const double* points, const double* normals, const uint8_t* valid,
+               const double* pref, const double* max_speed, const uint8_t* lane_active, double* out,
+               int32_t* fell_back, void* stream);
+int cw_orca_halfplanes(int n, const double* rel_pos, const double* rel_vel, const double* combined_radius,
+                       const double* horizon, double dt, const double* v_self, const double* share,
+                       double* point, double* normal, void* stream);
+int cw_crowd_constraints(const cw_crowd_params* params, const cw_crowd_state* state, int e0, int e1,
+                         const uint8_t* act, const double* robot_pos, const double* robot_vel,
+                         double robot_radius, int use_static, int lmax, double* pref, double* points,
+                         double* normals, uint8_t* valid, int32_t* inr, double* gap, void* stream);
 
 /* ---------------------------------------------------------------- robot */
 

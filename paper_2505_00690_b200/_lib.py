@@ -36,6 +36,7 @@ class SceneParams(ctypes.Structure):
         ("cat_reach", c_f64 * MAX_CAT), ("cat_zones", c_u32 * MAX_CAT),
         ("small_first", c_i32 * MAX_CAT), ("obj_count", c_i32), ("obj_max", c_i32),
         ("attempts", c_i32), ("region", c_i32), ("peds", c_i32), ("spawn_region", c_i32),
+        ("route_roadway", c_i32), ("route_max_radius", c_f64),
     ]
 
 
@@ -43,7 +44,7 @@ SCENE_BUFFER_FIELDS = [
     "zones", "labels", "elev", "assign", "n_tiles", "tile_code", "tile_kind", "tile_param",
     "tile_p", "tile_w", "allowed", "noise_seed", "wfc_attempts", "obj_cat", "obj_pose", "obj_n",
     "overflow", "nearest", "has_obs", "walk", "walk_n", "reach", "moves", "sp_pos", "sp_goal", "sp_kind", "sp_pref",
-    "status", "scratch_i32", "scratch_f64", "zone_params", "block_var",
+    "status", "scratch_i32", "scratch_f64", "zone_params", "block_var", "region",
 ]
 
 
@@ -105,17 +106,36 @@ EXPORTS = ["cw_scene_seed_scratch_bytes", "cw_sample_scenes", "cw_spawn_agents",
            "cw_traversability_scratch_bytes", "cw_traversability", "cw_robot_step", "cw_robot_observe",
            "cw_route_scratch_bytes", "cw_route_anchors", "cw_seed_streams", "cw_child_seeds", "cw_abi_sizes",
            "cw_scene_rle", "cw_crowd_run_scratch_bytes", "cw_crowd_run",
-           "cw_crowd_run_rounds", "cw_crowd_run_window"]
+           "cw_crowd_run_rounds", "cw_crowd_run_window", "cw_sample_routes", "cw_connected_components",
+           "cw_rasterize", "cw_orca_lp", "cw_orca_halfplanes", "cw_crowd_constraints", "cw_trig_probe"]
 
 _lib = None
 
 
 def build(force=False, verbose=False):
-    """Compile the CUDA library in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+    """Compile the CUDA library in-tree for sm_100a (nvcc cross-compiles without a GPU).
+    One nvcc per translation unit in parallel, then one link."""
+    from concurrent.futures import ThreadPoolExecutor
     newest = max(os.path.getmtime(p) for p in SOURCES + HEADERS)
     if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
         return LIB_PATH
-    cmd = ["nvcc"] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", LIB_PATH] + SOURCES
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in NVCC_FLAGS if f != "-shared"]
+    inc = ["-I", os.path.join(ROOT, "include")]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = ["nvcc"] + cflags + inc + ["-c", src, "-o", obj]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(len(SOURCES)) as pool:
+        objs = list(pool.map(compile_one, SOURCES))
+    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+           "-o", LIB_PATH] + objs
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
@@ -184,6 +204,24 @@ def lib():
     L.cw_route_anchors.restype = ctypes.c_int
     L.cw_route_anchors.argtypes = [ctypes.POINTER(SceneParams), ctypes.c_int, P, P,
                                    ctypes.POINTER(SceneBuffers), P, P, P, ctypes.c_int, P]
+    L.cw_sample_routes.restype = ctypes.c_int
+    L.cw_sample_routes.argtypes = [ctypes.POINTER(SceneParams), ctypes.c_int, P, P, P,
+                                   ctypes.POINTER(SceneBuffers), P]
+    L.cw_connected_components.restype = ctypes.c_int
+    L.cw_connected_components.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P]
+    L.cw_rasterize.restype = ctypes.c_int
+    L.cw_rasterize.argtypes = [ctypes.POINTER(SceneParams), ctypes.c_int, P, ctypes.c_int, ctypes.c_int,
+                               ctypes.c_double, ctypes.POINTER(SceneBuffers), P]
+    L.cw_orca_lp.restype = ctypes.c_int
+    L.cw_orca_lp.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P, P, P, P, P, P, P]
+    L.cw_orca_halfplanes.restype = ctypes.c_int
+    L.cw_orca_halfplanes.argtypes = [ctypes.c_int, P, P, P, P, ctypes.c_double, P, P, P, P, P]
+    L.cw_crowd_constraints.restype = ctypes.c_int
+    L.cw_crowd_constraints.argtypes = [ctypes.POINTER(CrowdParams), ctypes.POINTER(CrowdState), ctypes.c_int,
+                                       ctypes.c_int, P, P, P, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                       P, P, P, P, P, P, P]
+    L.cw_trig_probe.restype = ctypes.c_int
+    L.cw_trig_probe.argtypes = [ctypes.c_int, P, P, P, ctypes.c_int, P]
     L.cw_abi_sizes.restype = ctypes.c_int
     L.cw_abi_sizes.argtypes = [ctypes.POINTER(ctypes.c_size_t), ctypes.c_int]
     sizes = (ctypes.c_size_t * 6)()

@@ -23,18 +23,19 @@
 #include <vector>
 #include <math_constants.h>
 #include "common.cuh"
-#include "crowd_types.cuh"
+#include "citywalk_b200.h"
 #include "rng.cuh"
-#include "scene_types.cuh"
 
 namespace cw {
 
 constexpr int MAXC = 12;   // neighbour lanes (<= 10) + robot + static
 constexpr double kWaypointReach = 0.5, kStrayLimit = 1.0;
 
-struct WarpCons {
-  double px[MAXC], py[MAXC], nx[MAXC], ny[MAXC];
+template <int C>
+struct ConsT {
+  double px[C], py[C], nx[C], ny[C];
 };
+using WarpCons = ConsT<MAXC>;
 
 // ---------------------------------------------------------------- VO half-plane
 // field.py:448-495 for one lane (the selected branch of the vectorised where()).
@@ -127,11 +128,12 @@ CW_DEV bool solve_on_line_dir(const double* cpx, const double* cpy, const double
   return true;
 }
 
-CW_DEV void least_violation(const WarpCons& C, int nc, int begin, double ms, double& r0,
+template <int CAP>
+CW_DEV void least_violation(const ConsT<CAP>& C, int nc, int begin, double ms, double& r0,
                             double& r1) {
   // orca.py:196-212
   double dist = 0.0;
-  double qpx[MAXC], qpy[MAXC], qnx[MAXC], qny[MAXC];
+  double qpx[CAP], qpy[CAP], qnx[CAP], qny[CAP];
   for (int i = begin; i < nc; ++i) {
     double pix = C.px[i], piy = C.py[i], nix = C.nx[i], niy = C.ny[i];
     double viol = -dot2_blas(r0 - pix, r1 - piy, nix, niy);
@@ -171,7 +173,8 @@ CW_DEV void least_violation(const WarpCons& C, int nc, int begin, double ms, dou
 }
 
 // out-of-line copy for the lane path (rare; keeps the round kernel's hot code small)
-__device__ __noinline__ void least_violation_ool(const WarpCons& C, int nc, int begin, double ms, double& r0,
+template <int CAP>
+__device__ __noinline__ void least_violation_ool(const ConsT<CAP>& C, int nc, int begin, double ms, double& r0,
                                                  double& r1) {
   least_violation(C, nc, begin, ms, r0, r1);
 }
@@ -339,12 +342,14 @@ CW_DEV bool warp_lp(const WarpCons& C, WarpCons& Q, int nc, double pf0, double p
 constexpr int MAXK = MAXC - 2;   // neighbour lanes
 
 // slot read with a run-time index (thread-local array, see put_slot)
-CW_DEV double get_slot(const double (&a)[MAXC], int k) {
+template <int CAP>
+CW_DEV double get_slot(const double (&a)[CAP], int k) {
   return a[k];
 }
 
-CW_DEV bool lane_lp(const double (&cpx)[MAXC], const double (&cpy)[MAXC], const double (&cnx)[MAXC],
-                    const double (&cny)[MAXC], int nc, double pf0, double pf1, double ms, double& r0,
+template <int CAP>
+CW_DEV bool lane_lp(const double (&cpx)[CAP], const double (&cpy)[CAP], const double (&cnx)[CAP],
+                    const double (&cny)[CAP], int nc, double pf0, double pf1, double ms, double& r0,
                     double& r1) {
   double pn = sqrt(pf0 * pf0 + pf1 * pf1);
   double sc = pn > ms ? ms / fmax(pn, kEps) : 1.0;
@@ -380,9 +385,9 @@ CW_DEV bool lane_lp(const double (&cpx)[MAXC], const double (&cpy)[MAXC], const 
     tr = fmin(tr, trj);
     bad |= tl > tr;
     if (bad) {
-      WarpCons C;
+      ConsT<CAP> C;
 #pragma unroll
-      for (int k = 0; k < MAXC; ++k) { C.px[k] = cpx[k]; C.py[k] = cpy[k]; C.nx[k] = cnx[k]; C.ny[k] = cny[k]; }
+      for (int k = 0; k < CAP; ++k) { C.px[k] = cpx[k]; C.py[k] = cpy[k]; C.nx[k] = cnx[k]; C.ny[k] = cny[k]; }
       least_violation_ool(C, nc, i, ms, r0, r1);
       return true;
     }
@@ -396,7 +401,8 @@ CW_DEV bool lane_lp(const double (&cpx)[MAXC], const double (&cpy)[MAXC], const 
 
 // slot write / read with a run-time index: the arrays live in thread-local memory
 // (measured faster than a select chain over register arrays: run 0.342 -> 0.308 ms/tick)
-CW_DEV void put_slot(double (&a)[MAXC], int k, double v) {
+template <int CAP>
+CW_DEV void put_slot(double (&a)[CAP], int k, double v) {
   a[k] = v;
 }
 
@@ -446,7 +452,9 @@ __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
   const size_t N = (size_t)nx * ny;
   const uint8_t* lab = S.labels + e * N;
   const double res = P.res;
-  long long scanned = 0;
+  long long scanned = 0;   // remaining path points the reference's stray check scans
+  long long pts_read = 0;  // path points this kernel reads (scans stop at the first hit)
+  long long los_read = 0;  // line-of-sight samples (label bytes) read
   AstarReq* reqs = reinterpret_cast<AstarReq*>(S.astar_req);
   // Every decision below is a boolean (near the path: min distance <= 1 m,
   // field.py:190; line of sight clear), so scans stop at the first hit.
@@ -482,7 +490,9 @@ __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
           bool near = glibc_hypot(qx - px, qy - py) <= kStrayLimit;
           double bx = qx, by = qy;
           const int kend = min(n, kLaneSegs + 1);
+          ++pts_read;
           for (int k = 1; k < kend && !near; ++k) {
+            ++pts_read;
             const double ax = bx, ay = by;
             path_point(cells, head, n, k, gx, gy, res, nx, bx, by);
             double abx = bx - ax, aby = by - ay;
@@ -521,6 +531,7 @@ __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
           const int k = k0 + lane;
           bool mine = false;
           if (k < sn) {
+            ++pts_read;
             double ax, ay, bx, by;
             path_point(cells, shead, sn, k - 1, sgx, sgy, res, nx, ax, ay);
             path_point(cells, shead, sn, k, sgx, sgy, res, nx, bx, by);
@@ -553,6 +564,7 @@ __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
         const long long k = k0 + lane;
         bool blocked = false;
         if (k < ns) {
+          ++los_read;
           double t = k == ns - 1 ? 1.0 : (double)k * step + 0.0;
           double xs = spx + (sgx - spx) * t, ys = spy + (sgy - spy) * t;
           long long rr = clampll(trunc_ll(ys / res), 0, ny - 1);
@@ -587,10 +599,16 @@ __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     scanned += __shfl_xor_sync(0xffffffffu, scanned, o);
+    pts_read += __shfl_xor_sync(0xffffffffu, pts_read, o);
+    los_read += __shfl_xor_sync(0xffffffffu, los_read, o);
     my_req += __shfl_xor_sync(0xffffffffu, my_req, o);
   }
   if (lane == 0 && scanned && S.counters)
     atomicAdd((unsigned long long*)&S.counters[1], (unsigned long long)scanned);
+  if (lane == 0 && pts_read && S.counters)
+    atomicAdd((unsigned long long*)&S.counters[12], (unsigned long long)pts_read);
+  if (lane == 0 && los_read && S.counters)
+    atomicAdd((unsigned long long*)&S.counters[13], (unsigned long long)los_read);
   if (lane == 0 && my_req) atomicAdd(&s_req, my_req);
   __syncthreads();
   const int n_req = s_req;
@@ -1613,6 +1631,166 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
   return (int)cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------- ORCA building blocks
+// The pieces of the tick as standalone batched calls, for the reference's
+// module-level / private entry points (crowd/orca.py, field.py:229-566).  They
+// run the same device functions as k_orca.
+constexpr int kApiCap = 64;   // constraints per row accepted by cw_orca_lp
+
+// _batched_lp (field.py:500-566): thread per row; the valid lanes of a row are
+// compacted in lane order (the fallback's `begin` is then the compacted index,
+// as searchsorted(lanes, fail) in the reference).
+__global__ void k_orca_lp(int N, int L, const double* __restrict__ points, const double* __restrict__ normals,
+                          const uint8_t* __restrict__ valid, const double* __restrict__ pref,
+                          const double* __restrict__ max_speed, const uint8_t* __restrict__ lane_active,
+                          double* __restrict__ out, int32_t* __restrict__ fell_back) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  double cpx[kApiCap], cpy[kApiCap], cnx[kApiCap], cny[kApiCap];
+  int nc = 0;
+  if (!lane_active || lane_active[i]) {
+    for (int l = 0; l < L; ++l) {
+      if (!valid[(size_t)i * L + l]) continue;
+      const size_t q = ((size_t)i * L + l) * 2;
+      put_slot(cpx, nc, points[q]); put_slot(cpy, nc, points[q + 1]);
+      put_slot(cnx, nc, normals[q]); put_slot(cny, nc, normals[q + 1]);
+      ++nc;
+    }
+  }
+  double v0, v1;
+  const bool fb = lane_lp(cpx, cpy, cnx, cny, nc, pref[2 * i], pref[2 * i + 1], max_speed[i], v0, v1);
+  out[2 * i] = v0;
+  out[2 * i + 1] = v1;
+  if (fell_back) fell_back[i] = fb ? 1 : 0;
+}
+
+// _vo_halfplane / orca_halfplane (field.py:448-495, orca.py:23-73): thread per row.
+__global__ void k_orca_halfplanes(int n, const double* __restrict__ rel_pos, const double* __restrict__ rel_vel,
+                                  const double* __restrict__ rr, const double* __restrict__ horizon, double dt,
+                                  const double* __restrict__ v_self, const double* __restrict__ share,
+                                  double* __restrict__ pt, double* __restrict__ nm) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  vo_halfplane(rel_pos[2 * i], rel_pos[2 * i + 1], rel_vel[2 * i], rel_vel[2 * i + 1], rr[i], horizon[i], dt,
+               v_self[2 * i], v_self[2 * i + 1], share[i], pt[2 * i], pt[2 * i + 1], nm[2 * i], nm[2 * i + 1]);
+}
+
+// _preferred_velocities + _build_constraints (field.py:214-350) for envs [e0, e1),
+// thread per agent, every lane in the reference layout: lanes [0, kmax) the stable
+// top-K neighbours by (fp32 Gram key, index) (invalid: point 0, normal (1, 0)),
+// lane kmax the robot (computed for every row, valid iff act and in range), lane
+// kmax + use_robot the static obstacle (every row; obstacle point 0 where none).
+// inr[row] = in-range neighbour count (the reference trims K to its maximum),
+// gap[row] = nearest-neighbour gap or +inf (last_gap_by_env, field.py:268-271).
+__global__ void k_crowd_constraints(cw_crowd_params P, cw_crowd_state S, int e0, int e1,
+                                    const uint8_t* __restrict__ act, const double* __restrict__ robot_pos,
+                                    const double* __restrict__ robot_vel, double robot_radius, int use_static,
+                                    int Lmax, double* __restrict__ pref, double* __restrict__ points,
+                                    double* __restrict__ normals, uint8_t* __restrict__ valid,
+                                    int32_t* __restrict__ inr, double* __restrict__ gap) {
+  const int A = P.A;
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;   // (e - e0) * A + a
+  if (row >= (e1 - e0) * A) return;
+  const int e = e0 + row / A, a = row % A;
+  const size_t eA = (size_t)e * A, ia = eA + a;
+  const uint8_t* ae = act + (size_t)(e - e0) * A;
+  const bool me = ae[a] != 0;
+  const double px = S.pos[ia * 2], py = S.pos[ia * 2 + 1];
+  const double vxa = S.vel[ia * 2], vya = S.vel[ia * 2 + 1], ra = S.radius[ia];
+  // preferred velocity (field.py:214-227); 0 for inactive rows
+  {
+    const double sp = S.pref_speed[ia];
+    const double tw0 = S.waypoint[ia * 2] - px, tw1 = S.waypoint[ia * 2 + 1] - py;
+    const double dist = sqrt(tw0 * tw0 + tw1 * tw1);
+    const double safe = fmax(dist, kEps);
+    double pf0 = tw0 / safe * sp, pf1 = tw1 / safe * sp;
+    const double tg0 = S.goal[ia * 2] - px, tg1 = S.goal[ia * 2 + 1] - py;
+    const double dg = sqrt(tg0 * tg0 + tg1 * tg1);
+    const double scl = fmin(1.0, dg / fmax(sp * P.dt * 4, kEps));
+    pref[(size_t)row * 2] = me ? pf0 * scl : 0.0;
+    pref[(size_t)row * 2 + 1] = me ? pf1 * scl : 0.0;
+  }
+  const int kmax = min(P.max_neighbors, max(A - 1, 0));
+  double* prow = points + (size_t)row * Lmax * 2;
+  double* nrow = normals + (size_t)row * Lmax * 2;
+  uint8_t* vrow = valid + (size_t)row * Lmax;
+  for (int l = 0; l < Lmax; ++l) { prow[2 * l] = 0.0; prow[2 * l + 1] = 0.0; nrow[2 * l] = 1.0; nrow[2 * l + 1] = 0.0; vrow[l] = 0; }
+  // neighbours: fp32 key (sq_i + sq_j) - 2 fma(y_i, y_j, x_i x_j), stable by index
+  const float xi = (float)px, yi = (float)py;
+  const float sqi = __fadd_rn(__fmul_rn(xi, xi), __fmul_rn(yi, yi));
+  int cnt = 0, nb = 0;
+  float lk = -CUDART_INF_F;
+  int lj = -1;
+  if (me) {
+    for (int round = 0; round <= kmax; ++round) {
+      float bk = CUDART_INF_F;
+      int bj = -1;
+      for (int j = 0; j < A; ++j) {
+        if (j == a || !ae[j]) continue;
+        const float xj = (float)S.pos[(eA + j) * 2], yj = (float)S.pos[(eA + j) * 2 + 1];
+        const float sqj = __fadd_rn(__fmul_rn(xj, xj), __fmul_rn(yj, yj));
+        const float dot = __fmaf_rn(yi, yj, __fmul_rn(xi, xj));
+        const float key = __fsub_rn(__fadd_rn(sqi, sqj), __fmul_rn(2.0f, dot));
+        if (!(key < P.nd2_f32)) continue;
+        if (round == 0) ++cnt;
+        const bool after = key > lk || (key == lk && j > lj);
+        const bool better = bj < 0 || key < bk || (key == bk && j < bj);
+        if (after && better) { bk = key; bj = j; }
+      }
+      if (bj < 0 || round == kmax) break;
+      lk = bk;
+      lj = bj;
+      const size_t ij = eA + bj;
+      const double rp0 = S.pos[ij * 2] - px, rp1 = S.pos[ij * 2 + 1] - py;
+      const double rv0 = vxa - S.vel[ij * 2], rv1 = vya - S.vel[ij * 2 + 1];
+      const double rr = ra + S.radius[ij] + P.safety_margin;
+      vo_halfplane(rp0, rp1, rv0, rv1, rr, P.time_horizon, P.dt, vxa, vya, 0.5, prow[2 * nb], prow[2 * nb + 1],
+                   nrow[2 * nb], nrow[2 * nb + 1]);
+      vrow[nb] = 1;
+      if (nb == 0) gap[row] = sqrt(rp0 * rp0 + rp1 * rp1) - (ra + S.radius[ij]);
+      ++nb;
+    }
+  }
+  if (nb == 0) gap[row] = CUDART_INF;
+  inr[row] = cnt;
+  int lane = kmax;
+  if (robot_pos) {
+    const double rpx = robot_pos[e * 2], rpy = robot_pos[e * 2 + 1];
+    const double rvx = robot_vel ? robot_vel[e * 2] : 0.0, rvy = robot_vel ? robot_vel[e * 2 + 1] : 0.0;
+    const double rp0 = rpx - px, rp1 = rpy - py;
+    const double d2 = rp0 * rp0 + rp1 * rp1;
+    const double rr = ra + robot_radius + P.safety_margin;
+    vo_halfplane(rp0, rp1, vxa - rvx, vya - rvy, rr, P.obstacle_time_horizon, P.dt, vxa, vya, 1.0,
+                 prow[2 * lane], prow[2 * lane + 1], nrow[2 * lane], nrow[2 * lane + 1]);
+    vrow[lane] = me && d2 < P.nd2;
+    ++lane;
+  }
+  if (use_static) {
+    const int nx = P.nx, ny = P.ny;
+    const size_t N = (size_t)nx * ny;
+    const double res = P.res;
+    double ox = 0.0, oy = 0.0;
+    bool has = false;
+    if (S.has_obs[e]) {
+      const long long ri = clampll(trunc_ll(py / res), 0, ny - 1);
+      const long long ci = clampll(trunc_ll(px / res), 0, nx - 1);
+      const int flat = S.nearest[e * N + ri * nx + ci];
+      has = flat >= 0;
+      const int f = max(flat, 0);
+      const int orow = f / nx, ocol = f - orow * nx;
+      ox = ((double)ocol + 0.5) * res;
+      oy = ((double)orow + 0.5) * res;
+    }
+    const double rp0 = ox - px, rp1 = oy - py;
+    const double d2 = rp0 * rp0 + rp1 * rp1;
+    const double margin = 0.5 * kSqrt2 * P.res0;
+    const double rr = ra + margin + P.safety_margin;
+    vo_halfplane(rp0, rp1, vxa, vya, rr, P.obstacle_time_horizon, P.dt, vxa, vya, 1.0, prow[2 * lane],
+                 prow[2 * lane + 1], nrow[2 * lane], nrow[2 * lane + 1]);
+    vrow[lane] = has && me && d2 < P.nd2;
+  }
+}
 }  // namespace cw
 
 extern "C" {
@@ -1713,6 +1891,40 @@ int cw_child_seeds(int n, const uint64_t* parent, int label_id, const uint64_t* 
                    void* stream) {
   if (n <= 0) return 0;
   cw::k_child_seeds<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(n, parent, label_id, k, out);
+  return (int)cudaGetLastError();
+}
+
+
+// ---------------------------------------------------------------- ORCA building blocks
+int cw_orca_lp(int N, int L, const double* points, const double* normals, const uint8_t* valid,
+               const double* pref, const double* max_speed, const uint8_t* lane_active, double* out,
+               int32_t* fell_back, void* stream) {
+  if (N <= 0) return 0;
+  if (L < 0 || L > cw::kApiCap) return (int)cudaErrorInvalidValue;
+  cw::k_orca_lp<<<(N + 127) / 128, 128, 0, (cudaStream_t)stream>>>(N, L, points, normals, valid, pref, max_speed,
+                                                                   lane_active, out, fell_back);
+  return (int)cudaGetLastError();
+}
+
+int cw_orca_halfplanes(int n, const double* rel_pos, const double* rel_vel, const double* combined_radius,
+                       const double* horizon, double dt, const double* v_self, const double* share,
+                       double* point, double* normal, void* stream) {
+  if (n <= 0) return 0;
+  cw::k_orca_halfplanes<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(n, rel_pos, rel_vel, combined_radius,
+                                                                           horizon, dt, v_self, share, point,
+                                                                           normal);
+  return (int)cudaGetLastError();
+}
+
+int cw_crowd_constraints(const cw_crowd_params* P, const cw_crowd_state* S, int e0, int e1, const uint8_t* act,
+                         const double* robot_pos, const double* robot_vel, double robot_radius, int use_static,
+                         int lmax, double* pref, double* points, double* normals, uint8_t* valid, int32_t* inr,
+                         double* gap, void* stream) {
+  const int rows = (e1 - e0) * P->A;
+  if (rows <= 0) return 0;
+  cw::k_crowd_constraints<<<(rows + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
+      *P, *S, e0, e1, act, robot_pos, robot_vel, robot_radius, use_static, lmax, pref, points, normals, valid,
+      inr, gap);
   return (int)cudaGetLastError();
 }
 

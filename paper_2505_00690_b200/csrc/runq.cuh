@@ -19,7 +19,8 @@ namespace cw {
 enum { kRunGuide = 0, kRunWait = 1, kRunDone = 3, kRunBusy = 1 << 30 };
 constexpr int kPendingGuard = 1 << 24;   // > any per-env request count
 constexpr long long kSpinCycles = 8ll << 30;    // ~4.5 s: a full ring slot is an error, not a hang
-constexpr long long kIdleCycles = 64ll << 30;   // ~35 s backstop for an idle server warp (the
+constexpr long long kIdleCycles = 64ll << 30;   // ~35 s backstop for a server warp that saw no
+                                                // env-tick complete anywhere for that long (the
                                                 // host normally ends the run via q->shutdown)
 
 struct RunQueue {                 // device-resident control words
@@ -136,9 +137,14 @@ CW_DEV int ready_pop(const RunArgs& ra) {
 CW_DEV bool ring_pop(const RunArgs& ra, AstarReq& R) {
   const unsigned long long pos = atomicAdd(&ra.q->head, 1ull);
   unsigned long long* sq = ra.seq + (pos & ra.mask);
-  const long long t0 = clock64();
+  // the idle clock restarts whenever the run makes progress: an obstacle-free
+  // batch never queues a search, so a long run must not time its server out
+  long long t0 = clock64();
+  int seen = *(volatile int*)&ra.q->progress;
   while (ld_acquire_u64(sq) != pos + 1) {
     if (*(volatile int*)&ra.q->shutdown) return false;
+    const int now = *(volatile int*)&ra.q->progress;
+    if (now != seen) { seen = now; t0 = clock64(); }
     if (clock64() - t0 > kIdleCycles) { atomicCAS(&ra.q->error, 0, 2); return false; }
     __nanosleep(64);
   }

@@ -13,10 +13,11 @@
 //   k_spawn      kinds, routes, speeds              step.py:37-63, routes.py:14-87
 //
 // One CTA (or warp) owns one env; results do not depend on launch shape.
+#include <algorithm>
 #include <cstdio>
 #include "common.cuh"
 #include "rng.cuh"
-#include "scene_types.cuh"
+#include "citywalk_b200.h"
 
 namespace cw {
 
@@ -806,7 +807,7 @@ __global__ void __launch_bounds__(TER_WARPS * 32) k_terrain(cw_scene_params P, i
                                                             cw_scene_buffers B) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int e = blockIdx.x * TER_WARPS + wid;
+  const int e = blockIdx.x * (blockDim.x >> 5) + wid;   // warps per CTA: as many lattices as fit
   if (e >= E) return;
   const int slot = env_slot(slots, e);
   if (B.status[slot] != CW_OK) return;
@@ -1402,6 +1403,16 @@ CW_DEV bool spawn_region_ok(const cw_scene_params& P, int c) {
   return false;
 }
 
+// candidate cell of sample_routes (routes.py:50-56): Walkable (| Roadway for vehicle
+// kinds), the Traverse strip mask (batch.py:174-177) and a caller region mask
+CW_DEV bool route_ok(const cw_scene_params& P, const cw_scene_buffers& B, int slot, const uint8_t* Lb, int f,
+                     int N) {
+  const uint8_t l = Lb[f];
+  if (!(l == L_WALKABLE || (P.route_roadway && l == L_ROADWAY))) return false;
+  if (P.spawn_region == 1 && !spawn_region_ok(P, f % P.nx)) return false;
+  return !B.region || B.region[(size_t)slot * N + f] != 0;
+}
+
 // numpy Generator.permutation(n) = Fisher-Yates from the top over a pure next32
 // stream (random_interval, masked rejection).  Only the first few entries of the
 // final order are consumed (routes.py:69-83), so the kernel (1) generates the
@@ -1428,9 +1439,11 @@ CW_DEV int resolve_final(int k, const int32_t* jj, const int32_t* head, const in
   }
 }
 
+// route_seeds == nullptr: spawn_agents (step.py:37-63: kinds, routes seed, speeds);
+// else sample_routes(occ, peds, route_seeds[e], ..., max_radius) alone (routes.py:35).
 __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const int32_t* slots,
                                                  const EnvSeeds* __restrict__ seeds,
-                                                 cw_scene_buffers B) {
+                                                 cw_scene_buffers B, const uint64_t* __restrict__ route_seeds) {
   const int e = blockIdx.x;
   const int slot = env_slot(slots, e);
   const int A = P.peds;
@@ -1460,7 +1473,10 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
   double* sty = stx + A;
   int8_t* kind_out = B.sp_kind + (size_t)slot * A;
   double* pref_out = B.sp_pref + (size_t)slot * A;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && route_seeds) {
+    s_seed = route_seeds[e];
+    s_maxr = P.route_max_radius;
+  } else if (threadIdx.x == 0) {
     // step.py:41-61 (the spawn stream is independent of the routes stream)
     Pcg64 rng = pcg_load(seeds[e].spawn);
     double maxr = 0.0;
@@ -1481,7 +1497,7 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
   int base = 0;
   for (int f0 = 0; f0 < N; f0 += SP_NT) {
     int f = f0 + threadIdx.x;
-    int ok = f < N && Lb[f] == L_WALKABLE && (P.spawn_region != 1 || spawn_region_ok(P, f % nx));
+    int ok = f < N && route_ok(P, B, slot, Lb, f, N);
     if (f < N) { comp[f] = ok ? f : -1; head[f] = -1; csize[f] = 0; }
     int tot;
     int off = block_excl_scan<SP_NT>(ok, sh, tot);
@@ -1497,9 +1513,7 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
   }
   // 8-connected components (routes.py:14-32); only label equality is used
   // downstream (routes.py:62, 74), so any labelling works.
-  grid_components<SP_NT, true>(comp, nx, ny, [&](int f) {
-    return Lb[f] == L_WALKABLE && (P.spawn_region != 1 || spawn_region_ok(P, f % nx));
-  });
+  grid_components<SP_NT, true>(comp, nx, ny, [&](int f) { return route_ok(P, B, slot, Lb, f, N); });
   for (int q = threadIdx.x; q < n; q += SP_NT) atomicAdd(&csize[comp[cand[q]]], 1);
   __syncthreads();
   // ---- permutation draws (warp 0): stream generation + warp-speculative
@@ -1725,6 +1739,67 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
   if (threadIdx.x == 0 && s_acc < A) B.status[slot] = CW_E_NOROUTE;
 }
 
+
+// connected_components (routes.py:14-32): the reference numbers components in the
+// order of their first cell in row-major order; the union-find root is the
+// component's smallest flat index, so id = rank of the root among the roots.
+__global__ void __launch_bounds__(1024) k_components(int nx, int ny, const uint8_t* __restrict__ ok,
+                                                     int32_t* __restrict__ comp, int32_t* __restrict__ rank) {
+  const int e = blockIdx.x;
+  const int N = nx * ny;
+  const uint8_t* okb = ok + (size_t)e * N;
+  volatile int32_t* par = comp + (size_t)e * N;
+  int32_t* rk = rank + (size_t)e * N;
+  grid_components<1024, true>(par, nx, ny, [&](int f) { return okb[f] != 0; });
+  __shared__ int sh[1024 / 32 + 1];
+  int base = 0;
+  for (int f0 = 0; f0 < N; f0 += 1024) {
+    const int f = f0 + threadIdx.x;
+    const int root = f < N && par[f] == f;
+    int tot;
+    const int off = block_excl_scan<1024>(root, sh, tot);
+    if (root) rk[f] = base + off;
+    base += tot;
+  }
+  __syncthreads();
+  for (int f = threadIdx.x; f < N; f += 1024) {
+    const int r = par[f];
+    par[f] = r >= 0 ? rk[r] : -1;
+  }
+}
+
+// rasterize_occupancy at any resolution (occupancy.py:28-57): labels from the zone
+// grid at (row, col) = min(((i + 0.5) res) / zone_res, zone_n - 1) (truncated),
+// elevation at cell centres; k_footprint then marks the objects.
+__global__ void __launch_bounds__(256) k_raster_res(cw_scene_params P, int E, const int32_t* slots, int zx, int zy,
+                                                    double zone_res, cw_scene_buffers B) {
+  const int e = blockIdx.y;
+  const int slot = env_slot(slots, e);
+  if (B.status[slot] != CW_OK) return;
+  const size_t N = (size_t)P.nx * P.ny;
+  const size_t f = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= N) return;
+  const int r = (int)(f / P.nx), c = (int)(f - (size_t)r * P.nx);
+  const long long zr = (long long)fmin(((double)r + 0.5) * P.res / zone_res, (double)(zy - 1));
+  const long long zc = (long long)fmin(((double)c + 0.5) * P.res / zone_res, (double)(zx - 1));
+  B.labels[(size_t)slot * N + f] = zone_to_label(B.zones[(size_t)slot * zx * zy + zr * zx + zc]);
+  const int32_t* A = B.assign + (size_t)slot * P.trows * P.tcols;
+  const int8_t* cd = B.tile_code + (size_t)slot * CW_MAX_TILES;
+  const double* tp = B.tile_p + (size_t)slot * CW_MAX_TILES * 4;
+  const double x = ((double)c + 0.5) * P.res, y = ((double)r + 0.5) * P.res;
+  B.elev[(size_t)slot * N + f] = (float)elevation_at(x, y, P.trows, P.tcols, A, cd, tp, B.noise_seed[slot]);
+}
+
+
+// trig probe (parity tooling): the device sin/cos the sampling kernels can use
+__global__ void k_trig_probe(int n, const double* __restrict__ x, double* __restrict__ s, double* __restrict__ c,
+                             int mode) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (mode == 1) cr_sincos(x[i], s + i, c + i);
+  else sincos(x[i], s + i, c + i);
+}
+
 struct SideStreams {
   int dev = -1;
   cudaStream_t s[2];
@@ -1770,9 +1845,13 @@ int cw_sample_scenes(const cw_scene_params* P, int E, const uint64_t* scene_seed
   k_seeds<<<(E + 127) / 128, 128, 0, st>>>(E, scene_seeds, crowd_seeds, S);
   if (p.layout == 1) k_zones_blk<<<E, 512, 0, st>>>(p, E, slots, S, b);
   else k_zones<<<E, 256, 0, st>>>(p, E, slots, S, b);
-  const size_t tsm = terrain_warp_smem(p.trows * p.tcols) * TER_WARPS;
+  // one warp per env; up to TER_WARPS lattices per CTA (large lattices: fewer, <= 227 KB)
+  const size_t per = terrain_warp_smem(p.trows * p.tcols);
+  const int wpc = (int)std::max<size_t>(1, std::min<size_t>(TER_WARPS, (227u * 1024u) / per));
+  if (per > 227u * 1024u) return (int)cudaErrorInvalidValue;
+  const size_t tsm = per * wpc;
   cudaFuncSetAttribute(k_terrain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-  k_terrain<<<(E + TER_WARPS - 1) / TER_WARPS, TER_WARPS * 32, tsm, st>>>(p, E, slots, S, b);
+  k_terrain<<<(E + wpc - 1) / wpc, wpc * 32, tsm, st>>>(p, E, slots, S, b);
   k_place<<<(E + 3) / 4, 128, 0, st>>>(p, E, slots, S, b);
   const int quads = (p.nx * p.ny + 3) / 4;
   k_raster<<<dim3((quads + 255) / 256, E), 256, 0, st>>>(p, E, slots, b);
@@ -1789,7 +1868,7 @@ int cw_sample_scenes(const cw_scene_params* P, int E, const uint64_t* scene_seed
   if (p.peds > 0) {
     size_t sm = (size_t)p.peds * 2 * sizeof(double);
     if (sm > 48 * 1024) cudaFuncSetAttribute(k_spawn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_spawn<<<E, SP_NT, sm, st>>>(p, E, slots, S, b);
+    k_spawn<<<E, SP_NT, sm, st>>>(p, E, slots, S, b, nullptr);
   }
   cudaEventRecord(ss.join[0], ss.s[0]);
   cudaEventRecord(ss.join[1], ss.s[1]);
@@ -1809,7 +1888,56 @@ int cw_spawn_agents(const cw_scene_params* P, int E, const uint64_t* crowd_seeds
   k_seeds<<<(E + 127) / 128, 128, 0, st>>>(E, crowd_seeds, crowd_seeds, S);
   size_t sm = (size_t)P->peds * 2 * sizeof(double);
   if (sm > 48 * 1024) cudaFuncSetAttribute(k_spawn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_spawn<<<E, SP_NT, sm, st>>>(*P, E, slots, S, *B);
+  k_spawn<<<E, SP_NT, sm, st>>>(*P, E, slots, S, *B, nullptr);
+  return (int)cudaGetLastError();
+}
+
+
+// sample_routes(occupancy, count, seed, kind, region_mask, max_radius) (routes.py:35-87)
+// for rows slots[e] of buffers->labels: params->peds routes, route_roadway for
+// vehicle kinds, route_max_radius the separation radius, buffers->region an optional
+// (E, ny*nx) u8 mask; starts / goals in sp_pos / sp_goal, NoRouteAvailable in status.
+int cw_sample_routes(const cw_scene_params* P, int E, const uint64_t* route_seeds, const int32_t* slots,
+                     void* seed_scratch, const cw_scene_buffers* B, void* stream) {
+  using namespace cw;
+  if (E <= 0 || P->peds <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  EnvSeeds* S = (EnvSeeds*)seed_scratch;
+  size_t sm = (size_t)P->peds * 2 * sizeof(double);
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_spawn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_spawn<<<E, SP_NT, sm, st>>>(*P, E, slots, S, *B, route_seeds);
+  return (int)cudaGetLastError();
+}
+
+// connected_components(ok) (routes.py:14-32) for E grids ok (E, ny*nx) u8 -> comp
+// (E, ny*nx) int32 (-1 where not ok); rank_scratch (E, ny*nx) int32.
+int cw_connected_components(int nx, int ny, int E, const uint8_t* ok, int32_t* comp, int32_t* rank_scratch,
+                            void* stream) {
+  if (E <= 0 || nx <= 0 || ny <= 0) return 0;
+  cw::k_components<<<E, 1024, 0, (cudaStream_t)stream>>>(nx, ny, ok, comp, rank_scratch);
+  return (int)cudaGetLastError();
+}
+
+// rasterize_occupancy(scene, resolution) (occupancy.py:28-57) at params->res /
+// nx / ny for rows slots[e]: buffers->zones holds the (zone_ny, zone_nx) zone grid
+// at zone_res, assign / tile_code / tile_p / noise_seed the terrain, obj_* the
+// objects; writes labels and elev (ny*nx) of the row; status must be zero.
+int cw_rasterize(const cw_scene_params* P, int E, const int32_t* slots, int zone_nx, int zone_ny,
+                 double zone_res, const cw_scene_buffers* B, void* stream) {
+  using namespace cw;
+  if (E <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t N = (size_t)P->nx * P->ny;
+  k_raster_res<<<dim3((unsigned)((N + 255) / 256), E), 256, 0, st>>>(*P, E, slots, zone_nx, zone_ny, zone_res, *B);
+  if (P->obj_max > 0) k_footprint<<<dim3((P->obj_max + 3) / 4, E), 128, 0, st>>>(*P, E, slots, *B);
+  return (int)cudaGetLastError();
+}
+
+
+// sin / cos of n doubles on the device: mode 0 CUDA sincos, 1 cr_sincos (common.cuh).
+int cw_trig_probe(int n, const double* x, double* s, double* c, int mode, void* stream) {
+  if (n <= 0) return 0;
+  cw::k_trig_probe<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(n, x, s, c, mode);
   return (int)cudaGetLastError();
 }
 

@@ -20,7 +20,7 @@
 #include <cstdint>
 
 #include "common.cuh"
-#include "scene_types.cuh"
+#include "citywalk_b200.h"
 
 namespace {
 

@@ -21,11 +21,11 @@ from enum import Enum
 import numpy as np
 
 from . import _lib
-from .crowd import CrowdConfig, CrowdField
+from .crowd import CrowdConfig, CrowdField, DeviceView
 from .errors import BatchShapeMismatch, SlotOutOfRange
 from .rng import child_seed, child_seeds_device, seeds_to_tensor
 from .robot import EVENT_NAMES, ROBOT_MODELS, RewardConfig, RobotBatch
-from .urbangen import SceneSampler, SceneSpec
+from .urbangen import SceneSampler, SceneSpec, as_spec
 
 
 class Scheme(str, Enum):
@@ -80,11 +80,11 @@ class BatchedEnv:
         import torch
         self.config = config or EnvConfig()
         self.scheme = Scheme(scheme)
-        if isinstance(specs, SceneSpec):
+        if hasattr(specs, "to_dict"):
             k = 1 if k is None else k
-            base = specs
+            base = as_spec(specs)
         else:
-            specs = list(specs)
+            specs = [as_spec(s) for s in specs]
             k = len(specs)
             base = specs[0]
             if any(replace(s, seed=0) != replace(base, seed=0) for s in specs):
@@ -226,26 +226,19 @@ class BatchedEnv:
         """Install robot poses (e.g. the reference's route-anchor spawns)."""
         self.robot.set_state(x, y, yaw, goal, vx=vx, vy=vy, elev=elev, tick=tick, rows=rows)
 
-    # robot pose arrays as the reference exposes them (batch.py:98-110), host copies
-    @property
-    def x(self):
-        return self.robot.x.cpu().numpy()
-
-    @property
-    def y(self):
-        return self.robot.y.cpu().numpy()
-
-    @property
-    def yaw(self):
-        return self.robot.yaw.cpu().numpy()
-
-    @property
-    def vx(self):
-        return self.robot.vx.cpu().numpy()
-
-    @property
-    def vy(self):
-        return self.robot.vy.cpu().numpy()
+    # robot state arrays as the reference exposes them (batch.py:98-110): DeviceView
+    # windows onto the device tensors (reads copy to the host, item assignment
+    # writes through, e.g. ``env.goal[0] = (x, y)``)
+    x = property(lambda self: DeviceView(self.robot.x))
+    y = property(lambda self: DeviceView(self.robot.y))
+    yaw = property(lambda self: DeviceView(self.robot.yaw))
+    vx = property(lambda self: DeviceView(self.robot.vx))
+    vy = property(lambda self: DeviceView(self.robot.vy))
+    elev = property(lambda self: DeviceView(self.robot.el))
+    goal = property(lambda self: DeviceView(self.robot.goal))
+    tick = property(lambda self: DeviceView(self.robot.tick))
+    terminated = property(lambda self: DeviceView(self.robot.terminated, bool))
+    truncated = property(lambda self: DeviceView(self.robot.truncated, bool))
 
     def robot_state(self, i=0):
         r = self.robot
@@ -323,7 +316,7 @@ def _scene_out_fields():
     """SceneBatch outputs a re-sampled row consists of (everything but scratch)."""
     global _SCENE_OUT
     if _SCENE_OUT is None:
-        _SCENE_OUT = [n for n in _lib.SCENE_BUFFER_FIELDS if not n.startswith("scratch")] + [
+        _SCENE_OUT = [n for n in _lib.SCENE_BUFFER_FIELDS if not n.startswith("scratch") and n != "region"] + [
             "routes", "n_routes", "scene_seed"]
     return _SCENE_OUT
 

@@ -33,9 +33,12 @@ def gather_env_stats(stats, group=None):
     if not dist.is_available() or not dist.is_initialized():
         return stats
     world = dist.get_world_size(group)
+    dev = stats.device
+    if dist.get_backend(group) == "gloo" and dev.type != "cpu":
+        stats = stats.cpu()         # gloo gathers host tensors
     out = [torch.empty_like(stats) for _ in range(world)]
     dist.all_gather(out, stats.contiguous(), group=group)
-    return torch.cat(out, 0)
+    return torch.cat(out, 0).to(dev)
 
 
 def max_over_ranks(value, device=None, group=None):
@@ -44,9 +47,24 @@ def max_over_ranks(value, device=None, group=None):
     import torch.distributed as dist
     if not dist.is_available() or not dist.is_initialized():
         return float(value)
+    if dist.get_backend(group) == "gloo":
+        device = "cpu"
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+def max_tensor_over_ranks(t, group=None):
+    """Elementwise max of a float64 tensor over ranks (NCCL device / gloo host)."""
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized():
+        return t
+    dev = t.device
+    if dist.get_backend(group) == "gloo" and dev.type != "cpu":
+        t = t.cpu()
+    t = t.clone()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return t.to(dev)
 
 
 _P = 2147483647   # 2^31 - 1: every product below stays < 2^62, every row sum < 2^63

@@ -234,6 +234,9 @@ class ZoneMap:
     def shape(self):
         return self.grid.shape
 
+    def counts(self):
+        return {z.name: int(np.count_nonzero(self.grid == int(z))) for z in Zone}
+
 
 @dataclass
 class TerrainTile:
@@ -262,6 +265,26 @@ class TerrainGrid:
     noise_seed: int
     assignment_rle: list = None
 
+    def kind_at(self, row, col):
+        return self.tiles[int(self.assignment[row, col])].kind
+
+    def to_dict(self):
+        """types.py:274-285."""
+        from .sceneio import rle_encode
+        rle = self.assignment_rle if self.assignment_rle is not None else rle_encode(
+            np.asarray(self.assignment).astype(np.int64))
+        return {"tile_size": float(self.tile_size), "rows": int(self.rows), "cols": int(self.cols),
+                "tiles": [t.to_dict() for t in self.tiles], "assignment_rle": rle,
+                "noise_seed": int(self.noise_seed)}
+
+    @staticmethod
+    def from_dict(d):
+        from .sceneio import rle_decode
+        a = rle_decode(d["assignment_rle"], dtype=np.int64).reshape(d["rows"], d["cols"]).astype(np.int32)
+        return TerrainGrid(float(d["tile_size"]), int(d["rows"]), int(d["cols"]),
+                           [TerrainTile.from_dict(t) for t in d["tiles"]], a, int(d["noise_seed"]),
+                           assignment_rle=list(d["assignment_rle"]))
+
 
 @dataclass
 class AssetInstance:
@@ -282,6 +305,14 @@ class AssetInstance:
     def from_dict(d):
         return AssetInstance(d["category"], float(d["x"]), float(d["y"]), float(d["yaw"]),
                              (float(d["footprint"][0]), float(d["footprint"][1])), float(d["height"]))
+
+    def corners(self):
+        """types.py:355-361: world-space corners of the oriented footprint, (4, 2)
+        (a host convenience for callers; placement itself runs in k_place)."""
+        hw, hl = self.footprint[0] / 2.0, self.footprint[1] / 2.0
+        local = np.array([[-hw, -hl], [hw, -hl], [hw, hl], [-hw, hl]])
+        c, s = np.cos(self.yaw), np.sin(self.yaw)
+        return local @ np.array([[c, -s], [s, c]]).T + np.array([self.x, self.y])
 
 
 @dataclass
@@ -336,8 +367,8 @@ def scene_params(spec, catalog=None, obj_max=None):
         p.quad_cdf[i] = float(cdf[i])
     p.trows = max(1, int(np.ceil(p.ny * res / TILE_SIZE_M)))
     p.tcols = max(1, int(np.ceil(p.nx * res / TILE_SIZE_M)))
-    if p.trows * p.tcols > 1024:
-        raise NotImplementedError("terrain lattices above 32x32 tiles")
+    if p.trows * p.tcols > 10000:
+        raise NotImplementedError("terrain lattices above 100x100 tiles (one WFC warp's shared memory)")
     p.cpt = int(round(TILE_SIZE_M / res))
     p.nonflat_split_col = int(p.nx * 0.5) if task == TaskKind.TRAVERSE else -1
     p.n_cat = len(catalog)
@@ -407,6 +438,7 @@ class SceneBatch:
         self.scene_seed = z((E,), dtype=torch.int64, **d)
         self.zone_params = z((E, _lib.ZONE_PARAMS), dtype=torch.float64, **d)   # ZoneMap.params
         self.block_var = z((E, _lib.MAX_BLOCKS), dtype=torch.uint8, **d)        # connect_blocks
+        self.region = None   # optional (E, N) u8 route region mask (spawn_agents(region_mask=))
         self._scratch_rows = 0
         self._ensure_scratch(min(E, SceneSampler.max_rows))
 
@@ -426,7 +458,8 @@ class SceneBatch:
     def buffers(self):
         b = _lib.SceneBuffers()
         for name in _lib.SCENE_BUFFER_FIELDS:
-            setattr(b, name, getattr(self, name).data_ptr())
+            t = getattr(self, name)
+            setattr(b, name, None if t is None else t.data_ptr())
         return b
 
     def check_status(self, rows=None):
@@ -554,16 +587,79 @@ def _as_u64_tensor(seeds, device):
     return torch.from_numpy(arr).to(device)
 
 
+def as_spec(spec):
+    """A SceneSpec from any spec object with the reference's ``to_dict`` (e.g. the
+    reference's own SceneSpec passed to the drop-in)."""
+    return spec if isinstance(spec, SceneSpec) else SceneSpec.from_dict(spec.to_dict())
+
+
 def generate_scene(spec, catalog=None, device="cuda"):
     """scene.py:38 generate_scene on the device (including the route anchors).
     The returned scene already carries its occupancy raster."""
+    spec = as_spec(spec)
     s = SceneSampler(spec, 1, catalog, device)
     b = s.sample([spec.seed])
     return b.scene(0, spec, s.catalog)
 
 
 def rasterize_occupancy(scene, resolution=None):
-    """occupancy.py:28 -- the device pipeline rasterises at the spec resolution."""
-    if resolution is not None and resolution != scene.spec.grid_resolution_m:
-        raise NotImplementedError("the B200 path rasterises at spec.grid_resolution_m only")
-    return scene.occupancy
+    """occupancy.py:28-57.  At the spec resolution a sampled scene already carries
+    its device raster; any other resolution (or a scene without one, e.g. loaded
+    from JSON) is rasterised on the device by ``cw_rasterize`` from the scene's zone
+    grid, terrain tiles and objects."""
+    import torch
+    if resolution is None:
+        resolution = scene.spec.grid_resolution_m
+    if resolution <= 0:
+        raise ValueError("resolution must be > 0")
+    if resolution == scene.spec.grid_resolution_m and getattr(scene, "occupancy", None) is not None:
+        return scene.occupancy
+    from .sceneio import _T_CORNER, _T_ROUGH, _T_STAIR_U, _T_STAIR_V
+    w, l = scene.spec.extent_m
+    nx, ny = int(np.ceil(w / resolution)), int(np.ceil(l / resolution))
+    zg = np.ascontiguousarray(np.asarray(scene.zones.grid, dtype=np.uint8))
+    zy, zx = zg.shape
+    terr = scene.terrain
+    tiles = list(terr.tiles)
+    if len(tiles) > _lib.MAX_TILES:
+        raise ValueError(f"more than {_lib.MAX_TILES} terrain tiles")
+    code = np.zeros(_lib.MAX_TILES, dtype=np.int8)
+    tp = np.zeros((_lib.MAX_TILES, 4), dtype=np.float64)
+    for i, t in enumerate(tiles):
+        sh = t.shape
+        if sh["type"] == "corner":
+            code[i], tp[i] = _T_CORNER, sh["h"]
+        elif sh["type"] == "stair":
+            code[i] = _T_STAIR_U if sh["axis"] == "u" else _T_STAIR_V
+            tp[i, :2] = sh["a"], sh["b"]
+        else:
+            code[i] = _T_ROUGH
+            tp[i, :2] = sh["base"], sh["amp"]
+    objs = list(scene.objects)
+    foot = sorted({(float(o.footprint[0]), float(o.footprint[1])) for o in objs})
+    if len(foot) > _lib.MAX_CAT:
+        raise ValueError(f"more than {_lib.MAX_CAT} distinct object footprints")
+    p = _lib.SceneParams()
+    p.nx, p.ny, p.res = nx, ny, float(resolution)
+    p.trows, p.tcols = int(terr.rows), int(terr.cols)
+    p.n_cat = len(foot)
+    for k, (fw, fl) in enumerate(foot):
+        p.cat_w[k], p.cat_l[k] = fw, fl
+    p.obj_max = max(1, len(objs))
+    b = SceneBatch(p, 1)
+    dev = b.device
+    b.zones = torch.from_numpy(zg.reshape(1, zy * zx)).to(dev)
+    b.assign[0] = torch.from_numpy(np.asarray(terr.assignment, dtype=np.int32)).to(dev)
+    b.tile_code[0] = torch.from_numpy(code).to(dev)
+    b.tile_p[0] = torch.from_numpy(tp).to(dev)
+    b.noise_seed[0] = int(np.uint64(int(terr.noise_seed) & ((1 << 64) - 1)).view(np.int64))
+    if objs:
+        b.obj_cat[0, :len(objs)] = torch.tensor([foot.index((float(o.footprint[0]), float(o.footprint[1])))
+                                                 for o in objs], dtype=torch.int32, device=dev)
+        b.obj_pose[0, :len(objs)] = torch.tensor([[o.x, o.y, o.yaw] for o in objs], dtype=torch.float64,
+                                                 device=dev)
+    b.obj_n[0] = len(objs)
+    _lib.check(_lib.lib().cw_rasterize(p, 1, None, zx, zy, float(scene.zones.resolution), b.buffers(),
+                                       _lib.stream_ptr()), "cw_rasterize")
+    return OccupancyGrid(resolution=float(resolution), labels=b.labels[0].cpu().numpy(),
+                         elevation=b.elev[0].cpu().numpy())
