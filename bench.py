@@ -281,6 +281,9 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     run_resampled = 0
+    prof_range = bool(os.environ.get("CW_PROFILE_RANGE"))   # ncu --replay-mode app-range window
+    if prof_range:
+        torch.cuda.profiler.start()
     t_run0 = time.perf_counter()
     r0.record(st)
     if CFG["resample"] > 0:
@@ -297,6 +300,8 @@ def run_ours(args):
     r1.record(st)
     torch.cuda.synchronize()
     t_run1 = time.perf_counter()
+    if prof_range:
+        torch.cuda.profiler.stop()
     f.check_flags()
     run_ms = r0.elapsed_time(r1)
     c_run = f.stats()
@@ -304,11 +309,11 @@ def run_ours(args):
         rs_ = f.last_run_stats
         # per window: init, server, finish + its rounds; per batched re-sample: the
         # sampling pipeline (~17 kernels incl. route anchors) + the respawn copies
-        launches = rs_["rounds"] + 3 * rs_["windows"] + 17 * rs_["sample_calls"]
+        launches = rs_["rounds"] + rs_["servers"] + 2 * rs_["windows"] + 17 * rs_["sample_calls"]
         rounds = rs_["rounds"]
     elif args.mode == "run":
         rounds = int(_lib.lib().cw_crowd_run_rounds())
-        launches = rounds + 3   # rounds + init + search server + finish
+        launches = rounds + int(_lib.lib().cw_crowd_run_servers()) + 2   # rounds + servers + init + finish
     else:
         rounds = 0
         launches = 4 * args.steps

@@ -220,6 +220,7 @@ int cw_crowd_step_phases(const cw_crowd_params* params, const cw_crowd_state* st
  * The final state is bit-identical to the synchronous ticks (last_gap included).
  * Blocks the calling host thread until the run is done (it polls the device to
  * stop launching rounds); device work is ordered after prior work on `stream`.
+ * Correct with or without concurrent kernel execution.
  * scratch: cw_crowd_run_scratch_bytes(E, A, ticks) bytes of device memory.
  * Returns 0, a CUDA error, 9001 (device queue error) or 9002 (no env-tick completed for
  * 120 s: the host watchdog ended the run). */
@@ -238,6 +239,10 @@ int cw_crowd_run_window(const cw_crowd_params* params, const cw_crowd_state* sta
 /* Round kernels the last cw_crowd_run launched (host-only query; the run also
  * launches one init, one search-server and one finish kernel). */
 long long cw_crowd_run_rounds(void);
+/* Search-server launches of the last cw_crowd_run (host-only query): the server exits
+ * when the run goes quiet and is relaunched when searches are queued, so it never
+ * waits on kernels that cannot run beside it (serialised launches, profilers). */
+long long cw_crowd_run_servers(void);
 int cw_crowd_run(const cw_crowd_params* params, const cw_crowd_state* state,
                  const double* robot_pos, const double* robot_vel, double robot_radius,
                  const uint8_t* env_mask, int threads, int ticks, void* scratch, void* stream);

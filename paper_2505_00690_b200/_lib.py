@@ -106,7 +106,7 @@ EXPORTS = ["cw_scene_seed_scratch_bytes", "cw_sample_scenes", "cw_spawn_agents",
            "cw_traversability_scratch_bytes", "cw_traversability", "cw_robot_step", "cw_robot_observe",
            "cw_route_scratch_bytes", "cw_route_anchors", "cw_seed_streams", "cw_child_seeds", "cw_abi_sizes",
            "cw_scene_rle", "cw_crowd_run_scratch_bytes", "cw_crowd_run",
-           "cw_crowd_run_rounds", "cw_crowd_run_window", "cw_sample_routes", "cw_connected_components",
+           "cw_crowd_run_rounds", "cw_crowd_run_servers", "cw_crowd_run_window", "cw_sample_routes", "cw_connected_components",
            "cw_rasterize", "cw_orca_lp", "cw_orca_halfplanes", "cw_crowd_constraints", "cw_trig_probe"]
 
 _lib = None
@@ -179,6 +179,8 @@ def lib():
                                       ctypes.c_double, P, ctypes.c_int, ctypes.c_int, P, P, ctypes.c_int, P, P]
     L.cw_crowd_run_rounds.restype = ctypes.c_longlong
     L.cw_crowd_run_rounds.argtypes = []
+    L.cw_crowd_run_servers.restype = ctypes.c_longlong
+    L.cw_crowd_run_servers.argtypes = []
     L.cw_crowd_run.restype = ctypes.c_int
     L.cw_crowd_run.argtypes = [ctypes.POINTER(CrowdParams), ctypes.POINTER(CrowdState), P, P,
                                ctypes.c_double, P, ctypes.c_int, ctypes.c_int, P, P]

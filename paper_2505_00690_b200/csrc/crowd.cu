@@ -1160,6 +1160,7 @@ __global__ void __launch_bounds__(NT) k_round(cw_crowd_params P, cw_crowd_state 
                                               RunArgs ra) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ int s_e, s_st, s_go;
+  if (threadIdx.x == 0) atomicAdd(&ra.q->active_rounds, 1);   // seen by the server's exit test
   while (true) {
     if (threadIdx.x == 0) {
       const int e = ready_pop(ra);
@@ -1177,7 +1178,10 @@ __global__ void __launch_bounds__(NT) k_round(cw_crowd_params P, cw_crowd_state 
     }
     __syncthreads();
     const int e = s_e;
-    if (e < 0) return;
+    if (e < 0) {
+      if (threadIdx.x == 0) atomicSub(&ra.q->active_rounds, 1);
+      return;
+    }
     int t = s_st >> 2;
     const int stop = ra.stop ? ra.stop[e] : ra.T;
     if (t >= stop) {   // nothing to run in this call (cw_crowd_run_window)
@@ -1257,7 +1261,7 @@ __global__ void k_run_init(RunArgs ra) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (ra.trace && i < (size_t)ra.E) ra.trace[i * 8 + kTrMark] = global_ns();
   // every env starts in the ready ring (positions 0..E-1)
-  if (i == 0) *ra.q = RunQueue{0ull, 0ull, 0, 0, 0, 0, 0ull, (unsigned long long)ra.E, 0ull, 0ull};
+  if (i == 0) *ra.q = RunQueue{0ull, 0ull, 0, 0, 0, 0, 0, 0, 0ull, (unsigned long long)ra.E, 0ull, 0ull};
   if (i < (size_t)ra.E) {
     ra.env_state[i] = (ra.start ? ra.start[i] : 0) << 2;   // kRunGuide at the env's first tick
     ra.pending[i] = 0;
@@ -1362,6 +1366,7 @@ static RunLayout run_layout(int E, int A, int T) {
 
 constexpr int kRoundStreams = 8;
 static long long g_last_rounds = 0;   // rounds launched by the last cw_crowd_run
+static long long g_last_servers = 0;  // search-server launches of the last cw_crowd_run
 
 template <int NT>
 static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const double* rp,
@@ -1496,13 +1501,20 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
   int srv_ctas = P.astar_ctas - std::max(4, margin > 0 ? margin : margin_def);
   if (const char* v = getenv("CW_RUN_SERVER_CTAS")) srv_ctas = std::min(srv_ctas, atoi(v));
   srv_ctas = std::max(srv_ctas, 1);
-  if (srv_w == 4)
-    k_astar<kAstarWarps, true><<<srv_ctas, 32 * kAstarWarps, shp.smem, TS.hi>>>(P, S, shp.NC, shp.NS, ra);
-  else if (srv_w == 2)
-    k_astar<2, true><<<srv_ctas, 64, shp.smem, TS.hi>>>(P, S, shp.NC, shp.NS, ra);
-  else
-    k_astar<1, true><<<srv_ctas, 32, shp.smem, TS.hi>>>(P, S, shp.NC, shp.NS, ra);
-  cudaEventRecord(H.srv_done, TS.hi);
+  // the search server exits when the run goes quiet (runq.cuh ring_pop) and is
+  // relaunched whenever requests are queued and no server launch is pending
+  long long n_servers = 0;
+  auto launch_server = [&]() {
+    if (srv_w == 4)
+      k_astar<kAstarWarps, true><<<srv_ctas, 32 * kAstarWarps, shp.smem, TS.hi>>>(P, S, shp.NC, shp.NS, ra);
+    else if (srv_w == 2)
+      k_astar<2, true><<<srv_ctas, 64, shp.smem, TS.hi>>>(P, S, shp.NC, shp.NS, ra);
+    else
+      k_astar<1, true><<<srv_ctas, 32, shp.smem, TS.hi>>>(P, S, shp.NC, shp.NS, ra);
+    cudaEventRecord(H.srv_done, TS.hi);
+    ++n_servers;
+  };
+  launch_server();
   int err = (int)cudaGetLastError();
   auto t_progress = std::chrono::steady_clock::now();
   int last_progress = -1;
@@ -1518,7 +1530,7 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
     cudaStream_t rs = H.rs[i % n_rs];
     if (lanes) k_round<NT, true><<<round_ctas, NT, sm, rs>>>(P, S, rp, rv, rr, em, bins, ra);
     else k_round<NT, false><<<round_ctas, NT, sm, rs>>>(P, S, rp, rv, rr, em, bins, ra);
-    cudaMemcpyAsync(H.poll + (i & 7) * 8, ra.q, 32, cudaMemcpyDeviceToHost, rs);
+    cudaMemcpyAsync(H.poll + (i & 7) * 8, ra.q, 32, cudaMemcpyDeviceToHost, rs);   // head..progress
     cudaEventRecord(H.ev[i & 7], rs);
     if (i >= kInFlight) {
       const long long j = i - kInFlight;
@@ -1533,6 +1545,9 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
       }
       if (pv[0] >= P.E) break;
       if (pv[2]) { status = 9001; break; }
+      // searches queued and the last server launch has finished: start another
+      const unsigned long long* hq = reinterpret_cast<const unsigned long long*>(pv - 4);
+      if (hq[1] > hq[0] && cudaEventQuery(H.srv_done) == cudaSuccess) launch_server();
       // watchdog: a run may take long, but it must keep completing env-ticks
       const auto now = std::chrono::steady_clock::now();
       if (pv[3] != last_progress) {
@@ -1544,6 +1559,7 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
     }
   }
   g_last_rounds = n_rounds;
+  g_last_servers = n_servers;
   if (ra.trace) {
     cudaDeviceSynchronize();
     std::vector<long long> tr((size_t)P.E * 8);
@@ -1811,6 +1827,8 @@ size_t cw_crowd_run_scratch_bytes(int E, int A, int ticks) {
 
 // Round kernels launched by the last cw_crowd_run (host-only query).
 long long cw_crowd_run_rounds(void) { return cw::g_last_rounds; }
+// Search-server launches by the last cw_crowd_run (host-only query).
+long long cw_crowd_run_servers(void) { return cw::g_last_servers; }
 
 // `ticks` synchronous cw_crowd_step calls with the same inputs, run without a
 // per-tick barrier (runq.cuh); same final state bit for bit.

@@ -115,7 +115,7 @@ CW_DEV void integrate_motion(const cw_robot_model& m, double x, double y, double
   if (m.holonomic) {
     const double ex = a0 * m.max_speed, ey = a1 * m.max_speed;
     double s, c;
-    sincos(yaw, &s, &c);
+    cr_sincos(yaw, &s, &c);
     vx = c * ex - s * ey;
     vy = s * ex + c * ey;
     nx = x + vx * dt;
@@ -123,7 +123,7 @@ CW_DEV void integrate_motion(const cw_robot_model& m, double x, double y, double
     const double speed = glibc_hypot(vx, vy);
     const double target = speed > 1e-9 ? atan2(vy, vx) : yaw;
     double ds, dc;
-    sincos(target - yaw, &ds, &dc);
+    cr_sincos(target - yaw, &ds, &dc);
     double dyaw = atan2(ds, dc);
     const double lim = kTwoPi * dt;
     dyaw = fmin(fmax(dyaw, -lim), lim);
@@ -135,7 +135,7 @@ CW_DEV void integrate_motion(const cw_robot_model& m, double x, double y, double
   const double yaw_rate = v * tan(steer) / m.wheelbase;
   nyaw = yaw + yaw_rate * dt;
   double s, c;
-  sincos(yaw, &s, &c);
+  cr_sincos(yaw, &s, &c);
   vx = v * c;
   vy = v * s;
   nx = x + vx * dt;
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kRays) k_observe(cw_robot_params P, cw_robot_s
   S.depth[(size_t)e * kRays + k] = depth;
   // ego-aligned height patch (observe.py:112-121), 160 samples over the CTA
   double s, c;
-  sincos(yaw, &s, &c);
+  cr_sincos(yaw, &s, &c);
   for (int q = k; q < kHX * kHY; q += kRays) {
     const int i = q / kHY, j = q - i * kHY;
     const double hx = ((double)i + 0.5) / kHX * kHL;

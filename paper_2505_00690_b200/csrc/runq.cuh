@@ -22,10 +22,15 @@ constexpr long long kSpinCycles = 8ll << 30;    // ~4.5 s: a full ring slot is a
 constexpr long long kIdleCycles = 64ll << 30;   // ~35 s backstop for a server warp that saw no
                                                 // env-tick complete anywhere for that long (the
                                                 // host normally ends the run via q->shutdown)
+constexpr long long kGraceCycles = 1ll << 19;   // ~0.27 ms: a server warp with an empty ring and
+                                                // no resident round CTA for this long exits (the
+                                                // host relaunches the server when searches queue)
 
 struct RunQueue {                 // device-resident control words
   unsigned long long head, tail;  // search ring positions claimed by consumers / producers
   int n_done, shutdown, error, progress;   // progress: env-ticks completed (wraps; host watchdog)
+  int active_rounds;              // round CTAs currently resident (the server's exit test)
+  int pad_;
   unsigned long long rhead, rtail;  // ready-env ring (start, yields)
   unsigned long long uhead, utail;  // urgent ring: envs the server released (their chain waits)
 };
@@ -133,24 +138,44 @@ CW_DEV int ready_pop(const RunArgs& ra) {
   return e >= 0 ? e : env_pop(ra, &ra.q->rhead, ra.rseq, ra.ritems);
 }
 
-// consumer (lane 0 of a server warp): false on shutdown / error
+// consumer (lane 0 of a server warp): false on shutdown / error, or when the run
+// has gone quiet -- the ring empty and no round CTA resident for kGraceCycles.
+// A position is claimed only once its item is there (Vyukov try-pop), so a warp
+// that leaves never strands a request.  The server therefore never waits on
+// kernels that cannot run beside it: when launches are serialised (e.g. under a
+// profiler) the server drains the queue and exits, the host launches the rounds
+// queued behind it and relaunches the server when searches are queued again.
 CW_DEV bool ring_pop(const RunArgs& ra, AstarReq& R) {
-  const unsigned long long pos = atomicAdd(&ra.q->head, 1ull);
-  unsigned long long* sq = ra.seq + (pos & ra.mask);
-  // the idle clock restarts whenever the run makes progress: an obstacle-free
-  // batch never queues a search, so a long run must not time its server out
-  long long t0 = clock64();
+  long long t0 = clock64(), tq = t0;
   int seen = *(volatile int*)&ra.q->progress;
-  while (ld_acquire_u64(sq) != pos + 1) {
+  unsigned long long pos = *(volatile unsigned long long*)&ra.q->head;
+  while (true) {
+    unsigned long long* sq = ra.seq + (pos & ra.mask);
+    const long long dif = (long long)(ld_acquire_u64(sq) - (pos + 1));
+    if (dif == 0) {
+      const unsigned long long old = atomicCAS(&ra.q->head, pos, pos + 1);
+      if (old == pos) {
+        R = ra.items[pos & ra.mask];
+        st_release_u64(sq, pos + ra.mask + 1);
+        return true;
+      }
+      pos = old;
+      continue;
+    }
+    if (dif > 0) {   // another consumer took it
+      pos = *(volatile unsigned long long*)&ra.q->head;
+      continue;
+    }
     if (*(volatile int*)&ra.q->shutdown) return false;
-    const int now = *(volatile int*)&ra.q->progress;
-    if (now != seen) { seen = now; t0 = clock64(); }
-    if (clock64() - t0 > kIdleCycles) { atomicCAS(&ra.q->error, 0, 2); return false; }
+    const long long now = clock64();
+    const int prog = *(volatile int*)&ra.q->progress;
+    if (prog != seen) { seen = prog; t0 = now; }
+    if (now - t0 > kIdleCycles) { atomicCAS(&ra.q->error, 0, 2); return false; }
+    if (*(volatile int*)&ra.q->active_rounds > 0) tq = now;
+    else if (now - tq > kGraceCycles) return false;
     __nanosleep(64);
+    pos = *(volatile unsigned long long*)&ra.q->head;
   }
-  R = ra.items[pos & ra.mask];
-  st_release_u64(sq, pos + ra.mask + 1);
-  return true;
 }
 
 }  // namespace cw

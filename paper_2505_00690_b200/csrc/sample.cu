@@ -1064,7 +1064,7 @@ __global__ void __launch_bounds__(128) k_place(cw_scene_params P, int E, const i
       yaw = __shfl_sync(0xffffffffu, yaw, 0);
       const double fw = P.cat_w[k], fl = P.cat_l[k];
       double cs, sn;
-      sincos(yaw, &sn, &cs);
+      cr_sincos(yaw, &sn, &cs);   // correctly rounded: matches glibc (np.cos / np.sin) but in its rare misroundings
       double cx[4], cy[4];
       footprint_corners(fw, fl, x, y, cs, sn, cx, cy);
       FootBox bb = footprint_box(P, cx, cy);
@@ -1227,7 +1227,7 @@ __global__ void __launch_bounds__(128) k_footprint(cw_scene_params P, int E, con
   const double x = pose[0], y = pose[1], yaw = pose[2];
   const double fw = P.cat_w[k], fl = P.cat_l[k];
   double cs, sn;
-  sincos(yaw, &sn, &cs);
+  cr_sincos(yaw, &sn, &cs);
   double cx[4], cy[4];
   footprint_corners(fw, fl, x, y, cs, sn, cx, cy);
   FootBox bb = footprint_box(P, cx, cy);

@@ -352,7 +352,7 @@ def run_with_resampling(sampler, field, env_seeds, counts, events, ticks, robot_
     cur = np.zeros(E, dtype=np.int64)            # each env's next tick
     env_t = env_seeds if isinstance(env_seeds, torch.Tensor) else seeds_to_tensor(env_seeds, dev)
     first, resampled = True, 0
-    windows = rounds = samples = 0
+    windows = rounds = samples = servers = 0
     w_end = 0
     saved = field.run_server_warps
     field.run_server_warps = saved or 4   # respawned envs plan every agent: search bursts
@@ -422,6 +422,7 @@ def run_with_resampling(sampler, field, env_seeds, counts, events, ticks, robot_
                          robot_radius, check=False)
         windows += 1
         rounds += int(_lib.lib().cw_crowd_run_rounds())
+        servers += int(_lib.lib().cw_crowd_run_servers())
         first = False
         cur = stop
         if last and pending is None:
@@ -429,5 +430,5 @@ def run_with_resampling(sampler, field, env_seeds, counts, events, ticks, robot_
     field.run_server_warps = saved
     field.prepare_step()
     field.check_flags()
-    field.last_run_stats = {"windows": windows, "rounds": rounds, "sample_calls": samples}
+    field.last_run_stats = {"windows": windows, "rounds": rounds, "servers": servers, "sample_calls": samples}
     return resampled
