@@ -424,16 +424,21 @@ def run_ours(args):
     avg_ms = run_ms / steps
     scenes = E * world / (sample_ms / 1e3)
     peak, peak_src = peaks()
-    # roofline, dominant kernel of the synchronous tick.  Algorithmic bytes per launch:
-    # k_guide = 40 B/agent (pos, goal, waypoint in; waypoint out) + 8 B per path point
-    # read + 1 B per line-of-sight label sample; k_astar = 80 B per expansion (popped g,
-    # 8 neighbour g + move byte); k_orca = 34 B/agent + 20 B/env (SURVEY 8d rest).
+    # roofline, dominant kernel of the synchronous tick.  Algorithmic bytes per launch, with
+    # the state in float64 (the dtype the path computes in; SURVEY 8d sized it for fp32):
+    #   k_guide = 57 B/agent (active 1, goal 16, pos 16, path head + count 8 in; waypoint
+    #             16 out) + 4 B per path point read (int32 cell) + 1 B per line-of-sight
+    #             label sample;
+    #   k_astar = 80 B per expansion (popped g, 8 neighbour g + move byte);
+    #   k_orca  = 126 B/agent (pos, vel, goal, waypoint 16 each, pref, radius, max_speed 8
+    #             each, active 1 in; pos, vel 16 each out; nearest 4 + label 1 at the agent's
+    #             cells) + 80 B/env (robot pos + vel 32, PCG64 stream 48).
     exp_step = ph_counters["astar_expansions"] / n_ph
     pts_step = ph_counters["path_points_read"] / n_ph
     los_step = ph_counters["los_samples_read"] / n_ph
-    kb = {"k_guide": 40.0 * active + 8.0 * pts_step + 1.0 * los_step,
+    kb = {"k_guide": 57.0 * active + 4.0 * pts_step + 1.0 * los_step,
           "k_astar": 80.0 * exp_step,
-          "k_orca": 34.0 * active + 20.0 * E}
+          "k_orca": 126.0 * active + 80.0 * E}
     names = ["k_guide", "k_astar", "k_orca"]
     dom = names[int(np.argmax(ph_avg))]
     dom_ms = float(ph_avg[names.index(dom)])
@@ -441,10 +446,13 @@ def run_ours(args):
     traffic, tsrc = traffic_of(args.config, dom)
     if args.traffic is not None:
         traffic, tsrc = args.traffic, "--traffic"
-    # whole step: 74 B per active agent-step + 20 B per env-step (robot) + the
-    # guidance reads the device actually makes (8 B per path point, 1 B per LOS sample)
+    # whole step (SURVEY 8d's fields at float64): per active agent-step read pos, vel, goal,
+    # waypoint 16 each, pref, radius, max_speed 8 each, active 1, path head + count 8 (97 B),
+    # write pos, vel, waypoint 16 each + path head + count 8 (56 B), grid lookups 5 B
+    # -> 158 B; per env-step 80 B (robot, PCG64 stream); plus the guidance reads the device
+    # makes (4 B per path point, 1 B per LOS sample; device counters)
     def step_bytes(c, n):
-        return 74.0 * active + 20.0 * E + (8.0 * c["path_points_read"] + 1.0 * c["los_samples_read"]) / n
+        return 158.0 * active + 80.0 * E + (4.0 * c["path_points_read"] + 1.0 * c["los_samples_read"]) / n
     bytes_run = step_bytes(c_run, steps)
     ach_run = bytes_run / (avg_ms / 1e3) / 1e9
     bytes_sync = step_bytes(c_sync, n_sync)
@@ -487,15 +495,16 @@ def run_ours(args):
                      "frac": round(dom_ach / peak, 7), "traffic": traffic, "traffic_source": tsrc,
                      "kernel": dom, "peak_source": peak_src, "bytes_per_launch": round(kb[dom], 1),
                      "avg_launch_ms": round(dom_ms, 4),
-                     "bytes_model": {"k_guide": "40 B/agent + 8 B/path point read + 1 B/LOS sample",
-                                     "k_astar": "80 B/expansion", "k_orca": "34 B/agent + 20 B/env"},
+                     "bytes_model": {"k_guide": "57 B/agent + 4 B/path point read + 1 B/LOS sample",
+                                     "k_astar": "80 B/expansion", "k_orca": "126 B/agent + 80 B/env",
+                                     "state": "float64"},
                      "note": "dominant kernel of the synchronous tick (events around each launch on the "
                              "launching stream); a latency-bound serial search"},
         "roofline_step": {"bound": "hbm", "achieved": round(ach_run, 3), "peak": peak, "unit": "GB/s",
                           "frac": round(ach_run / peak, 7), "bytes_per_step": round(bytes_run, 1),
                           "bytes_per_step_sync": round(bytes_sync, 1),
-                          "model": "SURVEY 8d: 74 B/agent-step + 20 B/env-step + the guidance reads made "
-                                   "(8 B/path point, 1 B/LOS sample; device counters)"},
+                          "model": "SURVEY 8d fields at float64: 158 B/agent-step + 80 B/env-step + the "
+                                   "guidance reads made (4 B/path point, 1 B/LOS sample; device counters)"},
         "roofline_sampling": {"bound": "hbm", "achieved": round(ach_sample, 3), "peak": peak, "unit": "GB/s",
                               "frac": round(ach_sample / peak, 7), "bytes_per_batch": round(bytes_sample, 1),
                               "model": "SURVEY 8d: 9N + 4W + 40A bytes per env-sample (elev, labels, "

@@ -108,6 +108,14 @@ int cw_sample_scenes(const cw_scene_params* params, int E, const uint64_t* scene
                      const uint64_t* crowd_seeds, const int32_t* slots, void* seed_scratch,
                      const cw_scene_buffers* buffers, void* stream);
 
+/* cw_sample_scenes + cw_route_anchors (below) as one pipeline: the route anchors read
+ * only the labels, so they run on a side stream beside the nearest-obstacle BFS, walk
+ * list and spawn.  Same outputs as the two calls in sequence. */
+int cw_sample_scenes_routes(const cw_scene_params* params, int E, const uint64_t* scene_seeds,
+                            const uint64_t* crowd_seeds, const int32_t* slots, void* seed_scratch,
+                            const cw_scene_buffers* buffers, double* routes, int32_t* n_routes,
+                            void* route_scratch, int chunk, void* stream);
+
 /* Run-length coding of the sampled grids for scene_to_dict (urbangen/scene.py:163-178,
  * jsonio.rle_encode jsonio.py:42-54): rows rows[e] (NULL = e) of buffers->zones (ny*nx u8)
  * and buffers->assign (trows*tcols int32).  Count pass (offsets = pairs = NULL):

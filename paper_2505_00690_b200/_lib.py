@@ -100,7 +100,7 @@ class RobotState(ctypes.Structure):
     _fields_ = [(n, P) for n in ROBOT_STATE_FIELDS]
 
 
-EXPORTS = ["cw_scene_seed_scratch_bytes", "cw_sample_scenes", "cw_spawn_agents", "cw_prepare_envs",
+EXPORTS = ["cw_scene_seed_scratch_bytes", "cw_sample_scenes", "cw_sample_scenes_routes", "cw_spawn_agents", "cw_prepare_envs",
            "cw_crowd_step_smem_bytes",
            "cw_crowd_step", "cw_crowd_step_phases", "cw_astar_slot_bytes", "cw_astar_warps",
            "cw_traversability_scratch_bytes", "cw_traversability", "cw_robot_step", "cw_robot_observe",
@@ -158,6 +158,9 @@ def lib():
     L.cw_sample_scenes.restype = ctypes.c_int
     L.cw_sample_scenes.argtypes = [ctypes.POINTER(SceneParams), ctypes.c_int, P, P, P, P,
                                    ctypes.POINTER(SceneBuffers), P]
+    L.cw_sample_scenes_routes.restype = ctypes.c_int
+    L.cw_sample_scenes_routes.argtypes = [ctypes.POINTER(SceneParams), ctypes.c_int, P, P, P, P,
+                                          ctypes.POINTER(SceneBuffers), P, P, P, ctypes.c_int, P]
     L.cw_spawn_agents.restype = ctypes.c_int
     L.cw_spawn_agents.argtypes = [ctypes.POINTER(SceneParams), ctypes.c_int, P, P, P,
                                   ctypes.POINTER(SceneBuffers), P]

@@ -1025,10 +1025,15 @@ CW_DEV bool region_ok(const cw_scene_params& P, uint8_t zone, int c) {
   return true;
 }
 
-// warp per env
-__global__ void __launch_bounds__(128) k_place(cw_scene_params P, int E, const int32_t* slots,
-                                               const EnvSeeds* __restrict__ seeds,
-                                               cw_scene_buffers B) {
+// Warp per env.  kStage: the env's zone grid (4 bits per cell) and the placed
+// objects' SAT data live in shared memory for the whole rejection loop (one env per
+// CTA), so every footprint / overlap test reads shared memory; else global (grids
+// whose packed zone tile does not fit).
+template <bool kStage>
+__global__ void __launch_bounds__(kStage ? 32 : 128) k_place(cw_scene_params P, int E, const int32_t* slots,
+                                                           const EnvSeeds* __restrict__ seeds,
+                                                           cw_scene_buffers B) {
+  extern __shared__ __align__(16) unsigned char place_sm[];
   const int lane = threadIdx.x & 31;
   const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (e >= E) return;
@@ -1041,6 +1046,31 @@ __global__ void __launch_bounds__(128) k_place(cw_scene_params P, int E, const i
   double* cache = B.scratch_f64 + (size_t)e * (size_t)max(P.obj_max * 8, (int)N);  // corners
   int32_t* ocat = B.obj_cat + (size_t)slot * P.obj_max;
   double* opose = B.obj_pose + (size_t)slot * P.obj_max * 3;
+  // staged layout: zones (2 cells per byte), then per placed object 8 corner doubles,
+  // x, y, reach
+  uint8_t* zs = place_sm;
+  double* os = reinterpret_cast<double*>(place_sm + ((N / 2 + 1 + 15) & ~(size_t)15));
+  if (kStage) {
+    const uint4* Z16 = reinterpret_cast<const uint4*>(Z);   // N % 32 == 0 (checked by the launch)
+    for (size_t q = lane; q < N / 16; q += 32) {
+      const uint4 v = Z16[q];
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+      uint32_t out[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t o = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) o |= ((w[2 * h + b / 4] >> (8 * (b % 4))) & 15u) << (4 * b);
+        out[h] = o;
+      }
+      reinterpret_cast<uint2*>(zs)[q] = make_uint2(out[0], out[1]);
+    }
+    __syncwarp();
+  }
+  auto zone_at = [&](size_t f) -> uint8_t {
+    if (kStage) return (uint8_t)((zs[f >> 1] >> ((f & 1) * 4)) & 15u);
+    return Z[f];
+  };
   Pcg64 rng;
   if (lane == 0) rng = pcg_load(seeds[e].objects);
   int placed = 0;
@@ -1075,7 +1105,7 @@ __global__ void __launch_bounds__(128) k_place(cw_scene_params P, int E, const i
         int r = bb.r0 + q / bw, c = bb.c0 + q % bw;
         if (!cell_inside(P, r, c, x, y, cs, sn, fw, fl)) continue;
         any = true;
-        uint8_t z = Z[(size_t)r * P.nx + c];
+        uint8_t z = zone_at((size_t)r * P.nx + c);
         if (!((P.cat_zones[k] >> z) & 1u) || !region_ok(P, z, c)) bad = true;
       }
       any = __any_sync(0xffffffffu, any);
@@ -1084,7 +1114,7 @@ __global__ void __launch_bounds__(128) k_place(cw_scene_params P, int E, const i
         // degenerate small footprint: the centre cell (placement.py:54-58)
         long long rc = trunc_ll(y / P.res), cc = trunc_ll(x / P.res);
         if (!(rc >= 0 && rc < P.ny && cc >= 0 && cc < P.nx)) continue;
-        uint8_t z = Z[(size_t)rc * P.nx + cc];
+        uint8_t z = zone_at((size_t)rc * P.nx + cc);
         if (!((P.cat_zones[k] >> z) & 1u) || !region_ok(P, z, (int)cc)) continue;
       } else if (bad) {
         continue;
@@ -1098,9 +1128,9 @@ __global__ void __launch_bounds__(128) k_place(cw_scene_params P, int E, const i
       bool hit = false;
       const double reach = P.cat_reach[k];
       for (int j = lane; j < placed; j += 32) {
-        const double* o = cache + (size_t)j * 8;
-        double ox = opose[j * 3 + 0], oy = opose[j * 3 + 1];
-        double rr = reach + P.cat_reach[ocat[j]];
+        const double* o = kStage ? os + (size_t)j * 11 : cache + (size_t)j * 8;
+        const double ox = kStage ? o[8] : opose[j * 3 + 0], oy = kStage ? o[9] : opose[j * 3 + 1];
+        double rr = reach + (kStage ? o[10] : P.cat_reach[ocat[j]]);
         double dx = x - ox, dy = y - oy;
         if (dx * dx + dy * dy > rr * rr) continue;
         if (sat_overlap(cx, cy, o, o + 4)) hit = true;
@@ -1111,8 +1141,9 @@ __global__ void __launch_bounds__(128) k_place(cw_scene_params P, int E, const i
         opose[placed * 3 + 0] = x;
         opose[placed * 3 + 1] = y;
         opose[placed * 3 + 2] = yaw;
-        double* o = cache + (size_t)placed * 8;
+        double* o = kStage ? os + (size_t)placed * 11 : cache + (size_t)placed * 8;
         for (int i = 0; i < 4; ++i) { o[i] = cx[i]; o[4 + i] = cy[i]; }
+        if (kStage) { o[8] = x; o[9] = y; o[10] = reach; }
       }
       __syncwarp();
       ++placed;
@@ -1124,6 +1155,12 @@ __global__ void __launch_bounds__(128) k_place(cw_scene_params P, int E, const i
     B.obj_n[slot] = placed;
     B.overflow[slot] = overflow;
   }
+}
+
+// shared memory of the staged k_place: packed zones + 11 doubles per object
+CW_HD size_t place_stage_bytes(const cw_scene_params& p) {
+  const size_t N = (size_t)p.nx * p.ny;
+  return ((N / 2 + 1 + 15) & ~(size_t)15) + (size_t)p.obj_max * 11 * sizeof(double);
 }
 
 // ================================================================= raster
@@ -1802,8 +1839,8 @@ __global__ void k_trig_probe(int n, const double* __restrict__ x, double* __rest
 
 struct SideStreams {
   int dev = -1;
-  cudaStream_t s[2];
-  cudaEvent_t fork, join[2];
+  cudaStream_t s[3];
+  cudaEvent_t fork, join[3];
 };
 
 static SideStreams& side_streams() {
@@ -1812,7 +1849,7 @@ static SideStreams& side_streams() {
   cudaGetDevice(&d);
   SideStreams& S = g[d & 15];
   if (S.dev != d) {
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < 3; ++k) {
       cudaStreamCreateWithFlags(&S.s[k], cudaStreamNonBlocking);
       cudaEventCreateWithFlags(&S.join[k], cudaEventDisableTiming);
     }
@@ -1821,6 +1858,13 @@ static SideStreams& side_streams() {
   }
   return S;
 }
+
+struct RouteJob {   // cw_sample_scenes_routes: the route anchors, forked off the labels
+  double* routes;
+  int32_t* n_routes;
+  void* scratch;
+  int chunk;
+};
 
 }  // namespace cw
 
@@ -1833,9 +1877,9 @@ size_t cw_scene_seed_scratch_bytes(int E) { return (size_t)E * sizeof(cw::EnvSee
 // zones -> terrain -> placement -> raster -> nearest-obstacle BFS -> walk list -> spawn.
 // Rows are written at slots[e] (slots may be NULL = identity).  Returns 0 or a
 // cudaError_t; per-env failures are reported in B->status.
-int cw_sample_scenes(const cw_scene_params* P, int E, const uint64_t* scene_seeds,
-                     const uint64_t* crowd_seeds, const int32_t* slots, void* seed_scratch,
-                     const cw_scene_buffers* B, void* stream) {
+static int sample_impl(const cw_scene_params* P, int E, const uint64_t* scene_seeds, const uint64_t* crowd_seeds,
+                       const int32_t* slots, void* seed_scratch, const cw_scene_buffers* B, const cw::RouteJob* rj,
+                       void* stream) {
   using namespace cw;
   if (E <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
@@ -1852,16 +1896,27 @@ int cw_sample_scenes(const cw_scene_params* P, int E, const uint64_t* scene_seed
   const size_t tsm = per * wpc;
   cudaFuncSetAttribute(k_terrain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
   k_terrain<<<(E + wpc - 1) / wpc, wpc * 32, tsm, st>>>(p, E, slots, S, b);
-  k_place<<<(E + 3) / 4, 128, 0, st>>>(p, E, slots, S, b);
+  {
+    const size_t psm = place_stage_bytes(p);
+    const size_t N = (size_t)p.nx * p.ny;
+    if (psm <= 200u * 1024u && N % 32 == 0) {
+      cudaFuncSetAttribute(k_place<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
+      k_place<true><<<E, 32, psm, st>>>(p, E, slots, S, b);
+    } else {
+      k_place<false><<<(E + 3) / 4, 128, 0, st>>>(p, E, slots, S, b);
+    }
+  }
   const int quads = (p.nx * p.ny + 3) / 4;
   k_raster<<<dim3((quads + 255) / 256, E), 256, 0, st>>>(p, E, slots, b);
   if (p.obj_max > 0) k_footprint<<<dim3((p.obj_max + 3) / 4, E), 128, 0, st>>>(p, E, slots, b);
-  // the label consumers are independent: BFS and components/walk list run on
-  // side streams joined back before returning (fork/join keeps stream order)
+  // the label consumers are independent: BFS, components / walk list and the route
+  // anchors run on side streams joined back before returning (fork/join keeps
+  // stream order)
   SideStreams& ss = side_streams();
+  const int nside = rj ? 3 : 2;
   cudaEventRecord(ss.fork, st);
-  cudaStreamWaitEvent(ss.s[0], ss.fork, 0);
-  cudaStreamWaitEvent(ss.s[1], ss.fork, 0);
+  for (int k = 0; k < nside; ++k) cudaStreamWaitEvent(ss.s[k], ss.fork, 0);
+  if (rj) cw_route_anchors(P, E, scene_seeds, slots, B, rj->routes, rj->n_routes, rj->scratch, rj->chunk, ss.s[2]);
   k_nearest<<<E, BFS_NT, 0, ss.s[0]>>>(p, E, slots, b);
   k_walk<<<E, 1024, 0, ss.s[1]>>>(p, E, slots, b);
   k_reach<<<E, 1024, 0, ss.s[1]>>>(p, E, slots, b);
@@ -1870,11 +1925,31 @@ int cw_sample_scenes(const cw_scene_params* P, int E, const uint64_t* scene_seed
     if (sm > 48 * 1024) cudaFuncSetAttribute(k_spawn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k_spawn<<<E, SP_NT, sm, st>>>(p, E, slots, S, b, nullptr);
   }
-  cudaEventRecord(ss.join[0], ss.s[0]);
-  cudaEventRecord(ss.join[1], ss.s[1]);
-  cudaStreamWaitEvent(st, ss.join[0], 0);
-  cudaStreamWaitEvent(st, ss.join[1], 0);
+  for (int k = 0; k < nside; ++k) {
+    cudaEventRecord(ss.join[k], ss.s[k]);
+    cudaStreamWaitEvent(st, ss.join[k], 0);
+  }
   return (int)cudaGetLastError();
+}
+
+// Sample E scenes (one per scene_seed) end to end on `stream`:
+// zones -> terrain -> placement -> raster -> nearest-obstacle BFS -> walk list -> spawn.
+// Rows are written at slots[e] (slots may be NULL = identity).  Returns 0 or a
+// cudaError_t; per-env failures are reported in B->status.
+int cw_sample_scenes(const cw_scene_params* P, int E, const uint64_t* scene_seeds,
+                     const uint64_t* crowd_seeds, const int32_t* slots, void* seed_scratch,
+                     const cw_scene_buffers* B, void* stream) {
+  return sample_impl(P, E, scene_seeds, crowd_seeds, slots, seed_scratch, B, nullptr, stream);
+}
+
+// cw_sample_scenes + cw_route_anchors in one pipeline: the route anchors only read the
+// labels, so they run on a side stream beside the BFS, walk list and spawn.
+int cw_sample_scenes_routes(const cw_scene_params* P, int E, const uint64_t* scene_seeds,
+                            const uint64_t* crowd_seeds, const int32_t* slots, void* seed_scratch,
+                            const cw_scene_buffers* B, double* routes, int32_t* n_routes, void* route_scratch,
+                            int chunk, void* stream) {
+  const cw::RouteJob rj{routes, n_routes, route_scratch, chunk};
+  return sample_impl(P, E, scene_seeds, crowd_seeds, slots, seed_scratch, B, &rj, stream);
 }
 
 // spawn_agents(occupancy, count, seed) for caller-supplied labels (step.py:37-63).

@@ -547,22 +547,24 @@ class SceneSampler:
             self.batch.scene_seed[:E] = seeds
         self.batch._ensure_scratch(E)
         b = self.batch.buffers()
-        err = _lib.lib().cw_sample_scenes(
-            self.params, E, _lib.ptr(seeds), _lib.ptr(cseeds), _lib.ptr(sl),
-            _lib.ptr(self.batch.seed_scratch), b, _lib.stream_ptr(stream))
-        _lib.check(err, "cw_sample_scenes")
         if self.routes:
-            # route anchors (scene.py:87, 102-178), chunked through their own scratch
+            # route anchors (scene.py:87, 102-178) forked off the labels inside the
+            # pipeline (cw_sample_scenes_routes), chunked through their own scratch
             p = self.params
             chunk = min(E, self.route_chunk)
             nbytes = int(_lib.lib().cw_route_scratch_bytes(p.nx, p.ny, chunk))
             if getattr(self.batch, "route_scratch", None) is None or self.batch.route_scratch.numel() * 8 < nbytes:
                 self.batch.route_scratch = torch.empty(nbytes // 8 + 1, dtype=torch.int64, device=dev)
-            err = _lib.lib().cw_route_anchors(
-                p, E, _lib.ptr(seeds), _lib.ptr(sl), b, _lib.ptr(self.batch.routes),
-                _lib.ptr(self.batch.n_routes), _lib.ptr(self.batch.route_scratch), chunk,
-                _lib.stream_ptr(stream))
-            _lib.check(err, "cw_route_anchors")
+            err = _lib.lib().cw_sample_scenes_routes(
+                self.params, E, _lib.ptr(seeds), _lib.ptr(cseeds), _lib.ptr(sl),
+                _lib.ptr(self.batch.seed_scratch), b, _lib.ptr(self.batch.routes), _lib.ptr(self.batch.n_routes),
+                _lib.ptr(self.batch.route_scratch), chunk, _lib.stream_ptr(stream))
+            _lib.check(err, "cw_sample_scenes_routes")
+        else:
+            err = _lib.lib().cw_sample_scenes(
+                self.params, E, _lib.ptr(seeds), _lib.ptr(cseeds), _lib.ptr(sl),
+                _lib.ptr(self.batch.seed_scratch), b, _lib.stream_ptr(stream))
+            _lib.check(err, "cw_sample_scenes")
         if check:
             self.batch.check_status(None if sl is None else sl.long())
         return self.batch

@@ -26,9 +26,8 @@ if [ "$LAUNCH" = 1 ]; then
 fi
 if [ "$STEPS" = 1 ]; then
   for C in $CFGS; do
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_astar|k_orca|k_guide' \
-      -s 30 -c 3 -o $NCU_DIR/step_${C} -f python bench.py --config $C --mode step --steps 12 --warmup 10 \
-      --no-cpu-baseline --no-step-batch --sample-reps 1 --sync-steps 1 --e2e-steps 1 --phase-steps 1 \
+    timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
+      -k regex:'k_astar|k_orca|k_guide' -o $NCU_DIR/step_${C} -f python tools/tick_once.py $C 20 \
       > gpurun_out/${TAG}_ncu_step_${C}.log 2>&1
     echo "step $C rc=$?"
     ncu -i $NCU_DIR/step_${C}.ncu-rep --page raw --csv > gpurun_out/${TAG}_step_${C}_raw.csv 2>/dev/null
@@ -42,7 +41,7 @@ if [ "$SAMPLE" = 1 ]; then
   ncu -i $NCU_DIR/sample_cfg2.ncu-rep --page raw --csv > gpurun_out/${TAG}_sample_cfg2_raw.csv 2>/dev/null
 fi
 if [ "$RANGE" = 1 ]; then
-  CW_PROFILE_RANGE=1 timeout 1200 ncu --replay-mode app-range --profile-from-start off --clock-control none \
+  CW_PROFILE_RANGE=1 timeout 1200 ncu --replay-mode app-range --clock-control none \
     --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__inst_executed.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__warps_active.avg.pct_of_peak_sustained_active,sm__throughput.avg.pct_of_peak_sustained_elapsed \
     -o $NCU_DIR/run_range_cfg2 -f python bench.py --steps 100 --warmup 20 --no-cpu-baseline --no-step-batch \
     --sample-reps 1 --sync-steps 2 --e2e-steps 2 --phase-steps 2 > gpurun_out/${TAG}_ncu_range.log 2>&1
