@@ -372,6 +372,8 @@ def run_ours(args):
     for k in range(e2e_steps):
         rp = rpos_h.to(dev, non_blocking=True)
         rv = rvel_h.to(dev, non_blocking=True)
+        if masks:
+            resample_mix((args.warmup + k) % len(masks))   # cfg5: the re-sampling is part of the step
         f.step(rp, rv, 0.35, check=False)
         out_pos.copy_(f.pos_t, non_blocking=True)
         out_vel.copy_(f.vel_t, non_blocking=True)
@@ -480,9 +482,9 @@ def run_ours(args):
                  "CrowdField.step calls" if args.mode == "run" else "K CrowdField.step calls"),
         "e2e": {"value": round(E * world * e2e_steps / e2e_s, 1), "unit": "env-steps/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
-                "what": "the reference's per-tick API: CrowdField.step once per tick; robot pos/vel "
-                        "copied in from pinned host memory and crowd pos/vel read back to the host "
-                        "every tick (stream synchronised per tick)"},
+                "what": "the reference's per-tick API: CrowdField.step once per tick (cfg5: after the "
+                        "tick's Bernoulli re-sampling); robot pos/vel copied in from pinned host memory "
+                        "and crowd pos/vel read back to the host every tick (stream synchronised per tick)"},
         "tick_sync": {"value": round(E * world / (sync_ms / 1e3), 1), "ms_per_step": round(sync_ms, 4),
                       "steps": n_sync, "l2": "flushed (256 MB write) between timed ticks",
                       "clocks": clk.summary(t_sync0, t_sync1),
