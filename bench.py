@@ -329,6 +329,8 @@ def run_ours(args):
     for k in range(n_sync):
         flush.fill_(float(k))          # untimed
         starts[k].record(st)
+        if masks:
+            resample_mix((args.warmup + k) % len(masks))   # cfg5: the re-sampling is part of the step
         f.step(rpos, rvel, 0.35, check=False)
         ends[k].record(st)
     torch.cuda.synchronize()
@@ -488,7 +490,8 @@ def run_ours(args):
         "tick_sync": {"value": round(E * world / (sync_ms / 1e3), 1), "ms_per_step": round(sync_ms, 4),
                       "steps": n_sync, "l2": "flushed (256 MB write) between timed ticks",
                       "clocks": clk.summary(t_sync0, t_sync1),
-                      "what": "one CrowdField.step per tick, device-resident inputs (events per tick)"},
+                      "what": "one CrowdField.step per tick (cfg5: after the tick's re-sampling), "
+                              "device-resident inputs (events per tick)"},
         "scenes_per_sec": round(scenes, 1), "sample_ms_per_batch": round(sample_ms, 3),
         "sample_includes": "zones, WFC terrain, placement, raster + heightfield, nearest-obstacle map, "
                            "walk list, reach labels, A* move table, pedestrian spawn, route anchors",

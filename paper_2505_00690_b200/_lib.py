@@ -147,9 +147,10 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        raise RuntimeError(f"libcitywalk_b200.so not built ({LIB_PATH}); run __graft_entry__.build()")
-    L = ctypes.CDLL(LIB_PATH)
+    path = os.environ.get("CW_LIB_PATH", LIB_PATH)   # A/B builds of the same ABI (tools/)
+    if not os.path.exists(path):
+        raise RuntimeError(f"libcitywalk_b200.so not built ({path}); run __graft_entry__.build()")
+    L = ctypes.CDLL(path)
     L.cw_scene_seed_scratch_bytes.restype = ctypes.c_size_t
     L.cw_scene_seed_scratch_bytes.argtypes = [ctypes.c_int]
     L.cw_scene_rle.restype = ctypes.c_int

@@ -26,10 +26,14 @@
 //      3.5e-4 * 2^24 gap), so relaxations are atomicMin's.  Four 256-thread
 //      groups run the four source fields at once as Dial's algorithm with unit
 //      buckets on the exact length: bucket = floor(a + b sqrt2) = key >> 52
-//      (exact for b < 3400).  Every move costs >= 1, so a bucket's cells are final when
-//      it is expanded and pushes land in the next two buckets (three rotating
-//      lists, pushes deduplicated by per-cell bucket stamps, stale entries
-//      skipped) -- every cell is expanded once and the fields are exact.  geo = (a + b*sqrt(2)) * res then decides
+//      (exact for b < 3400).  Every move costs >= 1, so a bucket's keys are final
+//      when it is expanded and pushes land in the next two buckets (three rotating
+//      lists).  A list entry carries the key it was pushed with, and an entry whose
+//      cell has since improved is expanded anyway with its old key -- its moves
+//      then improve nothing -- so a level costs two dependent memory round trips
+//      (list entry, atomicMin) instead of five (no key reload, no pre-filter read,
+//      no de-duplication stamp); every cell is still expanded with its final key
+//      in its final bucket, so the fields are exact.  geo = (a + b*sqrt(2)) * res then decides
 //      the window tests as the reference except on exact-equality coincidences
 //      (none in the golden set, tests/test_gpu_routes.py).
 //   4. the windowed pair draws of scene.py:121-144 with the scene's
@@ -158,33 +162,28 @@ CW_DEV void chamfer_row(double* row, const double* prev, int nx, int lane) {
   __syncwarp();
 }
 
-// scratch per env: 4 fields x (key u64 + two bucket-list halves i32 + stamp i32),
-// cand N i32, ok N i32 (the chamfer's D aliases field 0's keys)
-CW_HD size_t route_scratch_per_env(int nx, int ny) { return (size_t)nx * ny * (4 * 20 + 4 + 4); }
+// scratch per env: 4 fields x (key u64 + three bucket lists of N entries {key u64,
+// cell i32}), cand N i32, ok N i32 (the chamfer's D aliases field 0's keys)
+CW_HD size_t route_scratch_per_env(int nx, int ny) { return (size_t)nx * ny * (4 * (8 + 3 * 12) + 4 + 4); }
 
-__global__ void __launch_bounds__(RT_NT, 1) k_routes(cw_scene_params P, int e0, int n,
-                                                     const uint64_t* __restrict__ scene_seeds,
-                                                     const int32_t* slots, cw_scene_buffers B,
-                                                     double* routes, int32_t* n_routes,
-                                                     unsigned char* scratch) {
+// One env on the whole CTA (scratch `base` is the CTA's slot).
+__device__ void route_env(const cw_scene_params& P, int e, const uint64_t* __restrict__ scene_seeds,
+                          const int32_t* slots, const cw_scene_buffers& B, double* routes, int32_t* n_routes,
+                          unsigned char* base) {
   extern __shared__ uint32_t s_walk[];   // walkable bits
   __shared__ int sh[RT_NT / 32 + 1];
   __shared__ int s_src[4], s_np, s_changed[4];
   __shared__ double s_pairs[RT_MAX * 4];
-  const int k = blockIdx.x;
-  if (k >= n) return;
-  const int e = e0 + k;
   const int row_e = route_row(slots, e);
   if (B.status[row_e] != CW_OK) return;
   const int nx = P.nx, ny = P.ny, N = nx * ny;
   const double res = P.res;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint8_t* lab = B.labels + (size_t)row_e * N;
-  unsigned char* base = scratch + (size_t)k * route_scratch_per_env(nx, ny);
   unsigned long long* F = reinterpret_cast<unsigned long long*>(base);           // 4 x N
-  int32_t* FL = reinterpret_cast<int32_t*>(base + (size_t)N * 32);               // 4 x 2 x N lists
-  int32_t* ST = FL + (size_t)N * 8;                                              // 4 x N stamps
-  int32_t* cand = ST + (size_t)N * 4;
+  unsigned long long* LKs = F + (size_t)N * 4;                                   // 4 x 3 x N list keys
+  int32_t* LCs = reinterpret_cast<int32_t*>(LKs + (size_t)N * 12);               // 4 x 3 x N list cells
+  int32_t* cand = LCs + (size_t)N * 12;
   int32_t* okl = cand + N;
   double* D = reinterpret_cast<double*>(F);                                      // chamfer (field 0)
   const int NW = (N + 31) / 32;
@@ -282,22 +281,26 @@ __global__ void __launch_bounds__(RT_NT, 1) k_routes(cw_scene_params P, int e0, 
   __syncthreads();
   const int nf = traverse ? 1 : 4;
   // fields: group g (256 threads) owns source g; Dial's buckets with atomicMin
-  // keys, one named barrier (id 1 + g) per group.  Lists: 3 rotating buckets of
-  // capacity 2N/3 each carved from the group's 2N list space.
+  // keys, one named barrier (id 1 + g) per group; three rotating bucket lists of
+  // N entries each (an entry per improving relaxation; overflow is reported)
   const int g = tid >> 8, gt = tid & 255;
   __shared__ int s_fn[4][3];   // bucket list sizes
+  __shared__ int s_ovf;
+  if (tid == 0) s_ovf = 0;
+  __syncthreads();
   if (g < nf) {
     unsigned long long* Fg = F + (size_t)g * N;
-    const int cap = (2 * N) / 3;
-    int32_t* Lb = FL + (size_t)g * 2 * N;
-    int32_t* St = ST + (size_t)g * N;
-    for (int f = gt; f < N; f += 256) { Fg[f] = kNoDist; St[f] = -1; }
+    const int cap = N;
+    unsigned long long* LK = LKs + (size_t)g * 3 * N;
+    int32_t* LC = LCs + (size_t)g * 3 * N;
+    for (int f = gt; f < N; f += 256) Fg[f] = kNoDist;
     auto gsync = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory"); };
     gsync();
     if (gt == 0) {
       const int f0 = cand[s_src[g]];
       Fg[f0] = ab_key(0, 0);
-      Lb[0] = ((f0 / nx) << 16) | (f0 % nx);
+      LK[0] = ab_key(0, 0);
+      LC[0] = ((f0 / nx) << 16) | (f0 % nx);
       s_fn[g][0] = 1;
       s_fn[g][1] = 0;
       s_fn[g][2] = 0;
@@ -307,29 +310,28 @@ __global__ void __launch_bounds__(RT_NT, 1) k_routes(cw_scene_params P, int e0, 
       const int cur = (int)(k % 3);
       const int n_cur = s_fn[g][cur];
       if (n_cur == 0 && s_fn[g][(cur + 1) % 3] == 0 && s_fn[g][(cur + 2) % 3] == 0) break;
-      const int32_t* Lc = Lb + (size_t)cur * cap;
-      // items (cell, move) in batches of 4 per thread: loads and atomics of a
-      // batch are issued back to back; list entries are packed (row << 16 | col)
+      const unsigned long long* Kc = LK + (size_t)cur * cap;
+      const int32_t* Cc = LC + (size_t)cur * cap;
+      // items (entry, move) in batches of 4 per thread: the loads and atomics of a
+      // batch are issued back to back; cells are packed (row << 16 | col)
       constexpr int BT = 4;
       for (int q0 = gt; q0 < n_cur * 8; q0 += 256 * BT) {
-        int pu[BT], v[BT], rv[BT], cv[BT];
+        int pu[BT], rv[BT], cv[BT], v[BT];
         unsigned long long kk[BT];
         bool ok[BT];
 #pragma unroll
         for (int i = 0; i < BT; ++i) {
           const int q = q0 + i * 256;
-          pu[i] = q < n_cur * 8 ? Lc[q >> 3] : -1;
+          pu[i] = q < n_cur * 8 ? Cc[q >> 3] : -1;
+          kk[i] = q < n_cur * 8 ? Kc[q >> 3] : ~0ull;
         }
-#pragma unroll
-        for (int i = 0; i < BT; ++i)
-          kk[i] = pu[i] >= 0 ? (unsigned long long)((volatile unsigned long long*)Fg)[(pu[i] >> 16) * nx + (pu[i] & 0xFFFF)] : ~0ull;
 #pragma unroll
         for (int i = 0; i < BT; ++i) {
           const int d = (q0 + i * 256) & 7;
           ok[i] = false;
           v[i] = 0;
           rv[i] = cv[i] = 0;
-          if (pu[i] < 0 || ab_bucket(kk[i]) != k) continue;   // stale: improved into an earlier bucket
+          if (pu[i] < 0) continue;
           const int ru = pu[i] >> 16, cu = pu[i] & 0xFFFF;
           const int dr = (int)((0x22001120u >> (4 * d)) & 0xF) - 1;
           const int dc = (int)((0x20202011u >> (4 * d)) & 0xF) - 1;
@@ -342,8 +344,8 @@ __global__ void __launch_bounds__(RT_NT, 1) k_routes(cw_scene_params P, int e0, 
           v[i] = rv[i] * nx + cv[i];
           ok[i] = true;
         }
-        // most relaxations improve nothing: a cached read filters them before the atomic
         unsigned long long old[BT];
+#ifdef CW_ROUTES_PREFILTER   // A/B: a plain read filters relaxations that cannot improve
 #pragma unroll
         for (int i = 0; i < BT; ++i) old[i] = ok[i] ? (unsigned long long)((volatile unsigned long long*)Fg)[v[i]] : 0ull;
 #pragma unroll
@@ -351,26 +353,36 @@ __global__ void __launch_bounds__(RT_NT, 1) k_routes(cw_scene_params P, int e0, 
           ok[i] = ok[i] && kk[i] < old[i];
           if (ok[i]) old[i] = atomicMin(&Fg[v[i]], kk[i]);
         }
-        int jj[BT], st_old[BT];
+#else
+#pragma unroll
+        for (int i = 0; i < BT; ++i) old[i] = ok[i] ? atomicMin(&Fg[v[i]], kk[i]) : 0ull;
+#endif
 #pragma unroll
         for (int i = 0; i < BT; ++i) {
-          ok[i] = ok[i] && kk[i] < old[i];
-          jj[i] = ok[i] ? (int)ab_bucket(kk[i]) : -1;   // k + 1 or k + 2
-        }
-#pragma unroll
-        for (int i = 0; i < BT; ++i) st_old[i] = ok[i] ? atomicExch(&St[v[i]], jj[i]) : jj[i];
-#pragma unroll
-        for (int i = 0; i < BT; ++i) {
-          if (ok[i] && st_old[i] != jj[i]) {
-            const int slot = jj[i] % 3;
-            Lb[(size_t)slot * cap + atomicAdd(&s_fn[g][slot], 1)] = (rv[i] << 16) | cv[i];
+          if (ok[i] && kk[i] < old[i]) {
+            const int slot = (int)(ab_bucket(kk[i]) % 3);   // k + 1 or k + 2
+            const int at = atomicAdd(&s_fn[g][slot], 1);
+            if (at < cap) {
+              LK[(size_t)slot * cap + at] = kk[i];
+              LC[(size_t)slot * cap + at] = (rv[i] << 16) | cv[i];
+            } else {
+              s_ovf = 1;
+            }
           }
         }
       }
       gsync();
-      if (gt == 0) s_fn[g][cur] = 0;
+      if (gt == 0) {
+        s_fn[g][cur] = 0;
+        for (int b = 0; b < 3; ++b) s_fn[g][b] = min(s_fn[g][b], cap);
+      }
       gsync();
     }
+  }
+  __syncthreads();
+  if (s_ovf) {   // a bucket list overflowed: the field may be incomplete -- report, never guess
+    if (tid == 0) { B.status[row_e] = CW_E_HEAPCAP; n_routes[row_e] = 0; }
+    return;
   }
   __syncthreads();
   auto geo_of = [&](int fi, int f) -> double {
@@ -467,12 +479,30 @@ __global__ void __launch_bounds__(RT_NT, 1) k_routes(cw_scene_params P, int e0, 
   }
 }
 
+// Persistent CTAs (one scratch slot each) take envs from a counter until all are
+// done: no launch-to-launch tails between env chunks.
+__global__ void __launch_bounds__(RT_NT, 1) k_routes(cw_scene_params P, int E, const uint64_t* __restrict__ scene_seeds,
+                                                     const int32_t* slots, cw_scene_buffers B, double* routes,
+                                                     int32_t* n_routes, unsigned char* scratch, int* counter) {
+  __shared__ int s_e;
+  unsigned char* base = scratch + (size_t)blockIdx.x * route_scratch_per_env(P.nx, P.ny);
+  while (true) {
+    if (threadIdx.x == 0) s_e = atomicAdd(counter, 1);
+    __syncthreads();
+    const int e = s_e;
+    __syncthreads();
+    if (e >= E) return;
+    route_env(P, e, scene_seeds, slots, B, routes, n_routes, base);
+    __syncthreads();
+  }
+}
+
 }  // namespace cw
 
 extern "C" {
 
 size_t cw_route_scratch_bytes(int nx, int ny, int chunk) {
-  return (size_t)chunk * cw::route_scratch_per_env(nx, ny);
+  return (size_t)chunk * cw::route_scratch_per_env(nx, ny) + 256;   // + the env counter
 }
 
 // scene.py:102-178 for rows slots[e] of B->labels (scene seeds as for sampling);
@@ -487,11 +517,11 @@ int cw_route_anchors(const cw_scene_params* P, int E, const uint64_t* scene_seed
   const size_t smem = (size_t)((P->nx * P->ny + 31) / 32) * 4;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_routes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  for (int e0 = 0; e0 < E; e0 += chunk) {
-    const int n = min(chunk, E - e0);
-    k_routes<<<n, RT_NT, smem, st>>>(*P, e0, n, scene_seeds, slots, *B, routes, n_routes,
-                                     (unsigned char*)scratch);
-  }
+  int* counter = reinterpret_cast<int*>(static_cast<unsigned char*>(scratch) +
+                                        (size_t)chunk * route_scratch_per_env(P->nx, P->ny));
+  cudaMemsetAsync(counter, 0, sizeof(int), st);
+  k_routes<<<min(chunk, E), RT_NT, smem, st>>>(*P, E, scene_seeds, slots, *B, routes, n_routes,
+                                               (unsigned char*)scratch, counter);
   return (int)cudaGetLastError();
 }
 
