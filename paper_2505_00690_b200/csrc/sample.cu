@@ -1025,10 +1025,11 @@ CW_DEV bool region_ok(const cw_scene_params& P, uint8_t zone, int c) {
   return true;
 }
 
-// Warp per env.  kStage: the env's zone grid (4 bits per cell) and the placed
-// objects' SAT data live in shared memory for the whole rejection loop (one env per
-// CTA), so every footprint / overlap test reads shared memory; else global (grids
-// whose packed zone tile does not fit).
+// Warp per env.  kStage: the env's zone grid (4 bits per cell, 32 KB at 256^2) lives in
+// shared memory for the whole rejection loop (one env per CTA, all 1024 cfg2 envs
+// resident at once), so every footprint zone / region test reads shared memory; the
+// placed objects' SAT data stay in the L1-cached global scratch.  Without kStage
+// (grids whose packed tile does not fit) the zones are read from global memory.
 template <bool kStage>
 __global__ void __launch_bounds__(kStage ? 32 : 128) k_place(cw_scene_params P, int E, const int32_t* slots,
                                                            const EnvSeeds* __restrict__ seeds,
@@ -1046,10 +1047,7 @@ __global__ void __launch_bounds__(kStage ? 32 : 128) k_place(cw_scene_params P, 
   double* cache = B.scratch_f64 + (size_t)e * (size_t)max(P.obj_max * 8, (int)N);  // corners
   int32_t* ocat = B.obj_cat + (size_t)slot * P.obj_max;
   double* opose = B.obj_pose + (size_t)slot * P.obj_max * 3;
-  // staged layout: zones (2 cells per byte), then per placed object 8 corner doubles,
-  // x, y, reach
-  uint8_t* zs = place_sm;
-  double* os = reinterpret_cast<double*>(place_sm + ((N / 2 + 1 + 15) & ~(size_t)15));
+  uint8_t* zs = place_sm;   // staged zones, 2 cells per byte
   if (kStage) {
     const uint4* Z16 = reinterpret_cast<const uint4*>(Z);   // N % 32 == 0 (checked by the launch)
     for (size_t q = lane; q < N / 16; q += 32) {
@@ -1128,9 +1126,9 @@ __global__ void __launch_bounds__(kStage ? 32 : 128) k_place(cw_scene_params P, 
       bool hit = false;
       const double reach = P.cat_reach[k];
       for (int j = lane; j < placed; j += 32) {
-        const double* o = kStage ? os + (size_t)j * 11 : cache + (size_t)j * 8;
-        const double ox = kStage ? o[8] : opose[j * 3 + 0], oy = kStage ? o[9] : opose[j * 3 + 1];
-        double rr = reach + (kStage ? o[10] : P.cat_reach[ocat[j]]);
+        const double* o = cache + (size_t)j * 8;
+        const double ox = opose[j * 3 + 0], oy = opose[j * 3 + 1];
+        double rr = reach + P.cat_reach[ocat[j]];
         double dx = x - ox, dy = y - oy;
         if (dx * dx + dy * dy > rr * rr) continue;
         if (sat_overlap(cx, cy, o, o + 4)) hit = true;
@@ -1141,9 +1139,8 @@ __global__ void __launch_bounds__(kStage ? 32 : 128) k_place(cw_scene_params P, 
         opose[placed * 3 + 0] = x;
         opose[placed * 3 + 1] = y;
         opose[placed * 3 + 2] = yaw;
-        double* o = kStage ? os + (size_t)placed * 11 : cache + (size_t)placed * 8;
+        double* o = cache + (size_t)placed * 8;
         for (int i = 0; i < 4; ++i) { o[i] = cx[i]; o[4 + i] = cy[i]; }
-        if (kStage) { o[8] = x; o[9] = y; o[10] = reach; }
       }
       __syncwarp();
       ++placed;
@@ -1157,10 +1154,10 @@ __global__ void __launch_bounds__(kStage ? 32 : 128) k_place(cw_scene_params P, 
   }
 }
 
-// shared memory of the staged k_place: packed zones + 11 doubles per object
+// shared memory of the staged k_place: the packed zones
 CW_HD size_t place_stage_bytes(const cw_scene_params& p) {
   const size_t N = (size_t)p.nx * p.ny;
-  return ((N / 2 + 1 + 15) & ~(size_t)15) + (size_t)p.obj_max * 11 * sizeof(double);
+  return (N / 2 + 1 + 15) & ~(size_t)15;
 }
 
 // ================================================================= raster
