@@ -506,22 +506,35 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
     st.err = 0;
   }
   int found = 0;
+  // Held pop: in ~70 % of expansions exactly one new key is below the head's minimum
+  // (the plateau descent toward the goal; tools/astar_faststat.py) -- that key is the
+  // next pop (every head key > it, every pool key >= T > it), so it is kept aside
+  // instead of being inserted into the head and popped again.
+  bool held = false;
+  Key hk = key_inf();
   __syncwarp();
   while (true) {
-    if (st.h == 0) {
+    if (!held && st.h == 0) {
       if (st.nn == 0 && st.nf == 0) break;
       st = refill(st, pl, lane);
       if (st.err) { found = -1; break; }
       continue;
     }
-    // ---------------- pop the head minimum
-    const Key popped = shfl_key(st.hd, 0);
-    const u64 topk = popped.k;
-    {
+    // ---------------- pop the minimum: the held key, else the head's first
+    const bool from_held = held;
+    Key popped, h0;   // h0: the head's minimum after the pop (+inf if empty)
+    if (from_held) {
+      popped = hk;
+      h0 = shfl_key(st.hd, 0);
+      held = false;
+    } else {
+      popped = shfl_key(st.hd, 0);
+      h0 = shfl_key(st.hd, 1);
       const Key nxt = shfl_key_down(st.hd, 1);
       st.hd = lane < 31 ? nxt : key_inf();
+      st.h -= 1;
     }
-    st.h -= 1;
+    const u64 topk = popped.k;
     const int r = (int)(topk >> 31) & 1023, c = (int)(topk >> 21) & 1023;
     const int sx = (int)(topk >> 5) & 0xFFFF;
     const int x = r * nx + c;
@@ -575,6 +588,19 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
       const int leader = __ffs(peers) - 1;
       const unsigned lm = __ballot_sync(0xffffffffu, need && leader == lane);
       if (!take(__popc(lm))) {   // only when !kGlob: hand the search over (see Resume)
+        if (from_held && st.h == 32) {   // the popped key goes back into a full head
+          const Key ev = shfl_key(st.hd, 31);
+          const bool evn = klt(ev, st.F2);
+          if (lane == 0) {
+            OpenEnt o = {ev.f, ev.k};
+            if (evn) pl.near[st.nn] = o;
+            else pl.far[st.nf] = o;
+          }
+          st.nn += evn;
+          st.nf += !evn;
+          st.T = ev;
+          st.h = 31;
+        }
         const Key up = shfl_key_up(st.hd, 1);
         st.hd = lane == 0 ? popped : up;
         st.h += 1;
@@ -607,6 +633,26 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
     if (toF) { OpenEnt o = {ne.f, ne.k}; pl.far[st.nf + __popc(fmk & lt_mask)] = o; }
     st.nn += __popc(nmk);
     st.nf += __popc(fmk);
+#ifndef CW_ASTAR_NO_HOLD
+    {
+      const unsigned lo = __ballot_sync(0xffffffffu, toH & klt(ne0, h0));
+      if (__popc(lo) == 1) {
+        const int s = __ffs(lo) - 1;
+        mh &= ~(1u << s);
+        hk = shfl_key(ne, s);
+        if ((decm >> s) & 1u) {   // its stale entry leaves the head (see below)
+          const unsigned om = __ballot_sync(0xffffffffu, ((st.hd.k ^ hk.k) & kCellMask2) == 0ull);
+          if (om) {
+            const int L = __ffs(om) - 1;
+            const Key dn = shfl_key_down(st.hd, 1);
+            if (lane >= L) st.hd = lane < st.h - 1 ? dn : key_inf();
+            st.h -= 1;
+          }
+        }
+        held = true;
+      }
+    }
+#endif
     while (mh) {
       const int s = __ffs(mh) - 1;
       mh &= mh - 1;
