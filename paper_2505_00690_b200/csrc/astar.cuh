@@ -355,7 +355,10 @@ CW_HD size_t astar_slot_bytes(int nx, int ny, int S) {
 // free slot ids), so a lone long search can use nearly all of it.  W = 1 is
 // the latency shape (few searches per tick: the tick waits on the longest
 // one), W = 4 the throughput shape (many searches per tick).
-constexpr int kAstarWarps = 4;   // scratch is sized for the larger shape
+#ifndef CW_ASTAR_WARPS
+#define CW_ASTAR_WARPS 4
+#endif
+constexpr int kAstarWarps = CW_ASTAR_WARPS;   // scratch is sized for the larger shape
 
 struct AstarShape {
   int NC, NS, W;
