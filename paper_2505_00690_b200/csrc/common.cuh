@@ -71,8 +71,8 @@ CW_DEV long long clampll(long long v, long long lo, long long hi) {
 // The reference's trig (np.cos / np.sin on float64 = glibc libm) is accurate to
 // within one ulp and rounds correctly in all but rare cases; CUDA's sincos has a
 // 2-ulp bound.  cr_sincos evaluates sin and cos in double-double (Cody-Waite
-// reduction by pi/2 in four parts, Taylor series to degree 27 on |r| <= pi/4,
-// error ~2^-100 relative) and rounds once, so it returns the correctly rounded
+// reduction by pi/2 in four parts, Taylor series to degree 27 on |r| <= pi/4 with the
+// leading terms in double-double, error < 2^-73 relative) and rounds once: the correctly rounded
 // value -- glibc's result whenever glibc rounds correctly.  Used where a trig
 // value feeds a geometric decision (footprint corners, SAT, cell tests).
 struct DD { double hi, lo; };
@@ -94,24 +94,25 @@ CW_DEV DD dd_mul(DD a, DD b) {
   return dd_fast(p, __dadd_rn(e, __dadd_rn(__dmul_rn(a.hi, b.lo), __dmul_rn(a.lo, b.hi))));
 }
 
+// 1/n! as double-doubles (hi, lo), n = 0..27
+static __constant__ double kInvFactHi[28] = {
+    0x1p+0, 0x1p+0, 0x1p-1, 0x1.5555555555555p-3, 0x1.5555555555555p-5, 0x1.1111111111111p-7,
+    0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-13, 0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19,
+    0x1.27e4fb7789f5cp-22, 0x1.ae64567f544e4p-26, 0x1.1eed8eff8d898p-29, 0x1.6124613a86d09p-33,
+    0x1.93974a8c07c9dp-37, 0x1.ae7f3e733b81fp-41, 0x1.ae7f3e733b81fp-45, 0x1.952c77030ad4ap-49,
+    0x1.6827863b97d97p-53, 0x1.2f49b46814157p-57, 0x1.e542ba4020225p-62, 0x1.71b8ef6dcf572p-66,
+    0x1.0ce396db7f853p-70, 0x1.761b41316381ap-75, 0x1.f2cf01972f578p-80, 0x1.3f3ccdd165fa9p-84,
+    0x1.88e85fc6a4e5ap-89, 0x1.d1ab1c2dccea3p-94};
+static __constant__ double kInvFactLo[9] = {
+    0.0, 0.0, 0.0, 0x1.5555555555555p-57, 0x1.5555555555555p-59, 0x1.1111111111111p-63,
+    -0x1.f49f49f49f49fp-65, 0x1.a01a01a01a01ap-73, 0x1.a01a01a01a01ap-76};
+
+// sin and cos of x in double-double, rounded once.  Reduction by pi/2 in four parts;
+// on |r| <= pi/4 the series in y = -r^2 keeps its leading terms (sin/r: y^0..y^3,
+// cos: y^0..y^4) in double-double and evaluates the rest (from r^9 resp. r^10 on,
+// magnitude < 3e-6) in double: total relative error < 2^-73, so the result is the
+// correctly rounded value but in cases within 2^-73 of a rounding midpoint.
 CW_DEV void cr_sincos(double x, double* s_out, double* c_out) {
-  // 1/n! as double-doubles, n = 0..27
-  const double fh[28] = {
-      0x1p+0, 0x1p+0, 0x1p-1, 0x1.5555555555555p-3, 0x1.5555555555555p-5, 0x1.1111111111111p-7,
-      0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-13, 0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19,
-      0x1.27e4fb7789f5cp-22, 0x1.ae64567f544e4p-26, 0x1.1eed8eff8d898p-29, 0x1.6124613a86d09p-33,
-      0x1.93974a8c07c9dp-37, 0x1.ae7f3e733b81fp-41, 0x1.ae7f3e733b81fp-45, 0x1.952c77030ad4ap-49,
-      0x1.6827863b97d97p-53, 0x1.2f49b46814157p-57, 0x1.e542ba4020225p-62, 0x1.71b8ef6dcf572p-66,
-      0x1.0ce396db7f853p-70, 0x1.761b41316381ap-75, 0x1.f2cf01972f578p-80, 0x1.3f3ccdd165fa9p-84,
-      0x1.88e85fc6a4e5ap-89, 0x1.d1ab1c2dccea3p-94};
-  const double fl[28] = {
-      0.0, 0.0, 0.0, 0x1.5555555555555p-57, 0x1.5555555555555p-59, 0x1.1111111111111p-63,
-      -0x1.f49f49f49f49fp-65, 0x1.a01a01a01a01ap-73, 0x1.a01a01a01a01ap-76, -0x1.c154f8ddc6c00p-73,
-      0x1.cbbc05b4fa99ap-76, -0x1.c062e06d1f209p-80, -0x1.2aec959e14c06p-83, 0x1.f28e0cc748ebep-87,
-      0x1.05d6f8a2efd1fp-92, 0x1.1d8656b0ee8cbp-97, 0x1.1d8656b0ee8cbp-101, 0x1.ac981465ddc6cp-103,
-      0x1.eec01221a8b0bp-107, 0x1.2650f61dbdcb4p-112, 0x1.ea72b4afe3c2fp-120, -0x1.d043ae40c4647p-120,
-      -0x1.aebcdbd20331cp-124, -0x1.3423c7d91404fp-130, -0x1.9ada5fcc1ab14p-135, -0x1.58ddadf344487p-139,
-      -0x1.71c37ebd16540p-143, 0x1.054d0c78aea14p-149};
   if (!(fabs(x) < 0x1p+20)) { sincos(x, s_out, c_out); return; }   // not used by the path
   // pi/2 = P1 + P2 + P3 + P4 (P1..P3 carry 33 bits: k * Pi is exact for |k| < 2^20)
   const double P1 = 0x1.921fb544p+0, P2 = 0x1.0b4611a6p-34, P3 = 0x1.3198a2ep-69, P4 = 0x1.b839a252049c1p-104;
@@ -121,14 +122,18 @@ CW_DEV void cr_sincos(double x, double* s_out, double* c_out) {
   r = dd_add(r, DD{-__dmul_rn(k, P3), 0.0});
   r = dd_add(r, DD{-__dmul_rn(k, P4), 0.0});
   const DD r2 = dd_mul(r, r);
-  DD ps{fh[27], fl[27]}, pc{fh[26], fl[26]};
-#pragma unroll 1
-  for (int n = 25; n >= 1; n -= 2) {   // sin: odd 1/n!, cos: even 1/(n-1)!, alternating signs
-    ps = dd_mul(ps, DD{-r2.hi, -r2.lo});
-    ps = dd_add(ps, DD{fh[n], fl[n]});
-    pc = dd_mul(pc, DD{-r2.hi, -r2.lo});
-    pc = dd_add(pc, DD{fh[n - 1], fl[n - 1]});
-  }
+  const DD y{-r2.hi, -r2.lo};
+  // double tails: sin/r terms y^4..y^13 (1/9! .. 1/27!), cos terms y^5..y^13 (1/10! .. 1/26!)
+  double ts = kInvFactHi[27], tc = kInvFactHi[26];
+#pragma unroll
+  for (int n = 25; n >= 9; n -= 2) ts = __dadd_rn(__dmul_rn(ts, y.hi), kInvFactHi[n]);
+#pragma unroll
+  for (int n = 24; n >= 10; n -= 2) tc = __dadd_rn(__dmul_rn(tc, y.hi), kInvFactHi[n]);
+  DD ps{ts, 0.0}, pc{tc, 0.0};
+#pragma unroll
+  for (int n = 7; n >= 1; n -= 2) ps = dd_add(dd_mul(ps, y), DD{kInvFactHi[n], kInvFactLo[n]});
+#pragma unroll
+  for (int n = 8; n >= 0; n -= 2) pc = dd_add(dd_mul(pc, y), DD{kInvFactHi[n], kInvFactLo[n]});
   const DD sr = dd_mul(ps, r);
   const double sv = __dadd_rn(sr.hi, sr.lo), cv = __dadd_rn(pc.hi, pc.lo);
   const int q = (int)((long long)k & 3);

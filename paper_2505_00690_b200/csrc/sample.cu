@@ -717,14 +717,15 @@ constexpr int TER_WARPS = 4;
 struct WarpWfc {
   TileSet T;
   unsigned long long nib[4][11][16];  // support tables: OR of allowed[d][t] over a nibble of tiles
+  double pw[CW_MAX_TILES];            // choice(): the options' weights / probabilities / cdf
 };
 
+// tiles allowed next to a cell with domain `dom` in direction d: the OR of the nibble
+// tables, all 11 lookups independent (nib[..][0] = 0)
 CW_DEV unsigned long long support(const WarpWfc& W, int d, unsigned long long dom) {
   unsigned long long s = 0;
-  for (int k = 0; dom; ++k, dom >>= 4) {
-    unsigned v = (unsigned)(dom & 15ull);
-    if (v) s |= W.nib[d][k][v];
-  }
+#pragma unroll
+  for (int k = 0; k < 11; ++k) s |= W.nib[d][k][(unsigned)(dom >> (4 * k)) & 15u];
   return s;
 }
 
@@ -891,33 +892,49 @@ __global__ void __launch_bounds__(TER_WARPS * 32) k_terrain(cw_scene_params P, i
         best = y < best ? y : best;
       }
       if (best == ~0ull) break;  // fully collapsed
+      // Generator.choice(no, p=w/tot) (wfc.py:71-77): the divisions and the
+      // searchsorted tests run one option per lane (each an independent IEEE op, so the
+      // same bits); the pairwise total and the cumsum stay sequential in lane 0
+      const int x = (int)(best & 0xffffffffu);
+      const unsigned long long d = dom[x];
+      const int no = __popcll(d);
+      const unsigned lo32 = (unsigned)d, hi32 = (unsigned)(d >> 32);
+      const int nlo = __popc(lo32);
+      auto opt_of = [&](int k) {   // the k-th set bit of d
+        return k < nlo ? (int)__fns(lo32, 0, k + 1) : 32 + (int)__fns(hi32, 0, k - nlo + 1);
+      };
+      for (int k = lane; k < no; k += 32) W.pw[k] = T.w[opt_of(k)];
+      __syncwarp();
+      double tot = 0.0;
+      if (lane == 0) tot = np_pairwise_sum(W.pw, no);
+      tot = __shfl_sync(0xffffffffu, tot, 0);
+      const bool uniform_w = !(tot > 0);
+      if (uniform_w) tot = (double)no;
+      double pk[2] = {0.0, 0.0};
+      for (int i = 0; i < 2; ++i) {
+        const int k = lane + 32 * i;
+        if (k < no) pk[i] = (uniform_w ? 1.0 : W.pw[k]) / tot;
+      }
+      __syncwarp();
+      for (int i = 0; i < 2; ++i) if (lane + 32 * i < no) W.pw[lane + 32 * i] = pk[i];
+      __syncwarp();
+      double u = 0.0;
+      if (lane == 0) {   // cdf = cumsum(p) in order
+        double acc = W.pw[0];
+        for (int k = 1; k < no; ++k) { acc = acc + W.pw[k]; W.pw[k] = acc; }
+        u = next_double(rng);
+      }
+      __syncwarp();
+      u = __shfl_sync(0xffffffffu, u, 0);
+      const double last = W.pw[no - 1];
+      // searchsorted(cdf / last, u, 'right') = the first k with cdf[k] / last > u
+      unsigned hit0 = __ballot_sync(0xffffffffu, lane < no && W.pw[lane] / last > u);
+      unsigned hit1 = __ballot_sync(0xffffffffu, lane + 32 < no && W.pw[lane + 32] / last > u);
+      const int idx = hit0 ? __ffs(hit0) - 1 : (hit1 ? 32 + __ffs(hit1) - 1 : no);
+      __syncwarp();
       int okl = 1;
       if (lane == 0) {
-        const int x = (int)(best & 0xffffffffu);
-        const unsigned long long d = dom[x];
-        int opts[CW_MAX_TILES];
-        double w[CW_MAX_TILES];
-        int no = 0;
-        for (int t = 0; t < n; ++t)
-          if ((d >> t) & 1ull) { opts[no] = t; w[no] = T.w[t]; ++no; }
-        double tot = np_pairwise_sum(w, no);
-        if (tot <= 0) {
-          for (int k = 0; k < no; ++k) w[k] = 1.0;
-          tot = (double)no;
-        }
-        // Generator.choice(no, p=w/tot): cdf = cumsum(p); cdf /= cdf[-1]; searchsorted right
-        double cdf[CW_MAX_TILES];
-        double acc = 0.0;
-        for (int k = 0; k < no; ++k) {
-          const double pk = w[k] / tot;
-          acc = k ? acc + pk : pk;
-          cdf[k] = acc;
-        }
-        const double last = cdf[no - 1];
-        const double u = next_double(rng);
-        int idx = 0;
-        while (idx < no && !(cdf[idx] / last > u)) ++idx;
-        dom[x] = 1ull << opts[idx];
+        dom[x] = 1ull << opt_of(idx);
         okl = wfc_propagate_from(W, dom, stack, inq, x, rows, cols);
       }
       ok = __shfl_sync(0xffffffffu, okl, 0) != 0;
