@@ -894,6 +894,10 @@ class DeviceView:
         return f"DeviceView({self.__array__()!r})"
 
     def __getattr__(self, name):          # shape, dtype, copy, sum, reshape, tolist, ...
+        if name.startswith("__"):
+            # never hand out a temporary array's buffer protocol (__array_interface__,
+            # __array_struct__ ...): numpy must go through __array__ and own its copy
+            raise AttributeError(name)
         return getattr(self.__array__(), name)
 
     def __array_ufunc__(self, ufunc, method, *inputs, **kw):
