@@ -52,6 +52,7 @@ CONFIGS = {
 CFG = dict(CONFIGS["cfg2"])
 METRIC = "env-steps/sec and scenes sampled/sec at N envs on 1/2/4/8 B200; % of HBM peak"
 ROBOT_SEED = 1234     # static robot: torch.Generator(cpu).manual_seed(ROBOT_SEED + rank)
+REF_BUDGET_S = 150.0  # CPU arms: stop timing ticks after this long per process (bounded sample)
 
 
 def peaks():
@@ -639,6 +640,7 @@ def _ref_worker(job):
     nx = labels.shape[1]
     rp = np.array([[(c % nx + 0.5) * cfg["res"], (c // nx + 0.5) * cfg["res"]]])
     rv = np.zeros((1, 2))
+    t_start = time.perf_counter()
     for _ in range(warm):
         f.step(robot_pos=rp, robot_vel=rv, robot_radius=0.35)
     t = []
@@ -646,6 +648,8 @@ def _ref_worker(job):
         t0 = time.perf_counter()
         f.step(robot_pos=rp, robot_vel=rv, robot_radius=0.35)
         t.append(time.perf_counter() - t0)
+        if t0 - t_start > REF_BUDGET_S:   # bounded sample (e.g. cfg4: seconds per tick)
+            break
     return t, t_scene
 
 
@@ -657,10 +661,11 @@ def _cpu_pool(n_env, steps, warm, use_ref):
         t0 = time.perf_counter()
         res = pool.map(_ref_worker, jobs)
         wall = time.perf_counter() - t0
-    times = np.array([r[0] for r in res])
+    k = min(len(r[0]) for r in res)                   # ticks every process completed
+    times = np.array([r[0][:k] for r in res])
     t_scene = max(r[1] for r in res)                 # all processes sample one scene each, in parallel
     total = float(np.max(times, axis=0).sum())       # all processes step in parallel
-    return n_env * steps / total, total, t_scene, wall
+    return n_env * k / total, total, t_scene, wall, k
 
 
 def cpu_baseline(args):
@@ -670,7 +675,7 @@ def cpu_baseline(args):
     use_ref = _reference_available()
     steps = max(1, min(args.steps, args.cpu_steps))
     warm = min(args.warmup, 60)
-    v, total, t_scene, wall = _cpu_pool(usable, steps, warm, use_ref)
+    v, total, t_scene, wall, steps = _cpu_pool(usable, steps, warm, use_ref)
     return {"value": round(v, 3), "unit": "env-steps/s", "cores": usable, "physical_cores": phys,
             "kind": "reference" if use_ref else "port", "seconds": round(total, 2),
             "scenes_per_sec": round(usable / t_scene, 4),
@@ -690,7 +695,7 @@ def run_reference(args):
     # whole run stays within a few minutes
     warm = min(args.warmup, 100)
     steps = max(1, min(args.steps, args.ref_steps))
-    v, total, t_scene, wall = _cpu_pool(usable, steps, warm, use_ref)
+    v, total, t_scene, wall, steps = _cpu_pool(usable, steps, warm, use_ref)
     kind = "reference" if use_ref else "port"
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "env-steps/s",
             "n_gpus": world, "steps": steps, "warmup": warm,
