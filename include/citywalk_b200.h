@@ -100,6 +100,8 @@ typedef struct cw_scene_buffers {
   uint8_t* block_var;   /* (E, CW_MAX_BLOCKS) block variant kind*4 + orientation of
                            connect_blocks (blocks.py:34-77), row-major; layout 1 only */
   const uint8_t* region; /* (E, ny*nx) optional route region mask (step.py:37 region_mask); NULL = none */
+  int32_t* epoch;       /* (E) optional grid generation: +1 for every row a sampling call writes
+                           (validates the crowd's next-tick search prefetch, cw_spec_create) */
 } cw_scene_buffers;
 
 size_t cw_scene_seed_scratch_bytes(int E);
@@ -205,9 +207,27 @@ typedef struct cw_crowd_state {
   void* astar_req;      /* (E*A, 16 B) replanning queue {env, agent, start, goal} */
   int64_t* counters;
   uint8_t* env_req;     /* (E) scratch: env queued a replan this tick (k_guide -> k_orca) */
+  void* spec;           /* optional host handle from cw_spec_create: next-tick search prefetch
+                           for cw_crowd_step (NULL = off; results are identical either way) */
+  const int32_t* env_epoch; /* (E) grid generation of each env; required with `spec`: must change
+                           whenever the env's labels / moves / reach change */
 } cw_crowd_state;
 
 size_t cw_crowd_step_smem_bytes(int A, int threads);
+
+/* Next-tick search prefetch for cw_crowd_step (no reference counterpart: it changes no
+ * result).  While a tick's longest A* searches run, the envs that already committed
+ * predict their next tick's replans (the guidance pass, read-only) and search them on a
+ * side stream into a per-agent cache; the next tick's k_astar takes a cached result
+ * whose (start, goal, grid generation) equals its request, waits for one in flight,
+ * and searches everything else as usual.  The context owns its device memory
+ * (cw_spec_bytes); destroy synchronises the side streams before freeing it. */
+size_t cw_spec_bytes(const cw_crowd_params* params);
+int cw_spec_create(const cw_crowd_params* params, void** handle);
+int cw_spec_destroy(void* handle);
+/* counters: [0] batches launched, plus per-context device totals read back on demand:
+ * [1] cache hits, [2] waits on a running prediction, [3] claims of a queued one */
+int cw_spec_stats(void* handle, long long* out4);
 
 int cw_crowd_step(const cw_crowd_params* params, const cw_crowd_state* state,
                   const double* robot_pos, const double* robot_vel, double robot_radius,

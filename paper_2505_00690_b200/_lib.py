@@ -44,7 +44,7 @@ SCENE_BUFFER_FIELDS = [
     "zones", "labels", "elev", "assign", "n_tiles", "tile_code", "tile_kind", "tile_param",
     "tile_p", "tile_w", "allowed", "noise_seed", "wfc_attempts", "obj_cat", "obj_pose", "obj_n",
     "overflow", "nearest", "has_obs", "walk", "walk_n", "reach", "moves", "sp_pos", "sp_goal", "sp_kind", "sp_pref",
-    "status", "scratch_i32", "scratch_f64", "zone_params", "block_var", "region",
+    "status", "scratch_i32", "scratch_f64", "zone_params", "block_var", "region", "epoch",
 ]
 
 
@@ -67,7 +67,7 @@ CROWD_STATE_FIELDS = [
     "pos", "vel", "goal", "waypoint", "radius", "pref_speed", "max_speed", "active", "path_cells",
     "path_head", "path_n", "labels", "nearest", "has_obs", "walk", "walk_n", "reach", "moves",
     "rng", "last_gap", "gap_tmp", "flags", "astar_rec", "astar_heap", "astar_req",
-    "counters", "env_req",
+    "counters", "env_req", "spec", "env_epoch",
 ]
 
 
@@ -107,7 +107,8 @@ EXPORTS = ["cw_scene_seed_scratch_bytes", "cw_sample_scenes", "cw_sample_scenes_
            "cw_route_scratch_bytes", "cw_route_anchors", "cw_seed_streams", "cw_child_seeds", "cw_abi_sizes",
            "cw_scene_rle", "cw_crowd_run_scratch_bytes", "cw_crowd_run",
            "cw_crowd_run_rounds", "cw_crowd_run_servers", "cw_crowd_run_window", "cw_sample_routes", "cw_connected_components",
-           "cw_rasterize", "cw_orca_lp", "cw_orca_halfplanes", "cw_crowd_constraints", "cw_trig_probe"]
+           "cw_rasterize", "cw_orca_lp", "cw_orca_halfplanes", "cw_crowd_constraints", "cw_trig_probe",
+           "cw_spec_bytes", "cw_spec_create", "cw_spec_destroy", "cw_spec_stats"]
 
 _lib = None
 
@@ -185,6 +186,14 @@ def lib():
     L.cw_crowd_run_rounds.argtypes = []
     L.cw_crowd_run_servers.restype = ctypes.c_longlong
     L.cw_crowd_run_servers.argtypes = []
+    L.cw_spec_bytes.restype = ctypes.c_size_t
+    L.cw_spec_bytes.argtypes = [ctypes.POINTER(CrowdParams)]
+    L.cw_spec_create.restype = ctypes.c_int
+    L.cw_spec_create.argtypes = [ctypes.POINTER(CrowdParams), ctypes.POINTER(ctypes.c_void_p)]
+    L.cw_spec_destroy.restype = ctypes.c_int
+    L.cw_spec_destroy.argtypes = [ctypes.c_void_p]
+    L.cw_spec_stats.restype = ctypes.c_int
+    L.cw_spec_stats.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_longlong)]
     L.cw_crowd_run.restype = ctypes.c_int
     L.cw_crowd_run.argtypes = [ctypes.POINTER(CrowdParams), ctypes.POINTER(CrowdState), P, P,
                                ctypes.c_double, P, ctypes.c_int, ctypes.c_int, P, P]

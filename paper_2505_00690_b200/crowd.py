@@ -23,6 +23,7 @@ Every computation here runs in the CUDA library; the host code only moves
 arguments and results.
 """
 
+import os
 from dataclasses import dataclass
 from enum import IntEnum
 
@@ -100,9 +101,14 @@ class CrowdField:
     OccupancyGrid (host labels, uploaded once) or a device ``SceneBatch``."""
 
     def __init__(self, occupancies, config, env_seeds, resample_goals=True, device="cuda",
-                 threads=128, path_cap=None, heap_cap=None, astar_warps=None):
+                 threads=128, path_cap=None, heap_cap=None, astar_warps=None, prefetch=None):
         import torch
         self.config = config
+        # next-tick search prefetch in step() (cw_spec_create): results are identical with
+        # or without it; CW_PREFETCH=0 turns it off for A/B runs
+        self.prefetch = (os.environ.get("CW_PREFETCH", "1") != "0") if prefetch is None else bool(prefetch)
+        self._spec_h = None
+        self._spec_key = None
         self.resample_goals = resample_goals
         self.device = torch.device(device)
         self.threads = threads
@@ -119,6 +125,7 @@ class CrowdField:
             self.labels_t, self.nearest_t, self.has_obs_t = b.labels, b.nearest, b.has_obs
             self.walk_t, self.walk_n_t = b.walk, b.walk_n
             self.reach_t, self.moves_t = b.reach, b.moves
+            self.epoch_t = b.epoch   # grid generation, bumped by every sampling call
             self._batch = b
         else:
             occs = list(occupancies)
@@ -131,6 +138,7 @@ class CrowdField:
             self.res = float(occs[0].resolution)
             self.res0 = self.res
             self._batch = None
+            self.epoch_t = torch.zeros((self.E,), dtype=torch.int32, device=self.device)
             self._upload_grids(occs)
         if self.nx > 1024 or self.ny > 1024:
             raise NotImplementedError("grids above 1024 x 1024 cells (A* packs row/col in 10 bits)")
@@ -174,6 +182,7 @@ class CrowdField:
         self.reach_t = torch.empty((E, ny * nx), dtype=torch.int32, device=self.device)
         self.moves_t = torch.zeros((E, ny * nx), dtype=torch.uint8, device=self.device)
         self._prepare(None)
+        self.epoch_t += 1
 
     def _prepare(self, rows):
         """field.py:60-67 (_prepare_env) for all envs or the given rows."""
@@ -290,6 +299,7 @@ class CrowdField:
         self.kind_t[idx] = batch.sp_kind[idx]
         self.active_t[idx] = 1
         self.path_n_t[idx] = 0
+        self.epoch_t[idx] += 1   # the rows' grids were (re)sampled
 
     def replace_env(self, e, occupancy):
         """field.py:403-413 for a host OccupancyGrid."""
@@ -298,6 +308,7 @@ class CrowdField:
             raise ValueError("replacement grid must keep the batch shape")
         self.labels_t[e] = torch.from_numpy(np.ascontiguousarray(occupancy.labels)).to(self.device)
         self._prepare([e])
+        self.epoch_t[e] += 1
         self._invalidate()
 
     # -- stepping (field.py:90-163) -----------------------------------------------
@@ -338,10 +349,37 @@ class CrowdField:
                  moves=self.moves_t, rng=self.rng_t,
                  last_gap=self.last_gap_t, gap_tmp=self.gap_tmp_t, flags=self.flags_t,
                  astar_rec=self.astar_rec_t, astar_req=self.astar_req_t,
-                 astar_heap=self.astar_heap_t, counters=self.counters_t, env_req=self.env_req_t)
+                 astar_heap=self.astar_heap_t, counters=self.counters_t, env_req=self.env_req_t,
+                 env_epoch=self.epoch_t)
         for k, v in m.items():
             setattr(s, k, v.data_ptr())
+        s.spec = self._spec_handle()
         return s
+
+    def _spec_handle(self):
+        """The next-tick prefetch context for the current shapes (None when off)."""
+        import ctypes
+        if not self.prefetch or self.device.type != "cuda" or self.A == 0:
+            return None
+        p = self._params()
+        key = (p.E, p.A, p.nx, p.ny, p.path_cap, p.heap_cap)
+        if key != self._spec_key:
+            self._spec_free()
+            h = ctypes.c_void_p()
+            _lib.check(_lib.lib().cw_spec_create(p, ctypes.byref(h)), "cw_spec_create")
+            self._spec_h, self._spec_key = h.value, key
+        return self._spec_h
+
+    def _spec_free(self):
+        if self._spec_h:
+            _lib.lib().cw_spec_destroy(self._spec_h)
+        self._spec_h, self._spec_key = None, None
+
+    def __del__(self):
+        try:
+            self._spec_free()
+        except Exception:
+            pass
 
     def prepare_step(self):
         """Build the launch arguments (rebuilt automatically after set_agents /
@@ -631,7 +669,18 @@ class CrowdField:
                 "astar_cycles": int(c[4]), "astar_max_cycles": int(c[5]),
                 "cta_cycles": int(c[6]), "cta_max_cycles": int(c[7]),
                 "astar_global_retries": int(c[10]), "path_points_read": int(c[12]),
-                "los_samples_read": int(c[13])}
+                "los_samples_read": int(c[13]), **self.prefetch_stats()}
+
+    def prefetch_stats(self):
+        """Next-tick prefetch: batches launched, cached results used, waits on a
+        prediction still running, queued predictions searched in place."""
+        import ctypes
+        if not self._spec_h:
+            return {}
+        v = (ctypes.c_longlong * 4)()
+        _lib.check(_lib.lib().cw_spec_stats(self._spec_h, v), "cw_spec_stats")
+        return {"prefetch_batches": v[0], "prefetch_hits": v[1], "prefetch_waits": v[2],
+                "prefetch_claims": v[3]}
 
 
 def step_crowd(agents, robot_state, occupancy, config, seed=0, resample_goals=True):

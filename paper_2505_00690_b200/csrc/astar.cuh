@@ -106,6 +106,9 @@ struct Pools {
 
 CW_DEV double octile(int r, int c, int gr, int gc);
 
+template <class T>
+CW_DEV T ld_grid(const T* p, bool cg) { return cg ? __ldcg(p) : *p; }
+
 // An entry whose cell has since been improved is stale for good (g only
 // decreases); the reference pops it and skips it (paths.py:70-71), so it can
 // be dropped whenever the pools are scanned.  Key layout: see make_key2.
@@ -406,6 +409,9 @@ struct SearchEnv {
   int32_t* parent;       // global, this warp: N
   int32_t* s2t;          // global, this warp: allocation k -> slot << 16 | tile
   long long* trace;      // debug (counters[15]): expanded cell + f bits of one search
+#ifdef CW_ASTAR_PHASES
+  long long* ph;         // debug: [head inserts, insert cycles, held pops, refill cycles]
+#endif
 };
 
 // Take n slots from the CTA pool (lane 0; false if it holds fewer).
@@ -444,7 +450,8 @@ struct Resume {
 
 template <bool kGlob>
 CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int start, int goal,
-                      double& delta, double& delta2, unsigned& s_exp, int& used, int lane, Resume& rs) {
+                      double& delta, double& delta2, unsigned& s_exp, int& used, int lane, Resume& rs,
+                      bool cg) {
   double* const gt = kGlob ? E.gtg : E.gts;
   uint8_t* const mt = kGlob ? E.mtg : E.mts;
   const int nx = E.nx, ny = E.ny, TW = E.TW, NT = E.NT, NC = pl.NC;
@@ -470,7 +477,7 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
     gp[lane + 32] = CUDART_INF;
     for (int j = lane; j < 64; j += 32) {
       const int rr = r0 + (j >> 3), cc = c0 + (j & 7);
-      mp[j] = (rr < ny && cc < nx) ? mvt[rr * nx + cc] : (uint8_t)0;
+      mp[j] = (rr < ny && cc < nx) ? ld_grid(mvt + rr * nx + cc, cg) : (uint8_t)0;
     }
     if (lane == 0) E.tmap[t] = (uint16_t)s;
     return s;
@@ -519,7 +526,13 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
   while (true) {
     if (!held && st.h == 0) {
       if (st.nn == 0 && st.nf == 0) break;
+#ifdef CW_ASTAR_PHASES
+      const long long tr0 = clock64();
       st = refill(st, pl, lane);
+      E.ph[3] += clock64() - tr0;
+#else
+      st = refill(st, pl, lane);
+#endif
       if (st.err) { found = -1; break; }
       continue;
     }
@@ -656,6 +669,11 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
       }
     }
 #endif
+#ifdef CW_ASTAR_PHASES
+    E.ph[0] += __popc(mh);
+    E.ph[2] += held;
+    const long long ti0 = clock64();
+#endif
     while (mh) {
       const int s = __ffs(mh) - 1;
       mh &= mh - 1;
@@ -705,6 +723,9 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
       if (lane == p) st.hd = v;
       st.h += 1;
     }
+#ifdef CW_ASTAR_PHASES
+    E.ph[1] += clock64() - ti0;
+#endif
     __syncwarp();
   }
   delta = st.delta;
@@ -719,9 +740,12 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
 // kRing: persistent search server of cw_crowd_run -- requests come from the
 // run ring (runq.cuh) until q->shutdown, and each finished search decrements
 // its env's pending count.
+// sp.mode (SpecArgs, crowd.cu): 0 plain; 1 the tick's searches, each looked up in the
+// next-tick prefetch cache first; 2 a speculative batch (requests from the dry guidance
+// pass, results into the cache, its own scratch, no state or error-flag writes).
 template <int W, bool kRing>
 __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd_state S, int NC, int NS,
-                                                     RunArgs ra) {
+                                                     RunArgs ra, SpecArgs sp) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gw = blockIdx.x * kAstarWarps + w;       // global search-warp id (scratch slot)
@@ -739,7 +763,9 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
   Pools pl;
   pl.near = reinterpret_cast<OpenEnt*>(wblk);
   pl.stg = pl.near + NC;
-  pl.far = reinterpret_cast<OpenEnt*>(S.astar_heap) + (size_t)gw * P.heap_cap;
+  const bool spec = !kRing && sp.mode == 2;
+  const size_t slot = spec ? (size_t)sm_id() * kAstarWarps + w : (size_t)gw;
+  pl.far = (spec ? sp.heap : reinterpret_cast<OpenEnt*>(S.astar_heap)) + slot * P.heap_cap;
   pl.NC = NC;
   pl.far_cap = P.heap_cap;
 
@@ -750,8 +776,8 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
   E.gts = reinterpret_cast<double*>(pool + 16 + (((size_t)NS * 2 + 15) & ~(size_t)15));
   E.mts = reinterpret_cast<uint8_t*>(E.gts + (size_t)NS * 64);
   E.wbuf = reinterpret_cast<uint16_t*>(pl.stg) + 0;   // staging area doubles as the slot buffer
-  unsigned char* const gbase = reinterpret_cast<unsigned char*>(S.astar_rec) +
-                               (size_t)gw * astar_slot_stride(nx, E.ny);
+  unsigned char* const gbase = (spec ? sp.rec : reinterpret_cast<unsigned char*>(S.astar_rec)) +
+                               slot * astar_slot_stride(nx, E.ny);
   const int NTG = NT + astar_ns_cap(nx, E.ny);   // global store: every tile + the pool's slot ids
   E.gtg = reinterpret_cast<double*>(gbase);
   E.mtg = gbase + (size_t)NTG * 64 * 8;
@@ -761,9 +787,9 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
   for (int i = threadIdx.x; i < NS; i += blockDim.x) E.free_ids[i] = (uint16_t)i;
   if (threadIdx.x == 0) { E.pool_lock[0] = 0; E.pool_lock[1] = NS; }
   __syncthreads();
-  long long* const dbg = (!kRing && S.counters && S.counters[14])
+  long long* const dbg = (!kRing && !spec && S.counters && S.counters[14])
                              ? reinterpret_cast<long long*>(S.counters[14]) : nullptr;
-  long long* const trace = (!kRing && S.counters && S.counters[15])
+  long long* const trace = (!kRing && !spec && S.counters && S.counters[15])
                                ? reinterpret_cast<long long*>(S.counters[15]) : nullptr;
   long long t_max = 0, t_sum = 0;
   unsigned long long n_exp = 0, n_glob = 0;
@@ -779,6 +805,25 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
       R.agent = __shfl_sync(0xffffffffu, R.agent, 0);
       R.start = __shfl_sync(0xffffffffu, R.start, 0);
       R.goal = __shfl_sync(0xffffffffu, R.goal, 0);
+    } else if (spec) {
+      // a queued prediction is this warp's once its entry moves queued -> running
+      int ok = 0;
+      if (lane == 0) {
+        q = atomicAdd(&sp.qn[1], 1);
+        if (q < *(volatile int*)&sp.qn[0]) {
+          R = sp.q[q];
+          const unsigned long long t = sp.tag << 8;
+          ok = atomicCAS(&sp.ent[(size_t)R.env * P.A + R.agent].word, t | kSpQueued, t | kSpRunning) ==
+               (t | kSpQueued) ? 1 : 2;
+        }
+      }
+      ok = __shfl_sync(0xffffffffu, ok, 0);
+      if (ok == 0) break;
+      if (ok == 2) continue;
+      R.env = __shfl_sync(0xffffffffu, R.env, 0);
+      R.agent = __shfl_sync(0xffffffffu, R.agent, 0);
+      R.start = __shfl_sync(0xffffffffu, R.start, 0);
+      R.goal = __shfl_sync(0xffffffffu, R.goal, 0);
     } else {
       if (lane == 0) q = atomicAdd(&S.flags[5], 1);
       q = __shfl_sync(0xffffffffu, q, 0);
@@ -787,6 +832,10 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
     }
     const long long t0 = clock64();
     E.trace = (trace && q == 0) ? trace : nullptr;
+#ifdef CW_ASTAR_PHASES
+    long long phv[4] = {0, 0, 0, 0};
+    E.ph = phv;
+#endif
 
     const int e = R.env;
     const uint8_t* mvt = S.moves + (size_t)e * N;
@@ -819,12 +868,69 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
       __syncwarp();
       used = 0;
     };
-    if (lab[start] != L_OBSTACLE && lab[goal] != L_OBSTACLE && reach[start] == reach[goal]) {
+    const size_t ia = (size_t)e * P.A + R.agent;
+    int32_t* cells = (spec ? sp.cells : S.path_cells) + ia * P.path_cap;
+    // 1: the cache entry holds this search's result (cells copied below)
+    int hit = 0, h_count = 0, h_found = 0, h_over = 0, ep = 0;
+    if (spec) {
+      if (lane == 0) ep = ld_acquire_i32(&sp.epoch[e]);   // before any read of the env's grid
+      __syncwarp();
+    } else if (!kRing && sp.mode == 1 && lane == 0) {
+      SpecEnt* en = sp.ent + ia;
+      const int cur = *(volatile const int*)&sp.epoch[e];
+      bool waited = false;
+      while (true) {
+        const unsigned long long wd = *(volatile unsigned long long*)&en->word;
+        const int st = (int)(wd & 0xFFull);
+        const bool same = *(volatile int*)&en->start == start && *(volatile int*)&en->goal == goal;
+        const unsigned long long claimed = (wd & ~0xFFull) | kSpClaimed;
+        if (st == kSpQueued) {   // not started: search it here (a stale prediction is dropped)
+          if (atomicCAS(&en->word, wd, claimed) != wd) continue;
+          if (same) atomicAdd(&sp.stats[3], 1ull);
+          break;
+        }
+        if (!same) break;
+        if (st == kSpRunning) {
+          if (!waited) atomicAdd(&sp.stats[2], 1ull);
+          waited = true;
+          __nanosleep(256);
+          continue;
+        }
+        if (st == kSpDone) {
+          __threadfence();
+          if (*(volatile int*)&en->epoch == cur) {
+            atomicAdd(&sp.stats[1], 1ull);
+            hit = 1;
+            h_count = *(volatile int*)&en->count;
+            h_found = *(volatile int*)&en->found;
+            h_over = *(volatile int*)&en->over;
+          }
+        }
+        break;
+      }
+    }
+    if (!kRing && sp.mode == 1) {
+      hit = __shfl_sync(0xffffffffu, hit, 0);
+      if (hit) {
+        h_count = __shfl_sync(0xffffffffu, h_count, 0);
+        h_found = __shfl_sync(0xffffffffu, h_found, 0);
+        h_over = __shfl_sync(0xffffffffu, h_over, 0);
+        if (h_found == 1 && !h_over) {
+          const int32_t* src = sp.cells + ia * P.path_cap;
+          for (int k = P.path_cap - h_count + lane; k < P.path_cap; k += 32) cells[k] = src[k];
+        }
+        found = h_found;
+      }
+    }
+    // a speculative batch may outlive a grid rewrite of its env (a later generation):
+    // its grid reads bypass L1, which may still hold the earlier generation's lines
+    if (!hit && ld_grid(lab + start, spec) != L_OBSTACLE && ld_grid(lab + goal, spec) != L_OBSTACLE &&
+        ld_grid(reach + start, spec) == ld_grid(reach + goal, spec)) {
       Resume rs;
       rs.active = 0;
       rs.slot_base = 0;
       rs.gcount = 0;
-      found = run_search<false>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs);
+      found = run_search<false>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs, spec);
       if (found == -2 && rs.active) {
         // the shared tile pool ran dry mid-search: move the used tiles to the
         // global store at their slot ids, give the slots back to the CTA pool
@@ -856,7 +962,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
         rs.slot_base = NS;
         rs.gcount = 0;
         ++n_glob;
-        found = run_search<true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs);
+        found = run_search<true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs, spec);
       } else if (found == -2) {   // no tile even for the start cell: all-global from scratch
         release();
         pooled = false;
@@ -865,20 +971,22 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
         rs.active = 0;
         rs.slot_base = 0;
         rs.gcount = 0;
-        found = run_search<true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs);
+        found = run_search<true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs, spec);
       }
     }
     // ---- write the guidance result (field.py:204-212)
-    const size_t ia = (size_t)e * P.A + R.agent;
-    int32_t* cells = S.path_cells + ia * P.path_cap;
     int pn = 1, head = 0;
-    double wx = S.goal[ia * 2], wy = S.goal[ia * 2 + 1];
-    if (found == -1 && lane == 0) atomicCAS(&S.flags[1], 0, (int)CW_E_HEAPCAP);
+    double wx = 0.0, wy = 0.0;
+    if (!spec) {
+      wx = S.goal[ia * 2];
+      wy = S.goal[ia * 2 + 1];
+    }
+    if (found == -1 && lane == 0 && !spec) atomicCAS(&S.flags[1], 0, (int)CW_E_HEAPCAP);
     if (found == 1) {
       // one walk of the parent chain (goal -> start, L2 pointer chasing), writing the
       // cells back to front: the path is cells[head .. path_cap - 1] in forward order
-      int count = 0, over = 0;
-      if (lane == 0) {
+      int count = h_count, over = h_over;
+      if (lane == 0 && !hit) {
         for (int v = goal; v != start; v = E.parent[v]) {
           if (count == P.path_cap) { over = 1; break; }
           cells[P.path_cap - 1 - count] = v;
@@ -888,7 +996,10 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
       count = __shfl_sync(0xffffffffu, count, 0);
       over = __shfl_sync(0xffffffffu, over, 0);
       __syncwarp();
-      if (over) {
+      if (spec) {
+        h_count = count;
+        h_over = over;
+      } else if (over) {
         if (lane == 0) atomicCAS(&S.flags[1], 0, (int)CW_E_PATHCAP);
       } else if (count >= 1) {
         pn = count + 1;
@@ -898,7 +1009,17 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
         wy = ((double)(f0 / nx) + 0.5) * P.res;
       }
     }
-    if (lane == 0) {
+    if (spec) {   // publish the prediction (the cells are written above)
+      if (lane == 0) {
+        SpecEnt* en = sp.ent + ia;
+        en->epoch = ep;
+        en->count = h_count;
+        en->found = found;
+        en->over = h_over;
+        __threadfence();
+        atomicExch(&en->word, (sp.tag << 8) | (found == -1 ? kSpFailed : kSpDone));
+      }
+    } else if (lane == 0) {
       S.path_head[ia] = head;
       S.path_n[ia] = pn;
       S.waypoint[ia * 2] = wx;
@@ -925,12 +1046,15 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
     if (dbg && lane == 0) {
       long long* d = dbg + (size_t)q * 8;
       d[0] = dt; d[1] = s_exp; d[2] = e; d[3] = used_final;
+#ifdef CW_ASTAR_PHASES
+      d[4] = phv[0]; d[5] = phv[1]; d[6] = phv[2]; d[7] = phv[3];
+#endif
     }
     n_exp += s_exp;
     t_sum += dt;
     t_max = max(t_max, dt);
   }
-  if (lane == 0 && S.counters) {
+  if (lane == 0 && S.counters && !spec) {
     if (n_exp) atomicAdd((unsigned long long*)&S.counters[0], n_exp);
     if (t_sum) atomicAdd((unsigned long long*)&S.counters[4], (unsigned long long)t_sum);
     if (t_max) atomicMax((unsigned long long*)&S.counters[5], (unsigned long long)t_max);

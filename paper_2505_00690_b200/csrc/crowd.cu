@@ -415,6 +415,42 @@ CW_DEV double octile(int r, int c, int gr, int gc) {
 struct AstarReq { int32_t env, agent, start, goal; };
 struct __align__(16) OpenEnt { unsigned long long f, k; };
 
+// ---- next-tick search prefetch (cw_spec_create; see launch_step)
+// An A* result is a pure function of (env grid, start cell, goal cell).  While a tick's
+// longest searches run, the envs that have already committed (no replan this tick)
+// predict their next tick's replans with a read-only copy of the guidance pass and
+// search them ahead on a side stream into a per-agent cache entry.  The next tick's
+// k_astar looks each request up: an entry with the same (start, goal) and the env's
+// current grid generation is the search's result (copied), one still running is
+// waited for, one still queued is claimed and searched in place; anything else is
+// searched as usual.  Nothing the tick computes depends on whether an entry was used.
+enum : int { kSpEmpty = 0, kSpWriting, kSpQueued, kSpRunning, kSpDone, kSpClaimed, kSpFailed };
+struct __align__(16) SpecEnt {
+  unsigned long long word;   // batch tag << 8 | state (CAS-owned transitions)
+  int32_t start, goal;       // the predicted request
+  int32_t epoch;             // grid generation read before the search read the grid
+  int32_t count, found, over;   // result: cells in cells[path_cap - count, path_cap)
+};
+struct SpecArgs {
+  int mode;                  // 0: plain, 1: tick search with cache lookup, 2: speculative batch
+  SpecEnt* ent;              // (E * A)
+  int32_t* cells;            // (E * A, path_cap)
+  const int32_t* epoch;      // (E) grid generation of each env (bumped by every grid write)
+  AstarReq* q;               // mode 2 (and the dry guide): the batch's requests
+  int* qn;                   // [0] count, [1] next
+  unsigned char* rec;        // mode 2: search scratch per (SM, warp) -- at most one search
+  OpenEnt* heap;             //   CTA is resident per SM (shared memory), so %smid indexes it
+  size_t rec_stride;
+  unsigned long long tag;    // mode 2 / dry guide: this batch's tag
+  unsigned long long* stats; // [1] hits, [2] waits on a running prediction, [3] claims
+};
+
+CW_DEV unsigned sm_id() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
 }  // namespace cw
 #include "runq.cuh"
 #include "astar.cuh"
@@ -430,17 +466,43 @@ CW_DEV void path_point(const int32_t* cells, int head, int n, int k, double gx, 
   y = ((double)r + 0.5) * res;
 }
 
+// Queue one predicted request (lane 0 of the guiding warp).  An entry still queued or
+// running belongs to an earlier batch and is left alone; an entry already holding this
+// (start, goal) for the current grid is kept as it is.
+CW_DEV void spec_request(const SpecArgs& sp, const AstarReq& R, size_t ia) {
+  SpecEnt* en = sp.ent + ia;
+  const unsigned long long w = *(volatile unsigned long long*)&en->word;
+  const int st = (int)(w & 0xFFull);
+  if (st == kSpWriting || st == kSpQueued || st == kSpRunning) return;
+  if (st == kSpDone && *(volatile int*)&en->start == R.start && *(volatile int*)&en->goal == R.goal &&
+      *(volatile int*)&en->epoch == *(volatile const int*)&sp.epoch[R.env])
+    return;
+  if (atomicCAS(&en->word, w, (sp.tag << 8) | kSpWriting) != w) return;
+  en->start = R.start;
+  en->goal = R.goal;
+  const int q = atomicAdd(&sp.qn[0], 1);
+  sp.q[q] = R;
+  __threadfence();
+  atomicExch(&en->word, (sp.tag << 8) | kSpQueued);
+}
+
 // k_guide: field.py:165-212 minus the A* itself (queued for k_astar).
 // Body shared by k_guide (requests appended to astar_req) and k_round (requests
 // pushed to the run ring).  Returns the env's request count (CTA-uniform).
-template <int NT, bool kRing>
+// kDry (next-tick search prefetch): the same decisions on the committed state, no
+// state writes; each replan it would queue becomes a speculative cache request.  The
+// state it reads may be rewritten concurrently by the host (a prediction only), so
+// every index it derives is clamped.
+template <int NT, bool kRing, bool kDry = false>
 __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int e,
-                         const uint8_t* __restrict__ env_mask, const RunArgs* ra) {
+                         const uint8_t* __restrict__ env_mask, const RunArgs* ra,
+                         const SpecArgs* sp = nullptr) {
   const int lane = threadIdx.x & 31;
   const int A = P.A;
   const size_t eA = (size_t)e * A;
   __shared__ int s_req;   // replans this env queued
-  if (env_mask && !env_mask[e]) {
+  if (kDry && S.env_req[e]) return 0;   // still searching this tick: not predicted
+  if (!kDry && env_mask && !env_mask[e]) {
     if (threadIdx.x == 0) S.env_req[e] = 0;
     return 0;
   }
@@ -473,14 +535,20 @@ __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
       gx = S.goal[ia * 2];
       gy = S.goal[ia * 2 + 1];
       if (!has_obs) {
-        S.waypoint[ia * 2] = gx;
-        S.waypoint[ia * 2 + 1] = gy;
+        if (!kDry) {
+          S.waypoint[ia * 2] = gx;
+          S.waypoint[ia * 2 + 1] = gy;
+        }
       } else {
         px = S.pos[ia * 2];
         py = S.pos[ia * 2 + 1];
         const int32_t* cells = S.path_cells + ia * P.path_cap;
         head = S.path_head[ia];
         n = S.path_n[ia];
+        if (kDry) {
+          head = min(max(head, 0), P.path_cap);
+          n = min(max(n, 0), P.path_cap - head + 1);
+        }
         need = 2;
         if (n > 0) {
           double qx, qy;
@@ -503,10 +571,12 @@ __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
           }
           scanned += n;   // the reference scans every remaining point (traffic model)
           if (near) {
-            S.path_head[ia] = head;
-            S.path_n[ia] = n;
-            S.waypoint[ia * 2] = qx;
-            S.waypoint[ia * 2 + 1] = qy;
+            if (!kDry) {
+              S.path_head[ia] = head;
+              S.path_n[ia] = n;
+              S.waypoint[ia * 2] = qx;
+              S.waypoint[ia * 2 + 1] = qy;
+            }
             need = 0;
           } else if (n > kLaneSegs + 1) {
             need = 1;
@@ -544,7 +614,7 @@ __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
           near = __any_sync(0xffffffffu, mine);
         }
         if (near) {
-          if (lane == 0) {
+          if (!kDry && lane == 0) {
             double wx, wy;
             path_point(cells, shead, sn, 0, sgx, sgy, res, nx, wx, wy);
             S.path_head[sia] = shead;
@@ -558,6 +628,7 @@ __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
       // _line_of_sight (field.py:601-610), 32 samples per step
       double d = glibc_hypot(sgx - spx, sgy - spy);
       long long ns = max(2LL, trunc_ll(2.0 * d / res) + 2);
+      if (kDry) ns = min(ns, 4LL * (nx + ny) + 2);   // torn reads must not run away
       double step = 1.0 / (double)(ns - 1);
       bool clear = true;
       for (long long k0 = 0; k0 < ns && clear; k0 += 32) {
@@ -575,17 +646,21 @@ __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
       }
       if (lane == 0) {
         if (clear) {
-          S.path_head[sia] = 0;
-          S.path_n[sia] = 1;
-          S.waypoint[sia * 2] = sgx;
-          S.waypoint[sia * 2 + 1] = sgy;
+          if (!kDry) {
+            S.path_head[sia] = 0;
+            S.path_n[sia] = 1;
+            S.waypoint[sia * 2] = sgx;
+            S.waypoint[sia * 2 + 1] = sgy;
+          }
         } else {
           int sr = (int)fmin(fmax(spy / res, 0.0), (double)(ny - 1));
           int sc = (int)fmin(fmax(spx / res, 0.0), (double)(nx - 1));
           int gr = (int)fmin(fmax(sgy / res, 0.0), (double)(ny - 1));
           int gc = (int)fmin(fmax(sgx / res, 0.0), (double)(nx - 1));
           AstarReq R = {e, sa, sr * nx + sc, gr * nx + gc};
-          if (kRing) {
+          if (kDry) {
+            spec_request(*sp, R, sia);
+          } else if (kRing) {
             ring_push(*ra, R);
           } else {
             int q = atomicAdd(&S.flags[4], 1);
@@ -603,6 +678,7 @@ __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
     los_read += __shfl_xor_sync(0xffffffffu, los_read, o);
     my_req += __shfl_xor_sync(0xffffffffu, my_req, o);
   }
+  if (kDry) return 0;
   if (lane == 0 && scanned && S.counters)
     atomicAdd((unsigned long long*)&S.counters[1], (unsigned long long)scanned);
   if (lane == 0 && pts_read && S.counters)
@@ -614,6 +690,12 @@ __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
   const int n_req = s_req;
   if (threadIdx.x == 0) S.env_req[e] = (uint8_t)(n_req > 0);
   return n_req;
+}
+
+// The dry guidance pass over the envs that committed without a replan this tick.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_guide_dry(cw_crowd_params P, cw_crowd_state S, SpecArgs sp) {
+  guide_env<NT, false, true>(P, S, blockIdx.x, nullptr, nullptr, &sp);
 }
 
 template <int NT>
@@ -1326,12 +1408,82 @@ static TickStreams& tick_streams() {
   return t;
 }
 
-static void launch_astar(const cw_crowd_params& P, const cw_crowd_state& S, cudaStream_t st) {
+static void launch_astar(const cw_crowd_params& P, const cw_crowd_state& S, cudaStream_t st,
+                         const SpecArgs& sp = SpecArgs{}) {
   const int W = P.astar_warps == 1 ? 1 : kAstarWarps;
   const AstarShape A = astar_shape(P.nx, P.ny, W);
   const RunArgs none = {};
-  if (W == 1) k_astar<1, false><<<P.astar_ctas, 32, A.smem, st>>>(P, S, A.NC, A.NS, none);
-  else k_astar<kAstarWarps, false><<<P.astar_ctas, 32 * kAstarWarps, A.smem, st>>>(P, S, A.NC, A.NS, none);
+  if (W == 1) k_astar<1, false><<<P.astar_ctas, 32, A.smem, st>>>(P, S, A.NC, A.NS, none, sp);
+  else k_astar<kAstarWarps, false><<<P.astar_ctas, 32 * kAstarWarps, A.smem, st>>>(P, S, A.NC, A.NS, none, sp);
+}
+
+// ---- next-tick search prefetch context (cw_spec_create)
+// Batches rotate over kSpecBatches low-priority streams: a batch may still be
+// finishing a search the next tick waits for while the following batch starts.
+// Scratch is indexed by (SM, warp): a search CTA needs more than half of an SM's
+// shared memory, so no two are ever resident on one SM.
+constexpr int kSpecBatches = 3;
+struct SpecCtx {
+  int E = 0, A = 0, path_cap = 0, heap_cap = 0, nx = 0, ny = 0, nsm = 0;
+  SpecEnt* ent = nullptr;
+  int32_t* cells = nullptr;
+  AstarReq* q[kSpecBatches] = {};
+  int* qn = nullptr;                       // kSpecBatches x 4
+  unsigned long long* stats = nullptr;     // 4
+  unsigned char* rec = nullptr;
+  OpenEnt* heap = nullptr;
+  size_t stride = 0;
+  cudaEvent_t guided = nullptr;            // the last dry guidance pass is done
+  int next = 0;
+  unsigned long long tag = 0;
+  long long batches = 0;
+};
+
+static cudaStream_t spec_stream(int b) {
+  static cudaStream_t s[kSpecBatches] = {};
+  if (!s[0]) {
+    int least, greatest;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    for (int k = 0; k < kSpecBatches; ++k) cudaStreamCreateWithPriority(&s[k], cudaStreamNonBlocking, least);
+  }
+  return s[b];
+}
+
+__global__ void k_nsmid(int* out) {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%nsmid;" : "=r"(r));
+  *out = (int)r;
+}
+
+static size_t spec_layout(const cw_crowd_params& P, int nsm, size_t* parts) {
+  const size_t EA = (size_t)P.E * P.A;
+  auto up = [](size_t v) { return (v + 255) & ~(size_t)255; };
+  const size_t warps = (size_t)nsm * kAstarWarps;
+  parts[0] = up(EA * sizeof(SpecEnt));
+  parts[1] = up(EA * (size_t)P.path_cap * 4);
+  parts[2] = up(EA * sizeof(AstarReq)) * kSpecBatches;
+  parts[3] = up((size_t)kSpecBatches * 4 * 4 + 4 * 8);
+  parts[4] = warps * astar_slot_stride(P.nx, P.ny);
+  parts[5] = up(warps * (size_t)P.heap_cap * sizeof(OpenEnt));
+  size_t t = 0;
+  for (int k = 0; k < 6; ++k) t += parts[k];
+  return t;
+}
+
+static SpecArgs spec_args(const SpecCtx* X, int mode, const int32_t* epoch, int b) {
+  SpecArgs a{};
+  a.mode = mode;
+  a.ent = X->ent;
+  a.cells = X->cells;
+  a.epoch = epoch;
+  a.q = X->q[b];
+  a.qn = X->qn + 4 * b;
+  a.rec = X->rec;
+  a.heap = X->heap;
+  a.rec_stride = X->stride;
+  a.tag = X->tag;
+  a.stats = X->stats;
+  return a;
 }
 
 // ---- cw_crowd_run scratch layout
@@ -1506,11 +1658,11 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
   long long n_servers = 0;
   auto launch_server = [&]() {
     if (srv_w == 4)
-      k_astar<kAstarWarps, true><<<srv_ctas, 32 * kAstarWarps, shp.smem, TS.hi>>>(P, S, shp.NC, shp.NS, ra);
+      k_astar<kAstarWarps, true><<<srv_ctas, 32 * kAstarWarps, shp.smem, TS.hi>>>(P, S, shp.NC, shp.NS, ra, SpecArgs{});
     else if (srv_w == 2)
-      k_astar<2, true><<<srv_ctas, 64, shp.smem, TS.hi>>>(P, S, shp.NC, shp.NS, ra);
+      k_astar<2, true><<<srv_ctas, 64, shp.smem, TS.hi>>>(P, S, shp.NC, shp.NS, ra, SpecArgs{});
     else
-      k_astar<1, true><<<srv_ctas, 32, shp.smem, TS.hi>>>(P, S, shp.NC, shp.NS, ra);
+      k_astar<1, true><<<srv_ctas, 32, shp.smem, TS.hi>>>(P, S, shp.NC, shp.NS, ra, SpecArgs{});
     cudaEventRecord(H.srv_done, TS.hi);
     ++n_servers;
   };
@@ -1611,6 +1763,9 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
   size_t sm = cw_crowd_step_smem_bytes(P.A, NT) + bins_smem_bytes(bins, P.A);
   if ((phases & 4) && sm > 48 * 1024)
     cudaFuncSetAttribute(k_orca<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  SpecCtx* X = (S.spec && S.env_epoch) ? static_cast<SpecCtx*>(S.spec) : nullptr;
+  // the previous tick's dry guidance pass reads the state this tick rewrites
+  if (X) cudaStreamWaitEvent(st, X->guided, 0);
   if (phases == 7) {
     // overlapped tick: envs without replans commit beside the A* searches.  An SM
     // runs one L1 / shared-memory split at a time, so k_orca asks for the same
@@ -1626,11 +1781,28 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
     cudaEventRecord(T.guided, st);
     cudaStreamWaitEvent(T.hi, T.guided, 0);
     cudaStreamWaitEvent(T.lo, T.guided, 0);
-    launch_astar(P, S, T.hi);
+    launch_astar(P, S, T.hi, X ? spec_args(X, 1, S.env_epoch, 0) : SpecArgs{});
     k_orca<NT><<<P.E, NT, sm, T.lo>>>(P, S, rp, rv, rr, em, bins, 1);
     k_orca<NT><<<P.E, NT, sm, T.hi>>>(P, S, rp, rv, rr, em, bins, 2);
     cudaEventRecord(T.hi_done, T.hi);
     cudaEventRecord(T.lo_done, T.lo);
+    if (X) {
+      // the committed envs' next tick: dry guidance, then its searches, on a side
+      // stream that the caller's stream does not join
+      const int b = X->next;
+      X->next = (b + 1) % kSpecBatches;
+      ++X->tag;
+      ++X->batches;
+      cudaStream_t ss = spec_stream(b);
+      const SpecArgs sa = spec_args(X, 2, S.env_epoch, b);
+      cudaStreamWaitEvent(ss, T.lo_done, 0);
+      cudaMemsetAsync(sa.qn, 0, 4 * sizeof(int), ss);
+      k_guide_dry<NT><<<P.E, NT, 0, ss>>>(P, S, sa);
+      cudaEventRecord(X->guided, ss);
+      const AstarShape A = astar_shape(P.nx, P.ny, kAstarWarps);
+      const RunArgs none = {};
+      k_astar<kAstarWarps, false><<<P.astar_ctas, 32 * kAstarWarps, A.smem, ss>>>(P, S, A.NC, A.NS, none, sa);
+    }
     cudaStreamWaitEvent(st, T.hi_done, 0);
     cudaStreamWaitEvent(st, T.lo_done, 0);
     return (int)cudaGetLastError();
@@ -1820,6 +1992,85 @@ size_t cw_crowd_step_smem_bytes(int A, int nt) {
 // Search warps per k_astar CTA (astar_rec / astar_heap hold one slot per warp).
 int cw_astar_warps(void) { return cw::kAstarWarps; }
 
+static int spec_nsm() {
+  static int n = 0;
+  if (!n) {
+    int* d = nullptr;
+    if (cudaMalloc(&d, sizeof(int)) != cudaSuccess) return 0;
+    cw::k_nsmid<<<1, 1>>>(d);
+    cudaMemcpy(&n, d, sizeof(int), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+  }
+  return n;
+}
+
+size_t cw_spec_bytes(const cw_crowd_params* P) {
+  size_t parts[6];
+  const int nsm = spec_nsm();
+  return nsm ? cw::spec_layout(*P, nsm, parts) : 0;
+}
+
+int cw_spec_create(const cw_crowd_params* P, void** handle) {
+  using namespace cw;
+  *handle = nullptr;
+  const int nsm = spec_nsm();
+  if (!nsm || P->E <= 0 || P->A <= 0) return (int)cudaErrorInvalidValue;
+  size_t parts[6];
+  const size_t total = spec_layout(*P, nsm, parts);
+  unsigned char* base = nullptr;
+  cudaError_t err = cudaMalloc(&base, total);
+  if (err != cudaSuccess) return (int)err;
+  SpecCtx* X = new SpecCtx();
+  X->E = P->E; X->A = P->A; X->path_cap = P->path_cap; X->heap_cap = P->heap_cap;
+  X->nx = P->nx; X->ny = P->ny; X->nsm = nsm;
+  size_t o = 0;
+  X->ent = reinterpret_cast<SpecEnt*>(base + o); o += parts[0];
+  X->cells = reinterpret_cast<int32_t*>(base + o); o += parts[1];
+  const size_t qb = parts[2] / kSpecBatches;
+  for (int b = 0; b < kSpecBatches; ++b) X->q[b] = reinterpret_cast<AstarReq*>(base + o + b * qb);
+  o += parts[2];
+  X->qn = reinterpret_cast<int*>(base + o);
+  X->stats = reinterpret_cast<unsigned long long*>(base + o + kSpecBatches * 4 * 4);
+  o += parts[3];
+  X->rec = base + o; o += parts[4];
+  X->heap = reinterpret_cast<OpenEnt*>(base + o);
+  X->stride = astar_slot_stride(P->nx, P->ny);
+  cudaMemset(X->ent, 0, parts[0]);
+  cudaMemset(X->qn, 0, parts[3]);
+  cudaEventCreateWithFlags(&X->guided, cudaEventDisableTiming);
+  for (int b = 0; b < kSpecBatches; ++b) spec_stream(b);
+  err = cudaDeviceSynchronize();
+  if (err != cudaSuccess) {
+    cudaFree(base);
+    delete X;
+    return (int)err;
+  }
+  *handle = X;
+  return 0;
+}
+
+int cw_spec_destroy(void* handle) {
+  using namespace cw;
+  if (!handle) return 0;
+  SpecCtx* X = static_cast<SpecCtx*>(handle);
+  for (int b = 0; b < kSpecBatches; ++b) cudaStreamSynchronize(spec_stream(b));
+  cudaFree(X->ent);   // the base of the one allocation
+  cudaEventDestroy(X->guided);
+  delete X;
+  return (int)cudaGetLastError();
+}
+
+int cw_spec_stats(void* handle, long long* out) {
+  using namespace cw;
+  if (!handle) return (int)cudaErrorInvalidValue;
+  SpecCtx* X = static_cast<SpecCtx*>(handle);
+  unsigned long long v[4] = {0, 0, 0, 0};
+  const cudaError_t err = cudaMemcpy(v, X->stats, sizeof(v), cudaMemcpyDeviceToHost);
+  out[0] = X->batches;
+  for (int k = 1; k < 4; ++k) out[k] = (long long)v[k];
+  return (int)err;
+}
+
 // Scratch bytes of cw_crowd_run for E envs x A agents over `ticks` ticks.
 size_t cw_crowd_run_scratch_bytes(int E, int A, int ticks) {
   return cw::run_layout(E, A, ticks).total;
@@ -1840,6 +2091,8 @@ int cw_crowd_run_window(const cw_crowd_params* P, const cw_crowd_state* S, const
   if (P->E <= 0 || P->A <= 0 || ticks <= 0) return 0;
   if (!scratch) return (int)cudaErrorInvalidValue;
   cudaStream_t st = (cudaStream_t)stream;
+  if (S->spec && S->env_epoch)   // a dry guidance pass may still read the state
+    cudaStreamWaitEvent(st, static_cast<SpecCtx*>(S->spec)->guided, 0);
   const double* rp = robot_pos;
   const double* rv = robot_vel;
   if (threads == 32)

@@ -1891,6 +1891,12 @@ size_t cw_scene_seed_scratch_bytes(int E) { return (size_t)E * sizeof(cw::EnvSee
 // zones -> terrain -> placement -> raster -> nearest-obstacle BFS -> walk list -> spawn.
 // Rows are written at slots[e] (slots may be NULL = identity).  Returns 0 or a
 // cudaError_t; per-env failures are reported in B->status.
+// grid generation of the rows just written (cw_scene_buffers.epoch)
+__global__ void k_bump_epoch(int E, const int32_t* slots, int32_t* epoch) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < E) epoch[slots ? slots[e] : e] += 1;
+}
+
 static int sample_impl(const cw_scene_params* P, int E, const uint64_t* scene_seeds, const uint64_t* crowd_seeds,
                        const int32_t* slots, void* seed_scratch, const cw_scene_buffers* B, const cw::RouteJob* rj,
                        void* stream) {
@@ -1943,6 +1949,7 @@ static int sample_impl(const cw_scene_params* P, int E, const uint64_t* scene_se
     cudaEventRecord(ss.join[k], ss.s[k]);
     cudaStreamWaitEvent(st, ss.join[k], 0);
   }
+  if (b.epoch) k_bump_epoch<<<(E + 255) / 256, 256, 0, st>>>(E, slots, b.epoch);   // after every grid write
   return (int)cudaGetLastError();
 }
 

@@ -316,7 +316,7 @@ def _scene_out_fields():
     """SceneBatch outputs a re-sampled row consists of (everything but scratch)."""
     global _SCENE_OUT
     if _SCENE_OUT is None:
-        _SCENE_OUT = [n for n in _lib.SCENE_BUFFER_FIELDS if not n.startswith("scratch") and n != "region"] + [
+        _SCENE_OUT = [n for n in _lib.SCENE_BUFFER_FIELDS if not n.startswith("scratch") and n not in ("region", "epoch")] + [
             "routes", "n_routes", "scene_seed"]
     return _SCENE_OUT
 

@@ -87,7 +87,8 @@ def state_checksum(*arrays):
     an int64 < 2^62 per env).  Integer arithmetic only, so the value is the same
     on any device and for any sharding of the envs."""
     import torch
-    parts = [torch.as_tensor(a).reshape(a.shape[0], -1).to(torch.float64) for a in arrays]
+    as_t = lambda a: a if isinstance(a, torch.Tensor) else torch.as_tensor(np.asarray(a))   # state views: one copy
+    parts = [as_t(a).reshape(a.shape[0], -1).to(torch.float64) for a in arrays]
     x = torch.cat(parts, 1).contiguous().view(torch.int64)
     words = torch.stack([x & 0xFFFFFFFF, (x >> 32) & 0xFFFFFFFF], 2).reshape(x.shape[0], -1) % _P
     return _weighted_mod(words)

@@ -439,6 +439,7 @@ class SceneBatch:
         self.zone_params = z((E, _lib.ZONE_PARAMS), dtype=torch.float64, **d)   # ZoneMap.params
         self.block_var = z((E, _lib.MAX_BLOCKS), dtype=torch.uint8, **d)        # connect_blocks
         self.region = None   # optional (E, N) u8 route region mask (spawn_agents(region_mask=))
+        self.epoch = z((E,), dtype=torch.int32, **d)   # grid generation (+1 per row sampled)
         self._scratch_rows = 0
         self._ensure_scratch(min(E, SceneSampler.max_rows))
 

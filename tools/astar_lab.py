@@ -92,12 +92,17 @@ for k in range(steps):
         np.add.at(env_exp, d[:nreq, 2].astype(np.int64), d[:nreq, 1].astype(np.float64))
         env_ticks[np.unique(d[:nreq, 2].astype(np.int64))] += 1
     for r_ in d[np.argsort(-d[:, 0])[:2]]:
-        if os.environ.get("LAB_PHASES"):
-            ph_ = [(int(r_[4 + i // 2]) >> (32 * (i % 2))) & 0xFFFFFFFF for i in range(6)] + [int(r_[7])]
-            print("      phases/exp [pop, loads+stale, gy+push, alloc, store+key, route+pool, inserts]:",
-                  " ".join(f"{v / max(r_[1], 1):5.0f}" for v in ph_))
+        if os.environ.get("LAB_PHASES"):   # build with -DCW_ASTAR_PHASES
+            x_ = max(r_[1], 1)
+            print(f"      per exp: head inserts {r_[4]/x_:5.2f} insert cyc {r_[5]/x_:6.0f} "
+                  f"held {r_[6]/x_:5.2f} refill cyc {r_[7]/x_:6.0f}")
         print(f"   search cyc {r_[0]/1e6:6.2f}M exp {r_[1]:6d} cyc/exp {r_[0]/max(r_[1],1):6.0f} env {r_[2]:6d} "
               f"tiles {r_[3]:6d}")
+    if os.environ.get("LAB_PHASES"):
+        a_ = d[:nreq].sum(axis=0).astype(np.float64)
+        x_ = max(a_[1], 1)
+        print(f"   all: cyc/exp {a_[0]/x_:6.0f} inserts {a_[4]/x_:5.2f} insert cyc {a_[5]/x_:6.0f} "
+              f"held {a_[6]/x_:5.2f} refill cyc {a_[7]/x_:6.0f}")
     f.check_flags()
     run(4)
     tot += t
