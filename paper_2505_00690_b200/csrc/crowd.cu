@@ -1211,14 +1211,23 @@ __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S
   if (!skip) orca_env<NT, kLanes>(P, S, e, robot_pos, robot_vel, robot_radius, env_mask, bins, sm, nullptr, 0);
   // ---------------- last CTA: publish last_gap_by_env (only when some row had K > 0),
   // reset the per-step flags and the A* queue
+  __shared__ int s_last;
+  __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    int ticket = atomicAdd(&S.flags[2], 1);
+    const int ticket = atomicAdd(&S.flags[2], 1);
+    s_last = 0;
     if (ticket == (pass == 0 ? 1 : 2) * (int)gridDim.x - 1) {   // last CTA over all passes
       __threadfence();
-      if (atomicAdd(&S.flags[0], 0)) {
-        for (int k = 0; k < P.E; ++k) S.last_gap[k] = ((volatile double*)S.gap_tmp)[k];
-      }
+      s_last = atomicAdd(&S.flags[0], 0) ? 2 : 1;
+    }
+  }
+  __syncthreads();
+  if (s_last) {
+    if (s_last == 2)   // the whole CTA copies (one thread's serial copy cost ~0.3 ms at E = 1024)
+      for (int k = threadIdx.x; k < P.E; k += blockDim.x) S.last_gap[k] = ((volatile double*)S.gap_tmp)[k];
+    __syncthreads();
+    if (threadIdx.x == 0) {
       S.flags[0] = 0;
       S.flags[2] = 0;
       S.flags[4] = 0;
