@@ -179,8 +179,25 @@ CW_DEV void grid_components(volatile int32_t* par, int nx, int ny, OkF ok) {
     }
   }
   __syncthreads();
-  for (int f = threadIdx.x; f < N; f += NT)
-    if (par[f] >= 0) par[f] = uf_root(par, f);
+  // root pass, four cells' pointer chains in flight per thread (dependent global loads)
+  for (int f0 = threadIdx.x; f0 < N; f0 += 4 * NT) {
+    int x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = f0 + u * NT < N ? par[f0 + u * NT] : -1;
+    bool more = true;
+    while (more) {
+      more = false;
+      int nx_[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) nx_[u] = x[u] >= 0 ? par[x[u]] : x[u];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (nx_[u] < x[u]) { x[u] = nx_[u]; more = true; }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (x[u] >= 0) par[f0 + u * NT] = x[u];
+  }
   __syncthreads();
 }
 
@@ -1476,6 +1493,11 @@ CW_DEV bool route_ok(const cw_scene_params& P, const cw_scene_buffers& B, int sl
 //   smallest such step (the value at i* just before step i* swaps into p).
 constexpr int ORD_BATCH = SP_NT;
 
+// k_spawn dynamic shared memory: accepted starts (2 x A doubles) + the candidate bitmap
+CW_HD size_t spawn_smem_bytes(int A, int nx, int ny) {
+  return (size_t)A * 2 * sizeof(double) + (((size_t)nx * ny + 31) / 32) * 4;
+}
+
 CW_DEV int resolve_final(int k, const int32_t* jj, const int32_t* head, const int32_t* nxt) {
   int p, t;
   if (k >= 1) { p = jj[k]; t = k + 1; }
@@ -1522,6 +1544,7 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
   extern __shared__ __align__(16) unsigned char sp_smem[];
   double* stx = reinterpret_cast<double*>(sp_smem);  // accepted starts (A)
   double* sty = stx + A;
+  uint32_t* s_ok = reinterpret_cast<uint32_t*>(sty + A);   // route_ok bitmap (NW32 words)
   int8_t* kind_out = B.sp_kind + (size_t)slot * A;
   double* pref_out = B.sp_pref + (size_t)slot * A;
   if (threadIdx.x == 0 && route_seeds) {
@@ -1550,6 +1573,8 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
     int f = f0 + threadIdx.x;
     int ok = f < N && route_ok(P, B, slot, Lb, f, N);
     if (f < N) { comp[f] = ok ? f : -1; head[f] = -1; csize[f] = 0; }
+    const unsigned okb = __ballot_sync(0xffffffffu, ok);
+    if (lane == 0 && f < N) s_ok[f >> 5] = okb;
     int tot;
     int off = block_excl_scan<SP_NT>(ok, sh, tot);
     if (ok) cand[base + off] = f;
@@ -1564,8 +1589,15 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
   }
   // 8-connected components (routes.py:14-32); only label equality is used
   // downstream (routes.py:62, 74), so any labelling works.
-  grid_components<SP_NT, true>(comp, nx, ny, [&](int f) { return route_ok(P, B, slot, Lb, f, N); });
-  for (int q = threadIdx.x; q < n; q += SP_NT) atomicAdd(&csize[comp[cand[q]]], 1);
+  grid_components<SP_NT, true>(comp, nx, ny, [&](int f) { return ((s_ok[f >> 5] >> (f & 31)) & 1u) != 0u; });
+  // component sizes: one atomic per (warp, component) -- nearly every candidate is
+  // in the same component, so per-candidate atomics serialise on one address
+  for (int q0 = 0; q0 < n; q0 += SP_NT) {
+    const int q = q0 + threadIdx.x;
+    const int cq = q < n ? comp[cand[q]] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, cq);
+    if (cq >= 0 && lane == __ffs(peers) - 1) atomicAdd(&csize[cq], __popc(peers));
+  }
   __syncthreads();
   // ---- permutation draws (warp 0): stream generation + warp-speculative
   // accept/reject.  Within a window where i stays above mask>>1 the mask is
@@ -1658,7 +1690,16 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
   }
   __syncthreads();
   // ---- link steps by partner position
-  for (int i = 1 + threadIdx.x; i < n; i += SP_NT) nxt[i] = atomicExch(&head[jj[i]], i);
+  for (int i0 = 1 + threadIdx.x; i0 < n; i0 += 4 * SP_NT) {   // four atomics in flight
+    int jv[4], rv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) jv[u] = i0 + u * SP_NT < n ? jj[i0 + u * SP_NT] : -1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) rv[u] = jv[u] >= 0 ? atomicExch(&head[jv[u]], i0 + u * SP_NT) : 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (jv[u] >= 0) nxt[i0 + u * SP_NT] = rv[u];
+  }
   if (threadIdx.x == 0) {
     s_acc = 0;
     s_k = 0;
@@ -1941,8 +1982,8 @@ static int sample_impl(const cw_scene_params* P, int E, const uint64_t* scene_se
   k_walk<<<E, 1024, 0, ss.s[1]>>>(p, E, slots, b);
   k_reach<<<E, 1024, 0, ss.s[1]>>>(p, E, slots, b);
   if (p.peds > 0) {
-    size_t sm = (size_t)p.peds * 2 * sizeof(double);
-    if (sm > 48 * 1024) cudaFuncSetAttribute(k_spawn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    size_t sm = spawn_smem_bytes(p.peds, p.nx, p.ny);
+    if (sm > 32 * 1024) cudaFuncSetAttribute(k_spawn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k_spawn<<<E, SP_NT, sm, st>>>(p, E, slots, S, b, nullptr);
   }
   for (int k = 0; k < nside; ++k) {
@@ -1982,8 +2023,8 @@ int cw_spawn_agents(const cw_scene_params* P, int E, const uint64_t* crowd_seeds
   cudaStream_t st = (cudaStream_t)stream;
   EnvSeeds* S = (EnvSeeds*)seed_scratch;
   k_seeds<<<(E + 127) / 128, 128, 0, st>>>(E, crowd_seeds, crowd_seeds, S);
-  size_t sm = (size_t)P->peds * 2 * sizeof(double);
-  if (sm > 48 * 1024) cudaFuncSetAttribute(k_spawn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  size_t sm = spawn_smem_bytes(P->peds, P->nx, P->ny);
+  if (sm > 32 * 1024) cudaFuncSetAttribute(k_spawn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k_spawn<<<E, SP_NT, sm, st>>>(*P, E, slots, S, *B, nullptr);
   return (int)cudaGetLastError();
 }
@@ -1999,8 +2040,8 @@ int cw_sample_routes(const cw_scene_params* P, int E, const uint64_t* route_seed
   if (E <= 0 || P->peds <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
   EnvSeeds* S = (EnvSeeds*)seed_scratch;
-  size_t sm = (size_t)P->peds * 2 * sizeof(double);
-  if (sm > 48 * 1024) cudaFuncSetAttribute(k_spawn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  size_t sm = spawn_smem_bytes(P->peds, P->nx, P->ny);
+  if (sm > 32 * 1024) cudaFuncSetAttribute(k_spawn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k_spawn<<<E, SP_NT, sm, st>>>(*P, E, slots, S, *B, route_seeds);
   return (int)cudaGetLastError();
 }
