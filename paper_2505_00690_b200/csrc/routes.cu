@@ -166,11 +166,21 @@ CW_DEV void chamfer_row(double* row, const double* prev, int nx, int lane) {
 // cell i32}), cand N i32, ok N i32 (the chamfer's D aliases field 0's keys)
 CW_HD size_t route_scratch_per_env(int nx, int ny) { return (size_t)nx * ny * (4 * (8 + 3 * 12) + 4 + 4); }
 
+// Shared memory of k_routes: the walkable bitmap, plus (kMv) one byte per cell whose
+// bit d says move d of paths.py:35-40 is legal from it (in bounds, walkable, diagonals
+// need both orthogonal cells walkable).
+CW_HD size_t route_smem_bytes(int nx, int ny, bool mv) {
+  const size_t N = (size_t)nx * ny;
+  return ((N + 31) / 32) * 4 + (mv ? ((N + 15) & ~(size_t)15) : 0);
+}
+constexpr size_t kRouteMvSmem = 100 * 1024;   // above: bitmap only, (entry, move) per thread
+
 // One env on the whole CTA (scratch `base` is the CTA's slot).
+template <bool kMv>
 __device__ void route_env(const cw_scene_params& P, int e, const uint64_t* __restrict__ scene_seeds,
                           const int32_t* slots, const cw_scene_buffers& B, double* routes, int32_t* n_routes,
                           unsigned char* base) {
-  extern __shared__ uint32_t s_walk[];   // walkable bits
+  extern __shared__ uint32_t s_walk[];   // walkable bits (then the move bytes, kMv)
   __shared__ int sh[RT_NT / 32 + 1];
   __shared__ int s_src[4], s_np, s_changed[4];
   __shared__ double s_pairs[RT_MAX * 4];
@@ -197,6 +207,25 @@ __device__ void route_env(const cw_scene_params& P, int e, const uint64_t* __res
   }
   __syncthreads();
   auto walk = [&](int r, int c) { return (s_walk[(r * nx + c) >> 5] >> ((r * nx + c) & 31)) & 1u; };
+  uint8_t* s_mv = reinterpret_cast<uint8_t*>(s_walk + NW);
+  if (kMv) {
+    for (int f = tid; f < N; f += RT_NT) {
+      const int r = f / nx, c = f - r * nx;
+      unsigned m = 0;
+      if (walk(r, c)) {
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+          const int rr = r + (int)((0x22001120u >> (4 * d)) & 0xF) - 1;
+          const int cc = c + (int)((0x20202011u >> (4 * d)) & 0xF) - 1;
+          if (rr < 0 || rr >= ny || cc < 0 || cc >= nx || !walk(rr, cc)) continue;
+          if (d >= 4 && !(walk(r, cc) && walk(rr, c))) continue;
+          m |= 1u << d;
+        }
+      }
+      s_mv[f] = (uint8_t)m;
+    }
+    __syncthreads();
+  }
   // ---- 1. clearance
   const int rad = (int)ceil(kMinClear / res);
   const bool stencil = rad <= 6;
@@ -300,7 +329,7 @@ __device__ void route_env(const cw_scene_params& P, int e, const uint64_t* __res
       const int f0 = cand[s_src[g]];
       Fg[f0] = ab_key(0, 0);
       LK[0] = ab_key(0, 0);
-      LC[0] = ((f0 / nx) << 16) | (f0 % nx);
+      LC[0] = kMv ? f0 : ((f0 / nx) << 16) | (f0 % nx);
       s_fn[g][0] = 1;
       s_fn[g][1] = 0;
       s_fn[g][2] = 0;
@@ -312,10 +341,61 @@ __device__ void route_env(const cw_scene_params& P, int e, const uint64_t* __res
       if (n_cur == 0 && s_fn[g][(cur + 1) % 3] == 0 && s_fn[g][(cur + 2) % 3] == 0) break;
       const unsigned long long* Kc = LK + (size_t)cur * cap;
       const int32_t* Cc = LC + (size_t)cur * cap;
+      if (kMv) {
+        // one entry per thread, its legal moves (one shared byte) in two halves of four
+        // atomics in flight; pushes aggregated per warp and target list (an orthogonal
+        // move from bucket k lands in bucket k + 1, a diagonal one in k + 1 or k + 2)
+        const int s1 = cur == 2 ? 0 : cur + 1, s2 = s1 == 2 ? 0 : s1 + 1;
+        const unsigned lt = (1u << lane) - 1u;
+        for (int q0 = gt - lane; q0 < n_cur; q0 += 256) {
+          const int q = q0 + lane;
+          const bool live = q < n_cur;
+          const int u = live ? Cc[q] : 0;
+          const unsigned long long ku = live ? Kc[q] : 0ull;
+          const unsigned m = live ? s_mv[u] : 0u;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            unsigned long long kn[4], old[4];
+            int vv[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int d = 4 * h + j;
+              const int dr = (int)((0x22001120u >> (4 * d)) & 0xF) - 1;
+              const int dc = (int)((0x20202011u >> (4 * d)) & 0xF) - 1;
+              vv[j] = u + dr * nx + dc;
+              kn[j] = ku + (h ? kStepDiag : kStepOrth);
+              old[j] = ((m >> d) & 1u) ? atomicMin(&Fg[vv[j]], kn[j]) : 0ull;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const bool push = (((m >> (4 * h + j)) & 1u) != 0u) && kn[j] < old[j];
+              const bool far = push && h && ab_bucket(kn[j]) != k + 1;
+              const unsigned b1 = __ballot_sync(0xffffffffu, push && !far);
+              const unsigned b2 = __ballot_sync(0xffffffffu, far);
+              int at1 = 0, at2 = 0;
+              if (lane == 0 && b1) at1 = atomicAdd(&s_fn[g][s1], __popc(b1));
+              if (lane == 0 && b2) at2 = atomicAdd(&s_fn[g][s2], __popc(b2));
+              if (b1 | b2) {
+                at1 = __shfl_sync(0xffffffffu, at1, 0) + __popc(b1 & lt);
+                at2 = __shfl_sync(0xffffffffu, at2, 0) + __popc(b2 & lt);
+                if (push) {
+                  const int sl = far ? s2 : s1, at = far ? at2 : at1;
+                  if (at < cap) {
+                    LK[(size_t)sl * cap + at] = kn[j];
+                    LC[(size_t)sl * cap + at] = vv[j];
+                  } else {
+                    s_ovf = 1;
+                  }
+                }
+              }
+            }
+          }
+        }
+      } else
       // items (entry, move) in batches of 4 per thread: the loads and atomics of a
       // batch are issued back to back; cells are packed (row << 16 | col)
-      constexpr int BT = 4;
-      for (int q0 = gt; q0 < n_cur * 8; q0 += 256 * BT) {
+      for (int q0 = gt; q0 < n_cur * 8; q0 += 256 * 4) {
+        constexpr int BT = 4;
         int pu[BT], rv[BT], cv[BT], v[BT];
         unsigned long long kk[BT];
         bool ok[BT];
@@ -481,6 +561,7 @@ __device__ void route_env(const cw_scene_params& P, int e, const uint64_t* __res
 
 // Persistent CTAs (one scratch slot each) take envs from a counter until all are
 // done: no launch-to-launch tails between env chunks.
+template <bool kMv>
 __global__ void __launch_bounds__(RT_NT, 1) k_routes(cw_scene_params P, int E, const uint64_t* __restrict__ scene_seeds,
                                                      const int32_t* slots, cw_scene_buffers B, double* routes,
                                                      int32_t* n_routes, unsigned char* scratch, int* counter) {
@@ -492,7 +573,7 @@ __global__ void __launch_bounds__(RT_NT, 1) k_routes(cw_scene_params P, int E, c
     const int e = s_e;
     __syncthreads();
     if (e >= E) return;
-    route_env(P, e, scene_seeds, slots, B, routes, n_routes, base);
+    route_env<kMv>(P, e, scene_seeds, slots, B, routes, n_routes, base);
     __syncthreads();
   }
 }
@@ -514,14 +595,21 @@ int cw_route_anchors(const cw_scene_params* P, int E, const uint64_t* scene_seed
   using namespace cw;
   if (E <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t smem = (size_t)((P->nx * P->ny + 31) / 32) * 4;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_routes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const bool mv = route_smem_bytes(P->nx, P->ny, true) <= kRouteMvSmem;
+  const size_t smem = route_smem_bytes(P->nx, P->ny, mv);
+  if (smem > 32 * 1024) {
+    if (mv) cudaFuncSetAttribute(k_routes<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    else cudaFuncSetAttribute(k_routes<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
   int* counter = reinterpret_cast<int*>(static_cast<unsigned char*>(scratch) +
                                         (size_t)chunk * route_scratch_per_env(P->nx, P->ny));
   cudaMemsetAsync(counter, 0, sizeof(int), st);
-  k_routes<<<min(chunk, E), RT_NT, smem, st>>>(*P, E, scene_seeds, slots, *B, routes, n_routes,
-                                               (unsigned char*)scratch, counter);
+  if (mv)
+    k_routes<true><<<min(chunk, E), RT_NT, smem, st>>>(*P, E, scene_seeds, slots, *B, routes, n_routes,
+                                                     (unsigned char*)scratch, counter);
+  else
+    k_routes<false><<<min(chunk, E), RT_NT, smem, st>>>(*P, E, scene_seeds, slots, *B, routes, n_routes,
+                                                      (unsigned char*)scratch, counter);
   return (int)cudaGetLastError();
 }
 
