@@ -1322,6 +1322,13 @@ constexpr int BFS_NT = 1024;
 // Level-synchronous BFS that reproduces the FIFO deque of field.py:579-592:
 // a level-(k+1) cell belongs to the earliest-ranked level-k parent that
 // reaches it, and the next level is ordered by (parent rank, direction).
+// Visited cells (obstacles and every cell already claimed) are a bitmap in shared
+// memory: the claim pass issues its atomicMin only towards unvisited neighbours, as
+// fire-and-forget reductions, and the winner pass loads the owner word only for them
+// (all of a cell's candidates at once).  The FIFO order is unchanged: the owner word is
+// still the smallest (frontier position, move) key of the level.
+CW_HD size_t nearest_smem_bytes(int nx, int ny) { return (((size_t)nx * ny + 31) / 32) * 4; }
+
 __global__ void __launch_bounds__(BFS_NT) k_nearest(cw_scene_params P, int E, const int32_t* slots,
                                                     cw_scene_buffers B) {
   const int e = blockIdx.x;
@@ -1332,8 +1339,10 @@ __global__ void __launch_bounds__(BFS_NT) k_nearest(cw_scene_params P, int E, co
   int32_t* near = B.nearest + (size_t)slot * N;
   int32_t* owner = B.scratch_i32 + (size_t)e * SCRATCH_I32_PER_CELL * N + 8 * (size_t)N;
   int32_t* Q = owner + N;
+  extern __shared__ uint32_t s_vis[];
   __shared__ int sh[BFS_NT / 32 + 1];
   const int UNSEEN = 0x7fffffff;
+  const int lane = threadIdx.x & 31;
   // seed: obstacles in row-major order
   int base = 0;
   for (int f0 = 0; f0 < N; f0 += BFS_NT) {
@@ -1343,6 +1352,8 @@ __global__ void __launch_bounds__(BFS_NT) k_nearest(cw_scene_params P, int E, co
       owner[f] = ob ? -1 : UNSEEN;
       near[f] = ob ? f : -1;
     }
+    const unsigned vb = __ballot_sync(0xffffffffu, ob);
+    if (lane == 0 && f < N) s_vis[f >> 5] = vb;
     int tot;
     int off = block_excl_scan<BFS_NT>(ob, sh, tot);
     if (ob) Q[base + off] = f;
@@ -1352,35 +1363,42 @@ __global__ void __launch_bounds__(BFS_NT) k_nearest(cw_scene_params P, int E, co
   __syncthreads();
   const int dr[8] = {1, -1, 0, 0, 1, 1, -1, -1};
   const int dc[8] = {0, 0, 1, -1, 1, -1, 1, -1};
+  auto vis = [&](int x) { return (s_vis[x >> 5] >> (x & 31)) & 1u; };
   int lo = 0, hi = base;
   while (lo < hi) {
     for (int q = lo + threadIdx.x; q < hi; q += BFS_NT) {
-      int p = Q[q], r = p / nx, c = p - r * nx;
-      int key0 = (q - lo) * 8;
+      const int p = Q[q], r = p / nx, c = p - r * nx;
+      const int key0 = (q - lo) * 8;
+#pragma unroll
       for (int d = 0; d < 8; ++d) {
-        int rr = r + dr[d], cc = c + dc[d];
+        const int rr = r + dr[d], cc = c + dc[d];
         if (rr < 0 || rr >= ny || cc < 0 || cc >= nx) continue;
-        int x = rr * nx + cc;
-        if (owner[x] >= 0) atomicMin(&owner[x], key0 + d);
+        const int x = rr * nx + cc;
+        if (!vis(x)) atomicMin(&owner[x], key0 + d);   // result unused: a reduction
       }
     }
     __syncthreads();
     int out = hi;
     for (int q0 = lo; q0 < hi; q0 += BFS_NT) {
-      int q = q0 + threadIdx.x;
+      const int q = q0 + threadIdx.x;
       unsigned win = 0;
       int p = 0, r = 0, c = 0;
       if (q < hi) {
         p = Q[q]; r = p / nx; c = p - r * nx;
-        int key0 = (q - lo) * 8;
-        for (int d = 0; d < 8; ++d) {
-          int rr = r + dr[d], cc = c + dc[d];
-          if (rr < 0 || rr >= ny || cc < 0 || cc >= nx) continue;
-          if (owner[rr * nx + cc] == key0 + d) win |= 1u << d;
+        const int key0 = (q - lo) * 8;
+        int ow[8];
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {   // the candidates' owner words, loaded together
+          const int rr = r + dr[d], cc = c + dc[d];
+          const bool in = rr >= 0 && rr < ny && cc >= 0 && cc < nx && !vis(rr * nx + cc);
+          ow[d] = in ? ((volatile int32_t*)owner)[rr * nx + cc] : -1;
         }
+#pragma unroll
+        for (int d = 0; d < 8; ++d)
+          if (ow[d] == key0 + d) win |= 1u << d;
       }
       int tot;
-      int off = block_excl_scan<BFS_NT>(__popc(win), sh, tot);
+      int off = block_excl_scan<BFS_NT>(__popc(win), sh, tot);   // (barrier: every read above is done)
       if (win) {
         int src = near[p];
         int k = 0;
@@ -1390,6 +1408,7 @@ __global__ void __launch_bounds__(BFS_NT) k_nearest(cw_scene_params P, int E, co
           Q[out + off + k++] = x;
           near[x] = src;
           owner[x] = -1;
+          atomicOr(&s_vis[x >> 5], 1u << (x & 31));
         }
       }
       out += tot;
@@ -1978,7 +1997,11 @@ static int sample_impl(const cw_scene_params* P, int E, const uint64_t* scene_se
   cudaEventRecord(ss.fork, st);
   for (int k = 0; k < nside; ++k) cudaStreamWaitEvent(ss.s[k], ss.fork, 0);
   if (rj) cw_route_anchors(P, E, scene_seeds, slots, B, rj->routes, rj->n_routes, rj->scratch, rj->chunk, ss.s[2]);
-  k_nearest<<<E, BFS_NT, 0, ss.s[0]>>>(p, E, slots, b);
+  {
+    const size_t nsm = nearest_smem_bytes(p.nx, p.ny);
+    if (nsm > 32 * 1024) cudaFuncSetAttribute(k_nearest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nsm);
+    k_nearest<<<E, BFS_NT, nsm, ss.s[0]>>>(p, E, slots, b);
+  }
   k_walk<<<E, 1024, 0, ss.s[1]>>>(p, E, slots, b);
   k_reach<<<E, 1024, 0, ss.s[1]>>>(p, E, slots, b);
   if (p.peds > 0) {
@@ -2085,7 +2108,9 @@ int cw_prepare_envs(const cw_scene_params* P, int E, const int32_t* slots,
   using namespace cw;
   if (E <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
-  k_nearest<<<E, BFS_NT, 0, st>>>(*P, E, slots, *B);
+  const size_t nsm = nearest_smem_bytes(P->nx, P->ny);
+  if (nsm > 32 * 1024) cudaFuncSetAttribute(k_nearest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nsm);
+  k_nearest<<<E, BFS_NT, nsm, st>>>(*P, E, slots, *B);
   k_walk<<<E, 1024, 0, st>>>(*P, E, slots, *B);
   k_reach<<<E, 1024, 0, st>>>(*P, E, slots, *B);
   return (int)cudaGetLastError();
