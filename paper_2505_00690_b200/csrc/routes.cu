@@ -1,7 +1,7 @@
 // Route anchors (reference urbangen/scene.py:102-178) on B200:
 // the candidate (start, goal) pairs the robot spawns on (envcore/batch.py:183-198).
 //
-// One CTA (1024 threads) per env:
+// One CTA (512 threads) per env, two per SM:
 //   1. clearance test chamfer_distance(~walkable) * res >= 0.4 (gridmath.py:8-39).
 //      The two-pass (1, sqrt2) chamfer with full-row relaxation is the octile
 //      distance to the nearest non-walkable cell (shortest octile paths can be
@@ -23,7 +23,7 @@
 //      finds (a, b) exactly: a cell's distance is the 64-bit key
 //      (round((a + b sqrt2) 2^24) << 28) | b, whose integer order is the order of
 //      the exact lengths (the rounding error < b / 2 units is far below the
-//      3.5e-4 * 2^24 gap), so relaxations are atomicMin's.  Four 256-thread
+//      3.5e-4 * 2^24 gap), so relaxations are atomicMin's.  Four 128-thread
 //      groups run the four source fields at once as Dial's algorithm with unit
 //      buckets on the exact length: bucket = floor(a + b sqrt2) = key >> 52
 //      (exact for b < 3400).  Every move costs >= 1, so a bucket's keys are final
@@ -45,7 +45,8 @@
 
 namespace cw {
 
-constexpr int RT_NT = 1024;
+constexpr int RT_NT = 512;    // 64 registers: two CTAs (two envs) per SM
+constexpr int RT_GT = RT_NT / 4;   // threads per geodesic field
 constexpr int RT_MAX = 8;                 // MAX_ROUTE_ANCHORS
 constexpr double kMinClear = 0.4;         // MIN_ANCHOR_CLEARANCE_M
 constexpr unsigned long long kNoDist = ~0ull;
@@ -87,7 +88,7 @@ CW_DEV int rt_excl_scan(int v, int* sh, int& total) {
       const int y = __shfl_up_sync(0xffffffffu, s, o);
       if (lane >= o) s += y;
     }
-    sh[lane] = s;
+    if (lane < RT_NT / 32) sh[lane] = s;
   }
   __syncthreads();
   total = sh[RT_NT / 32 - 1];
@@ -309,10 +310,10 @@ __device__ void route_env(const cw_scene_params& P, int e, const uint64_t* __res
   }
   __syncthreads();
   const int nf = traverse ? 1 : 4;
-  // fields: group g (256 threads) owns source g; Dial's buckets with atomicMin
+  // fields: group g (RT_GT threads) owns source g; Dial's buckets with atomicMin
   // keys, one named barrier (id 1 + g) per group; three rotating bucket lists of
   // N entries each (an entry per improving relaxation; overflow is reported)
-  const int g = tid >> 8, gt = tid & 255;
+  const int g = tid / RT_GT, gt = tid % RT_GT;
   __shared__ int s_fn[4][3];   // bucket list sizes
   __shared__ int s_ovf;
   if (tid == 0) s_ovf = 0;
@@ -322,8 +323,8 @@ __device__ void route_env(const cw_scene_params& P, int e, const uint64_t* __res
     const int cap = N;
     unsigned long long* LK = LKs + (size_t)g * 3 * N;
     int32_t* LC = LCs + (size_t)g * 3 * N;
-    for (int f = gt; f < N; f += 256) Fg[f] = kNoDist;
-    auto gsync = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory"); };
+    for (int f = gt; f < N; f += RT_GT) Fg[f] = kNoDist;
+    auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(RT_GT) : "memory"); };
     gsync();
     if (gt == 0) {
       const int f0 = cand[s_src[g]];
@@ -347,7 +348,7 @@ __device__ void route_env(const cw_scene_params& P, int e, const uint64_t* __res
         // move from bucket k lands in bucket k + 1, a diagonal one in k + 1 or k + 2)
         const int s1 = cur == 2 ? 0 : cur + 1, s2 = s1 == 2 ? 0 : s1 + 1;
         const unsigned lt = (1u << lane) - 1u;
-        for (int q0 = gt - lane; q0 < n_cur; q0 += 256) {
+        for (int q0 = gt - lane; q0 < n_cur; q0 += RT_GT) {
           const int q = q0 + lane;
           const bool live = q < n_cur;
           const int u = live ? Cc[q] : 0;
@@ -394,20 +395,20 @@ __device__ void route_env(const cw_scene_params& P, int e, const uint64_t* __res
       } else
       // items (entry, move) in batches of 4 per thread: the loads and atomics of a
       // batch are issued back to back; cells are packed (row << 16 | col)
-      for (int q0 = gt; q0 < n_cur * 8; q0 += 256 * 4) {
+      for (int q0 = gt; q0 < n_cur * 8; q0 += RT_GT * 4) {
         constexpr int BT = 4;
         int pu[BT], rv[BT], cv[BT], v[BT];
         unsigned long long kk[BT];
         bool ok[BT];
 #pragma unroll
         for (int i = 0; i < BT; ++i) {
-          const int q = q0 + i * 256;
+          const int q = q0 + i * RT_GT;
           pu[i] = q < n_cur * 8 ? Cc[q >> 3] : -1;
           kk[i] = q < n_cur * 8 ? Kc[q >> 3] : ~0ull;
         }
 #pragma unroll
         for (int i = 0; i < BT; ++i) {
-          const int d = (q0 + i * 256) & 7;
+          const int d = (q0 + i * RT_GT) & 7;
           ok[i] = false;
           v[i] = 0;
           rv[i] = cv[i] = 0;
@@ -562,7 +563,7 @@ __device__ void route_env(const cw_scene_params& P, int e, const uint64_t* __res
 // Persistent CTAs (one scratch slot each) take envs from a counter until all are
 // done: no launch-to-launch tails between env chunks.
 template <bool kMv>
-__global__ void __launch_bounds__(RT_NT, 1) k_routes(cw_scene_params P, int E, const uint64_t* __restrict__ scene_seeds,
+__global__ void __launch_bounds__(RT_NT, 2) k_routes(cw_scene_params P, int E, const uint64_t* __restrict__ scene_seeds,
                                                      const int32_t* slots, cw_scene_buffers B, double* routes,
                                                      int32_t* n_routes, unsigned char* scratch, int* counter) {
   __shared__ int s_e;

@@ -506,7 +506,7 @@ class SceneSampler:
         self.batch = SceneBatch(self.params, capacity, device)
 
     max_rows = 2048   # envs per cw_sample_scenes call (bounds the scratch footprint)
-    route_chunk = 296  # envs per route-anchor launch (2 CTAs per SM; 184 B/cell/env scratch)
+    route_chunk = int(os.environ.get("CW_ROUTE_CHUNK", 296))  # envs in flight in the route-anchor kernel (CTAs, 2 per SM; 184 B/cell/env scratch)
 
     def sample(self, scene_seeds, crowd_seeds=None, slots=None, stream=None, check=True):
         """Sample len(scene_seeds) scenes into rows ``slots`` (default 0..E-1).
