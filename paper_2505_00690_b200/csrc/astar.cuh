@@ -787,6 +787,8 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
   for (int i = threadIdx.x; i < NS; i += blockDim.x) E.free_ids[i] = (uint16_t)i;
   if (threadIdx.x == 0) { E.pool_lock[0] = 0; E.pool_lock[1] = NS; }
   __syncthreads();
+  // early commit: the commit pass (k_orca_ec) may start once every search CTA is here
+  if (!kRing && sp.mode == 1 && sp.pend) asm volatile("griddepcontrol.launch_dependents;");
   long long* const dbg = (!kRing && !spec && S.counters && S.counters[14])
                              ? reinterpret_cast<long long*>(S.counters[14]) : nullptr;
   long long* const trace = (!kRing && !spec && S.counters && S.counters[15])
@@ -806,11 +808,27 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
       R.start = __shfl_sync(0xffffffffu, R.start, 0);
       R.goal = __shfl_sync(0xffffffffu, R.goal, 0);
     } else if (spec) {
-      // a queued prediction is this warp's once its entry moves queued -> running
+      // take the next queued item (the late committers may still be adding some: poll
+      // until they are all done, bounded by kSpecIdle); a prediction is this warp's
+      // once its entry moves queued -> running
       int ok = 0;
       if (lane == 0) {
-        q = atomicAdd(&sp.qn[1], 1);
-        if (q < *(volatile int*)&sp.qn[0]) {
+        const long long idle0 = clock64();
+        q = -1;
+        while (true) {
+          const int taken = *(volatile int*)&sp.qn[1];
+          if (taken < ld_acquire_i32(&sp.qn[0])) {
+            if (atomicCAS(&sp.qn[1], taken, taken + 1) == taken) { q = taken; break; }
+            continue;
+          }
+          if (ld_acquire_i32(&sp.qn[3]) >= *(volatile int*)&sp.qn[2] &&
+              *(volatile int*)&sp.qn[1] >= ld_acquire_i32(&sp.qn[0]))
+            break;   // every producer is done and the queue is drained
+          if (clock64() - idle0 > kSpecIdle) break;
+          __nanosleep(512);
+        }
+        if (q >= 0) {
+          while (ld_acquire_i32(&sp.qr[q]) != (int)sp.tag) __nanosleep(64);   // item written
           R = sp.q[q];
           const unsigned long long t = sp.tag << 8;
           ok = atomicCAS(&sp.ent[(size_t)R.env * P.A + R.agent].word, t | kSpQueued, t | kSpRunning) ==
@@ -1024,6 +1042,13 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
       S.path_n[ia] = pn;
       S.waypoint[ia * 2] = wx;
       S.waypoint[ia * 2 + 1] = wy;
+    }
+    if (!kRing && !spec && sp.mode == 1 && sp.pend) {   // early commit: one search of env e less
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        atomicSub(&sp.pend[e], 1);
+      }
     }
     const int used_final = used;
     release();

@@ -443,7 +443,13 @@ struct SpecArgs {
   size_t rec_stride;
   unsigned long long tag;    // mode 2 / dry guide: this batch's tag
   unsigned long long* stats; // [1] hits, [2] waits on a running prediction, [3] claims
+  int* qr;                   // (E * A) per queue item: the tag once the item is written
+  int* pend;                 // mode 1 with early commit: (E) the tick's searches still running per env
 };
+// qn layout: [0] items queued, [1] items taken, [2] envs committing after their searches
+// (their dry guidance pass adds items later), [3] of those done; a batch's search warps
+// keep polling until [3] == [2] and the queue is drained (or kSpecIdle cycles pass).
+constexpr long long kSpecIdle = 1ll << 23;
 
 CW_DEV unsigned sm_id() {
   unsigned r;
@@ -483,6 +489,7 @@ CW_DEV void spec_request(const SpecArgs& sp, const AstarReq& R, size_t ia) {
   const int q = atomicAdd(&sp.qn[0], 1);
   sp.q[q] = R;
   __threadfence();
+  atomicExch(&sp.qr[q], (int)sp.tag);
   atomicExch(&en->word, (sp.tag << 8) | kSpQueued);
 }
 
@@ -496,12 +503,12 @@ CW_DEV void spec_request(const SpecArgs& sp, const AstarReq& R, size_t ia) {
 template <int NT, bool kRing, bool kDry = false>
 __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int e,
                          const uint8_t* __restrict__ env_mask, const RunArgs* ra,
-                         const SpecArgs* sp = nullptr) {
+                         const SpecArgs* sp = nullptr, bool force = false) {
   const int lane = threadIdx.x & 31;
   const int A = P.A;
   const size_t eA = (size_t)e * A;
   __shared__ int s_req;   // replans this env queued
-  if (kDry && S.env_req[e]) return 0;   // still searching this tick: not predicted
+  if (kDry && !force && S.env_req[e]) return 0;   // still searching this tick: predicted by its commit
   if (!kDry && env_mask && !env_mask[e]) {
     if (threadIdx.x == 0) S.env_req[e] = 0;
     return 0;
@@ -700,8 +707,13 @@ __global__ void __launch_bounds__(NT) k_guide_dry(cw_crowd_params P, cw_crowd_st
 
 template <int NT>
 __global__ void __launch_bounds__(NT) k_guide(cw_crowd_params P, cw_crowd_state S,
-                                              const uint8_t* __restrict__ env_mask) {
-  guide_env<NT, false>(P, S, blockIdx.x, env_mask, nullptr);
+                                              const uint8_t* __restrict__ env_mask, int* pend = nullptr,
+                                              int* n_late = nullptr) {
+  const int n = guide_env<NT, false>(P, S, blockIdx.x, env_mask, nullptr);
+  if (pend && threadIdx.x == 0) {   // early commit: the env's searches, and one more late committer
+    pend[blockIdx.x] = n;
+    if (n) atomicAdd(n_late, 1);
+  }
 }
 
 // ---------------------------------------------------------------- ORCA + commit
@@ -1196,6 +1208,8 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
   }
 }
 
+CW_DEV void orca_tail(const cw_crowd_params& P, const cw_crowd_state& S, int pass, bool pdl = false);
+
 template <int NT, bool kLanes = false>
 __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S,
                                              const double* __restrict__ robot_pos,
@@ -1209,8 +1223,49 @@ __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S
   // pass 2: envs with requests (after k_astar).  The body is per env.
   const bool skip = (pass == 1 && S.env_req[e]) || (pass == 2 && !S.env_req[e]);
   if (!skip) orca_env<NT, kLanes>(P, S, e, robot_pos, robot_vel, robot_radius, env_mask, bins, sm, nullptr, 0);
-  // ---------------- last CTA: publish last_gap_by_env (only when some row had K > 0),
-  // reset the per-step flags and the A* queue
+  orca_tail(P, S, pass);
+}
+
+// Early commit (next-tick prefetch): pass 2 launched beside k_astar (programmatic
+// dependent launch: its CTAs start once every search CTA is resident, so waiting here
+// can never keep a search from running).  The CTA of an env with replans waits for
+// the env's own searches only, commits it, and at once predicts its next replans
+// (dry guidance pass) into the prefetch batch, whose search warps are still polling.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_orca_ec(cw_crowd_params P, cw_crowd_state S,
+                                                const double* __restrict__ robot_pos,
+                                                const double* __restrict__ robot_vel, double robot_radius,
+                                                const uint8_t* __restrict__ env_mask, Bins bins, SpecArgs sa) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int e = blockIdx.x;
+  if (S.env_req[e]) {
+    if (threadIdx.x == 0) {
+      while (ld_acquire_i32(&sa.pend[e]) > 0) __nanosleep(256);
+      __threadfence();
+    }
+    __syncthreads();
+    orca_env<NT, false>(P, S, e, robot_pos, robot_vel, robot_radius, env_mask, bins, sm, nullptr, 0);
+    __syncthreads();
+    guide_env<NT, false, true>(P, S, e, nullptr, nullptr, &sa, true);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&sa.qn[3], 1);
+    }
+  }
+  orca_tail(P, S, 2, true);
+  // block 0 waits for the search grid: this grid (and so the stream) completes after
+  // it, and its request queue is reset only when no search warp can still touch it
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    S.flags[4] = 0;
+    S.flags[5] = 0;
+  }
+}
+
+// ---------------- last CTA: publish last_gap_by_env (only when some row had K > 0),
+// reset the per-step flags and the A* queue
+CW_DEV void orca_tail(const cw_crowd_params& P, const cw_crowd_state& S, int pass, bool pdl) {
   __shared__ int s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1230,8 +1285,10 @@ __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S
     if (threadIdx.x == 0) {
       S.flags[0] = 0;
       S.flags[2] = 0;
-      S.flags[4] = 0;
-      S.flags[5] = 0;
+      if (!pdl) {   // beside k_astar (k_orca_ec) its block 0 resets the queue instead
+        S.flags[4] = 0;
+        S.flags[5] = 0;
+      }
     }
   }
 }
@@ -1437,6 +1494,9 @@ struct SpecCtx {
   SpecEnt* ent = nullptr;
   int32_t* cells = nullptr;
   AstarReq* q[kSpecBatches] = {};
+  int* qr[kSpecBatches] = {};              // per item: batch tag once written
+  int* pend = nullptr;                     // (E) early commit: searches left per env
+  cudaEvent_t bdone[kSpecBatches] = {};    // the batch's search kernel is done
   int* qn = nullptr;                       // kSpecBatches x 4
   unsigned long long* stats = nullptr;     // 4
   unsigned char* rec = nullptr;
@@ -1474,8 +1534,9 @@ static size_t spec_layout(const cw_crowd_params& P, int nsm, size_t* parts) {
   parts[3] = up((size_t)kSpecBatches * 4 * 4 + 4 * 8);
   parts[4] = warps * astar_slot_stride(P.nx, P.ny);
   parts[5] = up(warps * (size_t)P.heap_cap * sizeof(OpenEnt));
+  parts[6] = up(EA * 4) * kSpecBatches + up((size_t)P.E * 4);   // item flags, pending counts
   size_t t = 0;
-  for (int k = 0; k < 6; ++k) t += parts[k];
+  for (int k = 0; k < 7; ++k) t += parts[k];
   return t;
 }
 
@@ -1492,6 +1553,8 @@ static SpecArgs spec_args(const SpecCtx* X, int mode, const int32_t* epoch, int 
   a.rec_stride = X->stride;
   a.tag = X->tag;
   a.stats = X->stats;
+  a.qr = X->qr[b];
+  a.pend = nullptr;
   return a;
 }
 
@@ -1786,31 +1849,66 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
       carve = true;
     }
     TickStreams& T = tick_streams();
-    k_guide<NT><<<P.E, NT, 0, st>>>(P, S, em);
-    cudaEventRecord(T.guided, st);
-    cudaStreamWaitEvent(T.hi, T.guided, 0);
-    cudaStreamWaitEvent(T.lo, T.guided, 0);
-    launch_astar(P, S, T.hi, X ? spec_args(X, 1, S.env_epoch, 0) : SpecArgs{});
-    k_orca<NT><<<P.E, NT, sm, T.lo>>>(P, S, rp, rv, rr, em, bins, 1);
-    k_orca<NT><<<P.E, NT, sm, T.hi>>>(P, S, rp, rv, rr, em, bins, 2);
-    cudaEventRecord(T.hi_done, T.hi);
-    cudaEventRecord(T.lo_done, T.lo);
-    if (X) {
-      // the committed envs' next tick: dry guidance, then its searches, on a side
-      // stream that the caller's stream does not join
-      const int b = X->next;
+    // a new prefetch batch when its slot's previous batch is done (else this tick only
+    // uses the cache); with one, the envs with replans commit as soon as their own
+    // searches finish and predict their next tick at once (early commit, k_orca_ec)
+    const int b = X ? X->next : 0;
+    const bool batch = X && cudaEventQuery(X->bdone[b]) == cudaSuccess;
+    static const bool no_ec = getenv("CW_PREFETCH_NO_EC") != nullptr;
+    const bool ec = batch && !no_ec;
+    SpecArgs sa{};
+    if (batch) {
       X->next = (b + 1) % kSpecBatches;
       ++X->tag;
       ++X->batches;
+      sa = spec_args(X, 2, S.env_epoch, b);
+      sa.pend = X->pend;   // read by k_orca_ec (the batch's search kernel ignores it)
+      cudaMemsetAsync(sa.qn, 0, 4 * sizeof(int), st);
+    }
+    k_guide<NT><<<P.E, NT, 0, st>>>(P, S, em, ec ? X->pend : nullptr, ec ? sa.qn + 2 : nullptr);
+    cudaEventRecord(T.guided, st);
+    cudaStreamWaitEvent(T.hi, T.guided, 0);
+    cudaStreamWaitEvent(T.lo, T.guided, 0);
+    SpecArgs look = X ? spec_args(X, 1, S.env_epoch, b) : SpecArgs{};
+    if (ec) look.pend = X->pend;
+    launch_astar(P, S, T.hi, look);
+    k_orca<NT><<<P.E, NT, sm, T.lo>>>(P, S, rp, rv, rr, em, bins, 1);
+    if (ec) {
+      static bool ec_attr = false;
+      if (!ec_attr) {
+        cudaFuncSetAttribute(k_orca_ec<NT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)cudaSharedmemCarveoutMaxShared);
+        ec_attr = true;
+      }
+      if (sm > 48 * 1024)
+        cudaFuncSetAttribute(k_orca_ec<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(P.E);
+      cfg.blockDim = dim3(NT);
+      cfg.dynamicSmemBytes = sm;
+      cfg.stream = T.hi;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, k_orca_ec<NT>, P, S, rp, rv, rr, em, bins, sa);
+    } else {
+      k_orca<NT><<<P.E, NT, sm, T.hi>>>(P, S, rp, rv, rr, em, bins, 2);
+    }
+    cudaEventRecord(T.hi_done, T.hi);
+    cudaEventRecord(T.lo_done, T.lo);
+    if (batch) {
+      // the committed envs' next tick: dry guidance, then the batch's searches (polling
+      // for the late committers' predictions), on a side stream the caller's does not join
       cudaStream_t ss = spec_stream(b);
-      const SpecArgs sa = spec_args(X, 2, S.env_epoch, b);
       cudaStreamWaitEvent(ss, T.lo_done, 0);
-      cudaMemsetAsync(sa.qn, 0, 4 * sizeof(int), ss);
       k_guide_dry<NT><<<P.E, NT, 0, ss>>>(P, S, sa);
       cudaEventRecord(X->guided, ss);
       const AstarShape A = astar_shape(P.nx, P.ny, kAstarWarps);
       const RunArgs none = {};
       k_astar<kAstarWarps, false><<<P.astar_ctas, 32 * kAstarWarps, A.smem, ss>>>(P, S, A.NC, A.NS, none, sa);
+      cudaEventRecord(X->bdone[b], ss);
     }
     cudaStreamWaitEvent(st, T.hi_done, 0);
     cudaStreamWaitEvent(st, T.lo_done, 0);
@@ -2014,7 +2112,7 @@ static int spec_nsm() {
 }
 
 size_t cw_spec_bytes(const cw_crowd_params* P) {
-  size_t parts[6];
+  size_t parts[7];
   const int nsm = spec_nsm();
   return nsm ? cw::spec_layout(*P, nsm, parts) : 0;
 }
@@ -2024,7 +2122,7 @@ int cw_spec_create(const cw_crowd_params* P, void** handle) {
   *handle = nullptr;
   const int nsm = spec_nsm();
   if (!nsm || P->E <= 0 || P->A <= 0) return (int)cudaErrorInvalidValue;
-  size_t parts[6];
+  size_t parts[7];
   const size_t total = spec_layout(*P, nsm, parts);
   unsigned char* base = nullptr;
   cudaError_t err = cudaMalloc(&base, total);
@@ -2042,12 +2140,21 @@ int cw_spec_create(const cw_crowd_params* P, void** handle) {
   X->stats = reinterpret_cast<unsigned long long*>(base + o + kSpecBatches * 4 * 4);
   o += parts[3];
   X->rec = base + o; o += parts[4];
-  X->heap = reinterpret_cast<OpenEnt*>(base + o);
+  X->heap = reinterpret_cast<OpenEnt*>(base + o); o += parts[5];
+  {
+    const size_t qrb = ((size_t)P->E * P->A * 4 + 255) & ~(size_t)255;
+    for (int b = 0; b < kSpecBatches; ++b) X->qr[b] = reinterpret_cast<int*>(base + o + b * qrb);
+    X->pend = reinterpret_cast<int*>(base + o + kSpecBatches * qrb);
+    cudaMemset(base + o, 0, parts[6]);
+  }
   X->stride = astar_slot_stride(P->nx, P->ny);
   cudaMemset(X->ent, 0, parts[0]);
   cudaMemset(X->qn, 0, parts[3]);
   cudaEventCreateWithFlags(&X->guided, cudaEventDisableTiming);
-  for (int b = 0; b < kSpecBatches; ++b) spec_stream(b);
+  for (int b = 0; b < kSpecBatches; ++b) {
+    spec_stream(b);
+    cudaEventCreateWithFlags(&X->bdone[b], cudaEventDisableTiming);
+  }
   err = cudaDeviceSynchronize();
   if (err != cudaSuccess) {
     cudaFree(base);
@@ -2065,6 +2172,7 @@ int cw_spec_destroy(void* handle) {
   for (int b = 0; b < kSpecBatches; ++b) cudaStreamSynchronize(spec_stream(b));
   cudaFree(X->ent);   // the base of the one allocation
   cudaEventDestroy(X->guided);
+  for (int b = 0; b < kSpecBatches; ++b) cudaEventDestroy(X->bdone[b]);
   delete X;
   return (int)cudaGetLastError();
 }
