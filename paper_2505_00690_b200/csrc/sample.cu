@@ -1108,13 +1108,25 @@ __global__ void __launch_bounds__(kStage ? 32 : 128) k_place(cw_scene_params P, 
   int placed = 0;
   bool overflow = false;
   const int count = P.obj_count;
-  for (int obj = 0; obj < count && !overflow; ++obj) {
-    bool ok = false;
-    for (int att = 0; att < P.attempts && !ok; ++att) {
+  // One try = (category, x, y, yaw) drawn by lane 0 (placement.py:95-105), then the
+  // warp tests it.  Tries are drawn in batches of up to 32 ahead and lane t computes
+  // try t's correctly rounded sin/cos (the bulk of a try's latency) for all of them at
+  // once.  A try's draws depend on the history only through the category rule (first
+  // or second half of the object's attempts); a batch is drawn assuming every try of
+  // it fails and stops at the half, so an accepted try (attempts restart at 0) leaves
+  // the later tries of the batch drawn exactly as they would have been.  Second-half
+  // tries are drawn one at a time.
+  const int half = P.attempts / 2;
+  int obj = 0, att = 0;
+  while (obj < count && !overflow) {
+    const int nb = att < half ? min(32, half - att) : 1;
+    int my_k = 0;
+    double my_x = 0.0, my_y = 0.0, my_yaw = 0.0;
+    for (int t = 0; t < nb; ++t) {
       int k = 0;
       double x = 0, y = 0, yaw = 0;
       if (lane == 0) {
-        if (att < P.attempts / 2) k = (int)integers32(rng, (uint64_t)P.n_cat);
+        if (att + t < half) k = (int)integers32(rng, (uint64_t)P.n_cat);
         else k = P.small_first[integers32(rng, (uint64_t)min(5, P.n_cat))];
         x = uniform(rng, 0.0, P.nx * P.res);
         y = uniform(rng, 0.0, P.ny * P.res);
@@ -1124,63 +1136,79 @@ __global__ void __launch_bounds__(kStage ? 32 : 128) k_place(cw_scene_params P, 
       x = __shfl_sync(0xffffffffu, x, 0);
       y = __shfl_sync(0xffffffffu, y, 0);
       yaw = __shfl_sync(0xffffffffu, yaw, 0);
-      const double fw = P.cat_w[k], fl = P.cat_l[k];
-      double cs, sn;
-      cr_sincos(yaw, &sn, &cs);   // correctly rounded: matches glibc (np.cos / np.sin) but in its rare misroundings
-      double cx[4], cy[4];
-      footprint_corners(fw, fl, x, y, cs, sn, cx, cy);
-      FootBox bb = footprint_box(P, cx, cy);
-      if (bb.empty) continue;
-      const int bw = bb.c1 - bb.c0 + 1, nb = bw * (bb.r1 - bb.r0 + 1);
-      bool bad = false, any = false;
-      for (int q = lane; q < nb; q += 32) {
-        int r = bb.r0 + q / bw, c = bb.c0 + q % bw;
-        if (!cell_inside(P, r, c, x, y, cs, sn, fw, fl)) continue;
-        any = true;
-        uint8_t z = zone_at((size_t)r * P.nx + c);
-        if (!((P.cat_zones[k] >> z) & 1u) || !region_ok(P, z, c)) bad = true;
-      }
-      any = __any_sync(0xffffffffu, any);
-      bad = __any_sync(0xffffffffu, bad);
-      if (!any) {
-        // degenerate small footprint: the centre cell (placement.py:54-58)
-        long long rc = trunc_ll(y / P.res), cc = trunc_ll(x / P.res);
-        if (!(rc >= 0 && rc < P.ny && cc >= 0 && cc < P.nx)) continue;
-        uint8_t z = zone_at((size_t)rc * P.nx + cc);
-        if (!((P.cat_zones[k] >> z) & 1u) || !region_ok(P, z, (int)cc)) continue;
-      } else if (bad) {
-        continue;
-      }
-      {  // stair tile under the pose (placement.py:120-124)
-        int tr = min(P.trows - 1, (int)trunc_ll(y / 2.0));
-        int tc = min(P.tcols - 1, (int)trunc_ll(x / 2.0));
-        int kind = TK[A[tr * P.tcols + tc]];
-        if (kind == K_STUP || kind == K_STDOWN) continue;
-      }
-      bool hit = false;
-      const double reach = P.cat_reach[k];
-      for (int j = lane; j < placed; j += 32) {
-        const double* o = cache + (size_t)j * 8;
-        const double ox = opose[j * 3 + 0], oy = opose[j * 3 + 1];
-        double rr = reach + P.cat_reach[ocat[j]];
-        double dx = x - ox, dy = y - oy;
-        if (dx * dx + dy * dy > rr * rr) continue;
-        if (sat_overlap(cx, cy, o, o + 4)) hit = true;
-      }
-      if (__any_sync(0xffffffffu, hit)) continue;
-      if (lane == 0) {
-        ocat[placed] = k;
-        opose[placed * 3 + 0] = x;
-        opose[placed * 3 + 1] = y;
-        opose[placed * 3 + 2] = yaw;
-        double* o = cache + (size_t)placed * 8;
-        for (int i = 0; i < 4; ++i) { o[i] = cx[i]; o[4 + i] = cy[i]; }
-      }
-      __syncwarp();
-      ++placed;
-      ok = true;
+      if (lane == t) { my_k = k; my_x = x; my_y = y; my_yaw = yaw; }
     }
-    if (!ok) overflow = true;
+    double my_cs, my_sn;
+    cr_sincos(my_yaw, &my_sn, &my_cs);   // correctly rounded: matches glibc (np.cos / np.sin) but in its rare misroundings
+    for (int j = 0; j < nb && obj < count; ++j) {
+      const int k = __shfl_sync(0xffffffffu, my_k, j);
+      const double x = __shfl_sync(0xffffffffu, my_x, j), y = __shfl_sync(0xffffffffu, my_y, j);
+      const double yaw = __shfl_sync(0xffffffffu, my_yaw, j);
+      const double cs = __shfl_sync(0xffffffffu, my_cs, j), sn = __shfl_sync(0xffffffffu, my_sn, j);
+      const double fw = P.cat_w[k], fl = P.cat_l[k];
+      double cx[4], cy[4];
+      bool ok = false;
+      do {   // one try (break = rejected)
+        footprint_corners(fw, fl, x, y, cs, sn, cx, cy);
+        FootBox bb = footprint_box(P, cx, cy);
+        if (bb.empty) break;
+        const int bw = bb.c1 - bb.c0 + 1, nbx = bw * (bb.r1 - bb.r0 + 1);
+        bool bad = false, any = false;
+        for (int q = lane; q < nbx; q += 32) {
+          int r = bb.r0 + q / bw, c = bb.c0 + q % bw;
+          if (!cell_inside(P, r, c, x, y, cs, sn, fw, fl)) continue;
+          any = true;
+          uint8_t z = zone_at((size_t)r * P.nx + c);
+          if (!((P.cat_zones[k] >> z) & 1u) || !region_ok(P, z, c)) bad = true;
+        }
+        any = __any_sync(0xffffffffu, any);
+        bad = __any_sync(0xffffffffu, bad);
+        if (!any) {
+          // degenerate small footprint: the centre cell (placement.py:54-58)
+          long long rc = trunc_ll(y / P.res), cc = trunc_ll(x / P.res);
+          if (!(rc >= 0 && rc < P.ny && cc >= 0 && cc < P.nx)) break;
+          uint8_t z = zone_at((size_t)rc * P.nx + cc);
+          if (!((P.cat_zones[k] >> z) & 1u) || !region_ok(P, z, (int)cc)) break;
+        } else if (bad) {
+          break;
+        }
+        {  // stair tile under the pose (placement.py:120-124)
+          int tr = min(P.trows - 1, (int)trunc_ll(y / 2.0));
+          int tc = min(P.tcols - 1, (int)trunc_ll(x / 2.0));
+          int kind = TK[A[tr * P.tcols + tc]];
+          if (kind == K_STUP || kind == K_STDOWN) break;
+        }
+        bool hit = false;
+        const double reach = P.cat_reach[k];
+        for (int jj = lane; jj < placed; jj += 32) {
+          const double* o = cache + (size_t)jj * 8;
+          const double ox = opose[jj * 3 + 0], oy = opose[jj * 3 + 1];
+          double rr = reach + P.cat_reach[ocat[jj]];
+          double dx = x - ox, dy = y - oy;
+          if (dx * dx + dy * dy > rr * rr) continue;
+          if (sat_overlap(cx, cy, o, o + 4)) hit = true;
+        }
+        if (__any_sync(0xffffffffu, hit)) break;
+        ok = true;
+      } while (false);
+      if (ok) {
+        if (lane == 0) {
+          ocat[placed] = k;
+          opose[placed * 3 + 0] = x;
+          opose[placed * 3 + 1] = y;
+          opose[placed * 3 + 2] = yaw;
+          double* o = cache + (size_t)placed * 8;
+          for (int i = 0; i < 4; ++i) { o[i] = cx[i]; o[4 + i] = cy[i]; }
+        }
+        __syncwarp();
+        ++placed;
+        ++obj;
+        att = 0;
+      } else if (++att >= P.attempts) {
+        overflow = true;
+        break;
+      }
+    }
   }
   if (lane == 0) {
     B.obj_n[slot] = placed;
