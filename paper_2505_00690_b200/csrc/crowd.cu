@@ -1488,7 +1488,7 @@ static void launch_astar(const cw_crowd_params& P, const cw_crowd_state& S, cuda
 // finishing a search the next tick waits for while the following batch starts.
 // Scratch is indexed by (SM, warp): a search CTA needs more than half of an SM's
 // shared memory, so no two are ever resident on one SM.
-constexpr int kSpecBatches = 3;
+constexpr int kSpecBatches = 8;
 struct SpecCtx {
   int E = 0, A = 0, path_cap = 0, heap_cap = 0, nx = 0, ny = 0, nsm = 0;
   SpecEnt* ent = nullptr;
@@ -1849,11 +1849,11 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
       carve = true;
     }
     TickStreams& T = tick_streams();
-    // a new prefetch batch when its slot's previous batch is done (else this tick only
-    // uses the cache); with one, the envs with replans commit as soon as their own
-    // searches finish and predict their next tick at once (early commit, k_orca_ec)
+    // a new prefetch batch every tick (its slot's previous batch, eight ticks back, is
+    // waited for on the device: normally long done); the envs with replans commit as soon
+    // as their own searches finish and predict their next tick at once (early commit)
     const int b = X ? X->next : 0;
-    const bool batch = X && cudaEventQuery(X->bdone[b]) == cudaSuccess;
+    const bool batch = X != nullptr;
     static const bool no_ec = getenv("CW_PREFETCH_NO_EC") != nullptr;
     const bool ec = batch && !no_ec;
     SpecArgs sa{};
@@ -1863,6 +1863,7 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
       ++X->batches;
       sa = spec_args(X, 2, S.env_epoch, b);
       sa.pend = X->pend;   // read by k_orca_ec (the batch's search kernel ignores it)
+      cudaStreamWaitEvent(st, X->bdone[b], 0);
       cudaMemsetAsync(sa.qn, 0, 4 * sizeof(int), st);
     }
     k_guide<NT><<<P.E, NT, 0, st>>>(P, S, em, ec ? X->pend : nullptr, ec ? sa.qn + 2 : nullptr);
