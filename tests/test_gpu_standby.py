@@ -1,0 +1,62 @@
+"""Asynchronous scene sampling for per-tick re-sampling (envcore.SceneStandby): a reset
+that installs the row's standby scene (sampled ahead on a side stream with the seeds the
+reset would use) must leave exactly the state that re-sampling at the reset leaves --
+scenes, route anchors, spawned crowds and the crowd ticks that follow."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SCENE = ("labels", "elev", "nearest", "walk_n", "moves", "reach", "obj_pose", "obj_n", "routes", "n_routes",
+         "sp_pos", "sp_goal", "scene_seed")
+CROWD = ("pos_t", "vel_t", "goal_t", "waypoint_t", "path_n_t", "last_gap_t")
+
+
+def _world(E):
+    import torch
+    import bench
+    from paper_2505_00690_b200.crowd import CrowdConfig, CrowdField
+    from paper_2505_00690_b200.rng import child_seeds_device
+    from paper_2505_00690_b200.urbangen import SceneSampler
+    bench.CFG.clear()
+    bench.CFG.update(bench.CONFIGS["cfg5"])
+    zero = torch.zeros(E, dtype=torch.int64, device="cuda")
+    env = child_seeds_device(zero, "env", torch.arange(E, device="cuda"))
+    s = SceneSampler(bench.make_spec(), E)
+    s.sample(env, child_seeds_device(env, "crowd", 0))
+    seeds = [int(x) for x in child_seeds_device(env, "crowd-run").cpu().numpy().view(np.uint64)]
+    f = CrowdField(s.batch, CrowdConfig(neighbor_distance=bench.CFG["nd"]), seeds)
+    f.set_from_spawn(s.batch)
+    return s, f, env, torch.zeros(E, dtype=torch.int64, device="cuda")
+
+
+def test_standby_resets_equal_resampling(torch_cuda):
+    import torch
+    from paper_2505_00690_b200.envcore import SceneStandby
+    from paper_2505_00690_b200.rng import child_seeds_device
+    E = 48
+    sa, fa, env, ca = _world(E)      # re-samples at each reset
+    sb, fb, _, cb = _world(E)        # installs standby scenes
+    standby = SceneStandby(sb, env, cb)
+    rng = np.random.default_rng(5)
+    for k in range(25):
+        rows = np.flatnonzero(rng.random(E) < 0.12)
+        if k % 6 == 1:
+            rows = np.union1d(rows, [3])   # a row reset again while its next scene may still be sampling
+        if rows.size:
+            sl = torch.from_numpy(rows).to("cuda")
+            ca[sl] += 1
+            cb[sl] += 1
+            sa.sample(child_seeds_device(env[sl], "resample", ca[sl]), child_seeds_device(env[sl], "crowd", ca[sl]),
+                      slots=sl)
+            standby.take(rows)
+            fa.set_from_spawn(sa.batch, rows=sl)
+            fb.set_from_spawn(sb.batch, rows=sl)
+        fa.step()
+        fb.step()
+        for name in SCENE:
+            assert torch.equal(getattr(sa.batch, name), getattr(sb.batch, name)), (k, name)
+        for name in CROWD:
+            assert torch.equal(getattr(fa, name), getattr(fb, name)), (k, name)
+    sb.batch.check_status()
