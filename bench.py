@@ -261,13 +261,13 @@ def run_ours(args):
         if CFG["resample"] > 0 and masks[k].size:
             sl = torch.from_numpy(masks[k]).to(dev)
             counts[sl] += 1
-            if standby is not None:   # the rows' next scenes, sampled ahead on a side stream
-                standby.take(masks[k])
+            if standby is not None:   # the rows' next scenes (and first replans) sampled ahead
+                standby.take(masks[k])   # + set_from_spawn
             else:
                 env_k = env_seeds[sl]
                 new_scene = child_seeds_device(env_k, "resample", counts[sl])
                 sampler.sample(new_scene, child_seeds_device(env_k, "crowd", counts[sl]), slots=sl, check=False)
-            f.set_from_spawn(b, rows=sl)
+                f.set_from_spawn(b, rows=sl)
             resampled += int(masks[k].size)
 
     # ---- value: ticks W .. W+K from spawn through CrowdField.run (the same ticks,
@@ -330,7 +330,7 @@ def run_ours(args):
     # the pool's initial fill (every row's next scene) is setup, outside the timed regions
     if CFG["resample"] > 0 and not args.no_standby:
         from paper_2505_00690_b200.envcore import SceneStandby
-        standby = SceneStandby(sampler, env_seeds, counts)
+        standby = SceneStandby(sampler, env_seeds, counts, field=f)
         torch.cuda.synchronize()
 
     # ---- synchronous tick (CrowdField.step, barrier per tick), L2 flushed between ticks

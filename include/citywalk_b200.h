@@ -228,6 +228,14 @@ int cw_spec_destroy(void* handle);
 /* counters: [0] batches launched, plus per-context device totals read back on demand:
  * [1] cache hits, [2] waits on a running prediction, [3] claims of a queued one */
 int cw_spec_stats(void* handle, long long* out4);
+/* Asynchronous scene sampling (envcore.SceneStandby): predict and search, into `handle`,
+ * the first-tick replans of freshly spawned rows `rows` (state S as set_from_spawn leaves
+ * it, grids of the standby batch); then, when those scenes are installed into another
+ * batch, copy the finished predictions into that batch's context (generations remapped). */
+int cw_spec_predict(const cw_crowd_params* params, const cw_crowd_state* state, void* handle,
+                    const int32_t* rows, int n_rows, int threads, void* stream);
+int cw_spec_install(void* dst, void* src, const int32_t* dst_epoch, const int32_t* src_epoch,
+                    const int32_t* rows, int n_rows, void* stream);
 
 int cw_crowd_step(const cw_crowd_params* params, const cw_crowd_state* state,
                   const double* robot_pos, const double* robot_vel, double robot_radius,

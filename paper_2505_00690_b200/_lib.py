@@ -108,7 +108,8 @@ EXPORTS = ["cw_scene_seed_scratch_bytes", "cw_sample_scenes", "cw_sample_scenes_
            "cw_scene_rle", "cw_crowd_run_scratch_bytes", "cw_crowd_run",
            "cw_crowd_run_rounds", "cw_crowd_run_servers", "cw_crowd_run_window", "cw_sample_routes", "cw_connected_components",
            "cw_rasterize", "cw_orca_lp", "cw_orca_halfplanes", "cw_crowd_constraints", "cw_trig_probe",
-           "cw_spec_bytes", "cw_spec_create", "cw_spec_destroy", "cw_spec_stats"]
+           "cw_spec_bytes", "cw_spec_create", "cw_spec_destroy", "cw_spec_stats", "cw_spec_predict",
+           "cw_spec_install"]
 
 _lib = None
 
@@ -192,6 +193,11 @@ def lib():
     L.cw_spec_create.argtypes = [ctypes.POINTER(CrowdParams), ctypes.POINTER(ctypes.c_void_p)]
     L.cw_spec_destroy.restype = ctypes.c_int
     L.cw_spec_destroy.argtypes = [ctypes.c_void_p]
+    L.cw_spec_predict.restype = ctypes.c_int
+    L.cw_spec_predict.argtypes = [ctypes.POINTER(CrowdParams), ctypes.POINTER(CrowdState), ctypes.c_void_p, P,
+                                  ctypes.c_int, ctypes.c_int, P]
+    L.cw_spec_install.restype = ctypes.c_int
+    L.cw_spec_install.argtypes = [ctypes.c_void_p, ctypes.c_void_p, P, P, P, ctypes.c_int, P]
     L.cw_spec_stats.restype = ctypes.c_int
     L.cw_spec_stats.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_longlong)]
     L.cw_crowd_run.restype = ctypes.c_int

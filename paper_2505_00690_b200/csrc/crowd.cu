@@ -701,8 +701,53 @@ __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
 
 // The dry guidance pass over the envs that committed without a replan this tick.
 template <int NT>
-__global__ void __launch_bounds__(NT) k_guide_dry(cw_crowd_params P, cw_crowd_state S, SpecArgs sp) {
-  guide_env<NT, false, true>(P, S, blockIdx.x, nullptr, nullptr, &sp);
+__global__ void __launch_bounds__(NT) k_guide_dry(cw_crowd_params P, cw_crowd_state S, SpecArgs sp,
+                                                  const int32_t* rows = nullptr) {
+  if (rows) guide_env<NT, false, true>(P, S, rows[blockIdx.x], nullptr, nullptr, &sp, true);
+  else guide_env<NT, false, true>(P, S, blockIdx.x, nullptr, nullptr, &sp);
+}
+
+// Install the predictions of context `src` for rows (all agents) into context `dst`:
+// an entry of src that is done for the row's current src generation is copied with
+// dst's generation of the row (the caller has just installed the same grid there);
+// a dst entry a prediction is still running into is left alone (the tick searches it).
+__global__ void k_spec_install(int A, int path_cap, SpecEnt* __restrict__ dent, int32_t* __restrict__ dcells,
+                               const SpecEnt* __restrict__ sent, const int32_t* __restrict__ scells,
+                               const int32_t* __restrict__ depoch, const int32_t* __restrict__ sepoch,
+                               const int32_t* __restrict__ rows, unsigned long long tag) {
+  const int e = rows[blockIdx.x];
+  const int lane = threadIdx.x & 31;
+  for (int a = threadIdx.x >> 5; a < A; a += blockDim.x >> 5) {
+    const size_t ia = (size_t)e * A + a;
+    const SpecEnt* se = sent + ia;
+    SpecEnt* de = dent + ia;
+    int ok = 0, cnt = 0;
+    if (lane == 0) {
+      const unsigned long long sw = *(volatile const unsigned long long*)&se->word;
+      ok = (int)(sw & 0xFFull) == kSpDone && *(volatile const int*)&se->epoch == sepoch[e];
+      if (ok) {
+        const unsigned long long dw = *(volatile unsigned long long*)&de->word;
+        const int ds = (int)(dw & 0xFFull);
+        ok = ds != kSpRunning && ds != kSpWriting && atomicCAS(&de->word, dw, (tag << 8) | kSpWriting) == dw;
+      }
+      if (ok) cnt = se->found == 1 && !se->over ? se->count : 0;
+    }
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    cnt = __shfl_sync(0xffffffffu, cnt, 0);
+    if (!ok) continue;
+    for (int k = path_cap - cnt + lane; k < path_cap; k += 32) dcells[ia * path_cap + k] = scells[ia * path_cap + k];
+    __syncwarp();
+    if (lane == 0) {
+      de->start = se->start;
+      de->goal = se->goal;
+      de->count = se->count;
+      de->found = se->found;
+      de->over = se->over;
+      de->epoch = depoch[e];
+      __threadfence();
+      atomicExch(&de->word, (tag << 8) | kSpDone);
+    }
+  }
 }
 
 template <int NT>
@@ -1908,7 +1953,9 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
       cudaEventRecord(X->guided, ss);
       const AstarShape A = astar_shape(P.nx, P.ny, kAstarWarps);
       const RunArgs none = {};
-      k_astar<kAstarWarps, false><<<P.astar_ctas, 32 * kAstarWarps, A.smem, ss>>>(P, S, A.NC, A.NS, none, sa);
+      static const double share = getenv("CW_SPEC_SHARE") ? atof(getenv("CW_SPEC_SHARE")) : 1.0;
+      const int ctas = std::max(1, std::min(P.astar_ctas, (int)(P.astar_ctas * share)));
+      k_astar<kAstarWarps, false><<<ctas, 32 * kAstarWarps, A.smem, ss>>>(P, S, A.NC, A.NS, none, sa);
       cudaEventRecord(X->bdone[b], ss);
     }
     cudaStreamWaitEvent(st, T.hi_done, 0);
@@ -2175,6 +2222,57 @@ int cw_spec_destroy(void* handle) {
   cudaEventDestroy(X->guided);
   for (int b = 0; b < kSpecBatches; ++b) cudaEventDestroy(X->bdone[b]);
   delete X;
+  return (int)cudaGetLastError();
+}
+
+// Predict and search, into context `handle`, the first-tick replans of freshly spawned
+// rows (standby scenes; state S as a spawn leaves it: no paths) -- all on `stream`.
+int cw_spec_predict(const cw_crowd_params* P, const cw_crowd_state* S, void* handle, const int32_t* rows,
+                    int n_rows, int threads, void* stream) {
+  using namespace cw;
+  if (!handle || !S->env_epoch) return (int)cudaErrorInvalidValue;
+  if (n_rows <= 0) return 0;
+  SpecCtx* X = static_cast<SpecCtx*>(handle);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int b = X->next;
+  X->next = (b + 1) % kSpecBatches;
+  ++X->tag;
+  ++X->batches;
+  const SpecArgs sa = spec_args(X, 2, S->env_epoch, b);
+  cudaStreamWaitEvent(st, X->bdone[b], 0);
+  cudaMemsetAsync(sa.qn, 0, 4 * sizeof(int), st);
+  if (threads == 256) k_guide_dry<256><<<n_rows, 256, 0, st>>>(*P, *S, sa, rows);
+  else if (threads == 64) k_guide_dry<64><<<n_rows, 64, 0, st>>>(*P, *S, sa, rows);
+  else k_guide_dry<128><<<n_rows, 128, 0, st>>>(*P, *S, sa, rows);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_astar<kAstarWarps, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_astar<kAstarWarps, false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    attr = true;
+  }
+  const AstarShape A = astar_shape(P->nx, P->ny, kAstarWarps);
+  const RunArgs none = {};
+  // background work: a share of the SMs only, so the ticks' own searches always find some
+  static const double share = getenv("CW_STANDBY_SHARE") ? atof(getenv("CW_STANDBY_SHARE")) : 0.5;
+  const int ctas = std::max(1, std::min(P->astar_ctas, (int)(P->astar_ctas * share)));
+  k_astar<kAstarWarps, false><<<ctas, 32 * kAstarWarps, A.smem, st>>>(*P, *S, A.NC, A.NS, none, sa);
+  cudaEventRecord(X->bdone[b], st);
+  return (int)cudaGetLastError();
+}
+
+// Copy context `src`'s finished predictions for `rows` into context `dst` (see
+// k_spec_install); dst_epoch / src_epoch: the two contexts' grid generations (E).
+int cw_spec_install(void* dst, void* src, const int32_t* dst_epoch, const int32_t* src_epoch, const int32_t* rows,
+                    int n_rows, void* stream) {
+  using namespace cw;
+  if (!dst || !src) return (int)cudaErrorInvalidValue;
+  if (n_rows <= 0) return 0;
+  SpecCtx* D = static_cast<SpecCtx*>(dst);
+  SpecCtx* Sx = static_cast<SpecCtx*>(src);
+  if (D->E != Sx->E || D->A != Sx->A || D->path_cap != Sx->path_cap) return (int)cudaErrorInvalidValue;
+  k_spec_install<<<n_rows, 256, 0, (cudaStream_t)stream>>>(D->A, D->path_cap, D->ent, D->cells, Sx->ent, Sx->cells,
+                                                         dst_epoch, src_epoch, rows, ++D->tag);
   return (int)cudaGetLastError();
 }
 

@@ -333,9 +333,15 @@ class SceneStandby:
     ``sampler``: the main SceneSampler (its batch receives the scenes); ``env_seeds``
     (E,) int64 device tensor; ``counts`` (E,) int64 device tensor of reset counts, read
     when a standby is sampled (the caller increments it at each reset, as BatchedEnv
-    does)."""
+    does).  With ``field`` (the CrowdField over the main batch, next-tick prefetch on),
+    the first tick's replans of every standby crowd are predicted and searched on the
+    side stream as well (cw_spec_predict: the first guidance pass after a spawn depends
+    only on the spawn and the grid) and installed with the scene (cw_spec_install), so a
+    re-sampled env's first tick finds its searches done.  ``take`` then also respawns
+    the rows' crowds (``field.set_from_spawn``)."""
 
-    def __init__(self, sampler, env_seeds, counts):
+    def __init__(self, sampler, env_seeds, counts, field=None):
+        import ctypes
         import torch
         b = sampler.batch
         self.main, self.env, self.counts = sampler, env_seeds, counts
@@ -343,9 +349,41 @@ class SceneStandby:
         self.pool = SceneSampler(sampler.spec, b.E, catalog=sampler.catalog, device=self.device,
                                  routes=sampler.routes)
         self.side = torch.cuda.Stream(device=self.device)
+        self.pred = torch.cuda.Stream(device=self.device)   # first-tick predictions (never waited for)
         self.events = []                               # one per sampling launch
         self.row_launch = np.full(b.E, -1, dtype=np.int64)
+        self.field = field
+        self._spec = None
+        if field is not None and field.prefetch and field.A > 0:
+            field.prepare_step()
+            pb = self.pool.batch
+            E, A = field.E, field.A
+            d = self.device
+            # the crowd state a spawn leaves (set_from_spawn) over the standby grids
+            self._pool_keep = dict(active=torch.ones((E, A), dtype=torch.uint8, device=d),
+                                   path_n=torch.zeros((E, A), dtype=torch.int32, device=d),
+                                   env_req=torch.zeros((E,), dtype=torch.uint8, device=d))
+            st = _lib.CrowdState()
+            m = dict(pos=pb.sp_pos, goal=pb.sp_goal, waypoint=pb.sp_goal, vel=pb.sp_goal, active=self._pool_keep["active"],
+                     path_cells=field.path_cells_t, path_head=self._pool_keep["path_n"],
+                     path_n=self._pool_keep["path_n"], labels=pb.labels, nearest=pb.nearest, has_obs=pb.has_obs,
+                     walk=pb.walk, walk_n=pb.walk_n, reach=pb.reach, moves=pb.moves, env_req=self._pool_keep["env_req"],
+                     env_epoch=pb.epoch)
+            for k, v in m.items():
+                setattr(st, k, v.data_ptr())
+            self._pool_state = st
+            self._params = field._params()
+            h = ctypes.c_void_p()
+            _lib.check(_lib.lib().cw_spec_create(self._params, ctypes.byref(h)), "cw_spec_create")
+            self._spec = h.value
         self._launch(np.arange(b.E))
+
+    def __del__(self):
+        try:
+            if self._spec:
+                _lib.lib().cw_spec_destroy(self._spec)
+        except Exception:
+            pass
 
     def _launch(self, rows):
         import torch
@@ -356,10 +394,19 @@ class SceneStandby:
             cnt = self.counts[sl] + 1
             self.pool.sample(child_seeds_device(env_k, "resample", cnt), child_seeds_device(env_k, "crowd", cnt),
                              slots=sl, stream=self.side, check=False)
+            rows32 = sl.to(torch.int32)
             ev = torch.cuda.Event()
             ev.record(self.side)
         self.row_launch[rows] = len(self.events)
         self.events.append(ev)
+        if self._spec:
+            # on their own stream: a take waits for the scenes only and installs the
+            # predictions finished by then (a later rewrite of a row changes its generation)
+            self.pred.wait_event(ev)
+            rows32.record_stream(self.pred)
+            _lib.check(_lib.lib().cw_spec_predict(self._params, self._pool_state, self._spec, _lib.ptr(rows32),
+                                                  len(rows), self.field.threads, _lib.stream_ptr(self.pred)),
+                       "cw_spec_predict")
 
     def take(self, rows):
         """Install the standby scenes of ``rows`` (whose reset count was just incremented)
@@ -374,6 +421,14 @@ class SceneStandby:
         dst, src = self.main.batch, self.pool.batch
         for name in _scene_out_fields():
             getattr(dst, name).index_copy_(0, sl, getattr(src, name).index_select(0, sl))
+        f = self.field
+        if f is not None:
+            f.set_from_spawn(dst, rows=sl)
+            if self._spec and f._spec_handle():
+                rows32 = sl.to(torch.int32)
+                _lib.check(_lib.lib().cw_spec_install(f._spec_h, self._spec, _lib.ptr(f.epoch_t),
+                                                      _lib.ptr(self.pool.batch.epoch), _lib.ptr(rows32), len(rows),
+                                                      _lib.stream_ptr()), "cw_spec_install")
         self._launch(rows)
 
 

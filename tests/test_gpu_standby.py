@@ -31,14 +31,17 @@ def _world(E):
     return s, f, env, torch.zeros(E, dtype=torch.int64, device="cuda")
 
 
-def test_standby_resets_equal_resampling(torch_cuda):
+@pytest.mark.parametrize("with_field", [False, True])
+def test_standby_resets_equal_resampling(with_field, torch_cuda):
+    """with_field: the standby crowds' first-tick searches are predicted on the side and
+    installed into the field's prefetch cache with the scene (hits counted)."""
     import torch
     from paper_2505_00690_b200.envcore import SceneStandby
     from paper_2505_00690_b200.rng import child_seeds_device
     E = 48
     sa, fa, env, ca = _world(E)      # re-samples at each reset
     sb, fb, _, cb = _world(E)        # installs standby scenes
-    standby = SceneStandby(sb, env, cb)
+    standby = SceneStandby(sb, env, cb, field=fb if with_field else None)
     rng = np.random.default_rng(5)
     for k in range(25):
         rows = np.flatnonzero(rng.random(E) < 0.12)
@@ -52,7 +55,10 @@ def test_standby_resets_equal_resampling(torch_cuda):
                       slots=sl)
             standby.take(rows)
             fa.set_from_spawn(sa.batch, rows=sl)
-            fb.set_from_spawn(sb.batch, rows=sl)
+            if not with_field:
+                fb.set_from_spawn(sb.batch, rows=sl)
+        if k % 5 == 0:
+            torch.cuda.synchronize()   # let some standby predictions finish before their reset
         fa.step()
         fb.step()
         for name in SCENE:
@@ -60,3 +66,5 @@ def test_standby_resets_equal_resampling(torch_cuda):
         for name in CROWD:
             assert torch.equal(getattr(fa, name), getattr(fb, name)), (k, name)
     sb.batch.check_status()
+    if with_field:
+        assert fb.stats()["prefetch_hits"] > fa.stats()["prefetch_hits"]
