@@ -76,7 +76,7 @@ class BatchedEnv:
     identities are ``scene_hashes`` either way."""
 
     def __init__(self, specs, scheme, master_seed, k=None, cache=None, config=None,
-                 env_seeds=None, device="cuda", threads=128, catalog=None):
+                 env_seeds=None, device="cuda", threads=128, catalog=None, standby=False):
         import torch
         self.config = config or EnvConfig()
         self.scheme = Scheme(scheme)
@@ -125,6 +125,13 @@ class BatchedEnv:
                                 reach_threshold_m=self.config.reach_threshold_m,
                                 reward=self.config.reward, device=self.device)
         self._spawn(np.arange(k))
+        # standby: every slot's next scene (and its crowd's first replans) sampled ahead on
+        # side streams, so resample() installs instead of sampling (SceneStandby)
+        self.standby = None
+        if standby and self.scheme == Scheme.ASYNC:
+            self.counts_t = torch.zeros(k, dtype=torch.int64, device=self.device)
+            self.standby = SceneStandby(self.sampler, self.env_seeds_t, self.counts_t,
+                                        field=self.crowd if self.spec.pedestrian_count > 0 else None)
 
     # -- stacks (batch.py:132-150) ----------------------------------------------------
     @property
@@ -166,13 +173,22 @@ class BatchedEnv:
         env = self.env_seeds_t[sl]
         cnt = torch.from_numpy(self.reset_counts[slots]).to(self.device)
         new_scene = child_seeds_device(env, "resample", cnt)
-        crowd_seed = child_seeds_device(env, "crowd", cnt)
         self.scene_seeds_t[sl] = new_scene
-        self.sampler.sample(new_scene, crowd_seed, slots=sl)
+        if self.standby is not None and (respawn or self.spec.pedestrian_count == 0):
+            self.counts_t[sl] += 1
+            self.standby.take(slots)   # installs the scenes (+ set_from_spawn of their crowds)
+            self.batch.check_status(sl)
+        else:
+            if self.standby is not None:
+                self.counts_t[sl] += 1
+            crowd_seed = child_seeds_device(env, "crowd", cnt)
+            self.sampler.sample(new_scene, crowd_seed, slots=sl)
+            if respawn and self.spec.pedestrian_count > 0:
+                self.crowd.set_from_spawn(self.batch, rows=sl)
+            if self.standby is not None:
+                self.standby._launch(slots)   # the rows' standby is now their next-but-one
         for i in slots:
             self._scene_hashes[int(i)] = None
-        if respawn and self.spec.pedestrian_count > 0:
-            self.crowd.set_from_spawn(self.batch, rows=sl)
         self.crowd.prepare_step()
         if hasattr(self, "robot"):
             self.robot.refresh_passable(slots)

@@ -68,3 +68,31 @@ def test_standby_resets_equal_resampling(with_field, torch_cuda):
     sb.batch.check_status()
     if with_field:
         assert fb.stats()["prefetch_hits"] > fa.stats()["prefetch_hits"]
+
+
+def test_batched_env_standby_equals_resampling(torch_cuda):
+    """BatchedEnv(standby=True): resample() installs scenes sampled ahead; trajectories,
+    scenes and crowds equal the synchronous re-sampling ones (resets on purpose close
+    together, including a slot reset twice in a row)."""
+    import torch
+    from paper_2505_00690_b200.envcore import BatchedEnv, Scheme
+    from paper_2505_00690_b200.urbangen import SceneSpec, TaskKind
+    spec = SceneSpec(seed=0, extent_m=(16.0, 16.0), task_kind=TaskKind.NAV_DYNAMIC, pedestrian_count=6)
+    K = 12
+    envs = [BatchedEnv(spec, Scheme.ASYNC, master_seed=7, k=K, standby=sb) for sb in (False, True)]
+    rng = np.random.default_rng(2)
+    for t in range(40):
+        if t % 4 == 1:
+            slots = rng.choice(K, 3, replace=False)
+            if t % 8 == 1:
+                slots = np.union1d(slots, [4])
+            for env in envs:
+                env.resample(slots)
+        act = rng.uniform(-1, 1, (K, 2))
+        for env in envs:
+            env.step_batch(act)
+        a, b = envs
+        assert np.array_equal(np.stack([a.x, a.y, a.vx, a.vy]), np.stack([b.x, b.y, b.vx, b.vy])), t
+        assert torch.equal(a.batch.labels, b.batch.labels), t
+        assert torch.equal(a.crowd.pos_t, b.crowd.pos_t), t
+    assert a.scene_hashes == b.scene_hashes
