@@ -114,7 +114,7 @@ class CrowdField:
         self.threads = threads
         self.run_threads = None   # cw_crowd_run CTA size; None: one lane per agent
         self.run_history_bytes = 256 << 20   # per-call cap of the run's (env, tick) gap history
-        self.run_server_warps = None   # search warps per server CTA in cw_crowd_run (None: 2)
+        self.run_server_warps = None   # search warps per server CTA in cw_crowd_run (None: by round footprint, crowd.cu launch_run)
         self.astar_warps = astar_warps
         if isinstance(occupancies, SceneBatch):
             b = occupancies

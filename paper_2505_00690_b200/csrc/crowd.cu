@@ -1756,9 +1756,31 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
   // server's warps wait on the rounds' requests: they must never starve them).
   // two search warps per CTA: twice the concurrent searches of the latency shape
   // at nearly its per-expansion cost (the run is bound by each env's own chain)
+  // Default server shape by round footprint (bench.py steady state, B200, round 2):
+  //  * 32-thread lane-path rounds (A <= 32): 2 warps, 220 KB (cfg2: 0.29 ms/tick; 4 warps 0.32)
+  //  * wider lane-path rounds (A <= 128): 4 warps, 200 KB -- three round CTAs fit beside
+  //    the server (cfg3: 2.45 -> 1.90 ms/tick; 4 warps at 220 KB 2.52, 2 warps at 180 KB 2.53)
+  //  * warp-path rounds (A >= 128, binned neighbours; cfg4 ~86 KB per round CTA): 4 warps and
+  //    a pool small enough that one round CTA fits beside the server, 8 SMs left without a
+  //    server -- at 220 KB the rounds had only the margin SMs (cfg4: 42.2 -> 24.2 ms/tick;
+  //    pools of 80 / 120 / 139 KB within 3 %)
+  //  An explicit run_server_warps (the re-sampling windows: 4, search-heavy catch-up) keeps
+  //  220 KB and the 1/8 margin.
+  int w_def = 2, kb_def = 0, margin_auto = 0;
+  if (!P.run_server_warps) {
+    if (!lanes_ok) {
+      w_def = 4;
+      kb_def = std::min(100, 227 - (int)((sm + 1023) / 1024) - 3);
+      margin_auto = 8;
+    } else if (NT >= 64) {
+      w_def = 4;
+      kb_def = 200;
+    }
+  }
   static const int srv_w_env = getenv("CW_RUN_SERVER_W") ? atoi(getenv("CW_RUN_SERVER_W")) : 0;
-  const int srv_w = srv_w_env ? srv_w_env : (P.run_server_warps ? P.run_server_warps : 2);
-  static const int srv_kb = getenv("CW_RUN_SERVER_KB") ? atoi(getenv("CW_RUN_SERVER_KB")) : 0;
+  const int srv_w = srv_w_env ? srv_w_env : (P.run_server_warps ? P.run_server_warps : w_def);
+  static const int srv_kb_env = getenv("CW_RUN_SERVER_KB") ? atoi(getenv("CW_RUN_SERVER_KB")) : 0;
+  const int srv_kb = srv_kb_env ? srv_kb_env : kb_def;
   AstarShape shp = astar_shape(P.nx, P.ny, srv_w == 4 ? kAstarWarps : srv_w == 2 ? 2 : 1, srv_kb);
   shp.NS = std::min(shp.NS, astar_ns_cap(P.nx, P.ny));   // the global store holds NS slot ids
   static const int margin = getenv("CW_RUN_MARGIN") ? atoi(getenv("CW_RUN_MARGIN")) : 0;
@@ -1766,7 +1788,7 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
   // (A <= 32), which are light enough to run beside the server everywhere -- measured
   // at cfg2: margin 4 / 8 / 18 = 0.289 / 0.296 / 0.309 ms/tick; at cfg3 (64-thread
   // rounds) and cfg4 (256-thread warp-path rounds) a margin of 8 was 14 % / 2x slower
-  const int margin_def = (lanes_ok && NT == 32) ? 4 : P.astar_ctas / 8;
+  const int margin_def = margin_auto ? margin_auto : (lanes_ok && NT == 32) ? 4 : P.astar_ctas / 8;
   int srv_ctas = P.astar_ctas - std::max(4, margin > 0 ? margin : margin_def);
   if (const char* v = getenv("CW_RUN_SERVER_CTAS")) srv_ctas = std::min(srv_ctas, atoi(v));
   srv_ctas = std::max(srv_ctas, 1);
