@@ -201,6 +201,173 @@ CW_DEV void grid_components(volatile int32_t* par, int nx, int ny, OkF ok) {
   __syncthreads();
 }
 
+// Connected components by flood fill on row-aligned bitmaps in shared memory
+// (WPR = ceil(nx / 32) words per row; U = ok cells not yet labelled, C = the component
+// being grown).  Components are taken in increasing order of their smallest cell (the
+// first set bit of U), grown from it by dilation within U to the fixpoint -- a pass
+// re-evaluates the 3 x 3 word neighbourhoods of the words that grew in the previous
+// pass (a worklist; a word's runs fill at once) -- and labelled with that cell's
+// index: the same output as grid_components (par[f] = smallest flat index of f's
+// component, -1 where !ok) without global-memory pointer chasing.  A word is claimed
+// by one thread per pass, so C only grows; a word can only grow after a neighbour
+// did, so an empty worklist is the fixpoint.
+CW_HD int bm_words(int nx, int ny) { return ((nx + 31) >> 5) * ny; }
+constexpr size_t kBmCompMax = 100 * 1024;
+// dynamic shared memory of bitmap_components (U, C, the claim bitmap Q, two u16 word
+// lists), 0 when it exceeds kBmCompMax or the word ids need more than 16 bits (the
+// union-find path runs then)
+CW_HD size_t bmcomp_smem_bytes(int nx, int ny) {
+  const size_t n = (size_t)bm_words(nx, ny);
+  const size_t b = n * 8 + ((n + 31) / 32) * 4 + ((n * 2 * 2 + 15) & ~(size_t)15);
+  return (b <= kBmCompMax && n <= 65536) ? b : 0;
+}
+
+template <int NT, bool CONN8, typename OkF>
+CW_DEV void bitmap_components(int32_t* par, int nx, int ny, OkF ok, uint32_t* U) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int WPR = (nx + 31) >> 5, NWR = WPR * ny;
+  uint32_t* C = U + NWR;
+  uint32_t* Q = C + NWR;                                       // words claimed this pass
+  uint16_t* L = reinterpret_cast<uint16_t*>(Q + (NWR + 31) / 32);   // two lists of NWR
+  for (int i = threadIdx.x; i < (NWR + 31) / 32; i += NT) Q[i] = 0u;
+  __shared__ int s_w0, s_lo, s_hi, s_n[2];
+  for (int w = wid; w < NWR; w += NW) {   // warp per word, coalesced
+    const int r = w / WPR, c = (w - r * WPR) * 32 + lane;
+    const bool o = c < nx && ok(r * nx + c);
+    const unsigned b = __ballot_sync(0xffffffffu, o);
+    if (c < nx && !o) par[r * nx + c] = -1;
+    if (lane == 0) { U[w] = b; C[w] = 0u; }
+  }
+  if (threadIdx.x == 0) s_w0 = NWR;
+  __syncthreads();
+  // one word of row r: dilate C around it (rows r-1..r+1, neighbour words' edge bits),
+  // keep the ok bits, fill along the word's runs; true if C grew
+  auto step = [&](int r, int cw) -> bool {
+    const int w = r * WPR + cw;
+    const unsigned u = U[w];
+    if (!u) return false;
+    auto hd = [&](int ww) -> unsigned {
+      const unsigned x = C[ww];
+      const unsigned l = cw > 0 ? C[ww - 1] : 0u, rt = cw + 1 < WPR ? C[ww + 1] : 0u;
+      return x | (x << 1) | (l >> 31) | (x >> 1) | (rt << 31);
+    };
+    const unsigned cur = C[w];
+    unsigned d = hd(w);
+    if (CONN8) {
+      if (r > 0) d |= hd(w - WPR);
+      if (r + 1 < ny) d |= hd(w + WPR);
+    } else {
+      if (r > 0) d |= C[w - WPR];
+      if (r + 1 < ny) d |= C[w + WPR];
+    }
+    const unsigned x = (d & u) | cur;
+    if (x == cur) return false;
+    unsigned g = u, y = x;   // parallel-prefix fill, both directions
+    y |= (y << 1) & g; g &= g << 1;
+    y |= (y << 2) & g; g &= g << 2;
+    y |= (y << 4) & g; g &= g << 4;
+    y |= (y << 8) & g; g &= g << 8;
+    y |= (y << 16) & g;
+    unsigned h = u, z = x;
+    z |= (z >> 1) & h; h &= h >> 1;
+    z |= (z >> 2) & h; h &= h >> 2;
+    z |= (z >> 4) & h; h &= h >> 4;
+    z |= (z >> 8) & h; h &= h >> 8;
+    z |= (z >> 16) & h;
+    C[w] = y | z;
+    return true;
+  };
+  int cursor = 0;   // every word before it is empty in U
+  while (true) {
+    for (int w = cursor + (int)threadIdx.x; w < NWR; w += NT)
+      if (U[w]) { atomicMin(&s_w0, w); break; }
+    __syncthreads();
+    const int w0 = s_w0;
+    if (w0 >= NWR) break;
+    const int r0 = w0 / WPR;
+    const unsigned bit0 = (unsigned)__ffs(U[w0]) - 1u;
+    const int id = r0 * nx + (w0 - r0 * WPR) * 32 + (int)bit0;
+    cursor = w0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      C[w0] = 1u << bit0;
+      L[0] = (uint16_t)w0;
+      s_n[0] = 1;
+      s_n[1] = 0;
+      s_lo = s_hi = r0;
+      s_w0 = NWR;
+    }
+    __syncthreads();
+    // grow to the fixpoint: a pass evaluates the 3 x 3 word neighbourhoods of the words
+    // that grew in the previous pass, each word once (claimed in Q)
+    for (int p = 0;; p ^= 1) {
+      const int n_in = s_n[p];
+      const uint16_t* Lin = L + (size_t)p * NWR;
+      uint16_t* Lout = L + (size_t)(p ^ 1) * NWR;
+      int rmin = ny, rmax = -1;
+      for (int i = threadIdx.x; i < n_in * 9; i += NT) {
+        const int e = Lin[i / 9], k = i % 9;
+        const int er = e / WPR;
+        const int r = er + k / 3 - 1, cw = e - er * WPR + k % 3 - 1;
+        if (r < 0 || r >= ny || cw < 0 || cw >= WPR) continue;
+        const int wn = r * WPR + cw;
+        const unsigned bit = 1u << (wn & 31);
+        if (atomicOr(&Q[wn >> 5], bit) & bit) continue;
+        if (step(r, cw)) {
+          Lout[atomicAdd(&s_n[p ^ 1], 1)] = (uint16_t)wn;
+          rmin = min(rmin, r);
+          rmax = max(rmax, r);
+          // chase the growth up and down the word column in this pass (rows are the
+          // slow direction: a word boundary within a row is one pass, a row is one)
+          for (int dir = -1; dir <= 1; dir += 2) {
+            for (int rr = r + dir; rr >= 0 && rr < ny; rr += dir) {
+              const int wc = rr * WPR + cw;
+              const unsigned bc = 1u << (wc & 31);
+              if (atomicOr(&Q[wc >> 5], bc) & bc) break;
+              if (!step(rr, cw)) break;
+              Lout[atomicAdd(&s_n[p ^ 1], 1)] = (uint16_t)wc;
+              rmin = min(rmin, rr);
+              rmax = max(rmax, rr);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        rmin = min(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
+        rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+      }
+      if (lane == 0 && rmax >= 0) { atomicMin(&s_lo, rmin); atomicMax(&s_hi, rmax); }
+      __syncthreads();
+      const int n_out = s_n[p ^ 1];
+      for (int i = threadIdx.x; i < (NWR + 31) / 32; i += NT) Q[i] = 0u;   // release the claims
+      if (threadIdx.x == 0) s_n[p] = 0;
+      __syncthreads();
+      if (n_out == 0) break;
+    }
+    const int lo = s_lo, hi = s_hi;
+    for (int w = lo * WPR + wid; w < (hi + 1) * WPR; w += NW) {
+      const unsigned b = C[w];
+      if (!b) continue;
+      const int r = w / WPR, c = (w - r * WPR) * 32 + lane;
+      if ((b >> lane) & 1u) par[r * nx + c] = id;
+      __syncwarp();
+      if (lane == 0) { U[w] &= ~b; C[w] = 0u; }
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+}
+
+// bitmap_components when the caller has the shared bitmaps (bm != nullptr), else the
+// global-memory union-find
+template <int NT, bool CONN8, typename OkF>
+CW_DEV void components(int32_t* par, int nx, int ny, OkF ok, uint32_t* bm) {
+  if (bm) bitmap_components<NT, CONN8>(par, nx, ny, ok, bm);
+  else grid_components<NT, CONN8>((volatile int32_t*)par, nx, ny, ok);
+}
+
 // ================================================================= k_seeds
 __global__ void k_seeds(int E, const uint64_t* __restrict__ scene_seed,
                         const uint64_t* __restrict__ crowd_seed, EnvSeeds* __restrict__ out) {
@@ -1498,8 +1665,17 @@ __global__ void __launch_bounds__(1024) k_reach(cw_scene_params P, int E, const 
   if (B.status[slot] != CW_OK) return;
   const int nx = P.nx, N = nx * P.ny;
   const uint8_t* Lb = B.labels + (size_t)slot * N;
-  volatile int32_t* R = B.reach + (size_t)slot * N;
-  grid_components<1024, false>(R, nx, P.ny, [&](int f) { return Lb[f] != L_OBSTACLE; });
+  int32_t* R = B.reach + (size_t)slot * N;
+  extern __shared__ uint32_t reach_bm[];   // bmcomp_smem_bytes(nx, ny) (0: union-find)
+  components<1024, false>(R, nx, P.ny, [&](int f) { return Lb[f] != L_OBSTACLE; },
+                          bmcomp_smem_bytes(nx, P.ny) ? reach_bm : nullptr);
+}
+
+static void launch_reach(const cw_scene_params& p, int E, const int32_t* slots, const cw_scene_buffers& b,
+                         cudaStream_t st) {
+  const size_t bm = bmcomp_smem_bytes(p.nx, p.ny);
+  if (bm > 48 * 1024) cudaFuncSetAttribute(k_reach, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bm);
+  k_reach<<<E, 1024, bm, st>>>(p, E, slots, b);
 }
 
 // ================================================================= spawn + routes
@@ -1542,7 +1718,7 @@ constexpr int ORD_BATCH = SP_NT;
 
 // k_spawn dynamic shared memory: accepted starts (2 x A doubles) + the candidate bitmap
 CW_HD size_t spawn_smem_bytes(int A, int nx, int ny) {
-  return (size_t)A * 2 * sizeof(double) + (((size_t)nx * ny + 31) / 32) * 4;
+  return (size_t)A * 2 * sizeof(double) + (((size_t)nx * ny + 31) / 32) * 4 + bmcomp_smem_bytes(nx, ny);
 }
 
 CW_DEV int resolve_final(int k, const int32_t* jj, const int32_t* head, const int32_t* nxt) {
@@ -1636,7 +1812,8 @@ __global__ void __launch_bounds__(SP_NT) k_spawn(cw_scene_params P, int E, const
   }
   // 8-connected components (routes.py:14-32); only label equality is used
   // downstream (routes.py:62, 74), so any labelling works.
-  grid_components<SP_NT, true>(comp, nx, ny, [&](int f) { return ((s_ok[f >> 5] >> (f & 31)) & 1u) != 0u; });
+  components<SP_NT, true>(comp, nx, ny, [&](int f) { return ((s_ok[f >> 5] >> (f & 31)) & 1u) != 0u; },
+                          bmcomp_smem_bytes(nx, ny) ? s_ok + NW32 : nullptr);
   // component sizes: one atomic per (warp, component) -- nearly every candidate is
   // in the same component, so per-candidate atomics serialise on one address
   for (int q0 = 0; q0 < n; q0 += SP_NT) {
@@ -1887,9 +2064,11 @@ __global__ void __launch_bounds__(1024) k_components(int nx, int ny, const uint8
   const int e = blockIdx.x;
   const int N = nx * ny;
   const uint8_t* okb = ok + (size_t)e * N;
-  volatile int32_t* par = comp + (size_t)e * N;
+  int32_t* par = comp + (size_t)e * N;
   int32_t* rk = rank + (size_t)e * N;
-  grid_components<1024, true>(par, nx, ny, [&](int f) { return okb[f] != 0; });
+  extern __shared__ uint32_t comp_bm[];   // bmcomp_smem_bytes(nx, ny) (0: union-find)
+  components<1024, true>(par, nx, ny, [&](int f) { return okb[f] != 0; },
+                         bmcomp_smem_bytes(nx, ny) ? comp_bm : nullptr);
   __shared__ int sh[1024 / 32 + 1];
   int base = 0;
   for (int f0 = 0; f0 < N; f0 += 1024) {
@@ -2031,7 +2210,7 @@ static int sample_impl(const cw_scene_params* P, int E, const uint64_t* scene_se
     k_nearest<<<E, BFS_NT, nsm, ss.s[0]>>>(p, E, slots, b);
   }
   k_walk<<<E, 1024, 0, ss.s[1]>>>(p, E, slots, b);
-  k_reach<<<E, 1024, 0, ss.s[1]>>>(p, E, slots, b);
+  launch_reach(p, E, slots, b, ss.s[1]);
   if (p.peds > 0) {
     size_t sm = spawn_smem_bytes(p.peds, p.nx, p.ny);
     if (sm > 32 * 1024) cudaFuncSetAttribute(k_spawn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -2102,7 +2281,9 @@ int cw_sample_routes(const cw_scene_params* P, int E, const uint64_t* route_seed
 int cw_connected_components(int nx, int ny, int E, const uint8_t* ok, int32_t* comp, int32_t* rank_scratch,
                             void* stream) {
   if (E <= 0 || nx <= 0 || ny <= 0) return 0;
-  cw::k_components<<<E, 1024, 0, (cudaStream_t)stream>>>(nx, ny, ok, comp, rank_scratch);
+  const size_t bm = cw::bmcomp_smem_bytes(nx, ny);
+  if (bm > 48 * 1024) cudaFuncSetAttribute(cw::k_components, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bm);
+  cw::k_components<<<E, 1024, bm, (cudaStream_t)stream>>>(nx, ny, ok, comp, rank_scratch);
   return (int)cudaGetLastError();
 }
 
@@ -2140,7 +2321,7 @@ int cw_prepare_envs(const cw_scene_params* P, int E, const int32_t* slots,
   if (nsm > 32 * 1024) cudaFuncSetAttribute(k_nearest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nsm);
   k_nearest<<<E, BFS_NT, nsm, st>>>(*P, E, slots, *B);
   k_walk<<<E, 1024, 0, st>>>(*P, E, slots, *B);
-  k_reach<<<E, 1024, 0, st>>>(*P, E, slots, *B);
+  launch_reach(*P, E, slots, *B, st);
   return (int)cudaGetLastError();
 }
 
