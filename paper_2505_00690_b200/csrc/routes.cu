@@ -174,7 +174,11 @@ CW_HD size_t route_smem_bytes(int nx, int ny, bool mv) {
   const size_t N = (size_t)nx * ny;
   return ((N + 31) / 32) * 4 + (mv ? ((N + 15) & ~(size_t)15) : 0);
 }
-constexpr size_t kRouteMvSmem = 100 * 1024;   // above: bitmap only, (entry, move) per thread
+// above: bitmap only, (entry, move) per thread.  Measured (B200, round 2): at 256^2 the
+// bitmap-only path is faster (k_routes 13.3 -> 12.2 ms per 1024 cfg2 envs: 8 KB instead of
+// 72 KB of shared memory leaves the L1 to the list / key traffic); at 128^2 the move
+// table is 2 % faster.
+constexpr size_t kRouteMvSmem = 32 * 1024;
 
 // One env on the whole CTA (scratch `base` is the CTA's slot).
 template <bool kMv>
@@ -198,17 +202,14 @@ __device__ void route_env(const cw_scene_params& P, int e, const uint64_t* __res
   int32_t* okl = cand + N;
   double* D = reinterpret_cast<double*>(F);                                      // chamfer (field 0)
   const int NW = (N + 31) / 32;
-  for (int w = tid; w < NW; w += RT_NT) {
-    uint32_t bits = 0;
-    for (int b = 0; b < 32; ++b) {
-      const int f = w * 32 + b;
-      if (f < N && lab[f] == L_WALKABLE) bits |= 1u << b;
-    }
-    s_walk[w] = bits;
+  for (int w = wid; w < NW; w += RT_NT / 32) {   // warp per word: coalesced label reads
+    const int f = w * 32 + lane;
+    const unsigned bits = __ballot_sync(0xffffffffu, f < N && lab[f] == L_WALKABLE);
+    if (lane == 0) s_walk[w] = bits;
   }
+  uint8_t* s_mv = reinterpret_cast<uint8_t*>(s_walk + NW);
   __syncthreads();
   auto walk = [&](int r, int c) { return (s_walk[(r * nx + c) >> 5] >> ((r * nx + c) & 31)) & 1u; };
-  uint8_t* s_mv = reinterpret_cast<uint8_t*>(s_walk + NW);
   if (kMv) {
     for (int f = tid; f < N; f += RT_NT) {
       const int r = f / nx, c = f - r * nx;
