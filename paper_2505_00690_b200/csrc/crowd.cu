@@ -37,6 +37,17 @@ struct ConsT {
 };
 using WarpCons = ConsT<MAXC>;
 
+// x / h, as a multiplication when h is a power of two (the default horizons 2 s and
+// 1 s): x * 2^-k and x / 2^k are the correctly rounded values of the same real number,
+// so the result is bit-identical and a long double-precision division leaves the chain.
+CW_DEV double div_h(double x, double h) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(h);
+  const unsigned long long ex = (b >> 52) & 0x7FFull;
+  if ((b & 0x800FFFFFFFFFFFFFull) == 0ull && ex >= 1ull && ex <= 2045ull)
+    return x * __longlong_as_double((long long)((2046ull - ex) << 52));
+  return x / h;
+}
+
 // ---------------------------------------------------------------- VO half-plane
 // field.py:448-495 for one lane (the selected branch of the vectorised where()).
 CW_DEV void vo_halfplane(double rp0, double rp1, double rv0, double rv1, double rr, double horizon,
@@ -62,14 +73,14 @@ CW_DEV void vo_halfplane(double rp0, double rp1, double rv0, double rv1, double 
     u0 = k * uc0; u1 = k * uc1;
     n0 = uc0; n1 = uc1;
   } else {
-    double w0 = rv0 - rp0 / horizon, w1 = rv1 - rp1 / horizon;
+    double w0 = rv0 - div_h(rp0, horizon), w1 = rv1 - div_h(rp1, horizon);
     double wlsq = w0 * w0 + w1 * w1;
     double d1 = w0 * rp0 + w1 * rp1;
     if (d1 < 0.0 && d1 * d1 > rsq * wlsq) {
       double wl = sqrt(wlsq);
       double s = fmax(wl, kEps);
       double uw0 = w0 / s, uw1 = w1 / s;
-      double k = rr / horizon - wl;
+      double k = div_h(rr, horizon) - wl;
       u0 = k * uw0; u1 = k * uw1;
       n0 = uw0; n1 = uw1;
     } else {
