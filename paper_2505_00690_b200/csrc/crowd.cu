@@ -645,7 +645,7 @@ __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
       }
       // _line_of_sight (field.py:601-610), 32 samples per step
       double d = glibc_hypot(sgx - spx, sgy - spy);
-      long long ns = max(2LL, trunc_ll(2.0 * d / res) + 2);
+      long long ns = max(2LL, trunc_ll(div_h(2.0 * d, res)) + 2);
       if (kDry) ns = min(ns, 4LL * (nx + ny) + 2);   // torn reads must not run away
       double step = 1.0 / (double)(ns - 1);
       bool clear = true;
@@ -656,8 +656,8 @@ __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
           ++los_read;
           double t = k == ns - 1 ? 1.0 : (double)k * step + 0.0;
           double xs = spx + (sgx - spx) * t, ys = spy + (sgy - spy) * t;
-          long long rr = clampll(trunc_ll(ys / res), 0, ny - 1);
-          long long cc = clampll(trunc_ll(xs / res), 0, nx - 1);
+          long long rr = clampll(trunc_ll(div_h(ys, res)), 0, ny - 1);
+          long long cc = clampll(trunc_ll(div_h(xs, res)), 0, nx - 1);
           blocked = lab[rr * nx + cc] == L_OBSTACLE;
         }
         clear = !__any_sync(0xffffffffu, blocked);
@@ -671,10 +671,10 @@ __device__ int guide_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
             S.waypoint[sia * 2 + 1] = sgy;
           }
         } else {
-          int sr = (int)fmin(fmax(spy / res, 0.0), (double)(ny - 1));
-          int sc = (int)fmin(fmax(spx / res, 0.0), (double)(nx - 1));
-          int gr = (int)fmin(fmax(sgy / res, 0.0), (double)(ny - 1));
-          int gc = (int)fmin(fmax(sgx / res, 0.0), (double)(nx - 1));
+          int sr = (int)fmin(fmax(div_h(spy, res), 0.0), (double)(ny - 1));
+          int sc = (int)fmin(fmax(div_h(spx, res), 0.0), (double)(nx - 1));
+          int gr = (int)fmin(fmax(div_h(sgy, res), 0.0), (double)(ny - 1));
+          int gc = (int)fmin(fmax(div_h(sgx, res), 0.0), (double)(nx - 1));
           AstarReq R = {e, sa, sr * nx + sc, gr * nx + gc};
           if (kDry) {
             spec_request(*sp, R, sia);
@@ -912,6 +912,14 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
         if (a >= A || !s_act[a]) continue;
         const double px = s_px[a], py = s_py[a];
         const size_t ia = eA + a;
+        // the static lane's nearest-obstacle cell, loaded first (a dependent random read
+        // that the neighbour selection below hides)
+        int flat_pre = -1;
+        if (P.use_static && has_obs) {
+          const long long ri = clampll(trunc_ll(div_h(py, res)), 0, ny - 1);
+          const long long ci = clampll(trunc_ll(div_h(px, res)), 0, nx - 1);
+          flat_pre = S.nearest[e * N + ri * nx + ci];
+        }
         const double gx = S.goal[ia * 2], gy = S.goal[ia * 2 + 1];
         const double wx = S.waypoint[ia * 2], wy = S.waypoint[ia * 2 + 1];
         const double sp = S.pref_speed[ia];
@@ -1000,9 +1008,7 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
           }
         }
         if (P.use_static && has_obs) {
-          long long ri = clampll(trunc_ll(py / res), 0, ny - 1);
-          long long ci = clampll(trunc_ll(px / res), 0, nx - 1);
-          int flat = S.nearest[e * N + ri * nx + ci];
+          const int flat = flat_pre;
           if (flat >= 0) {
             int orow = flat / nx, ocol = flat - orow * nx;
             double rp0 = ((double)ocol + 0.5) * res - px, rp1 = ((double)orow + 0.5) * res - py;
@@ -1033,8 +1039,8 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
         }
         double npx = px + v0 * P.dt, npy = py + v1 * P.dt;
         bool out = npx < 0 || npy < 0 || npx >= nx * res || npy >= ny * res;
-        long long rr = clampll(trunc_ll(npy / res), 0, ny - 1);
-        long long cc = clampll(trunc_ll(npx / res), 0, nx - 1);
+        long long rr = clampll(trunc_ll(div_h(npy, res)), 0, ny - 1);
+        long long cc = clampll(trunc_ll(div_h(npx, res)), 0, nx - 1);
         bool blocked = out || lab[rr * nx + cc] == L_OBSTACLE;
         if (!blocked) {
           S.pos[ia * 2] = npx;
@@ -1151,8 +1157,8 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
         }
       }
       if (P.use_static && has_obs) {
-        long long ri = clampll(trunc_ll(py / res), 0, ny - 1);
-        long long ci = clampll(trunc_ll(px / res), 0, nx - 1);
+        long long ri = clampll(trunc_ll(div_h(py, res)), 0, ny - 1);
+        long long ci = clampll(trunc_ll(div_h(px, res)), 0, nx - 1);
         int flat = S.nearest[e * N + ri * nx + ci];
         if (flat >= 0) {
           int orow = flat / nx, ocol = flat - orow * nx;
@@ -1185,8 +1191,8 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
       // ---------------- commit (field.py:152-160, 352-366)
       double npx = px + v0 * P.dt, npy = py + v1 * P.dt;
       bool out = npx < 0 || npy < 0 || npx >= nx * res || npy >= ny * res;
-      long long rr = clampll(trunc_ll(npy / res), 0, ny - 1);
-      long long cc = clampll(trunc_ll(npx / res), 0, nx - 1);
+      long long rr = clampll(trunc_ll(div_h(npy, res)), 0, ny - 1);
+      long long cc = clampll(trunc_ll(div_h(npx, res)), 0, nx - 1);
       bool blocked = out || lab[rr * nx + cc] == L_OBSTACLE;
       if (lane == 0) {
         if (!blocked) {
@@ -2149,8 +2155,8 @@ __global__ void k_crowd_constraints(cw_crowd_params P, cw_crowd_state S, int e0,
     double ox = 0.0, oy = 0.0;
     bool has = false;
     if (S.has_obs[e]) {
-      const long long ri = clampll(trunc_ll(py / res), 0, ny - 1);
-      const long long ci = clampll(trunc_ll(px / res), 0, nx - 1);
+      const long long ri = clampll(trunc_ll(div_h(py, res)), 0, ny - 1);
+      const long long ci = clampll(trunc_ll(div_h(px, res)), 0, nx - 1);
       const int flat = S.nearest[e * N + ri * nx + ci];
       has = flat >= 0;
       const int f = max(flat, 0);
