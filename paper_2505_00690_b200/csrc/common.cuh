@@ -62,6 +62,18 @@ CW_DEV double glibc_hypot(double x, double y) {
 // Python int(x) / numpy astype(int64) truncation of a finite double.
 CW_DEV long long trunc_ll(double x) { return (long long)x; }
 
+// x / h, as a multiplication when h is a power of two (the default horizons 2 s / 1 s,
+// grid resolutions 0.125 / 0.25 m): x * 2^-k and x / 2^k are the correctly rounded
+// values of the same real number, so the result is bit-identical and a long
+// double-precision division leaves the dependency chain.
+CW_DEV double div_h(double x, double h) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(h);
+  const unsigned long long ex = (b >> 52) & 0x7FFull;
+  if ((b & 0x800FFFFFFFFFFFFFull) == 0ull && ex >= 1ull && ex <= 2045ull)
+    return x * __longlong_as_double((long long)((2046ull - ex) << 52));
+  return x / h;
+}
+
 CW_DEV long long clampll(long long v, long long lo, long long hi) {
   return v < lo ? lo : (v > hi ? hi : v);
 }

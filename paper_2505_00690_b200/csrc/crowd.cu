@@ -37,17 +37,6 @@ struct ConsT {
 };
 using WarpCons = ConsT<MAXC>;
 
-// x / h, as a multiplication when h is a power of two (the default horizons 2 s and
-// 1 s): x * 2^-k and x / 2^k are the correctly rounded values of the same real number,
-// so the result is bit-identical and a long double-precision division leaves the chain.
-CW_DEV double div_h(double x, double h) {
-  const unsigned long long b = (unsigned long long)__double_as_longlong(h);
-  const unsigned long long ex = (b >> 52) & 0x7FFull;
-  if ((b & 0x800FFFFFFFFFFFFFull) == 0ull && ex >= 1ull && ex <= 2045ull)
-    return x * __longlong_as_double((long long)((2046ull - ex) << 52));
-  return x / h;
-}
-
 // ---------------------------------------------------------------- VO half-plane
 // field.py:448-495 for one lane (the selected branch of the vectorised where()).
 CW_DEV void vo_halfplane(double rp0, double rp1, double rv0, double rv1, double rr, double horizon,

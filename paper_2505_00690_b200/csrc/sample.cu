@@ -40,10 +40,10 @@ struct Rect { int r0, r1, c0, c1; };
 CW_DEV Rect rect_bounds(const cw_scene_params& P, double x0, double y0, double x1, double y1) {
   // gridmath.py:59-69
   Rect R;
-  R.c0 = (int)max(0LL, (long long)ceil(x0 / P.res - 0.5));
-  R.c1 = (int)min((long long)P.nx, (long long)ceil(x1 / P.res - 0.5));
-  R.r0 = (int)max(0LL, (long long)ceil(y0 / P.res - 0.5));
-  R.r1 = (int)min((long long)P.ny, (long long)ceil(y1 / P.res - 0.5));
+  R.c0 = (int)max(0LL, (long long)ceil(div_h(x0, P.res) - 0.5));
+  R.c1 = (int)min((long long)P.nx, (long long)ceil(div_h(x1, P.res) - 0.5));
+  R.r0 = (int)max(0LL, (long long)ceil(div_h(y0, P.res) - 0.5));
+  R.r1 = (int)min((long long)P.ny, (long long)ceil(div_h(y1, P.res) - 0.5));
   return R;
 }
 CW_DEV bool rect_nonempty(const Rect& a) { return a.c1 > a.c0 && a.r1 > a.r0; }
@@ -1174,10 +1174,10 @@ CW_DEV FootBox footprint_box(const cw_scene_params& P, const double* cx, const d
     y0 = fmin(y0, cy[i]); y1 = fmax(y1, cy[i]);
   }
   FootBox b;
-  b.c0 = (int)max(0LL, trunc_ll(x0 / P.res) - 1);
-  b.c1 = (int)min((long long)P.nx - 1, trunc_ll(x1 / P.res) + 1);
-  b.r0 = (int)max(0LL, trunc_ll(y0 / P.res) - 1);
-  b.r1 = (int)min((long long)P.ny - 1, trunc_ll(y1 / P.res) + 1);
+  b.c0 = (int)max(0LL, trunc_ll(div_h(x0, P.res)) - 1);
+  b.c1 = (int)min((long long)P.nx - 1, trunc_ll(div_h(x1, P.res)) + 1);
+  b.r0 = (int)max(0LL, trunc_ll(div_h(y0, P.res)) - 1);
+  b.r1 = (int)min((long long)P.ny - 1, trunc_ll(div_h(y1, P.res)) + 1);
   b.empty = b.c1 < b.c0 || b.r1 < b.r0;
   return b;
 }
