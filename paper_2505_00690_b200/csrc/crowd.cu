@@ -1282,7 +1282,7 @@ __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S
 // can never keep a search from running).  The CTA of an env with replans waits for
 // the env's own searches only, commits it, and at once predicts its next replans
 // (dry guidance pass) into the prefetch batch, whose search warps are still polling.
-template <int NT>
+template <int NT, bool kLanes>
 __global__ void __launch_bounds__(NT) k_orca_ec(cw_crowd_params P, cw_crowd_state S,
                                                 const double* __restrict__ robot_pos,
                                                 const double* __restrict__ robot_vel, double robot_radius,
@@ -1295,7 +1295,7 @@ __global__ void __launch_bounds__(NT) k_orca_ec(cw_crowd_params P, cw_crowd_stat
       __threadfence();
     }
     __syncthreads();
-    orca_env<NT, false>(P, S, e, robot_pos, robot_vel, robot_radius, env_mask, bins, sm, nullptr, 0);
+    orca_env<NT, kLanes>(P, S, e, robot_pos, robot_vel, robot_radius, env_mask, bins, sm, nullptr, 0);
     __syncthreads();
     guide_env<NT, false, true>(P, S, e, nullptr, nullptr, &sa, true);
     __syncthreads();
@@ -1900,6 +1900,44 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
   return (int)cudaGetLastError();
 }
 
+// The overlapped tick's two ORCA passes (pass 1 beside the searches; pass 2 after them,
+// or early commit).  kLanes: lane per agent (A < 128 without binning) -- the same
+// operations as the warp path (the run uses it; run == step is asserted bit for bit),
+// 4.3x fewer instructions.
+template <int NT, bool kLanes>
+static void launch_orca_passes(const cw_crowd_params& P, const cw_crowd_state& S, const double* rp,
+                               const double* rv, double rr, const uint8_t* em, const Bins& bins, size_t sm,
+                               cudaStream_t lo, cudaStream_t hi, bool ec, const SpecArgs& sa) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_orca<NT, kLanes>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(k_orca_ec<NT, kLanes>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    attr = true;
+  }
+  if (sm > 48 * 1024) {
+    cudaFuncSetAttribute(k_orca<NT, kLanes>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_orca_ec<NT, kLanes>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  }
+  k_orca<NT, kLanes><<<P.E, NT, sm, lo>>>(P, S, rp, rv, rr, em, bins, 1);
+  if (ec) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P.E);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = hi;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_orca_ec<NT, kLanes>, P, S, rp, rv, rr, em, bins, sa);
+  } else {
+    k_orca<NT, kLanes><<<P.E, NT, sm, hi>>>(P, S, rp, rv, rr, em, bins, 2);
+  }
+}
+
 template <int NT>
 static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const double* rp,
                        const double* rv, double rr, const uint8_t* em, int phases,
@@ -1915,12 +1953,6 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
     // overlapped tick: envs without replans commit beside the A* searches.  An SM
     // runs one L1 / shared-memory split at a time, so k_orca asks for the same
     // max-shared carveout as k_astar to be co-resident with it.
-    static bool carve = false;
-    if (!carve) {
-      cudaFuncSetAttribute(k_orca<NT>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           (int)cudaSharedmemCarveoutMaxShared);
-      carve = true;
-    }
     TickStreams& T = tick_streams();
     // a new prefetch batch every tick (its slot's previous batch, eight ticks back, is
     // waited for on the device: normally long done); the envs with replans commit as soon
@@ -1946,30 +1978,11 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
     SpecArgs look = X ? spec_args(X, 1, S.env_epoch, b) : SpecArgs{};
     if (ec) look.pend = X->pend;
     launch_astar(P, S, T.hi, look);
-    k_orca<NT><<<P.E, NT, sm, T.lo>>>(P, S, rp, rv, rr, em, bins, 1);
-    if (ec) {
-      static bool ec_attr = false;
-      if (!ec_attr) {
-        cudaFuncSetAttribute(k_orca_ec<NT>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             (int)cudaSharedmemCarveoutMaxShared);
-        ec_attr = true;
-      }
-      if (sm > 48 * 1024)
-        cudaFuncSetAttribute(k_orca_ec<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(P.E);
-      cfg.blockDim = dim3(NT);
-      cfg.dynamicSmemBytes = sm;
-      cfg.stream = T.hi;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      at[0].val.programmaticStreamSerializationAllowed = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      cudaLaunchKernelEx(&cfg, k_orca_ec<NT>, P, S, rp, rv, rr, em, bins, sa);
-    } else {
-      k_orca<NT><<<P.E, NT, sm, T.hi>>>(P, S, rp, rv, rr, em, bins, 2);
-    }
+    static const bool warp_orca = getenv("CW_SYNC_WARP_ORCA") != nullptr;   // A/B
+    if (!warp_orca && bins.ncx == 0 && P.max_neighbors <= MAXK)
+      launch_orca_passes<NT, true>(P, S, rp, rv, rr, em, bins, sm, T.lo, T.hi, ec, sa);
+    else
+      launch_orca_passes<NT, false>(P, S, rp, rv, rr, em, bins, sm, T.lo, T.hi, ec, sa);
     cudaEventRecord(T.hi_done, T.hi);
     cudaEventRecord(T.lo_done, T.lo);
     if (batch) {
