@@ -758,7 +758,7 @@ def main():
     ap.add_argument("--mode", default="run", choices=["run", "step"],
                     help="value through CrowdField.run (default) or K CrowdField.step calls")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
-    ap.add_argument("--threads", type=int, default=128)
+    ap.add_argument("--threads", type=int, default=None)
     ap.add_argument("--sample-warmup", type=int, default=1)
     ap.add_argument("--sample-reps", type=int, default=3)
     ap.add_argument("--sync-steps", type=int, default=100)

@@ -101,7 +101,7 @@ class CrowdField:
     OccupancyGrid (host labels, uploaded once) or a device ``SceneBatch``."""
 
     def __init__(self, occupancies, config, env_seeds, resample_goals=True, device="cuda",
-                 threads=128, path_cap=None, heap_cap=None, astar_warps=None, prefetch=None):
+                 threads=None, path_cap=None, heap_cap=None, astar_warps=None, prefetch=None):
         import torch
         self.config = config
         # next-tick search prefetch in step() (cw_spec_create): results are identical with
@@ -111,7 +111,7 @@ class CrowdField:
         self._spec_key = None
         self.resample_goals = resample_goals
         self.device = torch.device(device)
-        self.threads = threads
+        self.threads = threads    # step CTA size per env; None: by crowd size (_step_nt)
         self.run_threads = None   # cw_crowd_run CTA size; None: one lane per agent
         self.run_history_bytes = 256 << 20   # per-call cap of the run's (env, tick) gap history
         self.run_server_warps = None   # search warps per server CTA in cw_crowd_run (None: by round footprint, crowd.cu launch_run)
@@ -400,7 +400,7 @@ class CrowdField:
         rv = self._dev(robot_vel, torch.float64, (self.E, 2)) if robot_pos is not None else None
         em = self._dev(env_mask, torch.uint8, (self.E,))
         err = _lib.lib().cw_crowd_step(self._p, self._s, _lib.ptr(rp), _lib.ptr(rv),
-                                       float(robot_radius), _lib.ptr(em), self.threads,
+                                       float(robot_radius), _lib.ptr(em), self._step_nt(),
                                        _lib.stream_ptr(stream))
         _lib.check(err, "cw_crowd_step")
         if check:
@@ -468,6 +468,12 @@ class CrowdField:
         if check:
             self.check_flags()
 
+    def _step_nt(self):
+        """Step CTA size per env: 64 threads for lane-path crowds (A < 128: one lane per
+        agent in the ORCA passes; measured 1-6 % faster ticks than 128 at cfg2 / cfg3 / cfg5),
+        128 for the warp-per-agent shape with cell binning."""
+        return int(self.threads or (64 if self.A < 128 else 128))
+
     def _run_nt(self):
         """Round CTA size: one lane per agent below 128 agents (lane ORCA / guide),
         else the warp-per-agent shape with cell binning."""
@@ -479,7 +485,7 @@ class CrowdField:
         if "_p" not in self.__dict__:
             self.prepare_step()
         err = _lib.lib().cw_crowd_step_phases(self._p, self._s, _lib.ptr(robot_pos), _lib.ptr(robot_vel),
-                                              float(robot_radius), _lib.ptr(env_mask), self.threads,
+                                              float(robot_radius), _lib.ptr(env_mask), self._step_nt(),
                                               int(phase), _lib.stream_ptr(stream))
         _lib.check(err, "cw_crowd_step_phases")
 

@@ -76,7 +76,7 @@ class BatchedEnv:
     identities are ``scene_hashes`` either way."""
 
     def __init__(self, specs, scheme, master_seed, k=None, cache=None, config=None,
-                 env_seeds=None, device="cuda", threads=128, catalog=None, standby=False):
+                 env_seeds=None, device="cuda", threads=None, catalog=None, standby=False):
         import torch
         self.config = config or EnvConfig()
         self.scheme = Scheme(scheme)
@@ -421,7 +421,7 @@ class SceneStandby:
             self.pred.wait_event(ev)
             rows32.record_stream(self.pred)
             _lib.check(_lib.lib().cw_spec_predict(self._params, self._pool_state, self._spec, _lib.ptr(rows32),
-                                                  len(rows), self.field.threads, _lib.stream_ptr(self.pred)),
+                                                  len(rows), self.field._step_nt(), _lib.stream_ptr(self.pred)),
                        "cw_spec_predict")
 
     def take(self, rows):

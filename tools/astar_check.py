@@ -47,7 +47,7 @@ labs = {e: b.labels[e].cpu().numpy() != 0 for e in watch}
 
 
 def phase(ph):
-    _lib.check(L.cw_crowd_step_phases(f._p, f._s, _lib.ptr(rpos), _lib.ptr(rvel), 0.35, None, f.threads, ph,
+    _lib.check(L.cw_crowd_step_phases(f._p, f._s, _lib.ptr(rpos), _lib.ptr(rvel), 0.35, None, f._step_nt(), ph,
                                       _lib.stream_ptr(None)), "phase")
 
 

@@ -49,7 +49,7 @@ L = _lib.lib()
 
 
 def phase(ph):
-    _lib.check(L.cw_crowd_step_phases(f._p, f._s, _lib.ptr(rpos), _lib.ptr(rvel), 0.35, None, f.threads, ph,
+    _lib.check(L.cw_crowd_step_phases(f._p, f._s, _lib.ptr(rpos), _lib.ptr(rvel), 0.35, None, f._step_nt(), ph,
                                       _lib.stream_ptr(None)), "phase")
 
 

@@ -56,7 +56,7 @@ st = torch.cuda.current_stream()
 
 
 def run(phases):
-    err = L.cw_crowd_step_phases(f._p, f._s, _lib.ptr(rpos), _lib.ptr(rvel), 0.35, None, f.threads,
+    err = L.cw_crowd_step_phases(f._p, f._s, _lib.ptr(rpos), _lib.ptr(rvel), 0.35, None, f._step_nt(),
                                  phases, _lib.stream_ptr(None))
     _lib.check(err, "phase")
 
