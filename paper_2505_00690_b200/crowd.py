@@ -477,9 +477,15 @@ class CrowdField:
         return int(self.threads or (64 if self.A < 128 else 256))
 
     def _run_nt(self):
-        """Round CTA size: one lane per agent below 128 agents (lane ORCA / guide),
-        else the warp-per-agent shape with cell binning."""
-        return 32 if self.A <= 32 else 64 if self.A <= 64 else 128 if self.A < 128 else 256
+        """Round CTA size: one lane per agent (lane ORCA / guide; cell binning from 128
+        agents on)."""
+        if self.A >= 128:
+            # lane path with cell binning (max_neighbors <= 10): 128 threads, so a round CTA
+            # (~220 registers per thread) shares an SM with a search-server CTA -- cfg4 run
+            # 24.5 -> 23.8 ms/tick (256 threads: 66 ms, one CTA per SM and none beside the
+            # server); the warp-per-agent path (more neighbours): 256
+            return 128 if self.config.max_neighbors <= 10 else 256
+        return 32 if self.A <= 32 else 64 if self.A <= 64 else 128
 
     def step_phase(self, phase, robot_pos=None, robot_vel=None, robot_radius=0.35, env_mask=None,
                    stream=None):

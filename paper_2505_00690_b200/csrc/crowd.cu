@@ -876,14 +876,15 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
     double my_gap = CUDART_INF;
     int my_anynb = 0;
     long long fallbacks = 0, stalls = 0;
-    // kLanes: the caller guarantees no binning (A < 128) and max_neighbors <= MAXK,
-    // so each instantiation holds one of the two paths (code size, registers)
+    // kLanes: the caller guarantees max_neighbors <= MAXK, so each instantiation holds
+    // one of the two paths (code size, registers)
     constexpr bool lanes = kLanes;
     if (lanes) {
-      // ---------------- lane per agent (A < 128): same operations as the warp path
+      // ---------------- lane per agent: same operations as the warp path
       const int kmax = min(P.max_neighbors, max(A - 1, 0));
-      // the fp32 Gram operands of every agent, once (field.py:246-253: p32, |p32|^2)
-      float* s_fx = reinterpret_cast<float*>(s_cend);
+      // the fp32 Gram operands of every agent, once (field.py:246-253: p32, |p32|^2); without
+      // binning they alias the unused bins region, with it they follow the agent cells
+      float* s_fx = reinterpret_cast<float*>(bins.ncx > 0 ? s_cell + A : s_cend);
       float* s_fy = s_fx + A;
       float* s_fsq = s_fy + A;
       for (int a = threadIdx.x; a < A; a += NT) {
@@ -932,7 +933,41 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
         for (int k = 0; k < MAXK; ++k) { tk[k] = CUDART_INF_F; tj[k] = 0; }
         int nb = 0;
         // per 32-candidate chunk: the range test for every j without divergence
-        // (a bitmask), then each lane inserts only its own in-range j, in j order
+        // (a bitmask), then each lane inserts only its own in-range j.  The insertion
+        // orders by (key, index), so the visiting order does not matter (binned
+        // candidates come in cell order)
+        auto insert = [&](float key, int j) {
+          int pos = 0;
+#pragma unroll
+          for (int k = 0; k < MAXK; ++k) pos += (k < nb && (tk[k] < key || (tk[k] == key && tj[k] < j)));
+          if (pos >= kmax) return;
+#pragma unroll
+          for (int k = MAXK - 1; k > 0; --k)
+            if (k > pos) { tk[k] = tk[k - 1]; tj[k] = tj[k - 1]; }
+#pragma unroll
+          for (int k = 0; k < MAXK; ++k)
+            if (k == pos) { tk[k] = key; tj[k] = j; }
+          nb = min(nb + 1, kmax);
+        };
+        if (bins.ncx > 0) {
+          // every j with key < nd^2 lies in the 3 x 3 cells around a's cell (see above)
+          const int cx = s_cell[a] % bins.ncx, cy = s_cell[a] / bins.ncx;
+          const int x0 = max(cx - 1, 0), x1 = min(cx + 1, bins.ncx - 1);
+          for (int d = 0; d < 3; ++d) {
+            const int row = cy - 1 + d;
+            if (row < 0 || row >= bins.ncy) continue;
+            const int c0 = row * bins.ncx + x0, c1 = row * bins.ncx + x1;
+            const int t1 = s_cend[c1];
+            for (int tt = c0 > 0 ? s_cend[c0 - 1] : 0; tt < t1; ++tt) {
+              const int j = s_sorted[tt];   // active agents only
+              if (j == a) continue;
+              const float xj = s_fx[j], yj = s_fy[j], sqj = s_fsq[j];
+              float dot = __fmaf_rn(yi, yj, __fmul_rn(xi, xj));
+              float key = __fsub_rn(__fadd_rn(sqi, sqj), __fmul_rn(2.0f, dot));
+              if (key < P.nd2_f32) insert(key, j);
+            }
+          }
+        } else
         for (int j0 = 0; j0 < A; j0 += 32) {
          unsigned inr = 0u;
          const int jn = min(32, A - j0);
@@ -949,17 +984,7 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
           const float xj = s_fx[j], yj = s_fy[j], sqj = s_fsq[j];
           float dot = __fmaf_rn(yi, yj, __fmul_rn(xi, xj));
           float key = __fsub_rn(__fadd_rn(sqi, sqj), __fmul_rn(2.0f, dot));
-          int pos = 0;
-#pragma unroll
-          for (int k = 0; k < MAXK; ++k) pos += (k < nb && tk[k] <= key);
-          if (pos >= kmax) continue;
-#pragma unroll
-          for (int k = MAXK - 1; k > 0; --k)
-            if (k > pos) { tk[k] = tk[k - 1]; tj[k] = tj[k - 1]; }
-#pragma unroll
-          for (int k = 0; k < MAXK; ++k)
-            if (k == pos) { tk[k] = key; tj[k] = j; }
-          nb = min(nb + 1, kmax);
+          insert(key, j);
          }
         }
         // thread-local arrays indexed at run time (local memory, L1-resident): slots
@@ -1648,11 +1673,12 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
                       const double* rv, double rr, const uint8_t* em, int ticks, const int32_t* start,
                       const int32_t* stop, int flags, void* scratch, cudaStream_t st) {
   const Bins bins = make_bins(P);
-  const bool lanes_ok = bins.ncx == 0 && P.max_neighbors <= MAXK;
+  static const bool warp_orca = getenv("CW_RUN_WARP_ORCA") != nullptr;   // A/B
+  const bool lanes_ok = P.max_neighbors <= MAXK && !warp_orca;
   // the lane path needs no per-warp constraint block: a smaller footprint lets two
   // round CTAs share an SM with a search-server CTA
   const size_t sm = lanes_ok ? (size_t)P.A * 7 * sizeof(double) + (size_t)((P.A + 15) & ~15) + 16 +
-                                   (size_t)P.A * 3 * sizeof(float)
+                                   (size_t)P.A * 3 * sizeof(float) + bins_smem_bytes(bins, P.A)
                              : cw_crowd_step_smem_bytes(P.A, NT) + bins_smem_bytes(bins, P.A);
   static bool attrs = false;
   if (!attrs) {
@@ -1689,8 +1715,8 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
     cudaGetLastError();
     attrs = true;
   }
-  // lane-per-agent ORCA below 128 agents; the binned warp path (96 registers,
-  // so its CTAs share SMs with the search server) above
+  // lane-per-agent ORCA (cell-binned candidates from 128 agents on); the warp path only
+  // for more than MAXK neighbours (CW_RUN_WARP_ORCA forces it for A/B runs)
   const bool lanes = lanes_ok;
   if (sm > 48 * 1024) {
     cudaFuncSetAttribute(k_round<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1774,7 +1800,7 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
   //  220 KB and the 1/8 margin.
   int w_def = 2, kb_def = 0, margin_auto = 0;
   if (!P.run_server_warps) {
-    if (!lanes_ok) {
+    if (sm > 16 * 1024) {   // large rounds (binned crowds)
       w_def = 4;
       kb_def = std::min(100, 227 - (int)((sm + 1023) / 1024) - 3);
       margin_auto = 8;
@@ -1979,7 +2005,7 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
     if (ec) look.pend = X->pend;
     launch_astar(P, S, T.hi, look);
     static const bool warp_orca = getenv("CW_SYNC_WARP_ORCA") != nullptr;   // A/B
-    if (!warp_orca && bins.ncx == 0 && P.max_neighbors <= MAXK)
+    if (!warp_orca && P.max_neighbors <= MAXK)
       launch_orca_passes<NT, true>(P, S, rp, rv, rr, em, bins, sm, T.lo, T.hi, ec, sa);
     else
       launch_orca_passes<NT, false>(P, S, rp, rv, rr, em, bins, sm, T.lo, T.hi, ec, sa);
