@@ -785,7 +785,7 @@ CW_HD size_t bins_smem_bytes(const Bins& b, int A) {
 // ORCA + commit + goal resample of env e (body of k_orca and k_round).  With
 // ra != nullptr the env's gap goes to the run history at ``tick`` instead of
 // gap_tmp / flags[0].
-template <int NT, bool kLanes>
+template <int NT, int kLanes>   // 0 warp per agent, 1 lane per agent, 2 lanes + cell binning
 __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int e,
                          const double* __restrict__ robot_pos, const double* __restrict__ robot_vel,
                          double robot_radius, const uint8_t* __restrict__ env_mask, const Bins& bins,
@@ -878,13 +878,13 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
     long long fallbacks = 0, stalls = 0;
     // kLanes: the caller guarantees max_neighbors <= MAXK, so each instantiation holds
     // one of the two paths (code size, registers)
-    constexpr bool lanes = kLanes;
+    constexpr bool lanes = kLanes != 0;
     if (lanes) {
       // ---------------- lane per agent: same operations as the warp path
       const int kmax = min(P.max_neighbors, max(A - 1, 0));
       // the fp32 Gram operands of every agent, once (field.py:246-253: p32, |p32|^2); without
       // binning they alias the unused bins region, with it they follow the agent cells
-      float* s_fx = reinterpret_cast<float*>(bins.ncx > 0 ? s_cell + A : s_cend);
+      float* s_fx = reinterpret_cast<float*>(kLanes == 2 ? s_cell + A : s_cend);
       float* s_fy = s_fx + A;
       float* s_fsq = s_fy + A;
       for (int a = threadIdx.x; a < A; a += NT) {
@@ -949,7 +949,7 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
             if (k == pos) { tk[k] = key; tj[k] = j; }
           nb = min(nb + 1, kmax);
         };
-        if (bins.ncx > 0) {
+        if constexpr (kLanes == 2) {
           // every j with key < nd^2 lies in the 3 x 3 cells around a's cell (see above)
           const int cx = s_cell[a] % bins.ncx, cy = s_cell[a] / bins.ncx;
           const int x0 = max(cx - 1, 0), x1 = min(cx + 1, bins.ncx - 1);
@@ -967,7 +967,7 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
               if (key < P.nd2_f32) insert(key, j);
             }
           }
-        } else
+        } else {
         for (int j0 = 0; j0 < A; j0 += 32) {
          unsigned inr = 0u;
          const int jn = min(32, A - j0);
@@ -984,8 +984,21 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
           const float xj = s_fx[j], yj = s_fy[j], sqj = s_fsq[j];
           float dot = __fmaf_rn(yi, yj, __fmul_rn(xi, xj));
           float key = __fsub_rn(__fadd_rn(sqi, sqj), __fmul_rn(2.0f, dot));
-          insert(key, j);
+          // j increases, so every kept entry has a smaller index: (key, index) order is
+          // "after every kept entry with key <= this key"
+          int pos = 0;
+#pragma unroll
+          for (int k = 0; k < MAXK; ++k) pos += (k < nb && tk[k] <= key);
+          if (pos >= kmax) continue;
+#pragma unroll
+          for (int k = MAXK - 1; k > 0; --k)
+            if (k > pos) { tk[k] = tk[k - 1]; tj[k] = tj[k - 1]; }
+#pragma unroll
+          for (int k = 0; k < MAXK; ++k)
+            if (k == pos) { tk[k] = key; tj[k] = j; }
+          nb = min(nb + 1, kmax);
          }
+        }
         }
         // thread-local arrays indexed at run time (local memory, L1-resident): slots
         // >= nc are never read
@@ -1286,7 +1299,7 @@ __device__ void orca_env(const cw_crowd_params& P, const cw_crowd_state& S, int 
 
 CW_DEV void orca_tail(const cw_crowd_params& P, const cw_crowd_state& S, int pass, bool pdl = false);
 
-template <int NT, bool kLanes = false>
+template <int NT, int kLanes = 0>
 __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S,
                                              const double* __restrict__ robot_pos,
                                              const double* __restrict__ robot_vel,
@@ -1307,7 +1320,7 @@ __global__ void __launch_bounds__(NT) k_orca(cw_crowd_params P, cw_crowd_state S
 // can never keep a search from running).  The CTA of an env with replans waits for
 // the env's own searches only, commits it, and at once predicts its next replans
 // (dry guidance pass) into the prefetch batch, whose search warps are still polling.
-template <int NT, bool kLanes>
+template <int NT, int kLanes>
 __global__ void __launch_bounds__(NT) k_orca_ec(cw_crowd_params P, cw_crowd_state S,
                                                 const double* __restrict__ robot_pos,
                                                 const double* __restrict__ robot_vel, double robot_radius,
@@ -1376,7 +1389,7 @@ CW_DEV void orca_tail(const cw_crowd_params& P, const cw_crowd_state& S, int pas
 // reaches T; a CTA exits when no env is ready, and the host keeps launching
 // rounds until every env is done.  An env is in the ring at most once, so no
 // two CTAs ever work on the same env.
-template <int NT, bool kLanes>
+template <int NT, int kLanes>
 __global__ void __launch_bounds__(NT) k_round(cw_crowd_params P, cw_crowd_state S,
                                               const double* __restrict__ robot_pos,
                                               const double* __restrict__ robot_vel, double robot_radius,
@@ -1693,9 +1706,11 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
                          (int)cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(k_astar<kAstarWarps, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          (int)cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(k_round<NT, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncSetAttribute(k_round<NT, 2>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          (int)cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(k_round<NT, false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncSetAttribute(k_round<NT, 1>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(k_round<NT, 0>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          (int)cudaSharedmemCarveoutMaxShared);
     // Reserve the per-thread local memory (stack) of every kernel of the run now, while
     // nothing is running: a launch that outgrows the reservation makes the driver grow
@@ -1703,8 +1718,9 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
     // after the rounds that launch is holding back.
     size_t need = 0;
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, k_round<NT, true>) == cudaSuccess) need = std::max(need, fa.localSizeBytes);
-    if (cudaFuncGetAttributes(&fa, k_round<NT, false>) == cudaSuccess) need = std::max(need, fa.localSizeBytes);
+    if (cudaFuncGetAttributes(&fa, k_round<NT, 2>) == cudaSuccess) need = std::max(need, fa.localSizeBytes);
+    if (cudaFuncGetAttributes(&fa, k_round<NT, 1>) == cudaSuccess) need = std::max(need, fa.localSizeBytes);
+    if (cudaFuncGetAttributes(&fa, k_round<NT, 0>) == cudaSuccess) need = std::max(need, fa.localSizeBytes);
     if (cudaFuncGetAttributes(&fa, k_astar<1, true>) == cudaSuccess) need = std::max(need, fa.localSizeBytes);
     if (cudaFuncGetAttributes(&fa, k_astar<2, true>) == cudaSuccess) need = std::max(need, fa.localSizeBytes);
     if (cudaFuncGetAttributes(&fa, k_astar<kAstarWarps, true>) == cudaSuccess)
@@ -1719,8 +1735,9 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
   // for more than MAXK neighbours (CW_RUN_WARP_ORCA forces it for A/B runs)
   const bool lanes = lanes_ok;
   if (sm > 48 * 1024) {
-    cudaFuncSetAttribute(k_round<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(k_round<NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_round<NT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_round<NT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_round<NT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   }
   const RunLayout L = run_layout(P.E, P.A, ticks);
   unsigned char* base = static_cast<unsigned char*>(scratch);
@@ -1851,8 +1868,9 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
   for (long long i = 0;; ++i) {
     n_rounds = i + 1;
     cudaStream_t rs = H.rs[i % n_rs];
-    if (lanes) k_round<NT, true><<<round_ctas, NT, sm, rs>>>(P, S, rp, rv, rr, em, bins, ra);
-    else k_round<NT, false><<<round_ctas, NT, sm, rs>>>(P, S, rp, rv, rr, em, bins, ra);
+    if (lanes && bins.ncx > 0) k_round<NT, 2><<<round_ctas, NT, sm, rs>>>(P, S, rp, rv, rr, em, bins, ra);
+    else if (lanes) k_round<NT, 1><<<round_ctas, NT, sm, rs>>>(P, S, rp, rv, rr, em, bins, ra);
+    else k_round<NT, 0><<<round_ctas, NT, sm, rs>>>(P, S, rp, rv, rr, em, bins, ra);
     cudaMemcpyAsync(H.poll + (i & 7) * 8, ra.q, 32, cudaMemcpyDeviceToHost, rs);   // head..progress
     cudaEventRecord(H.ev[i & 7], rs);
     if (i >= kInFlight) {
@@ -1927,10 +1945,10 @@ static int launch_run(const cw_crowd_params& P, const cw_crowd_state& S, const d
 }
 
 // The overlapped tick's two ORCA passes (pass 1 beside the searches; pass 2 after them,
-// or early commit).  kLanes: lane per agent (A < 128 without binning) -- the same
+// or early commit).  kLanes: 1 lane per agent, 2 the same with cell binning -- the same
 // operations as the warp path (the run uses it; run == step is asserted bit for bit),
 // 4.3x fewer instructions.
-template <int NT, bool kLanes>
+template <int NT, int kLanes>
 static void launch_orca_passes(const cw_crowd_params& P, const cw_crowd_state& S, const double* rp,
                                const double* rv, double rr, const uint8_t* em, const Bins& bins, size_t sm,
                                cudaStream_t lo, cudaStream_t hi, bool ec, const SpecArgs& sa) {
@@ -2006,9 +2024,10 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
     launch_astar(P, S, T.hi, look);
     static const bool warp_orca = getenv("CW_SYNC_WARP_ORCA") != nullptr;   // A/B
     if (!warp_orca && P.max_neighbors <= MAXK)
-      launch_orca_passes<NT, true>(P, S, rp, rv, rr, em, bins, sm, T.lo, T.hi, ec, sa);
+      (bins.ncx > 0 ? launch_orca_passes<NT, 2> : launch_orca_passes<NT, 1>)(P, S, rp, rv, rr, em, bins, sm,
+                                                                             T.lo, T.hi, ec, sa);
     else
-      launch_orca_passes<NT, false>(P, S, rp, rv, rr, em, bins, sm, T.lo, T.hi, ec, sa);
+      launch_orca_passes<NT, 0>(P, S, rp, rv, rr, em, bins, sm, T.lo, T.hi, ec, sa);
     cudaEventRecord(T.hi_done, T.hi);
     cudaEventRecord(T.lo_done, T.lo);
     if (batch) {
@@ -2033,8 +2052,13 @@ static int launch_step(const cw_crowd_params& P, const cw_crowd_state& S, const 
   if (phases & 2) launch_astar(P, S, st);
   static const bool lanes_dbg = getenv("CW_ORCA_LANES") != nullptr;   // profiling the lane path
   if ((phases & 4) && lanes_dbg) {
-    if (sm > 48 * 1024) cudaFuncSetAttribute(k_orca<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_orca<NT, true><<<P.E, NT, sm, st>>>(P, S, rp, rv, rr, em, bins, 0);
+    if (bins.ncx > 0) {
+      if (sm > 48 * 1024) cudaFuncSetAttribute(k_orca<NT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_orca<NT, 2><<<P.E, NT, sm, st>>>(P, S, rp, rv, rr, em, bins, 0);
+    } else {
+      if (sm > 48 * 1024) cudaFuncSetAttribute(k_orca<NT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_orca<NT, 1><<<P.E, NT, sm, st>>>(P, S, rp, rv, rr, em, bins, 0);
+    }
   } else if (phases & 4) {
     k_orca<NT><<<P.E, NT, sm, st>>>(P, S, rp, rv, rr, em, bins, 0);
   }
