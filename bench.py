@@ -280,13 +280,6 @@ def run_ours(args):
             f.step(rpos, rvel, 0.35, check=False)
     torch.cuda.synchronize()
     f.check_flags()
-    # cfg5: the timed loops re-sample through the standby pool: each reset installs a scene
-    # sampled ahead (same seeds) and starts sampling the row's next one beside the ticks;
-    # the pool's initial fill (every row's next scene) is setup, outside the timed regions
-    if CFG["resample"] > 0 and not args.no_standby:
-        from paper_2505_00690_b200.envcore import SceneStandby
-        standby = SceneStandby(sampler, env_seeds, counts, field=f)
-        torch.cuda.synchronize()
     f.counters_t.zero_()
     flush.fill_(-1.0)                   # L2 flushed once; the grids read (>600 MB) exceed L2
     r0, r1 = ev(), ev()
@@ -300,12 +293,11 @@ def run_ours(args):
     t_run0 = time.perf_counter()
     r0.record(st)
     if CFG["resample"] > 0:
-        # cfg5 driver: the same Bernoulli re-sampling schedule through
-        # envcore.run_with_resampling -- tick by tick with the standby pool (default), or
-        # as barrier-free windows between batched re-samples (--no-standby)
+        # cfg5 driver: the same Bernoulli re-sampling schedule, run as barrier-free
+        # segments between batched re-samples (envcore.run_with_resampling)
         from paper_2505_00690_b200.envcore import run_with_resampling
         run_resampled = run_with_resampling(sampler, f, env_seeds, counts, masks[args.warmup:], args.steps,
-                                            rpos, rvel, 0.35, standby=standby)
+                                            rpos, rvel, 0.35)
     elif args.mode == "run":
         f.run(args.steps, rpos, rvel, 0.35)
     else:
@@ -319,14 +311,7 @@ def run_ours(args):
     f.check_flags()
     run_ms = r0.elapsed_time(r1)
     c_run = f.stats()
-    if CFG["resample"] > 0 and standby is not None:
-        rs_ = f.last_run_stats
-        # per tick: guide, search, ORCA pass 1, early commit, dry guidance, prefetch
-        # searches; per take: the standby pool's sampling pipeline (~17 kernels incl.
-        # route anchors), the first-tick prediction (guide + searches) and its install
-        launches = 6 * rs_["ticks"] + 20 * rs_["takes"]
-        rounds = 0
-    elif CFG["resample"] > 0:
+    if CFG["resample"] > 0:
         rs_ = f.last_run_stats
         # per window: init, server, finish + its rounds; per batched re-sample: the
         # sampling pipeline (~17 kernels incl. route anchors) + the respawn copies
@@ -340,6 +325,13 @@ def run_ours(args):
         launches = 4 * args.steps
     csum_value = shard.state_checksum(f.pos_t, f.vel_t, f.goal_t, f.last_gap_t)   # per env, exact
 
+    # the per-tick loops re-sample through the standby pool: each reset installs a scene
+    # sampled ahead (same seeds) and starts sampling the row's next one beside the ticks;
+    # the pool's initial fill (every row's next scene) is setup, outside the timed regions
+    if CFG["resample"] > 0 and not args.no_standby:
+        from paper_2505_00690_b200.envcore import SceneStandby
+        standby = SceneStandby(sampler, env_seeds, counts, field=f)
+        torch.cuda.synchronize()
 
     # ---- synchronous tick (CrowdField.step, barrier per tick), L2 flushed between ticks
     n_sync = min(args.steps, args.sync_steps)
@@ -494,20 +486,14 @@ def run_ours(args):
         "n_gpus": world, "steps": steps, "warmup": args.warmup,
         "ms_per_step": round(avg_ms, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded procedural scenes)",
-        "mode": args.mode if not CFG["resample"] else ("ticks_standby" if standby is not None else "run_windows"),
+        "mode": args.mode if not CFG["resample"] else "run_windows",
         "config": {"workload": workload, "envs_per_gpu": E, "grid": [nx, nx], "objects": CFG["objects"],
                    "peds": CFG["peds"], "parallelism": f"env-shard x{world} ({args.backend})",
                    "l2": "flushed (256 MB write) before the timed run; the per-env grids it reads "
                          "(labels, nearest, reach, moves: >600 MB at cfg2) exceed the 126 MB L2",
                    "robot": "static per env at a seeded walkable cell, zero velocity",
                    "resampled_envs": run_resampled or resampled},
-        "what": ("envcore.run_with_resampling(K) with the standby pool: each tick installs its re-sampled "
-                 "rows' scenes sampled ahead on a side stream (same seeds) and steps every env "
-                 "(CrowdField.step, next-tick prefetch) -- the same state as re-sampling and stepping "
-                 "tick by tick" if CFG["resample"] and standby is not None else
-                 "envcore.run_with_resampling(K) as barrier-free windows between batched re-samples"
-                 if CFG["resample"] else
-                 "CrowdField.run(K): K ticks of every env without a per-tick barrier across envs "
+        "what": ("CrowdField.run(K): K ticks of every env without a per-tick barrier across envs "
                  "(persistent A* server + ready-env ring + round kernels), bit-identical to K "
                  "CrowdField.step calls" if args.mode == "run" else "K CrowdField.step calls"),
         "e2e": {"value": round(E * world * e2e_steps / e2e_s, 1), "unit": "env-steps/s",

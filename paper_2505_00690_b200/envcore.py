@@ -449,7 +449,7 @@ class SceneStandby:
 
 
 def run_with_resampling(sampler, field, env_seeds, counts, events, ticks, robot_pos=None, robot_vel=None,
-                        robot_radius=0.35, window=5, overlap=False, standby=None):
+                        robot_radius=0.35, window=5, overlap=False):
     """``ticks`` crowd ticks of every env where env e's scene is re-sampled before
     tick t for every e in ``events[t]`` (the bench's cfg5 driver):
     re-sample seed ``child_seed(env_seed, "resample", n)``, crowd respawn seed
@@ -465,30 +465,8 @@ def run_with_resampling(sampler, field, env_seeds, counts, events, ticks, robot_
     end), so with ``overlap`` their scenes are sampled into a pool batch on a side
     stream while the window runs and copied into their rows at the boundary (off by
     default: the sampling kernels compete with the run for the SMs, measured slower).
-
-    With a ``standby`` (SceneStandby over ``sampler`` and ``field``) it runs tick by tick
-    instead: each tick's re-sampled rows install their standby scenes (sampled ahead on a
-    side stream, their first replans predicted) and every env steps once
-    (``CrowdField.step``, next-tick prefetch).  Same state; measured faster at cfg5
-    (13.9 vs 22.2 ms per tick, DESIGN 4.7): the windows pay the re-sampling and the
-    respawned envs' first-tick search bursts on their critical path.
     Returns the number of re-sampled scenes."""
     import torch
-    if standby is not None:
-        resampled = 0
-        for t in range(ticks):
-            rows = np.asarray(events[t], dtype=np.int64).reshape(-1)
-            if rows.size:
-                sl = torch.as_tensor(rows, dtype=torch.int64, device=field.device)
-                counts[sl] += 1
-                standby.take(rows)   # + set_from_spawn
-                resampled += int(rows.size)
-            field.step(robot_pos, robot_vel, robot_radius, check=False)
-        field.check_flags()
-        field.last_run_stats = {"windows": 0, "rounds": 0, "servers": 0, "sample_calls": 0,
-                                "ticks": ticks, "takes": int(sum(1 for t in range(ticks)
-                                                                 if np.asarray(events[t]).size))}
-        return resampled
     from .urbangen import SceneSampler
     dev = field.device
     E = field.E
