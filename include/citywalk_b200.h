@@ -354,6 +354,9 @@ typedef struct cw_robot_state {
   double* goal_vector;          /* (E, 2) ego frame */
   double* proj_vel;             /* (E) */
   float* height_map;            /* (E, 16, 10) */
+  uint8_t* semantics;           /* (E, 128) label of the cell each ray stopped in, 0 when it
+                                   reached the cap or left the grid (observe.py:84-85,
+                                   include_semantics); NULL = not written */
 } cw_robot_state;
 
 /* traversability_maps (robot.py:127-179): passable[e] for rows slots[e] (NULL =

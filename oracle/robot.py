@@ -134,6 +134,7 @@ def observe(x, y, yaw, goal, vel, elev_r, labels, elev, res, rise):
     prev = np.broadcast_to(elev_r.astype(np.float32)[:, None], (K, N_RAYS)).copy()
     alive = np.ones((K, N_RAYS), bool)
     depth = np.full((K, N_RAYS), np.float32(CAP), np.float32)
+    sem = np.zeros((K, N_RAYS), np.uint8)   # observe.py:49, 84-85: hit cell's label, else 0
     inv = np.float32(1.0 / res)
     lim = np.float32(rise)
     el32 = elev.astype(np.float32)
@@ -152,6 +153,7 @@ def observe(x, y, yaw, goal, vel, elev_r, labels, elev, res, rise):
         el = el32[ki, r0, c0]
         wall = alive & inside & ((lab == L_OBSTACLE) | (el - prev > lim))
         depth[wall] = t
+        sem[wall] = lab[wall]
         alive &= inside & ~wall
         prev = np.where(alive, el, prev)
     gvx, gvy = goal[:, 0] - x, goal[:, 1] - y
@@ -169,7 +171,7 @@ def observe(x, y, yaw, goal, vel, elev_r, labels, elev, res, rise):
     hin = (wx >= 0) & (wx < gnx * res) & (wy >= 0) & (wy < gny * res)
     hm = np.where(hin, elev[ki, hr, hc] - elev_r[:, None], 0.0)
     return dict(depth=depth, goal_vector=gvec, proj_vel=pvel,
-                height_map=hm.reshape(K, HX_N, HY_N).astype(np.float32))
+                height_map=hm.reshape(K, HX_N, HY_N).astype(np.float32), semantics=sem)
 
 
 class RobotBatch:

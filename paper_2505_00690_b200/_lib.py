@@ -92,7 +92,7 @@ class RobotParams(ctypes.Structure):
 ROBOT_STATE_FIELDS = [
     "x", "y", "yaw", "vx", "vy", "elev", "goal", "tick", "terminated", "truncated", "labels",
     "grid_elev", "passable", "crowd_pos", "crowd_radius", "crowd_active", "reward", "events",
-    "distance", "path_inc", "depth", "goal_vector", "proj_vel", "height_map",
+    "distance", "path_inc", "depth", "goal_vector", "proj_vel", "height_map", "semantics",
 ]
 
 

@@ -14,7 +14,8 @@
 //   k_observe      CTA per env, thread per ray: float32 march in res steps to
 //       10 m (obstacle or a rise above max_step_rise stops a ray, leaving the
 //       grid ends it at the cap), the 16 x 10 ego height patch, goal vector and
-//       projected velocity.
+//       projected velocity; with include_semantics the label of the cell each
+//       ray stopped in (observe.py:84-85).
 //
 // Compiled with -fmad=false: float64 / float32 expressions round once per op
 // like numpy.  sin / cos / atan2 / tan / tanh come from CUDA's libdevice
@@ -248,6 +249,7 @@ __global__ void __launch_bounds__(kRays) k_observe(cw_robot_params P, cw_robot_s
   const float lim = (float)P.model.max_step_rise;
   float prev = (float)er;
   float depth = (float)kCap;
+  uint8_t sem = 0;   // observe.py:49, 84-85
   const int n_steps = (int)(kCap / res);
   for (int s = 1; s <= n_steps; ++s) {
     const float t = (float)(s * res);
@@ -258,10 +260,12 @@ __global__ void __launch_bounds__(kRays) k_observe(cw_robot_params P, cw_robot_s
     if (!(cc >= 0 && cc < gnx && rr >= 0 && rr < gny)) break;   // left the grid: cap
     const size_t f = (size_t)rr * gnx + cc;
     const float ev = el[f];
-    if (lab[f] == L_OBSTACLE || __fsub_rn(ev, prev) > lim) { depth = t; break; }
+    const uint8_t lf = lab[f];
+    if (lf == L_OBSTACLE || __fsub_rn(ev, prev) > lim) { depth = t; sem = lf; break; }
     prev = ev;
   }
   S.depth[(size_t)e * kRays + k] = depth;
+  if (S.semantics) S.semantics[(size_t)e * kRays + k] = sem;
   // ego-aligned height patch (observe.py:112-121), 160 samples over the CTA
   double s, c;
   cr_sincos(yaw, &s, &c);

@@ -117,13 +117,12 @@ class BatchedEnv:
                                 device=device, threads=threads)
         if self.spec.pedestrian_count > 0:
             self.crowd.set_from_spawn(self.batch)
-        if self.config.include_semantics:
-            raise NotImplementedError("per-ray semantics (observe.py:84-85) are not built yet")
         self.model = ROBOT_MODELS[self.config.robot]
         self.robot = RobotBatch(self.batch.labels, self.batch.elev, self.resolution, self.model,
                                 horizon=self.config.horizon, dt=self.config.dt,
                                 reach_threshold_m=self.config.reach_threshold_m,
-                                reward=self.config.reward, device=self.device)
+                                reward=self.config.reward, device=self.device,
+                                semantics=self.config.include_semantics)
         self._spawn(np.arange(k))
         # standby: every slot's next scene (and its crowd's first replans) sampled ahead on
         # side streams, so resample() installs instead of sampling (SceneStandby)
@@ -296,14 +295,16 @@ class BatchedEnv:
         out = self.step_batch_device(acts, check=True)
         if live is None:
             live = np.ones(self.K, bool)
-        h = {k: v.cpu().numpy() for k, v in out.items()}
+        h = {k: v.cpu().numpy() for k, v in out.items() if v is not None}
+        sem = h.get("semantics")
         results = []
         for i in range(self.K):
             ev = {n: bool(h["events"][i, j]) for j, n in enumerate(EVENT_NAMES)}
             ev["distance_to_goal"] = float(h["distance"][i])
             ev["path_increment"] = float(h["path_inc"][i])
             obs = Observation(depth=h["depth"][i], goal_vector=h["goal_vector"][i],
-                              projected_velocity=float(h["proj_vel"][i]), height_map=h["height_map"][i])
+                              projected_velocity=float(h["proj_vel"][i]), height_map=h["height_map"][i],
+                              semantics=None if sem is None else sem[i])
             results.append(StepResult(observation=obs, reward=float(h["reward"][i]),
                                       terminated=bool(h["terminated"][i]), truncated=bool(h["truncated"][i]),
                                       events=ev))
@@ -322,7 +323,8 @@ class BatchedEnv:
         self.robot.observe()
         r = self.robot
         return Observation(depth=r.depth[i].cpu().numpy(), goal_vector=r.goal_vector[i].cpu().numpy(),
-                           projected_velocity=float(r.proj_vel[i]), height_map=r.height_map[i].cpu().numpy())
+                           projected_velocity=float(r.proj_vel[i]), height_map=r.height_map[i].cpu().numpy(),
+                           semantics=None if r.semantics is None else r.semantics[i].cpu().numpy())
 
 
 _SCENE_OUT = None

@@ -101,7 +101,7 @@ class RobotBatch:
     (E, ny, nx)); ``passable`` is computed once per scene (and per resampled row)."""
 
     def __init__(self, labels, elev, res, model="quadruped", horizon=200, dt=0.05,
-                 reach_threshold_m=0.5, reward=None, device=None):
+                 reach_threshold_m=0.5, reward=None, device=None, semantics=False):
         import torch
         self.labels, self.elev = labels, elev
         self.device = labels.device if device is None else torch.device(device)
@@ -127,6 +127,8 @@ class RobotBatch:
         self.goal_vector = torch.zeros((E, 2), **f64)
         self.proj_vel = torch.zeros(E, **f64)
         self.height_map = torch.zeros((E, HMAP_NX, HMAP_NY), dtype=torch.float32, device=d)
+        # per-ray hit labels (observe.py:84-85), only when the batch asks for them
+        self.semantics = torch.zeros((E, N_RAYS), dtype=torch.uint8, device=d) if semantics else None
         self.refresh_passable()
 
     # -- traversability (robot.py:127-179) -------------------------------------------
@@ -191,6 +193,8 @@ class RobotBatch:
                  goal_vector=self.goal_vector, proj_vel=self.proj_vel, height_map=self.height_map)
         for k, v in m.items():
             setattr(s, k, v.data_ptr())
+        if self.semantics is not None:
+            s.semantics = self.semantics.data_ptr()
         if crowd is not None:
             pos, radius, active = crowd
             s.crowd_pos, s.crowd_radius, s.crowd_active = pos.data_ptr(), radius.data_ptr(), active.data_ptr()
@@ -217,4 +221,5 @@ class RobotBatch:
         """Device views of the last tick's outputs (no host copies)."""
         return dict(reward=self.reward, events=self.events, distance=self.distance, path_inc=self.path_inc,
                     depth=self.depth, goal_vector=self.goal_vector, proj_vel=self.proj_vel,
-                    height_map=self.height_map, terminated=self.terminated, truncated=self.truncated)
+                    height_map=self.height_map, terminated=self.terminated, truncated=self.truncated,
+                    semantics=self.semantics)

@@ -114,7 +114,9 @@ def test_batched_env_step_batch_matches_reference(torch_cuda):
                      object_density=20 / 41, pedestrian_count=8,
                      terrain_mix={"Flat": 0.25, "Slope": 0.25, "Stair": 0.25, "Rough": 0.25},
                      grid_resolution_m=0.25)
-    env = BatchedEnv(spec, Scheme.ASYNC, master_seed=0, k=K, config=EnvConfig(robot="quadruped"))
+    env = BatchedEnv(spec, Scheme.ASYNC, master_seed=0, k=K,
+                     config=EnvConfig(robot="quadruped", include_semantics=True))
+    sg = load_golden("robot_semantics.npz")
     assert np.array_equal(env.labels_stack.cpu().numpy(), g["labels"])
     # the device spawn (route anchors + batch.py:183-198) lands on the reference's poses
     for i in range(K):
@@ -133,5 +135,33 @@ def test_batched_env_step_batch_matches_reference(torch_cuda):
         assert np.array_equal(ev, g["events"][t]), t
         dep = np.stack([r.observation.depth for r in res])
         assert np.array_equal(dep, g["depth"][t]), t
+        sem = np.stack([r.observation.semantics for r in res])
+        assert np.array_equal(sem, sg["quadruped_semantics"][t]), t
     st = [env.robot_state(i) for i in range(K)]
     assert np.abs(np.array([s["x"] for s in st]) - g["x"][-1]).max() <= 1e-7
+
+
+def test_observe_semantics_rise_walls_match_reference(torch_cuda):
+    """Per-ray semantics (observe.py:84-85) through cw_robot_observe on the synthetic
+    terraces of tests/golden/robot_semantics.npz (reference observe_batch output):
+    rays stopped by rises carry labels 1-3, obstacle hits and cap / exit rays 0.
+    Depth, semantics and the height patch are exact."""
+    import torch
+    from paper_2505_00690_b200.robot import RobotBatch
+    s = load_golden("robot_semantics.npz")
+    rb = RobotBatch(torch.from_numpy(s["synth_labels"]).cuda(), torch.from_numpy(s["synth_elev"]).cuda(),
+                    float(s["synth_res"]), "wheeled", semantics=True)
+    assert rb.model.max_step_rise == float(s["synth_rise"])
+    K = s["synth_x"].shape[0]
+    rb.set_state(s["synth_x"], s["synth_y"], s["synth_yaw"], s["synth_goal"], vx=s["synth_vel"][:, 0],
+                 vy=s["synth_vel"][:, 1], elev=s["synth_er"], tick=np.zeros(K, np.int64),
+                 terminated=np.zeros(K, bool), truncated=np.zeros(K, bool))
+    rb.observe()
+    assert np.array_equal(rb.semantics.cpu().numpy(), s["synth_semantics"])
+    assert np.array_equal(rb.depth.cpu().numpy(), s["synth_depth"])
+    assert np.array_equal(rb.height_map.cpu().numpy(), s["synth_height_map"])
+    assert np.abs(rb.proj_vel.cpu().numpy() - s["synth_proj_vel"]).max() <= TOL
+    # without include_semantics nothing is allocated or written
+    rb2 = RobotBatch(torch.from_numpy(s["synth_labels"]).cuda(), torch.from_numpy(s["synth_elev"]).cuda(),
+                     float(s["synth_res"]), "wheeled")
+    assert rb2.semantics is None and rb2.outputs()["semantics"] is None

@@ -75,3 +75,33 @@ def test_reach_and_out_of_bounds_terminate():
     assert rb.terminated.all()
     rew2, _, _ = rb.step(np.zeros((2, 2)))
     assert (rew2 == 0.0).all() and (rb.tick == 1).all()
+
+
+@pytest.mark.parametrize("run", ["quadruped", "small"])
+def test_observe_semantics_match_reference(run):
+    """observe.py:84-85 per-ray semantics on every post-step state of the robot goldens
+    (oracle/make_golden_semantics.py)."""
+    from oracle import robot as R
+    g = load_golden(f"robot_{run}.npz")
+    s = load_golden("robot_semantics.npz")
+    rise = R.MODELS[str(g["robot"])].max_step_rise
+    for t in range(g["x"].shape[0]):
+        vel = np.stack([g["vx"][t], g["vy"][t]], -1)
+        o = R.observe(g["x"][t], g["y"][t], g["yaw"][t], g["goal"][t], vel, g["elev"][t],
+                      g["labels"], g["grid_elev"], float(g["res"]), rise)
+        assert np.array_equal(o["semantics"], s[f"{run}_semantics"][t]), t
+        assert np.array_equal(o["depth"], s[f"{run}_depth"][t]), t
+
+
+def test_observe_semantics_rise_walls_match_reference():
+    """Synthetic terraces: rays stopped by rises carry the walkable / roadway / ground
+    label of the cell they stop in (labels 1-3 present in the fixture)."""
+    from oracle import robot as R
+    s = load_golden("robot_semantics.npz")
+    o = R.observe(s["synth_x"], s["synth_y"], s["synth_yaw"], s["synth_goal"], s["synth_vel"],
+                  s["synth_er"], s["synth_labels"], s["synth_elev"], float(s["synth_res"]),
+                  float(s["synth_rise"]))
+    assert set(np.unique(s["synth_semantics"]).tolist()) == {0, 1, 2, 3}
+    assert np.array_equal(o["semantics"], s["synth_semantics"])
+    assert np.array_equal(o["depth"], s["synth_depth"])
+    assert np.array_equal(o["height_map"], s["synth_height_map"])
