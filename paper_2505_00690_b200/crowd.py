@@ -140,8 +140,12 @@ class CrowdField:
             self._batch = None
             self.epoch_t = torch.zeros((self.E,), dtype=torch.int32, device=self.device)
             self._upload_grids(occs)
-        if self.nx > 1024 or self.ny > 1024:
-            raise NotImplementedError("grids above 1024 x 1024 cells (A* packs row/col in 10 bits)")
+        bits = lambda n: max(int(n) - 1, 0).bit_length()
+        if (max(bits(self.nx), 10 if max(self.nx, self.ny) <= 1024 else 0) + bits(self.ny) > 20
+                or max(self.nx, self.ny) + 0.4143 * min(self.nx, self.ny) >= 2047.0):
+            # A* keys (astar.cuh make_key2): row << cb | col in 20 bits, floor(h * 4096) in 23
+            raise NotImplementedError("grids whose row and column need more than 20 bits together, "
+                                      "or whose octile diameter reaches 2047 cells")
         if len(env_seeds) != self.E:
             raise ValueError("env_seeds must have one seed per env")
         self.rng_t = torch.empty((self.E, 48), dtype=torch.uint8, device=self.device)

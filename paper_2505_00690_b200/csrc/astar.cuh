@@ -44,6 +44,16 @@ constexpr u64 kInf64 = ~0ull;
 
 CW_DEV Key key_inf() { return {kInf64, kInf64}; }
 
+// cell of a key2 (row << cb | col in bits [40:21], cb = column bits; see make_key2)
+CW_DEV int key_col(u64 k, int cb) { return (int)(k >> 21) & ((1 << cb) - 1); }
+CW_DEV int key_row(u64 k, int cb) { return (int)(k >> (21 + cb)) & ((1 << (20 - cb)) - 1); }
+// column bits of an nx x ny grid
+CW_HD int key_col_bits(int nx, int ny) {
+  int b = 0;
+  while ((1 << b) < nx) ++b;
+  return b <= 10 && ny <= 1024 ? 10 : b;
+}
+
 // branch-free lexicographic compare (bitwise predicate logic: no short-circuit
 // control flow for the compiler to turn into divergent branches)
 CW_DEV bool klt(const Key& a, const Key& b) {
@@ -102,6 +112,7 @@ struct Pools {
   int NC, far_cap;
   const double* gt;    // g tiles of the running search (shared or global)
   int gr, gc;          // goal row / col of the running search
+  int cb;              // column bits of the key2 cell field
 };
 
 CW_DEV double octile(int r, int c, int gr, int gc);
@@ -113,7 +124,7 @@ CW_DEV T ld_grid(const T* p, bool cg) { return cg ? __ldcg(p) : *p; }
 // decreases); the reference pops it and skips it (paths.py:70-71), so it can
 // be dropped whenever the pools are scanned.  Key layout: see make_key2.
 CW_DEV bool stale_entry(const OpenEnt& v, const Pools& pl) {
-  const int r = (int)(v.k >> 31) & 1023, c = (int)(v.k >> 21) & 1023;
+  const int r = key_row(v.k, pl.cb), c = key_col(v.k, pl.cb);
   const int sl = (int)(v.k >> 5) & 0xFFFF;
   const double g = pl.gt[(size_t)sl * 64 + (r & 7) * 8 + (c & 7)];
   return __longlong_as_double((long long)v.f) > g + octile(r, c, pl.gr, pl.gc) + 1e-12;
@@ -333,12 +344,17 @@ __device__ __noinline__ OpenSet refill(OpenSet st, const Pools pl, int lane) {
 // g(x) and moves(x) directly.  Key k2 layout (ordering = (h, row, col)):
 //   [63:41] floor(h * 4096)   distinct octile h differ by > 3.5e-4, so this is
 //                             injective and monotone on the values that occur
-//   [40:31] row  [30:21] col  [20:5] tile slot  [4:0] 0
+//   [40:21] row << cb | col   [20:5] tile slot  [4:0] 0
+// cb = column bits: 10 for grids up to 1024 x 1024 (row and col 10 bits each); a wider
+// grid (Traverse strips: 120 m x 10 m at 0.1 m = 1200 x 100) takes cb = ceil(log2 nx) and
+// leaves 20 - cb bits to the row -- (row << cb | col) orders like (row, col) either way.
+// The host admits grids with ceil(log2 nx) + ceil(log2 ny) <= 20 and octile h < 2048
+// (23 bits of floor(h * 4096)); crowd.py checks both.
 constexpr u64 kCellMask2 = ((1ull << 20) - 1ull) << 21;
 constexpr unsigned kNoSlot = 0xFFFFu;
 
-CW_DEV u64 make_key2(double h, int r, int c, int slot) {
-  return ((u64)(h * 4096.0) << 41) | ((u64)r << 31) | ((u64)c << 21) | ((u64)slot << 5);
+CW_DEV u64 make_key2(double h, int r, int c, int slot, int cb) {
+  return ((u64)(h * 4096.0) << 41) | ((u64)((r << cb) | c) << 21) | ((u64)slot << 5);
 }
 
 // bytes of the per-warp global scratch for an nx x ny grid with S shared
@@ -505,7 +521,7 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
       E.parent[start] = -1;
     }
     st.hd = key_inf();
-    if (lane == 0) st.hd = {(u64)__double_as_longlong(h0), make_key2(h0, sr, sc, s0)};
+    if (lane == 0) st.hd = {(u64)__double_as_longlong(h0), make_key2(h0, sr, sc, s0, pl.cb)};
     st.T = key_inf();
     st.F2 = {f_plus((u64)__double_as_longlong(h0), delta2), 0ull};
     st.delta = delta;
@@ -551,7 +567,7 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
       st.h -= 1;
     }
     const u64 topk = popped.k;
-    const int r = (int)(topk >> 31) & 1023, c = (int)(topk >> 21) & 1023;
+    const int r = key_row(topk, pl.cb), c = key_col(topk, pl.cb);
     const int sx = (int)(topk >> 5) & 0xFFFF;
     const int x = r * nx + c;
     const int ix = sx * 64 + (r & 7) * 8 + (c & 7);
@@ -583,7 +599,7 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
     const bool fresh = gy == CUDART_INF;
     // routing never looks at the tile slot ((h, row, col) is unique per
     // cell), so it is decided together with the first-write test
-    const Key ne0 = {(u64)__double_as_longlong(ng + hh), make_key2(hh, rr, cc, 0)};
+    const Key ne0 = {(u64)__double_as_longlong(ng + hh), make_key2(hh, rr, cc, 0, pl.cb)};
     if (st.nn + 16 > NC) {
       st = split_near(st, pl, lane);
       if (st.err) { found = -1; break; }
@@ -768,6 +784,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
   pl.far = (spec ? sp.heap : reinterpret_cast<OpenEnt*>(S.astar_heap)) + slot * P.heap_cap;
   pl.NC = NC;
   pl.far_cap = P.heap_cap;
+  pl.cb = key_col_bits(P.nx, P.ny);
 
   E.tmap = reinterpret_cast<uint16_t*>(pl.stg + 64);
   unsigned char* const pool = sm + (size_t)W * shp.per_warp;

@@ -28,6 +28,29 @@ from .robot import EVENT_NAMES, ROBOT_MODELS, RewardConfig, RobotBatch
 from .urbangen import SceneSampler, SceneSpec, as_spec
 
 
+class _SlotSeq:
+    """Read-only per-slot sequence whose elements are built on access."""
+
+    def __init__(self, n, get):
+        self._n, self._get = int(n), get
+
+    def __len__(self):
+        return self._n
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(self._n))]
+        i = int(i)
+        if i < 0:
+            i += self._n
+        if not 0 <= i < self._n:
+            raise IndexError(i)
+        return self._get(i)
+
+    def __iter__(self):
+        return (self._get(i) for i in range(self._n))
+
+
 class Scheme(str, Enum):
     ASYNC = "Async"
     SYNC = "Sync"
@@ -144,6 +167,18 @@ class BatchedEnv:
     @property
     def resolution(self):
         return float(self.batch.params.res)
+
+    @property
+    def occs(self):
+        """batch.py:99, 129: every slot's OccupancyGrid -- host copies of the slot's device
+        raster, taken when an element is read (so they follow re-sampling)."""
+        return _SlotSeq(self.K, self.batch.occupancy)
+
+    @property
+    def scenes(self):
+        """batch.py:98, 128: every slot's SceneDescription (zones, terrain, objects, routes),
+        rebuilt from the device batch when an element is read."""
+        return _SlotSeq(self.K, lambda i: self.batch.scene(i, self.spec, self.sampler.catalog))
 
     @property
     def scene_hashes(self):

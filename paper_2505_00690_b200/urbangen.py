@@ -145,6 +145,11 @@ class OccupancyGrid:
     def cell_of(self, x, y):
         return int(y / self.resolution), int(x / self.resolution)
 
+    def in_bounds_cell(self, row, col):
+        """types.py:377-379."""
+        ny, nx = self.labels.shape
+        return 0 <= row < ny and 0 <= col < nx
+
 
 BLOCK_KINDS = ("Straight", "Curve", "Roundabout", "Diverging", "Merging", "Intersection",
                "TIntersection")
