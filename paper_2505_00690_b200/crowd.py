@@ -140,12 +140,7 @@ class CrowdField:
             self._batch = None
             self.epoch_t = torch.zeros((self.E,), dtype=torch.int32, device=self.device)
             self._upload_grids(occs)
-        bits = lambda n: max(int(n) - 1, 0).bit_length()
-        if (max(bits(self.nx), 10 if max(self.nx, self.ny) <= 1024 else 0) + bits(self.ny) > 20
-                or max(self.nx, self.ny) + 0.4143 * min(self.nx, self.ny) >= 2047.0):
-            # A* keys (astar.cuh make_key2): row << cb | col in 20 bits, floor(h * 4096) in 23
-            raise NotImplementedError("grids whose row and column need more than 20 bits together, "
-                                      "or whose octile diameter reaches 2047 cells")
+        check_grid_shape(self.nx, self.ny)
         if len(env_seeds) != self.E:
             raise ValueError("env_seeds must have one seed per env")
         self.rng_t = torch.empty((self.E, 48), dtype=torch.uint8, device=self.device)
@@ -733,6 +728,22 @@ def _grid_batch(occupancy, count, region_mask):
             raise ValueError("region_mask must have the grid's shape")
         b.region = torch.from_numpy(m.astype(np.uint8)).to(b.device).reshape(1, ny * nx)
     return p, b
+
+
+def key_col_bits(nx, ny):
+    """Column bits of the A* key's cell field (astar.cuh key_col_bits): 10 up to
+    1024 x 1024 cells, else ceil(log2 nx)."""
+    b = max(int(nx) - 1, 0).bit_length()
+    return 10 if b <= 10 and ny <= 1024 else b
+
+
+def check_grid_shape(nx, ny):
+    """Grids the device crowd accepts: the A* key (astar.cuh make_key2) packs
+    row << cb | col in 20 bits and floor(h * 4096) in 23 bits."""
+    if (key_col_bits(nx, ny) + max(int(ny) - 1, 0).bit_length() > 20
+            or max(nx, ny) + 0.4143 * min(nx, ny) >= 2047.0):
+        raise NotImplementedError("grids whose row and column need more than 20 bits together, "
+                                  "or whose octile diameter reaches 2047 cells")
 
 
 def spawn_agents(occupancy, count, seed, region_mask=None):
