@@ -111,7 +111,7 @@ struct Pools {
   OpenEnt* far;        // global, far_cap entries
   int NC, far_cap;
   const double* gt;    // g tiles of the running search (shared or global)
-  int gr, gc;          // goal row / col of the running search
+  short gr, gc;        // goal row / col of the running search (< 2048, crowd.py)
   int cb;              // column bits of the key2 cell field
 };
 
@@ -464,10 +464,13 @@ struct Resume {
   int gcount;      // global tiles handed out so far
 };
 
-template <bool kGlob>
+// kWide: the grid's key2 cell field is not the default 10 / 10 split (pl.cb != 10); the
+// default instantiation decodes with constant shifts (the per-expansion critical path)
+template <bool kGlob, bool kWide = false>
 CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int start, int goal,
                       double& delta, double& delta2, unsigned& s_exp, int& used, int lane, Resume& rs,
                       bool cg) {
+  const int cb = kWide ? (int)pl.cb : 10;
   double* const gt = kGlob ? E.gtg : E.gts;
   uint8_t* const mt = kGlob ? E.mtg : E.mts;
   const int nx = E.nx, ny = E.ny, TW = E.TW, NT = E.NT, NC = pl.NC;
@@ -521,7 +524,7 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
       E.parent[start] = -1;
     }
     st.hd = key_inf();
-    if (lane == 0) st.hd = {(u64)__double_as_longlong(h0), make_key2(h0, sr, sc, s0, pl.cb)};
+    if (lane == 0) st.hd = {(u64)__double_as_longlong(h0), make_key2(h0, sr, sc, s0, cb)};
     st.T = key_inf();
     st.F2 = {f_plus((u64)__double_as_longlong(h0), delta2), 0ull};
     st.delta = delta;
@@ -567,7 +570,7 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
       st.h -= 1;
     }
     const u64 topk = popped.k;
-    const int r = key_row(topk, pl.cb), c = key_col(topk, pl.cb);
+    const int r = key_row(topk, cb), c = key_col(topk, cb);
     const int sx = (int)(topk >> 5) & 0xFFFF;
     const int x = r * nx + c;
     const int ix = sx * 64 + (r & 7) * 8 + (c & 7);
@@ -599,7 +602,7 @@ CW_DEV int run_search(const SearchEnv& E, Pools& pl, const uint8_t* mvt, int sta
     const bool fresh = gy == CUDART_INF;
     // routing never looks at the tile slot ((h, row, col) is unique per
     // cell), so it is decided together with the first-write test
-    const Key ne0 = {(u64)__double_as_longlong(ng + hh), make_key2(hh, rr, cc, 0, pl.cb)};
+    const Key ne0 = {(u64)__double_as_longlong(ng + hh), make_key2(hh, rr, cc, 0, cb)};
     if (st.nn + 16 > NC) {
       st = split_near(st, pl, lane);
       if (st.err) { found = -1; break; }
@@ -965,7 +968,9 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
       rs.active = 0;
       rs.slot_base = 0;
       rs.gcount = 0;
-      found = run_search<false>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs, spec);
+      found = pl.cb == 10
+                  ? run_search<false>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs, spec)
+                  : run_search<false, true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs, spec);
       if (found == -2 && rs.active) {
         // the shared tile pool ran dry mid-search: move the used tiles to the
         // global store at their slot ids, give the slots back to the CTA pool
@@ -997,7 +1002,9 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
         rs.slot_base = NS;
         rs.gcount = 0;
         ++n_glob;
-        found = run_search<true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs, spec);
+        found = pl.cb == 10
+                    ? run_search<true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs, spec)
+                    : run_search<true, true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs, spec);
       } else if (found == -2) {   // no tile even for the start cell: all-global from scratch
         release();
         pooled = false;
@@ -1006,7 +1013,9 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
         rs.active = 0;
         rs.slot_base = 0;
         rs.gcount = 0;
-        found = run_search<true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs, spec);
+        found = pl.cb == 10
+                    ? run_search<true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs, spec)
+                    : run_search<true, true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs, spec);
       }
     }
     // ---- write the guidance result (field.py:204-212)
