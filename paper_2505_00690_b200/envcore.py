@@ -122,6 +122,7 @@ class BatchedEnv:
         if len(env_seeds) != k:
             raise ValueError("env_seeds must have length K")
         self.env_seeds = [int(s) for s in env_seeds]
+        self.cache = cache
         self.env_seeds_t = seeds_to_tensor(self.env_seeds, self.device)
         if self.scheme == Scheme.SYNC:
             if self.config.resample_on_reset:
@@ -167,6 +168,40 @@ class BatchedEnv:
     @property
     def resolution(self):
         return float(self.batch.params.res)
+
+    @property
+    def extent(self):
+        """batch.py:148-149: (width, length) in metres of the grids."""
+        return (int(self.batch.labels.shape[2]) * self.resolution,
+                int(self.batch.labels.shape[1]) * self.resolution)
+
+    @property
+    def specs(self):
+        """batch.py:90-96: each slot's SceneSpec (Sync: the shared one)."""
+        if self.scheme == Scheme.SYNC:
+            return [replace(self.spec, seed=self.env_seeds[0])] * self.K
+        return [replace(self.spec, seed=s) for s in self.env_seeds]
+
+    @property
+    def env_index(self):
+        """batch.py:137-141: the scene row of each slot (rows are per slot on the device;
+        under Sync every row holds the shared scene, so slot i reads row i)."""
+        if self.scheme == Scheme.SYNC:
+            return np.zeros(self.K, dtype=np.int64)
+        return np.arange(self.K, dtype=np.int64)
+
+    @property
+    def passable_stack(self):
+        """batch.py:145 traversability ``passable`` per slot (device tensor)."""
+        return self.robot.passable
+
+    @property
+    def obstacle_stack(self):
+        """batch.py:146 traversability ``obstacle`` (labels == OBSTACLE) per slot (device)."""
+        return self.batch.labels == 0
+
+    # distance to the goal after the last step / at reset (batch.py:114, 198, 280)
+    prev_dist = property(lambda self: DeviceView(self.robot.distance))
 
     @property
     def occs(self):

@@ -180,6 +180,14 @@ class RobotBatch:
         self.tick[idx] = t(tick, torch.int64)
         self.terminated[idx] = t(terminated, torch.uint8)
         self.truncated[idx] = t(truncated, torch.uint8)
+        # distance to the goal at the new pose (batch.py:198 prev_dist): numpy's hypot
+        # on the host values (the reference's own call), torch's for device inputs
+        if not any(isinstance(v, torch.Tensor) for v in (x, y, goal)):
+            g = np.asarray(goal, np.float64).reshape(-1, 2)
+            d = np.hypot(g[:, 0] - np.asarray(x, np.float64), g[:, 1] - np.asarray(y, np.float64))
+            self.distance[idx] = torch.from_numpy(np.ascontiguousarray(d)).to(self.device)
+        else:
+            self.distance[idx] = torch.hypot(self.goal[idx, 0] - self.x[idx], self.goal[idx, 1] - self.y[idx])
 
     def live(self):
         return (self.terminated == 0) & (self.truncated == 0)

@@ -124,6 +124,13 @@ def test_batched_env_step_batch_matches_reference(torch_cuda):
         assert (st["x"], st["y"], st["yaw"], st["elevation"]) == (
             g["init_x"][i], g["init_y"][i], g["init_yaw"][i], g["init_elev"][i]), i
         assert st["goal"] == list(g["init_goal"][i]), i
+    # batch.py:114, 198: prev_dist at reset = hypot(goal - start) (numpy's, bit for bit)
+    d0 = np.hypot(g["init_goal"][:, 0] - g["init_x"], g["init_goal"][:, 1] - g["init_y"])
+    assert np.array_equal(np.asarray(env.prev_dist), d0)
+    assert env.extent == (32.0, 32.0) and list(env.env_index) == list(range(K))
+    assert [sp.seed for sp in env.specs] == env.env_seeds
+    assert np.array_equal(env.passable_stack.cpu().numpy(), g["passable"])
+    assert np.array_equal(env.obstacle_stack.cpu().numpy(), g["obstacle"].astype(bool))
     names = ("collision", "collision_static", "collision_dynamic", "on_walkable", "reached",
              "out_of_bounds")
     for t in range(T):
@@ -133,6 +140,7 @@ def test_batched_env_step_batch_matches_reference(torch_cuda):
         assert np.abs(np.array([r.reward for r in res]) - g["reward"][t]).max() <= TOL, t
         ev = np.array([[r.events[k] for k in names] for r in res])
         assert np.array_equal(ev, g["events"][t]), t
+        assert np.abs(np.asarray(env.prev_dist) - g["distance"][t]).max() <= TOL, t
         dep = np.stack([r.observation.depth for r in res])
         assert np.array_equal(dep, g["depth"][t]), t
         sem = np.stack([r.observation.semantics for r in res])

@@ -22,7 +22,7 @@ case "$1" in
     PYTHONDONTWRITEBYTECODE=1 PYTHONPATH="$ROOT/baseline/_ref:$ROOT:$ROOT/tools/refshim" \
       python -m pytest -p refshim_plugin -p no:cacheprovider -q -rfE \
       --junitxml="$ROOT/gpurun_out/reftests.xml" -o junit_family=xunit1 \
-      test_crowd.py test_urbangen.py test_envcore.py test_acceptance.py "$@"
+      . "$@"
     ;;
   *) echo "usage: $0 stage|run [pytest args]"; exit 2 ;;
 esac
