@@ -414,6 +414,13 @@ class CrowdField:
         ticks = int(ticks)
         if self.A == 0 or self.E == 0 or ticks <= 0:
             return
+        if key_col_bits(self.nx, self.ny) != 10:
+            # the run's search server keeps the default A* key packing (astar.cuh): grids
+            # wider or taller than 1024 cells step tick by tick (the same result)
+            for _ in range(ticks):
+                self.step(robot_pos=robot_pos, robot_vel=robot_vel, robot_radius=robot_radius,
+                          env_mask=env_mask, check=check)
+            return
         if "_p" not in self.__dict__:
             self.prepare_step()
         rp = self._dev(robot_pos, torch.float64, (self.E, 2))
@@ -446,6 +453,9 @@ class CrowdField:
         ticks = int(ticks)
         if self.A == 0 or self.E == 0 or ticks <= 0:
             return
+        if key_col_bits(self.nx, self.ny) != 10:
+            raise NotImplementedError("run_window on grids wider or taller than 1024 cells "
+                                      "(the run's search server keeps the default A* key packing)")
         if "_p" not in self.__dict__:
             self.prepare_step()
         rp = self._dev(robot_pos, torch.float64, (self.E, 2))

@@ -968,7 +968,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
       rs.active = 0;
       rs.slot_base = 0;
       rs.gcount = 0;
-      found = pl.cb == 10
+      found = (kRing || pl.cb == 10)   // the run's server: default packing only (crowd.py)
                   ? run_search<false>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs, spec)
                   : run_search<false, true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs, spec);
       if (found == -2 && rs.active) {
@@ -1002,7 +1002,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
         rs.slot_base = NS;
         rs.gcount = 0;
         ++n_glob;
-        found = pl.cb == 10
+        found = (kRing || pl.cb == 10)
                     ? run_search<true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs, spec)
                     : run_search<true, true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs, spec);
       } else if (found == -2) {   // no tile even for the start cell: all-global from scratch
@@ -1013,7 +1013,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_astar(cw_crowd_params P, cw_crowd
         rs.active = 0;
         rs.slot_base = 0;
         rs.gcount = 0;
-        found = pl.cb == 10
+        found = (kRing || pl.cb == 10)
                     ? run_search<true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs, spec)
                     : run_search<true, true>(E, pl, mvt, start, goal, delta, delta2, s_exp, used, lane, rs, spec);
       }

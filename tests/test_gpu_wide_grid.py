@@ -57,3 +57,23 @@ def test_wide_grid_crowd_matches_oracle(ext, task, torch_cuda):
         rp = rp + rv * 0.05
     assert np.array_equal(f.goal, ref.goal)
     assert f.stats()["astar_expansions"] > 0   # the searches ran on the wide packing
+
+
+def test_wide_grid_run_equals_steps(torch_cuda):
+    """CrowdField.run on a 1200 x 100 strip (stepped tick by tick there) equals steps."""
+    from oracle.rng import child_seed
+    from paper_2505_00690_b200.crowd import CrowdConfig, CrowdField
+    from paper_2505_00690_b200.urbangen import SceneSampler, SceneSpec, TaskKind
+    seeds = [child_seed(5, "env", i) for i in range(2)]
+    spec = SceneSpec(seed=seeds[0], extent_m=(120.0, 10.0), task_kind=TaskKind.NAV_DYNAMIC,
+                     object_density=1.0, pedestrian_count=12, terrain_mix=MIX, grid_resolution_m=0.1)
+    b = SceneSampler(spec, 2).sample(seeds, [child_seed(s, "crowd", 0) for s in seeds])
+    run = [child_seed(s, "crowd-run") for s in seeds]
+    fa, fb = CrowdField(b, CrowdConfig(), run), CrowdField(b, CrowdConfig(), run)
+    fa.set_from_spawn(b)
+    fb.set_from_spawn(b)
+    rp, rv = np.array([[60.0, 5.0]] * 2), np.zeros((2, 2))
+    fa.run(30, robot_pos=rp, robot_vel=rv)
+    for _ in range(30):
+        fb.step(robot_pos=rp, robot_vel=rv)
+    assert np.array_equal(fa.pos, fb.pos) and np.array_equal(fa.vel, fb.vel)
